@@ -1,0 +1,212 @@
+/* libbddc — B200-native (sm_100a) adaptive-BDDC PCG for RT0/P0 Darcy flow.
+ *
+ * C ABI: plain device pointers (FP64 / int32) and sizes, a caller-owned
+ * cudaStream_t passed as void*.  No torch types cross this boundary; the
+ * Python host layer (paper_1901_02090_b200) passes tensor.data_ptr() values.
+ * Every function returns 0 on success or a BDDC_ERR_* code; the message is
+ * available from bddc_last_error().  Error codes map 1:1 onto the reference
+ * exception classes (/root/reference/pkg/src/bddcflow/errors.py:4-48).
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/pkg/src/bddcflow/).
+ */
+#ifndef BDDC_H
+#define BDDC_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.py:4-48 */
+enum {
+  BDDC_OK = 0,
+  BDDC_ERR_ARG = 1,          /* InvalidArgumentError */
+  BDDC_ERR_NUMERICAL = 2,    /* NumericalFailureError(where) */
+  BDDC_ERR_RANK = 3,         /* ConstraintRankError */
+  BDDC_ERR_CONFIG = 4,       /* ConfigurationError */
+  BDDC_ERR_INTERNAL = 5,     /* InternalConsistencyError */
+  BDDC_ERR_CUDA = 6          /* CUDA runtime failure (no reference analogue) */
+};
+
+#define BDDC_MAX_STRIPS 64
+
+/* Grid + regular partition (grid.py:21-175, decomposition.py:128-151).
+ * 2D problems are represented with n[2] = 1, h[2] = 1, S[2] = 1. */
+typedef struct bddc_geom {
+  int dim;
+  int n[3];                        /* cells per axis */
+  double h[3];                     /* cell sizes */
+  double vol;                      /* cell volume (product of h over dim axes) */
+  int S[3];                        /* splits per axis */
+  int so[3][BDDC_MAX_STRIPS];      /* strip origins */
+  int sw[3][BDDC_MAX_STRIPS];      /* strip widths (near-equal, decomposition.py:128-130) */
+  int fam_off[4];                  /* flux dof offsets per face family */
+  int n_cells, n_flux, N, n_gamma, n_faces;
+  int maxG;                        /* padded interface slots per subdomain (multiple of 64) */
+  int maxP;                        /* padded cells per subdomain (multiple of 64) */
+  int maxL;                        /* max strip width */
+  int maxF;                        /* max dofs on one box face */
+} bddc_geom;
+
+const char* bddc_last_error(void);
+int bddc_version(void);
+
+/* ---------------------------------------------------------------- dense */
+
+/* C[b] = alpha op(A[b]) op(B[b]) + beta C[b], row-major FP64 on DMMA
+ * (mma.sync m8n8k4 f64).  upper != 0 computes only tiles on/above the
+ * diagonal.  Replaces the dense BLAS products of coarse.py:179-185 and
+ * adaptive.py:123-137. */
+int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha,
+                       const double* A, int lda, long long sA, const double* B, int ldb,
+                       long long sB, double beta, double* C, int ldc, long long sC, int batch,
+                       int upper, void* stream);
+
+/* In-place SPD inverse by the blocked symmetric sweep (block b, n % b == 0);
+ * replaces SuperLU splu (substructure.py:66, coarse.py:159) and the dense
+ * coarse lu_factor (coarse.py:196).  info counts non-positive pivots. */
+size_t bddc_spd_inverse_workspace(int n, int batch, int b);
+int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
+                             int* info, void* stream);
+
+/* ------------------------------------------------------- local operators */
+
+/* c_a = h_a^2 / (6 V k_a) per cell (grid.py:204-227, 270-291). coef: n_cells x 3. */
+int bddc_cell_coeffs(const bddc_geom* g, const double* k, double* coef, void* stream);
+/* delta per interface slot (decomposition.py:212-239), N x maxG. */
+int bddc_weights(const bddc_geom* g, int stiffness, const double* coef, const int* gcode,
+                 double* delta, void* stream);
+/* D_i = mean diag(A) over dofs touching subdomain i (grid.py:344-357). */
+int bddc_rescale(const bddc_geom* g, const double* coef, double* Dsub, void* stream);
+
+/* Interior KKT elimination (substructure.py:25-70) for all subdomains:
+ * P = B_I A_II^-1 B_I^T + alpha 11^T (maxP^2 each, identity padded), the
+ * line-compact G = B_G - B_I A_II^-1 A_IG (maxG x maxL) and S_A. */
+int bddc_local_build(const bddc_geom* g, const double* coef, const int* fslot, double* P, double* Gc,
+                     double* SAd, int* SApart, double* SAoff, double* alpha, void* stream);
+/* Q = P^+ from the swept inverse of P + alpha 11^T. */
+int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* alpha, void* stream);
+/* Dense S_i = sym(S_A + G^T Q G), identity padded (substructure.py:90-99). */
+int bddc_local_schur(const bddc_geom* g, const int* gcode, const double* Q, const double* Gc,
+                     const double* SAd, const int* SApart, const double* SAoff, double* Wt,
+                     double* S, void* stream);
+
+/* Batched interior KKT solves (substructure.py:72-116): harmonic_extend,
+ * trace_solve, condense and the interior recovery (solver.py:375-382). */
+typedef struct bddc_local_solve_args {
+  const double* f_flux;   /* global flux vector read at interior dofs (or NULL) */
+  double f_scale;
+  const double* g_cell;   /* global cell vector in D-scaled units (or NULL) */
+  double g_scale;
+  const double* x_gamma;  /* continuous interface vector (indexed like gamma) or NULL */
+  double x_scale;
+  double* u_out;          /* global flux vector: interior dofs written */
+  int u_mode;             /* 0: set, 1: add */
+  double* rg_broken;      /* if non-NULL: A_IG^T u_I + B_G^T p per slot (N x maxG) */
+  double* p_out;          /* if non-NULL: local pressures per cell */
+} bddc_local_solve_args;
+int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, const int* gpos,
+                     const int* fslot, const double* Q, const double* Dsub,
+                     const bddc_local_solve_args* a, void* stream);
+
+/* -------------------------------------------------------------- adaptive */
+
+/* Reduced pair eigenproblems on every face (adaptive.py:63-138), selection
+ * of eigenvalues > tau, harvested rows and the reference's dependence
+ * filter (adaptive.py:141-173, coarse.py:61-100); omega per face
+ * (adaptive.py:56-60). */
+size_t bddc_pair_scratch_bytes(int n_faces);
+int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
+                   const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
+                   int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
+                   int* err, void* stream);
+
+/* ---------------------------------------------------------------- coarse */
+
+/* Per-subdomain coarse pieces (coarse.py:130-185): Kc, Psi_Gamma, T, B0 row. */
+int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces, const int* fslot,
+                      const int* gcode, const double* rows, int maxsel, const double* Sinv,
+                      const double* Dsub, int maxC, double* Ct, double* Y, double* Kc, double* Psi,
+                      double* T, double* b0, void* inv_ws, int* info, void* stream);
+/* Deterministic S_Pi assembly (coarse.py:182-183). */
+int bddc_coarse_assemble(int N, int maxC, int nfc, int npad, const int* sub_rows, const double* Kc,
+                         double* SP, void* stream);
+/* Pinned coarse saddle (coarse.py:186-215) reduced to Mc (in place of SP) and Wq. */
+int bddc_coarse_factor(int N, int maxC, int nfc, int npad, int npc, const int* sub_rows,
+                       const double* b0, double* SP, double* Y0T, double* Pc, double* Wq, void* inv_ws,
+                       int* info_sp, int* info_pc, void* stream);
+
+/* ------------------------------------------------------------------- PCG */
+
+/* y_b = M_i (win .* gather(x)) per subdomain (solver.py:103-107 schur_matvec,
+ * solver.py:114-124 Delta part of precondition). */
+int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos, const double* Mats,
+                     const double* x, const double* win, double* yb, void* stream);
+/* v_i = Psi_i^T (win .* gather(x)) (coarse.py:225-235 weighted_restriction). */
+int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,
+                       const double* Psi, const double* x, const double* win, double* v,
+                       void* stream);
+int bddc_coarse_restrict(int nfc, const int* cown, const double* v, double* rhs, void* stream);
+/* out_b = wout .* (y_b + Psi_i sigma x_c) (coarse.py:217-223 local_combination). */
+int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* sub_rows, const double* Psi,
+                 const double* xc, const double* yb, const double* wout, double* outb, void* stream);
+/* y = sum over both copies (solver.py:100-101 scatter_add). */
+int bddc_scatter(int n_gamma, const int* gown, const double* yb, double* y, void* stream);
+/* Balanced projection (solver.py:166-179) as I - Phi^T (Phi Phi^T)^+ Phi. */
+int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const double* y,
+             double* phi, void* stream);
+int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
+                   double* z, void* stream);
+int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const double* z, double* y,
+                    void* stream);
+/* PCG pieces (solver.py:186-233): fused deterministic dots with scalar ops,
+ * vector updates, dense GEMV, Lanczos kappa (solver.py:236-251). */
+size_t bddc_dot_workspace(void);
+int bddc_dot(const double* x, const double* y, long long n, void* ws, double* scal, int op,
+             double* hist, int it, void* stream);
+int bddc_cg_update(long long n, const double* scal, double* x, const double* p, double* r,
+                   const double* Ap, void* stream);
+int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream);
+int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream);
+int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out,
+                 void* stream);
+int bddc_axpby(long long n, double a, const double* x, double b, double* y, void* stream);
+
+/* --------------------------------------------------------------- stencil */
+
+/* Matrix-free RT0 flux mass apply (grid.py:294-307): y = alpha A u + beta y. */
+int bddc_flux_A(const bddc_geom* g, const double* coef, const double* u, double alpha, double beta,
+                double* y, void* stream);
+/* out = s_f f + s_b D (B u) (grid.py:310-324, solver.py:337). */
+int bddc_cell_div(const bddc_geom* g, const double* u, const double* fvec, double s_f, double s_b,
+                  const int* cell_sub, const double* Dsub, double* out, void* stream);
+/* y = alpha B^T p + beta y. */
+int bddc_grad(const bddc_geom* g, const double* p, double alpha, double beta, double* y,
+              void* stream);
+/* Pressure recovery (solver.py:254-274) via DCT Neumann solve. */
+int bddc_dct_init(const bddc_geom* g, double* dct, void* stream);
+int bddc_neumann_solve(const bddc_geom* g, const double* dct, double* rhs, double* tmp,
+                       void* stream);
+int bddc_sub_mean(long long n, const double* sum, double* v, void* stream);
+
+/* Per-subdomain sums of a cell vector (solver.py:318 rq, 351-352 targets). */
+int bddc_sub_sum(const bddc_geom* g, const double* v, double* out, double scale, const double* Dsub,
+                 void* stream);
+/* Interface <-> flux vector moves: mode 0 set, 1 add, 2 gather into gv. */
+int bddc_gamma_flux(int n, const int* gamma, double* gv, double* flux, int mode, void* stream);
+/* balanced_shift (solver.py:146-164) from the unit-Laplacian solve z. */
+int bddc_face_shift(int n, int n_faces, const int* gface, const int* faces, const double* z,
+                    double* w, void* stream);
+
+/* fs = D f (grid.py:250-251). */
+int bddc_scale_cells(const bddc_geom* g, const double* f, const int* cell_sub, const double* Dsub,
+                     double* out, void* stream);
+
+size_t bddc_geom_size(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDDC_H */

@@ -1,0 +1,132 @@
+"""Generate golden fixtures from the UNMODIFIED reference (run in the build container).
+
+Imports `bddcflow` read-only from /root/reference/pkg/src (it is not on the
+GPU box) and writes small `.npz` files under tests/golden/.  Each fixture
+holds the inputs (grid, permeability, partition, config) and the
+reference's outputs: u, p, it, kappa, omega_tilde, n_c, residual history,
+per-pair eigenvalues and selected counts, one subdomain Schur complement,
+and one application of schur_matvec / precondition / project_balanced to a
+seeded vector.  Mode A (wells at cells 0 and n-1, no-flow) only: the
+reference cannot express BASELINE's pressure-drop boundary conditions.
+
+Usage:  python oracle/make_golden.py [name ...]
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+warnings.filterwarnings("ignore", message="coefficient jumps")
+
+from bddcflow import solver as R_solver          # noqa: E402
+from bddcflow import grid as R_grid              # noqa: E402
+from bddcflow import decomposition as R_dec      # noqa: E402
+
+from paper_1901_02090_b200 import fields         # noqa: E402
+
+
+def _random_k(counts, seed, orders=6.0):
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(counts))
+    return 10.0 ** rng.uniform(-orders / 2, orders / 2, (n, len(counts)))
+
+
+CASES = {
+    # name: (counts, sizes, splits, scaling, tau, tol, k-maker)
+    "g2d_small": ((8, 8), (1.0, 1.0), (2, 2), "multiplicity", math.inf,
+                  1e-10, lambda: _random_k((8, 8), 1)),
+    "g2d_adapt": ((12, 12), (1.0, 1.0), (3, 3), "stiffness", 3.0, 1e-10,
+                  lambda: _random_k((12, 12), 2)),
+    "g2d_aniso": ((9, 21), (2.0, 0.5), (3, 3), "multiplicity", 5.0, 1e-10,
+                  lambda: _random_k((9, 21), 7)),
+    "g3d_adapt": ((6, 6, 6), (1.0, 1.0, 1.0), (2, 2, 2), "multiplicity",
+                  5.0, 1e-10, lambda: _random_k((6, 6, 6), 3)),
+    "g3d_thin": ((5, 5, 5), (1.0, 2.0, 0.5), (3, 3, 3), "stiffness", 5.0,
+                 1e-10, lambda: _random_k((5, 5, 5), 4)),
+    "g3d_box": ((8, 6, 4), (20.0, 10.0, 2.0), (2, 2, 2), "stiffness", 10.0,
+                1e-10, lambda: _random_k((8, 6, 4), 9)),
+    "c0": (fields.CONFIGS[0]["counts"], fields.CONFIGS[0]["sizes"],
+           fields.CONFIGS[0]["splits"], "stiffness", math.inf, 1e-8,
+           lambda: fields.config_field(0)),
+    "c1": (fields.CONFIGS[1]["counts"], fields.CONFIGS[1]["sizes"],
+           fields.CONFIGS[1]["splits"], "stiffness", 10.0, 1e-8,
+           lambda: fields.config_field(1)),
+    "c2_tau10": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
+                 fields.CONFIGS[2]["splits"], "stiffness", 10.0, 1e-8,
+                 lambda: fields.config_field(2)),
+    "c2_tau2": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
+                fields.CONFIGS[2]["splits"], "stiffness", 2.0, 1e-8,
+                lambda: fields.config_field(2)),
+}
+
+
+def make(name):
+    counts, sizes, splits, scaling, tau, tol, kmaker = CASES[name]
+    k = np.asarray(kmaker(), dtype=np.float64)
+    dim = len(counts)
+    g = R_grid.build_grid(dim, counts, sizes)
+    perm = R_grid.Permeability(k)
+    system = R_grid.assemble_system(g, perm, R_grid.Wells(0, g.n_cells - 1))
+    dec = R_dec.regular_partition(g, splits)
+    mode = "adaptive" if math.isfinite(tau) else "initial"
+    cfg = R_solver.SolveConfig(tau=tau, scaling=scaling, constraints=mode,
+                               tol=tol)
+    t0 = time.time()
+    setup = R_solver.BddcSetup(system, dec, cfg)
+    t1 = time.time()
+    rep = R_solver.solve(system, dec, cfg, setup=setup)
+    t2 = time.time()
+
+    rng = np.random.default_rng(1234)
+    x = rng.standard_normal(len(dec.gamma))
+    out = dict(
+        counts=np.array(counts), sizes=np.array(sizes, dtype=np.float64),
+        splits=np.array(splits), scaling=scaling, tau=tau, tol=tol, k=k,
+        u=rep.u, p=rep.p, it=rep.it, kappa=rep.kappa,
+        omega_tilde=rep.omega_tilde, n_c=rep.n_c, residuals=rep.residuals,
+        u0=rep.u0, u_star=rep.u_star,
+        conservation_defect=rep.conservation_defect,
+        gamma=dec.gamma, x=x,
+        Sx=setup.schur_matvec(x), Mx=setup.precondition(x),
+        Px=setup.project_balanced(x),
+        S_sub0=setup.subs[0].schur_dense(),
+        S_sublast=setup.subs[-1].schur_dense(),
+        D=setup.system.D,
+        setup_s=t1 - t0, solve_s=t2 - t1,
+    )
+    # per-face selected counts and the leading eigenvalues of every pair
+    pairs = sorted(dec.faces.keys())
+    out["pairs"] = np.array(pairs, dtype=np.int64).reshape(-1, 2)
+    out["face_rows"] = np.array(
+        [len(setup.cset.rows_for_face(i, j)) // 2 for (i, j) in pairs])
+    if setup.pair_reports:
+        top = 24
+        lam = np.full((len(pairs), top), np.nan)
+        sel = np.zeros(len(pairs), dtype=np.int64)
+        for q, key in enumerate(pairs):
+            ev = setup.pair_reports[key].eigenvalues[:top]
+            lam[q, :len(ev)] = ev
+            sel[q] = setup.pair_reports[key].selected
+        out["pair_lam"] = lam
+        out["pair_selected"] = sel
+    path = os.path.join(REPO, "tests", "golden", f"{name}.npz")
+    np.savez_compressed(path, **out)
+    print(f"{name}: it={rep.it} kappa={rep.kappa:.6g} n_c={rep.n_c} "
+          f"omega={rep.omega_tilde:.6g} setup={t1 - t0:.2f}s "
+          f"solve={t2 - t1:.2f}s -> {os.path.getsize(path) / 1e3:.0f} KB")
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(CASES)
+    for n in names:
+        make(n)

@@ -1,0 +1,559 @@
+// Per-subdomain (local) operators for box subdomains, batched one CTA per
+// subdomain.  Replaces SubdomainOperator (substructure.py:24-119): instead of
+// a SuperLU factorisation of the interior KKT [[A_II,B_I^T,0],[B_I,0,V^T],
+// [0,V,0]] we use that A_II is block-diagonal by axis and tridiagonal along
+// grid lines, so
+//     P   = B_I A_II^{-1} B_I^T        (pressure Schur, summed line blocks)
+//     G   = B_G - B_I A_II^{-1} A_IG    (supported on one grid line per slot)
+//     S_A = A_GG - A_GI A_II^{-1} A_IG  (diagonal + opposite-end partner)
+//     S   = S_A + G^T P^+ G             (Schur complement on Gamma_i)
+// with P^+ obtained from the swept inverse of P + alpha 11^T.  D-scaling of B
+// (grid.py:344-357) cancels in S and enters only the pressure rhs/solution.
+#include "common.cuh"
+
+#define MAXL 32
+
+namespace {
+
+struct SlotLine {
+  int a, side, line, L, base, stride;
+};
+
+__device__ __forceinline__ int axis_stride(const Box& b, int a) {
+  return a == 0 ? 1 : (a == 1 ? b.L[0] : b.L[0] * b.L[1]);
+}
+
+__device__ __forceinline__ int line_base(const Box& b, int a, int line) {
+  int c[3];
+  line_coords(b, a, line, c);
+  return local_cell(b, c[0], c[1], c[2]);
+}
+
+__device__ __forceinline__ SlotLine decode_slot(const Box& b, int code) {
+  SlotLine s;
+  s.a = code & 3;
+  s.side = (code >> 2) & 1;
+  s.line = code >> 3;
+  s.L = b.L[s.a];
+  s.base = line_base(b, s.a, s.line);
+  s.stride = axis_stride(b, s.a);
+  return s;
+}
+
+// Global cell id of local cell k along line `line` of axis a.
+__device__ __forceinline__ int line_cell_global(const bddc_geom& G, const Box& b, int a, int line, int k) {
+  int c[3];
+  line_coords(b, a, line, c);
+  c[a] = k;
+  return cell_id(G, b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]);
+}
+
+// Global interior dof of interior face j (between line cells j and j+1).
+__device__ __forceinline__ int line_face_dof(const bddc_geom& G, const Box& b, int a, int line, int j) {
+  int c[3];
+  line_coords(b, a, line, c);
+  c[a] = j + 1;
+  return face_dof(G, a, b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]);
+}
+
+// Thomas factorisation of the line tridiagonal T (order m = L-1):
+// diag d_j = 2c_j + 2c_{j+1}, off e_j = c_{j+1}.  Stores the modified
+// super-diagonal cp and pivots piv.
+__device__ __forceinline__ void line_factor(const double* c, int L, double* cp, double* piv) {
+  int m = L - 1;
+  for (int j = 0; j < m; ++j) {
+    double d = 2.0 * c[j] + 2.0 * c[j + 1];
+    double sub = (j > 0) ? c[j] : 0.0;  // T[j][j-1] = c_j
+    double pv = d - ((j > 0) ? sub * cp[j - 1] : 0.0);
+    piv[j] = pv;
+    cp[j] = (j + 1 < m) ? c[j + 1] / pv : 0.0;  // T[j][j+1] = c_{j+1}
+  }
+}
+
+// Solve T x = r in place with a factored line.
+__device__ __forceinline__ void line_solve(const double* c, int L, const double* cp, const double* piv, double* r) {
+  int m = L - 1;
+  for (int j = 0; j < m; ++j) {
+    double sub = (j > 0) ? c[j] : 0.0;
+    r[j] = (r[j] - ((j > 0) ? sub * r[j - 1] : 0.0)) / piv[j];
+  }
+  for (int j = m - 2; j >= 0; --j) r[j] -= cp[j] * r[j + 1];
+}
+
+__global__ void cell_coeff_kernel(bddc_geom G, const double* __restrict__ k, double* __restrict__ coef) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= G.n_cells) return;
+  for (int a = 0; a < 3; ++a) {
+    double v = 0.0;
+    if (a < G.dim) v = G.h[a] * G.h[a] / (6.0 * G.vol) / k[(size_t)c * G.dim + a];
+    coef[(size_t)c * 3 + a] = v;
+  }
+}
+
+// delta per slot: 0.5 (multiplicity) or d_own/(d_own+d_other) with
+// d = h^2/(3 V k) = 2 c (stiffness, decomposition.py:212-239).
+__global__ void weights_kernel(bddc_geom G, int stiffness, const double* __restrict__ coef,
+                               const int* __restrict__ gcode, double* __restrict__ delta) {
+  int i = blockIdx.x;
+  Box b = sub_box(G, i);
+  for (int q = threadIdx.x; q < G.maxG; q += blockDim.x) {
+    int code = gcode[(size_t)i * G.maxG + q];
+    double w = 0.0;
+    if (code >= 0) {
+      w = 0.5;
+      if (stiffness) {
+        SlotLine s = decode_slot(b, code);
+        int k_own = s.side ? s.L - 1 : 0;
+        int own = line_cell_global(G, b, s.a, s.line, k_own);
+        int stride_g = s.a == 0 ? 1 : (s.a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+        int oth = s.side ? own + stride_g : own - stride_g;
+        double d_own = 2.0 * coef[(size_t)own * 3 + s.a];
+        double d_oth = 2.0 * coef[(size_t)oth * 3 + s.a];
+        w = d_own / (d_own + d_oth);
+      }
+    }
+    delta[(size_t)i * G.maxG + q] = w;
+  }
+}
+
+// D_i = mean of diag(A) over the interior dofs on faces of subdomain i
+// (grid.py:344-357).  diag(A) at a dof = 2 c_lo + 2 c_hi (both neighbours).
+__global__ void rescale_kernel(bddc_geom G, const double* __restrict__ coef, double* __restrict__ Dsub) {
+  __shared__ double red[32];
+  int i = blockIdx.x;
+  Box b = sub_box(G, i);
+  double acc = 0.0;
+  int cnt = 0;
+  for (int a = 0; a < G.dim; ++a) {
+    int nl = n_lines(b, a);
+    int L = b.L[a];
+    int nf = (L + 1) * nl;  // faces j = 0..L along every line
+    int stride_g = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+    for (int e = threadIdx.x; e < nf; e += blockDim.x) {
+      int line = e / (L + 1), j = e % (L + 1);
+      int fc = b.o[a] + j;  // global face coordinate along a
+      if (fc < 1 || fc > G.n[a] - 1) continue;
+      int c[3];
+      line_coords(b, a, line, c);
+      int gc[3] = {b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]};
+      gc[a] = fc;  // the cell above the face
+      int hi = cell_id(G, gc[0], gc[1], gc[2]);
+      int lo = hi - stride_g;
+      acc += 2.0 * coef[(size_t)hi * 3 + a] + 2.0 * coef[(size_t)lo * 3 + a];
+      cnt += 1;
+    }
+  }
+  double tot = block_sum(acc, red);
+  double cn = block_sum((double)cnt, red);
+  if (threadIdx.x == 0) Dsub[i] = tot / cn;
+}
+
+// Build P (+alpha 11^T, identity padding), line-compact G and S_A.
+// Gc layout: [i][q][k] (maxG x maxL per subdomain).
+__global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ fslot,
+                                   double* __restrict__ P, double* __restrict__ Gc, double* __restrict__ SAd,
+                                   int* __restrict__ SApart, double* __restrict__ SAoff, double* __restrict__ alpha) {
+  __shared__ double red[32];
+  const int i = blockIdx.x;
+  const Box b = sub_box(G, i);
+  const int np = b.L[0] * b.L[1] * b.L[2];
+  const int mp = G.maxP;
+  double* Pi = P + (size_t)i * mp * mp;
+  for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) Pi[e] = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)G.maxG * G.maxL; e += blockDim.x) Gc[(size_t)i * G.maxG * G.maxL + e] = 0.0;
+  for (int q = threadIdx.x; q < G.maxG; q += blockDim.x) {
+    SAd[(size_t)i * G.maxG + q] = 1.0;
+    SApart[(size_t)i * G.maxG + q] = -1;
+    SAoff[(size_t)i * G.maxG + q] = 0.0;
+  }
+  __syncthreads();
+  for (int a = 0; a < G.dim; ++a) {
+    const int L = b.L[a];
+    const int nl = n_lines(b, a);
+    const int st = axis_stride(b, a);
+    const bool has_lo = b.o[a] > 0, has_hi = b.o[a] + L < G.n[a];
+    for (int line = threadIdx.x; line < nl; line += blockDim.x) {
+      double c[MAXL], cp[MAXL], piv[MAXL], col[MAXL], colp[MAXL];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+      const int base = line_base(b, a, line);
+      const int m = L - 1;
+      if (m > 0) line_factor(c, L, cp, piv);
+      // P_line[k][k'] = Ainv[k-1][k'-1] - Ainv[k-1][k'] - Ainv[k][k'-1] + Ainv[k][k']
+      // Walk columns k' of P_line; keep Ainv columns k'-1 (colp) and k' (col).
+      double a00 = 0.0, aEE = 0.0, a0E = 0.0;
+      for (int j = 0; j < m; ++j) colp[j] = 0.0;
+      for (int kq = 0; kq < L; ++kq) {
+        // col = Ainv[:, kq] (zero if kq == m)
+        for (int j = 0; j < m; ++j) col[j] = (j == kq) ? 1.0 : 0.0;
+        if (kq < m) line_solve(c, L, cp, piv, col);
+        else
+          for (int j = 0; j < m; ++j) col[j] = 0.0;
+        if (kq == 0 && m > 0) {
+          a00 = col[0];
+          a0E = col[m - 1];  // Ainv[m-1][0] = Ainv[0][m-1]
+        }
+        if (kq == m - 1 && m > 0) aEE = col[m - 1];
+        for (int k = 0; k < L; ++k) {
+          double v = 0.0;
+          if (k >= 1) v += colp[k - 1] - col[k - 1];
+          if (k <= m - 1) v += -colp[k] + col[k];
+          // colp = Ainv[:, kq-1]: terms Ainv[k-1][kq-1] - Ainv[k][kq-1]; col: -Ainv[k-1][kq] + Ainv[k][kq]
+          // (signs arranged so that P_line = B Ainv B^T with B[k][k-1]=+1, B[k][k]=-1)
+          if (v != 0.0) Pi[(size_t)(base + k * st) * mp + base + kq * st] += v;
+        }
+        for (int j = 0; j < m; ++j) colp[j] = col[j];
+      }
+      // interface slots at the two ends of the line
+      for (int side = 0; side < 2; ++side) {
+        if (side == 0 && !has_lo) continue;
+        if (side == 1 && !has_hi) continue;
+        int q = fslot[((size_t)i * 6 + a * 2 + side) * G.maxF + line];
+        double* g = Gc + ((size_t)i * G.maxG + q) * G.maxL;
+        int kend = side ? L - 1 : 0;
+        double cend = c[kend];
+        // v = Ainv * (c_end e_jend), jend = 0 (low) or m-1 (high)
+        for (int k = 0; k < L; ++k) g[k] = 0.0;
+        g[kend] = side ? -1.0 : 1.0;
+        if (m > 0) {
+          int jend = side ? m - 1 : 0;
+          for (int j = 0; j < m; ++j) col[j] = (j == jend) ? cend : 0.0;
+          line_solve(c, L, cp, piv, col);
+          for (int k = 0; k < L; ++k) {
+            double bv = 0.0;
+            if (k >= 1) bv += col[k - 1];
+            if (k <= m - 1) bv -= col[k];
+            g[k] -= bv;
+          }
+        }
+        double d = 2.0 * cend;
+        if (m > 0) d -= cend * cend * (side ? aEE : a00);
+        SAd[(size_t)i * G.maxG + q] = d;
+        int other = side ? 0 : 1;
+        bool has_other = other ? has_hi : has_lo;
+        if (has_other) {
+          int q2 = fslot[((size_t)i * 6 + a * 2 + other) * G.maxF + line];
+          SApart[(size_t)i * G.maxG + q] = q2;
+          SAoff[(size_t)i * G.maxG + q] = (m > 0) ? -c[0] * c[L - 1] * a0E : c[0];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // alpha = trace(P)/np^2 ; P += alpha 11^T on the live block ; identity padding
+  double tr = 0.0;
+  for (int r = threadIdx.x; r < np; r += blockDim.x) tr += Pi[(size_t)r * mp + r];
+  tr = block_sum(tr, red);
+  double al = tr / ((double)np * np);
+  if (!(al > 0.0)) al = 1.0;
+  if (threadIdx.x == 0) alpha[i] = al;
+  for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
+    int r = (int)(e / mp), cc = (int)(e % mp);
+    if (r < np && cc < np) Pi[e] += al;
+    else if (r == cc) Pi[e] = 1.0;
+  }
+}
+
+// Q = (P + alpha 11^T)^{-1} - 11^T/(alpha np^2) on the live block; zero padding.
+__global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const double* __restrict__ alpha) {
+  const int i = blockIdx.y;
+  const Box b = sub_box(G, i);
+  const int np = b.L[0] * b.L[1] * b.L[2];
+  const int mp = G.maxP;
+  const double sh = 1.0 / (alpha[i] * (double)np * np);
+  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)mp * mp) return;
+  int r = (int)(e / mp), c = (int)(e % mp);
+  double* Pi = P + (size_t)i * mp * mp;
+  Pi[e] = (r < np && c < np) ? Pi[e] - sh : 0.0;
+}
+
+// Wt[i][q][r] = sum_k Q[cell(q,k)][r] * Gc[q][k]   (W = Q G, stored transposed)
+__global__ void schur_w_kernel(bddc_geom G, const int* __restrict__ gcode, const double* __restrict__ Q,
+                               const double* __restrict__ Gc, double* __restrict__ Wt, int qchunk) {
+  const int i = blockIdx.y;
+  const Box b = sub_box(G, i);
+  const int mp = G.maxP;
+  const double* Qi = Q + (size_t)i * mp * mp;
+  const int q0 = blockIdx.x * qchunk;
+  for (int q = q0; q < imin(q0 + qchunk, G.maxG); ++q) {
+    int code = gcode[(size_t)i * G.maxG + q];
+    double* w = Wt + ((size_t)i * G.maxG + q) * mp;
+    if (code < 0) {
+      for (int r = threadIdx.x; r < mp; r += blockDim.x) w[r] = 0.0;
+      continue;
+    }
+    SlotLine s = decode_slot(b, code);
+    const double* g = Gc + ((size_t)i * G.maxG + q) * G.maxL;
+    for (int r = threadIdx.x; r < mp; r += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < s.L; ++k) acc += Qi[(size_t)(s.base + k * s.stride) * mp + r] * g[k];
+      w[r] = acc;
+    }
+  }
+}
+
+// S[i][q][q'] = S_A[q][q'] + sum_k Gc[q'][k] Wt[q][cell(q',k)]
+__global__ void schur_s_kernel(bddc_geom G, const int* __restrict__ gcode, const double* __restrict__ Gc,
+                               const double* __restrict__ Wt, const double* __restrict__ SAd,
+                               const int* __restrict__ SApart, const double* __restrict__ SAoff,
+                               double* __restrict__ S, int qchunk) {
+  extern __shared__ double wrow[];
+  const int i = blockIdx.y;
+  const Box b = sub_box(G, i);
+  const int mp = G.maxP, mg = G.maxG;
+  const int q0 = blockIdx.x * qchunk;
+  for (int q = q0; q < imin(q0 + qchunk, mg); ++q) {
+    __syncthreads();
+    for (int r = threadIdx.x; r < mp; r += blockDim.x) wrow[r] = Wt[((size_t)i * mg + q) * mp + r];
+    __syncthreads();
+    int codeq = gcode[(size_t)i * mg + q];
+    int partner = SApart[(size_t)i * mg + q];
+    for (int q2 = threadIdx.x; q2 < mg; q2 += blockDim.x) {
+      int code = gcode[(size_t)i * mg + q2];
+      double v;
+      if (codeq < 0 || code < 0) {
+        v = (q == q2) ? 1.0 : 0.0;
+      } else {
+        SlotLine s = decode_slot(b, code);
+        const double* g = Gc + ((size_t)i * mg + q2) * G.maxL;
+        double acc = 0.0;
+        for (int k = 0; k < s.L; ++k) acc += g[k] * wrow[s.base + k * s.stride];
+        if (q2 == q) acc += SAd[(size_t)i * mg + q];
+        if (q2 == partner) acc += SAoff[(size_t)i * mg + q];
+        v = acc;
+      }
+      S[((size_t)i * mg + q) * mg + q2] = v;
+    }
+  }
+}
+
+// S <- (S + S^T)/2 (substructure.py:99), tile-wise through shared memory.
+__global__ void symmetrize_kernel(double* __restrict__ S, int n, long long stride) {
+  __shared__ double t1[32][33], t2[32][33];
+  const int i = blockIdx.z;
+  const int bx = blockIdx.x, by = blockIdx.y;
+  if (by > bx) return;
+  double* Si = S + i * stride;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    int gr = by * 32 + r, gc = bx * 32 + tx;
+    t1[r][tx] = (gr < n && gc < n) ? Si[(size_t)gr * n + gc] : 0.0;
+    int gr2 = bx * 32 + r, gc2 = by * 32 + tx;
+    t2[r][tx] = (gr2 < n && gc2 < n) ? Si[(size_t)gr2 * n + gc2] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    int gr = by * 32 + r, gc = bx * 32 + tx;
+    double v = 0.5 * (t1[r][tx] + t2[tx][r]);
+    if (gr < n && gc < n) Si[(size_t)gr * n + gc] = v;
+    int gr2 = bx * 32 + r, gc2 = by * 32 + tx;
+    double v2 = 0.5 * (t2[r][tx] + t1[tx][r]);
+    if (gr2 < n && gc2 < n) Si[(size_t)gr2 * n + gc2] = v2;
+  }
+}
+
+// Batched interior solve, one CTA per subdomain (see bddc.h).  With
+// B_loc = D B_u (grid.py:250):  p' = Q (B_u A^{-1} f - g/D),
+// u_I = A^{-1}(f - B_u^T p'), p = p'/D  where f = f_flux - A_IG x and
+// g = g_cell - D B_uG x (substructure.py:72-116).
+__global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ gcode,
+                                   const int* __restrict__ gpos, const int* __restrict__ fslot,
+                                   const double* __restrict__ Q, const double* __restrict__ Dsub,
+                                   bddc_local_solve_args A) {
+  extern __shared__ double sm[];
+  const int i = blockIdx.x;
+  const Box b = sub_box(G, i);
+  const int np = b.L[0] * b.L[1] * b.L[2];
+  const int mp = G.maxP, mg = G.maxG;
+  double* xg = sm;            // mg
+  double* rhs = xg + mg;      // mp
+  double* pp = rhs + mp;      // mp
+  double* tI = pp + mp;       // 3 mp (interior faces, per axis blocks)
+  int off[3];
+  {
+    int o = 0;
+    for (int a = 0; a < 3; ++a) {
+      off[a] = o;
+      if (a < G.dim) o += (b.L[a] - 1) * n_lines(b, a);
+    }
+  }
+  const double Di = Dsub[i];
+  for (int q = threadIdx.x; q < mg; q += blockDim.x) {
+    int gp = gpos[(size_t)i * mg + q];
+    xg[q] = (A.x_gamma && gp >= 0) ? A.x_scale * A.x_gamma[gp] : 0.0;
+  }
+  for (int c = threadIdx.x; c < mp; c += blockDim.x) {
+    double v = 0.0;
+    if (c < np && A.g_cell) {
+      int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
+      v = A.g_scale * A.g_cell[cell_id(G, b.o[0] + lx, b.o[1] + ly, b.o[2] + lz)] / Di;
+    }
+    rhs[c] = -v;
+  }
+  __syncthreads();
+  // rhs += B_uG x, one (axis, side) at a time (corner cells are shared)
+  if (A.x_gamma) {
+    for (int a = 0; a < G.dim; ++a) {
+      const int nl = n_lines(b, a), L = b.L[a], st = axis_stride(b, a);
+      for (int side = 0; side < 2; ++side) {
+        for (int line = threadIdx.x; line < nl; line += blockDim.x) {
+          int q = fslot[((size_t)i * 6 + a * 2 + side) * G.maxF + line];
+          if (q < 0) continue;
+          int cell = line_base(b, a, line) + (side ? (L - 1) * st : 0);
+          rhs[cell] += side ? -xg[q] : xg[q];
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // t = A^{-1}(f - A_IG x) per line; rhs += B_u t
+  for (int a = 0; a < G.dim; ++a) {
+    const int L = b.L[a], m = L - 1, nl = n_lines(b, a), st = axis_stride(b, a);
+    for (int line = threadIdx.x; line < nl; line += blockDim.x) {
+      if (m <= 0) continue;
+      double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+      line_factor(c, L, cp, piv);
+      for (int j = 0; j < m; ++j) r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j)] : 0.0;
+      if (A.x_gamma) {
+        int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
+        int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
+        if (qlo >= 0) r[0] -= c[0] * xg[qlo];
+        if (qhi >= 0) r[m - 1] -= c[L - 1] * xg[qhi];
+      }
+      line_solve(c, L, cp, piv, r);
+      double* t = tI + off[a] + line * m;
+      const int base = line_base(b, a, line);
+      for (int j = 0; j < m; ++j) t[j] = r[j];
+      for (int k = 0; k < L; ++k) {
+        double v = 0.0;
+        if (k >= 1) v += r[k - 1];
+        if (k <= m - 1) v -= r[k];
+        rhs[base + k * st] += v;
+      }
+    }
+    __syncthreads();
+  }
+  // p' = Q rhs  (Q symmetric: read row c, coalesced over r)
+  const double* Qi = Q + (size_t)i * mp * mp;
+  for (int r = threadIdx.x; r < mp; r += blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < np; ++c) acc += Qi[(size_t)c * mp + r] * rhs[c];
+    pp[r] = acc;
+  }
+  __syncthreads();
+  // u_I = t - A^{-1} B_u^T p'
+  for (int a = 0; a < G.dim; ++a) {
+    const int L = b.L[a], m = L - 1, nl = n_lines(b, a), st = axis_stride(b, a);
+    for (int line = threadIdx.x; line < nl; line += blockDim.x) {
+      if (m <= 0) continue;
+      double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+      line_factor(c, L, cp, piv);
+      const int base = line_base(b, a, line);
+      for (int j = 0; j < m; ++j) r[j] = pp[base + (j + 1) * st] - pp[base + j * st];
+      line_solve(c, L, cp, piv, r);
+      double* t = tI + off[a] + line * m;
+      for (int j = 0; j < m; ++j) {
+        double u = t[j] - r[j];
+        t[j] = u;
+        if (A.u_out) {
+          size_t d = (size_t)line_face_dof(G, b, a, line, j);
+          if (A.u_mode) A.u_out[d] += u;
+          else A.u_out[d] = u;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (A.p_out) {
+    for (int c = threadIdx.x; c < np; c += blockDim.x) {
+      int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
+      A.p_out[cell_id(G, b.o[0] + lx, b.o[1] + ly, b.o[2] + lz)] = pp[c] / Di;
+    }
+  }
+  if (A.rg_broken) {
+    for (int q = threadIdx.x; q < mg; q += blockDim.x) {
+      int code = gcode[(size_t)i * mg + q];
+      double v = 0.0;
+      if (code >= 0) {
+        SlotLine s = decode_slot(b, code);
+        int m = s.L - 1;
+        int kend = s.side ? s.L - 1 : 0;
+        if (m > 0) {
+          double cend = coef[(size_t)line_cell_global(G, b, s.a, s.line, kend) * 3 + s.a];
+          int jend = s.side ? m - 1 : 0;
+          v += cend * tI[off[s.a] + s.line * m + jend];
+        }
+        double pc = pp[s.base + kend * s.stride];
+        v += s.side ? -pc : pc;
+      }
+      A.rg_broken[(size_t)i * mg + q] = v;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int bddc_cell_coeffs(const bddc_geom* g, const double* k, double* coef, void* stream) {
+  cell_coeff_kernel<<<(g->n_cells + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*g, k, coef);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_weights(const bddc_geom* g, int stiffness, const double* coef, const int* gcode, double* delta,
+                            void* stream) {
+  weights_kernel<<<g->N, 128, 0, (cudaStream_t)stream>>>(*g, stiffness, coef, gcode, delta);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_rescale(const bddc_geom* g, const double* coef, double* Dsub, void* stream) {
+  rescale_kernel<<<g->N, 256, 0, (cudaStream_t)stream>>>(*g, coef, Dsub);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_local_build(const bddc_geom* g, const double* coef, const int* fslot, double* P, double* Gc,
+                                double* SAd, int* SApart, double* SAoff, double* alpha, void* stream) {
+  if (g->maxL > MAXL) return bddc_set_error(BDDC_ERR_ARG, "subdomain strip wider than MAXL=32 cells");
+  local_build_kernel<<<g->N, 128, 0, (cudaStream_t)stream>>>(*g, coef, fslot, P, Gc, SAd, SApart, SAoff, alpha);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* alpha, void* stream) {
+  size_t n = (size_t)g->maxP * g->maxP;
+  dim3 grid((unsigned)((n + 255) / 256), g->N);
+  pinv_fix_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*g, P, alpha);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_local_schur(const bddc_geom* g, const int* gcode, const double* Q, const double* Gc,
+                                const double* SAd, const int* SApart, const double* SAoff, double* Wt, double* S,
+                                void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int qchunk = 8;
+  dim3 gw((g->maxG + qchunk - 1) / qchunk, g->N);
+  schur_w_kernel<<<gw, 256, 0, s>>>(*g, gcode, Q, Gc, Wt, qchunk);
+  LAUNCH_OK();
+  size_t shm = (size_t)g->maxP * sizeof(double);
+  schur_s_kernel<<<gw, 256, shm, s>>>(*g, gcode, Gc, Wt, SAd, SApart, SAoff, S, qchunk);
+  LAUNCH_OK();
+  dim3 gs((g->maxG + 31) / 32, (g->maxG + 31) / 32, g->N);
+  symmetrize_kernel<<<gs, dim3(32, 8), 0, s>>>(S, g->maxG, (long long)g->maxG * g->maxG);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, const int* gpos,
+                                const int* fslot, const double* Q, const double* Dsub,
+                                const bddc_local_solve_args* a, void* stream) {
+  size_t shm = (size_t)(g->maxG + 5 * g->maxP) * sizeof(double);
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  local_solve_kernel<<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
+  LAUNCH_OK();
+  return 0;
+}

@@ -1,0 +1,446 @@
+// Interface operator, BDDC preconditioner pieces, balanced projection and
+// deterministic PCG vector kernels (solver.py:97-251).
+//
+// Interface vectors are "continuous" (indexed like dec.gamma) or "broken"
+// (per subdomain slot, N x maxG).  Scatter = owner reads both copies in the
+// fixed order low-subdomain + high-subdomain, which is the reference's
+// np.add.at order (solver.py:100-101); every reduction is a fixed-shape tree,
+// so repeated solves are bitwise identical (test_solver.py:165-173).
+#include "common.cuh"
+
+#define DOT_BLOCKS 296
+#define DOT_THREADS 256
+
+namespace {
+
+// y_b[i][q] = sum_c M_i[q][c] * win[i][c] * x[gpos[i][c]]   (c < nG[i])
+__global__ void gather_gemv_kernel(int maxG, const int* __restrict__ nG, const int* __restrict__ gpos,
+                                   const double* __restrict__ Mats, const double* __restrict__ x,
+                                   const double* __restrict__ win, double* __restrict__ yb) {
+  extern __shared__ double xs[];
+  const int i = blockIdx.x;
+  const int n = nG[i];
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double v = x[gpos[(size_t)i * maxG + c]];
+    if (win) v *= win[(size_t)i * maxG + c];
+    xs[c] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Mi = Mats + (size_t)i * maxG * maxG;
+  for (int q = warp; q < n; q += nw) {
+    const double* row = Mi + (size_t)q * maxG;
+    double acc = 0.0;
+    for (int c = lane; c < n; c += 32) acc += row[c] * xs[c];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) yb[(size_t)i * maxG + q] = acc;
+  }
+}
+
+// v[i][r] = sum_q Psi[i][q][r] * win[i][q] * x[gpos[i][q]]
+__global__ void gather_gemv_t_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ nC,
+                                     const int* __restrict__ gpos, const double* __restrict__ Psi,
+                                     const double* __restrict__ x, const double* __restrict__ win,
+                                     double* __restrict__ v) {
+  extern __shared__ double xs[];
+  const int i = blockIdx.x;
+  const int n = nG[i], nc = nC[i];
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double t = x[gpos[(size_t)i * maxG + c]];
+    if (win) t *= win[(size_t)i * maxG + c];
+    xs[c] = t;
+  }
+  __syncthreads();
+  const double* Pi = Psi + (size_t)i * maxG * maxC;
+  for (int r = threadIdx.x; r < maxC; r += blockDim.x) {
+    double acc = 0.0;
+    if (r < nc)
+      for (int q = 0; q < n; ++q) acc += Pi[(size_t)q * maxC + r] * xs[q];
+    v[(size_t)i * maxC + r] = acc;
+  }
+}
+
+// rhs[g] = v[lo] - v[hi]  (sigma = +1 lower owner, -1 upper owner)
+__global__ void coarse_restrict_kernel(int nfc, const int* __restrict__ cown, const double* __restrict__ v,
+                                       double* __restrict__ rhs) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nfc) return;
+  rhs[g] = v[cown[2 * g]] - v[cown[2 * g + 1]];
+}
+
+// out_b[i][q] = wout[i][q] * (y_b[i][q] + sum_r Psi[i][q][r] sigma_r xc[g_r])
+__global__ void prolong_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ sub_rows,
+                               const double* __restrict__ Psi, const double* __restrict__ xc,
+                               const double* __restrict__ yb, const double* __restrict__ wout,
+                               double* __restrict__ outb) {
+  extern __shared__ double cf[];
+  const int i = blockIdx.x;
+  const int n = nG[i];
+  for (int r = threadIdx.x; r < maxC; r += blockDim.x) {
+    const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
+    cf[r] = (sr[0] >= 0) ? (double)sr[3] * xc[sr[0]] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Pi = Psi + (size_t)i * maxG * maxC;
+  for (int q = warp; q < n; q += nw) {
+    const double* row = Pi + (size_t)q * maxC;
+    double acc = 0.0;
+    for (int r = lane; r < maxC; r += 32) acc += row[r] * cf[r];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      size_t s = (size_t)i * maxG + q;
+      double w = yb ? yb[s] + acc : acc;
+      outb[s] = wout ? wout[s] * w : w;
+    }
+  }
+}
+
+// y[d] = y_b[lo slot] + y_b[hi slot]
+__global__ void scatter_kernel(int n_gamma, const int* __restrict__ gown, const double* __restrict__ yb,
+                               double* __restrict__ y) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_gamma) return;
+  y[d] = yb[gown[2 * d]] + yb[gown[2 * d + 1]];
+}
+
+// phi[i] = sum_q sign_q y[gpos[i][q]], sign = +1 on the high side of the box
+__global__ void phi_kernel(int maxG, const int* __restrict__ nG, const int* __restrict__ gpos,
+                           const int* __restrict__ gcode, const double* __restrict__ y, double* __restrict__ phi) {
+  __shared__ double red[32];
+  const int i = blockIdx.x;
+  double acc = 0.0;
+  for (int q = threadIdx.x; q < nG[i]; q += blockDim.x) {
+    size_t s = (size_t)i * maxG + q;
+    double v = y[gpos[s]];
+    acc += ((gcode[s] >> 2) & 1) ? v : -v;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) phi[i] = acc;
+}
+
+// Separable Laplacian solve on the S[0] x S[1] x S[2] subdomain grid:
+// z = Dm (Qx (x) Qy (x) Qz) Lambda^+ (..)^T Dm phi  (Dm = D^{-1/2} or NULL).
+// eig layout: [Qx (Sx*Sx) | Qy | Qz | lx (Sx) | ly | lz], Q row-major Q[a][a'].
+__global__ void lap_solve_kernel(int S0, int S1, int S2, const double* __restrict__ eig,
+                                 const double* __restrict__ dm, const double* __restrict__ phi,
+                                 double* __restrict__ z) {
+  extern __shared__ double sm[];
+  const int N = S0 * S1 * S2;
+  double* u = sm;
+  double* w = u + N;
+  const double* Q[3] = {eig, eig + S0 * S0, eig + S0 * S0 + S1 * S1};
+  const double* lam = eig + S0 * S0 + S1 * S1 + S2 * S2;
+  const double* lx = lam;
+  const double* ly = lam + S0;
+  const double* lz = lam + S0 + S1;
+  const int Sd[3] = {S0, S1, S2};
+  const int st[3] = {1, S0, S0 * S1};
+  for (int e = threadIdx.x; e < N; e += blockDim.x) u[e] = dm ? dm[e] * phi[e] : phi[e];
+  __syncthreads();
+  // forward: apply Q_a^T along every axis
+  for (int a = 0; a < 3; ++a) {
+    double* src = (a & 1) ? w : u;
+    double* dst = (a & 1) ? u : w;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      int ca = (e / st[a]) % Sd[a];
+      int base = e - ca * st[a];
+      double acc = 0.0;
+      for (int k = 0; k < Sd[a]; ++k) acc += Q[a][k * Sd[a] + ca] * src[base + k * st[a]];
+      dst[e] = acc;
+    }
+    __syncthreads();
+  }
+  // after 3 passes the data is in w
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int a0 = e % S0, a1 = (e / S0) % S1, a2 = e / (S0 * S1);
+    double l = lx[a0] + ly[a1] + lz[a2];
+    w[e] = (a0 == 0 && a1 == 0 && a2 == 0) ? 0.0 : w[e] / l;
+  }
+  __syncthreads();
+  for (int a = 0; a < 3; ++a) {
+    double* src = (a & 1) ? u : w;
+    double* dst = (a & 1) ? w : u;
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      int ca = (e / st[a]) % Sd[a];
+      int base = e - ca * st[a];
+      double acc = 0.0;
+      for (int k = 0; k < Sd[a]; ++k) acc += Q[a][ca * Sd[a] + k] * src[base + k * st[a]];
+      dst[e] = acc;
+    }
+    __syncthreads();
+  }
+  // result in u
+  for (int e = threadIdx.x; e < N; e += blockDim.x) z[e] = dm ? dm[e] * u[e] : u[e];
+}
+
+// y[d] -= z[lo(d)] - z[hi(d)]   (Phi^T z with sign_lo = +1, sign_hi = -1)
+__global__ void proj_apply_kernel(int n_gamma, int maxG, const int* __restrict__ gown, const double* __restrict__ z,
+                                  double* __restrict__ y) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n_gamma) return;
+  int lo = gown[2 * d] / maxG, hi = gown[2 * d + 1] / maxG;
+  y[d] -= z[lo] - z[hi];
+}
+
+// ------------------------------------------------------------- dot products
+
+// Fused deterministic dot: per-block partials, the last block to finish sums
+// them in index order and applies `op` (see bddc_dot).
+__global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, long long n,
+                           double* __restrict__ partial, unsigned* __restrict__ counter,
+                           double* __restrict__ scal, int op, double* __restrict__ hist, int it) {
+  __shared__ double red[32];
+  __shared__ bool last;
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    acc += x[e] * y[e];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = acc;
+    __threadfence();
+    unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s = 0.0;
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += ((volatile double*)partial)[b];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    // scal slots: 0 rz, 1 pAp, 2 alpha, 3 rr, 4 res0, 5 relres, 6 rz_new, 7 beta, 8 bad
+    switch (op) {
+      case 0:  // rz (initial)
+        scal[0] = s;
+        break;
+      case 1: {  // pAp -> alpha
+        scal[1] = s;
+        double a = scal[0] / s;
+        if (!(s > 0.0)) scal[8] = 1.0;
+        scal[2] = a;
+        if (hist) hist[it] = a;
+        break;
+      }
+      case 2:  // rr -> relres
+        scal[3] = s;
+        scal[5] = sqrt(s) / scal[4];
+        break;
+      case 3: {  // rz_new -> beta
+        double b = s / scal[0];
+        scal[6] = s;
+        scal[7] = b;
+        scal[0] = s;
+        if (hist) hist[it] = b;
+        break;
+      }
+      case 4:  // res0 = sqrt(rr)
+        scal[3] = s;
+        scal[4] = sqrt(s);
+        break;
+      default:  // plain store into slot (op - 100)
+        scal[op - 100] = s;
+    }
+  }
+}
+
+// x += alpha p ; r -= alpha Ap
+__global__ void cg_update_kernel(long long n, const double* __restrict__ scal, double* __restrict__ x,
+                                 const double* __restrict__ p, double* __restrict__ r, const double* __restrict__ Ap) {
+  const double a = scal[2];
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    x[e] += a * p[e];
+    r[e] -= a * Ap[e];
+  }
+}
+
+// p = z + beta p
+__global__ void p_update_kernel(long long n, const double* __restrict__ scal, const double* __restrict__ z,
+                                double* __restrict__ p) {
+  const double b = scal[7];
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    p[e] = z[e] + b * p[e];
+}
+
+// Dense (row-major, symmetric) GEMV y = M x over n rows, warp per row.
+__global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ M, const double* __restrict__ x,
+                            double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const double* mr = M + (size_t)row * ld;
+  double acc = 0.0;
+  for (int c = lane; c < ncol; c += 32) acc += mr[c] * x[c];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[row] = acc;
+}
+
+// Lanczos tridiagonal from CG coefficients (solver.py:236-251); kappa by
+// Sturm bisection for the extreme eigenvalues.
+__device__ int sturm_count(const double* d, const double* e2, int m, double x) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (q < 0) ++cnt;
+  for (int k = 1; k < m; ++k) {
+    if (q == 0.0) q = 1e-300;
+    q = d[k] - x - e2[k - 1] / q;
+    if (q < 0) ++cnt;
+  }
+  return cnt;
+}
+
+__global__ void lanczos_kernel(int m, const double* __restrict__ al, const double* __restrict__ be,
+                               double* __restrict__ work, double* __restrict__ out) {
+  double* d = work;
+  double* e2 = work + m;
+  if (threadIdx.x == 0) {
+    d[0] = 1.0 / al[0];
+    for (int k = 1; k < m; ++k) {
+      d[k] = 1.0 / al[k] + be[k - 1] / al[k - 1];
+      double o = sqrt(fmax(be[k - 1], 0.0)) / al[k - 1];
+      e2[k - 1] = o * o;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double lo = 1e308, hi = -1e308;
+    for (int k = 0; k < m; ++k) {
+      double r = 0.0;
+      if (k > 0) r += sqrt(e2[k - 1]);
+      if (k < m - 1) r += sqrt(e2[k]);
+      lo = fmin(lo, d[k] - r);
+      hi = fmax(hi, d[k] + r);
+    }
+    // threadIdx 0: smallest (count >= 1), 1: largest (count >= m)
+    int target = threadIdx.x == 0 ? 1 : m;
+    double a = lo, b = hi;
+    for (int itb = 0; itb < 200; ++itb) {
+      double mid = 0.5 * (a + b);
+      if (mid == a || mid == b) break;
+      if (sturm_count(d, e2, m, mid) >= target) b = mid;
+      else a = mid;
+    }
+    out[threadIdx.x] = 0.5 * (a + b);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double lmin = fmax(out[0], 2.2250738585072014e-308);
+    out[2] = out[1] / lmin;
+  }
+}
+
+__global__ void axpby_kernel(long long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    y[e] = a * x[e] + (b == 0.0 ? 0.0 : b * y[e]);
+}
+
+}  // namespace
+
+extern "C" int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos, const double* Mats, const double* x,
+                                const double* win, double* yb, void* stream) {
+  gather_gemv_kernel<<<N, 256, maxG * sizeof(double), (cudaStream_t)stream>>>(maxG, nG, gpos, Mats, x, win, yb);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,
+                                  const double* Psi, const double* x, const double* win, double* v, void* stream) {
+  gather_gemv_t_kernel<<<N, 128, maxG * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, gpos, Psi, x,
+                                                                                  win, v);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_coarse_restrict(int nfc, const int* cown, const double* v, double* rhs, void* stream) {
+  if (nfc <= 0) return 0;
+  coarse_restrict_kernel<<<(nfc + 255) / 256, 256, 0, (cudaStream_t)stream>>>(nfc, cown, v, rhs);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* sub_rows, const double* Psi,
+                            const double* xc, const double* yb, const double* wout, double* outb, void* stream) {
+  prolong_kernel<<<N, 256, maxC * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, sub_rows, Psi, xc, yb,
+                                                                          wout, outb);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_scatter(int n_gamma, const int* gown, const double* yb, double* y, void* stream) {
+  if (n_gamma <= 0) return 0;
+  scatter_kernel<<<(n_gamma + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n_gamma, gown, yb, y);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const double* y, double* phi,
+                        void* stream) {
+  phi_kernel<<<N, 256, 0, (cudaStream_t)stream>>>(maxG, nG, gpos, gcode, y, phi);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi, double* z,
+                              void* stream) {
+  int N = S0 * S1 * S2;
+  size_t shm = 2 * (size_t)N * sizeof(double);
+  if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "lap_solve: too many subdomains for one CTA");
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(lap_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  lap_solve_kernel<<<1, 1024, shm, (cudaStream_t)stream>>>(S0, S1, S2, eig, dm, phi, z);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const double* z, double* y, void* stream) {
+  if (n_gamma <= 0) return 0;
+  proj_apply_kernel<<<(n_gamma + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n_gamma, maxG, gown, z, y);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" size_t bddc_dot_workspace(void) { return DOT_BLOCKS * sizeof(double) + 64; }
+
+extern "C" int bddc_dot(const double* x, const double* y, long long n, void* ws, double* scal, int op, double* hist,
+                        int it, void* stream) {
+  double* partial = (double*)ws;
+  unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
+  dot_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n, partial, counter, scal, op, hist, it);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_cg_update(long long n, const double* scal, double* x, const double* p, double* r, const double* Ap,
+                              void* stream) {
+  cg_update_kernel<<<DOT_BLOCKS, 256, 0, (cudaStream_t)stream>>>(n, scal, x, p, r, Ap);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream) {
+  p_update_kernel<<<DOT_BLOCKS, 256, 0, (cudaStream_t)stream>>>(n, scal, z, p);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream) {
+  if (n <= 0) return 0;
+  gemv_kernel<<<(n + 7) / 8, 256, 0, (cudaStream_t)stream>>>(n, ld, ncol, M, x, y);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out, void* stream) {
+  if (m <= 0) return 0;
+  lanczos_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(m, al, be, work, out);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_axpby(long long n, double a, const double* x, double b, double* y, void* stream) {
+  if (n <= 0) return 0;
+  axpby_kernel<<<DOT_BLOCKS, 256, 0, (cudaStream_t)stream>>>(n, a, x, b, y);
+  LAUNCH_OK();
+  return 0;
+}

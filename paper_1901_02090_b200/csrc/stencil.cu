@@ -1,0 +1,273 @@
+// Matrix-free RT0/P0 operators on the structured grid and the fast pressure
+// recovery (grid.py:270-341, solver.py:254-274, 337-342).
+//
+//  (A u)_d  = 2(c_lo + c_hi) u_d + c_lo u_{d-} + c_hi u_{d+}   (lines of axis a)
+//  (B u)_c  = sum_a u_{low face} - u_{high face}                 (boundary faces = 0)
+//  (B^T p)_d = p_hi - p_lo
+// Pressure recovery solves the D-free Neumann problem B B^T p = B(-A u)
+// (equivalent to the reference's pinned (Bs Bs^T) solve after unscaling and
+// re-centring) by an orthonormal DCT-II eigenbasis: three mode products with
+// dense cosine matrices on DMMA, a diagonal scale, and three more products.
+#include "common.cuh"
+
+extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
+                                  int lda, long long sA, const double* B, int ldb, long long sB, double beta,
+                                  double* C, int ldc, long long sC, int batch, int upper, void* stream);
+
+namespace {
+
+__device__ __forceinline__ void decode_dof(const bddc_geom& G, int d, int& a, int f[3]) {
+  a = (d >= G.fam_off[1]) + (d >= G.fam_off[2]);
+  int r = d - G.fam_off[a];
+  int e0 = G.n[0] - (a == 0), e1 = G.n[1] - (a == 1);
+  f[0] = r % e0;
+  f[1] = (r / e0) % e1;
+  f[2] = r / (e0 * e1);
+  f[a] += 1;  // face coordinate along a in 1..n_a-1
+}
+
+// y = alpha * A u + beta * y
+__global__ void flux_A_kernel(bddc_geom G, const double* __restrict__ coef, const double* __restrict__ u, double alpha,
+                              double beta, double* __restrict__ y) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
+       e += (long long)gridDim.x * blockDim.x) {
+    int d = (int)e, a, f[3];
+    decode_dof(G, d, a, f);
+    int hi = cell_id(G, f[0], f[1], f[2]);
+    int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+    int lo = hi - st;
+    double clo = coef[(size_t)lo * 3 + a], chi = coef[(size_t)hi * 3 + a];
+    double v = 2.0 * (clo + chi) * u[d];
+    // dof stride along a inside family a equals the cell stride st
+    if (f[a] > 1) v += clo * u[d - st];
+    if (f[a] < G.n[a] - 1) v += chi * u[d + st];
+    y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
+  }
+}
+
+// out_c = s_f * fvec_c + s_b * Dcell_c * (B u)_c   (Dcell = D of the cell's subdomain, or 1)
+__global__ void cell_div_kernel(bddc_geom G, const double* __restrict__ u, const double* __restrict__ fvec, double s_f,
+                                double s_b, const int* __restrict__ cell_sub, const double* __restrict__ Dsub,
+                                double* __restrict__ out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_cells;
+       e += (long long)gridDim.x * blockDim.x) {
+    int c = (int)e;
+    int x = c % G.n[0], y = (c / G.n[0]) % G.n[1], z = c / (G.n[0] * G.n[1]);
+    int cc[3] = {x, y, z};
+    double b = 0.0;
+    for (int a = 0; a < G.dim; ++a) {
+      if (cc[a] > 0) {  // low face interior
+        int f[3] = {x, y, z};
+        b += u[face_dof(G, a, f[0], f[1], f[2])];
+      }
+      if (cc[a] < G.n[a] - 1) {  // high face interior
+        int f[3] = {x, y, z};
+        f[a] += 1;
+        b -= u[face_dof(G, a, f[0], f[1], f[2])];
+      }
+    }
+    double D = Dsub ? Dsub[cell_sub[c]] : 1.0;
+    double v = s_b * D * b;
+    if (fvec) v += s_f * fvec[c];
+    out[c] = v;
+  }
+}
+
+// y_d = alpha (p_hi - p_lo) + beta y_d
+__global__ void grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha, double beta,
+                            double* __restrict__ y) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
+       e += (long long)gridDim.x * blockDim.x) {
+    int d = (int)e, a, f[3];
+    decode_dof(G, d, a, f);
+    int hi = cell_id(G, f[0], f[1], f[2]);
+    int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+    double v = alpha * (p[hi] - p[hi - st]);
+    y[d] = v + (beta == 0.0 ? 0.0 : beta * y[d]);
+  }
+}
+
+// Orthonormal DCT-II matrix C[k][x] = s_k cos(pi k (x+1/2)/n) and eigenvalues 4 sin^2(pi k/(2n)).
+__global__ void dct_matrix_kernel(int n, double* __restrict__ C, double* __restrict__ lam) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n * n) {
+    int k = e / n, x = e % n;
+    double s = (k == 0) ? sqrt(1.0 / n) : sqrt(2.0 / n);
+    C[e] = s * cospi((double)k * (x + 0.5) / n);
+  }
+  if (e < n) {
+    double sn = sinpi((double)e / (2.0 * n));
+    lam[e] = 4.0 * sn * sn;
+  }
+}
+
+__global__ void dct_scale_kernel(int nx, int ny, int nz, const double* __restrict__ lx, const double* __restrict__ ly,
+                                 const double* __restrict__ lz, double* __restrict__ v) {
+  long long n = (long long)nx * ny * nz;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    int x = (int)(e % nx), y = (int)((e / nx) % ny), z = (int)(e / ((long long)nx * ny));
+    double l = lx[x] + ly[y] + lz[z];
+    v[e] = (x == 0 && y == 0 && z == 0) ? 0.0 : v[e] / l;
+  }
+}
+
+__global__ void sub_mean_kernel(long long n, const double* __restrict__ sum, double* __restrict__ v) {
+  const double m = sum[0] / (double)n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    v[e] -= m;
+}
+
+}  // namespace
+
+extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double* u, double alpha, double beta,
+                           double* y, void* stream) {
+  flux_A_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, coef, u, alpha, beta, y);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_cell_div(const bddc_geom* g, const double* u, const double* fvec, double s_f, double s_b,
+                             const int* cell_sub, const double* Dsub, double* out, void* stream) {
+  cell_div_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b, cell_sub, Dsub, out);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_grad(const bddc_geom* g, const double* p, double alpha, double beta, double* y, void* stream) {
+  grad_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, p, alpha, beta, y);
+  LAUNCH_OK();
+  return 0;
+}
+
+// dct: workspace with C_x, C_y, C_z (n_a^2) and eigenvalues (n_a), built once.
+extern "C" int bddc_dct_init(const bddc_geom* g, double* dct, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double* p = dct;
+  for (int a = 0; a < 3; ++a) {
+    int n = g->n[a];
+    dct_matrix_kernel<<<(n * n + 255) / 256, 256, 0, s>>>(n, p, p + n * n);
+    LAUNCH_OK();
+    p += n * n + n;
+  }
+  return 0;
+}
+
+// Solve (B B^T) p = rhs for the zero-mean p, in place on rhs (n_cells).
+// tmp: n_cells doubles.
+extern "C" int bddc_neumann_solve(const bddc_geom* g, const double* dct, double* rhs, double* tmp, void* stream) {
+  const int nx = g->n[0], ny = g->n[1], nz = g->n[2];
+  const double* Cx = dct;
+  const double* lx = Cx + nx * nx;
+  const double* Cy = lx + nx;
+  const double* ly = Cy + ny * ny;
+  const double* Cz = ly + ny;
+  const double* lz = Cz + nz * nz;
+  int r;
+  // forward: v1 = rhs . Cx^T  (rows = (z,y), cols = x)
+  if ((r = bddc_dgemm_batched(0, 1, ny * nz, nx, nx, 1.0, rhs, nx, 0, Cx, nx, 0, 0.0, tmp, nx, 0, 1, 0, stream)))
+    return r;
+  // v2[z] = Cy . v1[z]
+  if ((r = bddc_dgemm_batched(0, 0, ny, nx, ny, 1.0, Cy, ny, 0, tmp, nx, (long long)nx * ny, 0.0, rhs, nx,
+                              (long long)nx * ny, nz, 0, stream)))
+    return r;
+  // v3 = Cz . v2  (rows z, cols (y,x))
+  if ((r = bddc_dgemm_batched(0, 0, nz, nx * ny, nz, 1.0, Cz, nz, 0, rhs, nx * ny, 0, 0.0, tmp, nx * ny, 0, 1, 0,
+                              stream)))
+    return r;
+  dct_scale_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, lx, ly, lz, tmp);
+  LAUNCH_OK();
+  // inverse: v2 = Cz^T v3
+  if ((r = bddc_dgemm_batched(1, 0, nz, nx * ny, nz, 1.0, Cz, nz, 0, tmp, nx * ny, 0, 0.0, rhs, nx * ny, 0, 1, 0,
+                              stream)))
+    return r;
+  // v1[z] = Cy^T v2[z]
+  if ((r = bddc_dgemm_batched(1, 0, ny, nx, ny, 1.0, Cy, ny, 0, rhs, nx, (long long)nx * ny, 0.0, tmp, nx,
+                              (long long)nx * ny, nz, 0, stream)))
+    return r;
+  // p = v1 . Cx
+  if ((r = bddc_dgemm_batched(0, 0, ny * nz, nx, nx, 1.0, tmp, nx, 0, Cx, nx, 0, 0.0, rhs, nx, 0, 1, 0, stream)))
+    return r;
+  return 0;
+}
+
+extern "C" int bddc_sub_mean(long long n, const double* sum, double* v, void* stream) {
+  sub_mean_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(n, sum, v);
+  LAUNCH_OK();
+  return 0;
+}
+
+namespace {
+
+// out[i] = scale * sum_{cells of i} v[c] / (Dsub ? Dsub[i] : 1)
+__global__ void sub_sum_kernel(bddc_geom G, const double* __restrict__ v, double* __restrict__ out, double scale,
+                               const double* __restrict__ Dsub) {
+  __shared__ double red[32];
+  const int i = blockIdx.x;
+  const Box b = sub_box(G, i);
+  const int np = b.L[0] * b.L[1] * b.L[2];
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < np; c += blockDim.x) {
+    int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
+    acc += v[cell_id(G, b.o[0] + lx, b.o[1] + ly, b.o[2] + lz)];
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) out[i] = scale * acc / (Dsub ? Dsub[i] : 1.0);
+}
+
+__global__ void gamma_flux_kernel(int n, const int* __restrict__ gamma, double* __restrict__ gv,
+                                  double* __restrict__ flux, int mode) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  if (mode == 0) flux[gamma[d]] = gv[d];
+  else if (mode == 1) flux[gamma[d]] += gv[d];
+  else gv[d] = flux[gamma[d]];
+}
+
+// balanced_shift (solver.py:146-164): w[d] = (z[i_f] - z[j_f]) / m_f
+__global__ void face_shift_kernel(int n, const int* __restrict__ gface, const int* __restrict__ faces,
+                                  const double* __restrict__ z, double* __restrict__ w) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  int f = gface[d];
+  w[d] = (z[faces[4 * f]] - z[faces[4 * f + 1]]) / (double)faces[4 * f + 3];
+}
+
+}  // namespace
+
+extern "C" int bddc_sub_sum(const bddc_geom* g, const double* v, double* out, double scale, const double* Dsub,
+                            void* stream) {
+  sub_sum_kernel<<<g->N, 256, 0, (cudaStream_t)stream>>>(*g, v, out, scale, Dsub);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_gamma_flux(int n, const int* gamma, double* gv, double* flux, int mode, void* stream) {
+  if (n <= 0) return 0;
+  gamma_flux_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, gamma, gv, flux, mode);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_face_shift(int n, int n_faces, const int* gface, const int* faces, const double* z, double* w,
+                               void* stream) {
+  if (n <= 0) return 0;
+  face_shift_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, gface, faces, z, w);
+  LAUNCH_OK();
+  return 0;
+}
+
+namespace {
+__global__ void scale_cells_kernel(int n, const double* __restrict__ f, const int* __restrict__ cell_sub,
+                                   const double* __restrict__ Dsub, double* __restrict__ out) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) out[c] = Dsub[cell_sub[c]] * f[c];
+}
+}  // namespace
+
+// fs = D f (grid.py:250-251)
+extern "C" int bddc_scale_cells(const bddc_geom* g, const double* f, const int* cell_sub, const double* Dsub,
+                                double* out, void* stream) {
+  scale_cells_kernel<<<(g->n_cells + 255) / 256, 256, 0, (cudaStream_t)stream>>>(g->n_cells, f, cell_sub, Dsub, out);
+  LAUNCH_OK();
+  return 0;
+}

@@ -1,0 +1,294 @@
+"""Regular (box) partitions and the interface topology, in closed form.
+
+Mirrors `regular_partition` / `Decomposition` of the reference
+(`/root/reference/pkg/src/bddcflow/decomposition.py:32-151`).  For box
+subdomains the reference's hinge-connected face components
+(`decomposition.py:84-100`) are always single rectangles and every
+subdomain is connected, so the topology has closed forms; the tables below
+are what the device kernels consume:
+
+* `gpos[i, q]`   position in `gamma` of the q-th interface slot of i
+                 (slots sorted by global dof, like `gamma_dofs[i]`)
+* `gcode[i, q]`  axis | side << 2 | line << 3 of that slot (side 1 = high
+                 face of the box, line = transverse local index, x-fastest)
+* `fslot[i, 2a+side, line]` inverse of gcode
+* `gown[d]`      broken-slot ids (i*maxG+q) of the low / high copy of dof d
+* `faces[f]`     (i, j, axis, m) for subdomain pairs i < j, sorted
+* eigen data of the separable subdomain-graph Laplacians used by the
+  balanced projection (solver.py:166-179) and the balanced shift
+  (solver.py:146-164).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+
+from .errors import InvalidArgumentError
+
+MAX_STRIPS = 64
+
+
+def near_equal_splits(n, s):
+    """decomposition.py:128-130."""
+    base, extra = divmod(n, s)
+    return [base + 1 if k < extra else base for k in range(s)]
+
+
+def _pad(n, m):
+    return max(m, ((n + m - 1) // m) * m)
+
+
+@dataclass(frozen=True)
+class FaceComponent:
+    """decomposition.py:22-29 (one component per box face)."""
+
+    i: int
+    j: int
+    dofs: np.ndarray
+    sign_i: np.ndarray
+
+
+class Decomposition:
+    def __init__(self, grid, splits):
+        splits = tuple(int(s) for s in splits)
+        if len(splits) != grid.dim or any(s < 1 for s in splits):
+            raise InvalidArgumentError("need one split >= 1 per axis")
+        if any(s > c for s, c in zip(splits, grid.counts)):
+            raise InvalidArgumentError("splits exceed cell counts")
+        if any(s > MAX_STRIPS for s in splits):
+            raise InvalidArgumentError(f"at most {MAX_STRIPS} strips per axis")
+        self.grid = grid
+        self.splits = splits
+        dim = grid.dim
+        n3 = tuple(grid.counts) + (1,) * (3 - dim)
+        S3 = splits + (1,) * (3 - dim)
+        self.n3, self.S3 = n3, S3
+        self.sw = [np.array(near_equal_splits(n3[a], S3[a]), dtype=np.int64)
+                   for a in range(3)]
+        self.so = [np.concatenate([[0], np.cumsum(w)[:-1]]) for w in self.sw]
+        strip_of = [np.repeat(np.arange(S3[a]), self.sw[a]) for a in range(3)]
+        self.strip_of = strip_of
+        N = int(np.prod(S3))
+        self.n_subdomains = N
+        sub = np.arange(N)
+        self.sub_strip = np.stack([sub % S3[0], (sub // S3[0]) % S3[1],
+                                   sub // (S3[0] * S3[1])], axis=1)
+        self.box_o = np.stack([self.so[a][self.sub_strip[:, a]]
+                               for a in range(3)], axis=1)
+        self.box_L = np.stack([self.sw[a][self.sub_strip[:, a]]
+                               for a in range(3)], axis=1)
+        cz, cy, cx = np.meshgrid(np.arange(n3[2]), np.arange(n3[1]),
+                                 np.arange(n3[0]), indexing="ij")
+        cx, cy, cz = cx.ravel(), cy.ravel(), cz.ravel()
+        self.part = (strip_of[0][cx] + S3[0] * (strip_of[1][cy]
+                     + S3[1] * strip_of[2][cz])).astype(np.int64)
+        self._build_interface()
+
+    # ------------------------------------------------------------ topology
+
+    def _build_interface(self):
+        g = self.grid
+        n3, S3 = self.n3, self.S3
+        fam_off = list(g.flux_offsets) + [g.flux_offsets[-1]] * (4 - len(g.flux_offsets))
+        self.fam_off = fam_off
+        subs, dofs, codes, face_key = [], [], [], []
+        face_rows = []
+        for a in range(g.dim):
+            t1 = 1 if a == 0 else 0
+            t2 = 1 if a == 2 else 2
+            c2, c1 = np.meshgrid(np.arange(n3[t2]), np.arange(n3[t1]), indexing="ij")
+            c1, c2 = c1.ravel(), c2.ravel()
+            s1, s2 = self.strip_of[t1][c1], self.strip_of[t2][c2]
+            l1 = c1 - self.so[t1][s1]
+            l2 = c2 - self.so[t2][s2]
+            line = l1 + self.sw[t1][s1] * l2
+            for s in range(1, S3[a]):
+                fa = int(self.so[a][s])
+                coords = np.zeros((len(c1), 3), dtype=np.int64)
+                coords[:, a] = fa
+                coords[:, t1] = c1
+                coords[:, t2] = c2
+                ext = [n3[d] - (1 if d == a else 0) for d in range(3)]
+                idx = (coords[:, 0] - (a == 0)) + ext[0] * (
+                    (coords[:, 1] - (a == 1)) + ext[1] * (coords[:, 2] - (a == 2)))
+                dof = fam_off[a] + idx
+                sst = [None, None, None]
+                sst[t1] = s1
+                sst[t2] = s2
+                sst[a] = np.full(len(c1), s - 1)
+                lo = sst[0] + S3[0] * (sst[1] + S3[1] * sst[2])
+                sst[a] = np.full(len(c1), s)
+                hi = sst[0] + S3[0] * (sst[1] + S3[1] * sst[2])
+                subs += [lo, hi]
+                dofs += [dof, dof]
+                codes += [a | (1 << 2) | (line << 3), a | (0 << 2) | (line << 3)]
+                # faces: one per (lo, hi) pair
+                key = lo * (self.n_subdomains + 1) + hi
+                face_key.append(key)
+                uk, first, cnt = np.unique(key, return_index=True, return_counts=True)
+                for fi, m in zip(first, cnt):
+                    face_rows.append((int(lo[fi]), int(hi[fi]), a, int(m)))
+        if subs:
+            subs = np.concatenate(subs)
+            dofs = np.concatenate(dofs)
+            codes = np.concatenate(codes)
+        else:
+            subs = dofs = codes = np.zeros(0, dtype=np.int64)
+        self.gamma = np.unique(dofs)
+        n_gamma = len(self.gamma)
+        o = np.lexsort((dofs, subs))
+        subs, dofs, codes = subs[o], dofs[o], codes[o]
+        N = self.n_subdomains
+        counts = np.bincount(subs, minlength=N)
+        starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+        slot = np.arange(len(subs)) - starts[subs]
+        self.nG = counts.astype(np.int32)
+        maxG = _pad(int(counts.max()) if len(counts) else 1, 64)
+        self.maxG = maxG
+        gpos = np.searchsorted(self.gamma, dofs)
+        self.gpos = np.full((N, maxG), -1, dtype=np.int32)
+        self.gcode = np.full((N, maxG), -1, dtype=np.int32)
+        self.gpos[subs, slot] = gpos
+        self.gcode[subs, slot] = codes
+        self._slot_sub, self._slot_q, self._slot_dof = subs, slot, dofs
+        # fslot
+        maxF = 1
+        for a in range(g.dim):
+            t1 = 1 if a == 0 else 0
+            t2 = 1 if a == 2 else 2
+            maxF = max(maxF, int(self.sw[t1].max() * self.sw[t2].max()))
+        self.maxF = maxF
+        self.fslot = np.full((N, 6, maxF), -1, dtype=np.int32)
+        a_ = codes & 3
+        side_ = (codes >> 2) & 1
+        line_ = codes >> 3
+        self.fslot[subs, 2 * a_ + side_, line_] = slot
+        # gown: low copy = the slot on the high side of the lower subdomain
+        own = np.zeros((n_gamma, 2), dtype=np.int32)
+        broken = subs * maxG + slot
+        own[gpos[side_ == 1], 0] = broken[side_ == 1]
+        own[gpos[side_ == 0], 1] = broken[side_ == 0]
+        self.gown = own
+        # faces sorted by (i, j)
+        fr = sorted(face_rows)
+        self.face_table = np.array(fr, dtype=np.int32).reshape(-1, 4)
+        self.n_faces = len(fr)
+        fidx = {(r[0], r[1]): k for k, r in enumerate(fr)}
+        lo_sub = subs[side_ == 1]
+        # the face of each gamma dof (via its low copy)
+        gface = np.zeros(n_gamma, dtype=np.int32)
+        hi_sub = np.zeros(n_gamma, dtype=np.int64)
+        hi_sub[gpos[side_ == 0]] = subs[side_ == 0]
+        lo_s = np.zeros(n_gamma, dtype=np.int64)
+        lo_s[gpos[side_ == 1]] = lo_sub
+        if self.n_faces:
+            keys = lo_s * (N + 1) + hi_sub
+            ftab_keys = self.face_table[:, 0].astype(np.int64) * (N + 1) + self.face_table[:, 1]
+            gface = np.searchsorted(ftab_keys, keys).astype(np.int32)
+        self.gface = gface
+        self.dof_sub_low = lo_s
+        self.dof_sub_high = hi_sub
+        self._fidx = fidx
+        P = np.prod([int(w.max()) for w in self.sw])
+        self.maxP = _pad(int(P), 64)
+        self.maxL = int(max(int(w.max()) for w in self.sw))
+
+    # -------------------------------------------------- Laplacian eigendata
+
+    def laplacian_eigs(self, weighted):
+        """Eigen data of K_a = D_a^-1/2 Lpath_a D_a^-1/2 (weighted) or Lpath_a."""
+        Qs, lams = [], []
+        for a in range(3):
+            s = self.S3[a]
+            L = np.zeros((s, s))
+            for k in range(s - 1):
+                L[k, k] += 1
+                L[k + 1, k + 1] += 1
+                L[k, k + 1] -= 1
+                L[k + 1, k] -= 1
+            if weighted:
+                dm = 1.0 / np.sqrt(self.sw[a].astype(np.float64))
+                L = dm[:, None] * L * dm[None, :]
+            lam, Q = np.linalg.eigh(L)
+            lam[0] = 0.0
+            Qs.append(Q.ravel())
+            lams.append(lam)
+        eig = np.concatenate(Qs + lams)
+        dm = None
+        if weighted:
+            ncell = (self.sw[0][self.sub_strip[:, 0]] * self.sw[1][self.sub_strip[:, 1]]
+                     * self.sw[2][self.sub_strip[:, 2]]).astype(np.float64)
+            dm = 1.0 / np.sqrt(ncell)
+        return eig, dm
+
+    # ------------------------------------------------ reference-compatible
+
+    @property
+    def n_gamma(self):
+        return len(self.gamma)
+
+    @cached_property
+    def cells(self):
+        o = np.argsort(self.part, kind="stable")
+        b = np.searchsorted(self.part[o], np.arange(self.n_subdomains + 1))
+        return [o[b[i]:b[i + 1]] for i in range(self.n_subdomains)]
+
+    @cached_property
+    def gamma_dofs(self):
+        return [self.gamma[self.gpos[i, :self.nG[i]]]
+                for i in range(self.n_subdomains)]
+
+    @cached_property
+    def faces(self):
+        out = {}
+        for f, (i, j, a, m) in enumerate(self.face_table):
+            d = self.gamma[self.gface == f]
+            out[(int(i), int(j))] = [FaceComponent(int(i), int(j), d,
+                                                   np.ones(len(d)))]
+        return out
+
+    def adjacent_pairs(self):
+        return [(int(i), int(j)) for i, j, _, _ in self.face_table]
+
+    @property
+    def max_faces_per_subdomain(self):
+        if not self.n_faces:
+            return 0
+        c = np.bincount(np.concatenate([self.face_table[:, 0],
+                                        self.face_table[:, 1]]),
+                        minlength=self.n_subdomains)
+        return int(c.max())
+
+    def sign_for(self, i, dofs):
+        """+1 where the +axis points out of subdomain i (decomposition.py:102-108)."""
+        pos = np.searchsorted(self.gamma, dofs)
+        return np.where(self.dof_sub_low[pos] == i, 1.0, -1.0)
+
+    def gamma_index(self, i, dofs):
+        pos = np.searchsorted(self.gamma_dofs[i], dofs)
+        if not np.array_equal(self.gamma_dofs[i][pos], dofs):
+            raise InvalidArgumentError("dofs not on this subdomain interface")
+        return pos
+
+    @cached_property
+    def cell_sub(self):
+        return self.part.astype(np.int32)
+
+    def geom_fields(self):
+        """Values for the C `bddc_geom` struct."""
+        g = self.grid
+        h3 = tuple(g.sizes) + (1.0,) * (3 - g.dim)
+        return dict(dim=g.dim, n=self.n3, h=h3, vol=g.cell_volume, S=self.S3,
+                    so=self.so, sw=self.sw, fam_off=self.fam_off,
+                    n_cells=g.n_cells, n_flux=g.n_flux_dofs,
+                    N=self.n_subdomains, n_gamma=self.n_gamma,
+                    n_faces=self.n_faces, maxG=self.maxG, maxP=self.maxP,
+                    maxL=self.maxL, maxF=self.maxF)
+
+
+def regular_partition(grid, splits):
+    """Tensor-product partition with near-equal strips (decomposition.py:133-151)."""
+    return Decomposition(grid, splits)

@@ -1,0 +1,154 @@
+"""Seeded synthetic permeability fields for the BASELINE configurations.
+
+SPE10 Model 2 is not available in this environment, so the benchmark and
+parity configs use seeded stand-ins with the value distributions that
+`BASELINE.json` lists (C0..C4).  These generators are *input* preparation
+(host NumPy, run once, identical bits for the oracle and the GPU path);
+they are not part of the solve path.
+
+Cell ids are x-fastest, matching the reference grid numbering
+(`/root/reference/pkg/src/bddcflow/grid.py:56-65`).  Every function returns
+`k` with shape (n_cells, dim), one value per axis.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+__all__ = [
+    "gaussian_field", "config_field", "CONFIGS", "channel_log10k",
+]
+
+
+def _embed_cov(shape, corr, kind="exponential"):
+    """Circulant-embedding spectrum of a stationary covariance on a grid.
+
+    `corr` is the correlation length per axis in cells.  The covariance is
+    exp(-r) with the anisotropic distance r = |(dx/lx, dy/ly, ...)|.
+    """
+    ext = [2 * n for n in shape]
+    grids = []
+    for a, (n2, l) in enumerate(zip(ext, corr)):
+        d = np.arange(n2, dtype=np.float64)
+        d = np.minimum(d, n2 - d) / float(l)
+        s = [1] * len(ext)
+        s[a] = n2
+        grids.append(d.reshape(s))
+    r2 = sum(g * g for g in grids)
+    if kind == "exponential":
+        c = np.exp(-np.sqrt(r2))
+    else:  # gaussian (squared-exponential), used for "smooth" fields
+        c = np.exp(-r2)
+    lam = np.fft.fftn(c).real
+    return np.maximum(lam, 0.0)
+
+
+def gaussian_field(shape_xyz, corr_xyz, std, mean=0.0, seed=0,
+                   kind="exponential"):
+    """Stationary Gaussian random field via FFT circulant embedding.
+
+    `shape_xyz` and `corr_xyz` are given in (x, y[, z]) order; the result is
+    flattened x-fastest (cell id order of the reference grid).
+    """
+    rng = np.random.default_rng(seed)
+    # work in C order (z, y, x) so that ravel() is x-fastest
+    shape = tuple(reversed(shape_xyz))
+    corr = tuple(reversed(corr_xyz))
+    lam = _embed_cov(shape, corr, kind)
+    ext = lam.shape
+    xi = rng.standard_normal(ext) + 1j * rng.standard_normal(ext)
+    field = np.fft.ifftn(np.sqrt(lam) * xi) * math.sqrt(np.prod(ext))
+    g = field.real[tuple(slice(0, n) for n in shape)]
+    g = (g - g.mean()) / max(g.std(), 1e-300)
+    return (mean + std * g).ravel()
+
+
+def channel_log10k(nx, ny, rng, n_channels=6, phase_shift=None,
+                   params=None):
+    """One 2D channelised layer (BASELINE config 2), log10 k, x-fastest.
+
+    Background log10 k ~ N(-1, 0.5) iid; channels along y with centre
+    x = a + b sin(2 pi y / lam + phi), a ~ U(0, nx), b ~ U[3, 10],
+    lam ~ U[40, 120], width ~ U[3, 6]; log10 k ~ N(3, 0.3) inside.
+    `params` (from a previous layer) and `phase_shift` allow slowly
+    drifting channels between the layers of the 3D config.
+    """
+    if params is None:
+        params = [dict(a=rng.uniform(0, nx), b=rng.uniform(3, 10),
+                       lam=rng.uniform(40, 120),
+                       phi=rng.uniform(0, 2 * math.pi),
+                       width=rng.uniform(3, 6))
+                  for _ in range(n_channels)]
+    shift = 0.0 if phase_shift is None else phase_shift
+    logk = rng.normal(-1.0, 0.5, size=(ny, nx))
+    x = np.arange(nx) + 0.5
+    for ch in params:
+        for y in range(ny):
+            c = ch["a"] + ch["b"] * math.sin(
+                2 * math.pi * (y + 0.5) / ch["lam"] + ch["phi"] + shift)
+            inside = np.abs(x - c) <= 0.5 * ch["width"]
+            n_in = int(inside.sum())
+            if n_in:
+                logk[y, inside] = rng.normal(3.0, 0.3, size=n_in)
+    return logk.ravel(), params
+
+
+def _iso(vals, dim):
+    return np.repeat(np.asarray(vals, dtype=np.float64)[:, None], dim, axis=1)
+
+
+def config_field(cfg, seed=None):
+    """Permeability (n_cells, dim) for BASELINE config `cfg` in 0..4."""
+    spec = CONFIGS[cfg]
+    seed = spec["seed"] if seed is None else seed
+    counts = spec["counts"]
+    if cfg == 0:
+        # k = exp(G), exponential covariance, corr 0.1 = 4 cells, std 2 (ln k)
+        g = gaussian_field(counts, (4.0, 4.0), 2.0, seed=seed)
+        return _iso(np.exp(g), 2)
+    if cfg == 1:
+        g = gaussian_field(counts, (4.0, 12.0), 1.5, seed=seed)
+        return _iso(10.0 ** np.clip(g, -3.0, 3.0), 2)
+    if cfg == 2:
+        rng = np.random.default_rng(seed)
+        logk, _ = channel_log10k(counts[0], counts[1], rng)
+        return _iso(10.0 ** logk, 2)
+    # 3D configs 3 and 4 share one field
+    nx, ny, nz = counts
+    rng = np.random.default_rng(seed)
+    top = 35
+    smooth = gaussian_field((nx, ny, top), (6.0, 20.0, 3.0), 1.0, seed=seed)
+    logk = np.empty(nx * ny * nz)
+    logk[:nx * ny * top] = smooth
+    params = None
+    for z in range(top, nz):
+        layer, params = channel_log10k(
+            nx, ny, rng, params=params, phase_shift=0.05 * (z - top))
+        logk[z * nx * ny:(z + 1) * nx * ny] = layer
+    kh = 10.0 ** logk
+    k = np.empty((nx * ny * nz, 3))
+    k[:, 0] = kh
+    k[:, 1] = kh
+    k[:, 2] = 0.1 * kh
+    return k
+
+
+CONFIGS = {
+    0: dict(dim=2, counts=(40, 40), sizes=(1 / 40, 1 / 40), splits=(4, 4),
+            scaling="stiffness", constraints="initial", tau=math.inf,
+            tol=1e-8, seed=0),
+    1: dict(dim=2, counts=(60, 220), sizes=(20.0, 10.0), splits=(6, 22),
+            scaling="stiffness", constraints="adaptive", tau=10.0,
+            tol=1e-8, seed=1),
+    2: dict(dim=2, counts=(60, 220), sizes=(20.0, 10.0), splits=(6, 22),
+            scaling="stiffness", constraints="adaptive", tau=10.0,
+            tol=1e-8, seed=2),
+    3: dict(dim=3, counts=(60, 220, 85), sizes=(20.0, 10.0, 2.0),
+            splits=(6, 22, 17), scaling="stiffness",
+            constraints="adaptive", tau=10.0, tol=1e-8, seed=3),
+    4: dict(dim=3, counts=(60, 220, 85), sizes=(20.0, 10.0, 2.0),
+            splits=(12, 44, 17), scaling="stiffness",
+            constraints="adaptive", tau=10.0, tol=1e-8, seed=3),
+}

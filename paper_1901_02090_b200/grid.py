@@ -1,0 +1,224 @@
+"""Grid, permeability, wells and the saddle system (host-side descriptors).
+
+Mirrors the reference's public types (`/root/reference/pkg/src/bddcflow/
+grid.py:21-357`): dof numbering is identical (interior faces only, x-faces
+then y-faces then z-faces, each family x-fastest).  No matrices are
+assembled on the solve path: the device kernels apply the RT0 operators
+matrix-free (csrc/stencil.cu, csrc/local.cu).  `SaddleSystem.A/.B` exist
+only for API compatibility (users and tests may multiply with them) and are
+built lazily on the host when first touched.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+
+from .errors import CompatibilityError, InvalidArgumentError
+
+
+@dataclass(frozen=True)
+class Grid:
+    """Tensor-product grid (grid.py:21-160)."""
+
+    dim: int
+    counts: tuple
+    sizes: tuple
+
+    @property
+    def n_cells(self):
+        return int(np.prod(self.counts))
+
+    @property
+    def cell_volume(self):
+        return float(np.prod(self.sizes))
+
+    @cached_property
+    def flux_offsets(self):
+        """Offsets of the interior-face families in the flux dof numbering."""
+        offs = [0]
+        for a in range(self.dim):
+            e = list(self.counts)
+            e[a] -= 1
+            offs.append(offs[-1] + int(np.prod(e)))
+        return tuple(offs)
+
+    @property
+    def n_flux_dofs(self):
+        return self.flux_offsets[-1]
+
+    @property
+    def total_dofs(self):
+        """All face dofs (including boundary) plus cell pressures (grid.py:51-54)."""
+        n = 0
+        for a in range(self.dim):
+            e = list(self.counts)
+            e[a] += 1
+            n += int(np.prod(e))
+        return n + self.n_cells
+
+    @cached_property
+    def cell_coords(self):
+        idx = np.arange(self.n_cells)
+        out = np.empty((self.n_cells, self.dim), dtype=np.int64)
+        for a in range(self.dim):
+            out[:, a] = idx % self.counts[a]
+            idx = idx // self.counts[a]
+        return out
+
+    def interior_face_dof(self, a, coords):
+        """Dof of the a-face at face coordinate `coords` (f_a in 1..n_a-1), -1 otherwise."""
+        coords = np.asarray(coords)
+        ca = coords[:, a]
+        ok = (ca >= 1) & (ca <= self.counts[a] - 1)
+        idx = np.zeros(len(coords), dtype=np.int64)
+        stride = 1
+        for d in range(self.dim):
+            ext = self.counts[d] - (1 if d == a else 0)
+            idx += (coords[:, d] - (1 if d == a else 0)) * stride
+            stride *= ext
+        return np.where(ok, self.flux_offsets[a] + idx, -1)
+
+    def cell_faces(self, a):
+        """(low, high) interior dofs of every cell's a-faces, -1 on the boundary."""
+        lo = self.interior_face_dof(a, self.cell_coords)
+        hi_c = self.cell_coords.copy()
+        hi_c[:, a] += 1
+        return lo, self.interior_face_dof(a, hi_c)
+
+
+def build_grid(dim, counts, sizes):
+    """Validate and construct a Grid (grid.py:163-175)."""
+    counts = tuple(int(c) for c in counts)
+    sizes = tuple(float(s) for s in sizes)
+    if dim not in (2, 3):
+        raise InvalidArgumentError(f"dim must be 2 or 3, got {dim}")
+    if len(counts) != dim or len(sizes) != dim:
+        raise InvalidArgumentError("counts/sizes length must equal dim")
+    if any(c < 1 for c in counts):
+        raise InvalidArgumentError(f"cell counts must be >= 1, got {counts}")
+    if any(not np.isfinite(s) or s <= 0 for s in sizes):
+        raise InvalidArgumentError(f"cell sizes must be > 0, got {sizes}")
+    return Grid(dim, counts, sizes)
+
+
+@dataclass(frozen=True)
+class Permeability:
+    """Per-cell permeability, one value per axis (grid.py:178-194)."""
+
+    k: np.ndarray
+
+    def __post_init__(self):
+        k = np.asarray(self.k, dtype=np.float64)
+        if not np.all(np.isfinite(k)) or np.any(k <= 0):
+            raise InvalidArgumentError("permeability must be positive finite")
+        object.__setattr__(self, "k", k)
+
+    @classmethod
+    def isotropic(cls, grid, values):
+        values = np.broadcast_to(np.asarray(values, dtype=np.float64),
+                                 (grid.n_cells,))
+        return cls(np.repeat(values[:, None], grid.dim, axis=1))
+
+
+@dataclass(frozen=True)
+class Wells:
+    src_cell: int
+    sink_cell: int
+    strength: float = 1.0
+
+
+class SaddleSystem:
+    """Mixed system [[A, B^T],[B, 0]](u, p) = (0, f) (grid.py:230-267).
+
+    Holds the host inputs (permeability, source vector f).  `D` is the
+    per-cell pressure rescaling filled in by the setup (grid.py:344-357).
+    """
+
+    def __init__(self, grid, perm, f, wells=None, D=None, lumped=False):
+        self.grid = grid
+        self.perm = perm
+        self.f = np.asarray(f, dtype=np.float64)
+        self.wells = wells
+        self.D = D
+        self.lumped = lumped
+
+    @property
+    def n_flux(self):
+        return self.grid.n_flux_dofs
+
+    @property
+    def n_pressure(self):
+        return self.grid.n_cells
+
+    @property
+    def fs(self):
+        return self.f if self.D is None else self.D * self.f
+
+    def unscale_pressure(self, p_bar):
+        return p_bar if self.D is None else self.D * p_bar
+
+    def with_rescaling(self, D):
+        return SaddleSystem(self.grid, self.perm, self.f, self.wells, D=D,
+                            lumped=self.lumped)
+
+    # -- host matrices for API compatibility only (not used by solve) ------
+
+    @cached_property
+    def A(self):
+        import scipy.sparse as sp
+        g, k = self.grid, self.perm.k
+        rows, cols, vals = [], [], []
+        for a in range(g.dim):
+            lo, hi = g.cell_faces(a)
+            c = g.sizes[a] ** 2 / (6.0 * g.cell_volume) / k[:, a]
+            for d, o in ((lo, hi), (hi, lo)):
+                m = d >= 0
+                rows += [d[m]]
+                cols += [d[m]]
+                vals += [2.0 * c[m]]
+                mo = m & (o >= 0)
+                rows += [d[mo]]
+                cols += [o[mo]]
+                vals += [c[mo]]
+        n = g.n_flux_dofs
+        return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
+                                                     np.concatenate(cols))),
+                             shape=(n, n)).tocsr()
+
+    @cached_property
+    def B(self):
+        import scipy.sparse as sp
+        g = self.grid
+        rows, cols, vals = [], [], []
+        cells = np.arange(g.n_cells)
+        for a in range(g.dim):
+            lo, hi = g.cell_faces(a)
+            for d, s in ((lo, 1.0), (hi, -1.0)):
+                m = d >= 0
+                rows += [cells[m]]
+                cols += [d[m]]
+                vals += [np.full(int(m.sum()), s)]
+        return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
+                                                     np.concatenate(cols))),
+                             shape=(g.n_cells, g.n_flux_dofs)).tocsr()
+
+
+def assemble_system(grid, perm, wells, lumped=False):
+    """Validate inputs and form the well source vector (grid.py:327-341)."""
+    if lumped:
+        raise InvalidArgumentError(
+            "lumped RT0 mass matrices are outside the accelerated path")
+    if perm.k.shape != (grid.n_cells, grid.dim):
+        raise InvalidArgumentError("permeability shape mismatch")
+    for c in (wells.src_cell, wells.sink_cell):
+        if not 0 <= c < grid.n_cells:
+            raise InvalidArgumentError(f"well cell {c} outside grid")
+    f = np.zeros(grid.n_cells)
+    f[wells.src_cell] -= wells.strength
+    f[wells.sink_cell] += wells.strength
+    if abs(f.sum()) > 1e-12 * max(np.abs(f).sum(), 1.0):
+        raise CompatibilityError("source terms must sum to zero")
+    return SaddleSystem(grid, perm, f, wells)

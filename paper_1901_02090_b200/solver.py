@@ -1,0 +1,705 @@
+"""BDDC setup, interface PCG and the three-step solve on one B200.
+
+Drop-in for the reference's `bddcflow.solver` path
+(`/root/reference/pkg/src/bddcflow/solver.py:29-398`): same `SolveConfig`,
+`SolveReport`, `BddcSetup`, `solve(system, dec, config, u_exact=None,
+setup=None, iterate_callback=None)` signatures, argument meaning and error
+classes.  Every numerical step runs in hand-written sm_100a kernels from
+libbddc.so (csrc/); torch only allocates device memory and provides the
+stream.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .decomposition import Decomposition
+from .errors import (ConfigurationError, InternalConsistencyError,
+                     InvalidArgumentError, NonConvergenceError,
+                     NumericalFailureError)
+
+_p = nat.ptr
+F64 = torch.float64
+I32 = torch.int32
+
+
+@dataclass
+class SolveConfig:
+    """solver.py:29-44."""
+
+    tau: float = math.inf
+    scaling: str = "multiplicity"
+    tol: float = 1e-6
+    maxit: int = 5000
+    constraints: str = "initial"   # initial | adaptive
+
+    def __post_init__(self):
+        if not 0.0 < self.tol < 1.0:
+            raise InvalidArgumentError("tol must lie in (0, 1)")
+        if not self.tau > 1.0:
+            raise InvalidArgumentError("tau must exceed 1")
+        if self.constraints not in ("initial", "adaptive", "multiscale"):
+            raise InvalidArgumentError(
+                f"unknown constraint mode {self.constraints!r}")
+        if self.constraints == "multiscale":
+            raise InvalidArgumentError(
+                "multiscale constraints are outside the accelerated path")
+        if self.scaling not in ("multiplicity", "stiffness"):
+            raise InvalidArgumentError(f"unknown scaling kind {self.scaling!r}")
+
+
+@dataclass
+class SolveReport:
+    """solver.py:47-62."""
+
+    u: np.ndarray
+    p: np.ndarray
+    it: int
+    kappa: float
+    omega_tilde: float
+    n_c: int
+    residuals: np.ndarray
+    u0: np.ndarray = None
+    u_star: np.ndarray = None
+    eps0: float = None
+    eps_star: float = None
+    conservation_defect: float = 0.0
+    pressure_warning: bool = False
+    converged: bool = True
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1901_02090_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda")
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _geom(dec):
+    f = dec.geom_fields()
+    g = nat.Geom()
+    g.dim = f["dim"]
+    for a in range(3):
+        g.n[a] = int(f["n"][a])
+        g.h[a] = float(f["h"][a])
+        g.S[a] = int(f["S"][a])
+        for s in range(len(f["so"][a])):
+            g.so[a][s] = int(f["so"][a][s])
+            g.sw[a][s] = int(f["sw"][a][s])
+    g.vol = f["vol"]
+    for a in range(4):
+        g.fam_off[a] = int(f["fam_off"][a])
+    for key in ("n_cells", "n_flux", "N", "n_gamma", "n_faces", "maxG", "maxP",
+                "maxL", "maxF"):
+        setattr(g, key, int(f[key]))
+    return g
+
+
+def _pad(n, m):
+    return max(m, ((n + m - 1) // m) * m)
+
+
+class BddcSetup:
+    """Everything reusable across solves (solver.py:65-183), resident in HBM.
+
+    Device state per subdomain i (maxP / maxG / maxC padded):
+      Q[i]    = P_i^+  pressure-Schur pseudo-inverse   (interior solves)
+      S[i]    = interface Schur complement              (operator)
+      T[i]    = Gamma block of the constrained inverse  (preconditioner)
+      Psi[i]  = Gamma rows of the coarse basis          (restriction/prolongation)
+    and the explicit coarse operators Mc (flux block of the pinned coarse
+    inverse) and Wq (pressure-rhs -> coarse flux, solve step 1).
+    """
+
+    def __init__(self, system, dec, config, timings=None):
+        if not isinstance(dec, Decomposition):
+            raise InvalidArgumentError("dec must come from regular_partition()")
+        dev = _dev()
+        nat.load()
+        self.system = system
+        self.dec = dec
+        self.config = config
+        self.dev = dev
+        self.geom = _geom(dec)
+        G = self.geom
+        gp = C.byref(G)
+        st = _stream()
+        self._timings = timings
+        ev = self._events()
+        N, mg, mp = dec.n_subdomains, dec.maxG, dec.maxP
+        self.N, self.maxG, self.maxP = N, mg, mp
+        t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        # topology tables
+        self.d_gpos = t(dec.gpos)
+        self.d_gcode = t(dec.gcode)
+        self.d_nG = t(dec.nG)
+        self.d_fslot = t(dec.fslot)
+        self.d_gown = t(dec.gown)
+        self.d_gamma = t(dec.gamma)
+        self.d_faces = t(dec.face_table if dec.n_faces else np.zeros((1, 4)))
+        self.d_gface = t(dec.gface)
+        self.d_cell_sub = t(dec.cell_sub)
+        eig_w, dm_w = dec.laplacian_eigs(True)
+        eig_u, _ = dec.laplacian_eigs(False)
+        self.d_eig_w = t(eig_w, F64)
+        self.d_dm_w = t(dm_w, F64)
+        self.d_eig_u = t(eig_u, F64)
+        # permeability -> cell coefficients, D, delta
+        k = np.ascontiguousarray(system.perm.k, dtype=np.float64)
+        self.d_k = torch.as_tensor(k, device=dev)
+        self.d_coef = torch.empty(G.n_cells * 3, dtype=F64, device=dev)
+        nat.call("bddc_cell_coeffs", gp, _p(self.d_k), _p(self.d_coef), st)
+        self.d_Dsub = torch.empty(N, dtype=F64, device=dev)
+        nat.call("bddc_rescale", gp, _p(self.d_coef), _p(self.d_Dsub), st)
+        self.d_delta = torch.empty(N * mg, dtype=F64, device=dev)
+        nat.call("bddc_weights", gp, int(config.scaling == "stiffness"),
+                 _p(self.d_coef), _p(self.d_gcode), _p(self.d_delta), st)
+        self._mark(ev, "prep")
+        # local interior elimination: P, G, S_A -> Q = P^+ -> S
+        self.d_Q = torch.empty(N * mp * mp, dtype=F64, device=dev)
+        Gc = torch.empty(N * mg * dec.maxL, dtype=F64, device=dev)
+        SAd = torch.empty(N * mg, dtype=F64, device=dev)
+        SApart = torch.empty(N * mg, dtype=I32, device=dev)
+        SAoff = torch.empty(N * mg, dtype=F64, device=dev)
+        alpha = torch.empty(N, dtype=F64, device=dev)
+        nat.call("bddc_local_build", gp, _p(self.d_coef), _p(self.d_fslot),
+                 _p(self.d_Q), _p(Gc), _p(SAd), _p(SApart), _p(SAoff),
+                 _p(alpha), st)
+        info = torch.zeros(4, dtype=I32, device=dev)
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, 64) // 8 + 2,
+                         dtype=F64, device=dev)
+        nat.call("bddc_spd_inverse_batched", _p(self.d_Q), mp, mp, mp * mp, N,
+                 64, _p(ws), _p(info), st)
+        del ws
+        nat.call("bddc_local_pinv_fix", gp, _p(self.d_Q), _p(alpha), st)
+        Wt = torch.empty(N * mg * mp, dtype=F64, device=dev)
+        self.d_S = torch.empty(N * mg * mg, dtype=F64, device=dev)
+        nat.call("bddc_local_schur", gp, _p(self.d_gcode), _p(self.d_Q), _p(Gc),
+                 _p(SAd), _p(SApart), _p(SAoff), _p(Wt), _p(self.d_S), st)
+        del Wt, Gc, SAd, SApart, SAoff
+        Sinv = self.d_S.clone()
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, 64) // 8 + 2,
+                         dtype=F64, device=dev)
+        nat.call("bddc_spd_inverse_batched", _p(Sinv), mg, mg, mg * mg, N, 64,
+                 _p(ws), _p(info[1:]), st)
+        del ws
+        self._mark(ev, "local")
+        # adaptive pair eigenproblems (adaptive.py:176-195)
+        nf = dec.n_faces
+        self.pair_reports = {}
+        self.omega_tilde = None
+        maxsel = 1
+        nadd = np.zeros(nf, dtype=np.int64)
+        rows = torch.zeros(1, dtype=F64, device=dev)
+        self.pair_lambda = None
+        if config.constraints == "adaptive" and nf:
+            maxsel = min(dec.maxF, 64)
+            lam_ld = dec.maxF
+            lam = torch.empty(nf * lam_ld, dtype=F64, device=dev)
+            d_nsel = torch.empty(nf, dtype=I32, device=dev)
+            d_nadd = torch.empty(nf, dtype=I32, device=dev)
+            rows = torch.zeros(nf * maxsel * 112, dtype=F64, device=dev)
+            omega = torch.empty(nf, dtype=F64, device=dev)
+            scratch = torch.empty(nat.load().bddc_pair_scratch_bytes(nf) // 8,
+                                  dtype=F64, device=dev)
+            err = torch.zeros(1, dtype=I32, device=dev)
+            tau = config.tau if math.isfinite(config.tau) else 1e308
+            nat.call("bddc_pair_eigs", gp, _p(self.d_faces), _p(self.d_fslot),
+                     _p(self.d_S), _p(Sinv), _p(self.d_delta), float(tau),
+                     maxsel, _p(lam), lam_ld, _p(d_nsel), _p(d_nadd), _p(rows),
+                     _p(omega), _p(scratch), _p(err), st)
+            del scratch
+            e = int(err.item())
+            if e & 1:
+                raise NumericalFailureError("pair eigensolver: M not positive definite")
+            if e & 2:
+                raise InternalConsistencyError(
+                    f"more than {maxsel} eigenvalues above tau on one face")
+            nadd = d_nadd.cpu().numpy().astype(np.int64)
+            self.pair_selected = d_nsel.cpu().numpy()
+            self.pair_added = nadd
+            self.pair_lambda = lam.view(nf, lam_ld)
+            self.face_omega = omega.cpu().numpy()
+            self.omega_tilde = float(max(self.face_omega.max(), 1.0)) if nf else 1.0
+        elif config.constraints == "adaptive":
+            self.omega_tilde = 1.0
+        self._mark(ev, "pairs")
+        # coarse dof numbering: per face [initial, adaptive...]
+        per_face = 1 + nadd
+        cstart = np.concatenate([[0], np.cumsum(per_face)[:-1]]).astype(np.int64)
+        self.n_flux_coarse = int(per_face.sum()) if nf else 0
+        self._build_coarse_tables(cstart, per_face, maxsel)
+        maxC = self.maxC
+        dev_rows = t(self.sub_rows)
+        self.d_sub_rows = dev_rows
+        self.d_cown = t(self.cown if len(self.cown) else np.zeros((1, 2)))
+        self.d_nC = t(self.nC)
+        Ct = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        Y = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        self.d_Kc = torch.empty(N * maxC * maxC, dtype=F64, device=dev)
+        self.d_Psi = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        self.d_T = torch.empty(N * mg * mg, dtype=F64, device=dev)
+        self.d_b0 = torch.empty(N * maxC, dtype=F64, device=dev)
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(maxC, N, 32) // 8 + 2,
+                         dtype=F64, device=dev)
+        nat.call("bddc_coarse_local", gp, _p(dev_rows), _p(self.d_faces),
+                 _p(self.d_fslot), _p(self.d_gcode), _p(rows), maxsel, _p(Sinv),
+                 _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(self.d_Kc),
+                 _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws),
+                 _p(info[2:]), st)
+        del Ct, Y, ws, Sinv
+        self._mark(ev, "coarse_local")
+        # global coarse: S_Pi -> Mc, Wq
+        nfc = self.n_flux_coarse
+        self.nfc = nfc
+        self.npad = _pad(max(nfc, 1), 64)
+        self.npc = _pad(max(N - 1, 1), 64)
+        self.d_Mc = None
+        self.d_Wq = None
+        if nfc:
+            self.d_Mc = torch.empty(self.npad * self.npad, dtype=F64, device=dev)
+            nat.call("bddc_coarse_assemble", N, maxC, nfc, self.npad,
+                     _p(dev_rows), _p(self.d_Kc), _p(self.d_Mc), st)
+            Y0T = torch.zeros(max(N - 1, 1) * self.npad, dtype=F64, device=dev)
+            Pc = torch.empty(self.npc * self.npc, dtype=F64, device=dev)
+            self.d_Wq = torch.zeros(self.npad * self.npc, dtype=F64, device=dev)
+            wsz = max(nat.load().bddc_spd_inverse_workspace(self.npad, 1, 64),
+                      nat.load().bddc_spd_inverse_workspace(self.npc, 1, 64))
+            ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
+            info2 = torch.zeros(2, dtype=I32, device=dev)
+            nat.call("bddc_coarse_factor", N, maxC, nfc, self.npad, self.npc,
+                     _p(dev_rows), _p(self.d_b0), _p(self.d_Mc), _p(Y0T), _p(Pc),
+                     _p(self.d_Wq), _p(ws), _p(info2), _p(info2[1:]), st)
+            del ws, Y0T, Pc
+            bad = info2.cpu().numpy()
+            if bad.any():
+                raise ConfigurationError(
+                    "coarse problem singular; initial constraints do not cover all faces")
+        bad = info.cpu().numpy()
+        if bad[0] or bad[1]:
+            raise NumericalFailureError("local interior factorization failed", where=None)
+        if bad[2]:
+            raise NumericalFailureError("constrained coarse basis system singular")
+        self._mark(ev, "coarse")
+        # persistent PCG workspaces
+        ng = dec.n_gamma
+        self.n_gamma = ng
+        z = lambda n: torch.zeros(max(n, 1), dtype=F64, device=dev)
+        self.w_yb = z(N * mg)
+        self.w_yb2 = z(N * mg)
+        self.w_v = z(N * maxC)
+        self.w_crhs = z(self.npad)
+        self.w_xc = z(self.npad)
+        self.w_phi = z(N)
+        self.w_z = z(N)
+        self.w_dot = torch.zeros(nat.load().bddc_dot_workspace() // 8 + 1, dtype=F64, device=dev)
+        self.w_scal = z(16)
+        self.d_dct = torch.empty(sum(n * n + n for n in dec.n3), dtype=F64, device=dev)
+        nat.call("bddc_dct_init", gp, _p(self.d_dct), st)
+        self._mark(ev, "done")
+        self.phase_ms = self._finish(ev)
+
+    # ---------------------------------------------------------------- util
+
+    def _events(self):
+        if self._timings is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return [("start", e)]
+
+    def _mark(self, ev, name):
+        if ev is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        ev.append((name, e))
+
+    def _finish(self, ev):
+        if ev is None:
+            return None
+        ev[-1][1].synchronize()
+        out = {}
+        for (_, a), (n, b) in zip(ev[:-1], ev[1:]):
+            out[n] = a.elapsed_time(b)
+        out["total"] = ev[0][1].elapsed_time(ev[-1][1])
+        if isinstance(self._timings, dict):
+            self._timings.update(out)
+        return out
+
+    def _build_coarse_tables(self, cstart, per_face, maxsel):
+        dec, N = self.dec, self.N
+        ft = dec.face_table
+        rows_per_sub = [[] for _ in range(N)]
+        for f in range(dec.n_faces):
+            i, j = int(ft[f, 0]), int(ft[f, 1])
+            for k in range(int(per_face[f])):
+                g = int(cstart[f] + k)
+                rows_per_sub[i].append((g, f, k, 1))
+                rows_per_sub[j].append((g, f, k, -1))
+        nC = np.array([len(r) for r in rows_per_sub], dtype=np.int32)
+        maxC = _pad(int(nC.max()) if N else 1, 32)
+        sub_rows = np.full((N, maxC, 4), -1, dtype=np.int32)
+        nfc = int(per_face.sum()) if dec.n_faces else 0
+        cown = np.zeros((nfc, 2), dtype=np.int32)
+        for i, rs in enumerate(rows_per_sub):
+            rs.sort(key=lambda r: (r[1], r[2]))
+            for r, (g, f, k, s) in enumerate(rs):
+                sub_rows[i, r] = (g, f, k, s)
+                cown[g, 0 if s > 0 else 1] = i * maxC + r
+        self.sub_rows, self.cown, self.nC, self.maxC = sub_rows, cown, nC, maxC
+
+    @property
+    def n_c(self):
+        return self.n_flux_coarse + self.N
+
+    # ----------------------------------------- interface operator (device)
+
+    def _schur(self, x, y):
+        """y = S x (continuous interface vectors), solver.py:103-107."""
+        st = _stream()
+        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_S), _p(x), None, _p(self.w_yb), st)
+        nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb), _p(y), st)
+
+    def _project(self, y):
+        """In-place balanced projection, solver.py:166-179."""
+        st = _stream()
+        nat.call("bddc_phi", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_gcode), _p(y), _p(self.w_phi), st)
+        S3 = self.dec.S3
+        nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(self.d_eig_w),
+                 _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), st)
+        nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
+                 _p(self.w_z), _p(y), st)
+
+    def _precond(self, r, out):
+        """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged."""
+        st = _stream()
+        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_T), _p(r), _p(self.d_delta), _p(self.w_yb), st)
+        if self.nfc:
+            nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                     _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
+                     _p(self.d_delta), _p(self.w_v), st)
+            nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
+                     _p(self.w_crhs), st)
+            nat.call("bddc_gemv", self.nfc, self.npad, self.nfc, _p(self.d_Mc),
+                     _p(self.w_crhs), _p(self.w_xc), st)
+        nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                 _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
+                 _p(self.d_delta), _p(self.w_yb2), st)
+        nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
+
+    # public reference-compatible applies (numpy in / numpy out)
+    def schur_matvec(self, x):
+        xd = torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.dev)
+        y = torch.empty_like(xd)
+        self._schur(xd, y)
+        return y.cpu().numpy()
+
+    def precondition(self, r):
+        rd = torch.as_tensor(np.asarray(r, dtype=np.float64), device=self.dev)
+        y = torch.empty_like(rd)
+        self._precond(rd, y)
+        return y.cpu().numpy()
+
+    def project_balanced(self, x):
+        xd = torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.dev).clone()
+        self._project(xd)
+        return xd.cpu().numpy()
+
+    def schur_dense(self, i):
+        """Dense S_i (n_Gamma_i x n_Gamma_i), substructure.py:90-99."""
+        n = int(self.dec.nG[i])
+        S = self.d_S.view(self.N, self.maxG, self.maxG)[i, :n, :n]
+        return S.cpu().numpy()
+
+    def net_flux_matrix(self):
+        import scipy.sparse as sp
+        dec = self.dec
+        rows, cols, vals = [], [], []
+        for i in range(dec.n_subdomains):
+            n = dec.nG[i]
+            cols.append(dec.gpos[i, :n])
+            rows.append(np.full(n, i))
+            side = (dec.gcode[i, :n] >> 2) & 1
+            vals.append(np.where(side == 1, 1.0, -1.0))
+        return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                             shape=(dec.n_subdomains, dec.n_gamma)).tocsr()
+
+
+def _suggest_scaling(setup):
+    """solver.py:286-298 (warning only)."""
+    if setup.config.scaling != "multiplicity":
+        return
+    dec = setup.dec
+    k = setup.system.perm.k
+    if not dec.n_gamma:
+        return
+    # per-face max/min ratio between low-side and high-side cells
+    g = dec.grid
+    fc_lo = np.empty(g.n_flux_dofs, dtype=np.int64)
+    fc_hi = np.empty(g.n_flux_dofs, dtype=np.int64)
+    cells = np.arange(g.n_cells)
+    for a in range(g.dim):
+        lo, hi = g.cell_faces(a)
+        m = hi >= 0
+        fc_lo[hi[m]] = cells[m]
+        m = lo >= 0
+        fc_hi[lo[m]] = cells[m]
+    for f in range(dec.n_faces):
+        d = dec.gamma[dec.gface == f]
+        ratio = k[fc_lo[d]].max() / max(k[fc_hi[d]].min(), 1e-300)
+        if ratio > 1e3 or ratio < 1e-3:
+            warnings.warn("coefficient jumps aligned with the partition detected; "
+                          "consider --scaling stiffness")
+            return
+
+
+class _Work:
+    """Per-solve device vectors."""
+
+    def __init__(self, setup):
+        dev = setup.dev
+        G = setup.geom
+        z = lambda n: torch.zeros(max(n, 1), dtype=F64, device=dev)
+        ng = setup.n_gamma
+        self.x = z(ng)
+        self.r = z(ng)
+        self.zv = z(ng)
+        self.p = z(ng)
+        self.Ap = z(ng)
+        self.g = z(ng)
+        self.wp = z(ng)
+        self.fs = z(G.n_cells)
+        self.dd = z(G.n_cells)
+        self.u0 = z(G.n_flux)
+        self.us = z(G.n_flux)
+        self.u = z(G.n_flux)
+        self.rf = z(G.n_flux)
+        self.tmpc = z(G.n_cells)
+        self.pc = z(G.n_cells)
+        self.rq = z(setup.N)
+        self.x0 = z(setup.npad)
+
+
+def _dot(setup, x, y, n, op, hist=None, it=0):
+    nat.call("bddc_dot", _p(x), _p(y), int(n), _p(setup.w_dot), _p(setup.w_scal), op,
+             _p(hist) if hist is not None else None, it, _stream())
+
+
+def _norm(setup, x, n):
+    _dot(setup, x, x, n, 100 + 10)
+    return math.sqrt(float(setup.w_scal[10].item()))
+
+
+def solve(system, dec, config, u_exact=None, setup=None, iterate_callback=None,
+          f_device=None, return_device=False):
+    """Three-step method + pressure recovery (solver.py:301-398)."""
+    if setup is None:
+        setup = BddcSetup(system, dec, config)
+    dec = setup.dec
+    G = setup.geom
+    gp = C.byref(G)
+    st = _stream()
+    _suggest_scaling(setup)
+    W = _Work(setup)
+    N, ng = setup.N, setup.n_gamma
+    # fs = D f
+    if f_device is None:
+        fh = torch.as_tensor(np.asarray(system.f, dtype=np.float64))
+        f_device = fh.pin_memory().to(setup.dev, non_blocking=True) if fh.numel() else fh.to(setup.dev)
+    _scale_fs(setup, f_device, W.fs)
+    # step 1: rq_i = sum fs over cells of i; x0 = Wq rq[1:]; g = average(Psi x0)
+    nat.call("bddc_sub_sum", gp, _p(W.fs), _p(W.rq), 1.0, None, st)
+    if setup.nfc and N > 1:
+        nat.call("bddc_gemv", setup.nfc, setup.npc, N - 1, _p(setup.d_Wq),
+                 _p(W.rq[1:]), _p(W.x0), st)
+    if ng:
+        nat.call("bddc_prolong", N, setup.maxG, setup.maxC, _p(setup.d_nG),
+                 _p(setup.d_sub_rows), _p(setup.d_Psi), _p(W.x0), None,
+                 _p(setup.d_delta), _p(setup.w_yb2), st)
+        nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb2), _p(W.g), st)
+        nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.g), _p(W.u0), 0, st)
+        nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.g), _p(W.us), 0, st)
+    # step 2: harmonic extension (u0) and trace solve (u*)
+    a = nat.LocalSolveArgs()
+    a.x_gamma, a.x_scale = _p(W.g).value, 1.0
+    a.u_out, a.u_mode = _p(W.u0).value, 0
+    nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
+             _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+    a = nat.LocalSolveArgs()
+    a.x_gamma, a.x_scale = _p(W.g).value, 1.0
+    a.g_cell, a.g_scale = _p(W.fs).value, 1.0
+    a.u_out, a.u_mode = _p(W.us).value, 0
+    nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
+             _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+    # div_defect = fs - Bs u*
+    nat.call("bddc_cell_div", gp, _p(W.us), _p(W.fs), 1.0, -1.0, _p(setup.d_cell_sub),
+             _p(setup.d_Dsub), _p(W.dd), st)
+    nfs = _norm(setup, W.fs, G.n_cells)
+    defect_norm = _norm(setup, W.dd, G.n_cells) / max(nfs, 1e-300)
+    # step 3 rhs: r = -A u*; r_G -= sum condense
+    nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.us), -1.0, 0.0, _p(W.rf), st)
+    w_cg_it = 0
+    kappa = 1.0
+    history = np.array([1.0])
+    converged = True
+    if ng:
+        nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.r), _p(W.rf), 2, st)
+        a = nat.LocalSolveArgs()
+        a.f_flux, a.f_scale = _p(W.rf).value, 1.0
+        a.g_cell, a.g_scale = _p(W.dd).value, 1.0
+        a.rg_broken = _p(setup.w_yb).value
+        nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
+                 _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+        nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb), _p(W.Ap), st)
+        nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
+        # subdomain net-flux targets (stiffness scaling only)
+        nat.call("bddc_sub_sum", gp, _p(W.dd), _p(setup.w_phi), -1.0, _p(setup.d_Dsub), st)
+        targets = setup.w_phi.cpu().numpy()
+        fs_abs = float(np.abs(system.f).dot(setup.d_Dsub.cpu().numpy()[dec.cell_sub]))
+        if np.abs(targets).max() > 1e-13 * max(fs_abs, 1.0):
+            S3 = dec.S3
+            nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
+                     _p(setup.w_phi), _p(setup.w_z), st)
+            nat.call("bddc_face_shift", ng, dec.n_faces, _p(setup.d_gface), _p(setup.d_faces),
+                     _p(setup.w_z), _p(W.wp), st)
+            setup._schur(W.wp, W.Ap)
+            nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
+        setup._project(W.r)
+        w_cg_it, kappa, history, converged = _pcg(setup, W, config, iterate_callback)
+        # u = u* + correction, interior recovery
+        nat.call("bddc_axpby", ng, 1.0, _p(W.wp), 1.0, _p(W.x), st)
+    nat.call("bddc_axpby", G.n_flux, 1.0, _p(W.us), 0.0, _p(W.u), st)
+    if ng:
+        nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.x), _p(W.u), 1, st)
+        a = nat.LocalSolveArgs()
+        a.f_flux, a.f_scale = _p(W.rf).value, 1.0
+        a.g_cell, a.g_scale = _p(W.dd).value, 1.0
+        a.x_gamma, a.x_scale = _p(W.x).value, 1.0
+        a.u_out, a.u_mode = _p(W.u).value, 1
+        nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
+                 _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+    # pressure recovery: B B^T p = B(-A u), zero mean
+    p_warn = _recover_pressure(setup, W, config.tol)
+    omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
+    if return_device:
+        return W, w_cg_it, kappa, history, converged
+    report = SolveReport(
+        u=W.u.cpu().numpy(), p=W.pc.cpu().numpy(), it=w_cg_it, kappa=kappa,
+        omega_tilde=omega, n_c=setup.n_c, residuals=history,
+        u0=W.u0.cpu().numpy(), u_star=W.us.cpu().numpy(),
+        conservation_defect=defect_norm, pressure_warning=p_warn,
+        converged=converged)
+    if u_exact is not None:
+        nrm = np.linalg.norm(u_exact)
+        if nrm == 0:
+            raise InvalidArgumentError("exact solution is zero")
+        report.eps0 = float(np.linalg.norm(report.u0 - u_exact) / nrm)
+        report.eps_star = float(np.linalg.norm(report.u_star - u_exact) / nrm)
+    if not converged:
+        raise NonConvergenceError(
+            f"CG did not converge in {config.maxit} iterations", report=report)
+    return report
+
+
+def _scale_fs(setup, f, fs):
+    """fs = D f (grid.py:250-251)."""
+    nat.call("bddc_scale_cells", C.byref(setup.geom), _p(f), _p(setup.d_cell_sub),
+             _p(setup.d_Dsub), _p(fs), _stream())
+
+
+def _recover_pressure(setup, W, tol):
+    G = setup.geom
+    gp = C.byref(G)
+    st = _stream()
+    nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.u), 1.0, 0.0, _p(W.rf), st)
+    # rhs = B(-A u)
+    nat.call("bddc_cell_div", gp, _p(W.rf), None, 0.0, -1.0, None, None, _p(W.pc), st)
+    nat.call("bddc_neumann_solve", gp, _p(setup.d_dct), _p(W.pc), _p(W.tmpc), st)
+    ones = _ones(setup, G.n_cells)
+    _dot(setup, W.pc, ones, G.n_cells, 100 + 11)
+    nat.call("bddc_sub_mean", G.n_cells, _p(setup.w_scal[11:]), _p(W.pc), st)
+    den = _norm(setup, W.rf, G.n_flux)
+    nat.call("bddc_grad", gp, _p(W.pc), 1.0, 1.0, _p(W.rf), st)
+    num = _norm(setup, W.rf, G.n_flux)
+    return bool(den > 0 and num > 10.0 * tol * den)
+
+
+def _ones(setup, n):
+    o = getattr(setup, "_ones_c", None)
+    if o is None or o.numel() < n:
+        o = torch.ones(n, dtype=F64, device=setup.dev)
+        setup._ones_c = o
+    return o
+
+
+def _pcg(setup, W, config, callback):
+    """PCG with Lanczos kappa (solver.py:186-233), scalars kept on device."""
+    ng = setup.n_gamma
+    st = _stream()
+    tol, maxit = config.tol, config.maxit
+    scal = setup.w_scal
+    scal.zero_()
+    W.x.zero_()
+    _dot(setup, W.r, W.r, ng, 4)
+    res0 = float(scal[4].item())
+    history = [1.0]
+    if res0 == 0.0:
+        return 0, 1.0, np.array(history), True
+    alphas = torch.zeros(maxit + 1, dtype=F64, device=setup.dev)
+    betas = torch.zeros(maxit + 1, dtype=F64, device=setup.dev)
+    setup._precond(W.r, W.zv)
+    setup._project(W.zv)
+    nat.call("bddc_axpby", ng, 1.0, _p(W.zv), 0.0, _p(W.p), st)
+    _dot(setup, W.r, W.zv, ng, 0)
+    converged = False
+    it = 0
+    host = torch.empty(16, dtype=F64, pin_memory=True)
+    for it in range(1, maxit + 1):
+        setup._schur(W.p, W.Ap)
+        setup._project(W.Ap)
+        _dot(setup, W.p, W.Ap, ng, 1, alphas, it - 1)
+        nat.call("bddc_cg_update", ng, _p(scal), _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), st)
+        _dot(setup, W.r, W.r, ng, 2)
+        host.copy_(scal, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if host[8] != 0.0:
+            raise NonConvergenceError(
+                f"non-positive curvature p'Sp = {float(host[1]):.3e} at iteration {it}; "
+                "iterate left the balanced subspace")
+        rel = float(host[5])
+        history.append(rel)
+        if callback is not None:
+            callback(W.x.cpu().numpy(), W.r.cpu().numpy())
+        if rel <= tol:
+            converged = True
+            break
+        setup._precond(W.r, W.zv)
+        setup._project(W.zv)
+        _dot(setup, W.r, W.zv, ng, 3, betas, it - 1)
+        nat.call("bddc_p_update", ng, _p(scal), _p(W.zv), _p(W.p), st)
+    kappa = _lanczos(setup, alphas, betas, it)
+    return it, kappa, np.array(history), converged
+
+
+def _lanczos(setup, alphas, betas, m):
+    """solver.py:236-251 on the device (Sturm bisection for the extremes)."""
+    if m <= 1:
+        return 1.0
+    work = torch.empty(2 * m + 2, dtype=F64, device=setup.dev)
+    out = torch.empty(4, dtype=F64, device=setup.dev)
+    nat.call("bddc_lanczos", m, _p(alphas), _p(betas), _p(work), _p(out), _stream())
+    return float(out[2].item())
