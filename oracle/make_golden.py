@@ -59,13 +59,16 @@ CASES = {
            fields.CONFIGS[0]["splits"], "stiffness", math.inf, 1e-8,
            lambda: fields.config_field(0)),
     "c1": (fields.CONFIGS[1]["counts"], fields.CONFIGS[1]["sizes"],
-           fields.CONFIGS[1]["splits"], "stiffness", 10.0, 1e-8,
+           fields.CONFIGS[1]["splits"], "multiplicity", 10.0, 1e-8,
            lambda: fields.config_field(1)),
+    "c1_rho": (fields.CONFIGS[1]["counts"], fields.CONFIGS[1]["sizes"],
+               fields.CONFIGS[1]["splits"], "stiffness", 10.0, 1e-8,
+               lambda: fields.config_field(1)),
     "c2_tau10": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
-                 fields.CONFIGS[2]["splits"], "stiffness", 10.0, 1e-8,
+                 fields.CONFIGS[2]["splits"], "multiplicity", 10.0, 1e-8,
                  lambda: fields.config_field(2)),
     "c2_tau2": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
-                fields.CONFIGS[2]["splits"], "stiffness", 2.0, 1e-8,
+                fields.CONFIGS[2]["splits"], "multiplicity", 2.0, 1e-8,
                 lambda: fields.config_field(2)),
 }
 

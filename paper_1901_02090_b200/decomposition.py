@@ -244,8 +244,10 @@ class Decomposition:
     @cached_property
     def faces(self):
         out = {}
+        o = np.argsort(self.gface, kind="stable")
+        b = np.searchsorted(self.gface[o], np.arange(self.n_faces + 1))
         for f, (i, j, a, m) in enumerate(self.face_table):
-            d = self.gamma[self.gface == f]
+            d = np.sort(self.gamma[o[b[f]:b[f + 1]]])
             out[(int(i), int(j))] = [FaceComponent(int(i), int(j), d,
                                                    np.ones(len(d)))]
         return out

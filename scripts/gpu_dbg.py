@@ -2,7 +2,7 @@ import sys, time, math, numpy as np, torch
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
 import _golden as GD
 import paper_1901_02090_b200 as B
-names = sys.argv[1:] or ['g2d_small']
+names = [a for a in sys.argv[1:] if not a.startswith("--")] or ['g2d_small']
 for name in names:
     d = GD.load(name)
     g = B.build_grid(len(d['counts']), d['counts'], d['sizes'])
@@ -27,3 +27,7 @@ for name in names:
     print('  Mx', GD.rel(st.precondition(d['x']), d['Mx']))
     t=time.time(); rep = B.solve(sysm, dec, cfg, setup=st); t2=time.time()-t
     print('  it', rep.it, int(d['it']), 'kappa', rep.kappa, float(d['kappa']), 'u', GD.rel(rep.u, d['u']), 'p', GD.rel(rep.p, d['p']), 'u0', GD.rel(rep.u0, d['u0']), 'us', GD.rel(rep.u_star, d['u_star']), 'solve %.3fs'%t2, 'pw', rep.pressure_warning)
+    if '--hist' in sys.argv or True:
+        h = d['residuals']; m = rep.residuals
+        n = min(len(h), len(m))
+        print('  hist tail ref', np.array2string(h[-4:], precision=3), 'mine', np.array2string(m[-4:], precision=3))
