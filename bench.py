@@ -1,0 +1,314 @@
+"""Benchmark: adaptive-BDDC PCG solve on BASELINE config 3 (60x220x85, 6x22x17, tau=10).
+
+One "step" = one `solve()` with a prebuilt `BddcSetup` (steps 1-3, PCG to
+rtol 1e-8, interior recovery, pressure recovery), inputs resident in HBM.
+value = PCG iterations per second over the timed steps (whole job over all
+ranks).  `e2e` repeats the step through the public API with the source
+vector in pinned host memory and the report (u, p, u0, u*) copied back.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3]
+  python bench.py --impl reference ...   (reference CPU path, bounded sample)
+
+Multi-GPU: the path does not shard (north_star: one GPU, no collectives), so
+N ranks run N independent replicas; value = all ranks' iterations / max time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4)
+                          if len(r) > 2 + j and r[2 + j].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _problem(cfg_id):
+    import paper_1901_02090_b200 as B
+    from paper_1901_02090_b200 import fields
+    c = fields.CONFIGS[cfg_id]
+    k = fields.config_field(cfg_id)
+    g = B.build_grid(c["dim"], c["counts"], c["sizes"])
+    dec = B.regular_partition(g, c["splits"])
+    system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
+    cfg = B.SolveConfig(tau=c["tau"], scaling=c["scaling"],
+                        constraints="adaptive" if math.isfinite(c["tau"]) else "initial",
+                        tol=c["tol"], maxit=5000)
+    return c, k, g, dec, system, cfg
+
+
+def _workload(c, cfg_id):
+    return {"workload": f"BASELINE config {cfg_id}: RT0/P0 Darcy {'x'.join(map(str, c['counts']))} "
+                        f"cells, {'x'.join(map(str, c['splits']))} subdomains, adaptive BDDC "
+                        f"tau={c['tau']}, {c['scaling']} scaling, PCG rtol {c['tol']:g}",
+            "bc": "mode A: wells at cells 0 and n-1, no-flow elsewhere (reference-native)",
+            "field": "seeded synthetic stand-in for SPE10 (fields.py)",
+            "step": "solve() with prebuilt BddcSetup: steps 1-3 + PCG + recovery + pressure",
+            "l2": "working set (S, T, Q, Psi, coarse) >> 126 MB L2; no flush needed"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu_sample
+    c, k, g, dec, system, cfg = _problem(args.config)
+    # iteration count and coarse size of this exact workload (from the oracle-pinned
+    # GPU run recorded in profiles/, or the defaults measured in round 1)
+    meta = _load_meta(args.config)
+    vals = []
+    last = None
+    for s in range(args.warmup + args.steps):
+        r = cpu_sample.sample_solve(c["counts"], c["sizes"], k, c["splits"], it=meta["it"],
+                                    n_coarse=meta["n_c"], rows_per_sub=meta["rows_per_sub"],
+                                    n_sub_sample=2, seed=s)
+        if s >= args.warmup:
+            vals.append(r["it_per_s"])
+        last = r
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": "bddc_pcg_iterations_per_s", "value": v, "unit": "it/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * meta["it"] / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": _workload(c, args.config),
+        "cpu_baseline": {"value": v, "unit": "it/s", "cores": last["cores"], "kind": "port",
+                         "sample": "extrapolated: " + last["sample"]},
+        "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": {k2: v2 for k2, v2 in last.items() if k2 not in ("sample",)},
+    }
+    print(json.dumps(line))
+
+
+def _load_meta(cfg_id):
+    p = os.path.join(ROOT, "profiles", f"workload_c{cfg_id}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {"it": 34, "n_c": 36249, "rows_per_sub": 30.0}
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1901_02090_b200 as B
+    from paper_1901_02090_b200 import _native as nat
+    from paper_1901_02090_b200 import solver as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    lib = nat.load()
+    c, k, g, dec, system, cfg = _problem(args.config)
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # ---- setup (timed separately, device events)
+    tm = {}
+    setup = B.BddcSetup(system, dec, cfg)            # warm (JIT-free, allocator warm)
+    del setup
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    setup = B.BddcSetup(system, dec, cfg, timings=tm)
+    e1.record()
+    torch.cuda.synchronize()
+    setup_s = allmax(e0.elapsed_time(e1) / 1000.0)
+    f_dev = torch.as_tensor(system.f, dtype=torch.float64, device=dev)
+
+    # ---- device-resident steps
+    its = []
+    for _ in range(args.warmup):
+        W, it, kappa, hist, conv = S.solve(system, dec, cfg, setup=setup, f_device=f_dev,
+                                           return_device=True)
+    # kernel timer on the dominant kernel (interface Schur GEMV) during the timed region
+    kt = {"ev": []}
+    setup._ktimer = kt
+    barrier()
+    torch.cuda.synchronize()
+    l0 = lib.bddc_launch_count()
+    with Clocks(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            W, it, kappa, hist, conv = S.solve(system, dec, cfg, setup=setup, f_device=f_dev,
+                                               return_device=True)
+            its.append(it)
+        t1.record()
+        torch.cuda.synchronize()
+    launches = lib.bddc_launch_count() - l0
+    setup._ktimer = None
+    barrier()
+    step_s = t0.elapsed_time(t1) / 1000.0
+    step_s_max = allmax(step_s)
+    tot_it = allsum(float(sum(its)))
+    value = tot_it / step_s_max
+    ms_per_step = 1000.0 * step_s_max / args.steps
+    kdur = [a.elapsed_time(b) / 1000.0 for a, b in kt["ev"]]
+    kmean = float(np.mean(kdur)) if kdur else float("nan")
+
+    # ---- roofline for the dominant kernel: S-GEMV, algorithmic bytes =
+    # packed-symmetric S_i (8 n(n+1)/2 per subdomain) + x gather + y write
+    nG = dec.nG.astype(np.float64)
+    alg_bytes = float(np.sum(8.0 * nG * (nG + 1) / 2 + 8.0 * nG * 2 + 4.0 * nG))
+    peak, peak_kind = _peaks()
+    achieved = alg_bytes / kmean / 1e9 if kdur else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_gather_gemv.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API (host f in pinned memory, report to host)
+    e2e_its = []
+    h2d = g.n_cells * 8
+    d2h = (3 * g.n_flux_dofs + g.n_cells) * 8   # u, u0, u_star and p
+    barrier()
+    torch.cuda.synchronize()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(args.steps):
+        rep = B.solve(system, dec, cfg, setup=setup)
+        e2e_its.append(rep.it)
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_s = allmax(a0.elapsed_time(a1) / 1000.0)
+    e2e_val = allsum(float(sum(e2e_its))) / e2e_s
+
+    line = {
+        "metric": "bddc_pcg_iterations_per_s", "value": value, "unit": "it/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(_workload(c, args.config), parallelism=f"replicas{world}"),
+        "time_to_solve_s": ms_per_step / 1000.0, "setup_s": setup_s,
+        "setup_phases_ms": tm, "pcg_iterations": int(its[-1]), "kappa": float(kappa),
+        "n_c": int(setup.n_c), "omega_tilde": setup.omega_tilde,
+        "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "roofline": {"bound": "hbm", "kernel": "gather_gemv_kernel (interface Schur S_i x_i)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                     "launches_timed": len(kdur), "mean_launch_s": kmean},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_sample
+        r = cpu_sample.sample_solve(c["counts"], c["sizes"], k, c["splits"], it=int(its[-1]),
+                                    n_coarse=int(setup.n_c),
+                                    rows_per_sub=float(setup.nC.mean()), n_sub_sample=2)
+        line["cpu_baseline"] = {"value": r["it_per_s"], "unit": "it/s", "cores": r["cores"],
+                                "kind": "port", "sample": "extrapolated: " + r["sample"]}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

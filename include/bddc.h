@@ -205,6 +205,8 @@ int bddc_scale_cells(const bddc_geom* g, const double* f, const int* cell_sub, c
                      double* out, void* stream);
 
 size_t bddc_geom_size(void);
+/* Kernel launches issued so far (bench.py's gpu_launches). */
+unsigned long long bddc_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -126,6 +126,7 @@ _SIGS = {
     "bddc_face_shift": [_I, _I, _P, _P, _P, _P, _P],
     "bddc_scale_cells": [_GP, _P, _P, _P, _P, _P],
     "bddc_geom_size": [],
+    "bddc_launch_count": [],
     "bddc_version": [],
     "bddc_last_error": [],
 }
@@ -134,6 +135,7 @@ _RESTYPES = {
     "bddc_pair_scratch_bytes": C.c_size_t,
     "bddc_dot_workspace": C.c_size_t,
     "bddc_geom_size": C.c_size_t,
+    "bddc_launch_count": C.c_ulonglong,
     "bddc_last_error": C.c_char_p,
 }
 
@@ -173,10 +175,41 @@ def load(path=None):
     return lib
 
 
+_PROFILE = None   # list of (name, start_event, end_event) when profiling
+
+
+def profile_start():
+    """Record CUDA events around every library call (dev tool, perturbs timing slightly)."""
+    global _PROFILE
+    _PROFILE = []
+
+
+def profile_stop():
+    """Return {name: (calls, total_ms)} for the calls recorded since profile_start()."""
+    global _PROFILE
+    import torch
+    torch.cuda.synchronize()
+    out = {}
+    for name, a, b in _PROFILE or []:
+        c, t = out.get(name, (0, 0.0))
+        out[name] = (c + 1, t + a.elapsed_time(b))
+    _PROFILE = None
+    return out
+
+
 def call(name, *args):
     """Invoke a status-returning entry point; map errors to the reference classes."""
     lib = load()
-    rc = getattr(lib, name)(*args)
+    if _PROFILE is not None:
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        rc = getattr(lib, name)(*args)
+        b.record()
+        _PROFILE.append((name, a, b))
+    else:
+        rc = getattr(lib, name)(*args)
     if rc:
         msg = lib.bddc_last_error().decode(errors="replace")
         raise _ERRMAP.get(rc, RuntimeError)(f"{name}: {msg}")

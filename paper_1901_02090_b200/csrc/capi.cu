@@ -17,3 +17,9 @@ extern "C" const char* bddc_last_error(void) { return g_msg; }
 extern "C" int bddc_version(void) { return 1; }
 
 extern "C" size_t bddc_geom_size(void) { return sizeof(bddc_geom); }
+
+// Number of kernel launches issued through this library (every launch site
+// is followed by LAUNCH_OK, which counts it).  Used by bench.py.
+static unsigned long long g_launches = 0;
+extern "C" void bddc_count_launch(void) { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+extern "C" unsigned long long bddc_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }

@@ -12,8 +12,11 @@
     if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
   } while (0)
 
+extern "C" void bddc_count_launch(void);
+
 #define LAUNCH_OK()                                                   \
   do {                                                                \
+    bddc_count_launch();                                              \
     cudaError_t _e = cudaGetLastError();                              \
     if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
   } while (0)

@@ -130,6 +130,7 @@ class BddcSetup:
         self.dec = dec
         self.config = config
         self.dev = dev
+        self._ktimer = None
         self.geom = _geom(dec)
         G = self.geom
         gp = C.byref(G)
@@ -368,8 +369,16 @@ class BddcSetup:
     def _schur(self, x, y):
         """y = S x (continuous interface vectors), solver.py:103-107."""
         st = _stream()
+        kt = self._ktimer
+        if kt is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                  _p(self.d_S), _p(x), None, _p(self.w_yb), st)
+        if kt is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            kt["ev"].append((e0, e1))
         nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb), _p(y), st)
 
     def _project(self, y):

@@ -35,3 +35,16 @@ for rep in range(a.reps):
     print(f"  solve {tsol:.3f}s it={r.it} kappa={r.kappa:.4f} it/s={r.it/tsol:.1f} cons={r.conservation_defect:.2e} pw={r.pressure_warning}", flush=True)
     del st
     torch.cuda.empty_cache()
+# per-call device-time breakdown of one setup + one solve
+from paper_1901_02090_b200 import _native as nat
+nat.profile_start()
+st = B.BddcSetup(system, dec, cfg)
+prof_setup = nat.profile_stop()
+nat.profile_start()
+r = B.solve(system, dec, cfg, setup=st)
+prof_solve = nat.profile_stop()
+for title, prof in (("SETUP", prof_setup), ("SOLVE", prof_solve)):
+    tot = sum(t for _, t in prof.values())
+    print(f"{title} total {tot:.1f} ms")
+    for name, (cnt, t) in sorted(prof.items(), key=lambda kv: -kv[1][1])[:14]:
+        print(f"   {name:28s} calls={cnt:5d} total={t:9.2f} ms  mean={t/cnt:8.3f} ms")

@@ -1,0 +1,52 @@
+"""Closed-form box topology of the package vs the oracle / reference counts."""
+import numpy as np
+import pytest
+
+import paper_1901_02090_b200 as B
+from oracle import bddc_oracle as O
+
+
+@pytest.mark.parametrize("counts,splits", [
+    ((8, 8), (2, 2)), ((9, 21), (3, 3)), ((60, 220), (6, 22)), ((5, 5, 5), (3, 3, 3)),
+    ((8, 6, 4), (2, 2, 2)), ((12, 7, 9), (3, 2, 4)), ((7, 5), (1, 2)), ((4, 4), (1, 1)),
+])
+def test_topology_matches_oracle(counts, splits):
+    g = B.build_grid(len(counts), counts, (1.0,) * len(counts))
+    d = B.regular_partition(g, splits)
+    P = O.BoxPartition(O.Mesh(counts, (1.0,) * len(counts)), splits)
+    np.testing.assert_array_equal(d.part, P.part)
+    np.testing.assert_array_equal(d.gamma, P.gamma)
+    for i in range(d.n_subdomains):
+        np.testing.assert_array_equal(d.gamma_dofs[i], P.gamma_dofs[i])
+        np.testing.assert_array_equal(d.cells[i], P.cells[i])
+    assert d.adjacent_pairs() == P.pairs
+    for f, (i, j) in enumerate(P.pairs):
+        np.testing.assert_array_equal(d.faces[(i, j)][0].dofs, P.face_dofs[f])
+        np.testing.assert_array_equal(d.sign_for(i, P.face_dofs[f]), P.sign(i, P.face_dofs[f]))
+    # slot tables are mutually consistent
+    for i in range(d.n_subdomains):
+        n = d.nG[i]
+        codes = d.gcode[i, :n]
+        a, side, line = codes & 3, (codes >> 2) & 1, codes >> 3
+        np.testing.assert_array_equal(d.fslot[i, 2 * a + side, line], np.arange(n))
+    lo = d.gown[:, 0] // d.maxG
+    hi = d.gown[:, 1] // d.maxG
+    np.testing.assert_array_equal(lo, d.dof_sub_low)
+    assert np.all(lo < hi)
+
+
+def test_counts_config3():
+    g = B.build_grid(3, (60, 220, 85), (20.0, 10.0, 2.0))
+    d = B.regular_partition(g, (6, 22, 17))
+    assert d.n_subdomains == 2244
+    assert d.n_faces == 6124
+    assert d.n_gamma == 411800
+    assert int(d.nG.max()) == 400
+
+
+def test_validation():
+    g = B.build_grid(2, (4, 4), (1.0, 1.0))
+    with pytest.raises(B.InvalidArgumentError):
+        B.regular_partition(g, (5, 1))
+    with pytest.raises(B.InvalidArgumentError):
+        B.regular_partition(g, (2,))

@@ -1,0 +1,113 @@
+"""Kernel-level numerics vs torch float64 references (DMMA GEMM, SPD sweep inverse,
+matrix-free RT0 operators, DCT Neumann solve, Lanczos)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_1901_02090_b200 import _native as nat
+    nat.load()
+    return nat
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K", [(0, 0, 130, 70, 33), (1, 0, 64, 200, 17), (0, 1, 5, 9, 300),
+                                         (1, 1, 257, 129, 64), (0, 0, 7, 9, 11)])
+def test_dgemm_vs_torch(ta, tb, M, N, K):
+    import torch
+    nat = _lib()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, device="cuda", generator=g)
+    Bm = torch.randn((N, K) if tb else (K, N), dtype=torch.float64, device="cuda", generator=g)
+    Cm = torch.randn((M, N), dtype=torch.float64, device="cuda", generator=g)
+    ref = 0.5 * Cm + 2.0 * ((A.T if ta else A) @ (Bm.T if tb else Bm))
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.call("bddc_dgemm_batched", ta, tb, M, N, K, 2.0, nat.ptr(A), A.shape[1], 0, nat.ptr(Bm),
+             Bm.shape[1], 0, 0.5, nat.ptr(Cm), N, 0, 1, 0, st)
+    torch.cuda.synchronize()
+    assert torch.allclose(Cm, ref, rtol=1e-13, atol=1e-12 * math.sqrt(K))
+
+
+@pytest.mark.parametrize("n,b,batch", [(64, 32, 3), (192, 64, 5), (512, 64, 2)])
+def test_spd_inverse_vs_torch(n, b, batch):
+    import torch
+    nat = _lib()
+    g = torch.Generator(device="cuda").manual_seed(2)
+    X = torch.randn(batch, n, n, dtype=torch.float64, device="cuda", generator=g)
+    A = X @ X.transpose(1, 2) + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    M = A.clone()
+    ws = torch.empty(nat.load().bddc_spd_inverse_workspace(n, batch, b) // 8 + 2,
+                     dtype=torch.float64, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.call("bddc_spd_inverse_batched", nat.ptr(M), n, n, n * n, batch, b, nat.ptr(ws),
+             nat.ptr(info), st)
+    ref = torch.linalg.inv(A)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    assert torch.allclose(M, ref, rtol=1e-11, atol=1e-14)
+
+
+def test_rt0_operators_vs_scipy():
+    import torch
+    import paper_1901_02090_b200 as B
+    from paper_1901_02090_b200 import solver as S
+    nat = _lib()
+    rng = np.random.default_rng(0)
+    g = B.build_grid(3, (7, 5, 6), (2.0, 1.0, 0.5))
+    k = 10 ** rng.uniform(-2, 2, (g.n_cells, 3))
+    system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
+    dec = B.regular_partition(g, (2, 1, 2))
+    st = B.BddcSetup(system, dec, B.SolveConfig())
+    u = rng.standard_normal(g.n_flux_dofs)
+    ud = torch.as_tensor(u, device="cuda")
+    y = torch.empty_like(ud)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.call("bddc_flux_A", C.byref(st.geom), nat.ptr(st.d_coef), nat.ptr(ud), 1.0, 0.0, nat.ptr(y), s)
+    np.testing.assert_allclose(y.cpu().numpy(), system.A @ u, rtol=1e-13, atol=1e-13)
+    c = torch.empty(g.n_cells, dtype=torch.float64, device="cuda")
+    nat.call("bddc_cell_div", C.byref(st.geom), nat.ptr(ud), None, 0.0, 1.0, None, None, nat.ptr(c), s)
+    np.testing.assert_allclose(c.cpu().numpy(), system.B @ u, rtol=1e-13, atol=1e-13)
+    # Neumann solve: B B^T p = B g with zero mean
+    gvec = system.B @ u
+    rhs = torch.as_tensor(gvec, device="cuda").clone()
+    tmp = torch.empty_like(rhs)
+    nat.call("bddc_neumann_solve", C.byref(st.geom), nat.ptr(st.d_dct), nat.ptr(rhs), nat.ptr(tmp), s)
+    p = rhs.cpu().numpy()
+    L = (system.B @ system.B.T).toarray()
+    np.testing.assert_allclose(L @ p, gvec, atol=1e-10 * np.abs(gvec).max())
+    assert abs(p.sum()) <= 1e-10 * np.abs(p).max()
+
+
+def test_lanczos_kappa_matches_host():
+    import torch
+    import scipy.linalg as sla
+    from paper_1901_02090_b200 import solver as S
+    rng = np.random.default_rng(0)
+    n = 40
+    Q = rng.standard_normal((n, n))
+    A = Q @ Q.T + n * np.eye(n)
+    b = rng.standard_normal(n)
+    # CG alphas/betas on the host
+    x = np.zeros(n); r = b.copy(); p = r.copy(); rz = r @ r
+    al, be = [], []
+    for _ in range(25):
+        Ap = A @ p; a = rz / (p @ Ap); x += a * p; r -= a * Ap; al.append(a)
+        rzn = r @ r; be.append(rzn / rz); rz = rzn; p = r + be[-1] * p
+    m = len(al)
+    d = np.empty(m); e = np.empty(m - 1)
+    d[0] = 1 / al[0]
+    for q in range(1, m):
+        d[q] = 1 / al[q] + be[q - 1] / al[q - 1]
+        e[q - 1] = math.sqrt(be[q - 1]) / al[q - 1]
+    ev = sla.eigh_tridiagonal(d, e, eigvals_only=True)
+
+    class _S:
+        dev = torch.device("cuda")
+    k = S._lanczos(_S, torch.tensor(al + [0.0], device="cuda", dtype=torch.float64),
+                   torch.tensor(be + [0.0], device="cuda", dtype=torch.float64), m)
+    assert abs(k - ev[-1] / ev[0]) <= 1e-10 * k
