@@ -130,13 +130,27 @@ int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces,
                       const int* gcode, const double* rows, int maxsel, const double* Sinv,
                       const double* Dsub, int maxC, double* Ct, double* Y, double* Kc, double* Psi,
                       double* T, double* b0, void* inv_ws, int* info, void* stream);
-/* Deterministic S_Pi assembly (coarse.py:182-183). */
-int bddc_coarse_assemble(int N, int maxC, int nfc, int npad, const int* sub_rows, const double* Kc,
-                         double* SP, void* stream);
-/* Pinned coarse saddle (coarse.py:186-215) reduced to Mc (in place of SP) and Wq. */
-int bddc_coarse_factor(int N, int maxC, int nfc, int npad, int npc, const int* sub_rows,
-                       const double* b0, double* SP, double* Y0T, double* Pc, double* Wq, void* inv_ws,
-                       int* info_sp, int* info_pc, void* stream);
+int bddc_pad_identity(double* M, int n, int npad, void* stream);
+
+/* Nested-dissection multifrontal coarse solver (replaces the dense coarse
+ * lu_factor / lu_solve of coarse.py:186-215; see coarse_nd.py). */
+int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, const int* cmap,
+                     const int* ckind, const int* sep_idx, double* F, const double* Fc, int Sc,
+                     int nfc, const double* Kc, const int* sub_rows, const double* b0, int maxC,
+                     void* stream);
+int bddc_nd_fwd(int m, int S, int Bf, int nf, long long xstride, const int* sep_idx,
+                const int* lptr, const int* lsrc, const double* F, const double* X, const double* r,
+                double* ybuf, double* cbuf, long long coff, void* stream);
+int bddc_nd_bwd(int m, int S, int Bf, long long xstride, const int* sep_idx, const int* bnd_idx,
+                const double* X, const double* ybuf, double* x, void* stream);
+/* Pinned pressure Schur Pc = -U_root[1:,1:] (coarse.py:192-194). */
+int bddc_nd_extract_pc(const double* F, int nf, int S, int N, double* Pc, int npc, void* stream);
+/* Pressure coupling B0 (coarse.py:184-193): out = B0[1:] Y, r += alpha B0[1:]^T z. */
+int bddc_b0_apply(int N, int maxC, const int* sub_rows, const double* b0, const double* Y, int ldy,
+                  int nrhs, double* out, int ldo, void* stream);
+int bddc_b0t_apply(int nfc, int maxC, const int* cown, const double* b0, const double* z, int ldz,
+                   int nrhs, double alpha, double* r, int ldr, void* stream);
+int bddc_fill(long long n, double v, double* a, void* stream);
 
 /* ------------------------------------------------------------------- PCG */
 
@@ -165,7 +179,7 @@ int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const double* z, dou
  * vector updates, dense GEMV, Lanczos kappa (solver.py:236-251). */
 size_t bddc_dot_workspace(void);
 int bddc_dot(const double* x, const double* y, long long n, void* ws, double* scal, int op,
-             double* hist, int it, void* stream);
+             double* hist, void* stream);
 int bddc_cg_update(long long n, const double* scal, double* x, const double* p, double* r,
                    const double* Ap, void* stream);
 int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream);
@@ -173,6 +187,16 @@ int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double*
 int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out,
                  void* stream);
 int bddc_axpby(long long n, double a, const double* x, double b, double* y, void* stream);
+
+/* Device-resident PCG loop (solver.py:204-227): a CUDA graph with a
+ * conditional WHILE node whose body is one captured PCG iteration. */
+int bddc_graph_begin(void** state_out, void* stream);
+int bddc_graph_while(void* state, void* stream);
+int bddc_graph_end(void* state, void* stream);
+int bddc_graph_launch(void* state, void* stream);
+int bddc_graph_destroy(void* state);
+unsigned long long bddc_graph_handle(void* state);
+int bddc_pcg_cond(void* state, const double* scal, double tol, int maxit, void* stream);
 
 /* --------------------------------------------------------------- stencil */
 

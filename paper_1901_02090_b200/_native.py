@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libbddc.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["capi.cu", "dense.cu", "local.cu", "adaptive.cu", "coarse.cu",
-           "pcg.cu", "stencil.cu"]
+           "nd.cu", "pcg.cu", "stencil.cu", "graph.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "-diag-suppress", "550"]
@@ -97,9 +97,23 @@ _SIGS = {
                        _P, _P, _P, _P],
     "bddc_coarse_local": [_GP, _P, _P, _P, _P, _P, _I, _P, _P, _I, _P, _P, _P,
                           _P, _P, _P, _P, _P, _P],
-    "bddc_coarse_assemble": [_I, _I, _I, _I, _P, _P, _P, _P],
-    "bddc_coarse_factor": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
-                           _P, _P],
+    "bddc_pad_identity": [_P, _I, _I, _P],
+    "bddc_graph_begin": [C.POINTER(C.c_void_p), _P],
+    "bddc_graph_while": [_P, _P],
+    "bddc_graph_end": [_P, _P],
+    "bddc_graph_launch": [_P, _P],
+    "bddc_graph_destroy": [_P],
+    "bddc_graph_handle": [_P],
+    "bddc_pcg_cond": [_P, _P, _D, _I, _P],
+    "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
+                         _P, _P, _I, _P],
+    "bddc_nd_fwd": [_I, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P, _P, _P, _L, _P],
+    "bddc_nd_extract_pc": [_P, _I, _I, _I, _P, _I, _P],
+    "bddc_nd_bwd": [_I, _I, _I, _L, _P, _P, _P, _P, _P, _P],
+    "bddc_b0_apply": [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P],
+    "bddc_b0t_apply": [_I, _I, _P, _P, _P, _I, _I, _D, _P, _I, _P],
+    "bddc_fill": [_L, _D, _P, _P],
+
     "bddc_gather_gemv": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "bddc_gather_gemv_t": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_coarse_restrict": [_I, _P, _P, _P, _P],
@@ -109,7 +123,7 @@ _SIGS = {
     "bddc_lap_solve": [_I, _I, _I, _P, _P, _P, _P, _P],
     "bddc_proj_apply": [_I, _I, _P, _P, _P, _P],
     "bddc_dot_workspace": [],
-    "bddc_dot": [_P, _P, _L, _P, _P, _I, _P, _I, _P],
+    "bddc_dot": [_P, _P, _L, _P, _P, _I, _P, _P],
     "bddc_cg_update": [_L, _P, _P, _P, _P, _P, _P],
     "bddc_p_update": [_L, _P, _P, _P, _P],
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
@@ -136,6 +150,7 @@ _RESTYPES = {
     "bddc_dot_workspace": C.c_size_t,
     "bddc_geom_size": C.c_size_t,
     "bddc_launch_count": C.c_ulonglong,
+    "bddc_graph_handle": C.c_ulonglong,
     "bddc_last_error": C.c_char_p,
 }
 

@@ -1,0 +1,283 @@
+"""Sparse coarse solver: structured nested dissection over the subdomain grid.
+
+The reference factors the coarse saddle problem densely (`coarse.py:186-215`:
+`lu_factor` of [[S_Pi, B0^T],[B0, 0]] with subdomain 0's pressure pinned).
+S_Pi couples coarse dofs only through shared subdomains, so for box
+partitions a plane of subdomain faces separates the subdomain grid.  We
+eliminate the flux coarse dofs by a multifrontal block-LDL^T over that
+nested-dissection tree while carrying the subdomain pressures along as
+never-eliminated front variables: the root's update matrix is then exactly
+-B0 S_Pi^-1 B0^T, whose pinned part Pc (drop subdomain 0) is inverted
+densely.  Coarse solves (solver.py:117-118, 318-319) become
+
+    flux rhs r, pressure rhs 0 :  x = S_Pi^-1 (r - B0^T Pc^-1 B0 S_Pi^-1 r)
+    flux rhs 0, pressure rhs q :  w = S_Pi^-1 B0[1:]^T Pc^-1 q[1:]
+
+which is algebraically the pinned solve of the reference.
+
+Tree: every node is a box of subdomain strips; an internal node splits its
+box at the middle of its longest axis; its separator = the coarse dofs on
+the faces of that plane; its boundary = coarse dofs on the box's faces
+toward the rest of the domain, then the pressures of the box's subdomains.
+Leaves are single subdomains whose contribution is the local block
+[[sigma sigma^T Kc_i, b0_i^T],[b0_i, 0]] (coarse.py:179-185).  Per internal
+node (front F over [sep | bnd]):
+    F11inv = F11^-1 (blocked symmetric sweep),  X = F21 F11inv,
+    U = F22 - X F12  (extend-added into the parent's front).
+Solve (flux part only): forward y_sep = F11inv (r_sep - descendant
+contributions), c = X r_sep (leaves -> root, left-looking gathers in a
+fixed order); backward x_sep = y_sep - X^T x_bnd (root -> leaves).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import ConfigurationError
+
+_p = nat.ptr
+F64 = torch.float64
+I32 = torch.int32
+
+
+def _pad(n, m):
+    return max(m, ((n + m - 1) // m) * m)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Level:
+    pass
+
+
+class CoarseND:
+    """Symbolic analysis (host, index tables only) + numeric factorisation (device)."""
+
+    def __init__(self, dec, per_face, cstart, sub_rows, nC, maxC, dev):
+        self.dev = dev
+        S3 = dec.S3
+        ft = dec.face_table
+        nfaces = dec.n_faces
+        N = dec.n_subdomains
+        self.N = N
+        self.nfc = nfc = int(per_face.sum()) if nfaces else 0
+        fkey = {}
+        for f in range(nfaces):
+            i, a = int(ft[f, 0]), int(ft[f, 2])
+            s = dec.sub_strip[i]
+            t = [d for d in range(3) if d != a]
+            fkey[(a, int(s[a]) + 1, int(s[t[0]]), int(s[t[1]]))] = f
+
+        def face_dofs(fl):
+            if not fl:
+                return np.zeros(0, dtype=np.int64)
+            return np.concatenate([cstart[f] + np.arange(per_face[f]) for f in fl])
+
+        def plane_faces(a, plane, lo, hi):
+            t = [d for d in range(3) if d != a]
+            return [fkey[(a, plane, u, v)] for v in range(lo[t[1]], hi[t[1]])
+                    for u in range(lo[t[0]], hi[t[0]])]
+
+        def box_subs(lo, hi):
+            z, y, x = np.meshgrid(np.arange(lo[2], hi[2]), np.arange(lo[1], hi[1]),
+                                  np.arange(lo[0], hi[0]), indexing="ij")
+            return np.sort((x + S3[0] * (y + S3[1] * z)).ravel())
+
+        nodes = []
+
+        def rec(lo, hi, depth):
+            idx = len(nodes)
+            nodes.append(None)
+            ext = [hi[a] - lo[a] for a in range(3)]
+            bnd = []
+            for a in range(3):
+                for plane in (lo[a], hi[a]):
+                    if 0 < plane < S3[a]:
+                        bnd += plane_faces(a, plane, lo, hi)
+            if all(e == 1 for e in ext):
+                sub = lo[0] + S3[0] * (lo[1] + S3[1] * lo[2])
+                nodes[idx] = dict(leaf=True, sub=int(sub), depth=depth)
+                return idx
+            a = int(np.argmax(ext))
+            mid = lo[a] + ext[a] // 2
+            sep = plane_faces(a, mid, lo, hi)
+            h1 = list(hi)
+            h1[a] = mid
+            l2 = list(lo)
+            l2[a] = mid
+            c1 = rec(lo, tuple(h1), depth + 1)
+            c2 = rec(tuple(l2), hi, depth + 1)
+            bf = face_dofs(bnd)
+            pres = nfc + box_subs(lo, hi)
+            nodes[idx] = dict(leaf=False, depth=depth, sep=face_dofs(sep), bndf=bf,
+                              bnd=np.concatenate([bf, pres]), ch=(c1, c2))
+            return idx
+
+        if N > 1 and nfc:
+            rec((0, 0, 0), tuple(S3), 0)
+        self.nodes = nodes
+        internal = [k for k, n in enumerate(nodes) if not n["leaf"]]
+        depths = sorted({nodes[k]["depth"] for k in internal}, reverse=True)
+        pos_in_level = {}
+        self.levels = []
+        t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        sub_g = sub_rows[:, :, 0]
+
+        def export(cn):
+            if cn["leaf"]:
+                i = cn["sub"]
+                return np.concatenate([sub_g[i, :nC[i]], [nfc + i]])
+            return cn["bnd"]
+
+        for d in depths:
+            ids = [k for k in internal if nodes[k]["depth"] == d]
+            L = _Level()
+            L.ids, L.m = ids, len(ids)
+            for q, k in enumerate(ids):
+                pos_in_level[k] = (len(self.levels), q)
+            L.S = _pad(max(len(nodes[k]["sep"]) for k in ids), 32)
+            L.B = _pad(max(len(nodes[k]["bnd"]) for k in ids), 2)
+            L.Bf = max(len(nodes[k]["bndf"]) for k in ids)
+            L.nf = L.S + L.B
+            sep_idx = np.full((L.m, L.S), -1, dtype=np.int32)
+            bnd_idx = np.full((L.m, max(L.Bf, 1)), -1, dtype=np.int32)
+            K = 1
+            maps = []
+            for q, k in enumerate(ids):
+                n = nodes[k]
+                sep_idx[q, :len(n["sep"])] = n["sep"]
+                bnd_idx[q, :len(n["bndf"])] = n["bndf"]
+                front = np.concatenate([n["sep"], n["bnd"]])
+                order = np.argsort(front, kind="stable")
+                fs = front[order]
+                ns = len(n["sep"])
+                mm = []
+                for c in n["ch"]:
+                    src = export(nodes[c])
+                    loc = np.searchsorted(fs, src)
+                    if len(src) and not np.array_equal(fs[np.minimum(loc, len(fs) - 1)], src):
+                        raise ConfigurationError("nested dissection: child export not in parent front")
+                    mp = order[loc]
+                    mm.append(np.where(mp < ns, mp, L.S + (mp - ns)).astype(np.int32))
+                    K = max(K, len(src))
+                maps.append(mm)
+            L.K = K
+            cmap = np.full((2, L.m, K), -1, dtype=np.int32)
+            ckind = np.zeros((2, L.m, 3), dtype=np.int32)
+            for q, k in enumerate(ids):
+                for slot, c in enumerate(nodes[k]["ch"]):
+                    cmap[slot, q, :len(maps[q][slot])] = maps[q][slot]
+                    cn = nodes[c]
+                    ckind[slot, q] = (1, cn["sub"], nC[cn["sub"]]) if cn["leaf"] else (0, -1, 0)
+            L.sep_idx_h = sep_idx
+            L.sep_idx, L.bnd_idx = t(sep_idx), t(bnd_idx)
+            L.cmap_h, L.ckind_h = cmap, ckind
+            self.levels.append(L)
+        for li, L in enumerate(self.levels):
+            for q, k in enumerate(L.ids):
+                for slot, c in enumerate(nodes[k]["ch"]):
+                    if not nodes[c]["leaf"]:
+                        lc, pc = pos_in_level[c]
+                        if lc != li - 1:
+                            raise ConfigurationError("nested dissection: child not one level below")
+                        L.ckind_h[slot, q] = (0, pc, 0)
+            L.cmap = t(L.cmap_h)
+            L.ckind = t(L.ckind_h)
+        # left-looking forward lists (flux boundary slots only): for every separator
+        # slot, the global-cbuf indices of all descendant contributions to its dof,
+        # ordered deeper level first, then node, then slot (vectorised)
+        coff = 0
+        gs, srcs = [], []
+        for L in self.levels:
+            L.coff = coff
+            Bp = max(L.Bf, 1)
+            for q, k in enumerate(L.ids):
+                b = nodes[k]["bndf"]
+                if len(b):
+                    gs.append(b)
+                    srcs.append(coff + q * Bp + np.arange(len(b)))
+            coff += L.m * Bp
+        self.cb_total = coff
+        if gs:
+            gs = np.concatenate(gs)
+            srcs = np.concatenate(srcs)
+            o = np.lexsort((srcs, gs))          # by dof, then by cbuf index (= level/node/slot order)
+            gs, srcs = gs[o], srcs[o]
+        else:
+            gs = srcs = np.zeros(0, np.int64)
+        for L in self.levels:
+            sep = L.sep_idx_h.ravel()
+            lo = np.searchsorted(gs, sep, side="left")
+            hi = np.searchsorted(gs, sep, side="right")
+            cnt = np.where(sep >= 0, hi - lo, 0)
+            ptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
+            idx = np.concatenate([np.arange(a_, b_) for a_, b_, c_ in zip(lo, hi, cnt) if c_]) \
+                if cnt.sum() else np.zeros(0, np.int64)
+            src = srcs[idx] if len(idx) else np.zeros(1, np.int64)
+            L.lptr = t(ptr)
+            L.lsrc = t(src.astype(np.int32))
+        self.maxC = maxC
+        self.factored = False
+
+    # --------------------------------------------------------------- numeric
+
+    def factor(self, Kc, sub_rows_dev, b0):
+        """Assemble and factor every front (leaves -> root); returns the root level."""
+        st = _stream()
+        lib = nat.load()
+        info = torch.zeros(1, dtype=I32, device=self.dev)
+        for li, L in enumerate(self.levels):
+            L.F = torch.empty(L.m * L.nf * L.nf, dtype=F64, device=self.dev)
+            child = self.levels[li - 1] if li > 0 else None
+            for slot in (0, 1):
+                nat.call("bddc_nd_assemble", L.m, L.S, L.B, L.nf, slot, L.K, _p(L.cmap),
+                         _p(L.ckind), _p(L.sep_idx), _p(L.F),
+                         _p(child.F) if child is not None else None,
+                         child.S if child is not None else 0,
+                         child.nf if child is not None else 1,
+                         _p(Kc), _p(sub_rows_dev), _p(b0), self.maxC, st)
+            ws = torch.empty(lib.bddc_spd_inverse_workspace(L.S, L.m, 32) // 8 + 2, dtype=F64,
+                             device=self.dev)
+            nat.call("bddc_spd_inverse_batched", _p(L.F), L.S, L.nf, L.nf * L.nf, L.m, 32,
+                     _p(ws), _p(info), st)
+            del ws
+            L.X = torch.empty(L.m * L.B * L.S, dtype=F64, device=self.dev)
+            F21 = L.F[L.S * L.nf:]
+            nat.call("bddc_dgemm_batched", 0, 0, L.B, L.S, L.S, 1.0, _p(F21), L.nf,
+                     L.nf * L.nf, _p(L.F), L.nf, L.nf * L.nf, 0.0, _p(L.X), L.S,
+                     L.B * L.S, L.m, 0, st)
+            F22 = L.F[L.S * L.nf + L.S:]
+            F12 = L.F[L.S:]
+            nat.call("bddc_dgemm_batched", 0, 0, L.B, L.B, L.S, -1.0, _p(L.X), L.S,
+                     L.B * L.S, _p(F12), L.nf, L.nf * L.nf, 1.0, _p(F22), L.nf,
+                     L.nf * L.nf, L.m, 0, st)
+        if int(info.item()):
+            raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
+        self.factored = True
+        self.bytes = sum(L.m * (L.S * L.S + max(L.Bf, 1) * L.S) * 8 for L in self.levels)
+        return self.levels[-1]
+
+    def solve(self, r, x, ld=None):
+        """x = S_Pi^-1 r (flux dofs); r is read-only."""
+        st = _stream()
+        ys, cb = self._bufs()
+        for li, L in enumerate(self.levels):
+            nat.call("bddc_nd_fwd", L.m, L.S, L.Bf, L.nf, L.B * L.S, _p(L.sep_idx), _p(L.lptr),
+                     _p(L.lsrc), _p(L.F), _p(L.X), _p(r), _p(ys[li]), _p(cb), L.coff, st)
+        for li in range(len(self.levels) - 1, -1, -1):
+            L = self.levels[li]
+            nat.call("bddc_nd_bwd", L.m, L.S, L.Bf, L.B * L.S, _p(L.sep_idx), _p(L.bnd_idx),
+                     _p(L.X), _p(ys[li]), _p(x), st)
+
+    def _bufs(self):
+        if getattr(self, "_yb", None) is None:
+            ys = [torch.empty(L.m * L.S, dtype=F64, device=self.dev) for L in self.levels]
+            cb = torch.empty(max(self.cb_total, 1), dtype=F64, device=self.dev)
+            self._yb = (ys, cb)
+        return self._yb

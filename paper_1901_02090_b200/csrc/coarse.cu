@@ -6,11 +6,8 @@
 //   Psi  = S^-1 C^T Kc                (Gamma rows of the coarse basis, coarse.py:166-171)
 //   T    = S^-1 - Psi (C S^-1)        (Gamma block of the constrained inverse, coarse.py:237-245)
 //   b0   = 1^T B_loc psi = -D_i sum_q sign_q Psi[q]   (coarse.py:184-185)
-// Global: S_Pi assembled deterministically, then the pinned coarse saddle
-// (coarse.py:186-215) is reduced to dense explicit operators
-//   Mc = S_Pi^-1 - Y0 Pc^-1 Y0^T   (flux block of the pinned inverse)
-//   Wq = Y0 Pc^-1                  (pressure-rhs to flux map, solve step 1)
-// with Y0 = S_Pi^-1 B0[1:]^T and Pc = B0[1:] Y0 (subdomain 0 pinned).
+// The global coarse problem (S_Pi and the pinned pressure block) is handled
+// by the nested-dissection multifrontal solver in nd.cu / coarse_nd.py.
 #include "common.cuh"
 
 extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
@@ -81,73 +78,13 @@ __global__ void b0_kernel(bddc_geom G, const int* __restrict__ gcode, const int*
   }
 }
 
-// S_Pi assembly.  pass 0: set entries owned by the lower subdomain of a
-// face (and all cross-face entries); pass 1: add the upper subdomain's
-// same-face entries.  Fixed order => deterministic (coarse.py:182).
-__global__ void assemble_spi_kernel(int N, int maxC, const int* __restrict__ sub_rows, const double* __restrict__ Kc,
-                                    double* __restrict__ SP, long long ldsp, int pass) {
-  const int i = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= maxC * maxC) return;
-  int r = e / maxC, c = e % maxC;
-  const int* a = sub_rows + ((size_t)i * maxC + r) * 4;
-  const int* b = sub_rows + ((size_t)i * maxC + c) * 4;
-  if (a[0] < 0 || b[0] < 0) return;
-  bool same = a[1] == b[1];
-  bool upper_owner = same && a[3] < 0;
-  if ((pass == 0) == upper_owner) return;
-  double v = (double)(a[3] * b[3]) * Kc[(size_t)i * maxC * maxC + e];
-  double* p = SP + (size_t)a[0] * ldsp + b[0];
-  if (pass == 0) *p = v;
-  else *p += v;
-}
-
-// Identity padding for the dense coarse matrix beyond n.
+// Identity padding for a dense matrix beyond n.
 __global__ void pad_tail_identity_kernel(double* M, int n, int npad) {
   long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long tot = (long long)npad * npad;
   if (e >= tot) return;
   int r = (int)(e / npad), c = (int)(e % npad);
   if (r >= n || c >= n) M[e] = (r == c) ? 1.0 : 0.0;
-}
-
-// Y0T[i-1][t] = sum_r b0[i][r] SPinv[g_r][t]   (i >= 1)
-__global__ void y0t_kernel(int N, int maxC, int nfc, int ldsp, const int* __restrict__ sub_rows,
-                           const double* __restrict__ b0, const double* __restrict__ SPinv,
-                           double* __restrict__ Y0T, int ldy) {
-  const int i = blockIdx.y + 1;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ldy) return;
-  double acc = 0.0;
-  if (t < nfc) {
-    for (int r = 0; r < maxC; ++r) {
-      int g = sub_rows[((size_t)i * maxC + r) * 4];
-      if (g < 0) continue;
-      acc += b0[(size_t)i * maxC + r] * SPinv[(size_t)g * ldsp + t];
-    }
-  }
-  Y0T[(size_t)(i - 1) * ldy + t] = acc;
-}
-
-// Pc[i-1][j-1] = sum_r b0[i][r] Y0T[j-1][g_r]; identity padding to npc.
-__global__ void pc_kernel(int N, int maxC, const int* __restrict__ sub_rows, const double* __restrict__ b0,
-                          const double* __restrict__ Y0T, int ldy, double* __restrict__ Pc, int npc) {
-  const int ii = blockIdx.y;
-  const int jj = blockIdx.x * blockDim.x + threadIdx.x;
-  if (jj >= npc) return;
-  double v;
-  if (ii >= N - 1 || jj >= N - 1) {
-    v = (ii == jj) ? 1.0 : 0.0;
-  } else {
-    const int i = ii + 1;
-    v = 0.0;
-    for (int r = 0; r < maxC; ++r) {
-      int g = sub_rows[((size_t)i * maxC + r) * 4];
-      if (g < 0) continue;
-      v += b0[(size_t)i * maxC + r] * Y0T[(size_t)jj * ldy + g];
-    }
-  }
-  Pc[(size_t)ii * npc + jj] = v;
 }
 
 __global__ void copy_kernel(const double* __restrict__ a, double* __restrict__ b, long long n) {
@@ -195,45 +132,10 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   return 0;
 }
 
-// Assemble S_Pi (nfc x nfc, leading dim ldsp = npad) with identity padding.
-extern "C" int bddc_coarse_assemble(int N, int maxC, int nfc, int npad, const int* sub_rows, const double* Kc,
-                                    double* SP, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  CUDA_OK(cudaMemsetAsync(SP, 0, (size_t)npad * npad * sizeof(double), s));
-  dim3 grid((maxC * maxC + 255) / 256, N);
-  assemble_spi_kernel<<<grid, 256, 0, s>>>(N, maxC, sub_rows, Kc, SP, npad, 0);
-  LAUNCH_OK();
-  assemble_spi_kernel<<<grid, 256, 0, s>>>(N, maxC, sub_rows, Kc, SP, npad, 1);
-  LAUNCH_OK();
+// Identity on rows/columns >= n of a dense npad x npad matrix.
+extern "C" int bddc_pad_identity(double* M, int n, int npad, void* stream) {
   long long tot = (long long)npad * npad;
-  pad_tail_identity_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(SP, nfc, npad);
+  pad_tail_identity_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(M, n, npad);
   LAUNCH_OK();
-  return 0;
-}
-
-// Reduce the pinned coarse saddle to Mc (in place of SP) and Wq.
-// SP: npad x npad (input S_Pi, output Mc); Y0T: (N-1) x npad; Pc: npc x npc;
-// Wq: npad x npc (columns >= N-1 zero).
-extern "C" int bddc_coarse_factor(int N, int maxC, int nfc, int npad, int npc, const int* sub_rows, const double* b0,
-                                  double* SP, double* Y0T, double* Pc, double* Wq, void* inv_ws, int* info_sp,
-                                  int* info_pc, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  int r;
-  if ((r = bddc_spd_inverse_batched(SP, npad, npad, 0, 1, 64, inv_ws, info_sp, stream))) return r;
-  if (N < 2) return 0;
-  dim3 gy((npad + 255) / 256, N - 1);
-  y0t_kernel<<<gy, 256, 0, s>>>(N, maxC, nfc, npad, sub_rows, b0, SP, Y0T, npad);
-  LAUNCH_OK();
-  dim3 gp((npc + 255) / 256, npc);
-  pc_kernel<<<gp, 256, 0, s>>>(N, maxC, sub_rows, b0, Y0T, npad, Pc, npc);
-  LAUNCH_OK();
-  if ((r = bddc_spd_inverse_batched(Pc, npc, npc, 0, 1, 64, inv_ws, info_pc, stream))) return r;
-  // Wq = Y0 Pc^-1 = (Y0T)^T Pcinv   (npad x npc); rows of Y0T beyond N-1 are not read
-  if ((r = bddc_dgemm_batched(1, 0, npad, npc, N - 1, 1.0, Y0T, npad, 0, Pc, npc, 0, 0.0, Wq, npc, 0, 1, 0, stream)))
-    return r;
-  // Mc = SPinv - Wq Y0^T
-  if ((r = bddc_dgemm_batched(0, 0, npad, npad, N - 1, -1.0, Wq, npc, 0, Y0T, npad, 0, 1.0, SP, npad, 0, 1, 0,
-                              stream)))
-    return r;
   return 0;
 }

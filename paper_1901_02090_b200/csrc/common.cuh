@@ -23,8 +23,8 @@ extern "C" void bddc_count_launch(void);
 
 extern "C" int bddc_set_error(int code, const char* msg);
 
-__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
-__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 
 // Subdomain box of subdomain i under a regular partition.
 struct Box {

@@ -189,7 +189,7 @@ __global__ void proj_apply_kernel(int n_gamma, int maxG, const int* __restrict__
 // them in index order and applies `op` (see bddc_dot).
 __global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, long long n,
                            double* __restrict__ partial, unsigned* __restrict__ counter,
-                           double* __restrict__ scal, int op, double* __restrict__ hist, int it) {
+                           double* __restrict__ scal, int op, double* __restrict__ hist) {
   __shared__ double red[32];
   __shared__ bool last;
   double acc = 0.0;
@@ -210,34 +210,44 @@ __global__ void dot_kernel(const double* __restrict__ x, const double* __restric
   s = block_sum(s, red);
   if (threadIdx.x == 0) {
     *counter = 0u;
-    // scal slots: 0 rz, 1 pAp, 2 alpha, 3 rr, 4 res0, 5 relres, 6 rz_new, 7 beta, 8 bad
+    // scal slots: 0 rz, 1 pAp, 2 alpha, 3 rr, 4 res0, 5 relres, 6 rz_new, 7 beta,
+    // 8 bad (non-positive curvature), 9 iterations completed (device counter)
+    const int itc = (int)scal[9];
     switch (op) {
       case 0:  // rz (initial)
         scal[0] = s;
         break;
-      case 1: {  // pAp -> alpha
+      case 1: {  // pAp -> alpha, alphas[it]
         scal[1] = s;
         double a = scal[0] / s;
         if (!(s > 0.0)) scal[8] = 1.0;
         scal[2] = a;
-        if (hist) hist[it] = a;
+        if (hist) hist[itc] = a;
         break;
       }
-      case 2:  // rr -> relres
+      case 2: {  // rr -> relres, it += 1, relres history[it]
         scal[3] = s;
-        scal[5] = sqrt(s) / scal[4];
+        double rel = sqrt(s) / scal[4];
+        scal[5] = rel;
+        scal[9] = (double)(itc + 1);
+        if (hist) hist[itc + 1] = rel;
         break;
-      case 3: {  // rz_new -> beta
+      }
+      case 3: {  // rz_new -> beta, betas[it-1]
         double b = s / scal[0];
         scal[6] = s;
         scal[7] = b;
         scal[0] = s;
-        if (hist) hist[it] = b;
+        if (hist && itc >= 1) hist[itc - 1] = b;
         break;
       }
-      case 4:  // res0 = sqrt(rr)
+      case 4:  // res0 = ||r||, reset the counter, history[0] = 1
         scal[3] = s;
         scal[4] = sqrt(s);
+        scal[5] = 1.0;
+        scal[8] = 0.0;
+        scal[9] = 0.0;
+        if (hist) hist[0] = 1.0;
         break;
       default:  // plain store into slot (op - 100)
         scal[op - 100] = s;
@@ -403,10 +413,10 @@ extern "C" int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const dou
 extern "C" size_t bddc_dot_workspace(void) { return DOT_BLOCKS * sizeof(double) + 64; }
 
 extern "C" int bddc_dot(const double* x, const double* y, long long n, void* ws, double* scal, int op, double* hist,
-                        int it, void* stream) {
+                        void* stream) {
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
-  dot_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n, partial, counter, scal, op, hist, it);
+  dot_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n, partial, counter, scal, op, hist);
   LAUNCH_OK();
   return 0;
 }

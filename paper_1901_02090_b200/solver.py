@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from .coarse_nd import CoarseND
 from .decomposition import Decomposition
 from .errors import (ConfigurationError, InternalConsistencyError,
                      InvalidArgumentError, NonConvergenceError,
@@ -260,32 +261,17 @@ class BddcSetup:
                  _p(info[2:]), st)
         del Ct, Y, ws, Sinv
         self._mark(ev, "coarse_local")
-        # global coarse: S_Pi -> Mc, Wq
+        # global coarse: multifrontal S_Pi (nested dissection) + pinned pressure Schur Pc
         nfc = self.n_flux_coarse
         self.nfc = nfc
         self.npad = _pad(max(nfc, 1), 64)
         self.npc = _pad(max(N - 1, 1), 64)
-        self.d_Mc = None
-        self.d_Wq = None
+        self.nd = None
+        self.d_Pcinv = None
         if nfc:
-            self.d_Mc = torch.empty(self.npad * self.npad, dtype=F64, device=dev)
-            nat.call("bddc_coarse_assemble", N, maxC, nfc, self.npad,
-                     _p(dev_rows), _p(self.d_Kc), _p(self.d_Mc), st)
-            Y0T = torch.zeros(max(N - 1, 1) * self.npad, dtype=F64, device=dev)
-            Pc = torch.empty(self.npc * self.npc, dtype=F64, device=dev)
-            self.d_Wq = torch.zeros(self.npad * self.npc, dtype=F64, device=dev)
-            wsz = max(nat.load().bddc_spd_inverse_workspace(self.npad, 1, 64),
-                      nat.load().bddc_spd_inverse_workspace(self.npc, 1, 64))
-            ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
-            info2 = torch.zeros(2, dtype=I32, device=dev)
-            nat.call("bddc_coarse_factor", N, maxC, nfc, self.npad, self.npc,
-                     _p(dev_rows), _p(self.d_b0), _p(self.d_Mc), _p(Y0T), _p(Pc),
-                     _p(self.d_Wq), _p(ws), _p(info2), _p(info2[1:]), st)
-            del ws, Y0T, Pc
-            bad = info2.cpu().numpy()
-            if bad.any():
-                raise ConfigurationError(
-                    "coarse problem singular; initial constraints do not cover all faces")
+            self.nd = CoarseND(dec, per_face, cstart, self.sub_rows, self.nC, maxC, dev)
+            root = self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
+            self._build_pressure_schur(root)
         bad = info.cpu().numpy()
         if bad[0] or bad[1]:
             raise NumericalFailureError("local interior factorization failed", where=None)
@@ -303,10 +289,21 @@ class BddcSetup:
         self.w_xc = z(self.npad)
         self.w_phi = z(N)
         self.w_z = z(N)
+        self.w_c1 = z(self.npad)
+        self.w_x1 = z(self.npad)
+        self.w_t = z(self.npc)
+        self.w_pz = z(self.npc)
         self.w_dot = torch.zeros(nat.load().bddc_dot_workspace() // 8 + 1, dtype=F64, device=dev)
         self.w_scal = z(16)
         self.d_dct = torch.empty(sum(n * n + n for n in dec.n3), dtype=F64, device=dev)
         nat.call("bddc_dct_init", gp, _p(self.d_dct), st)
+        self._graphs = {}
+        self._pcg_b = None
+        self._work = None
+        self._host_scal = torch.empty(16, dtype=F64, pin_memory=True)
+        self.stream = torch.cuda.Stream(device=dev)
+        self._scaling_checked = False
+        self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._mark(ev, "done")
         self.phase_ms = self._finish(ev)
 
@@ -325,6 +322,9 @@ class BddcSetup:
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         ev.append((name, e))
+        import time as _t
+        self._hmarks = getattr(self, "_hmarks", [])
+        self._hmarks.append((name, _t.perf_counter()))
 
     def _finish(self, ev):
         if ev is None:
@@ -334,35 +334,102 @@ class BddcSetup:
         for (_, a), (n, b) in zip(ev[:-1], ev[1:]):
             out[n] = a.elapsed_time(b)
         out["total"] = ev[0][1].elapsed_time(ev[-1][1])
+        hm = getattr(self, "_hmarks", [])
+        for (_, a), (n, b) in zip(hm[:-1], hm[1:]):
+            out["host_" + n] = 1000.0 * (b - a)
         if isinstance(self._timings, dict):
             self._timings.update(out)
         return out
 
     def _build_coarse_tables(self, cstart, per_face, maxsel):
+        """Per-subdomain coarse rows {g, face, k, sigma} in (face, k) order and the
+        two owners (i*maxC + r) of every coarse dof (vectorised bookkeeping)."""
         dec, N = self.dec, self.N
         ft = dec.face_table
-        rows_per_sub = [[] for _ in range(N)]
-        for f in range(dec.n_faces):
-            i, j = int(ft[f, 0]), int(ft[f, 1])
-            for k in range(int(per_face[f])):
-                g = int(cstart[f] + k)
-                rows_per_sub[i].append((g, f, k, 1))
-                rows_per_sub[j].append((g, f, k, -1))
-        nC = np.array([len(r) for r in rows_per_sub], dtype=np.int32)
+        nf = dec.n_faces
+        nfc = int(per_face.sum()) if nf else 0
+        f_of = np.repeat(np.arange(nf), per_face) if nf else np.zeros(0, np.int64)
+        k_of = np.arange(nfc) - np.repeat(cstart, per_face) if nf else np.zeros(0, np.int64)
+        g_of = np.arange(nfc)
+        sub = np.concatenate([ft[f_of, 0], ft[f_of, 1]]) if nf else np.zeros(0, np.int64)
+        sig = np.concatenate([np.ones(nfc, np.int64), -np.ones(nfc, np.int64)])
+        ff = np.concatenate([f_of, f_of])
+        kk = np.concatenate([k_of, k_of])
+        gg = np.concatenate([g_of, g_of])
+        o = np.lexsort((kk, ff, sub))
+        sub, sig, ff, kk, gg = sub[o], sig[o], ff[o], kk[o], gg[o]
+        nC = np.bincount(sub, minlength=N).astype(np.int32) if len(sub) else np.zeros(N, np.int32)
         maxC = _pad(int(nC.max()) if N else 1, 32)
+        starts = np.concatenate([[0], np.cumsum(nC)[:-1]])
+        r = np.arange(len(sub)) - starts[sub]
         sub_rows = np.full((N, maxC, 4), -1, dtype=np.int32)
-        nfc = int(per_face.sum()) if dec.n_faces else 0
+        sub_rows[sub, r] = np.stack([gg, ff, kk, sig], axis=1)
         cown = np.zeros((nfc, 2), dtype=np.int32)
-        for i, rs in enumerate(rows_per_sub):
-            rs.sort(key=lambda r: (r[1], r[2]))
-            for r, (g, f, k, s) in enumerate(rs):
-                sub_rows[i, r] = (g, f, k, s)
-                cown[g, 0 if s > 0 else 1] = i * maxC + r
+        cown[gg, np.where(sig > 0, 0, 1)] = sub * maxC + r
         self.sub_rows, self.cown, self.nC, self.maxC = sub_rows, cown, nC, maxC
 
     @property
     def n_c(self):
         return self.n_flux_coarse + self.N
+
+    def _pcg_bufs(self, maxit):
+        if self._pcg_b is None or self._pcg_b.maxit < maxit:
+            self._pcg_b = _PCGBufs(self, maxit)
+        return self._pcg_b
+
+    def work(self):
+        if self._work is None:
+            self._work = _Work(self)
+        return self._work
+
+    def __del__(self):
+        try:
+            lib = nat.load()
+            for g in getattr(self, "_graphs", {}).values():
+                lib.bddc_graph_destroy(g)
+        except Exception:
+            pass
+
+    def _build_pressure_schur(self, root):
+        """Pc = B0[1:] S_Pi^-1 B0[1:]^T (subdomain 0 pinned, coarse.py:192-194), inverted.
+
+        Read off the root front's update matrix (= -B0 S_Pi^-1 B0^T over all pressures).
+        """
+        N, npc, st = self.N, self.npc, _stream()
+        dev = self.dev
+        Pc = torch.empty(npc * npc, dtype=F64, device=dev)
+        nat.call("bddc_nd_extract_pc", _p(root.F), root.nf, root.S, N, _p(Pc), npc, st)
+        info = torch.zeros(1, dtype=I32, device=dev)
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(npc, 1, 64) // 8 + 2,
+                         dtype=F64, device=dev)
+        nat.call("bddc_spd_inverse_batched", _p(Pc), npc, npc, 0, 1, 64, _p(ws), _p(info), st)
+        if int(info.item()):
+            raise ConfigurationError(
+                "coarse problem singular; initial constraints do not cover all faces")
+        self.d_Pcinv = Pc
+
+    def _coarse_flux_solve(self, rhs, out):
+        """out = flux block of the pinned coarse inverse applied to rhs (r_q = 0)."""
+        st = _stream()
+        self.nd.solve(rhs, self.w_x1, ld=self.nfc)
+        if self.N > 1:
+            nat.call("bddc_b0_apply", self.N, self.maxC, _p(self.d_sub_rows), _p(self.d_b0),
+                     _p(self.w_x1), self.nfc, 1, _p(self.w_t), self.npc, st)
+            nat.call("bddc_gemv", self.N - 1, self.npc, self.N - 1, _p(self.d_Pcinv),
+                     _p(self.w_t), _p(self.w_pz), st)
+            nat.call("bddc_b0t_apply", self.nfc, self.maxC, _p(self.d_cown), _p(self.d_b0),
+                     _p(self.w_pz), self.npc, 1, -1.0, _p(rhs), self.nfc, st)
+        self.nd.solve(rhs, out, ld=self.nfc)
+
+    def _coarse_pressure_solve(self, rq1, out):
+        """Step 1 (solver.py:318-319): flux part of the pinned solve with rhs (0, r_q)."""
+        st = _stream()
+        nat.call("bddc_gemv", self.N - 1, self.npc, self.N - 1, _p(self.d_Pcinv), _p(rq1),
+                 _p(self.w_pz), st)
+        nat.call("bddc_fill", self.nfc, 0.0, _p(self.w_c1), st)
+        nat.call("bddc_b0t_apply", self.nfc, self.maxC, _p(self.d_cown), _p(self.d_b0),
+                 _p(self.w_pz), self.npc, 1, 1.0, _p(self.w_c1), self.nfc, st)
+        self.nd.solve(self.w_c1, out, ld=self.nfc)
 
     # ----------------------------------------- interface operator (device)
 
@@ -403,8 +470,7 @@ class BddcSetup:
                      _p(self.d_delta), _p(self.w_v), st)
             nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
                      _p(self.w_crhs), st)
-            nat.call("bddc_gemv", self.nfc, self.npad, self.nfc, _p(self.d_Mc),
-                     _p(self.w_crhs), _p(self.w_xc), st)
+            self._coarse_flux_solve(self.w_crhs, self.w_xc)
         nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG),
                  _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
                  _p(self.d_delta), _p(self.w_yb2), st)
@@ -502,11 +568,12 @@ class _Work:
         self.pc = z(G.n_cells)
         self.rq = z(setup.N)
         self.x0 = z(setup.npad)
+        self.f_dev = z(G.n_cells)
 
 
-def _dot(setup, x, y, n, op, hist=None, it=0):
+def _dot(setup, x, y, n, op, hist=None):
     nat.call("bddc_dot", _p(x), _p(y), int(n), _p(setup.w_dot), _p(setup.w_scal), op,
-             _p(hist) if hist is not None else None, it, _stream())
+             _p(hist) if hist is not None else None, _stream())
 
 
 def _norm(setup, x, n):
@@ -519,23 +586,36 @@ def solve(system, dec, config, u_exact=None, setup=None, iterate_callback=None,
     """Three-step method + pressure recovery (solver.py:301-398)."""
     if setup is None:
         setup = BddcSetup(system, dec, config)
+    if not setup._scaling_checked:
+        _suggest_scaling(setup)
+        setup._scaling_checked = True
+    caller = torch.cuda.current_stream()
+    setup.stream.wait_stream(caller)
+    with torch.cuda.stream(setup.stream):
+        out = _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
+                               return_device)
+    caller.wait_stream(setup.stream)
+    return out
+
+
+def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device, return_device):
     dec = setup.dec
     G = setup.geom
     gp = C.byref(G)
     st = _stream()
-    _suggest_scaling(setup)
-    W = _Work(setup)
+    W = setup.work()
     N, ng = setup.N, setup.n_gamma
     # fs = D f
     if f_device is None:
-        fh = torch.as_tensor(np.asarray(system.f, dtype=np.float64))
-        f_device = fh.pin_memory().to(setup.dev, non_blocking=True) if fh.numel() else fh.to(setup.dev)
+        fh = torch.as_tensor(np.asarray(system.f, dtype=np.float64)).pin_memory()
+        W.f_host = fh   # keep the pinned buffer alive until the copy ran
+        f_device = W.f_dev
+        f_device.copy_(fh, non_blocking=True)
     _scale_fs(setup, f_device, W.fs)
     # step 1: rq_i = sum fs over cells of i; x0 = Wq rq[1:]; g = average(Psi x0)
     nat.call("bddc_sub_sum", gp, _p(W.fs), _p(W.rq), 1.0, None, st)
     if setup.nfc and N > 1:
-        nat.call("bddc_gemv", setup.nfc, setup.npc, N - 1, _p(setup.d_Wq),
-                 _p(W.rq[1:]), _p(W.x0), st)
+        setup._coarse_pressure_solve(W.rq[1:], W.x0)
     if ng:
         nat.call("bddc_prolong", N, setup.maxG, setup.maxC, _p(setup.d_nG),
                  _p(setup.d_sub_rows), _p(setup.d_Psi), _p(W.x0), None,
@@ -588,6 +668,8 @@ def solve(system, dec, config, u_exact=None, setup=None, iterate_callback=None,
                      _p(setup.w_z), _p(W.wp), st)
             setup._schur(W.wp, W.Ap)
             nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
+        else:
+            nat.call("bddc_fill", ng, 0.0, _p(W.wp), st)
         setup._project(W.r)
         w_cg_it, kappa, history, converged = _pcg(setup, W, config, iterate_callback)
         # u = u* + correction, interior recovery
@@ -656,53 +738,115 @@ def _ones(setup, n):
     return o
 
 
+class _PCGBufs:
+    """Device-resident PCG history (alphas, betas, relative residuals)."""
+
+    def __init__(self, setup, maxit):
+        z = lambda n: torch.zeros(n, dtype=F64, device=setup.dev)
+        self.maxit = maxit
+        self.alphas = z(maxit + 2)
+        self.betas = z(maxit + 2)
+        self.res = z(maxit + 2)
+
+
+def _pcg_core(setup, W, B):
+    """Ap = P S p; alpha; x += alpha p; r -= alpha Ap; relres (solver.py:205-216)."""
+    ng = setup.n_gamma
+    setup._schur(W.p, W.Ap)
+    setup._project(W.Ap)
+    _dot(setup, W.p, W.Ap, ng, 1, B.alphas)
+    nat.call("bddc_cg_update", ng, _p(setup.w_scal), _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _stream())
+    _dot(setup, W.r, W.r, ng, 2, B.res)
+
+
+def _pcg_first(setup, W, B):
+    """z = P M r; p = z; rz = r.z; first iteration (solver.py:198-216)."""
+    ng = setup.n_gamma
+    setup._precond(W.r, W.zv)
+    setup._project(W.zv)
+    nat.call("bddc_axpby", ng, 1.0, _p(W.zv), 0.0, _p(W.p), _stream())
+    _dot(setup, W.r, W.zv, ng, 0)
+    _pcg_core(setup, W, B)
+
+
+def _pcg_body(setup, W, B):
+    """z = P M r; beta; p = z + beta p; next iteration (solver.py:222-227, 205-216)."""
+    ng = setup.n_gamma
+    setup._precond(W.r, W.zv)
+    setup._project(W.zv)
+    _dot(setup, W.r, W.zv, ng, 3, B.betas)
+    nat.call("bddc_p_update", ng, _p(setup.w_scal), _p(W.zv), _p(W.p), _stream())
+    _pcg_core(setup, W, B)
+
+
+def _pcg_graph(setup, W, B, tol, maxit):
+    """Build (once per setup/tol/maxit) the WHILE-conditional graph of the PCG loop."""
+    key = (float(tol), int(maxit))
+    cache = setup._graphs
+    if key in cache:
+        return cache[key]
+    st = _stream()
+    state = C.c_void_p()
+    nat.call("bddc_graph_begin", C.byref(state), st)
+    try:
+        _pcg_first(setup, W, B)
+        nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        nat.call("bddc_graph_while", state, st)
+        _pcg_body(setup, W, B)
+        nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        nat.call("bddc_graph_end", state, st)
+    except Exception:
+        nat.load().bddc_graph_destroy(state)
+        raise
+    cache[key] = state
+    return state
+
+
 def _pcg(setup, W, config, callback):
-    """PCG with Lanczos kappa (solver.py:186-233), scalars kept on device."""
+    """PCG with Lanczos kappa (solver.py:186-233), fully device resident.
+
+    Without a callback the whole loop is one CUDA-graph launch (conditional
+    WHILE node); with a callback every iteration syncs to hand x, r to the host.
+    """
     ng = setup.n_gamma
     st = _stream()
     tol, maxit = config.tol, config.maxit
     scal = setup.w_scal
-    scal.zero_()
-    W.x.zero_()
-    _dot(setup, W.r, W.r, ng, 4)
-    res0 = float(scal[4].item())
-    history = [1.0]
-    if res0 == 0.0:
-        return 0, 1.0, np.array(history), True
-    alphas = torch.zeros(maxit + 1, dtype=F64, device=setup.dev)
-    betas = torch.zeros(maxit + 1, dtype=F64, device=setup.dev)
-    setup._precond(W.r, W.zv)
-    setup._project(W.zv)
-    nat.call("bddc_axpby", ng, 1.0, _p(W.zv), 0.0, _p(W.p), st)
-    _dot(setup, W.r, W.zv, ng, 0)
-    converged = False
-    it = 0
-    host = torch.empty(16, dtype=F64, pin_memory=True)
-    for it in range(1, maxit + 1):
-        setup._schur(W.p, W.Ap)
-        setup._project(W.Ap)
-        _dot(setup, W.p, W.Ap, ng, 1, alphas, it - 1)
-        nat.call("bddc_cg_update", ng, _p(scal), _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), st)
-        _dot(setup, W.r, W.r, ng, 2)
+    B = setup._pcg_bufs(maxit)
+    nat.call("bddc_fill", 16, 0.0, _p(scal), st)
+    nat.call("bddc_fill", ng, 0.0, _p(W.x), st)
+    _dot(setup, W.r, W.r, ng, 4, B.res)
+    host = setup._host_scal
+    host.copy_(scal, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    if host[4] == 0.0:
+        return 0, 1.0, np.array([1.0]), True
+    if callback is None and not setup.force_eager:
+        # make sure every lazily-created buffer exists before capture
+        setup.nd is not None and setup.nd._bufs()
+        g = _pcg_graph(setup, W, B, tol, maxit)
+        nat.call("bddc_graph_launch", g, st)
         host.copy_(scal, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        if host[8] != 0.0:
-            raise NonConvergenceError(
-                f"non-positive curvature p'Sp = {float(host[1]):.3e} at iteration {it}; "
-                "iterate left the balanced subspace")
-        rel = float(host[5])
-        history.append(rel)
-        if callback is not None:
-            callback(W.x.cpu().numpy(), W.r.cpu().numpy())
-        if rel <= tol:
-            converged = True
-            break
-        setup._precond(W.r, W.zv)
-        setup._project(W.zv)
-        _dot(setup, W.r, W.zv, ng, 3, betas, it - 1)
-        nat.call("bddc_p_update", ng, _p(scal), _p(W.zv), _p(W.p), st)
-    kappa = _lanczos(setup, alphas, betas, it)
-    return it, kappa, np.array(history), converged
+    else:
+        _pcg_first(setup, W, B)
+        while True:
+            host.copy_(scal, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            if callback is not None:
+                callback(W.x.cpu().numpy(), W.r.cpu().numpy())
+            if host[5] <= tol or host[8] != 0.0 or int(host[9]) >= maxit:
+                break
+            _pcg_body(setup, W, B)
+    it = int(host[9])
+    if host[8] != 0.0:
+        raise NonConvergenceError(
+            f"non-positive curvature p'Sp = {float(host[1]):.3e} at iteration {it}; "
+            "iterate left the balanced subspace")
+    converged = bool(host[5] <= tol)
+    history = B.res[:it + 1].cpu().numpy()
+    kappa = _lanczos(setup, B.alphas, B.betas, it)
+    return it, kappa, history, converged
 
 
 def _lanczos(setup, alphas, betas, m):

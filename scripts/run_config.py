@@ -29,10 +29,11 @@ for rep in range(a.reps):
     torch.cuda.synchronize(); ts = time.time() - t
     print(f"setup {ts:.3f}s  phases(ms): " + " ".join(f"{k}={v:.1f}" for k, v in tm.items()), flush=True)
     print(f"  n_c={st.n_c} nfc={st.nfc} maxC={st.maxC} omega={st.omega_tilde} mem={torch.cuda.max_memory_allocated()/1e9:.1f}GB", flush=True)
-    t = time.time()
-    r = B.solve(system, dec, cfg, setup=st)
-    torch.cuda.synchronize(); tsol = time.time() - t
-    print(f"  solve {tsol:.3f}s it={r.it} kappa={r.kappa:.4f} it/s={r.it/tsol:.1f} cons={r.conservation_defect:.2e} pw={r.pressure_warning}", flush=True)
+    for rr in range(3):
+        t = time.time()
+        r = B.solve(system, dec, cfg, setup=st)
+        torch.cuda.synchronize(); tsol = time.time() - t
+        print(f"  solve[{rr}] {tsol:.3f}s it={r.it} kappa={r.kappa:.4f} it/s={r.it/tsol:.1f} cons={r.conservation_defect:.2e} pw={r.pressure_warning}", flush=True)
     del st
     torch.cuda.empty_cache()
 # per-call device-time breakdown of one setup + one solve
@@ -40,6 +41,8 @@ from paper_1901_02090_b200 import _native as nat
 nat.profile_start()
 st = B.BddcSetup(system, dec, cfg)
 prof_setup = nat.profile_stop()
+st.force_eager = True
+r = B.solve(system, dec, cfg, setup=st)
 nat.profile_start()
 r = B.solve(system, dec, cfg, setup=st)
 prof_solve = nat.profile_stop()
