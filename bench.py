@@ -220,12 +220,10 @@ def main():
     for _ in range(args.warmup):
         W, it, kappa, hist, conv = S.solve(system, dec, cfg, setup=setup, f_device=f_dev,
                                            return_device=True)
-    # kernel timer on the dominant kernel (interface Schur GEMV) during the timed region
-    kt = {"ev": []}
-    setup._ktimer = kt
     barrier()
     torch.cuda.synchronize()
     l0 = lib.bddc_launch_count()
+    g0 = setup.graph_kernels_run
     with Clocks(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -236,16 +234,19 @@ def main():
             its.append(it)
         t1.record()
         torch.cuda.synchronize()
-    launches = lib.bddc_launch_count() - l0
-    setup._ktimer = None
+    # host-issued launches + kernel nodes executed by the PCG graph launches
+    launches = (lib.bddc_launch_count() - l0) + (setup.graph_kernels_run - g0)
     barrier()
     step_s = t0.elapsed_time(t1) / 1000.0
     step_s_max = allmax(step_s)
     tot_it = allsum(float(sum(its)))
     value = tot_it / step_s_max
     ms_per_step = 1000.0 * step_s_max / args.steps
-    kdur = [a.elapsed_time(b) / 1000.0 for a, b in kt["ev"]]
-    kmean = float(np.mean(kdur)) if kdur else float("nan")
+    # the PCG loop runs as one CUDA graph, so the dominant kernel (interface Schur
+    # GEMV, same data and launch shape) is re-timed right after the timed region
+    kreps = 20
+    kmean = setup.time_kernel("S", kreps)
+    kdur = [kmean] * kreps
 
     # ---- roofline for the dominant kernel: S-GEMV, algorithmic bytes =
     # packed-symmetric S_i (8 n(n+1)/2 per subdomain) + x gather + y write
@@ -293,7 +294,9 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
-                     "launches_timed": len(kdur), "mean_launch_s": kmean},
+                     "launches_timed": len(kdur), "mean_launch_s": kmean,
+                     "timing": "CUDA events, 20 back-to-back launches after the timed region "
+                               "(the PCG loop itself is one graph launch)"},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
     }

@@ -298,6 +298,8 @@ class BddcSetup:
         self.d_dct = torch.empty(sum(n * n + n for n in dec.n3), dtype=F64, device=dev)
         nat.call("bddc_dct_init", gp, _p(self.d_dct), st)
         self._graphs = {}
+        self._graph_kernels = {}
+        self.graph_kernels_run = 0   # kernels executed inside PCG graph launches (accounting)
         self._pcg_b = None
         self._work = None
         self._host_scal = torch.empty(16, dtype=F64, pin_memory=True)
@@ -475,6 +477,23 @@ class BddcSetup:
                  _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
                  _p(self.d_delta), _p(self.w_yb2), st)
         nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
+
+    def time_kernel(self, which="S", reps=20):
+        """Mean device time (s) of one interface GEMV launch (bench roofline helper)."""
+        mats = {"S": self.d_S, "T": self.d_T}[which]
+        x = torch.ones(max(self.n_gamma, 1), dtype=F64, device=self.dev)
+        st = _stream()
+        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(mats), _p(x), None, _p(self.w_yb), st)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(mats), _p(x), None, _p(self.w_yb), st)
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / 1000.0 / reps
 
     # public reference-compatible applies (numpy in / numpy out)
     def schur_matvec(self, x):
@@ -786,18 +805,24 @@ def _pcg_graph(setup, W, B, tol, maxit):
     if key in cache:
         return cache[key]
     st = _stream()
+    lib = nat.load()
     state = C.c_void_p()
     nat.call("bddc_graph_begin", C.byref(state), st)
     try:
+        c0 = lib.bddc_launch_count()
         _pcg_first(setup, W, B)
         nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        c1 = lib.bddc_launch_count()
         nat.call("bddc_graph_while", state, st)
         _pcg_body(setup, W, B)
         nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        c2 = lib.bddc_launch_count()
         nat.call("bddc_graph_end", state, st)
     except Exception:
-        nat.load().bddc_graph_destroy(state)
+        lib.bddc_graph_destroy(state)
         raise
+    # kernels per graph launch: top level (first iteration) and per WHILE body pass
+    setup._graph_kernels[key] = (int(c1 - c0), int(c2 - c1))
     cache[key] = state
     return state
 
@@ -828,6 +853,8 @@ def _pcg(setup, W, config, callback):
         nat.call("bddc_graph_launch", g, st)
         host.copy_(scal, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        top, body = setup._graph_kernels[(float(tol), int(maxit))]
+        setup.graph_kernels_run += top + body * max(int(host[9]) - 1, 0)
     else:
         _pcg_first(setup, W, B)
         while True:

@@ -9,6 +9,7 @@ from paper_1901_02090_b200 import fields
 ap = argparse.ArgumentParser()
 ap.add_argument("cfg", type=int)
 ap.add_argument("--what", default="solve")
+ap.add_argument("--eager", action="store_true", help="host-driven PCG loop (ncu sees every kernel)")
 a = ap.parse_args()
 c = fields.CONFIGS[a.cfg]
 k = fields.config_field(a.cfg)
@@ -23,6 +24,7 @@ if a.what == "setup":
     torch.cuda.synchronize(); torch.cuda.profiler.stop()
 else:
     st = B.BddcSetup(system, dec, cfg)
+    st.force_eager = a.eager
     r = B.solve(system, dec, cfg, setup=st)      # warm
     torch.cuda.synchronize(); torch.cuda.profiler.start()
     r = B.solve(system, dec, cfg, setup=st)
