@@ -138,11 +138,18 @@ int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, const int* cm
                      const int* ckind, const int* sep_idx, double* F, const double* Fc, int Sc,
                      int nfc, const double* Kc, const int* sub_rows, const double* b0, int maxC,
                      void* stream);
-int bddc_nd_fwd(int m, int S, int Bf, int nf, long long xstride, const int* sep_idx,
-                const int* lptr, const int* lsrc, const double* F, const double* X, const double* r,
-                double* ybuf, double* cbuf, long long coff, void* stream);
-int bddc_nd_bwd(int m, int S, int Bf, long long xstride, const int* sep_idx, const int* bnd_idx,
-                const double* X, const double* ybuf, double* x, void* stream);
+/* Solves on the compact per-node layout (info = {s, bf, sep_ptr, bnd_ptr, cb_off}). */
+int bddc_nd_fwd(int ntasks, int smax, const int* tasks, const int* info, const long long* data_off,
+                const int* sep_flat, const int* lptr, const int* lsrc, const double* Fc,
+                const double* r, double* ybuf, double* cbuf, void* stream);
+int bddc_nd_bwd(int ntasks, int bfmax, const int* tasks, const int* info, const long long* data_off,
+                const int* sep_flat, const int* bnd_flat, const double* Fc, const double* ybuf,
+                double* x, void* stream);
+int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
+                    const long long* data_off, double* Fc, void* stream);
+/* Root pressure block of the pinned coarse solve: x_p = -Pc^-1 (r_p - contributions). */
+int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const int* psrc, const double* cbuf,
+                     const double* Pcinv, const double* r, double* rp, double* x, void* stream);
 /* Pinned pressure Schur Pc = -U_root[1:,1:] (coarse.py:192-194). */
 int bddc_nd_extract_pc(const double* F, int nf, int S, int N, double* Pc, int npc, void* stream);
 /* Pressure coupling B0 (coarse.py:184-193): out = B0[1:] Y, r += alpha B0[1:]^T z. */
@@ -158,14 +165,22 @@ int bddc_fill(long long n, double v, double* a, void* stream);
  * solver.py:114-124 Delta part of precondition). */
 int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos, const double* Mats,
                      const double* x, const double* win, double* yb, void* stream);
-/* v_i = Psi_i^T (win .* gather(x)) (coarse.py:225-235 weighted_restriction). */
+/* Tile-packed symmetric storage (32x32 upper tiles) and the gathered symmetric GEMV
+ * used for S_i and T_i in the PCG loop (same contract as bddc_gather_gemv). */
+size_t bddc_sym_packed_elems(int maxG);
+int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream);
+int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                     const double* x, const double* win, double* yb, void* stream);
+/* v_i = Psi_i^T (win .* gather(x)) (coarse.py:225-235 weighted_restriction); PsiT is
+ * stored maxC x maxG per subdomain. */
 int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,
-                       const double* Psi, const double* x, const double* win, double* v,
+                       const double* PsiT, const double* x, const double* win, double* v,
                        void* stream);
 int bddc_coarse_restrict(int nfc, const int* cown, const double* v, double* rhs, void* stream);
 /* out_b = wout .* (y_b + Psi_i sigma x_c) (coarse.py:217-223 local_combination). */
-int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* sub_rows, const double* Psi,
-                 const double* xc, const double* yb, const double* wout, double* outb, void* stream);
+int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* nC, const int* sub_rows,
+                 const double* PsiT, const double* xc, const double* yb, const double* wout,
+                 double* outb, void* stream);
 /* y = sum over both copies (solver.py:100-101 scatter_add). */
 int bddc_scatter(int n_gamma, const int* gown, const double* yb, double* y, void* stream);
 /* Balanced projection (solver.py:166-179) as I - Phi^T (Phi Phi^T)^+ Phi. */

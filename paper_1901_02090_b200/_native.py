@@ -107,17 +107,22 @@ _SIGS = {
     "bddc_pcg_cond": [_P, _P, _D, _I, _P],
     "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
                          _P, _P, _I, _P],
-    "bddc_nd_fwd": [_I, _I, _I, _I, _L, _P, _P, _P, _P, _P, _P, _P, _P, _L, _P],
+    "bddc_nd_fwd": [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_compact": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_pressure": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_nd_extract_pc": [_P, _I, _I, _I, _P, _I, _P],
-    "bddc_nd_bwd": [_I, _I, _I, _L, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_bwd": [_I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_b0_apply": [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P],
     "bddc_b0t_apply": [_I, _I, _P, _P, _P, _I, _I, _D, _P, _I, _P],
     "bddc_fill": [_L, _D, _P, _P],
 
     "bddc_gather_gemv": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_sym_packed_elems": [_I],
+    "bddc_pack_sym": [_I, _I, _P, _P, _P],
+    "bddc_gather_symv": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "bddc_gather_gemv_t": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_coarse_restrict": [_I, _P, _P, _P, _P],
-    "bddc_prolong": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_prolong": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_scatter": [_I, _P, _P, _P, _P],
     "bddc_phi": [_I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_lap_solve": [_I, _I, _I, _P, _P, _P, _P, _P],
@@ -148,6 +153,7 @@ _RESTYPES = {
     "bddc_spd_inverse_workspace": C.c_size_t,
     "bddc_pair_scratch_bytes": C.c_size_t,
     "bddc_dot_workspace": C.c_size_t,
+    "bddc_sym_packed_elems": C.c_size_t,
     "bddc_geom_size": C.c_size_t,
     "bddc_launch_count": C.c_ulonglong,
     "bddc_graph_handle": C.c_ulonglong,

@@ -189,39 +189,73 @@ class CoarseND:
                         L.ckind_h[slot, q] = (0, pc, 0)
             L.cmap = t(L.cmap_h)
             L.ckind = t(L.ckind_h)
-        # left-looking forward lists (flux boundary slots only): for every separator
-        # slot, the global-cbuf indices of all descendant contributions to its dof,
-        # ordered deeper level first, then node, then slot (vectorised)
+        # ---- compact solve layout over the combined vector [flux coarse dofs | pressures]:
+        # per node F11inv (s x s) then X (b x s) for the whole boundary (flux + pressures).
+        # Left-looking forward lists: for every separator slot (and every pressure) the
+        # cbuf indices of all descendant contributions to it, ordered deeper level
+        # first, then node, then slot (vectorised).
         coff = 0
         gs, srcs = [], []
         for L in self.levels:
-            L.coff = coff
-            Bp = max(L.Bf, 1)
+            L.s = np.array([len(nodes[k]["sep"]) for k in L.ids], dtype=np.int64)
+            L.b = np.array([len(nodes[k]["bnd"]) for k in L.ids], dtype=np.int64)
+            L.cb_off = coff + np.concatenate([[0], np.cumsum(L.b)[:-1]])
             for q, k in enumerate(L.ids):
-                b = nodes[k]["bndf"]
-                if len(b):
-                    gs.append(b)
-                    srcs.append(coff + q * Bp + np.arange(len(b)))
-            coff += L.m * Bp
-        self.cb_total = coff
+                bb = nodes[k]["bnd"]
+                if len(bb):
+                    gs.append(bb)
+                    srcs.append(L.cb_off[q] + np.arange(len(bb)))
+            coff += int(L.b.sum())
+        self.cb_total = max(coff, 1)
         if gs:
             gs = np.concatenate(gs)
             srcs = np.concatenate(srcs)
-            o = np.lexsort((srcs, gs))          # by dof, then by cbuf index (= level/node/slot order)
+            o = np.lexsort((srcs, gs))
             gs, srcs = gs[o], srcs[o]
         else:
             gs = srcs = np.zeros(0, np.int64)
-        for L in self.levels:
-            sep = L.sep_idx_h.ravel()
-            lo = np.searchsorted(gs, sep, side="left")
-            hi = np.searchsorted(gs, sep, side="right")
-            cnt = np.where(sep >= 0, hi - lo, 0)
+
+        def lists(keys):
+            lo = np.searchsorted(gs, keys, side="left")
+            hi = np.searchsorted(gs, keys, side="right")
+            cnt = hi - lo
             ptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
             idx = np.concatenate([np.arange(a_, b_) for a_, b_, c_ in zip(lo, hi, cnt) if c_]) \
                 if cnt.sum() else np.zeros(0, np.int64)
             src = srcs[idx] if len(idx) else np.zeros(1, np.int64)
-            L.lptr = t(ptr)
-            L.lsrc = t(src.astype(np.int32))
+            return ptr, src.astype(np.int32)
+
+        rows_per_task = 32
+        for L in self.levels:
+            sep_flat = np.concatenate([nodes[k]["sep"] for k in L.ids]).astype(np.int64)
+            bnd_flat = np.concatenate([nodes[k]["bnd"] for k in L.ids] + [np.zeros(0, np.int64)])
+            sep_ptr = np.concatenate([[0], np.cumsum(L.s)])
+            bnd_ptr = np.concatenate([[0], np.cumsum(L.b)])
+            data_off = np.concatenate([[0], np.cumsum(L.s * L.s + 2 * L.b * L.s)])
+            L.ysize = int(sep_ptr[-1])
+            L.csize = int(data_off[-1])
+            lptr, lsrc = lists(sep_flat)
+            info = np.stack([L.s, L.b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off], axis=1).astype(np.int32)
+            ft_, bt_ = [], []
+            for q in range(L.m):
+                for r0 in range(0, int(L.s[q] + L.b[q]), rows_per_task):
+                    ft_.append((q, r0))
+                for k0 in range(0, int(L.s[q]), 32):
+                    bt_.append((q, k0))
+            L.info = t(info)
+            L.data_off = t(data_off[:-1].astype(np.int64), torch.int64)
+            L.sep_flat = t(sep_flat.astype(np.int32))
+            L.bnd_flat = t(bnd_flat.astype(np.int32) if len(bnd_flat) else np.zeros(1, np.int32))
+            L.lptr = t(lptr)
+            L.lsrc = t(lsrc)
+            L.ftasks = t(np.array(ft_, dtype=np.int32).reshape(-1, 2))
+            L.btasks = t(np.array(bt_, dtype=np.int32).reshape(-1, 2))
+            L.n_ft, L.n_bt = len(ft_), len(bt_)
+            L.smax = int(L.s.max())
+            L.bmax = int(L.b.max())
+        # pressure gather lists (pressures 1..N-1; subdomain 0 is pinned)
+        pptr, psrc = lists(nfc + np.arange(1, N, dtype=np.int64))
+        self.pptr, self.psrc = t(pptr), t(psrc)
         self.maxC = maxC
         self.factored = False
 
@@ -260,24 +294,41 @@ class CoarseND:
         if int(info.item()):
             raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
         self.factored = True
-        self.bytes = sum(L.m * (L.S * L.S + max(L.Bf, 1) * L.S) * 8 for L in self.levels)
+        for L in self.levels:
+            L.Fc = torch.empty(max(L.csize, 1), dtype=F64, device=self.dev)
+            nat.call("bddc_nd_compact", L.m, L.S, L.nf, L.B, _p(L.F), _p(L.X), _p(L.info),
+                     _p(L.data_off), _p(L.Fc), st)
+        # bytes streamed per solve: F11inv + X (forward) + X^T (backward)
+        self.bytes = sum(L.csize * 8 for L in self.levels)
         return self.levels[-1]
 
-    def solve(self, r, x, ld=None):
-        """x = S_Pi^-1 r (flux dofs); r is read-only."""
+    def release_fronts(self):
+        """Drop the padded factorisation fronts once Pc has been read off the root."""
+        for L in self.levels:
+            L.F = None
+            L.X = None
+
+    def solve(self, r, x, Pcinv, npc):
+        """Pinned coarse solve on the combined vector [flux | pressures] (coarse.py:208-215).
+
+        r, x: length nfc + N.  r is read-only; x[nfc] (subdomain 0) is pinned to 0.
+        """
         st = _stream()
         ys, cb = self._bufs()
         for li, L in enumerate(self.levels):
-            nat.call("bddc_nd_fwd", L.m, L.S, L.Bf, L.nf, L.B * L.S, _p(L.sep_idx), _p(L.lptr),
-                     _p(L.lsrc), _p(L.F), _p(L.X), _p(r), _p(ys[li]), _p(cb), L.coff, st)
+            nat.call("bddc_nd_fwd", L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
+                     _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(ys[li]), _p(cb), st)
+        nat.call("bddc_nd_pressure", self.N, self.nfc, npc, _p(self.pptr), _p(self.psrc), _p(cb),
+                 _p(Pcinv), _p(r), _p(self._prhs), _p(x), st)
         for li in range(len(self.levels) - 1, -1, -1):
             L = self.levels[li]
-            nat.call("bddc_nd_bwd", L.m, L.S, L.Bf, L.B * L.S, _p(L.sep_idx), _p(L.bnd_idx),
-                     _p(L.X), _p(ys[li]), _p(x), st)
+            nat.call("bddc_nd_bwd", L.n_bt, L.bmax, _p(L.btasks), _p(L.info), _p(L.data_off),
+                     _p(L.sep_flat), _p(L.bnd_flat), _p(L.Fc), _p(ys[li]), _p(x), st)
 
     def _bufs(self):
         if getattr(self, "_yb", None) is None:
-            ys = [torch.empty(L.m * L.S, dtype=F64, device=self.dev) for L in self.levels]
-            cb = torch.empty(max(self.cb_total, 1), dtype=F64, device=self.dev)
+            ys = [torch.empty(max(L.ysize, 1), dtype=F64, device=self.dev) for L in self.levels]
+            cb = torch.empty(self.cb_total, dtype=F64, device=self.dev)
             self._yb = (ys, cb)
+            self._prhs = torch.empty(max(self.N, 1), dtype=F64, device=self.dev)
         return self._yb

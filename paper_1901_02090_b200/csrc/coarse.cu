@@ -3,7 +3,8 @@
 // Local pieces per subdomain, via the interface Schur complement S_i:
 //   constrained KKT solve with interface load  <=>  [[S, C^T],[C, 0]]
 //   Kc   = (C S^-1 C^T)^-1            (= Psi^T A Psi, coarse.py:179)
-//   Psi  = S^-1 C^T Kc                (Gamma rows of the coarse basis, coarse.py:166-171)
+//   Psi  = S^-1 C^T Kc                (Gamma rows of the coarse basis, coarse.py:166-171),
+//          stored transposed: PsiT = Kc (S^-1 C^T)^T, maxC x maxG per subdomain
 //   T    = S^-1 - Psi (C S^-1)        (Gamma block of the constrained inverse, coarse.py:237-245)
 //   b0   = 1^T B_loc psi = -D_i sum_q sign_q Psi[q]   (coarse.py:184-185)
 // The global coarse problem (S_Pi and the pinned pressure block) is handled
@@ -56,25 +57,28 @@ __global__ void pad_identity_kernel(int maxC, const int* __restrict__ sub_rows, 
   }
 }
 
-// b0[i][r] = sigma_r * D_i * sum_q (side_q ? -1 : +1) Psi[q][r]
+// b0[i][r] = sigma_r * D_i * sum_q (side_q ? -1 : +1) Psi[q][r]   (warp per row r)
 __global__ void b0_kernel(bddc_geom G, const int* __restrict__ gcode, const int* __restrict__ sub_rows,
-                          const double* __restrict__ Psi, const double* __restrict__ Dsub, int maxC,
+                          const double* __restrict__ PsiT, const double* __restrict__ Dsub, int maxC,
                           double* __restrict__ b0) {
   const int i = blockIdx.x;
   const int mg = G.maxG;
-  for (int r = threadIdx.x; r < maxC; r += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < maxC; r += nw) {
     const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
     double v = 0.0;
     if (sr[0] >= 0) {
-      for (int q = 0; q < mg; ++q) {
+      const double* row = PsiT + ((size_t)i * maxC + r) * mg;
+      for (int q = lane; q < mg; q += 32) {
         int code = gcode[(size_t)i * mg + q];
         if (code < 0) continue;
-        double p = Psi[((size_t)i * mg + q) * maxC + r];
+        double p = row[q];
         v += ((code >> 2) & 1) ? -p : p;
       }
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       v *= Dsub[i] * (double)sr[3];
     }
-    b0[(size_t)i * maxC + r] = v;
+    if (lane == 0) b0[(size_t)i * maxC + r] = v;
   }
 }
 
@@ -117,17 +121,17 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   pad_identity_kernel<<<N, 256, 0, s>>>(maxC, sub_rows, Kc);
   LAUNCH_OK();
   if ((r = bddc_spd_inverse_batched(Kc, maxC, maxC, sCC, N, 32, inv_ws, info, stream))) return r;
-  // Psi = Y Kc
-  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, maxC, 1.0, Y, maxC, sGC, Kc, maxC, sCC, 0.0, Psi, maxC, sGC, N, 0,
+  // PsiT = Kc Y^T   (maxC x maxG)
+  if ((r = bddc_dgemm_batched(0, 1, maxC, mg, maxC, 1.0, Kc, maxC, sCC, Y, maxC, sGC, 0.0, Psi, mg, sGC, N, 0,
                               stream)))
     return r;
-  // T = Sinv - Psi Y^T
+  // T = Sinv - Psi Y^T = Sinv - PsiT^T Y^T
   long long tot = (long long)N * sG;
   copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Sinv, T, tot);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Psi, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+  if ((r = bddc_dgemm_batched(1, 1, mg, mg, maxC, -1.0, Psi, mg, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
     return r;
-  b0_kernel<<<N, 128, 0, s>>>(*g, gcode, sub_rows, Psi, Dsub, maxC, b0);
+  b0_kernel<<<N, 256, 0, s>>>(*g, gcode, sub_rows, Psi, Dsub, maxC, b0);
   LAUNCH_OK();
   return 0;
 }

@@ -52,89 +52,125 @@ __global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K,
   }
 }
 
-// Forward (left-looking): r_sep[k] = r[g_k] - sum of the stored descendant
-// contributions for g_k (fixed order), then y = F11inv r_sep (rows < S) and
-// c = X r_sep (rows S..S+Bf-1) into the level's slice of the global cbuf.
-__global__ void nd_fwd_kernel(int m, int S, int Bf, int nf, long long xstride, const int* __restrict__ sep_idx,
+// Compact per-node solve layout (see coarse_nd.py): info[q] = {s, b, sep_ptr,
+// bnd_ptr, cb_off}; node data at data_off[q]: F11inv (s x s) then X (b x s) over the
+// whole boundary (flux dofs and pressures, indices into the combined vector).
+
+// Forward (left-looking), one task = 32 rows of one node:
+// r_sep[k] = r[g_k] - sum of descendant contributions (fixed list order),
+// rows < s: y = F11inv r_sep; rows s..s+bf-1: c = X r_sep into cbuf.
+__global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
+                              const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
                               const int* __restrict__ lptr, const int* __restrict__ lsrc,
-                              const double* __restrict__ F, const double* __restrict__ X,
-                              const double* __restrict__ r, double* __restrict__ ybuf, double* __restrict__ cbuf,
-                              long long coff, int rows_per_cta) {
-  extern __shared__ double rs[];  // S
-  const int q = blockIdx.x;
-  const int row0 = blockIdx.y * rows_per_cta;
-  const int Bp = Bf > 0 ? Bf : 1;
-  // thread per separator slot; contributions fetched 4 at a time (independent
-  // loads) and added strictly in list order (deterministic)
-  for (int k = threadIdx.x; k < S; k += blockDim.x) {
-    int g = sep_idx[(size_t)q * S + k];
-    double v = 0.0;
-    if (g >= 0) {
-      const int t = q * S + k;
-      int p = lptr[t];
-      const int p1 = lptr[t + 1];
-      double acc = 0.0;
-      for (; p + 4 <= p1; p += 4) {
-        int i0 = lsrc[p], i1 = lsrc[p + 1], i2 = lsrc[p + 2], i3 = lsrc[p + 3];
-        double c0 = cbuf[i0], c1 = cbuf[i1], c2 = cbuf[i2], c3 = cbuf[i3];
-        acc += c0;
-        acc += c1;
-        acc += c2;
-        acc += c3;
-      }
-      for (; p < p1; ++p) acc += cbuf[lsrc[p]];
-      v = r[g] - acc;
+                              const double* __restrict__ Fc, const double* __restrict__ r,
+                              double* __restrict__ ybuf, double* __restrict__ cbuf) {
+  extern __shared__ double rs[];
+  const int q = tasks[2 * blockIdx.x], row0 = tasks[2 * blockIdx.x + 1];
+  const int s = info[5 * q], bf = info[5 * q + 1], sp = info[5 * q + 2], cbo = info[5 * q + 4];
+  for (int k = threadIdx.x; k < s; k += blockDim.x) {
+    const int t = sp + k;
+    int p = lptr[t];
+    const int p1 = lptr[t + 1];
+    double acc = 0.0;
+    for (; p + 4 <= p1; p += 4) {
+      int i0 = lsrc[p], i1 = lsrc[p + 1], i2 = lsrc[p + 2], i3 = lsrc[p + 3];
+      double c0 = cbuf[i0], c1 = cbuf[i1], c2 = cbuf[i2], c3 = cbuf[i3];
+      acc += c0;
+      acc += c1;
+      acc += c2;
+      acc += c3;
     }
-    rs[k] = v;
+    for (; p < p1; ++p) acc += cbuf[lsrc[p]];
+    rs[k] = r[sep_flat[t]] - acc;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nrows = S + Bf;
-  for (int row = row0 + warp; row < imin(row0 + rows_per_cta, nrows); row += nw) {
-    const double* mr = (row < S) ? F + (size_t)q * nf * nf + (size_t)row * nf
-                                 : X + (size_t)q * xstride + (size_t)(row - S) * S;
+  const double* base = Fc + data_off[q];
+  const int nrows = imin(row0 + 32, s + bf);
+  for (int row = row0 + warp; row < nrows; row += nw) {
+    const double* mr = base + (size_t)row * s;   // F11inv rows then X rows, both of length s
     double acc = 0.0;
-    for (int c = lane; c < S; c += 32) acc += mr[c] * rs[c];
+    for (int c = lane; c < s; c += 32) acc += mr[c] * rs[c];
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-      if (row < S) ybuf[(size_t)q * S + row] = acc;
-      else cbuf[coff + (size_t)q * Bp + (row - S)] = acc;
+      if (row < s) ybuf[sp + row] = acc;
+      else cbuf[cbo + row - s] = acc;
     }
   }
 }
 
-// Backward: x_sep = y - X^T x_bnd.  CTA = 32 separator columns; the 8 warps
-// split the boundary rows and their partial sums are added in warp order.
-__global__ void nd_bwd_kernel(int m, int S, int Bf, long long xstride, const int* __restrict__ sep_idx,
-                              const int* __restrict__ bnd_idx, const double* __restrict__ X,
+// Backward, one task = 32 separator rows of one node: x_sep = y - X^T x_bnd with
+// X^T stored row-major (s x b) after X, so every warp streams whole rows.
+__global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
+                              const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
+                              const int* __restrict__ bnd_flat, const double* __restrict__ Fc,
                               const double* __restrict__ ybuf, double* __restrict__ x) {
-  extern __shared__ double xb[];  // Bf, then 8 x 32 partials
-  const int q = blockIdx.x;
-  const int k0 = blockIdx.y * 32;
-  const int Bp = Bf > 0 ? Bf : 1;
-  double* part = xb + Bp;
-  for (int mm = threadIdx.x; mm < Bf; mm += blockDim.x) {
-    int g = bnd_idx[(size_t)q * Bp + mm];
-    xb[mm] = (g >= 0) ? x[g] : 0.0;
-  }
+  extern __shared__ double xb[];  // bmax
+  const int q = tasks[2 * blockIdx.x], k0 = tasks[2 * blockIdx.x + 1];
+  const int s = info[5 * q], b = info[5 * q + 1], sp = info[5 * q + 2], bp = info[5 * q + 3];
+  for (int m = threadIdx.x; m < b; m += blockDim.x) xb[m] = x[bnd_flat[bp + m]];
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = k0 + lane;
-  double acc = 0.0;
-  if (k < S) {
-    const double* Xq = X + (size_t)q * xstride + k;
-    for (int mm = warp; mm < Bf; mm += 8) acc += Xq[(size_t)mm * S] * xb[mm];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* XT = Fc + data_off[q] + (size_t)s * s + (size_t)b * s;
+  const int kend = imin(k0 + 32, s);
+  for (int k = k0 + warp; k < kend; k += nw) {
+    const double* row = XT + (size_t)k * b;
+    double acc = 0.0;
+    for (int m = lane; m < b; m += 32) acc += row[m] * xb[m];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[sep_flat[sp + k]] = ybuf[sp + k] - acc;
   }
-  part[warp * 32 + lane] = acc;
-  __syncthreads();
-  if (warp == 0 && k < S) {
-    int g = sep_idx[(size_t)q * S + k];
-    if (g >= 0) {
-      double t = 0.0;
-      for (int w = 0; w < 8; ++w) t += part[w * 32 + lane];
-      x[g] = ybuf[(size_t)q * S + k] - t;
+}
+
+// Copy the padded fronts' F11inv and X blocks into the compact layout
+// (F11inv s x s, X b x s, X^T s x b).
+__global__ void nd_compact_kernel(int S, int nf, int B, const double* __restrict__ F, const double* __restrict__ X,
+                                  const int* __restrict__ info, const long long* __restrict__ data_off,
+                                  double* __restrict__ Fc) {
+  const int q = blockIdx.y;
+  const int s = info[5 * q], b = info[5 * q + 1];
+  double* out = Fc + data_off[q];
+  const long long ss = (long long)s * s, bs = (long long)b * s;
+  const long long tot = ss + 2 * bs;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    if (e < ss) {
+      int rr = (int)(e / s), cc = (int)(e % s);
+      out[e] = F[(size_t)q * nf * nf + (size_t)rr * nf + cc];
+    } else if (e < ss + bs) {
+      long long e2 = e - ss;
+      int j = (int)(e2 / s), cc = (int)(e2 % s);
+      out[e] = X[(size_t)q * B * S + (size_t)j * S + cc];
+    } else {
+      long long e2 = e - ss - bs;
+      int k = (int)(e2 / b), j = (int)(e2 % b);
+      out[e] = X[(size_t)q * B * S + (size_t)j * S + k];
     }
   }
+}
+
+// Root pressure block of the pinned coarse system: rp[i] = r_p[i] - contributions
+// (i >= 1), then x_p = -Pc^{-1} rp (the root update block is -Pc); x_p[0] = 0.
+__global__ void nd_pressure_gather_kernel(int N, int nfc, const int* __restrict__ pptr, const int* __restrict__ psrc,
+                                          const double* __restrict__ cbuf, const double* __restrict__ r,
+                                          double* __restrict__ rp) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N - 1) return;
+  double acc = 0.0;
+  for (int p = pptr[i]; p < pptr[i + 1]; ++p) acc += cbuf[psrc[p]];
+  rp[i] = r[nfc + 1 + i] - acc;
+}
+
+__global__ void nd_pressure_gemv_kernel(int N, int nfc, int npc, const double* __restrict__ Pcinv,
+                                        const double* __restrict__ rp, double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row == 0 && lane == 0) x[nfc] = 0.0;
+  if (row >= N - 1) return;
+  const double* mr = Pcinv + (size_t)row * npc;
+  double acc = 0.0;
+  for (int c = lane; c < N - 1; c += 32) acc += mr[c] * rp[c];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) x[nfc + 1 + row] = -acc;
 }
 
 // Pc[(i-1),(j-1)] = -U_root[i][j] (i, j >= 1): the pinned pressure Schur complement;
@@ -208,25 +244,47 @@ extern "C" int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, co
   return 0;
 }
 
-extern "C" int bddc_nd_fwd(int m, int S, int Bf, int nf, long long xstride, const int* sep_idx, const int* lptr,
-                           const int* lsrc, const double* F, const double* X, const double* r, double* ybuf,
-                           double* cbuf, long long coff, void* stream) {
-  const int rows_per_cta = 32;
-  dim3 g(m, (S + Bf + rows_per_cta - 1) / rows_per_cta);
-  size_t shm = (size_t)S * sizeof(double);
+extern "C" int bddc_nd_fwd(int ntasks, int smax, const int* tasks, const int* info, const long long* data_off,
+                           const int* sep_flat, const int* lptr, const int* lsrc, const double* Fc, const double* r,
+                           double* ybuf, double* cbuf, void* stream) {
+  if (ntasks <= 0) return 0;
+  size_t shm = (size_t)(smax > 0 ? smax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_fwd_kernel<<<g, 256, shm, (cudaStream_t)stream>>>(m, S, Bf, nf, xstride, sep_idx, lptr, lsrc, F, X, r, ybuf, cbuf,
-                                                       coff, rows_per_cta);
+  nd_fwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, lptr, lsrc, Fc, r, ybuf,
+                                                            cbuf);
   LAUNCH_OK();
   return 0;
 }
 
-extern "C" int bddc_nd_bwd(int m, int S, int Bf, long long xstride, const int* sep_idx, const int* bnd_idx,
-                           const double* X, const double* ybuf, double* x, void* stream) {
-  dim3 g(m, (S + 31) / 32);
-  size_t shm = ((size_t)(Bf > 0 ? Bf : 1) + 8 * 32) * sizeof(double);
+extern "C" int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const int* psrc, const double* cbuf,
+                                const double* Pcinv, const double* r, double* rp, double* x, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (N < 2) {
+    if (N == 1) CUDA_OK(cudaMemsetAsync(x + nfc, 0, sizeof(double), s));
+    return 0;
+  }
+  nd_pressure_gather_kernel<<<(N - 1 + 255) / 256, 256, 0, s>>>(N, nfc, pptr, psrc, cbuf, r, rp);
+  LAUNCH_OK();
+  nd_pressure_gemv_kernel<<<(N - 1 + 7) / 8 + 1, 256, 0, s>>>(N, nfc, npc, Pcinv, rp, x);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_nd_bwd(int ntasks, int bfmax, const int* tasks, const int* info, const long long* data_off,
+                           const int* sep_flat, const int* bnd_flat, const double* Fc, const double* ybuf, double* x,
+                           void* stream) {
+  if (ntasks <= 0) return 0;
+  size_t shm = (size_t)(bfmax > 0 ? bfmax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_bwd_kernel<<<g, 256, shm, (cudaStream_t)stream>>>(m, S, Bf, xstride, sep_idx, bnd_idx, X, ybuf, x);
+  nd_bwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, bnd_flat, Fc, ybuf, x);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
+                               const long long* data_off, double* Fc, void* stream) {
+  dim3 g(64, m);
+  nd_compact_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(S, nf, B, F, X, info, data_off, Fc);
   LAUNCH_OK();
   return 0;
 }

@@ -37,9 +37,108 @@ __global__ void gather_gemv_kernel(int maxG, const int* __restrict__ nG, const i
   }
 }
 
-// v[i][r] = sum_q Psi[i][q][r] * win[i][q] * x[gpos[i][q]]
+// ---------------------------------------------------------------------------
+// Symmetric interface matrices (S_i, T_i) in tile-packed upper storage:
+// 32x32 row-major tiles (bi <= bj), tile index t(bi,bj) = bi*nt - bi(bi-1)/2 + bj-bi,
+// nt = maxG/32.  Only ceil(nG_i/32) block rows are live; this halves the bytes
+// streamed per GEMV compared with full storage.
+
+__device__ __forceinline__ int tile_index(int bi, int bj, int nt) { return bi * nt - (bi * (bi - 1)) / 2 + (bj - bi); }
+
+__global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, double* __restrict__ packed) {
+  const int i = blockIdx.y;
+  const int nt = maxG / 32;
+  const int ntiles = nt * (nt + 1) / 2;
+  const double* F = full + (size_t)i * maxG * maxG;
+  double* Pk = packed + (size_t)i * ntiles * 1024;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)ntiles * 1024;
+       e += (long long)gridDim.x * blockDim.x) {
+    int t = (int)(e / 1024), w = (int)(e % 1024);
+    // invert tile index
+    int bi = 0;
+    while (bi + 1 < nt && tile_index(bi + 1, bi + 1, nt) <= t) ++bi;
+    int bj = bi + (t - tile_index(bi, bi, nt));
+    int r = bi * 32 + w / 32, c = bj * 32 + w % 32;
+    Pk[e] = F[(size_t)r * maxG + c];
+  }
+}
+
+// y_b[i][q] = sum_c M_i[q][c] * win[i][c] * x[gpos[i][c]] from tile-packed symmetric M_i.
+// Each warp streams whole tiles (coalesced rows), forms the column contribution in
+// registers and the row contribution with a 31-shuffle transpose-reduction; per-tile
+// partials are combined per output block in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) gather_symv_kernel(int maxG, const int* __restrict__ nG,
+                                                         const int* __restrict__ gpos,
+                                                         const double* __restrict__ packed,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ win, double* __restrict__ yb) {
+  extern __shared__ double sm[];
+  const int i = blockIdx.x;
+  const int n = nG[i];
+  const int nt = maxG / 32;
+  const int ntl = (n + 31) / 32;
+  const int ntiles = nt * (nt + 1) / 2;
+  double* xs = sm;                       // maxG
+  double* rowp = xs + maxG;              // ntiles x 32
+  double* colp = rowp + (size_t)ntiles * 32;  // ntiles x 32
+  for (int c = threadIdx.x; c < ntl * 32; c += blockDim.x) {
+    double v = 0.0;
+    if (c < n) {
+      v = x[gpos[(size_t)i * maxG + c]];
+      if (win) v *= win[(size_t)i * maxG + c];
+    }
+    xs[c] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Pk = packed + (size_t)i * ntiles * 1024;
+  const int nlive = ntl * (ntl + 1) / 2;
+  for (int u = warp; u < nlive; u += nw) {
+    // enumerate live tiles (bi <= bj < ntl) in row-major order
+    int bi = 0, rem = u;
+    while (rem >= ntl - bi) {
+      rem -= ntl - bi;
+      ++bi;
+    }
+    const int bj = bi + rem;
+    const double* T = Pk + (size_t)tile_index(bi, bj, nt) * 1024;
+    const double xl = xs[bj * 32 + lane];
+    double v[32];
+    double col = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      double a = T[r * 32 + lane];
+      v[r] = a * xl;
+      col += a * xs[bi * 32 + r];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const bool up = lane & off;
+#pragma unroll
+      for (int k = 0; k < off; ++k) {
+        double send = up ? v[k] : v[k + off];
+        double recv = __shfl_xor_sync(0xffffffffu, send, off);
+        v[k] = (up ? v[k + off] : v[k]) + recv;
+      }
+    }
+    const int t = tile_index(bi, bj, nt);
+    rowp[(size_t)t * 32 + lane] = v[0];
+    colp[(size_t)t * 32 + lane] = (bi != bj) ? col : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ntl * 32; e += blockDim.x) {
+    const int b = e / 32, l = e % 32;
+    if (e >= n) continue;
+    double acc = 0.0;
+    for (int bj = b; bj < ntl; ++bj) acc += rowp[(size_t)tile_index(b, bj, nt) * 32 + l];
+    for (int bi = 0; bi < b; ++bi) acc += colp[(size_t)tile_index(bi, b, nt) * 32 + l];
+    yb[(size_t)i * maxG + e] = acc;
+  }
+}
+
+// v[i][r] = sum_q PsiT[i][r][q] * win[i][q] * x[gpos[i][q]]   (warp per coarse row r)
 __global__ void gather_gemv_t_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ nC,
-                                     const int* __restrict__ gpos, const double* __restrict__ Psi,
+                                     const int* __restrict__ gpos, const double* __restrict__ PsiT,
                                      const double* __restrict__ x, const double* __restrict__ win,
                                      double* __restrict__ v) {
   extern __shared__ double xs[];
@@ -51,12 +150,16 @@ __global__ void gather_gemv_t_kernel(int maxG, int maxC, const int* __restrict__
     xs[c] = t;
   }
   __syncthreads();
-  const double* Pi = Psi + (size_t)i * maxG * maxC;
-  for (int r = threadIdx.x; r < maxC; r += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Pi = PsiT + (size_t)i * maxC * maxG;
+  for (int r = warp; r < maxC; r += nw) {
     double acc = 0.0;
-    if (r < nc)
-      for (int q = 0; q < n; ++q) acc += Pi[(size_t)q * maxC + r] * xs[q];
-    v[(size_t)i * maxC + r] = acc;
+    if (r < nc) {
+      const double* row = Pi + (size_t)r * maxG;
+      for (int q = lane; q < n; q += 32) acc += row[q] * xs[q];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    }
+    if (lane == 0) v[(size_t)i * maxC + r] = acc;
   }
 }
 
@@ -68,31 +171,26 @@ __global__ void coarse_restrict_kernel(int nfc, const int* __restrict__ cown, co
   rhs[g] = v[cown[2 * g]] - v[cown[2 * g + 1]];
 }
 
-// out_b[i][q] = wout[i][q] * (y_b[i][q] + sum_r Psi[i][q][r] sigma_r xc[g_r])
-__global__ void prolong_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ sub_rows,
-                               const double* __restrict__ Psi, const double* __restrict__ xc,
-                               const double* __restrict__ yb, const double* __restrict__ wout,
-                               double* __restrict__ outb) {
+// out_b[i][q] = wout[i][q] * (y_b[i][q] + sum_r PsiT[i][r][q] sigma_r xc[g_r])   (thread per slot q)
+__global__ void prolong_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ nC,
+                               const int* __restrict__ sub_rows, const double* __restrict__ PsiT,
+                               const double* __restrict__ xc, const double* __restrict__ yb,
+                               const double* __restrict__ wout, double* __restrict__ outb) {
   extern __shared__ double cf[];
   const int i = blockIdx.x;
-  const int n = nG[i];
-  for (int r = threadIdx.x; r < maxC; r += blockDim.x) {
+  const int n = nG[i], nc = nC[i];
+  for (int r = threadIdx.x; r < nc; r += blockDim.x) {
     const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
-    cf[r] = (sr[0] >= 0) ? (double)sr[3] * xc[sr[0]] : 0.0;
+    cf[r] = (double)sr[3] * xc[sr[0]];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* Pi = Psi + (size_t)i * maxG * maxC;
-  for (int q = warp; q < n; q += nw) {
-    const double* row = Pi + (size_t)q * maxC;
+  const double* Pi = PsiT + (size_t)i * maxC * maxG;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) {
     double acc = 0.0;
-    for (int r = lane; r < maxC; r += 32) acc += row[r] * cf[r];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      size_t s = (size_t)i * maxG + q;
-      double w = yb ? yb[s] + acc : acc;
-      outb[s] = wout ? wout[s] * w : w;
-    }
+    for (int r = 0; r < nc; ++r) acc += Pi[(size_t)r * maxG + q] * cf[r];
+    size_t s = (size_t)i * maxG + q;
+    double w = yb ? yb[s] + acc : acc;
+    outb[s] = wout ? wout[s] * w : w;
   }
 }
 
@@ -354,9 +452,33 @@ extern "C" int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos,
   return 0;
 }
 
+extern "C" size_t bddc_sym_packed_elems(int maxG) {
+  int nt = maxG / 32;
+  return (size_t)nt * (nt + 1) / 2 * 1024;
+}
+
+extern "C" int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream) {
+  if (maxG % 32) return bddc_set_error(BDDC_ERR_ARG, "pack_sym: maxG must be a multiple of 32");
+  dim3 g(64, N);
+  pack_sym_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(maxG, full, packed);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                                const double* x, const double* win, double* yb, void* stream) {
+  int nt = maxG / 32;
+  size_t shm = ((size_t)maxG + (size_t)nt * (nt + 1) * 32) * sizeof(double);
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(gather_symv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  gather_symv_kernel<<<N, 256, shm, (cudaStream_t)stream>>>(maxG, nG, gpos, packed, x, win, yb);
+  LAUNCH_OK();
+  return 0;
+}
+
 extern "C" int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,
-                                  const double* Psi, const double* x, const double* win, double* v, void* stream) {
-  gather_gemv_t_kernel<<<N, 128, maxG * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, gpos, Psi, x,
+                                  const double* PsiT, const double* x, const double* win, double* v, void* stream) {
+  gather_gemv_t_kernel<<<N, 256, maxG * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, gpos, PsiT, x,
                                                                                   win, v);
   LAUNCH_OK();
   return 0;
@@ -369,10 +491,11 @@ extern "C" int bddc_coarse_restrict(int nfc, const int* cown, const double* v, d
   return 0;
 }
 
-extern "C" int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* sub_rows, const double* Psi,
-                            const double* xc, const double* yb, const double* wout, double* outb, void* stream) {
-  prolong_kernel<<<N, 256, maxC * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, sub_rows, Psi, xc, yb,
-                                                                          wout, outb);
+extern "C" int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* nC, const int* sub_rows,
+                            const double* PsiT, const double* xc, const double* yb, const double* wout, double* outb,
+                            void* stream) {
+  prolong_kernel<<<N, 128, maxC * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc,
+                                                                          yb, wout, outb);
   LAUNCH_OK();
   return 0;
 }

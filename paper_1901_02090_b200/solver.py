@@ -117,7 +117,7 @@ class BddcSetup:
       Q[i]    = P_i^+  pressure-Schur pseudo-inverse   (interior solves)
       S[i]    = interface Schur complement              (operator)
       T[i]    = Gamma block of the constrained inverse  (preconditioner)
-      Psi[i]  = Gamma rows of the coarse basis          (restriction/prolongation)
+      PsiT[i] = Gamma rows of the coarse basis, transposed (restriction/prolongation)
     and the explicit coarse operators Mc (flux block of the pinned coarse
     inverse) and Wq (pressure-rhs -> coarse flux, solve step 1).
     """
@@ -260,6 +260,13 @@ class BddcSetup:
                  _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws),
                  _p(info[2:]), st)
         del Ct, Y, ws, Sinv
+        # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
+        npk = nat.load().bddc_sym_packed_elems(mg)
+        self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
+        self.d_Tp = torch.empty(N * npk, dtype=F64, device=dev)
+        nat.call("bddc_pack_sym", N, mg, _p(self.d_S), _p(self.d_Sp), st)
+        nat.call("bddc_pack_sym", N, mg, _p(self.d_T), _p(self.d_Tp), st)
+        del self.d_S, self.d_T
         self._mark(ev, "coarse_local")
         # global coarse: multifrontal S_Pi (nested dissection) + pinned pressure Schur Pc
         nfc = self.n_flux_coarse
@@ -272,6 +279,7 @@ class BddcSetup:
             self.nd = CoarseND(dec, per_face, cstart, self.sub_rows, self.nC, maxC, dev)
             root = self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
             self._build_pressure_schur(root)
+            self.nd.release_fronts()
         bad = info.cpu().numpy()
         if bad[0] or bad[1]:
             raise NumericalFailureError("local interior factorization failed", where=None)
@@ -285,14 +293,10 @@ class BddcSetup:
         self.w_yb = z(N * mg)
         self.w_yb2 = z(N * mg)
         self.w_v = z(N * maxC)
-        self.w_crhs = z(self.npad)
-        self.w_xc = z(self.npad)
+        self.w_rc = z(self.nfc + N)     # combined coarse rhs [flux | pressures]
+        self.w_xc = z(self.nfc + N)     # combined coarse solution
         self.w_phi = z(N)
         self.w_z = z(N)
-        self.w_c1 = z(self.npad)
-        self.w_x1 = z(self.npad)
-        self.w_t = z(self.npc)
-        self.w_pz = z(self.npc)
         self.w_dot = torch.zeros(nat.load().bddc_dot_workspace() // 8 + 1, dtype=F64, device=dev)
         self.w_scal = z(16)
         self.d_dct = torch.empty(sum(n * n + n for n in dec.n3), dtype=F64, device=dev)
@@ -410,28 +414,9 @@ class BddcSetup:
                 "coarse problem singular; initial constraints do not cover all faces")
         self.d_Pcinv = Pc
 
-    def _coarse_flux_solve(self, rhs, out):
-        """out = flux block of the pinned coarse inverse applied to rhs (r_q = 0)."""
-        st = _stream()
-        self.nd.solve(rhs, self.w_x1, ld=self.nfc)
-        if self.N > 1:
-            nat.call("bddc_b0_apply", self.N, self.maxC, _p(self.d_sub_rows), _p(self.d_b0),
-                     _p(self.w_x1), self.nfc, 1, _p(self.w_t), self.npc, st)
-            nat.call("bddc_gemv", self.N - 1, self.npc, self.N - 1, _p(self.d_Pcinv),
-                     _p(self.w_t), _p(self.w_pz), st)
-            nat.call("bddc_b0t_apply", self.nfc, self.maxC, _p(self.d_cown), _p(self.d_b0),
-                     _p(self.w_pz), self.npc, 1, -1.0, _p(rhs), self.nfc, st)
-        self.nd.solve(rhs, out, ld=self.nfc)
-
-    def _coarse_pressure_solve(self, rq1, out):
-        """Step 1 (solver.py:318-319): flux part of the pinned solve with rhs (0, r_q)."""
-        st = _stream()
-        nat.call("bddc_gemv", self.N - 1, self.npc, self.N - 1, _p(self.d_Pcinv), _p(rq1),
-                 _p(self.w_pz), st)
-        nat.call("bddc_fill", self.nfc, 0.0, _p(self.w_c1), st)
-        nat.call("bddc_b0t_apply", self.nfc, self.maxC, _p(self.d_cown), _p(self.d_b0),
-                 _p(self.w_pz), self.npc, 1, 1.0, _p(self.w_c1), self.nfc, st)
-        self.nd.solve(self.w_c1, out, ld=self.nfc)
+    def _coarse_solve(self):
+        """Pinned coarse solve w_xc = K0^-1 w_rc on [flux | pressures] (coarse.py:208-215)."""
+        self.nd.solve(self.w_rc, self.w_xc, self.d_Pcinv, self.npc)
 
     # ----------------------------------------- interface operator (device)
 
@@ -442,8 +427,8 @@ class BddcSetup:
         if kt is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_S), _p(x), None, _p(self.w_yb), st)
+        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_Sp), _p(x), None, _p(self.w_yb), st)
         if kt is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -464,32 +449,33 @@ class BddcSetup:
     def _precond(self, r, out):
         """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged."""
         st = _stream()
-        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_T), _p(r), _p(self.d_delta), _p(self.w_yb), st)
+        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_Tp), _p(r), _p(self.d_delta), _p(self.w_yb), st)
         if self.nfc:
             nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
                      _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
                      _p(self.d_delta), _p(self.w_v), st)
             nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
-                     _p(self.w_crhs), st)
-            self._coarse_flux_solve(self.w_crhs, self.w_xc)
-        nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                     _p(self.w_rc), st)
+            nat.call("bddc_fill", self.N, 0.0, _p(self.w_rc[self.nfc:]), st)
+            self._coarse_solve()
+        nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG), _p(self.d_nC),
                  _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
                  _p(self.d_delta), _p(self.w_yb2), st)
         nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
 
     def time_kernel(self, which="S", reps=20):
         """Mean device time (s) of one interface GEMV launch (bench roofline helper)."""
-        mats = {"S": self.d_S, "T": self.d_T}[which]
+        mats = {"S": self.d_Sp, "T": self.d_Tp}[which]
         x = torch.ones(max(self.n_gamma, 1), dtype=F64, device=self.dev)
         st = _stream()
-        nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                  _p(mats), _p(x), None, _p(self.w_yb), st)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(reps):
-            nat.call("bddc_gather_gemv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+            nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                      _p(mats), _p(x), None, _p(self.w_yb), st)
         b.record()
         b.synchronize()
@@ -514,10 +500,19 @@ class BddcSetup:
         return xd.cpu().numpy()
 
     def schur_dense(self, i):
-        """Dense S_i (n_Gamma_i x n_Gamma_i), substructure.py:90-99."""
+        """Dense S_i (n_Gamma_i x n_Gamma_i), substructure.py:90-99 (unpacked from tiles)."""
         n = int(self.dec.nG[i])
-        S = self.d_S.view(self.N, self.maxG, self.maxG)[i, :n, :n]
-        return S.cpu().numpy()
+        nt = self.maxG // 32
+        npk = nt * (nt + 1) // 2 * 1024
+        tiles = self.d_Sp[i * npk:(i + 1) * npk].view(-1, 32, 32).cpu().numpy()
+        full = np.zeros((self.maxG, self.maxG))
+        t = 0
+        for bi in range(nt):
+            for bj in range(bi, nt):
+                full[bi * 32:(bi + 1) * 32, bj * 32:(bj + 1) * 32] = tiles[t]
+                full[bj * 32:(bj + 1) * 32, bi * 32:(bi + 1) * 32] = tiles[t].T
+                t += 1
+        return full[:n, :n]
 
     def net_flux_matrix(self):
         import scipy.sparse as sp
@@ -634,9 +629,12 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     # step 1: rq_i = sum fs over cells of i; x0 = Wq rq[1:]; g = average(Psi x0)
     nat.call("bddc_sub_sum", gp, _p(W.fs), _p(W.rq), 1.0, None, st)
     if setup.nfc and N > 1:
-        setup._coarse_pressure_solve(W.rq[1:], W.x0)
+        nat.call("bddc_fill", setup.nfc, 0.0, _p(setup.w_rc), st)
+        nat.call("bddc_axpby", N, 1.0, _p(W.rq), 0.0, _p(setup.w_rc[setup.nfc:]), st)
+        setup._coarse_solve()
+        nat.call("bddc_axpby", setup.nfc, 1.0, _p(setup.w_xc), 0.0, _p(W.x0), st)
     if ng:
-        nat.call("bddc_prolong", N, setup.maxG, setup.maxC, _p(setup.d_nG),
+        nat.call("bddc_prolong", N, setup.maxG, setup.maxC, _p(setup.d_nG), _p(setup.d_nC),
                  _p(setup.d_sub_rows), _p(setup.d_Psi), _p(W.x0), None,
                  _p(setup.d_delta), _p(setup.w_yb2), st)
         nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb2), _p(W.g), st)
