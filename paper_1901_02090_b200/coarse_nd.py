@@ -56,71 +56,97 @@ class _Level:
     pass
 
 
+def nd_geometry(dec):
+    """Nested-dissection tree of the subdomain grid in face ids (cached on `dec`).
+
+    Node: dict(leaf, depth, sub | sep (face ids), bnd (face ids), pres (subdomain ids), ch).
+    """
+    cached = getattr(dec, "_nd_geometry", None)
+    if cached is not None:
+        return cached
+    S3 = dec.S3
+    ft = dec.face_table
+    fkey = {}
+    for f in range(dec.n_faces):
+        i, a = int(ft[f, 0]), int(ft[f, 2])
+        s = dec.sub_strip[i]
+        t = [d for d in range(3) if d != a]
+        fkey[(a, int(s[a]) + 1, int(s[t[0]]), int(s[t[1]]))] = f
+
+    def plane_faces(a, plane, lo, hi):
+        t = [d for d in range(3) if d != a]
+        return [fkey[(a, plane, u, v)] for v in range(lo[t[1]], hi[t[1]])
+                for u in range(lo[t[0]], hi[t[0]])]
+
+    def box_subs(lo, hi):
+        z, y, x = np.meshgrid(np.arange(lo[2], hi[2]), np.arange(lo[1], hi[1]),
+                              np.arange(lo[0], hi[0]), indexing="ij")
+        return np.sort((x + S3[0] * (y + S3[1] * z)).ravel())
+
+    nodes = []
+
+    def rec(lo, hi, depth):
+        idx = len(nodes)
+        nodes.append(None)
+        ext = [hi[a] - lo[a] for a in range(3)]
+        if all(e == 1 for e in ext):
+            nodes[idx] = dict(leaf=True, sub=int(lo[0] + S3[0] * (lo[1] + S3[1] * lo[2])),
+                              depth=depth)
+            return idx
+        bnd = []
+        for a in range(3):
+            for plane in (lo[a], hi[a]):
+                if 0 < plane < S3[a]:
+                    bnd += plane_faces(a, plane, lo, hi)
+        a = int(np.argmax(ext))
+        mid = lo[a] + ext[a] // 2
+        sep = plane_faces(a, mid, lo, hi)
+        h1 = list(hi)
+        h1[a] = mid
+        l2 = list(lo)
+        l2[a] = mid
+        c1 = rec(lo, tuple(h1), depth + 1)
+        c2 = rec(tuple(l2), hi, depth + 1)
+        nodes[idx] = dict(leaf=False, depth=depth, sep=np.array(sep, dtype=np.int64),
+                          bnd=np.array(bnd, dtype=np.int64), pres=box_subs(lo, hi), ch=(c1, c2))
+        return idx
+
+    if dec.n_subdomains > 1:
+        rec((0, 0, 0), tuple(S3), 0)
+    dec._nd_geometry = nodes
+    return nodes
+
+
 class CoarseND:
     """Symbolic analysis (host, index tables only) + numeric factorisation (device)."""
 
     def __init__(self, dec, per_face, cstart, sub_rows, nC, maxC, dev):
         self.dev = dev
-        S3 = dec.S3
-        ft = dec.face_table
-        nfaces = dec.n_faces
         N = dec.n_subdomains
         self.N = N
+        nfaces = dec.n_faces
         self.nfc = nfc = int(per_face.sum()) if nfaces else 0
-        fkey = {}
-        for f in range(nfaces):
-            i, a = int(ft[f, 0]), int(ft[f, 2])
-            s = dec.sub_strip[i]
-            t = [d for d in range(3) if d != a]
-            fkey[(a, int(s[a]) + 1, int(s[t[0]]), int(s[t[1]]))] = f
+        per_face = np.asarray(per_face, dtype=np.int64)
+        cstart = np.asarray(cstart, dtype=np.int64)
 
         def face_dofs(fl):
-            if not fl:
+            if len(fl) == 0:
                 return np.zeros(0, dtype=np.int64)
-            return np.concatenate([cstart[f] + np.arange(per_face[f]) for f in fl])
+            cnt = per_face[fl]
+            tot = int(cnt.sum())
+            first = np.cumsum(cnt) - cnt
+            return np.repeat(cstart[fl] - first, cnt) + np.arange(tot)
 
-        def plane_faces(a, plane, lo, hi):
-            t = [d for d in range(3) if d != a]
-            return [fkey[(a, plane, u, v)] for v in range(lo[t[1]], hi[t[1]])
-                    for u in range(lo[t[0]], hi[t[0]])]
-
-        def box_subs(lo, hi):
-            z, y, x = np.meshgrid(np.arange(lo[2], hi[2]), np.arange(lo[1], hi[1]),
-                                  np.arange(lo[0], hi[0]), indexing="ij")
-            return np.sort((x + S3[0] * (y + S3[1] * z)).ravel())
-
+        # geometry-only tree (cached on the decomposition), expanded to coarse dofs here
+        geo = nd_geometry(dec) if (N > 1 and nfc) else []
         nodes = []
-
-        def rec(lo, hi, depth):
-            idx = len(nodes)
-            nodes.append(None)
-            ext = [hi[a] - lo[a] for a in range(3)]
-            bnd = []
-            for a in range(3):
-                for plane in (lo[a], hi[a]):
-                    if 0 < plane < S3[a]:
-                        bnd += plane_faces(a, plane, lo, hi)
-            if all(e == 1 for e in ext):
-                sub = lo[0] + S3[0] * (lo[1] + S3[1] * lo[2])
-                nodes[idx] = dict(leaf=True, sub=int(sub), depth=depth)
-                return idx
-            a = int(np.argmax(ext))
-            mid = lo[a] + ext[a] // 2
-            sep = plane_faces(a, mid, lo, hi)
-            h1 = list(hi)
-            h1[a] = mid
-            l2 = list(lo)
-            l2[a] = mid
-            c1 = rec(lo, tuple(h1), depth + 1)
-            c2 = rec(tuple(l2), hi, depth + 1)
-            bf = face_dofs(bnd)
-            pres = nfc + box_subs(lo, hi)
-            nodes[idx] = dict(leaf=False, depth=depth, sep=face_dofs(sep), bndf=bf,
-                              bnd=np.concatenate([bf, pres]), ch=(c1, c2))
-            return idx
-
-        if N > 1 and nfc:
-            rec((0, 0, 0), tuple(S3), 0)
+        for gn in geo:
+            if gn["leaf"]:
+                nodes.append(dict(leaf=True, sub=gn["sub"], depth=gn["depth"]))
+            else:
+                bf = face_dofs(gn["bnd"])
+                nodes.append(dict(leaf=False, depth=gn["depth"], sep=face_dofs(gn["sep"]), bndf=bf,
+                                  bnd=np.concatenate([bf, nfc + gn["pres"]]), ch=gn["ch"]))
         self.nodes = nodes
         internal = [k for k, n in enumerate(nodes) if not n["leaf"]]
         depths = sorted({nodes[k]["depth"] for k in internal}, reverse=True)

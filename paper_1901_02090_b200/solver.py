@@ -528,15 +528,12 @@ class BddcSetup:
                              shape=(dec.n_subdomains, dec.n_gamma)).tocsr()
 
 
-def _suggest_scaling(setup):
-    """solver.py:286-298 (warning only): aligned coefficient jumps."""
-    if setup.config.scaling != "multiplicity":
-        return
-    dec = setup.dec
-    if not dec.n_gamma or not dec.n_faces:
-        return
+def _face_cells(dec):
+    """Per interface dof: low / high neighbour cell, grouped by face (cached on dec)."""
+    cached = getattr(dec, "_face_cells_cache", None)
+    if cached is not None:
+        return cached
     g = dec.grid
-    k = setup.system.perm.k
     cells = np.arange(g.n_cells)
     fc_lo = np.empty(g.n_flux_dofs, dtype=np.int64)
     fc_hi = np.empty(g.n_flux_dofs, dtype=np.int64)
@@ -549,8 +546,22 @@ def _suggest_scaling(setup):
     o = np.argsort(dec.gface, kind="stable")
     d = dec.gamma[o]
     starts = np.searchsorted(dec.gface[o], np.arange(dec.n_faces))
-    kmax = np.maximum.reduceat(k[fc_lo[d]].max(axis=1), starts)
-    kmin = np.minimum.reduceat(k[fc_hi[d]].min(axis=1), starts)
+    out = (fc_lo[d], fc_hi[d], starts)
+    dec._face_cells_cache = out
+    return out
+
+
+def _suggest_scaling(setup):
+    """solver.py:286-298 (warning only): aligned coefficient jumps."""
+    if setup.config.scaling != "multiplicity":
+        return
+    dec = setup.dec
+    if not dec.n_gamma or not dec.n_faces:
+        return
+    k = setup.system.perm.k
+    lo, hi, starts = _face_cells(dec)
+    kmax = np.maximum.reduceat(k[lo].max(axis=1), starts)
+    kmin = np.minimum.reduceat(k[hi].min(axis=1), starts)
     ratio = kmax / np.maximum(kmin, 1e-300)
     if np.any((ratio > 1e3) | (ratio < 1e-3)):
         warnings.warn("coefficient jumps aligned with the partition detected; "
