@@ -121,14 +121,16 @@ size_t bddc_pair_scratch_bytes(int n_faces);
 int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                    const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                    int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
-                   int* err, void* stream);
+                   double* qbasis, int* err, void* stream);
 
 /* ---------------------------------------------------------------- coarse */
 
-/* Per-subdomain coarse pieces (coarse.py:130-185): Kc, Psi_Gamma, T, B0 row. */
+/* Per-subdomain coarse pieces (coarse.py:130-185, 237-245): Kc, Psi_Gamma^T, the
+ * Delta-solve operator T (cancellation-free projected form) and the B0 row. */
 int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces, const int* fslot,
-                      const int* gcode, const double* rows, int maxsel, const double* Sinv,
-                      const double* Dsub, int maxC, double* Ct, double* Y, double* Kc, double* Psi,
+                      const int* gcode, const int* nG, const double* rows, const double* qbasis,
+                      int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
+                      double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi,
                       double* T, double* b0, void* inv_ws, int* info, void* stream);
 int bddc_pad_identity(double* M, int n, int npad, void* stream);
 

@@ -14,6 +14,9 @@
 // (coarse.py:111-118), so null(C_f R) is the complement of q = R^T 1/|R^T 1|.
 // The harvested row (adaptive.py:400-416) is L w restricted to the i side,
 // which reduces to  c = (I - 11^T/m) (A R) z,  normalised to unit max.
+// Eigen-solve: Householder tridiagonalisation, bisection for every eigenvalue
+// (Sturm counts), inverse iteration with full reorthogonalisation for the
+// eigenvalues above tau, back-transformation by the reflectors.
 // Rows then pass the reference's Gram-Schmidt dependence test per face
 // (coarse.py:61-100; rows on other faces have disjoint support).
 #include "common.cuh"
@@ -22,92 +25,66 @@
 
 namespace {
 
-__device__ __forceinline__ void jacobi_pair(int round, int k, int n, int& p, int& q) {
-  // circle method over n (even) players, player n-1 fixed
-  if (k == 0) {
-    p = round;
-    q = n - 1;
-  } else {
-    p = (round + k) % (n - 1);
-    q = (round - k + (n - 1)) % (n - 1);
+// Sturm count: number of eigenvalues of the symmetric tridiagonal (d, e) below x.
+__device__ int sturm_below(const double* d, const double* e, int m, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0) ++cnt;
+  for (int k = 1; k < m; ++k) {
+    q = d[k] - x - e[k - 1] * e[k - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) ++cnt;
   }
-  if (p > q) {
-    int t = p;
-    p = q;
-    q = t;
-  }
+  return cnt;
 }
 
-// Symmetric eigen-decomposition of X (m x m, leading dim ld) by parallel
-// cyclic Jacobi; eigenvectors accumulate in V.  Uses rot (3 * mpad/2).
-__device__ void jacobi_eig(double* X, double* V, int m, int ld, double* rot, double* red) {
-  const int mp = m + (m & 1);
-  for (int e = threadIdx.x; e < m * ld; e += blockDim.x) {
-    int r = e / ld, c = e % ld;
-    if (c < m) V[e] = (r == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    // convergence: off-diagonal mass relative to the diagonal
-    double off = 0.0, dia = 0.0;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      int r = e / m, c = e % m;
-      double v = X[r * ld + c];
-      if (r == c) dia += v * v;
-      else off += v * v;
+// One inverse-iteration solve (T - lam I) x = b for a symmetric tridiagonal with
+// partial pivoting (LAPACK dgttrf/dgtts2 pattern); b is overwritten by x.
+__device__ void tri_shift_solve(const double* d0, const double* e0, int m, double lam, double tiny, double* dd,
+                                double* du, double* du2, double* dl, unsigned char* piv, double* b) {
+  for (int i = 0; i < m; ++i) {
+    dd[i] = d0[i] - lam;
+    if (i < m - 1) {
+      du[i] = e0[i];
+      dl[i] = e0[i];
     }
-    off = block_sum(off, red);
-    dia = block_sum(dia, red);
-    if (off <= 1e-30 * dia || off == 0.0) break;
-    for (int round = 0; round < mp - 1; ++round) {
-      for (int k = threadIdx.x; k < mp / 2; k += blockDim.x) {
-        int p, q;
-        jacobi_pair(round, k, mp, p, q);
-        double c = 1.0, s = 0.0;
-        if (q < m) {
-          double apq = X[p * ld + q];
-          double app = X[p * ld + p], aqq = X[q * ld + q];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 1e-18 * sqrt(fabs(app * aqq))) {
-            double th = (aqq - app) / (2.0 * apq);
-            double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
-          }
-        }
-        rot[3 * k] = c;
-        rot[3 * k + 1] = s;
+    du2[i] = 0.0;
+    piv[i] = 0;
+  }
+  for (int i = 0; i < m - 1; ++i) {
+    if (fabs(dd[i]) >= fabs(dl[i])) {
+      if (dd[i] == 0.0) dd[i] = tiny;
+      double f = dl[i] / dd[i];
+      dl[i] = f;
+      dd[i + 1] -= f * du[i];
+    } else {
+      double f = dd[i] / dl[i];
+      dd[i] = dl[i];
+      dl[i] = f;
+      double t = du[i];
+      du[i] = dd[i + 1];
+      dd[i + 1] = t - f * dd[i + 1];
+      if (i < m - 2) {
+        du2[i] = du[i + 1];
+        du[i + 1] = -f * du[i + 1];
       }
-      __syncthreads();
-      // columns: X <- X J, V <- V J
-      const int npair = mp / 2;
-      for (int e = threadIdx.x; e < npair * m; e += blockDim.x) {
-        int k = e / m, r = e % m;
-        double c = rot[3 * k], s = rot[3 * k + 1];
-        if (s == 0.0) continue;
-        int p, q;
-        jacobi_pair(round, k, mp, p, q);
-        double xp = X[r * ld + p], xq = X[r * ld + q];
-        X[r * ld + p] = c * xp - s * xq;
-        X[r * ld + q] = s * xp + c * xq;
-        double vp = V[r * ld + p], vq = V[r * ld + q];
-        V[r * ld + p] = c * vp - s * vq;
-        V[r * ld + q] = s * vp + c * vq;
-      }
-      __syncthreads();
-      // rows: X <- J^T X
-      for (int e = threadIdx.x; e < npair * m; e += blockDim.x) {
-        int k = e / m, cidx = e % m;
-        double c = rot[3 * k], s = rot[3 * k + 1];
-        if (s == 0.0) continue;
-        int p, q;
-        jacobi_pair(round, k, mp, p, q);
-        double xp = X[p * ld + cidx], xq = X[q * ld + cidx];
-        X[p * ld + cidx] = c * xp - s * xq;
-        X[q * ld + cidx] = s * xp + c * xq;
-      }
-      __syncthreads();
+      piv[i] = 1;
     }
   }
+  if (dd[m - 1] == 0.0) dd[m - 1] = tiny;
+  for (int i = 0; i < m - 1; ++i) {
+    if (!piv[i]) {
+      b[i + 1] -= dl[i] * b[i];
+    } else {
+      double t = b[i];
+      b[i] = b[i + 1];
+      b[i + 1] = t - dl[i] * b[i];
+    }
+  }
+  b[m - 1] /= dd[m - 1];
+  if (m > 1) b[m - 2] = (b[m - 2] - du[m - 2] * b[m - 1]) / dd[m - 2];
+  for (int i = m - 3; i >= 0; --i) b[i] = (b[i] - du[i] * b[i + 1] - du2[i] * b[i + 2]) / dd[i];
 }
 
 __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, const int* __restrict__ fslot,
@@ -115,7 +92,7 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
                                 const double* __restrict__ delta, double tau, int maxsel,
                                 double* __restrict__ lam_out, int lam_ld, int* __restrict__ nsel,
                                 int* __restrict__ nadd, double* __restrict__ rows, double* __restrict__ omega,
-                                double* __restrict__ scratch, int* __restrict__ err) {
+                                double* __restrict__ scratch, double* __restrict__ qbasis, int* __restrict__ err) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ int bad;
@@ -123,11 +100,12 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   const int i = faces[4 * f], j = faces[4 * f + 1], a = faces[4 * f + 2], m = faces[4 * f + 3];
   const int ld = m + ((m & 1) ? 0 : 1);
   const int mg = G.maxG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* X = sm;                 // m x ld
   double* Y = X + m * ld;         // m x ld
-  double* vec = Y + m * ld;       // 4 * m
-  double* rot = vec + 4 * m;      // 3 * (m/2 + 1)
-  int* qi = (int*)(rot + 3 * (m / 2 + 1));
+  double* vec = Y + m * ld;       // 4 m
+  double* aux = vec + 4 * m;      // 3 (m/2 + 1) >= m
+  int* qi = (int*)(aux + 3 * (m / 2 + 1));
   int* qj = qi + m;
   double* T1 = scratch + (size_t)f * PAIR_MMAX * PAIR_MMAX;  // A R, m x m
   if (threadIdx.x == 0) bad = 0;
@@ -150,7 +128,7 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     Y[s * ld + t] = Ii[(size_t)as * mg + at] + Ij[(size_t)bs * mg + bt];
   }
   __syncthreads();
-  // Cholesky Y = R R^T (lower), symmetrised input
+  // ---- Cholesky M = R R^T (lower, in Y)
   for (int k = 0; k < m; ++k) {
     if (threadIdx.x == 0) {
       double d = Y[k * ld + k];
@@ -164,8 +142,9 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     double dk = Y[k * ld + k];
     for (int r = k + 1 + threadIdx.x; r < m; r += blockDim.x) Y[r * ld + k] /= dk;
     __syncthreads();
-    for (int e = threadIdx.x; e < (m - k - 1) * (m - k - 1); e += blockDim.x) {
-      int r = k + 1 + e / (m - k - 1), c = k + 1 + e % (m - k - 1);
+    const int w = m - k - 1;
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+      int r = k + 1 + e / w, c = k + 1 + e % w;
       if (c <= r) Y[r * ld + c] -= Y[r * ld + k] * Y[c * ld + k];
     }
     __syncthreads();
@@ -175,32 +154,22 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     if (c > r) Y[r * ld + c] = 0.0;
   }
   __syncthreads();
-  // X <- X R  (row by row through vec), save T1 = A R
-  for (int r = 0; r < m; ++r) {
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-      double acc = 0.0;
-      for (int k = c; k < m; ++k) acc += X[r * ld + k] * Y[k * ld + c];
-      vec[c] = acc;
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-      X[r * ld + c] = vec[c];
-      T1[(size_t)r * m + c] = vec[c];
-    }
-    __syncthreads();
+  // ---- T1 = A R (global scratch), then X = R^T T1, both one-shot
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    int r = e / m, c = e % m;
+    double acc = 0.0;
+    for (int k = c; k < m; ++k) acc += X[r * ld + k] * Y[k * ld + c];
+    T1[(size_t)r * m + c] = acc;
   }
-  // X <- R^T X (column by column)
-  for (int c = 0; c < m; ++c) {
-    for (int r = threadIdx.x; r < m; r += blockDim.x) {
-      double acc = 0.0;
-      for (int k = r; k < m; ++k) acc += Y[k * ld + r] * X[k * ld + c];
-      vec[r] = acc;
-    }
-    __syncthreads();
-    for (int r = threadIdx.x; r < m; r += blockDim.x) X[r * ld + c] = vec[r];
-    __syncthreads();
+  __syncthreads();
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    int r = e / m, c = e % m;
+    double acc = 0.0;
+    for (int k = r; k < m; ++k) acc += Y[k * ld + r] * T1[(size_t)k * m + c];
+    X[r * ld + c] = acc;
   }
-  // symmetrise and project out q = R^T 1 / |R^T 1|
+  __syncthreads();
+  // ---- symmetrise and project out q = R^T 1 / |R^T 1|
   double* qv = vec;       // m
   double* bq = vec + m;   // m
   for (int r = threadIdx.x; r < m; r += blockDim.x) {
@@ -236,44 +205,167 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     X[r * ld + c] += -qv[r] * bq[c] - bq[r] * qv[c] + sq * qv[r] * qv[c];
   }
   __syncthreads();
-  jacobi_eig(X, Y, m, ld, rot, red);
-  // sort eigenvalues descending (rank by value, ties by index)
-  double* lam = vec;            // m
-  int* order = (int*)(vec + m); // m ints
-  for (int r = threadIdx.x; r < m; r += blockDim.x) lam[r] = fmax(X[r * ld + r], 0.0);
-  __syncthreads();
+  // ---- Householder tridiagonalisation of X (Y rows hold the reflectors v_j)
+  double* pv = vec;       // m
+  double* qq = vec + m;   // m
+  for (int jj = 0; jj + 2 < m; ++jj) {
+    const int n1 = m - jj - 1;   // length of the column below the diagonal
+    double sx = 0.0;
+    for (int r = threadIdx.x; r < n1; r += blockDim.x) {
+      double v = X[(jj + 1 + r) * ld + jj];
+      sx += v * v;
+    }
+    sx = block_sum(sx, red);
+    const double x0 = X[(jj + 1) * ld + jj];
+    const double nrm = sqrt(sx);
+    const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+    const double vn2 = sx - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+    const bool skip = !(vn2 > 0.0) || nrm == 0.0;
+    const double inv = skip ? 0.0 : 1.0 / sqrt(vn2);
+    double* v = Y + jj * ld;   // reflector j stored in row jj (entries jj+1..m-1)
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      double val = 0.0;
+      if (r > jj) val = (r == jj + 1 ? x0 - alpha : X[r * ld + jj]) * inv;
+      v[r] = val;
+    }
+    __syncthreads();
+    if (!skip) {
+      // p = A22 v  (rows/cols jj+1..m-1)
+      for (int r = jj + 1 + warp; r < m; r += nw) {
+        double acc = 0.0;
+        for (int c = jj + 1 + lane; c < m; c += 32) acc += X[r * ld + c] * v[c];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) pv[r] = acc;
+      }
+      __syncthreads();
+      double K = 0.0;
+      for (int r = jj + 1 + threadIdx.x; r < m; r += blockDim.x) K += v[r] * pv[r];
+      K = block_sum(K, red);
+      for (int r = jj + 1 + threadIdx.x; r < m; r += blockDim.x) qq[r] = pv[r] - K * v[r];
+      __syncthreads();
+      for (int e = threadIdx.x; e < n1 * n1; e += blockDim.x) {
+        int r = jj + 1 + e / n1, c = jj + 1 + e % n1;
+        X[r * ld + c] -= 2.0 * (v[r] * qq[c] + qq[r] * v[c]);
+      }
+      if (threadIdx.x == 0) {
+        X[(jj + 1) * ld + jj] = alpha;
+        X[jj * ld + jj + 1] = alpha;
+      }
+    }
+    __syncthreads();
+  }
+  // ---- eigenvalues of the tridiagonal by bisection (thread per eigenvalue)
+  double* dg = vec;          // m
+  double* eo = vec + m;      // m
+  double* lam = vec + 2 * m; // m, ascending
   for (int r = threadIdx.x; r < m; r += blockDim.x) {
-    int rank = 0;
-    for (int k = 0; k < m; ++k) rank += (lam[k] > lam[r]) || (lam[k] == lam[r] && k < r);
-    order[rank] = r;
+    dg[r] = X[r * ld + r];
+    eo[r] = (r + 1 < m) ? X[(r + 1) * ld + r] : 0.0;
   }
   __syncthreads();
+  double tnorm = 0.0, gl = 1e308, gu = -1e308;
+  for (int r = 0; r < m; ++r) {
+    double rad = fabs(eo[r]) + (r > 0 ? fabs(eo[r - 1]) : 0.0);
+    gl = fmin(gl, dg[r] - rad);
+    gu = fmax(gu, dg[r] + rad);
+  }
+  tnorm = fmax(fabs(gl), fabs(gu));
+  const double pivmin = fmax(1e-300, tnorm * 1e-300);
+  for (int kk = threadIdx.x; kk < m; kk += blockDim.x) {
+    double lo = gl - 1e-14 * tnorm, hi = gu + 1e-14 * tnorm;
+    for (int it = 0; it < 200; ++it) {
+      double mid = 0.5 * (lo + hi);
+      if (mid <= lo || mid >= hi || hi - lo <= 2e-16 * fmax(fabs(lo), fabs(hi))) break;
+      if (sturm_below(dg, eo, m, mid, pivmin) > kk) hi = mid;
+      else lo = mid;
+    }
+    lam[kk] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+  // descending order: lam_desc[t] = lam[m-1-t], clipped at 0 (adaptive.py:381)
   for (int r = threadIdx.x; r < lam_ld; r += blockDim.x)
-    lam_out[(size_t)f * lam_ld + r] = (r < m) ? lam[order[r]] : 0.0;
+    lam_out[(size_t)f * lam_ld + r] = (r < m) ? fmax(lam[m - 1 - r], 0.0) : 0.0;
+  __shared__ int ksel;
   if (threadIdx.x == 0) {
     int k = 0;
-    while (k < m && lam[order[k]] > tau) ++k;
+    while (k < m && fmax(lam[m - 1 - k], 0.0) > tau) ++k;
     // omega = max(first eigenvalue <= tau, 1); the full pencil always has zeros
-    omega[f] = (k < m) ? fmax(lam[order[k]], 1.0) : 1.0;
+    omega[f] = (k < m) ? fmax(fmax(lam[m - 1 - k], 0.0), 1.0) : 1.0;
     nsel[f] = k;
     if (k > maxsel) bad |= 2;
+    ksel = k < maxsel ? k : maxsel;
   }
   __syncthreads();
-  int k = nsel[f];
-  if (k > maxsel) k = maxsel;
-  // candidate rows: c = (I - 11^T/m) T1 z, normalised to unit max;
-  // Gram-Schmidt dependence filter against 1/sqrt(m) and accepted rows.
-  double* cv = vec + 2 * m;      // m
-  double* basis = X;             // reuse X rows as orthonormal basis (<= m rows)
+  const int k = ksel;
+  // ---- inverse iteration, one thread per selected eigenvalue; vectors -> X rows
+  if (threadIdx.x < k) {
+    const int l = threadIdx.x;
+    const double lv = lam[m - 1 - l];
+    double dd[PAIR_MMAX], du[PAIR_MMAX], du2[PAIR_MMAX], dl[PAIR_MMAX], b[PAIR_MMAX];
+    unsigned char pvt[PAIR_MMAX];
+    for (int r = 0; r < m; ++r) b[r] = 1.0 + 0.5 * sin(1.7 * (r + 1) + 0.61 * (l + 1));
+    const double tiny = fmax(2.2e-16 * tnorm, 1e-300);
+    for (int it = 0; it < 3; ++it) {
+      tri_shift_solve(dg, eo, m, lv, tiny, dd, du, du2, dl, pvt, b);
+      double nb = 0.0;
+      for (int r = 0; r < m; ++r) nb += b[r] * b[r];
+      nb = 1.0 / sqrt(nb);
+      for (int r = 0; r < m; ++r) b[r] *= nb;
+    }
+    for (int r = 0; r < m; ++r) X[l * ld + r] = b[r];
+  }
+  __syncthreads();
+  // full reorthogonalisation in descending-eigenvalue order (fixes near-degenerate clusters)
+  for (int l = 1; l < k; ++l) {
+    for (int pidx = warp; pidx < l; pidx += nw) {
+      double dsum = 0.0;
+      for (int r = lane; r < m; r += 32) dsum += X[pidx * ld + r] * X[l * ld + r];
+      for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      if (lane == 0) aux[pidx] = dsum;
+    }
+    __syncthreads();
+    double nn = 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      double v = X[l * ld + r];
+      for (int pidx = 0; pidx < l; ++pidx) v -= aux[pidx] * X[pidx * ld + r];
+      X[l * ld + r] = v;
+      nn += v * v;
+    }
+    nn = block_sum(nn, red);
+    nn = 1.0 / sqrt(nn);
+    for (int r = threadIdx.x; r < m; r += blockDim.x) X[l * ld + r] *= nn;
+    __syncthreads();
+  }
+  // ---- back-transform z = H_0 ... H_{m-3} y  (apply H_{m-3} first)
+  for (int jj = m - 3; jj >= 0; --jj) {
+    const double* v = Y + jj * ld;
+    for (int l = warp; l < k; l += nw) {
+      double dsum = 0.0;
+      for (int r = jj + 1 + lane; r < m; r += 32) dsum += v[r] * X[l * ld + r];
+      for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      if (lane == 0) aux[l] = dsum;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * m; e += blockDim.x) {
+      int l = e / m, r = e % m;
+      if (r > jj) X[l * ld + r] -= 2.0 * aux[l] * v[r];
+    }
+    __syncthreads();
+  }
+  // ---- candidate rows c = (I - 11^T/m) T1 z, unit max; dependence filter
+  // against 1/sqrt(m) and the accepted rows (coarse.py:61-100), basis in Y rows.
+  double* cv = vec + 2 * m;      // m (lam no longer needed)
+  double* w = vec + 3 * m;       // m
+  double* basis = Y;
   for (int c = threadIdx.x; c < m; c += blockDim.x) basis[c] = rsqrt((double)m);
   __syncthreads();
   int nb = 1, added = 0;
   for (int l = 0; l < k; ++l) {
-    int col = order[l];
-    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    for (int r = warp; r < m; r += nw) {
       double acc = 0.0;
-      for (int t = 0; t < m; ++t) acc += T1[(size_t)r * m + t] * Y[t * ld + col];
-      cv[r] = acc;
+      for (int t = lane; t < m; t += 32) acc += T1[(size_t)r * m + t] * X[l * ld + t];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) cv[r] = acc;
     }
     __syncthreads();
     double mean = 0.0;
@@ -288,26 +380,24 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     if (mx == 0.0) continue;
     for (int r = threadIdx.x; r < m; r += blockDim.x) cv[r] /= mx;
     __syncthreads();
-    // residual after one projection (independence test) then two-pass GS
     double nv = 0.0;
     for (int r = threadIdx.x; r < m; r += blockDim.x) nv += cv[r] * cv[r];
     nv = sqrt(block_sum(nv, red));
-    double* w = vec + 3 * m;
     for (int r = threadIdx.x; r < m; r += blockDim.x) w[r] = cv[r];
     __syncthreads();
-    for (int pass = 0; pass < 2; ++pass) {
-      // classical GS: w -= B^T (B w)
-      double* coefs = rot;  // nb <= m entries (rot holds >= 3*(m/2+1) >= m doubles)
-      for (int bidx = 0; bidx < nb; ++bidx) {
-        double d = 0.0;
-        for (int r = threadIdx.x; r < m; r += blockDim.x) d += basis[bidx * ld + r] * w[r];
-        d = block_sum(d, red);
-        if (threadIdx.x == 0) coefs[bidx] = d;
+    bool dep = false;
+    for (int pass = 0; pass < 2 && !dep; ++pass) {
+      // classical GS: w -= B^T (B w), coefficients by one warp each
+      for (int bidx = warp; bidx < nb; bidx += nw) {
+        double dsum = 0.0;
+        for (int r = lane; r < m; r += 32) dsum += basis[bidx * ld + r] * w[r];
+        for (int o = 16; o > 0; o >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        if (lane == 0) aux[bidx] = dsum;
       }
       __syncthreads();
       for (int r = threadIdx.x; r < m; r += blockDim.x) {
         double acc = w[r];
-        for (int bidx = 0; bidx < nb; ++bidx) acc -= coefs[bidx] * basis[bidx * ld + r];
+        for (int bidx = 0; bidx < nb; ++bidx) acc -= aux[bidx] * basis[bidx * ld + r];
         w[r] = acc;
       }
       __syncthreads();
@@ -315,24 +405,27 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
         double nr = 0.0;
         for (int r = threadIdx.x; r < m; r += blockDim.x) nr += w[r] * w[r];
         nr = sqrt(block_sum(nr, red));
-        if (!(nr > 1e-10 * fmax(nv, 1.0))) {
-          nv = -1.0;  // dependent: drop
-          break;
-        }
+        dep = !(nr > 1e-10 * fmax(nv, 1.0));
       }
     }
-    if (nv < 0.0) continue;
-    double nw = 0.0;
-    for (int r = threadIdx.x; r < m; r += blockDim.x) nw += w[r] * w[r];
-    nw = sqrt(block_sum(nw, red));
+    if (dep) continue;
+    double nwn = 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) nwn += w[r] * w[r];
+    nwn = sqrt(block_sum(nwn, red));
     if (nb < m) {
-      for (int r = threadIdx.x; r < m; r += blockDim.x) basis[nb * ld + r] = w[r] / nw;
+      for (int r = threadIdx.x; r < m; r += blockDim.x) basis[nb * ld + r] = w[r] / nwn;
       for (int r = threadIdx.x; r < m; r += blockDim.x)
         rows[((size_t)f * maxsel + added) * PAIR_MMAX + r] = cv[r];
     }
     __syncthreads();
     ++nb;
     ++added;
+  }
+  // orthonormal basis of the face's constraint span (initial row + accepted rows), used
+  // for the projected Delta-solve operator T (coarse.cu)
+  for (int e = threadIdx.x; e < nb * m; e += blockDim.x) {
+    int bidx = e / m, r = e % m;
+    if (bidx <= maxsel) qbasis[((size_t)f * (maxsel + 1) + bidx) * PAIR_MMAX + r] = basis[bidx * ld + r];
   }
   if (threadIdx.x == 0) {
     nadd[f] = added;
@@ -349,16 +442,17 @@ extern "C" size_t bddc_pair_scratch_bytes(int n_faces) {
 extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                               const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                               int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
-                              int* err, void* stream) {
+                              double* qbasis, int* err, void* stream) {
   if (g->maxF > PAIR_MMAX) return bddc_set_error(BDDC_ERR_ARG, "pair face larger than PAIR_MMAX=112 dofs");
   int m = g->maxF;
   int ld = m + ((m & 1) ? 0 : 1);
   size_t shm = (size_t)(2 * m * ld + 4 * m + 3 * (m / 2 + 1)) * sizeof(double) + 2 * m * sizeof(int) + 16;
+  // one CTA per face; the per-thread inverse-iteration arrays live in local memory
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(pair_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   pair_eig_kernel<<<g->n_faces, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel,
                                                                   lam_out, lam_ld, nsel, nadd, rows, omega,
-                                                                  scratch, err);
+                                                                  scratch, qbasis, err);
   LAUNCH_OK();
   return 0;
 }

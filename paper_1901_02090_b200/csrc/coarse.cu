@@ -5,7 +5,10 @@
 //   Kc   = (C S^-1 C^T)^-1            (= Psi^T A Psi, coarse.py:179)
 //   Psi  = S^-1 C^T Kc                (Gamma rows of the coarse basis, coarse.py:166-171),
 //          stored transposed: PsiT = Kc (S^-1 C^T)^T, maxC x maxG per subdomain
-//   T    = S^-1 - Psi (C S^-1)        (Gamma block of the constrained inverse, coarse.py:237-245)
+//   T    = Gamma block of the constrained inverse (coarse.py:237-245) = Z (Z^T S Z)^-1 Z^T,
+//          Z = null(C).  Computed without cancellation as
+//          T = (P S P + g Q Q^T)^-1 - Q Q^T / g,  P = I - Q Q^T,  g = tr(S)/n,
+//          Q = per-face orthonormal bases of the constraint rows (from the pair kernel).
 //   b0   = 1^T B_loc psi = -D_i sum_q sign_q Psi[q]   (coarse.py:184-185)
 // The global coarse problem (S_Pi and the pinned pressure block) is handled
 // by the nested-dissection multifrontal solver in nd.cu / coarse_nd.py.
@@ -82,6 +85,52 @@ __global__ void b0_kernel(bddc_geom G, const int* __restrict__ gcode, const int*
   }
 }
 
+// Qc (maxG x maxC): orthonormal basis of range(C^T) from the per-face bases
+// (qbasis[f][k], or 1/sqrt(m) for the initial row when qbasis is NULL).
+__global__ void qc_kernel(bddc_geom G, const int* __restrict__ sub_rows, const int* __restrict__ faces,
+                          const int* __restrict__ fslot, const double* __restrict__ qbasis, int maxsel, int maxC,
+                          double* __restrict__ Qc) {
+  const int i = blockIdx.x;
+  const int mg = G.maxG;
+  double* Q = Qc + (size_t)i * mg * maxC;
+  for (size_t e = threadIdx.x; e < (size_t)mg * maxC; e += blockDim.x) Q[e] = 0.0;
+  __syncthreads();
+  for (int r = 0; r < maxC; ++r) {
+    const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
+    if (sr[0] < 0) continue;
+    int f = sr[1], k = sr[2];
+    int a = faces[4 * f + 2], m = faces[4 * f + 3];
+    int side = (sr[3] > 0) ? 1 : 0;
+    for (int s = threadIdx.x; s < m; s += blockDim.x) {
+      int q = fslot[((size_t)i * 6 + a * 2 + side) * G.maxF + s];
+      double v = qbasis ? qbasis[((size_t)f * (maxsel + 1) + k) * PAIR_MMAX + s] : rsqrt((double)m);
+      Q[(size_t)q * maxC + r] = v;
+    }
+  }
+}
+
+// gamma_i = tr(S_i)/n_i ; QtSQ[i] += gamma_i I (live rows)
+__global__ void gamma_kernel(int mg, int maxC, const int* __restrict__ nG, const int* __restrict__ sub_rows,
+                             const double* __restrict__ S, double* __restrict__ gamma, double* __restrict__ QtSQ) {
+  __shared__ double red[32];
+  const int i = blockIdx.x;
+  const int n = nG[i];
+  double acc = 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) acc += S[((size_t)i * mg + q) * mg + q];
+  acc = block_sum(acc, red);
+  const double g = (n > 0 && acc > 0.0) ? acc / n : 1.0;
+  if (threadIdx.x == 0) gamma[i] = g;
+  for (int r = threadIdx.x; r < maxC; r += blockDim.x)
+    if (sub_rows[((size_t)i * maxC + r) * 4] >= 0) QtSQ[((size_t)i * maxC + r) * maxC + r] += g;
+}
+
+__global__ void scale_rows_kernel(long long per, const double* __restrict__ gamma, double* __restrict__ X) {
+  const int i = blockIdx.y;
+  const double sc = rsqrt(gamma[i]);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (long long)gridDim.x * blockDim.x)
+    X[(size_t)i * per + e] *= sc;
+}
+
 // Identity padding for a dense matrix beyond n.
 __global__ void pad_tail_identity_kernel(double* M, int n, int npad) {
   long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,12 +147,13 @@ __global__ void copy_kernel(const double* __restrict__ a, double* __restrict__ b
 
 }  // namespace
 
-// Per-subdomain coarse pieces.  Workspaces: Ct, Y (N*maxG*maxC each),
-// inv_ws (bddc_spd_inverse_workspace(maxC, N, 32)).
+// Per-subdomain coarse pieces.  Workspaces: Ct, Y, E (N*maxG*maxC each),
+// inv_ws (bddc_spd_inverse_workspace(max(maxC, maxG), N, 32|64)), gamma (N).
 extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces, const int* fslot,
-                                 const int* gcode, const double* rows, int maxsel, const double* Sinv,
-                                 const double* Dsub, int maxC, double* Ct, double* Y, double* Kc, double* Psi,
-                                 double* T, double* b0, void* inv_ws, int* info, void* stream) {
+                                 const int* gcode, const int* nG, const double* rows, const double* qbasis,
+                                 int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
+                                 double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi, double* T,
+                                 double* b0, void* inv_ws, int* info, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int N = g->N, mg = g->maxG;
   const long long sG = (long long)mg * mg, sGC = (long long)mg * maxC, sCC = (long long)maxC * maxC;
@@ -111,28 +161,53 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   coarse_ct_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, rows, maxsel, maxC, Ct);
   LAUNCH_OK();
   int r;
-  // Y = Sinv C^T
+  // Y = Sinv C^T ; Kinv = C Y ; Kc = Kinv^-1 ; PsiT = Kc Y^T ; b0
   if ((r = bddc_dgemm_batched(0, 0, mg, maxC, mg, 1.0, Sinv, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, stream)))
     return r;
-  // Kinv = C Y = (C^T)^T Y
   if ((r = bddc_dgemm_batched(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, Kc, maxC, sCC, N, 0,
                               stream)))
     return r;
   pad_identity_kernel<<<N, 256, 0, s>>>(maxC, sub_rows, Kc);
   LAUNCH_OK();
   if ((r = bddc_spd_inverse_batched(Kc, maxC, maxC, sCC, N, 32, inv_ws, info, stream))) return r;
-  // PsiT = Kc Y^T   (maxC x maxG)
   if ((r = bddc_dgemm_batched(0, 1, maxC, mg, maxC, 1.0, Kc, maxC, sCC, Y, maxC, sGC, 0.0, Psi, mg, sGC, N, 0,
                               stream)))
     return r;
-  // T = Sinv - Psi Y^T = Sinv - PsiT^T Y^T
-  long long tot = (long long)N * sG;
-  copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(Sinv, T, tot);
-  LAUNCH_OK();
-  if ((r = bddc_dgemm_batched(1, 1, mg, mg, maxC, -1.0, Psi, mg, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
-    return r;
   b0_kernel<<<N, 256, 0, s>>>(*g, gcode, sub_rows, Psi, Dsub, maxC, b0);
   LAUNCH_OK();
+  // ---- T = (P S P + g Q Q^T)^-1 - Q Q^T / g   (Q in Ct, S Q in Y, Q^T S Q in E[..maxC^2])
+  qc_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, qbasis, maxsel, maxC, Ct);
+  LAUNCH_OK();
+  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, mg, 1.0, S, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, stream)))
+    return r;
+  double* QtSQ = Kc;  // Kc is kept: use the tail of E for Q^T S Q instead
+  QtSQ = E + (size_t)N * sGC - (size_t)N * sCC;
+  if ((r = bddc_dgemm_batched(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, QtSQ, maxC, sCC, N, 0,
+                              stream)))
+    return r;
+  gamma_kernel<<<N, 128, 0, s>>>(mg, maxC, nG, sub_rows, S, gamma, QtSQ);
+  LAUNCH_OK();
+  // M = S - Q (SQ)^T - (SQ) Q^T + Q (Q^T S Q + g I) Q^T, built in T
+  long long tot = (long long)N * sG;
+  copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(S, T, tot);
+  LAUNCH_OK();
+  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+    return r;
+  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+    return r;
+  // Y <- Q (Q^T S Q + g I)   (reuse Y)
+  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, maxC, 1.0, Ct, maxC, sGC, QtSQ, maxC, sCC, 0.0, Y, maxC, sGC, N, 0,
+                              stream)))
+    return r;
+  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+    return r;
+  if ((r = bddc_spd_inverse_batched(T, mg, mg, sG, N, 64, inv_ws, info, stream))) return r;
+  // T -= (Q/sqrt g)(Q/sqrt g)^T
+  dim3 gsc(64, N);
+  scale_rows_kernel<<<gsc, 256, 0, s>>>(sGC, gamma, Ct);
+  LAUNCH_OK();
+  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+    return r;
   return 0;
 }
 

@@ -203,6 +203,7 @@ class BddcSetup:
         maxsel = 1
         nadd = np.zeros(nf, dtype=np.int64)
         rows = torch.zeros(1, dtype=F64, device=dev)
+        qbasis = None
         self.pair_lambda = None
         if config.constraints == "adaptive" and nf:
             maxsel = dec.maxF
@@ -214,12 +215,13 @@ class BddcSetup:
             omega = torch.empty(nf, dtype=F64, device=dev)
             scratch = torch.empty(nat.load().bddc_pair_scratch_bytes(nf) // 8,
                                   dtype=F64, device=dev)
+            qbasis = torch.zeros(nf * (maxsel + 1) * 112, dtype=F64, device=dev)
             err = torch.zeros(1, dtype=I32, device=dev)
             tau = config.tau if math.isfinite(config.tau) else 1e308
             nat.call("bddc_pair_eigs", gp, _p(self.d_faces), _p(self.d_fslot),
                      _p(self.d_S), _p(Sinv), _p(self.d_delta), float(tau),
                      maxsel, _p(lam), lam_ld, _p(d_nsel), _p(d_nadd), _p(rows),
-                     _p(omega), _p(scratch), _p(err), st)
+                     _p(omega), _p(scratch), _p(qbasis), _p(err), st)
             del scratch
             e = int(err.item())
             if e & 1:
@@ -248,18 +250,22 @@ class BddcSetup:
         self.d_nC = t(self.nC)
         Ct = torch.empty(N * mg * maxC, dtype=F64, device=dev)
         Y = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        E = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        gam = torch.empty(N, dtype=F64, device=dev)
         self.d_Kc = torch.empty(N * maxC * maxC, dtype=F64, device=dev)
         self.d_Psi = torch.empty(N * mg * maxC, dtype=F64, device=dev)
         self.d_T = torch.empty(N * mg * mg, dtype=F64, device=dev)
         self.d_b0 = torch.empty(N * maxC, dtype=F64, device=dev)
-        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(maxC, N, 32) // 8 + 2,
-                         dtype=F64, device=dev)
+        wsz = max(nat.load().bddc_spd_inverse_workspace(maxC, N, 32),
+                  nat.load().bddc_spd_inverse_workspace(mg, N, 64))
+        ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
         nat.call("bddc_coarse_local", gp, _p(dev_rows), _p(self.d_faces),
-                 _p(self.d_fslot), _p(self.d_gcode), _p(rows), maxsel, _p(Sinv),
-                 _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(self.d_Kc),
+                 _p(self.d_fslot), _p(self.d_gcode), _p(self.d_nG), _p(rows),
+                 _p(qbasis) if qbasis is not None else None, maxsel, _p(self.d_S), _p(Sinv),
+                 _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(E), _p(gam), _p(self.d_Kc),
                  _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws),
                  _p(info[2:]), st)
-        del Ct, Y, ws, Sinv
+        del Ct, Y, E, gam, ws, Sinv
         # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
         npk = nat.load().bddc_sym_packed_elems(mg)
         self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
