@@ -81,13 +81,14 @@ int bddc_weights(const bddc_geom* g, int stiffness, const double* coef, const in
 /* D_i = mean diag(A) over dofs touching subdomain i (grid.py:344-357). */
 int bddc_rescale(const bddc_geom* g, const double* coef, double* Dsub, void* stream);
 
-/* Interior KKT elimination (substructure.py:25-70) for all subdomains:
- * P = B_I A_II^-1 B_I^T + alpha 11^T (maxP^2 each, identity padded), the
- * line-compact G = B_G - B_I A_II^-1 A_IG (maxG x maxL) and S_A. */
+/* Interior KKT elimination (substructure.py:25-70) for all subdomains: the
+ * Jacobi-scaled pressure Schur Ps = D^-1/2 (B_I A_II^-1 B_I^T) D^-1/2 + v v^T
+ * (maxP^2 each, identity padded; scl = N x (maxP+1) scaling), the line-compact
+ * G = B_G - B_I A_II^-1 A_IG (maxG x maxL) and S_A. */
 int bddc_local_build(const bddc_geom* g, const double* coef, const int* fslot, double* P, double* Gc,
-                     double* SAd, int* SApart, double* SAoff, double* alpha, void* stream);
-/* Q = P^+ from the swept inverse of P + alpha 11^T. */
-int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* alpha, void* stream);
+                     double* SAd, int* SApart, double* SAoff, double* scl, void* stream);
+/* Q = P^+ from the inverse of Ps (in place). */
+int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* scl, void* stream);
 /* Dense S_i = sym(S_A + G^T Q G), identity padded (substructure.py:90-99). */
 int bddc_local_schur(const bddc_geom* g, const int* gcode, const double* Q, const double* Gc,
                      const double* SAd, const int* SApart, const double* SAoff, double* Wt,

@@ -41,6 +41,12 @@ def _random_k(counts, seed, orders=6.0):
     return 10.0 ** rng.uniform(-orders / 2, orders / 2, (n, len(counts)))
 
 
+def _c3_block(z0):
+    """30x30x15 cells cropped from the config-3 field (10x10x5 subdomains like C3)."""
+    k = fields.config_field(3).reshape(85, 220, 60, 3)
+    return np.ascontiguousarray(k[z0:z0 + 15, 40:70, 10:40].reshape(-1, 3))
+
+
 CASES = {
     # name: (counts, sizes, splits, scaling, tau, tol, k-maker)
     "g2d_small": ((8, 8), (1.0, 1.0), (2, 2), "multiplicity", math.inf,
@@ -55,6 +61,8 @@ CASES = {
                  1e-10, lambda: _random_k((5, 5, 5), 4)),
     "g3d_box": ((8, 6, 4), (20.0, 10.0, 2.0), (2, 2, 2), "stiffness", 10.0,
                 1e-10, lambda: _random_k((8, 6, 4), 9)),
+    "g3d_c3block": ((30, 30, 15), (20.0, 10.0, 2.0), (3, 3, 3), "multiplicity", 10.0,
+                    1e-8, lambda: _c3_block(28)),
     "c0": (fields.CONFIGS[0]["counts"], fields.CONFIGS[0]["sizes"],
            fields.CONFIGS[0]["splits"], "stiffness", math.inf, 1e-8,
            lambda: fields.config_field(0)),

@@ -4,11 +4,12 @@
 //    64x64x16 CTA tiles, 4 warps x (32x32) warp tiles of mma.sync m8n8k4 f64
 //    (SASS DMMA.8x8x4), cp.async double-buffered shared-memory staging.
 //    Optional upper-tile mask for symmetric updates.
-//  * bddc_spd_inverse_batched: in-place inverse of a batch of SPD matrices by
-//    the blocked symmetric sweep (Gauss-Jordan without pivoting; every pivot
-//    block is a Schur complement of an SPD matrix, hence SPD).  Each step is
-//    a small pivot-block inverse plus two DMMA GEMMs; the bulk of the flops is
-//    the symmetric rank-b trailing update.
+//  * bddc_spd_inverse_batched: in-place inverse of a batch of SPD matrices the
+//    LAPACK potrf -> trtri -> lauum way (M = U^T U, V = U^-1, M^-1 = V V^T),
+//    each phase recursive 2x2-blocked with large-K DMMA GEMMs and leaves
+//    (<= 64) in shared memory.  Schur complements are Gram updates of the
+//    factor, so the result is as accurate as a Cholesky solve (an explicit
+//    block inversion loses a further factor of the condition number).
 //
 // These replace SuperLU / LAPACK getrf+getrs / dense inverses of the
 // reference (substructure.py:66, coarse.py:159,196) with explicit inverses
@@ -183,106 +184,128 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
   }
 }
 
-// ---------------------------------------------------------------- sweep
+// ------------------------------------------------------- SPD inverse leaves
 
-// Pivot step of the blocked symmetric sweep: per matrix, read the b x b pivot
-// block D (upper storage), invert it in shared memory (scalar sweep), write
-// Dinv and the pre-step row panel X[k][c] = M[kb+k][c] (full row, read from the
-// upper triangle).
-__global__ void sweep_pivot_kernel(double* M, int n, int ld, long long sM, int kb, int b,
-                                   double* X, double* Dinv, int* info) {
-  extern __shared__ double sd[];  // b*b
+// Leaf of the Cholesky-based inverse, on the nb x nb diagonal block of every
+// matrix (one CTA per matrix, block in shared memory).
+//  mode 1 (factor): read the upper triangle, M = U^T U (upper Cholesky),
+//          V = U^-1 in place (column-oriented trtri), write V to the upper
+//          triangle and zeros below it.
+//  mode 2 (lauum):  read V (upper triangle; lower taken as zero), write V V^T.
+//  mode 3: both (the whole matrix fits one leaf).
+__global__ void leaf_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info, int mode) {
+  extern __shared__ double sd[];  // nb*nb + nb
+  double* tmp = sd + nb * nb;
+  __shared__ int bad;
   const int z = blockIdx.x;
   double* Mz = M + z * sM;
-  double* Xz = X + (size_t)z * b * n;
-  double* Dz = Dinv + (size_t)z * b * b;
   const int nt = blockDim.x;
-  for (int e = threadIdx.x; e < b * b; e += nt) {
-    int r = e / b, c = e % b;
-    int rr = imin(r, c), cc = imax(r, c);
-    sd[e] = Mz[(size_t)(kb + rr) * ld + kb + cc];
+  if (threadIdx.x == 0) bad = 0;
+  for (int e = threadIdx.x; e < nb * nb; e += nt) {
+    int r = e / nb, c = e % nb;
+    sd[e] = (c >= r) ? Mz[(size_t)r * ld + c] : 0.0;
   }
   __syncthreads();
-  // scalar symmetric sweep on the b x b block: result -D^{-1}
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int k = 0; k < b; ++k) {
-    double piv = sd[k * b + k];
-    if (!(piv > 0.0)) {
-      if (threadIdx.x == 0) bad = 1;
-      piv = 1.0;
+  if (mode & 1) {
+    // right-looking upper Cholesky
+    for (int k = 0; k < nb; ++k) {
+      double d = sd[k * nb + k];
+      if (!(d > 0.0)) {
+        if (threadIdx.x == 0) bad = 1;
+        d = 1.0;
+      }
+      d = sqrt(d);
+      __syncthreads();
+      for (int c = k + threadIdx.x; c < nb; c += nt) sd[k * nb + c] = (c == k) ? d : sd[k * nb + c] / d;
+      __syncthreads();
+      const int w = nb - k - 1;
+      for (int e = threadIdx.x; e < w * w; e += nt) {
+        int r = k + 1 + e / w, c = k + 1 + e % w;
+        if (c >= r) sd[r * nb + c] -= sd[k * nb + r] * sd[k * nb + c];
+      }
+      __syncthreads();
     }
-    double ip = 1.0 / piv;
-    __syncthreads();
-    for (int e = threadIdx.x; e < b * b; e += nt) {
-      int r = e / b, c = e % b;
-      if (r == k || c == k) continue;
-      sd[e] -= sd[r * b + k] * sd[k * b + c] * ip;
+    // V = U^-1 column by column: V[0:j, j] = -V[j][j] * V[0:j, 0:j] U[0:j, j]
+    for (int j = 0; j < nb; ++j) {
+      const double vjj = 1.0 / sd[j * nb + j];
+      for (int i = threadIdx.x; i < j; i += nt) tmp[i] = sd[i * nb + j];
+      __syncthreads();
+      for (int i = threadIdx.x; i < j; i += nt) {
+        double acc = 0.0;
+        for (int k = i; k < j; ++k) acc += sd[i * nb + k] * tmp[k];
+        sd[i * nb + j] = -vjj * acc;
+      }
+      if (threadIdx.x == 0) sd[j * nb + j] = vjj;
+      __syncthreads();
     }
-    __syncthreads();
-    for (int e = threadIdx.x; e < b; e += nt) {
-      if (e == k) continue;
-      double v = sd[e * b + k] * ip;
-      sd[e * b + k] = v;
-      sd[k * b + e] = v;
-    }
-    if (threadIdx.x == 0) sd[k * b + k] = -ip;
-    __syncthreads();
   }
   if (threadIdx.x == 0 && bad) atomicAdd(info, 1);
-  for (int e = threadIdx.x; e < b * b; e += nt) Dz[e] = -sd[e];
-  // row panel: c >= kb from row kb+k; c < kb from column (upper storage)
-  for (int e = threadIdx.x; e < b * n; e += nt) {
-    int c, k;
-    double v;
-    if (e < b * kb) {  // k fastest: read rows c < kb contiguous over k
-      c = e / b;
-      k = e % b;
-      v = Mz[(size_t)c * ld + kb + k];
-    } else {
-      int e2 = e - b * kb;
-      int w = n - kb;
-      k = e2 / w;
-      c = kb + e2 % w;
-      int r = kb + k;
-      v = (c >= r) ? Mz[(size_t)r * ld + c] : Mz[(size_t)c * ld + r];
+  if (mode & 2) {
+    // X = V V^T: X[r][c] = sum_{k >= max(r,c)} V[r][k] V[c][k]
+    for (int e = threadIdx.x; e < nb * nb; e += nt) {
+      int r = e / nb, c = e % nb;
+      int k0 = r > c ? r : c;
+      double acc = 0.0;
+      for (int k = k0; k < nb; ++k) acc += sd[r * nb + k] * sd[c * nb + k];
+      Mz[(size_t)r * ld + c] = acc;
     }
-    Xz[(size_t)k * n + c] = v;
-  }
-}
-
-// Write the swept K row/column: M[K, c] = W[:, c] (upper part), M[K,K] = -Dinv.
-__global__ void sweep_fix_kernel(double* M, int n, int ld, long long sM, int kb, int b,
-                                 const double* W, const double* Dinv) {
-  const int z = blockIdx.y;
-  double* Mz = M + z * sM;
-  const double* Wz = W + (size_t)z * b * n;
-  const double* Dz = Dinv + (size_t)z * b * b;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= b * n) return;
-  int k = e / n, c = e % n;
-  if (c >= kb && c < kb + b) {
-    int r = c - kb;
-    if (k <= r) Mz[(size_t)(kb + k) * ld + c] = -Dz[k * b + r];
-  } else if (c >= kb + b) {
-    Mz[(size_t)(kb + k) * ld + c] = Wz[(size_t)k * n + c];
   } else {
-    Mz[(size_t)c * ld + kb + k] = Wz[(size_t)k * n + c];
+    for (int e = threadIdx.x; e < nb * nb; e += nt) {
+      int r = e / nb, c = e % nb;
+      Mz[(size_t)r * ld + c] = sd[e];   // V upper, zeros below
+    }
   }
 }
 
-// A^{-1} = -M (upper) mirrored to full storage.
-__global__ void sweep_final_kernel(double* M, int n, int ld, long long sM) {
+// Zero / copy an r x c block (row-major, leading dim ld, batch stride sM / sW).
+__global__ void block_copy_kernel(double* dst, int ld, long long sD, const double* src, int lds, long long sS,
+                                  int rows, int cols) {
+  const int z = blockIdx.y;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r = (int)(e / cols), c = (int)(e % cols);
+    dst[z * sD + (size_t)r * ld + c] = src ? src[z * sS + (size_t)r * lds + c] : 0.0;
+  }
+}
+
+// Symmetric Jacobi scaling: mode 0: dsq = diag^-1/2 and M <- D^-1/2 M D^-1/2;
+// mode 1: M <- D^-1/2 M D^-1/2 with the stored dsq (turns inv(scaled) into inv(M)).
+__global__ void jacobi_scale_kernel(double* M, int n, int ld, long long sM, double* dsq, int mode) {
   const int z = blockIdx.y;
   double* Mz = M + z * sM;
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)n * n) return;
-  int r = (int)(e / n), c = (int)(e % n);
-  if (r > c) return;
-  double v = -Mz[(size_t)r * ld + c];
-  Mz[(size_t)r * ld + c] = v;
-  if (r != c) Mz[(size_t)c * ld + r] = v;
+  double* dz = dsq + (size_t)z * n;
+  if (mode == 0 && blockIdx.x == 0) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double d = Mz[(size_t)r * ld + r];
+      dz[r] = (d > 0.0) ? rsqrt(d) : 1.0;
+    }
+  }
+  __syncthreads();
+  if (mode == 0) return;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r = (int)(e / n), c = (int)(e % n);
+    Mz[(size_t)r * ld + c] *= dz[r] * dz[c];
+  }
+}
+
+// Lower triangle of an n x n block from its upper triangle (tile transposes).
+__global__ void lower_from_upper_kernel(double* M, int n, int ld, long long sM) {
+  __shared__ double t[32][33];
+  const int z = blockIdx.z;
+  const int bi = blockIdx.y, bj = blockIdx.x;   // target tile (bi > bj) below the diagonal
+  if (bi < bj) return;
+  double* Mz = M + z * sM;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int rr = ty; rr < 32; rr += 8) {        // source tile (bj, bi) in the upper triangle
+    int r = bj * 32 + rr, c = bi * 32 + tx;
+    t[rr][tx] = (r < n && c < n) ? Mz[(size_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  for (int cc = ty; cc < 32; cc += 8) {
+    int r = bi * 32 + tx, c = bj * 32 + cc;
+    if (r < n && c < n && r > c) Mz[(size_t)r * ld + c] = t[cc][tx];
+  }
 }
 
 }  // namespace
@@ -319,41 +342,112 @@ extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, d
 }
 
 extern "C" size_t bddc_spd_inverse_workspace(int n, int batch, int b) {
-  return (size_t)batch * (2 * (size_t)b * n + (size_t)b * b) * sizeof(double) + 16;
+  (void)b;
+  return (size_t)batch * ((size_t)n * n / 2 + 2 * (size_t)n + 64) * sizeof(double) + 64;
 }
 
-// In-place inverse of `batch` SPD matrices of order n (leading dim ld, batch
-// stride sM).  Only the upper triangle of the input is read.  `ws` must hold
-// bddc_spd_inverse_workspace(n, batch, b) bytes; `info` (device int) counts
-// non-positive pivots (NumericalFailureError on the host side).
-extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM, int batch, int b,
-                                        void* ws, int* info, void* stream) {
+namespace {
+
+int block_copy(double* dst, int ld, long long sD, const double* src, int lds, long long sS, int rows, int cols,
+               int batch, cudaStream_t s) {
+  long long tot = (long long)rows * cols;
+  int gx = (int)((tot + 255) / 256);
+  if (gx > 64) gx = 64;
+  block_copy_kernel<<<dim3(gx, batch), 256, 0, s>>>(dst, ld, sD, src, lds, sS, rows, cols);
+  LAUNCH_OK();
+  return 0;
+}
+
+int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
+  size_t shm = (size_t)(n * n + n) * sizeof(double);
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  leaf_chol_inv_kernel<<<batch, 256, shm, s>>>(M, n, ld, sM, info, mode);
+  LAUNCH_OK();
+  return 0;
+}
+
+int split_of(int n, int b) {
+  int n1 = ((n / 2 + b - 1) / b) * b;
+  if (n1 >= n) n1 = n - b;
+  return n1;
+}
+
+// Factor phase: overwrite the upper triangle of every n x n block with
+// V = U^-1 where M = U^T U, and the strict lower triangle with zeros.
+//   M = [A B; B^T C]:  V11 = rec(A);  U12 = V11^T B;  C <- C - U12^T U12;
+//   V22 = rec(C);  V12 = -V11 U12 V22.
+// The Schur complement is formed as a Gram update of the Cholesky factor, so
+// rounding never sees an explicitly inverted pivot block (LAPACK potrf/trtri).
+int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, double* ws, int* info, cudaStream_t s) {
+  if (n <= b) return leaf_launch(M, n, ld, sM, batch, info, 1, s);
+  const int n1 = split_of(n, b), n2 = n - n1;
+  double* A = M;
+  double* B = M + n1;
+  double* C = M + (size_t)n1 * ld + n1;
+  double* W = ws;                                  // batch x n1 x n2
+  double* ws_next = ws + (size_t)batch * n1 * n2;
+  const long long sW = (long long)n1 * n2;
+  int r;
+  if ((r = chol_inv_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
+  if ((r = bddc_dgemm_batched(1, 0, n1, n2, n1, 1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = bddc_dgemm_batched(1, 0, n2, n2, n1, -1.0, W, n2, sW, W, n2, sW, 1.0, C, ld, sM, batch, 1, s))) return r;
+  if ((r = chol_inv_rec(C, n2, ld, sM, batch, b, ws_next, info, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 0, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  return block_copy(M + (size_t)n1 * ld, ld, sM, nullptr, 0, 0, n2, n1, batch, s);
+}
+
+// Lauum phase: upper triangle of V V^T from V (upper, zeros below):
+//   [V11 V12; 0 V22] -> [V11 V11^T + V12 V12^T, V12 V22^T; ., V22 V22^T].
+int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* ws, int* info, cudaStream_t s) {
+  if (n <= b) return leaf_launch(M, n, ld, sM, batch, info, 2, s);
+  const int n1 = split_of(n, b), n2 = n - n1;
+  double* A = M;
+  double* B = M + n1;
+  double* C = M + (size_t)n1 * ld + n1;
+  double* W = ws;
+  double* ws_next = ws + (size_t)batch * n1 * n2;
+  const long long sW = (long long)n1 * n2;
+  int r;
+  if ((r = lauum_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 1, n1, n1, n2, 1.0, B, ld, sM, B, ld, sM, 1.0, A, ld, sM, batch, 1, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 1, n1, n2, n2, 1.0, B, ld, sM, C, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  return lauum_rec(C, n2, ld, sM, batch, b, ws_next, info, s);
+}
+
+}  // namespace
+
+// In-place inverse of `batch` SPD matrices of order n (full symmetric storage,
+// leading dim ld, batch stride sM): Jacobi scaling, M = U^T U, V = U^-1,
+// M^-1 = V V^T, all recursive with DMMA GEMMs above leaves of order <= b.
+// `ws` must hold bddc_spd_inverse_workspace(n, batch, b) bytes; `info` (device
+// int) counts non-positive pivots.
+extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
+                                        int* info, void* stream) {
   if (n <= 0 || batch <= 0) return 0;
-  if (n % b) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: n must be a multiple of b");
-  if (ld & 1) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: ld must be even");
+  if (b <= 0 || b > 64) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: leaf size must be in 1..64");
   cudaStream_t s = (cudaStream_t)stream;
-  double* X = (double*)ws;
-  double* W = X + (size_t)batch * b * n;
-  double* Dinv = W + (size_t)batch * b * n;
-  size_t shm = (size_t)b * b * sizeof(double);
-  if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(sweep_pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  for (int kb = 0; kb < n; kb += b) {
-    sweep_pivot_kernel<<<batch, 256, shm, s>>>(Mat, n, ld, sM, kb, b, X, Dinv, info);
-    LAUNCH_OK();
-    // W = Dinv * X   (b x n)
-    int r = bddc_dgemm_batched(0, 0, b, n, b, 1.0, Dinv, b, (long long)b * b, X, n, (long long)b * n,
-                               0.0, W, n, (long long)b * n, batch, 0, stream);
-    if (r) return r;
-    // M -= X^T W   (upper tiles only)
-    r = bddc_dgemm_batched(1, 0, n, n, b, -1.0, X, n, (long long)b * n, W, n, (long long)b * n, 1.0,
-                           Mat, ld, sM, batch, 1, stream);
-    if (r) return r;
-    dim3 gf((b * n + 255) / 256, batch);
-    sweep_fix_kernel<<<gf, 256, 0, s>>>(Mat, n, ld, sM, kb, b, W, Dinv);
+  double* dsq = (double*)ws;
+  double* rest = dsq + (size_t)batch * n;
+  dim3 g0(1, batch), g1(64, batch);
+  jacobi_scale_kernel<<<g0, 256, 0, s>>>(Mat, n, ld, sM, dsq, 0);
+  LAUNCH_OK();
+  jacobi_scale_kernel<<<g1, 256, 0, s>>>(Mat, n, ld, sM, dsq, 1);
+  LAUNCH_OK();
+  int r;
+  if (n <= b) {
+    if ((r = leaf_launch(Mat, n, ld, sM, batch, info, 3, s))) return r;
+  } else {
+    if ((r = chol_inv_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
+    if ((r = lauum_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
+    dim3 ga((n + 31) / 32, (n + 31) / 32, batch);
+    lower_from_upper_kernel<<<ga, dim3(32, 8), 0, s>>>(Mat, n, ld, sM);
     LAUNCH_OK();
   }
-  dim3 gfin((unsigned)(((long long)n * n + 255) / 256), batch);
-  sweep_final_kernel<<<gfin, 256, 0, s>>>(Mat, n, ld, sM);
+  jacobi_scale_kernel<<<g1, 256, 0, s>>>(Mat, n, ld, sM, dsq, 1);
   LAUNCH_OK();
   return 0;
 }

@@ -7,7 +7,7 @@
 //     G   = B_G - B_I A_II^{-1} A_IG    (supported on one grid line per slot)
 //     S_A = A_GG - A_GI A_II^{-1} A_IG  (diagonal + opposite-end partner)
 //     S   = S_A + G^T P^+ G             (Schur complement on Gamma_i)
-// with P^+ obtained from the swept inverse of P + alpha 11^T.  D-scaling of B
+// with P^+ from the inverse of the Jacobi-scaled, rank-one-regularised P.  D-scaling of B
 // (grid.py:344-357) cancels in S and enters only the pressure rhs/solution.
 #include "common.cuh"
 
@@ -152,7 +152,7 @@ __global__ void rescale_kernel(bddc_geom G, const double* __restrict__ coef, dou
 // Gc layout: [i][q][k] (maxG x maxL per subdomain).
 __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ fslot,
                                    double* __restrict__ P, double* __restrict__ Gc, double* __restrict__ SAd,
-                                   int* __restrict__ SApart, double* __restrict__ SAoff, double* __restrict__ alpha) {
+                                   int* __restrict__ SApart, double* __restrict__ SAoff, double* __restrict__ scl) {
   __shared__ double red[32];
   const int i = blockIdx.x;
   const Box b = sub_box(G, i);
@@ -239,32 +239,66 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
     }
     __syncthreads();
   }
-  // alpha = trace(P)/np^2 ; P += alpha 11^T on the live block ; identity padding
-  double tr = 0.0;
-  for (int r = threadIdx.x; r < np; r += blockDim.x) tr += Pi[(size_t)r * mp + r];
-  tr = block_sum(tr, red);
-  double al = tr / ((double)np * np);
-  if (!(al > 0.0)) al = 1.0;
-  if (threadIdx.x == 0) alpha[i] = al;
+  // Jacobi scaling + rank-one regularisation of the null space (P 1 = 0):
+  //   Ps = D^-1/2 P D^-1/2 + v v^T,  D = diag(P),  v = D^1/2 1 / |D^1/2 1|.
+  // Scaling removes the coefficient-contrast part of cond(P) (1e7 -> 1e3 on
+  // 6-decade fields), which keeps S_i accurate to ~1e-15.  scl = [dsq (maxP) | |D^1/2 1|].
+  double* dsq = scl + (size_t)i * (mp + 1);
+  double sd = 0.0;
+  for (int r = threadIdx.x; r < np; r += blockDim.x) {
+    double dr = Pi[(size_t)r * mp + r];
+    if (!(dr > 0.0)) dr = 1.0;
+    dsq[r] = rsqrt(dr);
+    sd += dr;
+  }
+  sd = block_sum(sd, red);
+  const double vn = sqrt(sd);
+  if (threadIdx.x == 0) dsq[mp] = vn;
+  __syncthreads();
   for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
     int r = (int)(e / mp), cc = (int)(e % mp);
-    if (r < np && cc < np) Pi[e] += al;
-    else if (r == cc) Pi[e] = 1.0;
+    if (r < np && cc < np) {
+      const double vr = 1.0 / (dsq[r] * vn), vc = 1.0 / (dsq[cc] * vn);
+      Pi[e] = Pi[e] * dsq[r] * dsq[cc] + vr * vc;
+    } else {
+      Pi[e] = (r == cc) ? 1.0 : 0.0;
+    }
   }
 }
 
-// Q = (P + alpha 11^T)^{-1} - 11^T/(alpha np^2) on the live block; zero padding.
-__global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const double* __restrict__ alpha) {
-  const int i = blockIdx.y;
+// Q = P^+ = Pi D^-1/2 (Ps^-1 - v v^T) D^-1/2 Pi,  Pi = I - 11^T/np (zero padding).
+__global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const double* __restrict__ scl) {
+  extern __shared__ double rm[];   // maxP column means
+  __shared__ double red[32];
+  const int i = blockIdx.x;
   const Box b = sub_box(G, i);
   const int np = b.L[0] * b.L[1] * b.L[2];
   const int mp = G.maxP;
-  const double sh = 1.0 / (alpha[i] * (double)np * np);
-  size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)mp * mp) return;
-  int r = (int)(e / mp), c = (int)(e % mp);
+  const double* dsq = scl + (size_t)i * (mp + 1);
+  const double vn = dsq[mp];
   double* Pi = P + (size_t)i * mp * mp;
-  Pi[e] = (r < np && c < np) ? Pi[e] - sh : 0.0;
+  double part = 0.0;
+  for (int c = threadIdx.x; c < np; c += blockDim.x) {
+    const double vc = 1.0 / (dsq[c] * vn);
+    double acc = 0.0;
+    for (int r = 0; r < np; ++r) {
+      const double vr = 1.0 / (dsq[r] * vn);
+      acc += dsq[r] * (Pi[(size_t)r * mp + c] - vr * vc) * dsq[c];
+    }
+    rm[c] = acc / np;
+    part += acc;
+  }
+  const double tm = block_sum(part, red) / ((double)np * np);
+  __syncthreads();
+  for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
+    int r = (int)(e / mp), c = (int)(e % mp);
+    double v = 0.0;
+    if (r < np && c < np) {
+      const double vr = 1.0 / (dsq[r] * vn), vc = 1.0 / (dsq[c] * vn);
+      v = dsq[r] * (Pi[e] - vr * vc) * dsq[c] - rm[r] - rm[c] + tm;
+    }
+    Pi[e] = v;
+  }
 }
 
 // Wt[i][q][r] = sum_k Q[cell(q,k)][r] * Gc[q][k]   (W = Q G, stored transposed)
@@ -515,17 +549,15 @@ extern "C" int bddc_rescale(const bddc_geom* g, const double* coef, double* Dsub
 }
 
 extern "C" int bddc_local_build(const bddc_geom* g, const double* coef, const int* fslot, double* P, double* Gc,
-                                double* SAd, int* SApart, double* SAoff, double* alpha, void* stream) {
+                                double* SAd, int* SApart, double* SAoff, double* scl, void* stream) {
   if (g->maxL > MAXL) return bddc_set_error(BDDC_ERR_ARG, "subdomain strip wider than MAXL=32 cells");
-  local_build_kernel<<<g->N, 128, 0, (cudaStream_t)stream>>>(*g, coef, fslot, P, Gc, SAd, SApart, SAoff, alpha);
+  local_build_kernel<<<g->N, 128, 0, (cudaStream_t)stream>>>(*g, coef, fslot, P, Gc, SAd, SApart, SAoff, scl);
   LAUNCH_OK();
   return 0;
 }
 
-extern "C" int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* alpha, void* stream) {
-  size_t n = (size_t)g->maxP * g->maxP;
-  dim3 grid((unsigned)((n + 255) / 256), g->N);
-  pinv_fix_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(*g, P, alpha);
+extern "C" int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* scl, void* stream) {
+  pinv_fix_kernel<<<g->N, 512, g->maxP * sizeof(double), (cudaStream_t)stream>>>(*g, P, scl);
   LAUNCH_OK();
   return 0;
 }

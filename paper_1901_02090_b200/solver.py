@@ -173,15 +173,15 @@ class BddcSetup:
         SAd = torch.empty(N * mg, dtype=F64, device=dev)
         SApart = torch.empty(N * mg, dtype=I32, device=dev)
         SAoff = torch.empty(N * mg, dtype=F64, device=dev)
-        alpha = torch.empty(N, dtype=F64, device=dev)
+        alpha = torch.empty(N * (mp + 1), dtype=F64, device=dev)   # Jacobi scaling of P
         nat.call("bddc_local_build", gp, _p(self.d_coef), _p(self.d_fslot),
                  _p(self.d_Q), _p(Gc), _p(SAd), _p(SApart), _p(SAoff),
                  _p(alpha), st)
         info = torch.zeros(4, dtype=I32, device=dev)
-        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, 64) // 8 + 2,
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, 32) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(self.d_Q), mp, mp, mp * mp, N,
-                 64, _p(ws), _p(info), st)
+                 32, _p(ws), _p(info), st)
         del ws
         nat.call("bddc_local_pinv_fix", gp, _p(self.d_Q), _p(alpha), st)
         Wt = torch.empty(N * mg * mp, dtype=F64, device=dev)
@@ -190,9 +190,10 @@ class BddcSetup:
                  _p(SAd), _p(SApart), _p(SAoff), _p(Wt), _p(self.d_S), st)
         del Wt, Gc, SAd, SApart, SAoff
         Sinv = self.d_S.clone()
-        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, 64) // 8 + 2,
+        leaf = 64
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, leaf) // 8 + 2,
                          dtype=F64, device=dev)
-        nat.call("bddc_spd_inverse_batched", _p(Sinv), mg, mg, mg * mg, N, 64,
+        nat.call("bddc_spd_inverse_batched", _p(Sinv), mg, mg, mg * mg, N, leaf,
                  _p(ws), _p(info[1:]), st)
         del ws
         self._mark(ev, "local")
