@@ -142,12 +142,16 @@ int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, const int* cm
                      int nfc, const double* Kc, const int* sub_rows, const double* b0, int maxC,
                      void* stream);
 /* Solves on the compact per-node layout (info = {s, bf, sep_ptr, bnd_ptr, cb_off}). */
-int bddc_nd_fwd(int ntasks, int smax, const int* tasks, const int* info, const long long* data_off,
-                const int* sep_flat, const int* lptr, const int* lsrc, const double* Fc,
-                const double* r, double* ybuf, double* cbuf, void* stream);
-int bddc_nd_bwd(int ntasks, int bfmax, const int* tasks, const int* info, const long long* data_off,
-                const int* sep_flat, const int* bnd_flat, const double* Fc, const double* ybuf,
-                double* x, void* stream);
+/* tasks are triplets {node, row0, row1}; fwd gathers the level's separator
+ * right-hand sides into rsbuf (ysize entries) first. */
+int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
+                const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
+                const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
+                void* stream);
+/* bwd: wpr (1, 2, 4, 8) warps share one separator row (tasks then hold 8/wpr rows per pass). */
+int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
+                const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
+                const double* ybuf, double* x, void* stream);
 int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
                     const long long* data_off, double* Fc, void* stream);
 /* Root pressure block of the pinned coarse solve: x_p = -Pc^-1 (r_p - contributions). */

@@ -251,7 +251,13 @@ class CoarseND:
             src = srcs[idx] if len(idx) else np.zeros(1, np.int64)
             return ptr, src.astype(np.int32)
 
-        rows_per_task = 32
+        def rows_per_task(total):
+            # warp per row, 8 warps per CTA: aim for >= ~8 CTAs per SM per level
+            r = 8
+            while r < 64 and total / (2 * r) >= 148 * 8:
+                r *= 2
+            return r
+
         for L in self.levels:
             sep_flat = np.concatenate([nodes[k]["sep"] for k in L.ids]).astype(np.int64)
             bnd_flat = np.concatenate([nodes[k]["bnd"] for k in L.ids] + [np.zeros(0, np.int64)])
@@ -263,19 +269,27 @@ class CoarseND:
             lptr, lsrc = lists(sep_flat)
             info = np.stack([L.s, L.b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off], axis=1).astype(np.int32)
             ft_, bt_ = [], []
+            rf = rows_per_task(int((L.s + L.b).sum()))
+            # backward rows are long (b): split a row over wpr warps when the
+            # level has too few rows to fill the GPU
+            L.wpr = 1
+            while L.wpr < 8 and int(L.s.sum()) * L.wpr < 148 * 8 * 4 and int(L.b.max()) >= 128 * L.wpr:
+                L.wpr *= 2
+            rb = rows_per_task(int(L.s.sum()) * max(1, int(L.b.max()) // 64)) if L.wpr == 1 else 8 // L.wpr
             for q in range(L.m):
-                for r0 in range(0, int(L.s[q] + L.b[q]), rows_per_task):
-                    ft_.append((q, r0))
-                for k0 in range(0, int(L.s[q]), 32):
-                    bt_.append((q, k0))
+                nr, ns = int(L.s[q] + L.b[q]), int(L.s[q])
+                for r0 in range(0, nr, rf):
+                    ft_.append((q, r0, min(r0 + rf, nr)))
+                for k0 in range(0, ns, rb):
+                    bt_.append((q, k0, min(k0 + rb, ns)))
             L.info = t(info)
             L.data_off = t(data_off[:-1].astype(np.int64), torch.int64)
             L.sep_flat = t(sep_flat.astype(np.int32))
             L.bnd_flat = t(bnd_flat.astype(np.int32) if len(bnd_flat) else np.zeros(1, np.int32))
             L.lptr = t(lptr)
             L.lsrc = t(lsrc)
-            L.ftasks = t(np.array(ft_, dtype=np.int32).reshape(-1, 2))
-            L.btasks = t(np.array(bt_, dtype=np.int32).reshape(-1, 2))
+            L.ftasks = t(np.array(ft_, dtype=np.int32).reshape(-1, 3))
+            L.btasks = t(np.array(bt_, dtype=np.int32).reshape(-1, 3))
             L.n_ft, L.n_bt = len(ft_), len(bt_)
             L.smax = int(L.s.max())
             L.bmax = int(L.b.max())
@@ -342,13 +356,14 @@ class CoarseND:
         st = _stream()
         ys, cb = self._bufs()
         for li, L in enumerate(self.levels):
-            nat.call("bddc_nd_fwd", L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
-                     _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(ys[li]), _p(cb), st)
+            nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
+                     _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
+                     _p(cb), st)
         nat.call("bddc_nd_pressure", self.N, self.nfc, npc, _p(self.pptr), _p(self.psrc), _p(cb),
                  _p(Pcinv), _p(r), _p(self._prhs), _p(x), st)
         for li in range(len(self.levels) - 1, -1, -1):
             L = self.levels[li]
-            nat.call("bddc_nd_bwd", L.n_bt, L.bmax, _p(L.btasks), _p(L.info), _p(L.data_off),
+            nat.call("bddc_nd_bwd", L.n_bt, L.bmax, L.wpr, _p(L.btasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.bnd_flat), _p(L.Fc), _p(ys[li]), _p(x), st)
 
     def _bufs(self):
@@ -357,4 +372,5 @@ class CoarseND:
             cb = torch.empty(self.cb_total, dtype=F64, device=self.dev)
             self._yb = (ys, cb)
             self._prhs = torch.empty(max(self.N, 1), dtype=F64, device=self.dev)
+            self._rs = torch.empty(max(max(L.ysize for L in self.levels), 1), dtype=F64, device=self.dev)
         return self._yb

@@ -3,7 +3,9 @@
 //  * bddc_dgemm_batched: C[b] = alpha*op(A[b])*op(B[b]) + beta*C[b], row-major,
 //    64x64x16 CTA tiles, 4 warps x (32x32) warp tiles of mma.sync m8n8k4 f64
 //    (SASS DMMA.8x8x4), cp.async double-buffered shared-memory staging.
-//    Optional upper-tile mask for symmetric updates.
+//    `upper` flags: 1 = upper tiles only (symmetric results); 2/4 = op(A)
+//    upper/lower triangular, 8/16 = op(B) upper/lower triangular (skip the
+//    K blocks that are zero for the tile).
 //  * bddc_spd_inverse_batched: in-place inverse of a batch of SPD matrices the
 //    LAPACK potrf -> trtri -> lauum way (M = U^T U, V = U^-1, M^-1 = V V^T),
 //    each phase recursive 2x2-blocked with large-K DMMA GEMMs and leaves
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
                                                     double beta, double* __restrict__ C, int ldc,
                                                     long long sC, int upper) {
   const int bn = blockIdx.x, bm = blockIdx.y, bz = blockIdx.z;
-  if (upper && bm > bn) return;
+  if ((upper & 1) && bm > bn) return;
   A += bz * sA;
   B += bz * sB;
   C += bz * sC;
@@ -133,12 +135,22 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nk = (K + BK - 1) / BK;
+  // triangular operands: only the K range that can be nonzero for this tile
+  int kbeg = 0, kend = K;
+  if (upper & 2) kbeg = max(kbeg, m0);           // op(A) upper: k >= m
+  if (upper & 4) kend = min(kend, m0 + BM);      // op(A) lower: k <= m
+  if (upper & 8) kend = min(kend, n0 + BN);      // op(B) upper: k <= n
+  if (upper & 16) kbeg = max(kbeg, n0);          // op(B) lower: k >= n
+  kbeg = (kbeg / BK) * BK;
+  const int kt0 = kbeg / BK;
+  const int nk = (kend > kbeg) ? (kend + BK - 1) / BK : kt0;
+  if (kt0 < nk) {
   // A operand rows are m (R = M); B operand rows are n (R = N).
-  load_tile<transA, aligned>(As[0], A, lda, M, K, m0, 0);
-  load_tile<!transB, aligned>(Bs[0], B, ldb, N, K, n0, 0);
+  load_tile<transA, aligned>(As[kt0 & 1], A, lda, M, K, m0, kbeg);
+  load_tile<!transB, aligned>(Bs[kt0 & 1], B, ldb, N, K, n0, kbeg);
   cp_async_commit();
-  for (int kt = 0; kt < nk; ++kt) {
+  }
+  for (int kt = kt0; kt < nk; ++kt) {
     if (kt + 1 < nk) {
       load_tile<transA, aligned>(As[(kt + 1) & 1], A, lda, M, K, m0, (kt + 1) * BK);
       load_tile<!transB, aligned>(Bs[(kt + 1) & 1], B, ldb, N, K, n0, (kt + 1) * BK);
@@ -390,11 +402,11 @@ int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, doubl
   const long long sW = (long long)n1 * n2;
   int r;
   if ((r = chol_inv_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
-  if ((r = bddc_dgemm_batched(1, 0, n1, n2, n1, 1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = bddc_dgemm_batched(1, 0, n1, n2, n1, 1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 4, s))) return r;
   if ((r = bddc_dgemm_batched(1, 0, n2, n2, n1, -1.0, W, n2, sW, W, n2, sW, 1.0, C, ld, sM, batch, 1, s))) return r;
   if ((r = chol_inv_rec(C, n2, ld, sM, batch, b, ws_next, info, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 0, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 8, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 2, s))) return r;
   if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
   return block_copy(M + (size_t)n1 * ld, ld, sM, nullptr, 0, 0, n2, n1, batch, s);
 }
@@ -413,7 +425,7 @@ int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* 
   int r;
   if ((r = lauum_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
   if ((r = bddc_dgemm_batched(0, 1, n1, n1, n2, 1.0, B, ld, sM, B, ld, sM, 1.0, A, ld, sM, batch, 1, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 1, n1, n2, n2, 1.0, B, ld, sM, C, ld, sM, 0.0, W, n2, sW, batch, 0, s))) return r;
+  if ((r = bddc_dgemm_batched(0, 1, n1, n2, n2, 1.0, B, ld, sM, C, ld, sM, 0.0, W, n2, sW, batch, 16, s))) return r;
   if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
   return lauum_rec(C, n2, ld, sM, batch, b, ws_next, info, s);
 }

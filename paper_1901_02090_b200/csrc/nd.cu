@@ -53,45 +53,66 @@ __global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K,
 }
 
 // Compact per-node solve layout (see coarse_nd.py): info[q] = {s, b, sep_ptr,
-// bnd_ptr, cb_off}; node data at data_off[q]: F11inv (s x s) then X (b x s) over the
-// whole boundary (flux dofs and pressures, indices into the combined vector).
+// bnd_ptr, cb_off}; node data at data_off[q]: F11inv (s x s), X (b x s) over the
+// whole boundary (flux dofs and pressures, indices into the combined vector),
+// then X^T (s x b).
 
-// Forward (left-looking), one task = 32 rows of one node:
-// r_sep[k] = r[g_k] - sum of descendant contributions (fixed list order),
+// Warp dot product of a global row with a shared-memory vector; 8 independent
+// accumulators keep 8 loads per lane in flight (fixed order: deterministic).
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ row, const double* v, int len, int lane) {
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.0;
+  int c = lane;
+  for (; c + 224 < len; c += 256) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(row + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += x[u] * v[c + 32 * u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (c + 32 * u < len) a[u] += __ldg(row + c + 32 * u) * v[c + 32 * u];
+  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Forward gather (left-looking), 8 lanes per separator entry of the level:
+// rs[t] = r[g_t] - sum of the descendants' update entries (lane-strided over the
+// list, fixed shuffle tree: deterministic).
+__global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const int* __restrict__ lptr,
+                                 const int* __restrict__ lsrc, const double* __restrict__ cbuf,
+                                 const double* __restrict__ r, double* __restrict__ rs) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = gt >> 3, sub = gt & 7;
+  double acc = 0.0;
+  if (t < n) {
+    const int p1 = lptr[t + 1];
+    for (int p = lptr[t] + sub; p < p1; p += 8) acc += cbuf[lsrc[p]];
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  if (t < n && sub == 0) rs[t] = r[sep_flat[t]] - acc;
+}
+
+// Forward GEMV, task = rows [row0, row1) of one node, warp per row:
 // rows < s: y = F11inv r_sep; rows s..s+bf-1: c = X r_sep into cbuf.
 __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
-                              const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
-                              const int* __restrict__ lptr, const int* __restrict__ lsrc,
-                              const double* __restrict__ Fc, const double* __restrict__ r,
-                              double* __restrict__ ybuf, double* __restrict__ cbuf) {
-  extern __shared__ double rs[];
-  const int q = tasks[2 * blockIdx.x], row0 = tasks[2 * blockIdx.x + 1];
-  const int s = info[5 * q], bf = info[5 * q + 1], sp = info[5 * q + 2], cbo = info[5 * q + 4];
-  for (int k = threadIdx.x; k < s; k += blockDim.x) {
-    const int t = sp + k;
-    int p = lptr[t];
-    const int p1 = lptr[t + 1];
-    double acc = 0.0;
-    for (; p + 4 <= p1; p += 4) {
-      int i0 = lsrc[p], i1 = lsrc[p + 1], i2 = lsrc[p + 2], i3 = lsrc[p + 3];
-      double c0 = cbuf[i0], c1 = cbuf[i1], c2 = cbuf[i2], c3 = cbuf[i3];
-      acc += c0;
-      acc += c1;
-      acc += c2;
-      acc += c3;
-    }
-    for (; p < p1; ++p) acc += cbuf[lsrc[p]];
-    rs[k] = r[sep_flat[t]] - acc;
-  }
+                              const long long* __restrict__ data_off, const double* __restrict__ Fc,
+                              const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf) {
+  extern __shared__ double rsm[];
+  const int q = tasks[3 * blockIdx.x], row0 = tasks[3 * blockIdx.x + 1], row1 = tasks[3 * blockIdx.x + 2];
+  const int s = info[5 * q], sp = info[5 * q + 2], cbo = info[5 * q + 4];
+  for (int k = threadIdx.x; k < s; k += blockDim.x) rsm[k] = rs[sp + k];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* base = Fc + data_off[q];
-  const int nrows = imin(row0 + 32, s + bf);
-  for (int row = row0 + warp; row < nrows; row += nw) {
-    const double* mr = base + (size_t)row * s;   // F11inv rows then X rows, both of length s
-    double acc = 0.0;
-    for (int c = lane; c < s; c += 32) acc += mr[c] * rs[c];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int row = row0 + warp; row < row1; row += nw) {
+    const double acc = warp_row_dot(base + (size_t)row * s, rsm, s, lane);
     if (lane == 0) {
       if (row < s) ybuf[sp + row] = acc;
       else cbuf[cbo + row - s] = acc;
@@ -99,26 +120,45 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
   }
 }
 
-// Backward, one task = 32 separator rows of one node: x_sep = y - X^T x_bnd with
-// X^T stored row-major (s x b) after X, so every warp streams whole rows.
+// Backward, task = separator rows [k0, k1) of one node; wpr warps per row
+// split the row's columns, partials combined in fixed order:
+// x_sep = y - X^T x_bnd with X^T stored row-major (s x b) after X.
 __global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
                               const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
                               const int* __restrict__ bnd_flat, const double* __restrict__ Fc,
-                              const double* __restrict__ ybuf, double* __restrict__ x) {
+                              const double* __restrict__ ybuf, double* __restrict__ x, int wpr) {
   extern __shared__ double xb[];  // bmax
-  const int q = tasks[2 * blockIdx.x], k0 = tasks[2 * blockIdx.x + 1];
+  __shared__ double part[8];
+  const int q = tasks[3 * blockIdx.x], k0 = tasks[3 * blockIdx.x + 1], k1 = tasks[3 * blockIdx.x + 2];
   const int s = info[5 * q], b = info[5 * q + 1], sp = info[5 * q + 2], bp = info[5 * q + 3];
   for (int m = threadIdx.x; m < b; m += blockDim.x) xb[m] = x[bnd_flat[bp + m]];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* XT = Fc + data_off[q] + (size_t)s * s + (size_t)b * s;
-  const int kend = imin(k0 + 32, s);
-  for (int k = k0 + warp; k < kend; k += nw) {
-    const double* row = XT + (size_t)k * b;
+  if (wpr == 1) {
+    for (int k = k0 + warp; k < k1; k += nw) {
+      const double acc = warp_row_dot(XT + (size_t)k * b, xb, b, lane);
+      if (lane == 0) x[sep_flat[sp + k]] = ybuf[sp + k] - acc;
+    }
+    return;
+  }
+  const int rpc = nw / wpr;                 // rows per pass
+  const int rl = warp / wpr, pc = warp % wpr;
+  const int chunk = ((b + wpr - 1) / wpr + 31) & ~31;
+  const int c0 = imin(pc * chunk, b), c1 = imin(c0 + chunk, b);
+  for (int kb = k0; kb < k1; kb += rpc) {
+    const int k = kb + rl;
     double acc = 0.0;
-    for (int m = lane; m < b; m += 32) acc += row[m] * xb[m];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[sep_flat[sp + k]] = ybuf[sp + k] - acc;
+    if (k < k1) acc = warp_row_dot(XT + (size_t)k * b + c0, xb + c0, c1 - c0, lane);
+    if (lane == 0) part[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x < rpc && kb + threadIdx.x < k1) {
+      double t = 0.0;
+      for (int u = 0; u < wpr; ++u) t += part[threadIdx.x * wpr + u];
+      const int kk = kb + threadIdx.x;
+      x[sep_flat[sp + kk]] = ybuf[sp + kk] - t;
+    }
+    __syncthreads();
   }
 }
 
@@ -244,14 +284,18 @@ extern "C" int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, co
   return 0;
 }
 
-extern "C" int bddc_nd_fwd(int ntasks, int smax, const int* tasks, const int* info, const long long* data_off,
-                           const int* sep_flat, const int* lptr, const int* lsrc, const double* Fc, const double* r,
-                           double* ybuf, double* cbuf, void* stream) {
-  if (ntasks <= 0) return 0;
+extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
+                           const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
+                           const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
+                           void* stream) {
+  if (ntasks <= 0 || ysize <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  nd_gather_kernel<<<(unsigned)(((long long)ysize * 8 + 255) / 256), 256, 0, st>>>(ysize, sep_flat, lptr, lsrc,
+                                                                                     cbuf, r, rsbuf);
+  LAUNCH_OK();
   size_t shm = (size_t)(smax > 0 ? smax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_fwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, lptr, lsrc, Fc, r, ybuf,
-                                                            cbuf);
+  nd_fwd_kernel<<<ntasks, 256, shm, st>>>(tasks, info, data_off, Fc, rsbuf, ybuf, cbuf);
   LAUNCH_OK();
   return 0;
 }
@@ -270,13 +314,15 @@ extern "C" int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const 
   return 0;
 }
 
-extern "C" int bddc_nd_bwd(int ntasks, int bfmax, const int* tasks, const int* info, const long long* data_off,
-                           const int* sep_flat, const int* bnd_flat, const double* Fc, const double* ybuf, double* x,
-                           void* stream) {
+extern "C" int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
+                           const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
+                           const double* ybuf, double* x, void* stream) {
+  if (wpr != 1 && wpr != 2 && wpr != 4 && wpr != 8) return bddc_set_error(BDDC_ERR_ARG, "nd_bwd: wpr must be 1, 2, 4 or 8");
   if (ntasks <= 0) return 0;
   size_t shm = (size_t)(bfmax > 0 ? bfmax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_bwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, bnd_flat, Fc, ybuf, x);
+  nd_bwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, bnd_flat, Fc, ybuf, x,
+                                                            wpr);
   LAUNCH_OK();
   return 0;
 }

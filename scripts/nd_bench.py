@@ -29,3 +29,17 @@ nd.solve(r, x, st.d_Pcinv, st.npc)
 prof = nat.profile_stop()
 for n, (cnt, t) in prof.items():
     print(n, cnt, round(t, 3), "ms")
+# device time inside a CUDA graph (no host launch overhead)
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    nd.solve(r, x, st.d_Pcinv, st.npc)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        nd.solve(r, x, st.d_Pcinv, st.npc)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(50):
+    g.replay()
+e1.record(); torch.cuda.synchronize()
+print("nd solve graph mean ms", e0.elapsed_time(e1) / 50)
