@@ -282,6 +282,8 @@ class CoarseND:
                     ft_.append((q, r0, min(r0 + rf, nr)))
                 for k0 in range(0, ns, rb):
                     bt_.append((q, k0, min(k0 + rb, ns)))
+            L.h = dict(sep_flat=sep_flat, bnd_flat=bnd_flat, sep_ptr=sep_ptr, bnd_ptr=bnd_ptr,
+                       data_off=data_off, lptr=lptr, lsrc=lsrc)
             L.info = t(info)
             L.data_off = t(data_off[:-1].astype(np.int64), torch.int64)
             L.sep_flat = t(sep_flat.astype(np.int32))
@@ -298,6 +300,92 @@ class CoarseND:
         self.pptr, self.psrc = t(pptr), t(psrc)
         self.maxC = maxC
         self.factored = False
+        self.persistent = False   # per-level launches (faster than nd_persist.cu today)
+        if self.levels:
+            self._build_persistent(nodes, pos_in_level, pptr, t)
+
+    def _build_persistent(self, nodes, pos_in_level, pptr, t):
+        """Global node table + topologically ordered work items of the one-kernel solve
+        (csrc/nd_persist.cu)."""
+        levels = self.levels
+        nb = np.cumsum([0] + [L.m for L in levels])
+        sb = np.cumsum([0] + [L.ysize for L in levels])
+        bb = np.cumsum([0] + [len(L.h["bnd_flat"]) for L in levels])
+        lb = np.cumsum([0] + [int(L.h["lptr"][-1]) for L in levels])
+        fb = np.cumsum([0] + [L.csize for L in levels])
+        self.fc_base = fb
+        gid = {k: int(nb[li] + q) for k, (li, q) in pos_in_level.items()}
+        nn = int(nb[-1])
+        NC = 11
+        tab = np.zeros((nn, NC), dtype=np.int64)
+        off = np.zeros(nn, dtype=np.int64)
+        for li, L in enumerate(levels):
+            g0 = int(nb[li])
+            tab[g0:g0 + L.m, 0] = L.s
+            tab[g0:g0 + L.m, 1] = L.b
+            tab[g0:g0 + L.m, 2] = sb[li] + L.h["sep_ptr"][:-1]
+            tab[g0:g0 + L.m, 3] = bb[li] + L.h["bnd_ptr"][:-1]
+            tab[g0:g0 + L.m, 4] = L.cb_off
+            off[g0:g0 + L.m] = fb[li] + L.h["data_off"][:-1]
+        tab[:, 5:8] = -1
+        for k, g in gid.items():
+            for slot, c in enumerate(nodes[k]["ch"]):
+                if c in gid:
+                    tab[g, 6 + slot] = gid[c]
+                    tab[gid[c], 5] = g
+        lptr_g = [np.zeros(1, np.int64)]
+        for li, L in enumerate(levels):
+            lp = L.h["lptr"].astype(np.int64)
+            lptr_g.append(lp[1:] + lb[li])
+        lptr_g = np.concatenate(lptr_g)
+        lsrc_g = np.concatenate([L.h["lsrc"][:L.h["lptr"][-1]].astype(np.int64) for L in levels]
+                                + [np.zeros(1, np.int64)])
+        G = 296   # ~2 CTAs per SM worth of items per level
+        items = []
+        for li, L in enumerate(levels):
+            g0 = int(nb[li])
+            rows = (L.s + L.b).astype(np.int64)
+            rf = max(8, -(-int(rows.sum()) // G))
+            for q in range(L.m):
+                g = g0 + q
+                nr = int(rows[q])
+                nf = 0
+                for r0 in range(0, nr, rf):
+                    items.append((2, g, r0, min(r0 + rf, nr)))
+                    nf += 1
+                tab[g, 8], tab[g, 9] = nf, 0
+        npr = max(self.N - 1, 0)
+        pg = [(3, -1, e0, min(e0 + 256, npr)) for e0 in range(0, npr, 256)]
+        pv = [(4, -1, r0, min(r0 + 8, npr)) for r0 in range(0, npr, 8)]
+        items += pg + pv
+        for li in range(len(levels) - 1, -1, -1):
+            L = levels[li]
+            g0 = int(nb[li])
+            wpr = getattr(L, "wpr", 1)
+            rb = (8 // wpr) if wpr > 1 else max(8, -(-int(L.s.sum()) // G))
+            for q in range(L.m):
+                ns = int(L.s[q])
+                nbk = 0
+                for k0 in range(0, ns, rb):
+                    items.append((5 | (wpr << 8), g0 + q, k0, min(k0 + rb, ns)))
+                    nbk += 1
+                tab[g0 + q, 10] = nbk
+        self.p_items = t(np.array(items, dtype=np.int32).reshape(-1, 4))
+        self.p_nitems = len(items)
+        self.p_nodes = t(tab.astype(np.int32))
+        self.p_nn = nn
+        self.p_off = t(off, torch.int64)
+        self.p_sep = t(np.concatenate([L.h["sep_flat"] for L in levels]).astype(np.int32))
+        bf = np.concatenate([L.h["bnd_flat"] for L in levels]).astype(np.int32)
+        self.p_bnd = t(bf if len(bf) else np.zeros(1, np.int32))
+        self.p_lptr = t(lptr_g.astype(np.int32))
+        self.p_lsrc = t(lsrc_g.astype(np.int32))
+        self.p_npg, self.p_npv = len(pg), len(pv)
+        self.p_root = int(nb[-1]) - 1
+        self.p_ysize = int(sb[-1])
+        self.p_smem = int(max(max(int(L.s.max()) for L in levels),
+                              max(int(L.b.max()) for L in levels) + 8, npr, 1))
+        self.p_cnt = torch.zeros(3 + 3 * nn, dtype=I32, device=self.dev)
 
     # --------------------------------------------------------------- numeric
 
@@ -334,8 +422,9 @@ class CoarseND:
         if int(info.item()):
             raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
         self.factored = True
-        for L in self.levels:
-            L.Fc = torch.empty(max(L.csize, 1), dtype=F64, device=self.dev)
+        self.Fc_all = torch.empty(max(int(self.fc_base[-1]), 1), dtype=F64, device=self.dev)
+        for li, L in enumerate(self.levels):
+            L.Fc = self.Fc_all[int(self.fc_base[li]):int(self.fc_base[li]) + max(L.csize, 1)]
             nat.call("bddc_nd_compact", L.m, L.S, L.nf, L.B, _p(L.F), _p(L.X), _p(L.info),
                      _p(L.data_off), _p(L.Fc), st)
         # bytes streamed per solve: F11inv + X (forward) + X^T (backward)
@@ -355,6 +444,14 @@ class CoarseND:
         """
         st = _stream()
         ys, cb = self._bufs()
+        if self.persistent and self.levels:
+            nat.call("bddc_nd_solve_persist", self.p_nitems, _p(self.p_items), self.p_nn,
+                     _p(self.p_nodes), _p(self.p_off), _p(self.p_sep), _p(self.p_bnd),
+                     _p(self.p_lptr), _p(self.p_lsrc), _p(self.pptr), _p(self.psrc),
+                     _p(self.Fc_all), _p(Pcinv), _p(r), _p(self._rs_all), _p(self._y_all), _p(cb),
+                     _p(self._prhs), _p(x), _p(self.p_cnt), self.p_root, self.N, self.nfc, npc,
+                     self.p_npg, self.p_npv, self.p_smem, 0, st)
+            return
         for li, L in enumerate(self.levels):
             nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
@@ -373,4 +470,7 @@ class CoarseND:
             self._yb = (ys, cb)
             self._prhs = torch.empty(max(self.N, 1), dtype=F64, device=self.dev)
             self._rs = torch.empty(max(max(L.ysize for L in self.levels), 1), dtype=F64, device=self.dev)
+            py = max(getattr(self, "p_ysize", 0), 1)
+            self._rs_all = torch.empty(py, dtype=F64, device=self.dev)
+            self._y_all = torch.empty(py, dtype=F64, device=self.dev)
         return self._yb

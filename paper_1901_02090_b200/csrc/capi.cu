@@ -22,4 +22,7 @@ extern "C" size_t bddc_geom_size(void) { return sizeof(bddc_geom); }
 // is followed by LAUNCH_OK, which counts it).  Used by bench.py.
 static unsigned long long g_launches = 0;
 extern "C" void bddc_count_launch(void) { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+static int g_pdl = 1;
+extern "C" int bddc_pdl_enabled(void) { return g_pdl; }
+extern "C" void bddc_set_pdl(int on) { g_pdl = on ? 1 : 0; }
 extern "C" unsigned long long bddc_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }

@@ -26,6 +26,108 @@ extern "C" int bddc_set_error(int code, const char* msg);
 __host__ __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 
+// Ampere-style asynchronous global->shared copies (LDGSTS): every copy of a
+// staged tile is in flight at once, independent of the compiler's load schedule.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// start while its stream predecessor is still running.  Everything it does
+// before pdl_wait() must touch only data no earlier kernel writes (index
+// tables, factors); pdl_wait() returns once the predecessor grid completed and
+// its memory is visible.  pdl_trigger() lets the successor launch early.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+extern "C" int bddc_pdl_enabled(void);
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t shm, cudaStream_t s,
+                                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = shm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = bddc_pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+#define PDL_LAUNCH(kernel, grid, block, shm, stream, ...)                  \
+  do {                                                                    \
+    bddc_count_launch();                                                  \
+    cudaError_t _e = launch_pdl(kernel, grid, block, shm, stream, __VA_ARGS__); \
+    if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
+  } while (0)
+
+// Warp GEMV helpers over row-major rows (read-only matrix via the non-coherent
+// path, vector in shared memory).  Fixed summation order: deterministic.
+
+// One long row: 8 independent accumulators keep 8 loads per lane in flight.
+__device__ __forceinline__ double warp_row_dot(const double* __restrict__ row, const double* v, int len, int lane) {
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.0;
+  int c = lane;
+  for (; c + 224 < len; c += 256) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(row + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += x[u] * v[c + 32 * u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (c + 32 * u < len) a[u] += __ldg(row + c + 32 * u) * v[c + 32 * u];
+  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Four short rows at once (rows base + k*ld, k < nr <= 4): 16 loads per lane in
+// flight, so rows of ~100 entries do not serialise on memory latency.
+__device__ __forceinline__ void warp_rows4_dot(const double* __restrict__ base, size_t ld, int nr,
+                                               const double* v, int len, int lane, double out[4]) {
+  double a[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < len; c0 += 128) {
+    double x[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + lane + 32 * u;
+        x[k][u] = (k < nr && c < len) ? __ldg(base + (size_t)k * ld + c) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + lane + 32 * u;
+      const double vv = (c < len) ? v[c] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] += x[k][u] * vv;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+    out[k] = a[k];
+  }
+}
+
 // Subdomain box of subdomain i under a regular partition.
 struct Box {
   int o[3];   // origin (cells)

@@ -25,13 +25,6 @@ constexpr int LDK = BK + 4;    // [m][k] layout stride (doubles)
 constexpr int LDM = BM + 4;    // [k][m] layout stride (doubles)
 constexpr int TILE_ELEMS = (BM * LDK > BK * LDM) ? BM * LDK : BK * LDM;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -42,10 +35,6 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // Load a BM x BK (or BK x BM when K-major) operand tile into shared memory.
 // kmajor == false: element (r, k) at g[(r0+r)*ld + k0 + k]  -> s[r*LDK + k]
 // kmajor == true : element (r, k) at g[(k0+k)*ld + r0 + r]  -> s[k*LDM + r]
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
 
 template <bool kmajor, bool aligned>
 __device__ __forceinline__ void load_tile(double* s, const double* g, int ld, int R, int K,

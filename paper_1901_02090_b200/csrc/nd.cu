@@ -57,65 +57,72 @@ __global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K,
 // whole boundary (flux dofs and pressures, indices into the combined vector),
 // then X^T (s x b).
 
-// Warp dot product of a global row with a shared-memory vector; 8 independent
-// accumulators keep 8 loads per lane in flight (fixed order: deterministic).
-__device__ __forceinline__ double warp_row_dot(const double* __restrict__ row, const double* v, int len, int lane) {
-  double a[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) a[u] = 0.0;
-  int c = lane;
-  for (; c + 224 < len; c += 256) {
-    double x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = __ldg(row + c + 32 * u);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] += x[u] * v[c + 32 * u];
-  }
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    if (c + 32 * u < len) a[u] += __ldg(row + c + 32 * u) * v[c + 32 * u];
-  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc;
-}
-
 // Forward gather (left-looking), 8 lanes per separator entry of the level:
 // rs[t] = r[g_t] - sum of the descendants' update entries (lane-strided over the
 // list, fixed shuffle tree: deterministic).
 __global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const int* __restrict__ lptr,
                                  const int* __restrict__ lsrc, const double* __restrict__ cbuf,
                                  const double* __restrict__ r, double* __restrict__ rs) {
+  pdl_trigger();
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = gt >> 3, sub = gt & 7;
-  double acc = 0.0;
+  int p = 0, p1 = 0, g = 0;
   if (t < n) {
-    const int p1 = lptr[t + 1];
-    for (int p = lptr[t] + sub; p < p1; p += 8) acc += cbuf[lsrc[p]];
+    p = lptr[t] + sub;
+    p1 = lptr[t + 1];
+    g = sep_flat[t];
   }
+  pdl_wait();
+  double acc = 0.0;
+  for (; p < p1; p += 8) acc += cbuf[lsrc[p]];
   acc += __shfl_xor_sync(0xffffffffu, acc, 4);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-  if (t < n && sub == 0) rs[t] = r[sep_flat[t]] - acc;
+  if (t < n && sub == 0) rs[t] = r[g] - acc;
 }
 
-// Forward GEMV, task = rows [row0, row1) of one node, warp per row:
+// Forward GEMV, task = rows [row0, row1) of one node, 4 rows per warp pass:
 // rows < s: y = F11inv r_sep; rows s..s+bf-1: c = X r_sep into cbuf.
+// lpe > 0: the task gathers r_sep itself, lpe lanes per separator entry (small
+// separators: saves the separate gather launch); lpe == 0: r_sep from rs.
 __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
-                              const long long* __restrict__ data_off, const double* __restrict__ Fc,
-                              const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf) {
+                              const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
+                              const int* __restrict__ lptr, const int* __restrict__ lsrc,
+                              const double* __restrict__ Fc, const double* __restrict__ r,
+                              const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf,
+                              int lpe) {
   extern __shared__ double rsm[];
+  pdl_trigger();
   const int q = tasks[3 * blockIdx.x], row0 = tasks[3 * blockIdx.x + 1], row1 = tasks[3 * blockIdx.x + 2];
   const int s = info[5 * q], sp = info[5 * q + 2], cbo = info[5 * q + 4];
-  for (int k = threadIdx.x; k < s; k += blockDim.x) rsm[k] = rs[sp + k];
+  const double* base = Fc + data_off[q];
+  pdl_wait();
+  if (lpe > 0) {
+    const int per = blockDim.x / lpe, sub = threadIdx.x % lpe;
+    for (int tb = 0; tb < s; tb += per) {
+      const int t = tb + threadIdx.x / lpe;
+      double acc = 0.0;
+      if (t < s) {
+        const int p1 = lptr[sp + t + 1];
+        for (int p = lptr[sp + t] + sub; p < p1; p += lpe) acc += cbuf[lsrc[p]];
+      }
+      for (int o = lpe >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (t < s && sub == 0) rsm[t] = r[sep_flat[sp + t]] - acc;
+    }
+  } else {
+    for (int k = threadIdx.x; k < s; k += blockDim.x) rsm[k] = rs[sp + k];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* base = Fc + data_off[q];
-  for (int row = row0 + warp; row < row1; row += nw) {
-    const double acc = warp_row_dot(base + (size_t)row * s, rsm, s, lane);
-    if (lane == 0) {
-      if (row < s) ybuf[sp + row] = acc;
-      else cbuf[cbo + row - s] = acc;
+  for (int row = row0 + 4 * warp; row < row1; row += 4 * nw) {
+    const int nr = imin(4, row1 - row);
+    double acc[4];
+    warp_rows4_dot(base + (size_t)row * s, s, nr, rsm, s, lane, acc);
+    if (lane < nr) {
+      const double v = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      const int rr = row + lane;
+      if (rr < s) ybuf[sp + rr] = v;
+      else cbuf[cbo + rr - s] = v;
     }
   }
 }
@@ -129,16 +136,23 @@ __global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restri
                               const double* __restrict__ ybuf, double* __restrict__ x, int wpr) {
   extern __shared__ double xb[];  // bmax
   __shared__ double part[8];
+  pdl_trigger();
   const int q = tasks[3 * blockIdx.x], k0 = tasks[3 * blockIdx.x + 1], k1 = tasks[3 * blockIdx.x + 2];
   const int s = info[5 * q], b = info[5 * q + 1], sp = info[5 * q + 2], bp = info[5 * q + 3];
+  pdl_wait();
   for (int m = threadIdx.x; m < b; m += blockDim.x) xb[m] = x[bnd_flat[bp + m]];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* XT = Fc + data_off[q] + (size_t)s * s + (size_t)b * s;
   if (wpr == 1) {
-    for (int k = k0 + warp; k < k1; k += nw) {
-      const double acc = warp_row_dot(XT + (size_t)k * b, xb, b, lane);
-      if (lane == 0) x[sep_flat[sp + k]] = ybuf[sp + k] - acc;
+    for (int k = k0 + 4 * warp; k < k1; k += 4 * nw) {
+      const int nr = imin(4, k1 - k);
+      double acc[4];
+      warp_rows4_dot(XT + (size_t)k * b, b, nr, xb, b, lane, acc);
+      if (lane < nr) {
+        const double v = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+        x[sep_flat[sp + k + lane]] = ybuf[sp + k + lane] - v;
+      }
     }
     return;
   }
@@ -193,7 +207,9 @@ __global__ void nd_compact_kernel(int S, int nf, int B, const double* __restrict
 __global__ void nd_pressure_gather_kernel(int N, int nfc, const int* __restrict__ pptr, const int* __restrict__ psrc,
                                           const double* __restrict__ cbuf, const double* __restrict__ r,
                                           double* __restrict__ rp) {
+  pdl_trigger();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
   if (i >= N - 1) return;
   double acc = 0.0;
   for (int p = pptr[i]; p < pptr[i + 1]; ++p) acc += cbuf[psrc[p]];
@@ -202,8 +218,10 @@ __global__ void nd_pressure_gather_kernel(int N, int nfc, const int* __restrict_
 
 __global__ void nd_pressure_gemv_kernel(int N, int nfc, int npc, const double* __restrict__ Pcinv,
                                         const double* __restrict__ rp, double* __restrict__ x) {
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  pdl_wait();
   if (row == 0 && lane == 0) x[nfc] = 0.0;
   if (row >= N - 1) return;
   const double* mr = Pcinv + (size_t)row * npc;
@@ -290,13 +308,16 @@ extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, co
                            void* stream) {
   if (ntasks <= 0 || ysize <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  nd_gather_kernel<<<(unsigned)(((long long)ysize * 8 + 255) / 256), 256, 0, st>>>(ysize, sep_flat, lptr, lsrc,
-                                                                                     cbuf, r, rsbuf);
-  LAUNCH_OK();
+  // small separators: every task gathers its own r_sep (lanes per entry so one
+  // pass covers the separator); large ones: a separate level-wide gather
+  const int lpe = (smax <= 32 && ntasks <= 2 * ysize / (smax > 0 ? smax : 1)) ? 8 : 0;
+  if (lpe == 0)
+    PDL_LAUNCH(nd_gather_kernel, dim3((unsigned)(((long long)ysize * 8 + 255) / 256)), dim3(256), 0, st, ysize,
+               sep_flat, lptr, lsrc, (const double*)cbuf, r, rsbuf);
   size_t shm = (size_t)(smax > 0 ? smax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_fwd_kernel<<<ntasks, 256, shm, st>>>(tasks, info, data_off, Fc, rsbuf, ybuf, cbuf);
-  LAUNCH_OK();
+  PDL_LAUNCH(nd_fwd_kernel, dim3(ntasks), dim3(256), shm, st, tasks, info, data_off, sep_flat, lptr, lsrc, Fc, r,
+             (const double*)rsbuf, ybuf, cbuf, lpe);
   return 0;
 }
 
@@ -307,10 +328,9 @@ extern "C" int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const 
     if (N == 1) CUDA_OK(cudaMemsetAsync(x + nfc, 0, sizeof(double), s));
     return 0;
   }
-  nd_pressure_gather_kernel<<<(N - 1 + 255) / 256, 256, 0, s>>>(N, nfc, pptr, psrc, cbuf, r, rp);
-  LAUNCH_OK();
-  nd_pressure_gemv_kernel<<<(N - 1 + 7) / 8 + 1, 256, 0, s>>>(N, nfc, npc, Pcinv, rp, x);
-  LAUNCH_OK();
+  PDL_LAUNCH(nd_pressure_gather_kernel, dim3((N - 1 + 255) / 256), dim3(256), 0, s, N, nfc, pptr, psrc, cbuf, r, rp);
+  PDL_LAUNCH(nd_pressure_gemv_kernel, dim3((N - 1 + 7) / 8 + 1), dim3(256), 0, s, N, nfc, npc, Pcinv,
+             (const double*)rp, x);
   return 0;
 }
 
@@ -321,9 +341,8 @@ extern "C" int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, con
   if (ntasks <= 0) return 0;
   size_t shm = (size_t)(bfmax > 0 ? bfmax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  nd_bwd_kernel<<<ntasks, 256, shm, (cudaStream_t)stream>>>(tasks, info, data_off, sep_flat, bnd_flat, Fc, ybuf, x,
-                                                            wpr);
-  LAUNCH_OK();
+  PDL_LAUNCH(nd_bwd_kernel, dim3(ntasks), dim3(256), shm, (cudaStream_t)stream, tasks, info, data_off, sep_flat,
+             bnd_flat, Fc, ybuf, x, wpr);
   return 0;
 }
 

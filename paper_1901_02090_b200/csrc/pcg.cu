@@ -67,13 +67,15 @@ __global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, doubl
 // Each warp streams whole tiles (coalesced rows), forms the column contribution in
 // registers and the row contribution with a 31-shuffle transpose-reduction; per-tile
 // partials are combined per output block in a fixed order (deterministic).
-__global__ void __launch_bounds__(256) gather_symv_kernel(int maxG, const int* __restrict__ nG,
+__global__ void __launch_bounds__(256) gather_symv_kernel(int N, int maxG, const int* __restrict__ nG,
                                                          const int* __restrict__ gpos,
                                                          const double* __restrict__ packed,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ win, double* __restrict__ yb) {
   extern __shared__ double sm[];
-  const int i = blockIdx.x;
+  // grid-stride over subdomains: a grid smaller than N leaves SM room for the
+  // concurrently running coarse chain
+  for (int i = blockIdx.x; i < N; i += gridDim.x) {
   const int n = nG[i];
   const int nt = maxG / 32;
   const int ntl = (n + 31) / 32;
@@ -81,6 +83,7 @@ __global__ void __launch_bounds__(256) gather_symv_kernel(int maxG, const int* _
   double* xs = sm;                       // maxG
   double* rowp = xs + maxG;              // ntiles x 32
   double* colp = rowp + (size_t)ntiles * 32;  // ntiles x 32
+  __syncthreads();
   for (int c = threadIdx.x; c < ntl * 32; c += blockDim.x) {
     double v = 0.0;
     if (c < n) {
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(256) gather_symv_kernel(int maxG, const int* _
     for (int bi = 0; bi < b; ++bi) acc += colp[(size_t)tile_index(bi, b, nt) * 32 + l];
     yb[(size_t)i * maxG + e] = acc;
   }
+  }
 }
 
 // v[i][r] = sum_q PsiT[i][r][q] * win[i][q] * x[gpos[i][q]]   (warp per coarse row r)
@@ -152,14 +156,15 @@ __global__ void gather_gemv_t_kernel(int maxG, int maxC, const int* __restrict__
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* Pi = PsiT + (size_t)i * maxC * maxG;
-  for (int r = warp; r < maxC; r += nw) {
-    double acc = 0.0;
-    if (r < nc) {
-      const double* row = Pi + (size_t)r * maxG;
-      for (int q = lane; q < n; q += 32) acc += row[q] * xs[q];
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  // four coarse rows per warp pass (16 loads per lane in flight)
+  for (int r = 4 * warp; r < maxC; r += 4 * nw) {
+    const int nr = imax(0, imin(4, nc - r));
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (nr > 0) warp_rows4_dot(Pi + (size_t)r * maxG, maxG, nr, xs, n, lane, acc);
+    if (lane < 4 && r + lane < maxC) {
+      const double t = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
+      v[(size_t)i * maxC + r + lane] = (lane < nr) ? t : 0.0;
     }
-    if (lane == 0) v[(size_t)i * maxC + r] = acc;
   }
 }
 
@@ -171,26 +176,80 @@ __global__ void coarse_restrict_kernel(int nfc, const int* __restrict__ cown, co
   rhs[g] = v[cown[2 * g]] - v[cown[2 * g + 1]];
 }
 
-// out_b[i][q] = wout[i][q] * (y_b[i][q] + sum_r PsiT[i][r][q] sigma_r xc[g_r])   (thread per slot q)
-__global__ void prolong_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ nC,
-                               const int* __restrict__ sub_rows, const double* __restrict__ PsiT,
-                               const double* __restrict__ xc, const double* __restrict__ yb,
-                               const double* __restrict__ wout, double* __restrict__ outb) {
-  extern __shared__ double cf[];
+// out_b[i][q] = wout[i][q] * (y_b[i][q] + sum_r PsiT[i][r][q] sigma_r xc[g_r]).
+// The live rows of PsiT_i stream through shared memory in double-buffered
+// chunks of PRO_RB rows by cp.async (all copies of a chunk in flight at once);
+// thread per slot q reads its column from shared memory.
+#define PRO_RB 8
+#define PRO_QPT 4   // slots per thread: maxG <= 4 * blockDim
+template <bool al16>
+__global__ void __launch_bounds__(256) prolong_kernel(int maxG, int maxC, const int* __restrict__ nG,
+                                                      const int* __restrict__ nC, const int* __restrict__ sub_rows,
+                                                      const double* __restrict__ PsiT, const double* __restrict__ xc,
+                                                      const double* __restrict__ yb, const double* __restrict__ wout,
+                                                      double* __restrict__ outb) {
+  extern __shared__ __align__(16) double psm[];
   const int i = blockIdx.x;
   const int n = nG[i], nc = nC[i];
+  const int cpad = (maxC + 1) & ~1;
+  const int ldt = al16 ? ((n + 1) & ~1) : n;
+  double* cf = psm;
+  double* tile = psm + cpad;
   for (int r = threadIdx.x; r < nc; r += blockDim.x) {
     const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
     cf[r] = (double)sr[3] * xc[sr[0]];
   }
-  __syncthreads();
   const double* Pi = PsiT + (size_t)i * maxC * maxG;
-  for (int q = threadIdx.x; q < n; q += blockDim.x) {
-    double acc = 0.0;
-    for (int r = 0; r < nc; ++r) acc += Pi[(size_t)r * maxG + q] * cf[r];
-    size_t s = (size_t)i * maxG + q;
-    double w = yb ? yb[s] + acc : acc;
-    outb[s] = wout ? wout[s] * w : w;
+  const int nch = (nc + PRO_RB - 1) / PRO_RB;
+  auto issue = [&](int c) {
+    const int r0 = c * PRO_RB, rows = imin(PRO_RB, nc - r0);
+    double* dst = tile + (size_t)(c & 1) * PRO_RB * ldt;
+    if (al16) {
+      const int pr = ldt / 2;
+      for (int e = threadIdx.x; e < rows * pr; e += blockDim.x) {
+        const int rr = e / pr, pp = e - rr * pr;
+        cp_async16(dst + rr * ldt + 2 * pp, Pi + (size_t)(r0 + rr) * maxG + 2 * pp, 16);
+      }
+    } else {
+      for (int e = threadIdx.x; e < rows * ldt; e += blockDim.x) {
+        const int rr = e / ldt, q = e - rr * ldt;
+        cp_async8(dst + rr * ldt + q, Pi + (size_t)(r0 + rr) * maxG + q, 8);
+      }
+    }
+    cp_async_commit();
+  };
+  double acc[PRO_QPT];
+#pragma unroll
+  for (int k = 0; k < PRO_QPT; ++k) acc[k] = 0.0;
+  if (nch > 0) issue(0);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      issue(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* tb = tile + (size_t)(c & 1) * PRO_RB * ldt;
+    const int r0 = c * PRO_RB, rows = imin(PRO_RB, nc - r0);
+    for (int rr = 0; rr < rows; ++rr) {
+      const double w = cf[r0 + rr];
+#pragma unroll
+      for (int k = 0; k < PRO_QPT; ++k) {
+        const int q = threadIdx.x + k * blockDim.x;
+        if (q < n) acc[k] += tb[rr * ldt + q] * w;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < PRO_QPT; ++k) {
+    const int q = threadIdx.x + k * blockDim.x;
+    if (q < n) {
+      const size_t s = (size_t)i * maxG + q;
+      const double w = yb ? yb[s] + acc[k] : acc[k];
+      outb[s] = wout ? wout[s] * w : w;
+    }
   }
 }
 
@@ -227,8 +286,11 @@ __global__ void lap_solve_kernel(int S0, int S1, int S2, const double* __restric
   const int N = S0 * S1 * S2;
   double* u = sm;
   double* w = u + N;
-  const double* Q[3] = {eig, eig + S0 * S0, eig + S0 * S0 + S1 * S1};
-  const double* lam = eig + S0 * S0 + S1 * S1 + S2 * S2;
+  double* es = w + N;   // eigen data staged in shared memory
+  const int ne = S0 * S0 + S1 * S1 + S2 * S2 + S0 + S1 + S2;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) es[e] = eig[e];
+  const double* Q[3] = {es, es + S0 * S0, es + S0 * S0 + S1 * S1};
+  const double* lam = es + S0 * S0 + S1 * S1 + S2 * S2;
   const double* lx = lam;
   const double* ly = lam + S0;
   const double* lz = lam + S0 + S1;
@@ -466,12 +528,13 @@ extern "C" int bddc_pack_sym(int N, int maxG, const double* full, double* packed
 }
 
 extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
-                                const double* x, const double* win, double* yb, void* stream) {
+                                const double* x, const double* win, double* yb, int grid, void* stream) {
   int nt = maxG / 32;
   size_t shm = ((size_t)maxG + (size_t)nt * (nt + 1) * 32) * sizeof(double);
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(gather_symv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  gather_symv_kernel<<<N, 256, shm, (cudaStream_t)stream>>>(maxG, nG, gpos, packed, x, win, yb);
+  if (grid <= 0 || grid > N) grid = N;
+  gather_symv_kernel<<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
   LAUNCH_OK();
   return 0;
 }
@@ -494,8 +557,21 @@ extern "C" int bddc_coarse_restrict(int nfc, const int* cown, const double* v, d
 extern "C" int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* nC, const int* sub_rows,
                             const double* PsiT, const double* xc, const double* yb, const double* wout, double* outb,
                             void* stream) {
-  prolong_kernel<<<N, 128, maxC * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc,
-                                                                          yb, wout, outb);
+  if (maxG > PRO_QPT * 256) return bddc_set_error(BDDC_ERR_ARG, "prolong: maxG too large");
+  const bool al = !(maxG & 1) && !(((uintptr_t)PsiT) & 15);
+  const int ldt = al ? ((maxG + 1) & ~1) : maxG;
+  size_t shm = ((size_t)((maxC + 1) & ~1) + 2 * (size_t)PRO_RB * ldt) * sizeof(double);
+  if (al) {
+    if (shm > 48 * 1024)
+      CUDA_OK(cudaFuncSetAttribute(prolong_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    prolong_kernel<true><<<N, 256, shm, (cudaStream_t)stream>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc, yb, wout,
+                                                                outb);
+  } else {
+    if (shm > 48 * 1024)
+      CUDA_OK(cudaFuncSetAttribute(prolong_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    prolong_kernel<false><<<N, 256, shm, (cudaStream_t)stream>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc, yb, wout,
+                                                                 outb);
+  }
   LAUNCH_OK();
   return 0;
 }
@@ -517,7 +593,7 @@ extern "C" int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const i
 extern "C" int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi, double* z,
                               void* stream) {
   int N = S0 * S1 * S2;
-  size_t shm = 2 * (size_t)N * sizeof(double);
+  size_t shm = (2 * (size_t)N + S0 * S0 + S1 * S1 + S2 * S2 + S0 + S1 + S2) * sizeof(double);
   if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "lap_solve: too many subdomains for one CTA");
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(lap_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));

@@ -315,6 +315,10 @@ class BddcSetup:
         self._work = None
         self._host_scal = torch.empty(16, dtype=F64, pin_memory=True)
         self.stream = torch.cuda.Stream(device=dev)
+        # coarse chain of the preconditioner: high priority so its small latency-bound
+        # kernels get SM slots ahead of the queued T_i GEMV blocks
+        self.side_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._mark(ev, "done")
@@ -435,7 +439,7 @@ class BddcSetup:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
         nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_Sp), _p(x), None, _p(self.w_yb), st)
+                 _p(self.d_Sp), _p(x), None, _p(self.w_yb), 0, st)
         if kt is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -456,16 +460,33 @@ class BddcSetup:
     def _precond(self, r, out):
         """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged."""
         st = _stream()
-        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_Tp), _p(r), _p(self.d_delta), _p(self.w_yb), st)
+        main = torch.cuda.current_stream()
         if self.nfc:
-            nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
-                     _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
-                     _p(self.d_delta), _p(self.w_v), st)
-            nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
-                     _p(self.w_rc), st)
-            nat.call("bddc_fill", self.N, 0.0, _p(self.w_rc[self.nfc:]), st)
-            self._coarse_solve()
+            # the coarse chain (restriction, latency-bound ND solve) runs on a side
+            # stream, concurrently with the bandwidth-bound T_i GEMV (a fork/join
+            # inside the captured PCG graph); they meet at the prolongation
+            side = self.side_stream
+            fork = torch.cuda.Event()
+            fork.record(main)
+            side.wait_event(fork)
+            with torch.cuda.stream(side):
+                ss = _stream()
+                nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                         _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
+                         _p(self.d_delta), _p(self.w_v), ss)
+                nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
+                         _p(self.w_rc), ss)
+                nat.call("bddc_fill", self.N, 0.0, _p(self.w_rc[self.nfc:]), ss)
+                self._coarse_solve()
+                join = torch.cuda.Event()
+                join.record(side)
+        # T_i GEMV with one CTA per SM (grid-stride over subdomains) so the
+        # concurrent coarse chain finds free SM slots
+        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_Tp), _p(r), _p(self.d_delta), _p(self.w_yb),
+                 self.n_sm if self.nfc else 0, st)
+        if self.nfc:
+            main.wait_event(join)
         nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG), _p(self.d_nC),
                  _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
                  _p(self.d_delta), _p(self.w_yb2), st)
@@ -477,13 +498,13 @@ class BddcSetup:
         x = torch.ones(max(self.n_gamma, 1), dtype=F64, device=self.dev)
         st = _stream()
         nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(mats), _p(x), None, _p(self.w_yb), st)
+                 _p(mats), _p(x), None, _p(self.w_yb), 0, st)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(reps):
             nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                     _p(mats), _p(x), None, _p(self.w_yb), st)
+                     _p(mats), _p(x), None, _p(self.w_yb), 0, st)
         b.record()
         b.synchronize()
         return a.elapsed_time(b) / 1000.0 / reps
@@ -639,7 +660,9 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     N, ng = setup.N, setup.n_gamma
     # fs = D f
     if f_device is None:
-        fh = torch.as_tensor(np.asarray(system.f, dtype=np.float64)).pin_memory()
+        # staging through torch's caching pinned allocator (no cudaHostAlloc per call)
+        fh = torch.empty(G.n_cells, dtype=F64, pin_memory=True)
+        np.copyto(fh.numpy(), np.asarray(system.f, dtype=np.float64).reshape(-1))
         W.f_host = fh   # keep the pinned buffer alive until the copy ran
         f_device = W.f_dev
         f_device.copy_(fh, non_blocking=True)
@@ -670,6 +693,11 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     a.u_out, a.u_mode = _p(W.us).value, 0
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
              _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+    host = {}
+    if not return_device:
+        # u0 and u* are final here: stream them to pinned host memory on a copy
+        # stream while the PCG runs
+        host["u0"], host["us"] = _d2h_async(setup, (W.u0, W.us))
     # div_defect = fs - Bs u*
     nat.call("bddc_cell_div", gp, _p(W.us), _p(W.fs), 1.0, -1.0, _p(setup.d_cell_sub),
              _p(setup.d_Dsub), _p(W.dd), st)
@@ -693,9 +721,9 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
         # subdomain net-flux targets (stiffness scaling only)
         nat.call("bddc_sub_sum", gp, _p(W.dd), _p(setup.w_phi), -1.0, _p(setup.d_Dsub), st)
-        targets = setup.w_phi.cpu().numpy()
-        fs_abs = float(np.abs(system.f).dot(setup.d_Dsub.cpu().numpy()[dec.cell_sub]))
-        if np.abs(targets).max() > 1e-13 * max(fs_abs, 1.0):
+        # sum |fs| = sum_c |f_c| D_sub(c) (D > 0); one 2-scalar read
+        tmax, fs_abs = torch.stack([setup.w_phi.abs().max(), W.fs.abs().sum()]).tolist()
+        if tmax > 1e-13 * max(fs_abs, 1.0):
             S3 = dec.S3
             nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
                      _p(setup.w_phi), _p(setup.w_z), st)
@@ -724,10 +752,12 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
     if return_device:
         return W, w_cg_it, kappa, history, converged
+    hu, hp = _d2h_async(setup, (W.u, W.pc))
+    setup.copy_stream.synchronize()
     report = SolveReport(
-        u=W.u.cpu().numpy(), p=W.pc.cpu().numpy(), it=w_cg_it, kappa=kappa,
+        u=hu.numpy(), p=hp.numpy(), it=w_cg_it, kappa=kappa,
         omega_tilde=omega, n_c=setup.n_c, residuals=history,
-        u0=W.u0.cpu().numpy(), u_star=W.us.cpu().numpy(),
+        u0=host["u0"].numpy(), u_star=host["us"].numpy(),
         conservation_defect=defect_norm, pressure_warning=p_warn,
         converged=converged)
     if u_exact is not None:
@@ -740,6 +770,22 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         raise NonConvergenceError(
             f"CG did not converge in {config.maxit} iterations", report=report)
     return report
+
+
+def _d2h_async(setup, tensors):
+    """Copy device vectors into fresh pinned host tensors on the setup's copy stream
+    (ordered after the work queued so far on the current stream)."""
+    cs = getattr(setup, "copy_stream", None)
+    if cs is None:
+        cs = setup.copy_stream = torch.cuda.Stream(device=setup.dev)
+    cs.wait_stream(torch.cuda.current_stream())
+    out = []
+    with torch.cuda.stream(cs):
+        for t in tensors:
+            h = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            out.append(h)
+    return out
 
 
 def _scale_fs(setup, f, fs):
