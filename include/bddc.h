@@ -95,7 +95,8 @@ int bddc_local_schur(const bddc_geom* g, const int* gcode, const double* Q, cons
                      double* S, void* stream);
 
 /* Batched interior KKT solves (substructure.py:72-116): harmonic_extend,
- * trace_solve, condense and the interior recovery (solver.py:375-382). */
+ * trace_solve, condense and the interior recovery (solver.py:375-382).
+ * Q is tile-packed symmetric (bddc_pack_sym with n = maxP). */
 typedef struct bddc_local_solve_args {
   const double* f_flux;   /* global flux vector read at interior dofs (or NULL) */
   double f_scale;

@@ -128,6 +128,63 @@ __device__ __forceinline__ void warp_rows4_dot(const double* __restrict__ base, 
   }
 }
 
+// Tile-packed symmetric storage: upper-triangle 32x32 tiles (bi <= bj) in
+// row-major tile order, each tile row-major; nt = n / 32 tiles per row.
+__device__ __forceinline__ int tile_index(int bi, int bj, int nt) { return bi * nt - (bi * (bi - 1)) / 2 + (bj - bi); }
+
+// y = M x for one tile-packed symmetric matrix, whole CTA, vectors in shared
+// memory (x zero beyond the live size, ntl = live tiles per row).  Each warp
+// streams whole tiles (32 loads per lane in flight), forms the column
+// contribution directly and the row contribution by a transpose-reduction, and
+// accumulates into its own slice of yw (nwarps x ntl*32 doubles of shared
+// memory); the slices are summed in warp order: deterministic.
+__device__ __forceinline__ void cta_symv_packed(const double* __restrict__ Pk, int nt, int ntl, const double* x,
+                                                double* y, double* yw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int len = ntl * 32;
+  for (int e = threadIdx.x; e < nw * len; e += blockDim.x) yw[e] = 0.0;
+  __syncthreads();
+  double* my = yw + (size_t)warp * len;
+  const int nlive = ntl * (ntl + 1) / 2;
+  for (int u = warp; u < nlive; u += nw) {
+    int bi = 0, rem = u;
+    while (rem >= ntl - bi) {
+      rem -= ntl - bi;
+      ++bi;
+    }
+    const int bj = bi + rem;
+    const double* T = Pk + (size_t)tile_index(bi, bj, nt) * 1024;
+    const double xl = x[bj * 32 + lane];
+    double v[32];
+    double col = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const double a = __ldg(T + r * 32 + lane);
+      v[r] = a * xl;
+      col += a * x[bi * 32 + r];
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const bool up = lane & off;
+#pragma unroll
+      for (int k = 0; k < off; ++k) {
+        const double send = up ? v[k] : v[k + off];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, off);
+        v[k] = (up ? v[k + off] : v[k]) + recv;
+      }
+    }
+    my[bi * 32 + lane] += v[0];
+    if (bi != bj) my[bj * 32 + lane] += col;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < len; e += blockDim.x) {
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += yw[(size_t)w * len + e];
+    y[e] = acc;
+  }
+  __syncthreads();
+}
+
 // Subdomain box of subdomain i under a regular partition.
 struct Box {
   int o[3];   // origin (cells)

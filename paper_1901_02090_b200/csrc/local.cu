@@ -403,6 +403,7 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
   double* rhs = xg + mg;      // mp
   double* pp = rhs + mp;      // mp
   double* tI = pp + mp;       // 3 mp (interior faces, per axis blocks)
+  double* yw = tI + 3 * mp;   // (blockDim/32) x mp symv partials
   int off[3];
   {
     int o = 0;
@@ -468,14 +469,13 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
     }
     __syncthreads();
   }
-  // p' = Q rhs  (Q symmetric: read row c, coalesced over r)
-  const double* Qi = Q + (size_t)i * mp * mp;
-  for (int r = threadIdx.x; r < mp; r += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < np; ++c) acc += Qi[(size_t)c * mp + r] * rhs[c];
-    pp[r] = acc;
+  // p' = Q rhs, Q tile-packed symmetric (half the bytes of full storage)
+  {
+    const int nt = mp / 32, ntl = (np + 31) / 32;
+    cta_symv_packed(Q + (size_t)i * (nt * (nt + 1) / 2) * 1024, nt, ntl, rhs, pp, yw);
+    for (int r = ntl * 32 + threadIdx.x; r < mp; r += blockDim.x) pp[r] = 0.0;
+    __syncthreads();
   }
-  __syncthreads();
   // u_I = t - A^{-1} B_u^T p'
   for (int a = 0; a < G.dim; ++a) {
     const int L = b.L[a], m = L - 1, nl = n_lines(b, a), st = axis_stride(b, a);
@@ -582,7 +582,9 @@ extern "C" int bddc_local_schur(const bddc_geom* g, const int* gcode, const doub
 extern "C" int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, const int* gpos,
                                 const int* fslot, const double* Q, const double* Dsub,
                                 const bddc_local_solve_args* a, void* stream) {
-  size_t shm = (size_t)(g->maxG + 5 * g->maxP) * sizeof(double);
+  if (g->maxP % 32) return bddc_set_error(BDDC_ERR_ARG, "local_solve: maxP must be a multiple of 32");
+  size_t shm = (size_t)(g->maxG + 5 * g->maxP + 8 * g->maxP) * sizeof(double);
+  if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "local_solve: subdomain too large for shared memory");
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   local_solve_kernel<<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);

@@ -43,7 +43,6 @@ __global__ void gather_gemv_kernel(int maxG, const int* __restrict__ nG, const i
 // nt = maxG/32.  Only ceil(nG_i/32) block rows are live; this halves the bytes
 // streamed per GEMV compared with full storage.
 
-__device__ __forceinline__ int tile_index(int bi, int bj, int nt) { return bi * nt - (bi * (bi - 1)) / 2 + (bj - bi); }
 
 __global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, double* __restrict__ packed) {
   const int i = blockIdx.y;

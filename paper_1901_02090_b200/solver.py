@@ -189,6 +189,10 @@ class BddcSetup:
         nat.call("bddc_local_schur", gp, _p(self.d_gcode), _p(self.d_Q), _p(Gc),
                  _p(SAd), _p(SApart), _p(SAoff), _p(Wt), _p(self.d_S), st)
         del Wt, Gc, SAd, SApart, SAoff
+        # the local solves read Q tile-packed (symmetric upper tiles: half the bytes)
+        self.d_Qp = torch.empty(N * nat.load().bddc_sym_packed_elems(mp), dtype=F64, device=dev)
+        nat.call("bddc_pack_sym", N, mp, _p(self.d_Q), _p(self.d_Qp), st)
+        del self.d_Q
         Sinv = self.d_S.clone()
         leaf = 64
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, leaf) // 8 + 2,
@@ -686,13 +690,13 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     a.x_gamma, a.x_scale = _p(W.g).value, 1.0
     a.u_out, a.u_mode = _p(W.u0).value, 0
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
-             _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+             _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     a = nat.LocalSolveArgs()
     a.x_gamma, a.x_scale = _p(W.g).value, 1.0
     a.g_cell, a.g_scale = _p(W.fs).value, 1.0
     a.u_out, a.u_mode = _p(W.us).value, 0
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
-             _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+             _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     host = {}
     if not return_device:
         # u0 and u* are final here: stream them to pinned host memory on a copy
@@ -716,7 +720,7 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         a.g_cell, a.g_scale = _p(W.dd).value, 1.0
         a.rg_broken = _p(setup.w_yb).value
         nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
-                 _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+                 _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
         nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb), _p(W.Ap), st)
         nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
         # subdomain net-flux targets (stiffness scaling only)
@@ -746,7 +750,7 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         a.x_gamma, a.x_scale = _p(W.x).value, 1.0
         a.u_out, a.u_mode = _p(W.u).value, 1
         nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
-                 _p(setup.d_fslot), _p(setup.d_Q), _p(setup.d_Dsub), C.byref(a), st)
+                 _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     # pressure recovery: B B^T p = B(-A u), zero mean
     p_warn = _recover_pressure(setup, W, config.tol)
     omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
