@@ -153,18 +153,6 @@ int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* in
 int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
                 const double* ybuf, double* x, void* stream);
-/* The whole coarse solve (forward, root pressure block, backward) as one persistent
- * kernel over topologically ordered work items {type | wpr << 8, node, r0, r1}
- * with per-node completion counters (cnt: bddc_nd_persist_counters(nnodes) ints,
- * zeroed by the call).  grid <= 0: one full wave of CTAs. */
-int bddc_nd_persist_counters(int nnodes);
-int bddc_nd_solve_persist(int nitems, const int* items, int nnodes, const int* node,
-                          const long long* off, const int* sep_flat, const int* bnd_flat,
-                          const int* lptr, const int* lsrc, const int* pptr, const int* psrc,
-                          const double* Fc, const double* Pcinv, const double* r, double* rs,
-                          double* ybuf, double* cbuf, double* prhs, double* x, int* cnt, int root,
-                          int N, int nfc, int npc, int npg, int npv, int smem_doubles, int grid,
-                          void* stream);
 int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
                     const long long* data_off, double* Fc, void* stream);
 /* Root pressure block of the pinned coarse solve: x_p = -Pc^-1 (r_p - contributions). */

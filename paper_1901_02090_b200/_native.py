@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libbddc.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["capi.cu", "dense.cu", "local.cu", "adaptive.cu", "coarse.cu",
-           "nd.cu", "nd_persist.cu", "pcg.cu", "stencil.cu", "graph.cu"]
+           "nd.cu", "pcg.cu", "stencil.cu", "graph.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
               "-diag-suppress", "550"]
@@ -111,8 +111,6 @@ _SIGS = {
     "bddc_nd_compact": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_nd_pressure": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_nd_extract_pc": [_P, _I, _I, _I, _P, _I, _P],
-    "bddc_nd_persist_counters": [_I],
-    "bddc_nd_solve_persist": [_I, _P, _I] + [_P] * 17 + [_I] * 8 + [_P],
     "bddc_nd_bwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_b0_apply": [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P],
     "bddc_b0t_apply": [_I, _I, _P, _P, _P, _I, _I, _D, _P, _I, _P],

@@ -117,10 +117,60 @@ def nd_geometry(dec):
     return nodes
 
 
+def nd_geometry_flat(dec):
+    """Flat arrays of the internal nodes of nd_geometry (cached on `dec`)."""
+    cached = getattr(dec, "_nd_geometry_flat", None)
+    if cached is not None:
+        return cached
+    geo = nd_geometry(dec)
+    internal = [k for k, n in enumerate(geo) if not n["leaf"]]
+    gpos = {k: i for i, k in enumerate(internal)}
+
+    def csr(key):
+        parts = [np.asarray(geo[k][key], dtype=np.int64) for k in internal]
+        ptr = np.concatenate([[0], np.cumsum([len(p) for p in parts])]).astype(np.int64)
+        flat = np.concatenate(parts) if parts else np.zeros(0, np.int64)
+        return ptr, flat
+
+    F = dict(internal=np.array(internal, dtype=np.int64),
+             depth=np.array([geo[k]["depth"] for k in internal], dtype=np.int64))
+    F["sep_ptr"], F["sep"] = csr("sep")
+    F["bnd_ptr"], F["bnd"] = csr("bnd")
+    F["pres_ptr"], F["pres"] = csr("pres")
+    # children: internal index (>= 0) or -(1 + subdomain) for leaves
+    ch = np.zeros((len(internal), 2), dtype=np.int64)
+    for i, k in enumerate(internal):
+        for s_, c in enumerate(geo[k]["ch"]):
+            ch[i, s_] = gpos[c] if not geo[c]["leaf"] else -(1 + geo[c]["sub"])
+    F["ch"] = ch
+    dec._nd_geometry_flat = F
+    return F
+
+
+def _expand(ptr, faces, per_face, cstart):
+    """Face lists (CSR) -> coarse dof lists (CSR): face f -> cstart[f] .. + per_face[f]."""
+    cnt = per_face[faces]
+    tot = int(cnt.sum())
+    first = np.cumsum(cnt) - cnt
+    dofs = np.repeat(cstart[faces] - first, cnt) + np.arange(tot, dtype=np.int64)
+    csum = np.concatenate([[0], np.cumsum(cnt)])
+    return csum[ptr], dofs
+
+
+def _ranges(lo, cnt):
+    """concat(arange(lo[i], lo[i] + cnt[i]))."""
+    tot = int(cnt.sum())
+    if tot == 0:
+        return np.zeros(0, np.int64)
+    start = np.cumsum(cnt) - cnt
+    return np.repeat(lo - start, cnt) + np.arange(tot, dtype=np.int64)
+
+
 class CoarseND:
     """Symbolic analysis (host, index tables only) + numeric factorisation (device)."""
 
     def __init__(self, dec, per_face, cstart, sub_rows, nC, maxC, dev):
+        """Symbolic analysis, vectorised over all tree nodes (numpy, no per-node loops)."""
         self.dev = dev
         N = dec.n_subdomains
         self.N = N
@@ -128,264 +178,179 @@ class CoarseND:
         self.nfc = nfc = int(per_face.sum()) if nfaces else 0
         per_face = np.asarray(per_face, dtype=np.int64)
         cstart = np.asarray(cstart, dtype=np.int64)
-
-        def face_dofs(fl):
-            if len(fl) == 0:
-                return np.zeros(0, dtype=np.int64)
-            cnt = per_face[fl]
-            tot = int(cnt.sum())
-            first = np.cumsum(cnt) - cnt
-            return np.repeat(cstart[fl] - first, cnt) + np.arange(tot)
-
-        # geometry-only tree (cached on the decomposition), expanded to coarse dofs here
-        geo = nd_geometry(dec) if (N > 1 and nfc) else []
-        nodes = []
-        for gn in geo:
-            if gn["leaf"]:
-                nodes.append(dict(leaf=True, sub=gn["sub"], depth=gn["depth"]))
-            else:
-                bf = face_dofs(gn["bnd"])
-                nodes.append(dict(leaf=False, depth=gn["depth"], sep=face_dofs(gn["sep"]), bndf=bf,
-                                  bnd=np.concatenate([bf, nfc + gn["pres"]]), ch=gn["ch"]))
-        self.nodes = nodes
-        internal = [k for k, n in enumerate(nodes) if not n["leaf"]]
-        depths = sorted({nodes[k]["depth"] for k in internal}, reverse=True)
-        pos_in_level = {}
+        nC = np.asarray(nC, dtype=np.int64)
+        self.maxC = maxC
+        self.factored = False
         self.levels = []
         t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
-        sub_g = sub_rows[:, :, 0]
+        if not (N > 1 and nfc):
+            self.cb_total = 1
+            self.pptr = t(np.zeros(max(N, 1), np.int32))
+            self.psrc = t(np.zeros(1, np.int32))
+            return
+        G = nd_geometry_flat(dec)
+        nI = len(G["internal"])
+        # coarse dof lists per internal node: sep, boundary = boundary faces' dofs ++ pressures
+        sptr, sdofs = _expand(G["sep_ptr"], G["sep"], per_face, cstart)
+        fptr, fdofs = _expand(G["bnd_ptr"], G["bnd"], per_face, cstart)
+        ns = np.diff(sptr)
+        nbf = np.diff(fptr)
+        npres = np.diff(G["pres_ptr"])
+        nb = nbf + npres
+        bptr = np.concatenate([[0], np.cumsum(nb)])
+        node_b = np.repeat(np.arange(nI), nb)
+        within = np.arange(int(bptr[-1]), dtype=np.int64) - bptr[node_b]
+        isf = within < nbf[node_b]
+        bdofs = np.empty(int(bptr[-1]), dtype=np.int64)
+        bdofs[isf] = fdofs[fptr[node_b[isf]] + within[isf]]
+        nq = ~isf
+        bdofs[nq] = nfc + G["pres"][G["pres_ptr"][node_b[nq]] + within[nq] - nbf[node_b[nq]]]
+        # levels: deepest first; within a level, tree order
+        depth = G["depth"]
+        ud = np.unique(depth)[::-1]
+        lev = np.searchsorted(-ud, -depth)
+        order = np.lexsort((np.arange(nI), lev))
+        lev_start = np.searchsorted(lev[order], np.arange(len(ud) + 1))
+        pos = np.empty(nI, dtype=np.int64)
+        for li in range(len(ud)):
+            ids = order[lev_start[li]:lev_start[li + 1]]
+            pos[ids] = np.arange(len(ids))
+        ch = G["ch"]
+        internal_ch = ch >= 0
+        par = np.repeat(np.arange(nI)[:, None], 2, axis=1)
+        if np.any(lev[ch[internal_ch]] != lev[par[internal_ch]] - 1):
+            raise ConfigurationError("nested dissection: child not one level below")
+        sub_g = np.asarray(sub_rows[:, :, 0], dtype=np.int64)
+        M = nfc + N + 1
 
-        def export(cn):
-            if cn["leaf"]:
-                i = cn["sub"]
-                return np.concatenate([sub_g[i, :nC[i]], [nfc + i]])
-            return cn["bnd"]
-
-        for d in depths:
-            ids = [k for k in internal if nodes[k]["depth"] == d]
+        coff = 0
+        for li in range(len(ud)):
+            ids = order[lev_start[li]:lev_start[li + 1]]
             L = _Level()
-            L.ids, L.m = ids, len(ids)
-            for q, k in enumerate(ids):
-                pos_in_level[k] = (len(self.levels), q)
-            L.S = _pad(max(len(nodes[k]["sep"]) for k in ids), 32)
-            L.B = _pad(max(len(nodes[k]["bnd"]) for k in ids), 2)
-            L.Bf = max(len(nodes[k]["bndf"]) for k in ids)
-            L.nf = L.S + L.B
-            sep_idx = np.full((L.m, L.S), -1, dtype=np.int32)
-            bnd_idx = np.full((L.m, max(L.Bf, 1)), -1, dtype=np.int32)
+            L.m = m = len(ids)
+            s = ns[ids]
+            b = nb[ids]
+            L.S = S = _pad(int(s.max()), 32)
+            L.B = _pad(int(b.max()), 2)
+            L.nf = S + L.B
+            sep_flat = sdofs[_ranges(sptr[ids], s)]
+            bnd_flat = bdofs[_ranges(bptr[ids], b)]
+            srow = np.repeat(np.arange(m), s)
+            scol = _ranges(np.zeros(m, np.int64), s)
+            sep_idx = np.full((m, S), -1, dtype=np.int32)
+            sep_idx[srow, scol] = sep_flat
+            # parent fronts [sep | bnd] keyed by (parent, dof) -> position in the padded front
+            brow = np.repeat(np.arange(m), b)
+            bcol = _ranges(np.zeros(m, np.int64), b)
+            fk = np.concatenate([srow * M + sep_flat, brow * M + bnd_flat])
+            fv = np.concatenate([scol, S + bcol])
+            fo = np.argsort(fk, kind="stable")
+            fk, fv = fk[fo], fv[fo]
             K = 1
             maps = []
-            for q, k in enumerate(ids):
-                n = nodes[k]
-                sep_idx[q, :len(n["sep"])] = n["sep"]
-                bnd_idx[q, :len(n["bndf"])] = n["bndf"]
-                front = np.concatenate([n["sep"], n["bnd"]])
-                order = np.argsort(front, kind="stable")
-                fs = front[order]
-                ns = len(n["sep"])
-                mm = []
-                for c in n["ch"]:
-                    src = export(nodes[c])
-                    loc = np.searchsorted(fs, src)
-                    if len(src) and not np.array_equal(fs[np.minimum(loc, len(fs) - 1)], src):
-                        raise ConfigurationError("nested dissection: child export not in parent front")
-                    mp = order[loc]
-                    mm.append(np.where(mp < ns, mp, L.S + (mp - ns)).astype(np.int32))
-                    K = max(K, len(src))
-                maps.append(mm)
+            ckind = np.zeros((2, m, 3), dtype=np.int32)
+            for slot in (0, 1):
+                c = ch[ids, slot]
+                leafc = c < 0
+                subc = np.where(leafc, -c - 1, 0)
+                elen = np.where(leafc, nC[subc] + 1, nb[np.maximum(c, 0)])
+                erow = np.repeat(np.arange(m), elen)
+                ecol = _ranges(np.zeros(m, np.int64), elen)
+                cr = c[erow]
+                lf = cr < 0
+                dof = np.empty(len(erow), dtype=np.int64)
+                sr = -cr[lf] - 1
+                last = ecol[lf] == nC[sr]
+                dof_l = np.where(last, nfc + sr, sub_g[sr, np.minimum(ecol[lf], sub_g.shape[1] - 1)])
+                dof[lf] = dof_l
+                ci = cr[~lf]
+                dof[~lf] = bdofs[bptr[ci] + ecol[~lf]]
+                key = erow * M + dof
+                loc = np.searchsorted(fk, key)
+                if len(key) and not np.array_equal(fk[np.minimum(loc, len(fk) - 1)], key):
+                    raise ConfigurationError("nested dissection: child export not in parent front")
+                maps.append((erow, ecol, fv[loc].astype(np.int32)))
+                K = max(K, int(elen.max()) if m else 1)
+                ckind[slot, leafc, 0] = 1
+                ckind[slot, leafc, 1] = subc[leafc]
+                ckind[slot, leafc, 2] = nC[subc[leafc]]
+                ckind[slot, ~leafc, 1] = pos[c[~leafc]]
             L.K = K
-            cmap = np.full((2, L.m, K), -1, dtype=np.int32)
-            ckind = np.zeros((2, L.m, 3), dtype=np.int32)
-            for q, k in enumerate(ids):
-                for slot, c in enumerate(nodes[k]["ch"]):
-                    cmap[slot, q, :len(maps[q][slot])] = maps[q][slot]
-                    cn = nodes[c]
-                    ckind[slot, q] = (1, cn["sub"], nC[cn["sub"]]) if cn["leaf"] else (0, -1, 0)
-            L.sep_idx_h = sep_idx
-            L.sep_idx, L.bnd_idx = t(sep_idx), t(bnd_idx)
-            L.cmap_h, L.ckind_h = cmap, ckind
+            cmap = np.full((2, m, K), -1, dtype=np.int32)
+            for slot, (erow, ecol, v) in enumerate(maps):
+                cmap[slot, erow, ecol] = v
+            L.sep_idx = t(sep_idx)
+            L.cmap = t(cmap)
+            L.ckind = t(ckind)
+            L.s = s
+            L.b = b
+            L.cb_off = coff + np.concatenate([[0], np.cumsum(b)[:-1]])
+            coff += int(b.sum())
+            L._sep_flat, L._bnd_flat = sep_flat, bnd_flat
             self.levels.append(L)
-        for li, L in enumerate(self.levels):
-            for q, k in enumerate(L.ids):
-                for slot, c in enumerate(nodes[k]["ch"]):
-                    if not nodes[c]["leaf"]:
-                        lc, pc = pos_in_level[c]
-                        if lc != li - 1:
-                            raise ConfigurationError("nested dissection: child not one level below")
-                        L.ckind_h[slot, q] = (0, pc, 0)
-            L.cmap = t(L.cmap_h)
-            L.ckind = t(L.ckind_h)
-        # ---- compact solve layout over the combined vector [flux coarse dofs | pressures]:
-        # per node F11inv (s x s) then X (b x s) for the whole boundary (flux + pressures).
-        # Left-looking forward lists: for every separator slot (and every pressure) the
-        # cbuf indices of all descendant contributions to it, ordered deeper level
-        # first, then node, then slot (vectorised).
-        coff = 0
-        gs, srcs = [], []
-        for L in self.levels:
-            L.s = np.array([len(nodes[k]["sep"]) for k in L.ids], dtype=np.int64)
-            L.b = np.array([len(nodes[k]["bnd"]) for k in L.ids], dtype=np.int64)
-            L.cb_off = coff + np.concatenate([[0], np.cumsum(L.b)[:-1]])
-            for q, k in enumerate(L.ids):
-                bb = nodes[k]["bnd"]
-                if len(bb):
-                    gs.append(bb)
-                    srcs.append(L.cb_off[q] + np.arange(len(bb)))
-            coff += int(L.b.sum())
         self.cb_total = max(coff, 1)
-        if gs:
-            gs = np.concatenate(gs)
-            srcs = np.concatenate(srcs)
-            o = np.lexsort((srcs, gs))
-            gs, srcs = gs[o], srcs[o]
-        else:
-            gs = srcs = np.zeros(0, np.int64)
+        # left-looking forward lists: for every separator slot (and every pressure) the
+        # cbuf indices of all descendant contributions to it, ordered by cbuf index
+        gs = np.concatenate([L._bnd_flat for L in self.levels])
+        srcs = np.concatenate([_ranges(L.cb_off, L.b) for L in self.levels])
+        o = np.lexsort((srcs, gs))
+        gs, srcs = gs[o], srcs[o]
 
         def lists(keys):
             lo = np.searchsorted(gs, keys, side="left")
             hi = np.searchsorted(gs, keys, side="right")
             cnt = hi - lo
             ptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int32)
-            idx = np.concatenate([np.arange(a_, b_) for a_, b_, c_ in zip(lo, hi, cnt) if c_]) \
-                if cnt.sum() else np.zeros(0, np.int64)
+            idx = _ranges(lo, cnt)
             src = srcs[idx] if len(idx) else np.zeros(1, np.int64)
             return ptr, src.astype(np.int32)
 
         def rows_per_task(total):
-            # warp per row, 8 warps per CTA: aim for >= ~8 CTAs per SM per level
+            # 4 rows per warp pass, 8 warps per CTA: aim for >= ~8 CTAs per SM per level
             r = 8
             while r < 64 and total / (2 * r) >= 148 * 8:
                 r *= 2
             return r
 
+        def split(nrows, step):
+            k = -(-nrows // step)
+            q = np.repeat(np.arange(len(nrows)), k)
+            r0 = _ranges(np.zeros(len(nrows), np.int64), k) * step
+            return np.stack([q, r0, np.minimum(r0 + step, nrows[q])], axis=1).astype(np.int32)
+
         for L in self.levels:
-            sep_flat = np.concatenate([nodes[k]["sep"] for k in L.ids]).astype(np.int64)
-            bnd_flat = np.concatenate([nodes[k]["bnd"] for k in L.ids] + [np.zeros(0, np.int64)])
-            sep_ptr = np.concatenate([[0], np.cumsum(L.s)])
-            bnd_ptr = np.concatenate([[0], np.cumsum(L.b)])
-            data_off = np.concatenate([[0], np.cumsum(L.s * L.s + 2 * L.b * L.s)])
+            s, b = L.s, L.b
+            sep_ptr = np.concatenate([[0], np.cumsum(s)])
+            bnd_ptr = np.concatenate([[0], np.cumsum(b)])
+            data_off = np.concatenate([[0], np.cumsum(s * s + 2 * b * s)])
             L.ysize = int(sep_ptr[-1])
             L.csize = int(data_off[-1])
-            lptr, lsrc = lists(sep_flat)
-            info = np.stack([L.s, L.b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off], axis=1).astype(np.int32)
-            ft_, bt_ = [], []
-            rf = rows_per_task(int((L.s + L.b).sum()))
+            lptr, lsrc = lists(L._sep_flat)
+            info = np.stack([s, b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off], axis=1).astype(np.int32)
+            rf = rows_per_task(int((s + b).sum()))
             # backward rows are long (b): split a row over wpr warps when the
             # level has too few rows to fill the GPU
             L.wpr = 1
-            while L.wpr < 8 and int(L.s.sum()) * L.wpr < 148 * 8 * 4 and int(L.b.max()) >= 128 * L.wpr:
+            while L.wpr < 8 and int(s.sum()) * L.wpr < 148 * 8 * 4 and int(b.max()) >= 128 * L.wpr:
                 L.wpr *= 2
-            rb = rows_per_task(int(L.s.sum()) * max(1, int(L.b.max()) // 64)) if L.wpr == 1 else 8 // L.wpr
-            for q in range(L.m):
-                nr, ns = int(L.s[q] + L.b[q]), int(L.s[q])
-                for r0 in range(0, nr, rf):
-                    ft_.append((q, r0, min(r0 + rf, nr)))
-                for k0 in range(0, ns, rb):
-                    bt_.append((q, k0, min(k0 + rb, ns)))
-            L.h = dict(sep_flat=sep_flat, bnd_flat=bnd_flat, sep_ptr=sep_ptr, bnd_ptr=bnd_ptr,
-                       data_off=data_off, lptr=lptr, lsrc=lsrc)
+            rb = rows_per_task(int(s.sum()) * max(1, int(b.max()) // 64)) if L.wpr == 1 else 8 // L.wpr
+            ft = split(s + b, rf)
+            bt = split(s, rb)
             L.info = t(info)
             L.data_off = t(data_off[:-1].astype(np.int64), torch.int64)
-            L.sep_flat = t(sep_flat.astype(np.int32))
-            L.bnd_flat = t(bnd_flat.astype(np.int32) if len(bnd_flat) else np.zeros(1, np.int32))
+            L.sep_flat = t(L._sep_flat.astype(np.int32))
+            L.bnd_flat = t(L._bnd_flat.astype(np.int32) if len(L._bnd_flat) else np.zeros(1, np.int32))
             L.lptr = t(lptr)
             L.lsrc = t(lsrc)
-            L.ftasks = t(np.array(ft_, dtype=np.int32).reshape(-1, 3))
-            L.btasks = t(np.array(bt_, dtype=np.int32).reshape(-1, 3))
-            L.n_ft, L.n_bt = len(ft_), len(bt_)
-            L.smax = int(L.s.max())
-            L.bmax = int(L.b.max())
+            L.ftasks = t(ft)
+            L.btasks = t(bt)
+            L.n_ft, L.n_bt = len(ft), len(bt)
+            L.smax = int(s.max())
+            L.bmax = int(b.max())
+            del L._sep_flat, L._bnd_flat
         # pressure gather lists (pressures 1..N-1; subdomain 0 is pinned)
         pptr, psrc = lists(nfc + np.arange(1, N, dtype=np.int64))
         self.pptr, self.psrc = t(pptr), t(psrc)
-        self.maxC = maxC
-        self.factored = False
-        self.persistent = False   # per-level launches (faster than nd_persist.cu today)
-        if self.levels:
-            self._build_persistent(nodes, pos_in_level, pptr, t)
-
-    def _build_persistent(self, nodes, pos_in_level, pptr, t):
-        """Global node table + topologically ordered work items of the one-kernel solve
-        (csrc/nd_persist.cu)."""
-        levels = self.levels
-        nb = np.cumsum([0] + [L.m for L in levels])
-        sb = np.cumsum([0] + [L.ysize for L in levels])
-        bb = np.cumsum([0] + [len(L.h["bnd_flat"]) for L in levels])
-        lb = np.cumsum([0] + [int(L.h["lptr"][-1]) for L in levels])
-        fb = np.cumsum([0] + [L.csize for L in levels])
-        self.fc_base = fb
-        gid = {k: int(nb[li] + q) for k, (li, q) in pos_in_level.items()}
-        nn = int(nb[-1])
-        NC = 11
-        tab = np.zeros((nn, NC), dtype=np.int64)
-        off = np.zeros(nn, dtype=np.int64)
-        for li, L in enumerate(levels):
-            g0 = int(nb[li])
-            tab[g0:g0 + L.m, 0] = L.s
-            tab[g0:g0 + L.m, 1] = L.b
-            tab[g0:g0 + L.m, 2] = sb[li] + L.h["sep_ptr"][:-1]
-            tab[g0:g0 + L.m, 3] = bb[li] + L.h["bnd_ptr"][:-1]
-            tab[g0:g0 + L.m, 4] = L.cb_off
-            off[g0:g0 + L.m] = fb[li] + L.h["data_off"][:-1]
-        tab[:, 5:8] = -1
-        for k, g in gid.items():
-            for slot, c in enumerate(nodes[k]["ch"]):
-                if c in gid:
-                    tab[g, 6 + slot] = gid[c]
-                    tab[gid[c], 5] = g
-        lptr_g = [np.zeros(1, np.int64)]
-        for li, L in enumerate(levels):
-            lp = L.h["lptr"].astype(np.int64)
-            lptr_g.append(lp[1:] + lb[li])
-        lptr_g = np.concatenate(lptr_g)
-        lsrc_g = np.concatenate([L.h["lsrc"][:L.h["lptr"][-1]].astype(np.int64) for L in levels]
-                                + [np.zeros(1, np.int64)])
-        G = 296   # ~2 CTAs per SM worth of items per level
-        items = []
-        for li, L in enumerate(levels):
-            g0 = int(nb[li])
-            rows = (L.s + L.b).astype(np.int64)
-            rf = max(8, -(-int(rows.sum()) // G))
-            for q in range(L.m):
-                g = g0 + q
-                nr = int(rows[q])
-                nf = 0
-                for r0 in range(0, nr, rf):
-                    items.append((2, g, r0, min(r0 + rf, nr)))
-                    nf += 1
-                tab[g, 8], tab[g, 9] = nf, 0
-        npr = max(self.N - 1, 0)
-        pg = [(3, -1, e0, min(e0 + 256, npr)) for e0 in range(0, npr, 256)]
-        pv = [(4, -1, r0, min(r0 + 8, npr)) for r0 in range(0, npr, 8)]
-        items += pg + pv
-        for li in range(len(levels) - 1, -1, -1):
-            L = levels[li]
-            g0 = int(nb[li])
-            wpr = getattr(L, "wpr", 1)
-            rb = (8 // wpr) if wpr > 1 else max(8, -(-int(L.s.sum()) // G))
-            for q in range(L.m):
-                ns = int(L.s[q])
-                nbk = 0
-                for k0 in range(0, ns, rb):
-                    items.append((5 | (wpr << 8), g0 + q, k0, min(k0 + rb, ns)))
-                    nbk += 1
-                tab[g0 + q, 10] = nbk
-        self.p_items = t(np.array(items, dtype=np.int32).reshape(-1, 4))
-        self.p_nitems = len(items)
-        self.p_nodes = t(tab.astype(np.int32))
-        self.p_nn = nn
-        self.p_off = t(off, torch.int64)
-        self.p_sep = t(np.concatenate([L.h["sep_flat"] for L in levels]).astype(np.int32))
-        bf = np.concatenate([L.h["bnd_flat"] for L in levels]).astype(np.int32)
-        self.p_bnd = t(bf if len(bf) else np.zeros(1, np.int32))
-        self.p_lptr = t(lptr_g.astype(np.int32))
-        self.p_lsrc = t(lsrc_g.astype(np.int32))
-        self.p_npg, self.p_npv = len(pg), len(pv)
-        self.p_root = int(nb[-1]) - 1
-        self.p_ysize = int(sb[-1])
-        self.p_smem = int(max(max(int(L.s.max()) for L in levels),
-                              max(int(L.b.max()) for L in levels) + 8, npr, 1))
-        self.p_cnt = torch.zeros(3 + 3 * nn, dtype=I32, device=self.dev)
 
     # --------------------------------------------------------------- numeric
 
@@ -422,9 +387,8 @@ class CoarseND:
         if int(info.item()):
             raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
         self.factored = True
-        self.Fc_all = torch.empty(max(int(self.fc_base[-1]), 1), dtype=F64, device=self.dev)
-        for li, L in enumerate(self.levels):
-            L.Fc = self.Fc_all[int(self.fc_base[li]):int(self.fc_base[li]) + max(L.csize, 1)]
+        for L in self.levels:
+            L.Fc = torch.empty(max(L.csize, 1), dtype=F64, device=self.dev)
             nat.call("bddc_nd_compact", L.m, L.S, L.nf, L.B, _p(L.F), _p(L.X), _p(L.info),
                      _p(L.data_off), _p(L.Fc), st)
         # bytes streamed per solve: F11inv + X (forward) + X^T (backward)
@@ -444,14 +408,6 @@ class CoarseND:
         """
         st = _stream()
         ys, cb = self._bufs()
-        if self.persistent and self.levels:
-            nat.call("bddc_nd_solve_persist", self.p_nitems, _p(self.p_items), self.p_nn,
-                     _p(self.p_nodes), _p(self.p_off), _p(self.p_sep), _p(self.p_bnd),
-                     _p(self.p_lptr), _p(self.p_lsrc), _p(self.pptr), _p(self.psrc),
-                     _p(self.Fc_all), _p(Pcinv), _p(r), _p(self._rs_all), _p(self._y_all), _p(cb),
-                     _p(self._prhs), _p(x), _p(self.p_cnt), self.p_root, self.N, self.nfc, npc,
-                     self.p_npg, self.p_npv, self.p_smem, 0, st)
-            return
         for li, L in enumerate(self.levels):
             nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
@@ -469,8 +425,5 @@ class CoarseND:
             cb = torch.empty(self.cb_total, dtype=F64, device=self.dev)
             self._yb = (ys, cb)
             self._prhs = torch.empty(max(self.N, 1), dtype=F64, device=self.dev)
-            self._rs = torch.empty(max(max(L.ysize for L in self.levels), 1), dtype=F64, device=self.dev)
-            py = max(getattr(self, "p_ysize", 0), 1)
-            self._rs_all = torch.empty(py, dtype=F64, device=self.dev)
-            self._y_all = torch.empty(py, dtype=F64, device=self.dev)
+            self._rs = torch.empty(max([L.ysize for L in self.levels] + [1]), dtype=F64, device=self.dev)
         return self._yb
