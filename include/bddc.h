@@ -59,6 +59,13 @@ int bddc_version(void);
  * (mma.sync m8n8k4 f64).  upper != 0 computes only tiles on/above the
  * diagonal.  Replaces the dense BLAS products of coarse.py:179-185 and
  * adaptive.py:123-137. */
+/* Same with per-batch live sizes: dims[b*dstride + 0..2] = (M_b, N_b, K_b) <= (M, N, K);
+ * operands beyond them read as zero, output tiles entirely outside are
+ * zero-filled when beta == 0 and left untouched otherwise. */
+int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int K, double alpha,
+                            const double* A, int lda, long long sA, const double* B, int ldb,
+                            long long sB, double beta, double* C, int ldc, long long sC,
+                            int batch, int upper, const int* dims, int dstride, void* stream);
 int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha,
                        const double* A, int lda, long long sA, const double* B, int ldb,
                        long long sB, double beta, double* C, int ldc, long long sC, int batch,
@@ -133,7 +140,7 @@ int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces,
                       const int* gcode, const int* nG, const double* rows, const double* qbasis,
                       int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
                       double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi,
-                      double* T, double* b0, void* inv_ws, int* info, void* stream);
+                      double* T, double* b0, void* inv_ws, int* dims, int* info, void* stream);
 int bddc_pad_identity(double* M, int n, int npad, void* stream);
 
 /* Nested-dissection multifrontal coarse solver (replaces the dense coarse

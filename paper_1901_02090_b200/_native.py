@@ -82,6 +82,8 @@ _GP = C.POINTER(Geom)
 _SIGS = {
     "bddc_dgemm_batched": [_I, _I, _I, _I, _I, _D, _P, _I, _L, _P, _I, _L, _D,
                            _P, _I, _L, _I, _I, _P],
+    "bddc_dgemm_batched_dims": [_I, _I, _I, _I, _I, _D, _P, _I, _L, _P, _I, _L, _D,
+                                _P, _I, _L, _I, _I, _P, _I, _P],
     "bddc_spd_inverse_workspace": [_I, _I, _I],
     "bddc_spd_inverse_batched": [_P, _I, _I, _L, _I, _I, _P, _P, _P],
     "bddc_cell_coeffs": [_GP, _P, _P, _P],
@@ -96,7 +98,7 @@ _SIGS = {
     "bddc_pair_eigs": [_GP, _P, _P, _P, _P, _P, _D, _I, _P, _I, _P, _P, _P,
                        _P, _P, _P, _P, _P],
     "bddc_coarse_local": [_GP, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P,
-                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_pad_identity": [_P, _I, _I, _P],
     "bddc_graph_begin": [C.POINTER(C.c_void_p), _P],
     "bddc_graph_while": [_P, _P],

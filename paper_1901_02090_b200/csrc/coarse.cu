@@ -17,6 +17,10 @@
 extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
                                   int lda, long long sA, const double* B, int ldb, long long sB, double beta,
                                   double* C, int ldc, long long sC, int batch, int upper, void* stream);
+extern "C" int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int K, double alpha,
+                                       const double* A, int lda, long long sA, const double* B, int ldb,
+                                       long long sB, double beta, double* C, int ldc, long long sC,
+                                       int batch, int upper, const int* dims, int dstride, void* stream);
 extern "C" int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                                         int* info, void* stream);
 
@@ -131,6 +135,21 @@ __global__ void scale_rows_kernel(long long per, const double* __restrict__ gamm
     X[(size_t)i * per + e] *= sc;
 }
 
+// Per-subdomain live GEMM sizes (stride 16): nG_i and nC_i (= live coarse rows).
+//  0: (nG, nC, nG)  3: (nC, nC, nG)  6: (nC, nG, nC)  9: (nG, nG, nC)  12: (nG, nC, nC)
+__global__ void coarse_dims_kernel(int N, int maxC, const int* __restrict__ nG, const int* __restrict__ sub_rows,
+                                   int* __restrict__ dims) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int nc = 0;
+  while (nc < maxC && sub_rows[((size_t)i * maxC + nc) * 4] >= 0) ++nc;
+  const int ng = nG[i];
+  int* d = dims + (size_t)i * 16;
+  const int v[15] = {ng, nc, ng, nc, nc, ng, nc, ng, nc, ng, ng, nc, ng, nc, nc};
+  for (int k = 0; k < 15; ++k) d[k] = v[k];
+  d[15] = 0;
+}
+
 // Identity padding for a dense matrix beyond n.
 __global__ void pad_tail_identity_kernel(double* M, int n, int npad) {
   long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -153,37 +172,46 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
                                  const int* gcode, const int* nG, const double* rows, const double* qbasis,
                                  int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
                                  double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi, double* T,
-                                 double* b0, void* inv_ws, int* info, void* stream) {
+                                 double* b0, void* inv_ws, int* dims, int* info, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int N = g->N, mg = g->maxG;
   const long long sG = (long long)mg * mg, sGC = (long long)mg * maxC, sCC = (long long)maxC * maxC;
   if (maxC % 32) return bddc_set_error(BDDC_ERR_ARG, "coarse_local: maxC must be a multiple of 32");
   coarse_ct_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, rows, maxsel, maxC, Ct);
   LAUNCH_OK();
+  // every product below runs on the live nG_i x nC_i blocks only (maxC pads to the
+  // largest subdomain's coarse count; the mean is ~5x smaller)
+  coarse_dims_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, maxC, nG, sub_rows, dims);
+  LAUNCH_OK();
+  const int* dGCG = dims;
+  const int* dCCG = dims + 3;
+  const int* dCGC = dims + 6;
+  const int* dGGC = dims + 9;
+  const int* dGCC = dims + 12;
   int r;
   // Y = Sinv C^T ; Kinv = C Y ; Kc = Kinv^-1 ; PsiT = Kc Y^T ; b0
-  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, mg, 1.0, Sinv, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 0, mg, maxC, mg, 1.0, Sinv, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, dGCG, 16, stream)))
     return r;
-  if ((r = bddc_dgemm_batched(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, Kc, maxC, sCC, N, 0,
-                              stream)))
+  if ((r = bddc_dgemm_batched_dims(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, Kc, maxC, sCC, N, 0, dCCG,
+                                   16, stream)))
     return r;
   pad_identity_kernel<<<N, 256, 0, s>>>(maxC, sub_rows, Kc);
   LAUNCH_OK();
   if ((r = bddc_spd_inverse_batched(Kc, maxC, maxC, sCC, N, 32, inv_ws, info, stream))) return r;
-  if ((r = bddc_dgemm_batched(0, 1, maxC, mg, maxC, 1.0, Kc, maxC, sCC, Y, maxC, sGC, 0.0, Psi, mg, sGC, N, 0,
-                              stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, maxC, mg, maxC, 1.0, Kc, maxC, sCC, Y, maxC, sGC, 0.0, Psi, mg, sGC, N, 0, dCGC,
+                                   16, stream)))
     return r;
   b0_kernel<<<N, 256, 0, s>>>(*g, gcode, sub_rows, Psi, Dsub, maxC, b0);
   LAUNCH_OK();
   // ---- T = (P S P + g Q Q^T)^-1 - Q Q^T / g   (Q in Ct, S Q in Y, Q^T S Q in E[..maxC^2])
   qc_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, qbasis, maxsel, maxC, Ct);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, mg, 1.0, S, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 0, mg, maxC, mg, 1.0, S, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, dGCG, 16, stream)))
     return r;
   double* QtSQ = Kc;  // Kc is kept: use the tail of E for Q^T S Q instead
   QtSQ = E + (size_t)N * sGC - (size_t)N * sCC;
-  if ((r = bddc_dgemm_batched(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, QtSQ, maxC, sCC, N, 0,
-                              stream)))
+  if ((r = bddc_dgemm_batched_dims(1, 0, maxC, maxC, mg, 1.0, Ct, maxC, sGC, Y, maxC, sGC, 0.0, QtSQ, maxC, sCC, N, 0, dCCG,
+                                   16, stream)))
     return r;
   gamma_kernel<<<N, 128, 0, s>>>(mg, maxC, nG, sub_rows, S, gamma, QtSQ);
   LAUNCH_OK();
@@ -191,22 +219,22 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   long long tot = (long long)N * sG;
   copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(S, T, tot);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
     return r;
-  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
     return r;
   // Y <- Q (Q^T S Q + g I)   (reuse Y)
-  if ((r = bddc_dgemm_batched(0, 0, mg, maxC, maxC, 1.0, Ct, maxC, sGC, QtSQ, maxC, sCC, 0.0, Y, maxC, sGC, N, 0,
-                              stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 0, mg, maxC, maxC, 1.0, Ct, maxC, sGC, QtSQ, maxC, sCC, 0.0, Y, maxC, sGC, N, 0, dGCC,
+                                   16, stream)))
     return r;
-  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
     return r;
   if ((r = bddc_spd_inverse_batched(T, mg, mg, sG, N, 32, inv_ws, info, stream))) return r;
   // T -= (Q/sqrt g)(Q/sqrt g)^T
   dim3 gsc(64, N);
   scale_rows_kernel<<<gsc, 256, 0, s>>>(sGC, gamma, Ct);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
     return r;
   return 0;
 }

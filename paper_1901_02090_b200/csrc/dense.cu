@@ -105,12 +105,32 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
                                                     const double* __restrict__ A, int lda, long long sA,
                                                     const double* __restrict__ B, int ldb, long long sB,
                                                     double beta, double* __restrict__ C, int ldc,
-                                                    long long sC, int upper) {
+                                                    long long sC, int upper, const int* __restrict__ dims,
+                                                    int dstride) {
   const int bn = blockIdx.x, bm = blockIdx.y, bz = blockIdx.z;
   if ((upper & 1) && bm > bn) return;
   A += bz * sA;
   B += bz * sB;
   C += bz * sC;
+  int Ml = M, Nl = N;
+  if (dims) {
+    // per-batch live sizes (padded batches): operands beyond them read as zero,
+    // tiles entirely outside are zero-filled (beta == 0) or skipped
+    const int* d = dims + (size_t)bz * dstride;
+    const int Mb = imin(d[0], M), Nb = imin(d[1], N);
+    K = imin(d[2], K);
+    if (bm * BM >= Mb || bn * BN >= Nb) {
+      if (beta == 0.0) {
+        for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+          const int r = bm * BM + e / BN, c = bn * BN + e % BN;
+          if (r < M && c < N) C[(size_t)r * ldc + c] = 0.0;
+        }
+      }
+      return;
+    }
+    Ml = Mb;
+    Nl = Nb;
+  }
   __shared__ __align__(16) double As[2][TILE_ELEMS];
   __shared__ __align__(16) double Bs[2][TILE_ELEMS];
   const int m0 = bm * BM, n0 = bn * BN;
@@ -135,14 +155,14 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
   const int nk = (kend > kbeg) ? (kend + BK - 1) / BK : kt0;
   if (kt0 < nk) {
   // A operand rows are m (R = M); B operand rows are n (R = N).
-  load_tile<transA, aligned>(As[kt0 & 1], A, lda, M, K, m0, kbeg);
-  load_tile<!transB, aligned>(Bs[kt0 & 1], B, ldb, N, K, n0, kbeg);
+  load_tile<transA, aligned>(As[kt0 & 1], A, lda, Ml, K, m0, kbeg);
+  load_tile<!transB, aligned>(Bs[kt0 & 1], B, ldb, Nl, K, n0, kbeg);
   cp_async_commit();
   }
   for (int kt = kt0; kt < nk; ++kt) {
     if (kt + 1 < nk) {
-      load_tile<transA, aligned>(As[(kt + 1) & 1], A, lda, M, K, m0, (kt + 1) * BK);
-      load_tile<!transB, aligned>(Bs[(kt + 1) & 1], B, ldb, N, K, n0, (kt + 1) * BK);
+      load_tile<transA, aligned>(As[(kt + 1) & 1], A, lda, Ml, K, m0, (kt + 1) * BK);
+      load_tile<!transB, aligned>(Bs[(kt + 1) & 1], B, ldb, Nl, K, n0, (kt + 1) * BK);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -311,10 +331,23 @@ __global__ void lower_from_upper_kernel(double* M, int n, int ld, long long sM) 
 
 }  // namespace
 
+extern "C" int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int K, double alpha,
+                                       const double* A, int lda, long long sA, const double* B, int ldb,
+                                       long long sB, double beta, double* C, int ldc, long long sC,
+                                       int batch, int upper, const int* dims, int dstride, void* stream);
+
 extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha,
                                   const double* A, int lda, long long sA, const double* B, int ldb,
                                   long long sB, double beta, double* C, int ldc, long long sC,
                                   int batch, int upper, void* stream) {
+  return bddc_dgemm_batched_dims(transA, transB, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, batch,
+                                 upper, nullptr, 0, stream);
+}
+
+extern "C" int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int K, double alpha,
+                                       const double* A, int lda, long long sA, const double* B, int ldb,
+                                       long long sB, double beta, double* C, int ldc, long long sC,
+                                       int batch, int upper, const int* dims, int dstride, void* stream) {
   if (M <= 0 || N <= 0 || batch <= 0) return 0;
   if (K <= 0) {
     // C = beta*C is not needed by any caller; require K > 0
@@ -325,9 +358,11 @@ extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, d
   bool al = ((((uintptr_t)A) | ((uintptr_t)B)) % 16 == 0) && !((lda | ldb) & 1) && !((sA | sB) & 1);
 #define DG_LAUNCH(TA, TB)                                                                                   \
   if (al)                                                                                                   \
-    dgemm_kernel<TA, TB, true><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper); \
+    dgemm_kernel<TA, TB, true><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper, \
+                                                    dims, dstride);                                         \
   else                                                                                                      \
-    dgemm_kernel<TA, TB, false><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper);
+    dgemm_kernel<TA, TB, false><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper, \
+                                                     dims, dstride);
   if (!transA && !transB) {
     DG_LAUNCH(false, false)
   } else if (transA && !transB) {

@@ -264,13 +264,14 @@ class BddcSetup:
         wsz = max(nat.load().bddc_spd_inverse_workspace(maxC, N, 32),
                   nat.load().bddc_spd_inverse_workspace(mg, N, 64))
         ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
+        dims = torch.empty(N * 16, dtype=I32, device=dev)
         nat.call("bddc_coarse_local", gp, _p(dev_rows), _p(self.d_faces),
                  _p(self.d_fslot), _p(self.d_gcode), _p(self.d_nG), _p(rows),
                  _p(qbasis) if qbasis is not None else None, maxsel, _p(self.d_S), _p(Sinv),
                  _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(E), _p(gam), _p(self.d_Kc),
-                 _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws),
+                 _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws), _p(dims),
                  _p(info[2:]), st)
-        del Ct, Y, E, gam, ws, Sinv
+        del Ct, Y, E, gam, ws, Sinv, dims
         # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
         npk = nat.load().bddc_sym_packed_elems(mg)
         self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)

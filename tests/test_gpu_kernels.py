@@ -32,6 +32,50 @@ def test_dgemm_vs_torch(ta, tb, M, N, K):
     assert torch.allclose(Cm, ref, rtol=1e-13, atol=1e-12 * math.sqrt(K))
 
 
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_dgemm_per_batch_dims(beta):
+    """Live (M_b, N_b, K_b) per batch: padded operands beyond them are ignored (even
+    NaN), tiles outside are zero-filled (beta 0) or untouched (beta 1)."""
+    import torch
+    nat = _lib()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    M, N, K, batch = 200, 150, 170, 4
+    A = torch.randn(batch, M, K, dtype=torch.float64, device="cuda", generator=g)
+    Bm = torch.randn(batch, N, K, dtype=torch.float64, device="cuda", generator=g)
+    C0 = torch.randn(batch, M, N, dtype=torch.float64, device="cuda", generator=g)
+    dims = torch.tensor([[200, 150, 170], [37, 90, 5], [1, 1, 1], [130, 64, 129]], dtype=torch.int32,
+                        device="cuda")
+    ref = C0.clone() * beta
+    for z in range(batch):
+        m, n, k = dims[z].tolist()
+        A[z, m:, :] = float("nan")
+        A[z, :, k:] = float("nan")
+        Bm[z, n:, :] = float("nan")
+        Bm[z, :, k:] = float("nan")
+        ref[z, :m, :n] += A[z, :m, :k] @ Bm[z, :n, :k].T
+    Cm = C0.clone()
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.call("bddc_dgemm_batched_dims", 0, 1, M, N, K, 1.0, nat.ptr(A), K, M * K, nat.ptr(Bm), K, N * K,
+             beta, nat.ptr(Cm), N, M * N, batch, 0, nat.ptr(dims), 3, st)
+    torch.cuda.synchronize()
+    for z in range(batch):
+        m, n, k = dims[z].tolist()
+        assert torch.allclose(Cm[z, :m, :n], ref[z, :m, :n], rtol=1e-13, atol=1e-11)
+        outside = torch.ones(M, N, dtype=torch.bool, device="cuda")
+        outside[:m, :n] = False
+        # whole tiles outside the live block: zero (beta 0) or untouched (beta 1)
+        tiles = torch.zeros(M, N, dtype=torch.bool, device="cuda")
+        tiles[((m + 63) // 64) * 64:, :] = True
+        tiles[:, ((n + 63) // 64) * 64:] = True
+        exp = torch.zeros_like(C0[z]) if beta == 0.0 else C0[z]
+        assert torch.equal(Cm[z][tiles], exp[tiles])
+        part = outside & ~tiles
+        if beta == 0.0:
+            assert torch.all(Cm[z][part] == 0.0)
+        else:
+            assert torch.equal(Cm[z][part], C0[z][part])
+
+
 @pytest.mark.parametrize("n,b,batch", [(64, 32, 3), (192, 64, 5), (512, 64, 2)])
 def test_spd_inverse_vs_torch(n, b, batch):
     import torch
