@@ -207,74 +207,79 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
 
 // ------------------------------------------------------- SPD inverse leaves
 
-// Leaf of the Cholesky-based inverse, on the nb x nb diagonal block of every
-// matrix (one CTA per matrix, block in shared memory).
+// Leaf of the Cholesky-based inverse, on the nb x nb (nb <= 64) diagonal block
+// of every matrix: ONE WARP per matrix, block in shared memory (row stride
+// nb + 1: column walks are bank-conflict free), warp-synchronous (no CTA
+// barriers in the sequential column loops).
 //  mode 1 (factor): read the upper triangle, M = U^T U (upper Cholesky),
 //          V = U^-1 in place (column-oriented trtri), write V to the upper
 //          triangle and zeros below it.
 //  mode 2 (lauum):  read V (upper triangle; lower taken as zero), write V V^T.
 //  mode 3: both (the whole matrix fits one leaf).
-__global__ void leaf_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info, int mode) {
-  extern __shared__ double sd[];  // nb*nb + nb
-  double* tmp = sd + nb * nb;
-  __shared__ int bad;
-  const int z = blockIdx.x;
-  double* Mz = M + z * sM;
-  const int nt = blockDim.x;
-  if (threadIdx.x == 0) bad = 0;
-  for (int e = threadIdx.x; e < nb * nb; e += nt) {
-    int r = e / nb, c = e % nb;
-    sd[e] = (c >= r) ? Mz[(size_t)r * ld + c] : 0.0;
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(32) leaf_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info,
+                                                           int mode) {
+  extern __shared__ double sd[];
+  const int ldp = nb + 1;
+  const int lane = threadIdx.x;
+  double* Mz = M + blockIdx.x * sM;
+  for (int r = 0; r < nb; ++r)
+    for (int c = lane; c < nb; c += 32) sd[r * ldp + c] = (c >= r) ? Mz[(size_t)r * ld + c] : 0.0;
+  __syncwarp();
+  int bad = 0;
   if (mode & 1) {
-    // right-looking upper Cholesky
+    // right-looking upper Cholesky: lanes own columns
     for (int k = 0; k < nb; ++k) {
-      double d = sd[k * nb + k];
+      double d = sd[k * ldp + k];
       if (!(d > 0.0)) {
-        if (threadIdx.x == 0) bad = 1;
+        bad = 1;
         d = 1.0;
       }
       d = sqrt(d);
-      __syncthreads();
-      for (int c = k + threadIdx.x; c < nb; c += nt) sd[k * nb + c] = (c == k) ? d : sd[k * nb + c] / d;
-      __syncthreads();
-      const int w = nb - k - 1;
-      for (int e = threadIdx.x; e < w * w; e += nt) {
-        int r = k + 1 + e / w, c = k + 1 + e % w;
-        if (c >= r) sd[r * nb + c] -= sd[k * nb + r] * sd[k * nb + c];
+      const double id = 1.0 / d;
+      __syncwarp();
+      for (int c = k + lane; c < nb; c += 32) sd[k * ldp + c] = (c == k) ? d : sd[k * ldp + c] * id;
+      __syncwarp();
+      for (int c = k + 1 + lane; c < nb; c += 32) {
+        const double ukc = sd[k * ldp + c];
+        for (int r = k + 1; r <= c; ++r) sd[r * ldp + c] -= sd[k * ldp + r] * ukc;
       }
-      __syncthreads();
+      __syncwarp();
     }
-    // V = U^-1 column by column: V[0:j, j] = -V[j][j] * V[0:j, 0:j] U[0:j, j]
+    // V = U^-1 column by column: V[i][j] = -V[j][j] sum_{k=i}^{j-1} V[i][k] U[k][j]
     for (int j = 0; j < nb; ++j) {
-      const double vjj = 1.0 / sd[j * nb + j];
-      for (int i = threadIdx.x; i < j; i += nt) tmp[i] = sd[i * nb + j];
-      __syncthreads();
-      for (int i = threadIdx.x; i < j; i += nt) {
+      const double vjj = 1.0 / sd[j * ldp + j];
+      double nv[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int i = lane + 32 * t;
         double acc = 0.0;
-        for (int k = i; k < j; ++k) acc += sd[i * nb + k] * tmp[k];
-        sd[i * nb + j] = -vjj * acc;
+        if (i < j)
+          for (int k = i; k < j; ++k) acc += sd[i * ldp + k] * sd[k * ldp + j];
+        nv[t] = -vjj * acc;
       }
-      if (threadIdx.x == 0) sd[j * nb + j] = vjj;
-      __syncthreads();
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int i = lane + 32 * t;
+        if (i < j) sd[i * ldp + j] = nv[t];
+      }
+      if (lane == 0) sd[j * ldp + j] = vjj;
+      __syncwarp();
     }
   }
-  if (threadIdx.x == 0 && bad) atomicAdd(info, 1);
+  if (lane == 0 && bad) atomicAdd(info, 1);
   if (mode & 2) {
     // X = V V^T: X[r][c] = sum_{k >= max(r,c)} V[r][k] V[c][k]
-    for (int e = threadIdx.x; e < nb * nb; e += nt) {
-      int r = e / nb, c = e % nb;
-      int k0 = r > c ? r : c;
-      double acc = 0.0;
-      for (int k = k0; k < nb; ++k) acc += sd[r * nb + k] * sd[c * nb + k];
-      Mz[(size_t)r * ld + c] = acc;
-    }
+    for (int r = 0; r < nb; ++r)
+      for (int c = r + lane; c < nb; c += 32) {
+        double acc = 0.0;
+        for (int k = c; k < nb; ++k) acc += sd[r * ldp + k] * sd[c * ldp + k];
+        Mz[(size_t)r * ld + c] = acc;
+        if (mode == 3) Mz[(size_t)c * ld + r] = acc;
+      }
   } else {
-    for (int e = threadIdx.x; e < nb * nb; e += nt) {
-      int r = e / nb, c = e % nb;
-      Mz[(size_t)r * ld + c] = sd[e];   // V upper, zeros below
-    }
+    for (int r = 0; r < nb; ++r)
+      for (int c = lane; c < nb; c += 32) Mz[(size_t)r * ld + c] = (c >= r) ? sd[r * ldp + c] : 0.0;
   }
 }
 
@@ -286,27 +291,6 @@ __global__ void block_copy_kernel(double* dst, int ld, long long sD, const doubl
        e += (long long)gridDim.x * blockDim.x) {
     int r = (int)(e / cols), c = (int)(e % cols);
     dst[z * sD + (size_t)r * ld + c] = src ? src[z * sS + (size_t)r * lds + c] : 0.0;
-  }
-}
-
-// Symmetric Jacobi scaling: mode 0: dsq = diag^-1/2 and M <- D^-1/2 M D^-1/2;
-// mode 1: M <- D^-1/2 M D^-1/2 with the stored dsq (turns inv(scaled) into inv(M)).
-__global__ void jacobi_scale_kernel(double* M, int n, int ld, long long sM, double* dsq, int mode) {
-  const int z = blockIdx.y;
-  double* Mz = M + z * sM;
-  double* dz = dsq + (size_t)z * n;
-  if (mode == 0 && blockIdx.x == 0) {
-    for (int r = threadIdx.x; r < n; r += blockDim.x) {
-      double d = Mz[(size_t)r * ld + r];
-      dz[r] = (d > 0.0) ? rsqrt(d) : 1.0;
-    }
-  }
-  __syncthreads();
-  if (mode == 0) return;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * n;
-       e += (long long)gridDim.x * blockDim.x) {
-    int r = (int)(e / n), c = (int)(e % n);
-    Mz[(size_t)r * ld + c] *= dz[r] * dz[c];
   }
 }
 
@@ -395,10 +379,10 @@ int block_copy(double* dst, int ld, long long sD, const double* src, int lds, lo
 }
 
 int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
-  size_t shm = (size_t)(n * n + n) * sizeof(double);
+  size_t shm = (size_t)n * (n + 1) * sizeof(double);
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  leaf_chol_inv_kernel<<<batch, 256, shm, s>>>(M, n, ld, sM, info, mode);
+  leaf_chol_inv_kernel<<<batch, 32, shm, s>>>(M, n, ld, sM, info, mode);
   LAUNCH_OK();
   return 0;
 }
@@ -457,8 +441,9 @@ int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* 
 }  // namespace
 
 // In-place inverse of `batch` SPD matrices of order n (full symmetric storage,
-// leading dim ld, batch stride sM): Jacobi scaling, M = U^T U, V = U^-1,
-// M^-1 = V V^T, all recursive with DMMA GEMMs above leaves of order <= b.
+// leading dim ld, batch stride sM): M = U^T U, V = U^-1, M^-1 = V V^T, all
+// recursive with DMMA GEMMs above leaves of order <= b.  (No diagonal
+// rescaling: Cholesky-based inversion is insensitive to it, van der Sluis.)
 // `ws` must hold bddc_spd_inverse_workspace(n, batch, b) bytes; `info` (device
 // int) counts non-positive pivots.
 extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
@@ -466,13 +451,7 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
   if (n <= 0 || batch <= 0) return 0;
   if (b <= 0 || b > 64) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: leaf size must be in 1..64");
   cudaStream_t s = (cudaStream_t)stream;
-  double* dsq = (double*)ws;
-  double* rest = dsq + (size_t)batch * n;
-  dim3 g0(1, batch), g1(64, batch);
-  jacobi_scale_kernel<<<g0, 256, 0, s>>>(Mat, n, ld, sM, dsq, 0);
-  LAUNCH_OK();
-  jacobi_scale_kernel<<<g1, 256, 0, s>>>(Mat, n, ld, sM, dsq, 1);
-  LAUNCH_OK();
+  double* rest = (double*)ws;
   int r;
   if (n <= b) {
     if ((r = leaf_launch(Mat, n, ld, sM, batch, info, 3, s))) return r;
@@ -483,7 +462,5 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
     lower_from_upper_kernel<<<ga, dim3(32, 8), 0, s>>>(Mat, n, ld, sM);
     LAUNCH_OK();
   }
-  jacobi_scale_kernel<<<g1, 256, 0, s>>>(Mat, n, ld, sM, dsq, 1);
-  LAUNCH_OK();
   return 0;
 }

@@ -194,7 +194,7 @@ class BddcSetup:
         nat.call("bddc_pack_sym", N, mp, _p(self.d_Q), _p(self.d_Qp), st)
         del self.d_Q
         Sinv = self.d_S.clone()
-        leaf = 64
+        leaf = 32
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, leaf) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(Sinv), mg, mg, mg * mg, N, leaf,
@@ -424,7 +424,7 @@ class BddcSetup:
         info = torch.zeros(1, dtype=I32, device=dev)
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(npc, 1, 64) // 8 + 2,
                          dtype=F64, device=dev)
-        nat.call("bddc_spd_inverse_batched", _p(Pc), npc, npc, 0, 1, 64, _p(ws), _p(info), st)
+        nat.call("bddc_spd_inverse_batched", _p(Pc), npc, npc, 0, 1, 32, _p(ws), _p(info), st)
         if int(info.item()):
             raise ConfigurationError(
                 "coarse problem singular; initial constraints do not cover all faces")
