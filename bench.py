@@ -255,7 +255,7 @@ def main():
     peak, peak_kind = _peaks()
     achieved = alg_bytes / kmean / 1e9 if kdur else None
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_gather_gemv.json")
+    tp = os.path.join(ROOT, "profiles", "traffic_gather_symv.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")
