@@ -113,8 +113,49 @@ def nd_geometry(dec):
 
     if dec.n_subdomains > 1:
         rec((0, 0, 0), tuple(S3), 0)
+    nodes = _contract(nodes, ND_MERGE)
     dec._nd_geometry = nodes
     return nodes
+
+
+# Binary-tree levels merged per multifrontal node: a node eliminates the
+# separators of `ND_MERGE` consecutive bisection levels at once (up to
+# 2**ND_MERGE children), halving the number of sequential solve levels; the
+# level count, not the bytes, bounds the coarse solve's latency.
+ND_MERGE = 2
+
+
+def _contract(nodes, c):
+    """Merge c consecutive levels of the bisection tree into one node level."""
+    if c <= 1 or not nodes:
+        return nodes
+    out = []
+
+    def build(k, depth):
+        idx = len(out)
+        out.append(None)
+        n = nodes[k]
+        if n["leaf"]:
+            out[idx] = dict(leaf=True, sub=n["sub"], depth=depth)
+            return idx
+        seps = [n["sep"]]
+        frontier = list(n["ch"])
+        for _ in range(c - 1):
+            nxt = []
+            for x in frontier:
+                if nodes[x]["leaf"]:
+                    nxt.append(x)
+                else:
+                    seps.append(nodes[x]["sep"])
+                    nxt.extend(nodes[x]["ch"])
+            frontier = nxt
+        ch = tuple(build(x, depth + 1) for x in frontier)
+        out[idx] = dict(leaf=False, depth=depth, sep=np.concatenate(seps), bnd=n["bnd"],
+                        pres=n["pres"], ch=ch)
+        return idx
+
+    build(0, 0)
+    return out
 
 
 def nd_geometry_flat(dec):
@@ -137,12 +178,16 @@ def nd_geometry_flat(dec):
     F["sep_ptr"], F["sep"] = csr("sep")
     F["bnd_ptr"], F["bnd"] = csr("bnd")
     F["pres_ptr"], F["pres"] = csr("pres")
-    # children: internal index (>= 0) or -(1 + subdomain) for leaves
-    ch = np.zeros((len(internal), 2), dtype=np.int64)
+    # children: internal index (>= 0) or -(1 + subdomain) for leaves; nch per node
+    ns = max([len(geo[k]["ch"]) for k in internal] + [1])
+    ch = np.zeros((len(internal), ns), dtype=np.int64)
+    nch = np.zeros(len(internal), dtype=np.int64)
     for i, k in enumerate(internal):
+        nch[i] = len(geo[k]["ch"])
         for s_, c in enumerate(geo[k]["ch"]):
             ch[i, s_] = gpos[c] if not geo[c]["leaf"] else -(1 + geo[c]["sub"])
     F["ch"] = ch
+    F["nch"] = nch
     dec._nd_geometry_flat = F
     return F
 
@@ -216,8 +261,10 @@ class CoarseND:
             ids = order[lev_start[li]:lev_start[li + 1]]
             pos[ids] = np.arange(len(ids))
         ch = G["ch"]
-        internal_ch = ch >= 0
-        par = np.repeat(np.arange(nI)[:, None], 2, axis=1)
+        NS = ch.shape[1]
+        has = np.arange(NS)[None, :] < G["nch"][:, None]
+        internal_ch = (ch >= 0) & has
+        par = np.repeat(np.arange(nI)[:, None], NS, axis=1)
         if np.any(lev[ch[internal_ch]] != lev[par[internal_ch]] - 1):
             raise ConfigurationError("nested dissection: child not one level below")
         sub_g = np.asarray(sub_rows[:, :, 0], dtype=np.int64)
@@ -248,12 +295,15 @@ class CoarseND:
             fk, fv = fk[fo], fv[fo]
             K = 1
             maps = []
-            ckind = np.zeros((2, m, 3), dtype=np.int32)
-            for slot in (0, 1):
+            L.nslots = NS
+            ckind = np.zeros((NS, m, 3), dtype=np.int32)
+            for slot in range(NS):
                 c = ch[ids, slot]
-                leafc = c < 0
+                valid = has[ids, slot]
+                leafc = (c < 0) & valid
                 subc = np.where(leafc, -c - 1, 0)
                 elen = np.where(leafc, nC[subc] + 1, nb[np.maximum(c, 0)])
+                elen = np.where(valid, elen, 0)
                 erow = np.repeat(np.arange(m), elen)
                 ecol = _ranges(np.zeros(m, np.int64), elen)
                 cr = c[erow]
@@ -271,12 +321,14 @@ class CoarseND:
                     raise ConfigurationError("nested dissection: child export not in parent front")
                 maps.append((erow, ecol, fv[loc].astype(np.int32)))
                 K = max(K, int(elen.max()) if m else 1)
+                intc = valid & ~leafc
                 ckind[slot, leafc, 0] = 1
                 ckind[slot, leafc, 1] = subc[leafc]
                 ckind[slot, leafc, 2] = nC[subc[leafc]]
-                ckind[slot, ~leafc, 1] = pos[c[~leafc]]
+                ckind[slot, intc, 1] = pos[c[intc]]
+                ckind[slot, ~valid, 0] = 2
             L.K = K
-            cmap = np.full((2, m, K), -1, dtype=np.int32)
+            cmap = np.full((NS, m, K), -1, dtype=np.int32)
             for slot, (erow, ecol, v) in enumerate(maps):
                 cmap[slot, erow, ecol] = v
             L.sep_idx = t(sep_idx)
@@ -362,7 +414,7 @@ class CoarseND:
         for li, L in enumerate(self.levels):
             L.F = torch.empty(L.m * L.nf * L.nf, dtype=F64, device=self.dev)
             child = self.levels[li - 1] if li > 0 else None
-            for slot in (0, 1):
+            for slot in range(L.nslots):
                 nat.call("bddc_nd_assemble", L.m, L.S, L.B, L.nf, slot, L.K, _p(L.cmap),
                          _p(L.ckind), _p(L.sep_idx), _p(L.F),
                          _p(child.F) if child is not None else None,

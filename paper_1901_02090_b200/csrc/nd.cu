@@ -26,6 +26,7 @@ __global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K,
   const int* mp = cmap + ((size_t)slot * m + q) * K;
   const int* ck = ckind + ((size_t)slot * m + q) * 3;
   const int kind = ck[0], idx = ck[1], npr = ck[2];
+  if (kind == 2) return;   // no child in this slot
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)K * K;
        e += (long long)gridDim.x * blockDim.x) {
     int r = (int)(e / K), c = (int)(e % K);
