@@ -120,18 +120,23 @@ def nd_geometry(dec):
 
 # Binary-tree levels merged per multifrontal node: a node eliminates the
 # separators of `ND_MERGE` consecutive bisection levels at once (up to
-# 2**ND_MERGE children), halving the number of sequential solve levels; the
-# level count, not the bytes, bounds the coarse solve's latency.
-ND_MERGE = 2
+# 2**ND_MERGE children), dividing the number of sequential solve levels by
+# ND_MERGE (C3: 13 -> 5); the level count, not the bytes, bounds the coarse
+# solve's latency (C3 coarse solve 284 us binary, 192 us with 2, 166 us with 3,
+# 201 us with 4: the 3394-dof root front of 4 is bandwidth-bound).
+ND_MERGE = 3
 
 
 def _contract(nodes, c):
-    """Merge c consecutive levels of the bisection tree into one node level."""
-    if c <= 1 or not nodes:
+    """Merge c consecutive levels of the bisection tree into one node level
+    (c: int, or a per-depth list whose last entry repeats)."""
+    sched = list(c) if isinstance(c, (list, tuple)) else [c]
+    if max(sched) <= 1 or not nodes:
         return nodes
     out = []
 
     def build(k, depth):
+        c = sched[min(depth, len(sched) - 1)]
         idx = len(out)
         out.append(None)
         n = nodes[k]
