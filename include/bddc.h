@@ -213,6 +213,10 @@ int bddc_dot(const double* x, const double* y, long long n, void* ws, double* sc
 int bddc_cg_update(long long n, const double* scal, double* x, const double* p, double* r,
                    const double* Ap, void* stream);
 int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream);
+/* Dense (Phi Phi^T)^+ of the separable subdomain-grid Laplacian (setup; ws holds
+ * 2 N^2 doubles, N = S0 S1 S2): Lp = Dm W Lambda^+ W^T Dm, W = Qx (x) Qy (x) Qz. */
+int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const double* dm, double* ws, double* Lp,
+                   void* stream);
 int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream);
 int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out,
                  void* stream);

@@ -226,8 +226,25 @@ __global__ void nd_pressure_gemv_kernel(int N, int nfc, int npc, const double* _
   if (row == 0 && lane == 0) x[nfc] = 0.0;
   if (row >= N - 1) return;
   const double* mr = Pcinv + (size_t)row * npc;
-  double acc = 0.0;
-  for (int c = lane; c < N - 1; c += 32) acc += mr[c] * rp[c];
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.0;
+  const int n = N - 1;
+  int c = lane;
+  for (; c + 224 < n; c += 256) {
+    double m[8], v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      m[u] = __ldg(mr + c + 32 * u);
+      v[u] = rp[c + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (c + 32 * u < n) a[u] += __ldg(mr + c + 32 * u) * rp[c + 32 * u];
+  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) x[nfc + 1 + row] = -acc;
 }

@@ -433,16 +433,64 @@ __global__ void p_update_kernel(long long n, const double* __restrict__ scal, co
 }
 
 // Dense (row-major, symmetric) GEMV y = M x over n rows, warp per row.
+// y = M x, warp per row, 8 loads per lane in flight (fixed order: deterministic).
 __global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ M, const double* __restrict__ x,
                             double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n) return;
   const double* mr = M + (size_t)row * ld;
-  double acc = 0.0;
-  for (int c = lane; c < ncol; c += 32) acc += mr[c] * x[c];
+  double a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.0;
+  int c = lane;
+  for (; c + 224 < ncol; c += 256) {
+    double m[8], v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      m[u] = __ldg(mr + c + 32 * u);
+      v[u] = __ldg(x + c + 32 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (c + 32 * u < ncol) a[u] += __ldg(mr + c + 32 * u) * __ldg(x + c + 32 * u);
+  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) y[row] = acc;
+}
+
+// Dense pseudo-inverse of the separable subdomain-grid Laplacian (setup):
+// W[e][f] = Qx[ex][fx] Qy[ey][fy] Qz[ez][fz] (spatial e, mode f), Ws = W Lambda^+.
+__global__ void lap_kron_kernel(int S0, int S1, int S2, const double* __restrict__ eig, double* __restrict__ W,
+                                double* __restrict__ Ws) {
+  const int N = S0 * S1 * S2;
+  const double* Qx = eig;
+  const double* Qy = Qx + S0 * S0;
+  const double* Qz = Qy + S1 * S1;
+  const double* lx = Qz + S2 * S2;
+  const double* ly = lx + S0;
+  const double* lz = ly + S1;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)N * N;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(t / N), f = (int)(t % N);
+    const int ex = e % S0, ey = (e / S0) % S1, ez = e / (S0 * S1);
+    const int fx = f % S0, fy = (f / S0) % S1, fz = f / (S0 * S1);
+    const double w = Qx[ex * S0 + fx] * Qy[ey * S1 + fy] * Qz[ez * S2 + fz];
+    const double lam = lx[fx] + ly[fy] + lz[fz];
+    W[t] = w;
+    Ws[t] = (f == 0) ? 0.0 : w / lam;
+  }
+}
+
+__global__ void scale_sym_kernel(int N, const double* __restrict__ dm, double* __restrict__ M) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)N * N;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(t / N), f = (int)(t % N);
+    M[t] *= dm[e] * dm[f];
+  }
 }
 
 // Lanczos tridiagonal from CG coefficients (solver.py:236-251); kappa by
@@ -629,6 +677,29 @@ extern "C" int bddc_cg_update(long long n, const double* scal, double* x, const 
 extern "C" int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream) {
   p_update_kernel<<<DOT_BLOCKS, 256, 0, (cudaStream_t)stream>>>(n, scal, z, p);
   LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
+                                  int lda, long long sA, const double* B, int ldb, long long sB, double beta,
+                                  double* C, int ldc, long long sC, int batch, int upper, void* stream);
+
+// Lp = Dm W Lambda^+ W^T Dm (N x N, N = S0 S1 S2); ws: 2 N^2 doubles.
+extern "C" int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const double* dm, double* ws, double* Lp,
+                              void* stream) {
+  const int N = S0 * S1 * S2;
+  if (N <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* W = ws;
+  double* Ws = ws + (size_t)N * N;
+  lap_kron_kernel<<<1024, 256, 0, s>>>(S0, S1, S2, eig, W, Ws);
+  LAUNCH_OK();
+  int r = bddc_dgemm_batched(0, 1, N, N, N, 1.0, Ws, N, 0, W, N, 0, 0.0, Lp, N, 0, 1, 0, stream);
+  if (r) return r;
+  if (dm) {
+    scale_sym_kernel<<<1024, 256, 0, s>>>(N, dm, Lp);
+    LAUNCH_OK();
+  }
   return 0;
 }
 

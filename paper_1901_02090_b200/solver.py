@@ -155,6 +155,17 @@ class BddcSetup:
         eig_u, _ = dec.laplacian_eigs(False)
         self.d_eig_w = t(eig_w, F64)
         self.d_dm_w = t(dm_w, F64)
+        # dense (Phi Phi^T)^+ for the balanced projection: one multi-CTA GEMV per
+        # projection instead of the latency-bound single-CTA separable solve
+        # (N^2 doubles: used up to N = 4096, i.e. 134 MB per GEMV)
+        S3 = dec.S3
+        self.d_Lp = None
+        if N <= 4096:
+            ws = torch.empty(2 * N * N, dtype=F64, device=dev)
+            self.d_Lp = torch.empty(N * N, dtype=F64, device=dev)
+            nat.call("bddc_lap_dense", S3[0], S3[1], S3[2], _p(self.d_eig_w), _p(self.d_dm_w),
+                     _p(ws), _p(self.d_Lp), st)
+            del ws
         self.d_eig_u = t(eig_u, F64)
         # permeability -> cell coefficients, D, delta
         k = np.ascontiguousarray(system.perm.k, dtype=np.float64)
@@ -324,6 +335,7 @@ class BddcSetup:
         # kernels get SM slots ahead of the queued T_i GEMV blocks
         self.side_stream = torch.cuda.Stream(device=dev, priority=-1)
         self.n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.t_grid = 3 * self.n_sm   # T_i GEMV grid while the coarse chain runs (measured best)
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._mark(ev, "done")
@@ -456,9 +468,13 @@ class BddcSetup:
         st = _stream()
         nat.call("bddc_phi", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                  _p(self.d_gcode), _p(y), _p(self.w_phi), st)
-        S3 = self.dec.S3
-        nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(self.d_eig_w),
-                 _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), st)
+        if self.d_Lp is not None:
+            nat.call("bddc_gemv", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi), _p(self.w_z),
+                     st)
+        else:
+            S3 = self.dec.S3
+            nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(self.d_eig_w),
+                     _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), st)
         nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
                  _p(self.w_z), _p(y), st)
 
@@ -489,7 +505,7 @@ class BddcSetup:
         # concurrent coarse chain finds free SM slots
         nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                  _p(self.d_Tp), _p(r), _p(self.d_delta), _p(self.w_yb),
-                 self.n_sm if self.nfc else 0, st)
+                 self.t_grid if self.nfc else 0, st)
         if self.nfc:
             main.wait_event(join)
         nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG), _p(self.d_nC),

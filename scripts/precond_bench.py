@@ -86,3 +86,72 @@ for name, fn in [("gemv_t", gemv_t), ("prolong", prolong), ("lap_solve", lap), (
     torch.cuda.synchronize()
     print(f"{name:14s} {e0.elapsed_time(e1) / 50 * 1000:8.1f} us")
 
+
+for mult in (1, 2, 3, 0):
+    st.t_grid = st.n_sm * mult
+    s = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        full()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s):
+            full()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        gr.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"T grid {st.t_grid:5d}: precond {e0.elapsed_time(e1) / 50 * 1000:7.1f} us")
+
+
+def gt(fn, reps=50):
+    s = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s):
+            fn()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        gr.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1000
+
+
+def forked(first_side=True, tgrid=0):
+    def fn():
+        main = torch.cuda.current_stream()
+        side = st.side_stream
+        f = torch.cuda.Event()
+        f.record(main)
+        side.wait_event(f)
+        def do_side():
+            with torch.cuda.stream(side):
+                nd_only()
+                j = torch.cuda.Event()
+                j.record(side)
+            return j
+        if first_side:
+            j = do_side()
+        nat.call("bddc_gather_symv", st.N, st.maxG, _p(st.d_nG), _p(st.d_gpos), _p(st.d_Tp), _p(r),
+                 _p(st.d_delta), _p(st.w_yb), tgrid, _stream())
+        if not first_side:
+            j = do_side()
+        main.wait_event(j)
+    return fn
+
+
+print("T only %.1f, nd only %.1f, T then nd %.1f" % (gt(T_only), gt(nd_only), gt(lambda: (T_only(), nd_only()))))
+for fs in (True, False):
+    for tg in (148, 296, 0):
+        print(f"forked side_first={fs} tgrid={tg}: {gt(forked(fs, tg)):.1f} us")
