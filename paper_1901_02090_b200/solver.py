@@ -132,6 +132,7 @@ class BddcSetup:
         self.config = config
         self.dev = dev
         self._ktimer = None
+        self.pcg_timer = None   # list -> (start, end) CUDA events of every PCG graph launch
         self.geom = _geom(dec)
         G = self.geom
         gp = C.byref(G)
@@ -933,7 +934,15 @@ def _pcg(setup, W, config, callback):
         # make sure every lazily-created buffer exists before capture
         setup.nd is not None and setup.nd._bufs()
         g = _pcg_graph(setup, W, B, tol, maxit)
+        pt = setup.pcg_timer
+        if pt is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         nat.call("bddc_graph_launch", g, st)
+        if pt is not None:
+            e1.record()
+            pt.append((e0, e1))
         host.copy_(scal, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         top, body = setup._graph_kernels[(float(tol), int(maxit))]
