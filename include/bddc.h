@@ -125,7 +125,9 @@ int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, c
 /* Reduced pair eigenproblems on every face (adaptive.py:63-138), selection
  * of eigenvalues > tau, harvested rows and the reference's dependence
  * filter (adaptive.py:141-173, coarse.py:61-100); omega per face
- * (adaptive.py:56-60). */
+ * (adaptive.py:56-60).  lam_out holds, per face, the eigenvalues in descending
+ * order as far as the selection needs them (all above tau and the next one);
+ * the remaining entries are NaN. */
 size_t bddc_pair_scratch_bytes(int n_faces);
 int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                    const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,

@@ -271,7 +271,14 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   }
   tnorm = fmax(fabs(gl), fabs(gu));
   const double pivmin = fmax(1e-300, tnorm * 1e-300);
-  for (int kk = threadIdx.x; kk < m; kk += blockDim.x) {
+  // only the eigenvalues the selection uses are resolved: those above tau (one
+  // Sturm count at tau gives how many) and the next one (omega, adaptive.py:56-60)
+  __shared__ int nabove;
+  if (threadIdx.x == 0) nabove = (tau < gu) ? m - sturm_below(dg, eo, m, tau, pivmin) : 0;
+  __syncthreads();
+  const int ntop = imin(nabove + 1, m);
+  for (int r = threadIdx.x; r < ntop; r += blockDim.x) {
+    const int kk = m - 1 - r;
     double lo = gl - 1e-14 * tnorm, hi = gu + 1e-14 * tnorm;
     for (int it = 0; it < 200; ++it) {
       double mid = 0.5 * (lo + hi);
@@ -282,13 +289,14 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     lam[kk] = 0.5 * (lo + hi);
   }
   __syncthreads();
-  // descending order: lam_desc[t] = lam[m-1-t], clipped at 0 (adaptive.py:381)
+  // descending order: lam_desc[t] = lam[m-1-t], clipped at 0 (adaptive.py:381);
+  // entries beyond the resolved ones are NaN
   for (int r = threadIdx.x; r < lam_ld; r += blockDim.x)
-    lam_out[(size_t)f * lam_ld + r] = (r < m) ? fmax(lam[m - 1 - r], 0.0) : 0.0;
+    lam_out[(size_t)f * lam_ld + r] = (r < ntop) ? fmax(lam[m - 1 - r], 0.0) : __longlong_as_double(0x7ff8000000000000LL);
   __shared__ int ksel;
   if (threadIdx.x == 0) {
     int k = 0;
-    while (k < m && fmax(lam[m - 1 - k], 0.0) > tau) ++k;
+    while (k < ntop && fmax(lam[m - 1 - k], 0.0) > tau) ++k;
     // omega = max(first eigenvalue <= tau, 1); the full pencil always has zeros
     omega[f] = (k < m) ? fmax(fmax(lam[m - 1 - k], 0.0), 1.0) : 1.0;
     nsel[f] = k;

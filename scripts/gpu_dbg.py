@@ -22,7 +22,7 @@ for name in names:
         lam = st.pair_lambda.cpu().numpy()
         k = min(lam.shape[1], d['pair_lam'].shape[1])
         ref = d['pair_lam'][:, :k]; mine = lam[:, :k]
-        m = np.isfinite(ref) & (ref > 1e-8*np.nanmax(ref))
+        m = np.isfinite(ref) & np.isfinite(mine) & (ref > 1e-8*np.nanmax(ref))
         print('  lam maxrel', np.max(np.abs(mine[m]-ref[m])/ref[m]))
     print('  Mx', GD.rel(st.precondition(d['x']), d['Mx']))
     t=time.time(); rep = B.solve(sysm, dec, cfg, setup=st); t2=time.time()-t
