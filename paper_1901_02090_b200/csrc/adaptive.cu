@@ -92,11 +92,12 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
                                 const double* __restrict__ delta, double tau, int maxsel,
                                 double* __restrict__ lam_out, int lam_ld, int* __restrict__ nsel,
                                 int* __restrict__ nadd, double* __restrict__ rows, double* __restrict__ omega,
-                                double* __restrict__ scratch, double* __restrict__ qbasis, int* __restrict__ err) {
+                                double* __restrict__ scratch, double* __restrict__ qbasis, int* __restrict__ err,
+                                const int* __restrict__ flist) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ int bad;
-  const int f = blockIdx.x;
+  const int f = flist ? flist[blockIdx.x] : blockIdx.x;
   const int i = faces[4 * f], j = faces[4 * f + 1], a = faces[4 * f + 2], m = faces[4 * f + 3];
   const int ld = m + ((m & 1) ? 0 : 1);
   const int mg = G.maxG;
@@ -277,16 +278,24 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   if (threadIdx.x == 0) nabove = (tau < gu) ? m - sturm_below(dg, eo, m, tau, pivmin) : 0;
   __syncthreads();
   const int ntop = imin(nabove + 1, m);
-  for (int r = threadIdx.x; r < ntop; r += blockDim.x) {
+  // multisection: a warp per eigenvalue, 32 Sturm counts per round (interval / 33)
+  for (int r = warp; r < ntop; r += nw) {
     const int kk = m - 1 - r;
     double lo = gl - 1e-14 * tnorm, hi = gu + 1e-14 * tnorm;
-    for (int it = 0; it < 200; ++it) {
-      double mid = 0.5 * (lo + hi);
-      if (mid <= lo || mid >= hi || hi - lo <= 2e-16 * fmax(fabs(lo), fabs(hi))) break;
-      if (sturm_below(dg, eo, m, mid, pivmin) > kk) hi = mid;
-      else lo = mid;
+    for (int it = 0; it < 64; ++it) {
+      if (hi - lo <= 2e-16 * fmax(fabs(lo), fabs(hi))) break;
+      const double w = hi - lo;
+      const double x = lo + w * (double)(lane + 1) / 33.0;
+      const bool above = sturm_below(dg, eo, m, x, pivmin) > kk;
+      const unsigned msk = __ballot_sync(0xffffffffu, above);
+      const int fl = msk ? __ffs(msk) - 1 : 32;
+      const double nhi = (fl < 32) ? lo + w * (double)(fl + 1) / 33.0 : hi;
+      const double nlo = (fl > 0) ? lo + w * (double)fl / 33.0 : lo;
+      if (nlo == lo && nhi == hi) break;
+      lo = nlo;
+      hi = nhi;
     }
-    lam[kk] = 0.5 * (lo + hi);
+    if (lane == 0) lam[kk] = 0.5 * (lo + hi);
   }
   __syncthreads();
   // descending order: lam_desc[t] = lam[m-1-t], clipped at 0 (adaptive.py:381);
@@ -450,17 +459,21 @@ extern "C" size_t bddc_pair_scratch_bytes(int n_faces) {
 extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                               const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                               int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
-                              double* qbasis, int* err, void* stream) {
+                              double* qbasis, int* err, const int* flist, int nlist, int mmax, void* stream) {
   if (g->maxF > PAIR_MMAX) return bddc_set_error(BDDC_ERR_ARG, "pair face larger than PAIR_MMAX=112 dofs");
-  int m = g->maxF;
-  int ld = m + ((m & 1) ? 0 : 1);
+  // flist == NULL: every face (shared memory sized for maxF); else the nlist faces
+  // listed, all with at most mmax shared dofs (smaller faces -> more CTAs per SM)
+  const int nblk = flist ? nlist : g->n_faces;
+  if (nblk <= 0) return 0;
+  const int m = flist ? imin(mmax, g->maxF) : g->maxF;
+  const int ld = m + ((m & 1) ? 0 : 1);
   size_t shm = (size_t)(2 * m * ld + 4 * m + 3 * (m / 2 + 1)) * sizeof(double) + 2 * m * sizeof(int) + 16;
   // one CTA per face; the per-thread inverse-iteration arrays live in local memory
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(pair_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  pair_eig_kernel<<<g->n_faces, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel,
-                                                                  lam_out, lam_ld, nsel, nadd, rows, omega,
-                                                                  scratch, qbasis, err);
+  pair_eig_kernel<<<nblk, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel, lam_out,
+                                                            lam_ld, nsel, nadd, rows, omega, scratch, qbasis, err,
+                                                            flist);
   LAUNCH_OK();
   return 0;
 }

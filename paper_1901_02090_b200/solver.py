@@ -235,10 +235,16 @@ class BddcSetup:
             qbasis = torch.zeros(nf * (maxsel + 1) * 112, dtype=F64, device=dev)
             err = torch.zeros(1, dtype=I32, device=dev)
             tau = config.tau if math.isfinite(config.tau) else 1e308
-            nat.call("bddc_pair_eigs", gp, _p(self.d_faces), _p(self.d_fslot),
-                     _p(self.d_S), _p(Sinv), _p(self.d_delta), float(tau),
-                     maxsel, _p(lam), lam_ld, _p(d_nsel), _p(d_nadd), _p(rows),
-                     _p(omega), _p(scratch), _p(qbasis), _p(err), st)
+            # two launches by face size: small faces need a third of the shared
+            # memory, so three faces share an SM instead of one
+            fm = dec.face_table[:, 3]
+            for sel, mm in ((fm <= 64, 64), (fm > 64, int(dec.maxF))):
+                if sel.any():
+                    fl = t(np.nonzero(sel)[0].astype(np.int32))
+                    nat.call("bddc_pair_eigs", gp, _p(self.d_faces), _p(self.d_fslot),
+                             _p(self.d_S), _p(Sinv), _p(self.d_delta), float(tau),
+                             maxsel, _p(lam), lam_ld, _p(d_nsel), _p(d_nadd), _p(rows),
+                             _p(omega), _p(scratch), _p(qbasis), _p(err), _p(fl), len(fl), mm, st)
             del scratch
             e = int(err.item())
             if e & 1:
