@@ -441,34 +441,44 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
       }
     }
   }
-  // t = A^{-1}(f - A_IG x) per line; rhs += B_u t
-  for (int a = 0; a < G.dim; ++a) {
-    const int L = b.L[a], m = L - 1, nl = n_lines(b, a), st = axis_stride(b, a);
-    for (int line = threadIdx.x; line < nl; line += blockDim.x) {
-      if (m <= 0) continue;
-      double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
-      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
-      line_factor(c, L, cp, piv);
-      for (int j = 0; j < m; ++j) r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j)] : 0.0;
-      if (A.x_gamma) {
-        int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
-        int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
-        if (qlo >= 0) r[0] -= c[0] * xg[qlo];
-        if (qhi >= 0) r[m - 1] -= c[L - 1] * xg[qhi];
-      }
-      line_solve(c, L, cp, piv, r);
-      double* t = tI + off[a] + line * m;
-      const int base = line_base(b, a, line);
-      for (int j = 0; j < m; ++j) t[j] = r[j];
-      for (int k = 0; k < L; ++k) {
-        double v = 0.0;
-        if (k >= 1) v += r[k - 1];
-        if (k <= m - 1) v -= r[k];
-        rhs[base + k * st] += v;
-      }
+  // t = A^{-1}(f - A_IG x) per line, the lines of all axes at once (thread per
+  // line); rhs += B_u t through per-axis buffers (lines of one axis are
+  // cell-disjoint, different axes are not), summed after the barrier
+  int nla[3] = {0, 0, 0};
+  for (int a = 0; a < G.dim; ++a) nla[a] = n_lines(b, a);
+  double* radd = yw;   // 3 x mp, free until the symv
+  for (int c = threadIdx.x; c < 3 * mp; c += blockDim.x) radd[c] = 0.0;
+  __syncthreads();
+  for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
+    const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
+    const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
+    const int L = b.L[a], m = L - 1, st = axis_stride(b, a);
+    if (m <= 0) continue;
+    double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
+    for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+    line_factor(c, L, cp, piv);
+    for (int j = 0; j < m; ++j) r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j)] : 0.0;
+    if (A.x_gamma) {
+      int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
+      int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
+      if (qlo >= 0) r[0] -= c[0] * xg[qlo];
+      if (qhi >= 0) r[m - 1] -= c[L - 1] * xg[qhi];
     }
-    __syncthreads();
+    line_solve(c, L, cp, piv, r);
+    double* t = tI + off[a] + line * m;
+    const int base = line_base(b, a, line);
+    double* ra = radd + a * mp;
+    for (int j = 0; j < m; ++j) t[j] = r[j];
+    for (int k = 0; k < L; ++k) {
+      double v = 0.0;
+      if (k >= 1) v += r[k - 1];
+      if (k <= m - 1) v -= r[k];
+      ra[base + k * st] = v;
+    }
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < mp; c += blockDim.x) rhs[c] += (radd[c] + radd[mp + c]) + radd[2 * mp + c];
+  __syncthreads();
   // p' = Q rhs, Q tile-packed symmetric (half the bytes of full storage)
   {
     const int nt = mp / 32, ntl = (np + 31) / 32;
@@ -476,10 +486,12 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
     for (int r = ntl * 32 + threadIdx.x; r < mp; r += blockDim.x) pp[r] = 0.0;
     __syncthreads();
   }
-  // u_I = t - A^{-1} B_u^T p'
-  for (int a = 0; a < G.dim; ++a) {
-    const int L = b.L[a], m = L - 1, nl = n_lines(b, a), st = axis_stride(b, a);
-    for (int line = threadIdx.x; line < nl; line += blockDim.x) {
+  // u_I = t - A^{-1} B_u^T p' (lines of all axes at once: disjoint outputs)
+  for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
+    const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
+    const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
+    const int L = b.L[a], m = L - 1, st = axis_stride(b, a);
+    {
       if (m <= 0) continue;
       double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
