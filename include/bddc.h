@@ -128,12 +128,14 @@ int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, c
  * (adaptive.py:56-60).  lam_out holds, per face, the eigenvalues in descending
  * order as far as the selection needs them (all above tau and the next one);
  * the remaining entries are NaN.  flist (nlist face ids, each with at most mmax
- * shared dofs) restricts the launch to a size class; NULL = every face. */
+ * shared dofs) restricts the launch to a size class; NULL = every face.
+ * full != 0 resolves the whole reduced spectrum (eigs-report). */
 size_t bddc_pair_scratch_bytes(int n_faces);
 int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                    const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                    int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
-                   double* qbasis, int* err, const int* flist, int nlist, int mmax, void* stream);
+                   double* qbasis, int* err, const int* flist, int nlist, int mmax, int full,
+                   void* stream);
 
 /* ---------------------------------------------------------------- coarse */
 

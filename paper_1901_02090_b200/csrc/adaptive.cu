@@ -93,7 +93,7 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
                                 double* __restrict__ lam_out, int lam_ld, int* __restrict__ nsel,
                                 int* __restrict__ nadd, double* __restrict__ rows, double* __restrict__ omega,
                                 double* __restrict__ scratch, double* __restrict__ qbasis, int* __restrict__ err,
-                                const int* __restrict__ flist) {
+                                const int* __restrict__ flist, int full) {
   extern __shared__ double sm[];
   __shared__ double red[32];
   __shared__ int bad;
@@ -277,7 +277,7 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   __shared__ int nabove;
   if (threadIdx.x == 0) nabove = (tau < gu) ? m - sturm_below(dg, eo, m, tau, pivmin) : 0;
   __syncthreads();
-  const int ntop = imin(nabove + 1, m);
+  const int ntop = full ? m : imin(nabove + 1, m);
   // multisection: a warp per eigenvalue, 32 Sturm counts per round (interval / 33)
   for (int r = warp; r < ntop; r += nw) {
     const int kk = m - 1 - r;
@@ -459,7 +459,8 @@ extern "C" size_t bddc_pair_scratch_bytes(int n_faces) {
 extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                               const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                               int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
-                              double* qbasis, int* err, const int* flist, int nlist, int mmax, void* stream) {
+                              double* qbasis, int* err, const int* flist, int nlist, int mmax, int full,
+                              void* stream) {
   if (g->maxF > PAIR_MMAX) return bddc_set_error(BDDC_ERR_ARG, "pair face larger than PAIR_MMAX=112 dofs");
   // flist == NULL: every face (shared memory sized for maxF); else the nlist faces
   // listed, all with at most mmax shared dofs (smaller faces -> more CTAs per SM)
@@ -473,7 +474,7 @@ extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* f
     CUDA_OK(cudaFuncSetAttribute(pair_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   pair_eig_kernel<<<nblk, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel, lam_out,
                                                             lam_ld, nsel, nadd, rows, omega, scratch, qbasis, err,
-                                                            flist);
+                                                            flist, full);
   LAUNCH_OK();
   return 0;
 }

@@ -122,7 +122,7 @@ class BddcSetup:
     inverse) and Wq (pressure-rhs -> coarse flux, solve step 1).
     """
 
-    def __init__(self, system, dec, config, timings=None):
+    def __init__(self, system, dec, config, timings=None, pair_spectra=False):
         if not isinstance(dec, Decomposition):
             raise InvalidArgumentError("dec must come from regular_partition()")
         dev = _dev()
@@ -132,6 +132,9 @@ class BddcSetup:
         self.config = config
         self.dev = dev
         self._ktimer = None
+        # resolve every pair eigenvalue and keep PairEigenReports (eigs-report);
+        # the solve path only needs the ones above tau and the next one
+        self.pair_spectra = bool(pair_spectra)
         self.pcg_timer = None   # list -> (start, end) CUDA events of every PCG graph launch
         self.geom = _geom(dec)
         G = self.geom
@@ -244,7 +247,8 @@ class BddcSetup:
                     nat.call("bddc_pair_eigs", gp, _p(self.d_faces), _p(self.d_fslot),
                              _p(self.d_S), _p(Sinv), _p(self.d_delta), float(tau),
                              maxsel, _p(lam), lam_ld, _p(d_nsel), _p(d_nadd), _p(rows),
-                             _p(omega), _p(scratch), _p(qbasis), _p(err), _p(fl), len(fl), mm, st)
+                             _p(omega), _p(scratch), _p(qbasis), _p(err), _p(fl), len(fl), mm,
+                             int(self.pair_spectra), st)
             del scratch
             e = int(err.item())
             if e & 1:
@@ -256,6 +260,9 @@ class BddcSetup:
             self.pair_selected = d_nsel.cpu().numpy()
             self.pair_added = nadd
             self.pair_lambda = lam.view(nf, lam_ld)
+            if self.pair_spectra:
+                self.pair_reports = _pair_reports(dec, self.pair_lambda.cpu().numpy(),
+                                                  self.pair_selected)
             self.face_omega = omega.cpu().numpy()
             self.omega_tilde = float(max(self.face_omega.max(), 1.0)) if nf else 1.0
         elif config.constraints == "adaptive":
@@ -584,6 +591,53 @@ class BddcSetup:
             vals.append(np.where(side == 1, 1.0, -1.0))
         return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                              shape=(dec.n_subdomains, dec.n_gamma)).tocsr()
+
+
+@dataclass
+class PairEigenReport:
+    """Spectrum of one pair pencil (adaptive.py:46-60): eigenvalues descending,
+    clipped at 0, as many as the reference keeps (n_i + n_j minus the rank of
+    the face's initial constraint row); the nonzero part is the reduced m x m
+    pencil's, the rest are the zeros of (I - E)."""
+    i: int
+    j: int
+    eigenvalues: np.ndarray
+    selected: int = 0
+
+    def omega(self, tau):
+        lam = self.eigenvalues
+        below = lam[lam <= tau]
+        return float(max(below[0], 1.0)) if len(below) else 1.0
+
+
+def _pair_reports(dec, lam, selected):
+    ft = dec.face_table
+    out = {}
+    for f in range(dec.n_faces):
+        i, j, m = int(ft[f, 0]), int(ft[f, 1]), int(ft[f, 3])
+        n_keep = int(dec.nG[i] + dec.nG[j]) - 1
+        ev = np.maximum(lam[f, :m], 0.0)
+        ev = np.concatenate([ev, np.zeros(max(n_keep - m, 0))])
+        out[(min(i, j), max(i, j))] = PairEigenReport(min(i, j), max(i, j), ev, int(selected[f]))
+    return out
+
+
+def eigs_report(system, dec, config):
+    """Per-pair spectra against the initial constraints (cli.py:147-162): dict
+    (i, j) -> PairEigenReport, computed on the GPU."""
+    cfg = SolveConfig(tau=config.tau, scaling=config.scaling, tol=config.tol,
+                      maxit=config.maxit, constraints="adaptive")
+    return BddcSetup(system, dec, cfg, pair_spectra=True).pair_reports
+
+
+def write_eigs_csv(path, reports):
+    """i,j,rank,lambda with rank 1 = largest (io.py:256-262)."""
+    lines = ["i,j,rank,lambda"]
+    for (i, j) in sorted(reports):
+        for rank, lam in enumerate(reports[(i, j)].eigenvalues, 1):
+            lines.append(f"{i},{j},{rank},{float(lam)!r}")
+    with open(path, "w") as f:
+        f.write("\n".join(lines) + "\n")
 
 
 def _face_cells(dec):

@@ -82,3 +82,23 @@ def test_operator_parity(name):
     assert rel(st.schur_matvec(d["x"]), d["Sx"]) <= 1e-10
     assert rel(st.project_balanced(d["x"]), d["Px"]) <= 1e-13
     assert rel(st.precondition(d["x"]), d["Mx"]) <= 1e-9
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if "pair_selected" in load(n)])
+def test_eigs_report_full_spectra(name):
+    """eigs-report (cli.py:147-162): every pair's spectrum against
+    the initial constraints, compared with the reference's leading 24 eigenvalues
+    (zeros included) to 1e-8 of the pair's largest eigenvalue."""
+    d = load(name)
+    B, system, dec, cfg = _setup(d)
+    reports = B.eigs_report(system, dec, cfg)
+    pairs = [tuple(p) for p in d["pairs"]]
+    assert sorted(reports) == sorted(pairs)
+    for q, key in enumerate(pairs):
+        ref = d["pair_lam"][q]
+        ref = ref[np.isfinite(ref)]
+        mine = reports[key].eigenvalues[:len(ref)]
+        assert len(mine) == len(ref)
+        scale = max(float(ref.max()), 1.0)
+        np.testing.assert_allclose(mine, ref, rtol=0, atol=1e-8 * scale)
+        assert reports[key].selected == int(d["pair_selected"][q])
