@@ -630,6 +630,42 @@ def eigs_report(system, dec, config):
     return BddcSetup(system, dec, cfg, pair_spectra=True).pair_reports
 
 
+def preconditioned_spectrum(setup, max_n=8192):
+    """Eigenvalues of the preconditioned interface operator on the balanced
+    subspace (oracle.py:114-141), ascending: S and M materialised column by
+    column with the GPU applies, restricted to null(Phi), and the similar
+    symmetric form Mb^1/2 Sb Mb^1/2 solved on the device (diagnostic, small
+    cases: n_Gamma <= max_n)."""
+    n = setup.n_gamma
+    if n > max_n:
+        raise InvalidArgumentError(f"preconditioned_spectrum: n_Gamma = {n} > {max_n}")
+    dev = setup.dev
+    S = torch.empty(n, n, dtype=F64, device=dev)
+    M = torch.empty(n, n, dtype=F64, device=dev)
+    e = torch.zeros(n, dtype=F64, device=dev)
+    with torch.cuda.stream(setup.stream):
+        for c in range(n):
+            e.zero_()
+            e[c] = 1.0
+            setup._schur(e, S[c])
+            setup._precond(e, M[c])
+    torch.cuda.current_stream().wait_stream(setup.stream)
+    S, M = S.T, M.T   # columns are the applies
+    Phi = torch.as_tensor(setup.net_flux_matrix().toarray(), dtype=F64, device=dev)
+    Q, R = torch.linalg.qr(Phi.T, mode="complete")
+    d = torch.abs(torch.diagonal(R))
+    rank = int((d > 1e-12 * torch.clamp(d.max(), min=1e-300)).sum())
+    Z = Q[:, rank:]
+    Sb = Z.T @ S @ Z
+    Mb = Z.T @ M @ Z
+    Sb = 0.5 * (Sb + Sb.T)
+    Mb = 0.5 * (Mb + Mb.T)
+    w, V = torch.linalg.eigh(Mb)
+    W = (V * torch.sqrt(torch.clamp(w, min=0.0))) @ V.T
+    lam = torch.linalg.eigvalsh(W @ Sb @ W)
+    return torch.sort(lam).values.cpu().numpy()
+
+
 def write_eigs_csv(path, reports):
     """i,j,rank,lambda with rank 1 = largest (io.py:256-262)."""
     lines = ["i,j,rank,lambda"]

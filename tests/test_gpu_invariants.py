@@ -89,6 +89,12 @@ def test_spectrum_floor():
     lam = sla.eigh(W @ Sb @ W, eigvals_only=True)
     assert lam[0] >= 1.0 - 1e-8
     assert lam[-1] <= 2.0 * st.omega_tilde * dec.max_faces_per_subdomain ** 2
+    # the on-device diagnostic gives the same spectrum
+    lam_gpu = B.preconditioned_spectrum(st)
+    np.testing.assert_allclose(lam_gpu, np.sort(lam), rtol=1e-9, atol=1e-9)
+    # and the PCG's Lanczos kappa lies inside it
+    rep = B.solve(system, dec, cfg, setup=st)
+    assert rep.kappa <= lam_gpu[-1] / lam_gpu[0] * (1 + 1e-6)
 
 
 def test_bitwise_determinism():
