@@ -184,12 +184,16 @@ class BoxPartition:
 
     def __post_init__(self):
         mesh = self.mesh
-        self.splits = tuple(int(s) for s in self.splits)
+        # per axis: a strip count (near-equal strips) or explicit strip widths
+        widths = [list(map(int, s)) if not np.isscalar(s) and np.ndim(s) > 0 else None
+                  for s in self.splits]
+        self.splits = tuple(len(w) if w is not None else int(s)
+                            for w, s in zip(widths, self.splits))
         strip = []
         self.strip_lo = []
         self.strip_n = []
         for a in range(mesh.dim):
-            w = near_equal(mesh.counts[a], self.splits[a])
+            w = widths[a] if widths[a] is not None else near_equal(mesh.counts[a], self.splits[a])
             bounds = np.cumsum(w)
             strip.append(np.searchsorted(bounds, np.arange(mesh.counts[a]),
                                          side="right"))

@@ -63,6 +63,8 @@ CASES = {
                 1e-10, lambda: _random_k((8, 6, 4), 9)),
     "g3d_c3block": ((30, 30, 15), (20.0, 10.0, 2.0), (3, 3, 3), "multiplicity", 10.0,
                     1e-8, lambda: _c3_block(28)),
+    "g3d_uneven": ((12, 10, 8), (1.0, 2.0, 0.5), ((3, 5, 4), (2, 4, 4), (5, 3)), "multiplicity",
+                   5.0, 1e-10, lambda: _random_k((12, 10, 8), 11)),
     "c0": (fields.CONFIGS[0]["counts"], fields.CONFIGS[0]["sizes"],
            fields.CONFIGS[0]["splits"], "stiffness", math.inf, 1e-8,
            lambda: fields.config_field(0)),
@@ -88,7 +90,18 @@ def make(name):
     g = R_grid.build_grid(dim, counts, sizes)
     perm = R_grid.Permeability(k)
     system = R_grid.assemble_system(g, perm, R_grid.Wells(0, g.n_cells - 1))
-    dec = R_dec.regular_partition(g, splits)
+    if any(np.ndim(sp) > 0 for sp in splits):
+        # uneven strips: the reference's Decomposition(grid, part) with a box part
+        part = np.zeros(g.n_cells, dtype=np.int64)
+        stride = 1
+        for a in range(dim):
+            bounds = np.cumsum(splits[a])
+            strip = np.searchsorted(bounds, np.arange(counts[a]), side="right")
+            part += stride * strip[g.cell_coords[:, a]]
+            stride *= len(splits[a])
+        dec = R_dec.Decomposition(g, part)
+    else:
+        dec = R_dec.regular_partition(g, splits)
     mode = "adaptive" if math.isfinite(tau) else "initial"
     cfg = R_solver.SolveConfig(tau=tau, scaling=scaling, constraints=mode,
                                tol=tol)
@@ -102,7 +115,8 @@ def make(name):
     x = rng.standard_normal(len(dec.gamma))
     out = dict(
         counts=np.array(counts), sizes=np.array(sizes, dtype=np.float64),
-        splits=np.array(splits), scaling=scaling, tau=tau, tol=tol, k=k,
+        splits=np.array([len(sp) if np.ndim(sp) > 0 else sp for sp in splits]),
+        scaling=scaling, tau=tau, tol=tol, k=k,
         u=rep.u, p=rep.p, it=rep.it, kappa=rep.kappa,
         omega_tilde=rep.omega_tilde, n_c=rep.n_c, residuals=rep.residuals,
         u0=rep.u0, u_star=rep.u_star,
@@ -130,6 +144,9 @@ def make(name):
             sel[q] = setup.pair_reports[key].selected
         out["pair_lam"] = lam
         out["pair_selected"] = sel
+    if any(np.ndim(sp) > 0 for sp in splits):
+        wmax = max(len(sp) for sp in splits)
+        out["widths"] = np.array([list(sp) + [-1] * (wmax - len(sp)) for sp in splits])
     path = os.path.join(REPO, "tests", "golden", f"{name}.npz")
     np.savez_compressed(path, **out)
     print(f"{name}: it={rep.it} kappa={rep.kappa:.6g} n_c={rep.n_c} "

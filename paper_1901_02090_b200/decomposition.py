@@ -26,7 +26,7 @@ from functools import cached_property
 
 import numpy as np
 
-from .errors import InvalidArgumentError
+from .errors import ConfigurationError, InvalidArgumentError
 
 MAX_STRIPS = 64
 
@@ -51,8 +51,56 @@ class FaceComponent:
     sign_i: np.ndarray
 
 
+def _box_widths(grid, part):
+    """Strip widths of a tensor-product box partition given as a cell -> subdomain
+    map numbered x-fastest over the strips (what `regular_partition` and
+    `box_partition` produce); ConfigurationError for anything else."""
+    part = np.asarray(part, dtype=np.int64)
+    if part.shape != (grid.n_cells,):
+        raise InvalidArgumentError("partition length must equal n_cells")
+    coords = grid.cell_coords
+    widths, strip, stride = [], [], 1
+    for a in range(grid.dim):
+        # strip index along axis a read off the first line of cells along a
+        line = np.all(coords[:, [b for b in range(grid.dim) if b != a]] == 0, axis=1)
+        ids = part[line][np.argsort(coords[line, a])]
+        s_a = (ids // stride)
+        steps = np.diff(s_a)
+        if np.any((steps != 0) & (steps != 1)) or s_a[0] != 0:
+            raise ConfigurationError("only tensor-product box partitions numbered "
+                                     "x-fastest over the strips are supported")
+        w = np.bincount(s_a).astype(np.int64)
+        widths.append([int(v) for v in w])
+        strip.append(s_a)
+        stride *= len(w)
+    rebuilt = np.zeros(grid.n_cells, dtype=np.int64)
+    stride = 1
+    for a in range(grid.dim):
+        rebuilt += stride * strip[a][coords[:, a]]
+        stride *= len(widths[a])
+    if not np.array_equal(rebuilt, part):
+        raise ConfigurationError("only tensor-product box partitions numbered "
+                                 "x-fastest over the strips are supported")
+    return widths
+
+
 class Decomposition:
+    """Box partition: `splits` per axis is a strip count (near-equal strips,
+    decomposition.py:128-130) or a list of strip widths; `Decomposition(grid,
+    part)` with a cell -> subdomain array (the reference's constructor,
+    decomposition.py:33) is accepted when `part` is such a box partition."""
+
     def __init__(self, grid, splits):
+        if len(splits) == grid.n_cells and grid.n_cells != grid.dim:
+            splits = _box_widths(grid, np.asarray(splits))
+        widths = None
+        if any(not np.isscalar(s) and np.ndim(s) > 0 for s in splits):
+            widths = [[int(v) for v in np.atleast_1d(s)] for s in splits]
+            if len(widths) != grid.dim or any(len(w) < 1 or min(w) < 1 for w in widths):
+                raise InvalidArgumentError("need positive strip widths per axis")
+            if any(sum(w) != c for w, c in zip(widths, grid.counts)):
+                raise InvalidArgumentError("strip widths must sum to the cell counts")
+            splits = tuple(len(w) for w in widths)
         splits = tuple(int(s) for s in splits)
         if len(splits) != grid.dim or any(s < 1 for s in splits):
             raise InvalidArgumentError("need one split >= 1 per axis")
@@ -66,7 +114,8 @@ class Decomposition:
         n3 = tuple(grid.counts) + (1,) * (3 - dim)
         S3 = splits + (1,) * (3 - dim)
         self.n3, self.S3 = n3, S3
-        self.sw = [np.array(near_equal_splits(n3[a], S3[a]), dtype=np.int64)
+        self.sw = [np.array(widths[a] if (widths is not None and a < dim)
+                            else near_equal_splits(n3[a], S3[a]), dtype=np.int64)
                    for a in range(3)]
         self.so = [np.concatenate([[0], np.cumsum(w)[:-1]]) for w in self.sw]
         strip_of = [np.repeat(np.arange(S3[a]), self.sw[a]) for a in range(3)]
@@ -294,3 +343,32 @@ class Decomposition:
 def regular_partition(grid, splits):
     """Tensor-product partition with near-equal strips (decomposition.py:133-151)."""
     return Decomposition(grid, splits)
+
+
+def box_partition(grid, widths):
+    """Tensor-product partition with the given strip widths per axis."""
+    return Decomposition(grid, [list(w) for w in widths])
+
+
+def import_partition(path, grid):
+    """Read a PART file (decomposition.py:154-177): header 'PART <N> <ncells>', then
+    one 0-based subdomain id per cell, x-fastest.  Box partitions only (the ids
+    are compacted like the reference's, then checked for tensor-product form)."""
+    import warnings
+
+    from .errors import FormatError
+    with open(path) as fh:
+        header = fh.readline().split()
+        if len(header) < 3 or header[0] != "PART":
+            raise FormatError("expected header 'PART <N> <ncells>'")
+        n_declared, ncells = int(header[1]), int(header[2])
+        ids = np.array([int(line) for line in fh if line.strip()])
+    if len(ids) != ncells or ncells != grid.n_cells:
+        raise FormatError(
+            f"expected {grid.n_cells} ids, file declares {ncells}, found {len(ids)}")
+    if ids.min() < 0:
+        raise FormatError("subdomain ids must be non-negative")
+    uniq, compact = np.unique(ids, return_inverse=True)
+    if len(uniq) != n_declared:
+        warnings.warn(f"header declares {n_declared} subdomains, file uses {len(uniq)}")
+    return Decomposition(grid, compact)

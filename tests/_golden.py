@@ -17,6 +17,8 @@ def load(name):
     d["counts"] = tuple(int(c) for c in d["counts"])
     d["sizes"] = tuple(float(s) for s in d["sizes"])
     d["splits"] = tuple(int(s) for s in d["splits"])
+    if "widths" in d:   # uneven box strips: per-axis width lists
+        d["splits"] = tuple(tuple(int(v) for v in w if v > 0) for w in d["widths"])
     d["scaling"] = str(d["scaling"])
     d["tau"] = float(d["tau"])
     d["tol"] = float(d["tol"])

@@ -50,3 +50,24 @@ def test_validation():
         B.regular_partition(g, (5, 1))
     with pytest.raises(B.InvalidArgumentError):
         B.regular_partition(g, (2,))
+
+
+def test_box_partition_uneven_strips_and_part_roundtrip(tmp_path):
+    """Tensor-product box partitions with uneven strips (box
+    case): widths, the reference constructor Decomposition(grid, part) and PART
+    import all give the same topology; non-box maps are rejected."""
+    import paper_1901_02090_b200 as B
+    from paper_1901_02090_b200.errors import ConfigurationError
+    g = B.build_grid(3, (12, 10, 8), (1.0, 1.0, 1.0))
+    d1 = B.box_partition(g, [[3, 5, 4], [2, 4, 4], [5, 3]])
+    assert d1.splits == (3, 3, 2)
+    assert [list(map(int, w)) for w in d1.sw] == [[3, 5, 4], [2, 4, 4], [5, 3]]
+    d2 = B.Decomposition(g, d1.part)
+    np.testing.assert_array_equal(d1.gpos, d2.gpos)
+    np.testing.assert_array_equal(d1.gamma, d2.gamma)
+    path = tmp_path / "p.part"
+    path.write_text(f"PART {d1.n_subdomains} {g.n_cells}\n" + "\n".join(map(str, d1.part)) + "\n")
+    d3 = B.import_partition(str(path), g)
+    np.testing.assert_array_equal(d1.gcode, d3.gcode)
+    with pytest.raises(ConfigurationError):
+        B.Decomposition(g, np.random.default_rng(0).integers(0, 4, g.n_cells))
