@@ -208,6 +208,9 @@ int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, 
              double* phi, void* stream);
 int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
                    double* z, void* stream);
+/* Same, multi-CTA: six mode-product launches (PDL), ws = 2 N doubles. */
+int bddc_lap_solve_mc(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
+                      double* z, double* ws, void* stream);
 int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const double* z, double* y,
                     void* stream);
 /* PCG pieces (solver.py:186-233): fused deterministic dots with scalar ops,

@@ -128,6 +128,7 @@ _SIGS = {
     "bddc_scatter": [_I, _P, _P, _P, _P],
     "bddc_phi": [_I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_lap_solve": [_I, _I, _I, _P, _P, _P, _P, _P],
+    "bddc_lap_solve_mc": [_I, _I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_proj_apply": [_I, _I, _P, _P, _P, _P],
     "bddc_dot_workspace": [],
     "bddc_dot": [_P, _P, _L, _P, _P, _I, _P, _P],

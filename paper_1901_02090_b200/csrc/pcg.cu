@@ -637,6 +637,59 @@ extern "C" int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const i
   return 0;
 }
 
+// One mode product of the separable solve, thread per grid node (multi-CTA):
+// out[e] = dmo[e] * (sum_k Q_a[.] * dmi[g] * in[g]) (/ Lambda if lamdiv); forward
+// uses Q_a^T (Q[k][c]), backward Q_a (Q[c][k]).
+__global__ void lap_mode_kernel(int S0, int S1, int S2, int a, int backward, const double* __restrict__ eig,
+                                const double* __restrict__ dmi, const double* __restrict__ dmo, int lamdiv,
+                                const double* __restrict__ in, double* __restrict__ out) {
+  pdl_trigger();
+  const int N = S0 * S1 * S2;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Sd[3] = {S0, S1, S2};
+  const int st[3] = {1, S0, S0 * S1};
+  const double* Q = eig + (a == 0 ? 0 : (a == 1 ? S0 * S0 : S0 * S0 + S1 * S1));
+  const double* lam = eig + S0 * S0 + S1 * S1 + S2 * S2;
+  pdl_wait();
+  if (e >= N) return;
+  const int S = Sd[a], ca = (e / st[a]) % S, base = e - ca * st[a];
+  double acc = 0.0;
+  for (int k = 0; k < S; ++k) {
+    const int g = base + k * st[a];
+    const double v = dmi ? dmi[g] * in[g] : in[g];
+    acc += (backward ? Q[ca * S + k] : Q[k * S + ca]) * v;
+  }
+  if (lamdiv) {
+    const int a0 = e % S0, a1 = (e / S0) % S1, a2 = e / (S0 * S1);
+    const double l = lam[a0] + lam[S0 + a1] + lam[S0 + S1 + a2];
+    acc = (e == 0) ? 0.0 : acc / l;
+  }
+  out[e] = dmo ? dmo[e] * acc : acc;
+}
+
+extern "C" int bddc_lap_solve_mc(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
+                                 double* z, double* ws, void* stream) {
+  const int N = S0 * S1 * S2;
+  if (N <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* u = ws;
+  double* w = ws + N;
+  const dim3 g((N + 127) / 128), b(128);
+  // forward Q_x^T, Q_y^T, Q_z^T (D^-1/2 on the way in, Lambda^+ on the way out)
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 0, 0, eig, dm, (const double*)nullptr, 0, phi, u);
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 1, 0, eig, (const double*)nullptr, (const double*)nullptr, 0,
+             (const double*)u, w);
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 2, 0, eig, (const double*)nullptr, (const double*)nullptr, 1,
+             (const double*)w, u);
+  // backward Q_z, Q_y, Q_x (D^-1/2 on the way out)
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 2, 1, eig, (const double*)nullptr, (const double*)nullptr, 0,
+             (const double*)u, w);
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 1, 1, eig, (const double*)nullptr, (const double*)nullptr, 0,
+             (const double*)w, u);
+  PDL_LAUNCH(lap_mode_kernel, g, b, 0, s, S0, S1, S2, 0, 1, eig, (const double*)nullptr, dm, 0, (const double*)u, z);
+  return 0;
+}
+
 extern "C" int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi, double* z,
                               void* stream) {
   int N = S0 * S1 * S2;

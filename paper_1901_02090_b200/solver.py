@@ -164,6 +164,7 @@ class BddcSetup:
         # (N^2 doubles: used up to N = 4096, i.e. 134 MB per GEMV)
         S3 = dec.S3
         self.d_Lp = None
+        self._lap_ws = torch.empty(2 * N, dtype=F64, device=dev)   # multi-CTA separable solve
         if N <= 4096:
             ws = torch.empty(2 * N * N, dtype=F64, device=dev)
             self.d_Lp = torch.empty(N * N, dtype=F64, device=dev)
@@ -489,8 +490,8 @@ class BddcSetup:
                      st)
         else:
             S3 = self.dec.S3
-            nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(self.d_eig_w),
-                     _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), st)
+            nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_w),
+                     _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), _p(self._lap_ws), st)
         nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
                  _p(self.w_z), _p(y), st)
 

@@ -5,8 +5,9 @@ import torch
 import paper_1901_02090_b200 as B
 from paper_1901_02090_b200 import fields, _native as nat
 from paper_1901_02090_b200.solver import _p, _stream
-c = fields.CONFIGS[3]
-k = fields.config_field(3)
+CFG = int(os.environ.get("CFG", "3"))
+c = fields.CONFIGS[CFG]
+k = fields.config_field(CFG)
 g = B.build_grid(c["dim"], c["counts"], c["sizes"])
 dec = B.regular_partition(g, c["splits"])
 system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))

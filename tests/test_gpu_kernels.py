@@ -155,3 +155,38 @@ def test_lanczos_kappa_matches_host():
     k = S._lanczos(_S, torch.tensor(al + [0.0], device="cuda", dtype=torch.float64),
                    torch.tensor(be + [0.0], device="cuda", dtype=torch.float64), m)
     assert abs(k - ev[-1] / ev[0]) <= 1e-10 * k
+
+
+@pytest.mark.parametrize("S3", [(6, 22, 17), (12, 44, 17), (5, 7, 1)])
+def test_lap_solvers_agree(S3):
+    """The single-CTA separable Laplacian solve, its multi-CTA variant and the
+    dense (Phi Phi^T)^+ GEMV give the same projection solve."""
+    import torch
+    nat = _lib()
+    import paper_1901_02090_b200 as B
+    g = B.build_grid(3 if S3[2] > 1 else 2, tuple(2 * s for s in S3[:3 if S3[2] > 1 else 2]),
+                     (1.0,) * (3 if S3[2] > 1 else 2))
+    dec = B.regular_partition(g, S3[:3 if S3[2] > 1 else 2])
+    eig, dm = dec.laplacian_eigs(True)
+    dev = "cuda"
+    eig = torch.as_tensor(eig, device=dev)
+    dm = torch.as_tensor(dm, device=dev)
+    N = int(np.prod(S3))
+    phi = torch.randn(N, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    z1 = torch.empty_like(phi)
+    z2 = torch.empty_like(phi)
+    ws = torch.empty(2 * N, dtype=torch.float64, device=dev)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], nat.ptr(eig), nat.ptr(dm), nat.ptr(phi), nat.ptr(z1), st)
+    nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], nat.ptr(eig), nat.ptr(dm), nat.ptr(phi), nat.ptr(z2),
+             nat.ptr(ws), st)
+    torch.cuda.synchronize()
+    assert torch.allclose(z1, z2, rtol=1e-12, atol=1e-12 * float(z1.abs().max()))
+    if N <= 4096:
+        Lp = torch.empty(N * N, dtype=torch.float64, device=dev)
+        w2 = torch.empty(2 * N * N, dtype=torch.float64, device=dev)
+        z3 = torch.empty_like(phi)
+        nat.call("bddc_lap_dense", S3[0], S3[1], S3[2], nat.ptr(eig), nat.ptr(dm), nat.ptr(w2), nat.ptr(Lp), st)
+        nat.call("bddc_gemv", N, N, N, nat.ptr(Lp), nat.ptr(phi), nat.ptr(z3), st)
+        torch.cuda.synchronize()
+        assert torch.allclose(z1, z3, rtol=1e-11, atol=1e-11 * float(z1.abs().max()))
