@@ -131,6 +131,13 @@ int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, c
  * shared dofs) restricts the launch to a size class; NULL = every face.
  * full != 0 resolves the whole reduced spectrum (eigs-report). */
 size_t bddc_pair_scratch_bytes(int n_faces);
+/* MsMFEM baseline rows (adaptive.py:207-262) in Schur form, one per face:
+ * rg = interface residuals (N x maxG) of the interior solutions for each
+ * subdomain's unit source distribution; writes rows/qbasis like
+ * bddc_pair_eigs (maxsel >= 1) and nadd (0/1) per face. */
+int bddc_multiscale_rows(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
+                         const double* rg, int maxsel, double* rows, double* qbasis, int* nadd, int* err,
+                         void* stream);
 int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                    const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                    int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,

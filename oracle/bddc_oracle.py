@@ -577,6 +577,41 @@ class Coarse:
 
 # ------------------------------------------------------------------- setup
 
+def multiscale_row(setup, f):
+    """MsMFEM face row (adaptive.py:207-262): pair-local Darcy solve on the two
+    subdomains' cells with a unit source transfer (-1 spread over i, +1 over j,
+    uniformly or following the wells), no-flow on the pair's boundary, one
+    pressure pinned; the flux trace on the shared face, outward from i."""
+    P, mesh = setup.P, setup.mesh
+    i, j = P.pairs[f]
+    cells = np.concatenate([P.cells[i], P.cells[j]])
+    cell_pos = {c: n for n, c in enumerate(cells)}
+    dc = P._dof_cells
+    inside = np.isin(dc[:, 0], cells) & np.isin(dc[:, 1], cells)
+    dofs = np.flatnonzero(inside)
+    dof_pos = {d: n for n, d in enumerate(dofs)}
+    A = mass_matrix(mesh, setup.k, cells)[dofs][:, dofs].tocsr()
+    Bm = setup.B[cells][:, dofs].tocsr()
+    f_loc = np.zeros(len(cells))
+    for sub, sign in ((i, -1.0), (j, 1.0)):
+        sc = P.cells[sub]
+        well = setup.f[sc]
+        dist = well / well.sum() if abs(well.sum()) > 1e-14 else np.full(len(sc), 1.0 / len(sc))
+        for c, v in zip(sc, dist):
+            f_loc[cell_pos[c]] = sign * v
+    d = A.diagonal().mean()
+    K = sp.bmat([[A, d * Bm.T], [d * Bm, None]], format="csc")
+    n_u = len(dofs)
+    keep = np.ones(K.shape[0], dtype=bool)
+    keep[n_u] = False
+    rhs = np.concatenate([np.zeros(n_u), d * f_loc])
+    sol = np.zeros(K.shape[0])
+    sol[keep] = spla.spsolve(K[keep][:, keep].tocsc(), rhs[keep])
+    u = sol[:n_u]
+    fd = P.face_dofs[f]
+    return P.sign(i, fd) * u[[dof_pos[x] for x in fd]]
+
+
 @dataclass
 class Config:
     tau: float = math.inf
@@ -614,6 +649,10 @@ class Setup:
             self.omega_tilde = (max(r.omega(cfg.tau)
                                     for r in self.pairs.values())
                                 if self.pairs else 1.0)
+        if cfg.constraints == "multiscale":
+            # solver.py:89-90, adaptive.py:265-269
+            for f_ in range(len(self.P.pairs)):
+                self.cons.add(f_, multiscale_row(self, f_))
         self.coarse = Coarse(self)
 
     @property

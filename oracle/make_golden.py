@@ -65,6 +65,10 @@ CASES = {
                     1e-8, lambda: _c3_block(28)),
     "g3d_uneven": ((12, 10, 8), (1.0, 2.0, 0.5), ((3, 5, 4), (2, 4, 4), (5, 3)), "multiplicity",
                    5.0, 1e-10, lambda: _random_k((12, 10, 8), 11)),
+    "g2d_ms": ((12, 12), (1.0, 1.0), (3, 3), "multiplicity", math.inf, 1e-10,
+               lambda: _random_k((12, 12), 21)),
+    "g3d_ms": ((8, 6, 6), (20.0, 10.0, 2.0), (2, 3, 2), "stiffness", math.inf, 1e-10,
+               lambda: _random_k((8, 6, 6), 22)),
     "c0": (fields.CONFIGS[0]["counts"], fields.CONFIGS[0]["sizes"],
            fields.CONFIGS[0]["splits"], "stiffness", math.inf, 1e-8,
            lambda: fields.config_field(0)),
@@ -103,6 +107,8 @@ def make(name):
     else:
         dec = R_dec.regular_partition(g, splits)
     mode = "adaptive" if math.isfinite(tau) else "initial"
+    if name.endswith("_ms"):
+        mode = "multiscale"   # MsMFEM baseline (adaptive.py:207-269)
     cfg = R_solver.SolveConfig(tau=tau, scaling=scaling, constraints=mode,
                                tol=tol)
     t0 = time.time()
@@ -114,6 +120,7 @@ def make(name):
     rng = np.random.default_rng(1234)
     x = rng.standard_normal(len(dec.gamma))
     out = dict(
+        constraints=mode,
         counts=np.array(counts), sizes=np.array(sizes, dtype=np.float64),
         splits=np.array([len(sp) if np.ndim(sp) > 0 else sp for sp in splits]),
         scaling=scaling, tau=tau, tol=tol, k=k,

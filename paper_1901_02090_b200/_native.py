@@ -95,6 +95,7 @@ _SIGS = {
     "bddc_local_solve": [_GP, _P, _P, _P, _P, _P, _P,
                          C.POINTER(LocalSolveArgs), _P],
     "bddc_pair_scratch_bytes": [_I],
+    "bddc_multiscale_rows": [_GP, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P],
     "bddc_pair_eigs": [_GP, _P, _P, _P, _P, _P, _D, _I, _P, _I, _P, _P, _P,
                        _P, _P, _P, _P, _P, _I, _I, _I, _P],
     "bddc_coarse_local": [_GP, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P,

@@ -456,6 +456,156 @@ extern "C" size_t bddc_pair_scratch_bytes(int n_faces) {
   return (size_t)n_faces * PAIR_MMAX * PAIR_MMAX * sizeof(double);
 }
 
+// MsMFEM baseline rows (adaptive.py:207-262), one CTA per face (i low, j high),
+// in Schur form: the pair-local Darcy problem with a unit source transfer
+// (-1 spread over i, +1 over j) and no flow on the pair's other boundaries
+// reduces to its shared-face fluxes x:
+//   min 1/2 x^T M x - b^T x  s.t.  1^T x = 1   (net outflow of i = its sink)
+//   M = S_i[sh,sh] + S_j[sh,sh],  b = rg_i[sh] - rg_j[sh]
+// where rg_k is the interface residual of subdomain k's interior solution for
+// its unit source distribution (local_solve condense output); the Lagrange
+// multiplier is the pair's pressure-constant jump.  The row (outward from i)
+// passes the reference's dependence test against the initial row
+// (coarse.py:61-100) and is stored raw, with the orthonormal face basis.
+__global__ void multiscale_kernel(bddc_geom G, const int* __restrict__ faces, const int* __restrict__ fslot,
+                                  const double* __restrict__ S, const double* __restrict__ rg, int maxsel,
+                                  double* __restrict__ rows, double* __restrict__ qbasis, int* __restrict__ nadd,
+                                  int* __restrict__ err) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ int bad;
+  const int f = blockIdx.x;
+  const int i = faces[4 * f], j = faces[4 * f + 1], a = faces[4 * f + 2], m = faces[4 * f + 3];
+  const int ld = m + ((m & 1) ? 0 : 1);
+  const int mg = G.maxG;
+  double* M = sm;            // m x ld, Cholesky in place (lower)
+  double* y1 = M + m * ld;   // m: M^-1 b
+  double* y2 = y1 + m;       // m: M^-1 1
+  double* x = y2 + m;        // m
+  int* qi = (int*)(x + m);
+  int* qj = qi + m;
+  if (threadIdx.x == 0) bad = 0;
+  for (int s = threadIdx.x; s < m; s += blockDim.x) {
+    qi[s] = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + s];
+    qj[s] = fslot[((size_t)j * 6 + a * 2 + 0) * G.maxF + s];
+  }
+  __syncthreads();
+  const double* Si = S + (size_t)i * mg * mg;
+  const double* Sj = S + (size_t)j * mg * mg;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int r = e / m, c = e % m;
+    M[r * ld + c] = Si[(size_t)qi[r] * mg + qi[c]] + Sj[(size_t)qj[r] * mg + qj[c]];
+  }
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    y1[r] = rg[(size_t)i * mg + qi[r]] - rg[(size_t)j * mg + qj[r]];
+    y2[r] = 1.0;
+  }
+  __syncthreads();
+  // Cholesky M = L L^T (lower, in place)
+  for (int k = 0; k < m; ++k) {
+    if (threadIdx.x == 0) {
+      double d = M[k * ld + k];
+      if (!(d > 0.0)) {
+        bad = 1;
+        d = 1.0;
+      }
+      M[k * ld + k] = sqrt(d);
+    }
+    __syncthreads();
+    const double dk = M[k * ld + k];
+    for (int r = k + 1 + threadIdx.x; r < m; r += blockDim.x) M[r * ld + k] /= dk;
+    __syncthreads();
+    const int w = m - k - 1;
+    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
+      const int r = k + 1 + e / w, c = k + 1 + e % w;
+      if (c <= r) M[r * ld + c] -= M[r * ld + k] * M[c * ld + k];
+    }
+    __syncthreads();
+  }
+  // two right-hand sides: forward L z = [b, 1], then back L^T y = z
+  for (int k = 0; k < m; ++k) {
+    if (threadIdx.x == 0) {
+      y1[k] /= M[k * ld + k];
+      y2[k] /= M[k * ld + k];
+    }
+    __syncthreads();
+    for (int r = k + 1 + threadIdx.x; r < m; r += blockDim.x) {
+      y1[r] -= M[r * ld + k] * y1[k];
+      y2[r] -= M[r * ld + k] * y2[k];
+    }
+    __syncthreads();
+  }
+  for (int k = m - 1; k >= 0; --k) {
+    if (threadIdx.x == 0) {
+      y1[k] /= M[k * ld + k];
+      y2[k] /= M[k * ld + k];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+      y1[r] -= M[k * ld + r] * y1[k];
+      y2[r] -= M[k * ld + r] * y2[k];
+    }
+    __syncthreads();
+  }
+  double s1 = 0.0, s2 = 0.0;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    s1 += y1[r];
+    s2 += y2[r];
+  }
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  const double mu = (1.0 - s1) / s2;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) x[r] = y1[r] + mu * y2[r];
+  __syncthreads();
+  // dependence test against the initial row's basis q0 = 1/sqrt(m), two GS passes
+  const double q0 = rsqrt((double)m);
+  double nx = 0.0, d1 = 0.0;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    nx += x[r] * x[r];
+    d1 += x[r] * q0;
+  }
+  nx = sqrt(block_sum(nx, red));
+  d1 = block_sum(d1, red);
+  double d2 = 0.0;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) d2 += (x[r] - d1 * q0) * q0;
+  d2 = block_sum(d2, red);
+  double nr = 0.0;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const double v = x[r] - (d1 + d2) * q0;
+    nr += v * v;
+  }
+  nr = sqrt(block_sum(nr, red));
+  const bool keep = nr > 1e-10 * fmax(nx, 1.0);
+  for (int r = threadIdx.x; r < PAIR_MMAX; r += blockDim.x) {
+    qbasis[((size_t)f * (maxsel + 1)) * PAIR_MMAX + r] = (r < m) ? q0 : 0.0;
+    if (keep) {
+      rows[((size_t)f * maxsel) * PAIR_MMAX + r] = (r < m) ? x[r] : 0.0;
+      qbasis[((size_t)f * (maxsel + 1) + 1) * PAIR_MMAX + r] = (r < m) ? (x[r] - (d1 + d2) * q0) / nr : 0.0;
+    }
+  }
+  if (threadIdx.x == 0) {
+    nadd[f] = keep ? 1 : 0;
+    if (bad) atomicOr(err, 1);
+  }
+}
+
+extern "C" int bddc_multiscale_rows(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
+                                    const double* rg, int maxsel, double* rows, double* qbasis, int* nadd, int* err,
+                                    void* stream) {
+  if (g->n_faces <= 0) return 0;
+  if (g->maxF > PAIR_MMAX) return bddc_set_error(BDDC_ERR_ARG, "pair face larger than PAIR_MMAX=112 dofs");
+  if (maxsel < 1) return bddc_set_error(BDDC_ERR_ARG, "multiscale: maxsel must be >= 1");
+  const int m = g->maxF;
+  const int ld = m + ((m & 1) ? 0 : 1);
+  size_t shm = (size_t)(m * ld + 3 * m) * sizeof(double) + 2 * m * sizeof(int) + 16;
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(multiscale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  multiscale_kernel<<<g->n_faces, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, rg, maxsel, rows, qbasis,
+                                                                    nadd, err);
+  LAUNCH_OK();
+  return 0;
+}
+
 extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                               const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                               int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,

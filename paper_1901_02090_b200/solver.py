@@ -39,7 +39,7 @@ class SolveConfig:
     scaling: str = "multiplicity"
     tol: float = 1e-6
     maxit: int = 5000
-    constraints: str = "initial"   # initial | adaptive
+    constraints: str = "initial"   # initial | adaptive | multiscale
 
     def __post_init__(self):
         if not 0.0 < self.tol < 1.0:
@@ -49,9 +49,6 @@ class SolveConfig:
         if self.constraints not in ("initial", "adaptive", "multiscale"):
             raise InvalidArgumentError(
                 f"unknown constraint mode {self.constraints!r}")
-        if self.constraints == "multiscale":
-            raise InvalidArgumentError(
-                "multiscale constraints are outside the accelerated path")
         if self.scaling not in ("multiplicity", "stiffness"):
             raise InvalidArgumentError(f"unknown scaling kind {self.scaling!r}")
 
@@ -226,6 +223,7 @@ class BddcSetup:
         rows = torch.zeros(1, dtype=F64, device=dev)
         qbasis = None
         self.pair_lambda = None
+        self.pair_added = None   # rows added per face beyond the initial one
         if config.constraints == "adaptive" and nf:
             maxsel = dec.maxF
             lam_ld = dec.maxF
@@ -268,6 +266,15 @@ class BddcSetup:
             self.omega_tilde = float(max(self.face_omega.max(), 1.0)) if nf else 1.0
         elif config.constraints == "adaptive":
             self.omega_tilde = 1.0
+        elif config.constraints == "multiscale" and nf:
+            # MsMFEM baseline (solver.py:89-90, adaptive.py:207-269): one row per face
+            maxsel = 1
+            rows, qbasis, nadd = self._multiscale_rows(system, Sinv)
+            self.pair_added = nadd
+            # per face: the multiscale row on the shared dofs, outward from the lower subdomain
+            fm = dec.face_table[:, 3]
+            rh = rows.view(nf, 112).cpu().numpy()
+            self.multiscale_rows = [rh[q, :int(fm[q])].copy() for q in range(nf)]
         self._mark(ev, "pairs")
         # coarse dof numbering: per face [initial, adaptive...]
         per_face = 1 + nadd
@@ -391,6 +398,39 @@ class BddcSetup:
         if isinstance(self._timings, dict):
             self._timings.update(out)
         return out
+
+    def _multiscale_rows(self, system, Sinv):
+        """Face rows of the pair-local unit-transfer solves (adaptive.py:207-262),
+        from each subdomain's interior response to its unit source distribution
+        (uniform, or following the wells) and the S_i face blocks."""
+        dec, dev, st = self.dec, self.dev, _stream()
+        N, mg, nf = self.N, self.maxG, dec.n_faces
+        f = np.asarray(system.f, dtype=np.float64)
+        tot = np.bincount(dec.cell_sub, weights=f, minlength=N)
+        cnt = np.bincount(dec.cell_sub, minlength=N).astype(np.float64)
+        well = np.abs(tot) > 1e-14
+        dist = np.where(well[dec.cell_sub], f / np.where(well, tot, 1.0)[dec.cell_sub],
+                        1.0 / cnt[dec.cell_sub])
+        gdev = torch.as_tensor(dist, dtype=F64, device=dev)
+        g = torch.empty_like(gdev)
+        # D-scaled cell values (local_solve reads g / D)
+        nat.call("bddc_scale_cells", C.byref(self.geom), _p(gdev), _p(self.d_cell_sub),
+                 _p(self.d_Dsub), _p(g), st)
+        rg = torch.zeros(N * mg, dtype=F64, device=dev)
+        a = nat.LocalSolveArgs()
+        a.g_cell, a.g_scale = _p(g).value, 1.0
+        a.rg_broken = _p(rg).value
+        nat.call("bddc_local_solve", C.byref(self.geom), _p(self.d_coef), _p(self.d_gcode),
+                 _p(self.d_gpos), _p(self.d_fslot), _p(self.d_Qp), _p(self.d_Dsub), C.byref(a), st)
+        rows = torch.zeros(nf * 112, dtype=F64, device=dev)
+        qbasis = torch.zeros(nf * 2 * 112, dtype=F64, device=dev)
+        d_nadd = torch.zeros(nf, dtype=I32, device=dev)
+        err = torch.zeros(1, dtype=I32, device=dev)
+        nat.call("bddc_multiscale_rows", C.byref(self.geom), _p(self.d_faces), _p(self.d_fslot),
+                 _p(self.d_S), _p(rg), 1, _p(rows), _p(qbasis), _p(d_nadd), _p(err), st)
+        if int(err.item()) & 1:
+            raise NumericalFailureError("multiscale: pair face block not positive definite")
+        return rows, qbasis, d_nadd.cpu().numpy().astype(np.int64)
 
     def _build_coarse_tables(self, cstart, per_face, maxsel):
         """Per-subdomain coarse rows {g, face, k, sigma} in (face, k) order and the

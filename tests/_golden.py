@@ -23,6 +23,8 @@ def load(name):
     d["tau"] = float(d["tau"])
     d["tol"] = float(d["tol"])
     d["mode"] = "adaptive" if math.isfinite(d["tau"]) else "initial"
+    if "constraints" in d:
+        d["mode"] = str(d["constraints"])
     return d
 
 

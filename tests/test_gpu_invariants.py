@@ -141,3 +141,18 @@ def test_homogeneous_benchmark_2x7():
     dec = B.regular_partition(g, (2, 7))
     rep = B.solve(system, dec, B.SolveConfig(tol=1e-6))
     assert 8 <= rep.it <= 18 and 2.0 <= rep.kappa <= 6.0 and rep.n_c == 33
+
+
+def test_multiscale_rows_unit_net_flux():
+    """test_adaptive.py:102-111: every multiscale row carries the unit transfer, i.e.
+    sums to 1 for the lower subdomain of its pair."""
+    import paper_1901_02090_b200 as B
+    g = B.build_grid(2, (12, 12), (1.0, 1.0))
+    k = 10.0 ** np.random.default_rng(9).uniform(-3, 3, (g.n_cells, 2))
+    system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
+    dec = B.regular_partition(g, (3, 3))
+    st = B.BddcSetup(system, dec, B.SolveConfig(constraints="multiscale", tol=1e-8))
+    assert len(st.multiscale_rows) == dec.n_faces
+    for row in st.multiscale_rows:
+        assert row.sum() == pytest.approx(1.0, rel=1e-8)
+    assert st.n_c == 2 * dec.n_faces + dec.n_subdomains

@@ -40,7 +40,7 @@ def test_solution_parity(name):
     st = B.BddcSetup(system, dec, cfg)
     rep = B.solve(system, dec, cfg, setup=st)
     assert rep.n_c == int(d["n_c"])
-    np.testing.assert_array_equal(st.pair_added + 1 if st.pair_lambda is not None
+    np.testing.assert_array_equal(st.pair_added + 1 if st.pair_added is not None
                                   else np.ones(dec.n_faces, int), d["face_rows"])
     it_ref = int(d["it"])
     if _sensitive(d):
