@@ -152,7 +152,8 @@ int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces,
                       const int* gcode, const int* nG, const double* rows, const double* qbasis,
                       int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
                       double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi,
-                      double* T, double* b0, void* inv_ws, int* dims, int* info, void* stream);
+                      double* T, double* b0, void* inv_ws, int* dims, int* info, int part,
+                      void* stream);
 int bddc_pad_identity(double* M, int n, int npad, void* stream);
 
 /* Nested-dissection multifrontal coarse solver (replaces the dense coarse

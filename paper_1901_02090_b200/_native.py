@@ -99,7 +99,7 @@ _SIGS = {
     "bddc_pair_eigs": [_GP, _P, _P, _P, _P, _P, _D, _I, _P, _I, _P, _P, _P,
                        _P, _P, _P, _P, _P, _I, _I, _I, _P],
     "bddc_coarse_local": [_GP, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P,
-                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+                          _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "bddc_pad_identity": [_P, _I, _I, _P],
     "bddc_graph_begin": [C.POINTER(C.c_void_p), _P],
     "bddc_graph_while": [_P, _P],

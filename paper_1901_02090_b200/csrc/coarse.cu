@@ -166,29 +166,31 @@ __global__ void copy_kernel(const double* __restrict__ a, double* __restrict__ b
 
 }  // namespace
 
-// Per-subdomain coarse pieces.  Workspaces: Ct, Y, E (N*maxG*maxC each),
+// Per-subdomain coarse pieces (part 1: Kc, Psi, b0 and the live-size table dims;
+// part 2: T, after part 1 ran; 3: both).  Workspaces: Ct, Y, E (N*maxG*maxC each),
 // inv_ws (bddc_spd_inverse_workspace(max(maxC, maxG), N, 32|64)), gamma (N).
 extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces, const int* fslot,
                                  const int* gcode, const int* nG, const double* rows, const double* qbasis,
                                  int maxsel, const double* S, const double* Sinv, const double* Dsub, int maxC,
                                  double* Ct, double* Y, double* E, double* gamma, double* Kc, double* Psi, double* T,
-                                 double* b0, void* inv_ws, int* dims, int* info, void* stream) {
+                                 double* b0, void* inv_ws, int* dims, int* info, int part, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int N = g->N, mg = g->maxG;
   const long long sG = (long long)mg * mg, sGC = (long long)mg * maxC, sCC = (long long)maxC * maxC;
   if (maxC % 32) return bddc_set_error(BDDC_ERR_ARG, "coarse_local: maxC must be a multiple of 32");
-  coarse_ct_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, rows, maxsel, maxC, Ct);
-  LAUNCH_OK();
-  // every product below runs on the live nG_i x nC_i blocks only (maxC pads to the
-  // largest subdomain's coarse count; the mean is ~5x smaller)
-  coarse_dims_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, maxC, nG, sub_rows, dims);
-  LAUNCH_OK();
   const int* dGCG = dims;
   const int* dCCG = dims + 3;
   const int* dCGC = dims + 6;
   const int* dGGC = dims + 9;
   const int* dGCC = dims + 12;
   int r;
+  if (part & 1) {
+  coarse_ct_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, rows, maxsel, maxC, Ct);
+  LAUNCH_OK();
+  // every product below runs on the live nG_i x nC_i blocks only (maxC pads to the
+  // largest subdomain's coarse count; the mean is ~5x smaller)
+  coarse_dims_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, maxC, nG, sub_rows, dims);
+  LAUNCH_OK();
   // Y = Sinv C^T ; Kinv = C Y ; Kc = Kinv^-1 ; PsiT = Kc Y^T ; b0
   if ((r = bddc_dgemm_batched_dims(0, 0, mg, maxC, mg, 1.0, Sinv, mg, sG, Ct, maxC, sGC, 0.0, Y, maxC, sGC, N, 0, dGCG, 16, stream)))
     return r;
@@ -203,6 +205,8 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
     return r;
   b0_kernel<<<N, 256, 0, s>>>(*g, gcode, sub_rows, Psi, Dsub, maxC, b0);
   LAUNCH_OK();
+  }
+  if (!(part & 2)) return 0;
   // ---- T = (P S P + g Q Q^T)^-1 - Q Q^T / g   (Q in Ct, S Q in Y, Q^T S Q in E[..maxC^2])
   qc_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, qbasis, maxsel, maxC, Ct);
   LAUNCH_OK();

@@ -139,6 +139,9 @@ class BddcSetup:
         st = _stream()
         self._timings = timings
         ev = self._events()
+        # coarse chain of the preconditioner (and the T_i setup branch): high priority
+        # so its small latency-bound kernels get SM slots ahead of queued GEMV blocks
+        self.side_stream = torch.cuda.Stream(device=dev, priority=-1)
         N, mg, mp = dec.n_subdomains, dec.maxG, dec.maxP
         self.N, self.maxG, self.maxP = N, mg, mp
         t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
@@ -190,7 +193,7 @@ class BddcSetup:
         nat.call("bddc_local_build", gp, _p(self.d_coef), _p(self.d_fslot),
                  _p(self.d_Q), _p(Gc), _p(SAd), _p(SApart), _p(SAoff),
                  _p(alpha), st)
-        info = torch.zeros(4, dtype=I32, device=dev)
+        info = torch.zeros(5, dtype=I32, device=dev)
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, 32) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(self.d_Q), mp, mp, mp * mp, N,
@@ -298,20 +301,26 @@ class BddcSetup:
                   nat.load().bddc_spd_inverse_workspace(mg, N, 64))
         ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
         dims = torch.empty(N * 16, dtype=I32, device=dev)
-        nat.call("bddc_coarse_local", gp, _p(dev_rows), _p(self.d_faces),
-                 _p(self.d_fslot), _p(self.d_gcode), _p(self.d_nG), _p(rows),
-                 _p(qbasis) if qbasis is not None else None, maxsel, _p(self.d_S), _p(Sinv),
-                 _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(E), _p(gam), _p(self.d_Kc),
-                 _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws), _p(dims),
-                 _p(info[2:]), st)
-        del Ct, Y, E, gam, ws, Sinv, dims
-        # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
+        cl_args = [gp, _p(dev_rows), _p(self.d_faces), _p(self.d_fslot), _p(self.d_gcode),
+                   _p(self.d_nG), _p(rows), _p(qbasis) if qbasis is not None else None, maxsel,
+                   _p(self.d_S), _p(Sinv), _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(E), _p(gam),
+                   _p(self.d_Kc), _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws), _p(dims),
+                   _p(info[2:])]
+        nat.call("bddc_coarse_local", *cl_args, 1, st)
+        # T_i (its batched inverse) on a side stream, concurrently with the global coarse
+        # factorisation below, whose small-batch inverses are latency-bound
         npk = nat.load().bddc_sym_packed_elems(mg)
         self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
         self.d_Tp = torch.empty(N * npk, dtype=F64, device=dev)
+        main = torch.cuda.current_stream()
+        side = self.side_stream
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            ss = _stream()
+            nat.call("bddc_coarse_local", *cl_args[:-1], _p(info[4:]), 2, ss)
+            nat.call("bddc_pack_sym", N, mg, _p(self.d_T), _p(self.d_Tp), ss)
+        # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
         nat.call("bddc_pack_sym", N, mg, _p(self.d_S), _p(self.d_Sp), st)
-        nat.call("bddc_pack_sym", N, mg, _p(self.d_T), _p(self.d_Tp), st)
-        del self.d_S, self.d_T
         self._mark(ev, "coarse_local")
         # global coarse: multifrontal S_Pi (nested dissection) + pinned pressure Schur Pc
         nfc = self.n_flux_coarse
@@ -325,10 +334,12 @@ class BddcSetup:
             root = self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
             self._build_pressure_schur(root)
             self.nd.release_fronts()
+        main.wait_stream(side)   # T_i done; its workspaces may go now
+        del Ct, Y, E, gam, ws, Sinv, dims, cl_args, self.d_S, self.d_T
         bad = info.cpu().numpy()
         if bad[0] or bad[1]:
             raise NumericalFailureError("local interior factorization failed", where=None)
-        if bad[2]:
+        if bad[2] or bad[4]:
             raise NumericalFailureError("constrained coarse basis system singular")
         self._mark(ev, "coarse")
         # persistent PCG workspaces
@@ -353,9 +364,6 @@ class BddcSetup:
         self._work = None
         self._host_scal = torch.empty(16, dtype=F64, pin_memory=True)
         self.stream = torch.cuda.Stream(device=dev)
-        # coarse chain of the preconditioner: high priority so its small latency-bound
-        # kernels get SM slots ahead of the queued T_i GEMV blocks
-        self.side_stream = torch.cuda.Stream(device=dev, priority=-1)
         self.n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         # T_i GEMV grid beside the coarse chain: one CTA per SM (C3 whole solve: 29.5 ms
         # at 1x SMs, 30.9 at 2x and 3x, 31.5 with one CTA per subdomain)
