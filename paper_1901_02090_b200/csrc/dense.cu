@@ -99,7 +99,86 @@ __device__ __forceinline__ double frag(const double* s, int r, int k) {
   return kmajor ? s[k * LDM + r] : s[r * LDK + k];
 }
 
+// One 64x64 output tile: acc += op(A)[m0.., kbeg..kend) * op(B)[kbeg..kend), n0..),
+// cp.async double-buffered through As/Bs (2 x TILE_ELEMS each), DMMA m8n8k4.
 // transA: A stored K x M (so op(A) = A^T); transB: B stored N x K.
+template <bool transA, bool transB, bool aligned>
+__device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const double* __restrict__ A, int lda,
+                                         const double* __restrict__ B, int ldb, int Ml, int Nl, int K, int m0,
+                                         int n0, int kbeg, int kend, double (*As)[TILE_ELEMS],
+                                         double (*Bs)[TILE_ELEMS]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  kbeg = (kbeg / BK) * BK;
+  const int kt0 = kbeg / BK;
+  const int nk = (kend > kbeg) ? (kend + BK - 1) / BK : kt0;
+  if (kt0 < nk) {
+    // A operand rows are m (R = M); B operand rows are n (R = N).
+    load_tile<transA, aligned>(As[kt0 & 1], A, lda, Ml, K, m0, kbeg);
+    load_tile<!transB, aligned>(Bs[kt0 & 1], B, ldb, Nl, K, n0, kbeg);
+    cp_async_commit();
+  }
+  for (int kt = kt0; kt < nk; ++kt) {
+    if (kt + 1 < nk) {
+      load_tile<transA, aligned>(As[(kt + 1) & 1], A, lda, Ml, K, m0, (kt + 1) * BK);
+      load_tile<!transB, aligned>(Bs[(kt + 1) & 1], B, ldb, Nl, K, n0, (kt + 1) * BK);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* as = As[kt & 1];
+    const double* bs = Bs[kt & 1];
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = frag<transA>(as, wm + i * 8 + g, kk + t);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = frag<!transB>(bs, wn + j * 8 + g, kk + t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void tile_store(const double (&acc)[4][4][2], double* __restrict__ C, int ldc, int M,
+                                           int N, int m0, int n0, double alpha, double beta) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int r = m0 + wm + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int c = n0 + wn + j * 8 + 2 * t;
+      double* cp = C + (size_t)r * ldc + c;
+      if (c < N) {
+        double v = alpha * acc[i][j][0];
+        cp[0] = (beta == 0.0) ? v : v + beta * cp[0];
+      }
+      if (c + 1 < N) {
+        double v = alpha * acc[i][j][1];
+        cp[1] = (beta == 0.0) ? v : v + beta * cp[1];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void acc_zero(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
 template <bool transA, bool transB, bool aligned>
 __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double alpha,
                                                     const double* __restrict__ A, int lda, long long sA,
@@ -134,74 +213,57 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
   __shared__ __align__(16) double As[2][TILE_ELEMS];
   __shared__ __align__(16) double Bs[2][TILE_ELEMS];
   const int m0 = bm * BM, n0 = bn * BN;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const int g = lane >> 2, t = lane & 3;
-
   double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
+  acc_zero(acc);
   // triangular operands: only the K range that can be nonzero for this tile
   int kbeg = 0, kend = K;
   if (upper & 2) kbeg = max(kbeg, m0);           // op(A) upper: k >= m
   if (upper & 4) kend = min(kend, m0 + BM);      // op(A) lower: k <= m
   if (upper & 8) kend = min(kend, n0 + BN);      // op(B) upper: k <= n
   if (upper & 16) kbeg = max(kbeg, n0);          // op(B) lower: k >= n
-  kbeg = (kbeg / BK) * BK;
-  const int kt0 = kbeg / BK;
-  const int nk = (kend > kbeg) ? (kend + BK - 1) / BK : kt0;
-  if (kt0 < nk) {
-  // A operand rows are m (R = M); B operand rows are n (R = N).
-  load_tile<transA, aligned>(As[kt0 & 1], A, lda, Ml, K, m0, kbeg);
-  load_tile<!transB, aligned>(Bs[kt0 & 1], B, ldb, Nl, K, n0, kbeg);
-  cp_async_commit();
-  }
-  for (int kt = kt0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_tile<transA, aligned>(As[(kt + 1) & 1], A, lda, Ml, K, m0, (kt + 1) * BK);
-      load_tile<!transB, aligned>(Bs[(kt + 1) & 1], B, ldb, Nl, K, n0, (kt + 1) * BK);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* as = As[kt & 1];
-    const double* bs = Bs[kt & 1];
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = frag<transA>(as, wm + i * 8 + g, kk + t);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = frag<!transB>(bs, wn + j * 8 + g, kk + t);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
+  tile_mma<transA, transB, aligned>(acc, A, lda, B, ldb, Ml, Nl, K, m0, n0, kbeg, kend, As, Bs);
+  tile_store(acc, C, ldc, M, N, m0, n0, alpha, beta);
+}
+
+// In-place triangular products (TRMM) of the SPD inverse, no scratch copy:
+//  left:  B <- alpha U B   (U upper n1 x n1, B n1 x n2): a CTA owns a 64-column strip
+//         and walks its row tiles top-down (tile m reads rows >= m only);
+//  right: B <- alpha B U^T (U upper n2 x n2, B n1 x n2): a CTA owns a 64-row strip
+//         and walks its column tiles left to right (tile n reads columns >= n only).
+template <bool aligned>
+__global__ void __launch_bounds__(128) trmm_left_upper_kernel(int n1, int n2, double alpha,
+                                                              const double* __restrict__ U, double* B, int ld,
+                                                              long long sM) {
+  const int n0 = blockIdx.x * BN, bz = blockIdx.y;
+  const double* Uz = U + bz * sM;
+  double* Bz = B + bz * sM;
+  __shared__ __align__(16) double As[2][TILE_ELEMS];
+  __shared__ __align__(16) double Bs[2][TILE_ELEMS];
+  for (int m0 = 0; m0 < n1; m0 += BM) {
+    double acc[4][4][2];
+    acc_zero(acc);
+    tile_mma<false, false, aligned>(acc, Uz, ld, Bz, ld, n1, n2, n1, m0, n0, m0, n1, As, Bs);
+    tile_store(acc, Bz, ld, n1, n2, m0, n0, alpha, 0.0);
     __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int r = m0 + wm + i * 8 + g;
-    if (r >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int c = n0 + wn + j * 8 + 2 * t;
-      double* cp = C + (size_t)r * ldc + c;
-      if (c < N) {
-        double v = alpha * acc[i][j][0];
-        cp[0] = (beta == 0.0) ? v : v + beta * cp[0];
-      }
-      if (c + 1 < N) {
-        double v = alpha * acc[i][j][1];
-        cp[1] = (beta == 0.0) ? v : v + beta * cp[1];
-      }
-    }
+}
+
+template <bool aligned>
+__global__ void __launch_bounds__(128) trmm_right_upperT_kernel(int n1, int n2, double alpha,
+                                                                const double* __restrict__ U, double* B, int ld,
+                                                                long long sM) {
+  const int m0 = blockIdx.x * BM, bz = blockIdx.y;
+  const double* Uz = U + bz * sM;
+  double* Bz = B + bz * sM;
+  __shared__ __align__(16) double As[2][TILE_ELEMS];
+  __shared__ __align__(16) double Bs[2][TILE_ELEMS];
+  for (int n0 = 0; n0 < n2; n0 += BN) {
+    double acc[4][4][2];
+    acc_zero(acc);
+    // op(B)[k][n] = U[n][k]: nonzero for k >= n
+    tile_mma<false, true, aligned>(acc, Bz, ld, Uz, ld, n1, n2, n2, m0, n0, n0, n2, As, Bs);
+    tile_store(acc, Bz, ld, n1, n2, m0, n0, alpha, 0.0);
+    __syncthreads();
   }
 }
 
@@ -378,6 +440,29 @@ int block_copy(double* dst, int ld, long long sD, const double* src, int lds, lo
   return 0;
 }
 
+// The in-place TRMMs walk a strip's tiles in sequence: worth it only when the
+// strips alone fill the GPU (batched small matrices), not for a few large ones.
+bool trmm_inplace_pays(int n1, int n2, int batch) {
+  const long long strips = (long long)batch * ((imin(n1, n2) + 63) / 64);
+  return strips >= 2 * 148 && imax(n1, n2) <= 512;
+}
+
+int trmm_launch(int right, int n1, int n2, double alpha, const double* U, double* B, int ld, long long sM,
+                int batch, cudaStream_t s) {
+  const bool al = !(((uintptr_t)U | (uintptr_t)B) & 15) && !(ld & 1) && !(sM & 1);
+  if (!right) {
+    dim3 g((n2 + BN - 1) / BN, batch);
+    if (al) trmm_left_upper_kernel<true><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+    else trmm_left_upper_kernel<false><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+  } else {
+    dim3 g((n1 + BM - 1) / BM, batch);
+    if (al) trmm_right_upperT_kernel<true><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+    else trmm_right_upperT_kernel<false><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+  }
+  LAUNCH_OK();
+  return 0;
+}
+
 int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
   size_t shm = (size_t)n * (n + 1) * sizeof(double);
   if (shm > 48 * 1024)
@@ -387,8 +472,14 @@ int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, in
   return 0;
 }
 
+// Split point of the 2x2 recursion: a multiple of the GEMM tile (64) when the
+// block is large, so the DMMA GEMMs run on whole tiles (448 -> 256 + 192 rather
+// than 224 + 224, whose 3.5-tile edges waste a quarter of every product);
+// otherwise a multiple of the leaf size.
 int split_of(int n, int b) {
-  int n1 = ((n / 2 + b - 1) / b) * b;
+  const int q = (n > 128) ? 64 : b;
+  int n1 = ((n / 2 + q - 1) / q) * q;
+  if (n1 >= n) n1 = ((n / 2 + b - 1) / b) * b;
   if (n1 >= n) n1 = n - b;
   return n1;
 }
@@ -413,9 +504,15 @@ int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, doubl
   if ((r = bddc_dgemm_batched(1, 0, n1, n2, n1, 1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 4, s))) return r;
   if ((r = bddc_dgemm_batched(1, 0, n2, n2, n1, -1.0, W, n2, sW, W, n2, sW, 1.0, C, ld, sM, batch, 1, s))) return r;
   if ((r = chol_inv_rec(C, n2, ld, sM, batch, b, ws_next, info, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 8, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 2, s))) return r;
-  if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  if (trmm_inplace_pays(n1, n2, batch)) {
+    if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 8, s))) return r;
+    if ((r = trmm_launch(0, n1, n2, -1.0, A, B, ld, sM, batch, s))) return r;   // B <- -V11 B
+  } else {
+    // few matrices: full-grid GEMMs through the scratch block, then a copy
+    if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 8, s))) return r;
+    if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 2, s))) return r;
+    if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  }
   return block_copy(M + (size_t)n1 * ld, ld, sM, nullptr, 0, 0, n2, n1, batch, s);
 }
 
@@ -433,8 +530,12 @@ int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* 
   int r;
   if ((r = lauum_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
   if ((r = bddc_dgemm_batched(0, 1, n1, n1, n2, 1.0, B, ld, sM, B, ld, sM, 1.0, A, ld, sM, batch, 1, s))) return r;
-  if ((r = bddc_dgemm_batched(0, 1, n1, n2, n2, 1.0, B, ld, sM, C, ld, sM, 0.0, W, n2, sW, batch, 16, s))) return r;
-  if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  if (trmm_inplace_pays(n1, n2, batch)) {
+    if ((r = trmm_launch(1, n1, n2, 1.0, C, B, ld, sM, batch, s))) return r;   // B <- V12 V22^T
+  } else {
+    if ((r = bddc_dgemm_batched(0, 1, n1, n2, n2, 1.0, B, ld, sM, C, ld, sM, 0.0, W, n2, sW, batch, 16, s))) return r;
+    if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
+  }
   return lauum_rec(C, n2, ld, sM, batch, b, ws_next, info, s);
 }
 

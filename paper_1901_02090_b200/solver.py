@@ -313,7 +313,7 @@ class BddcSetup:
         self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
         self.d_Tp = torch.empty(N * npk, dtype=F64, device=dev)
         main = torch.cuda.current_stream()
-        side = self.side_stream
+        side = torch.cuda.Stream(device=dev)   # normal priority: the ND branch is the critical path
         side.wait_stream(main)
         with torch.cuda.stream(side):
             ss = _stream()
