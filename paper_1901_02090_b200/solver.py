@@ -370,6 +370,14 @@ class BddcSetup:
         self.t_grid = self.n_sm
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
+        self._solves = 0   # public solves run on this setup
+        # per-solve buffers, allocated here on the allocating stream while the device
+        # finishes the setup (allocations on the solve stream could not reuse the
+        # blocks the setup freed and would each go to cudaMalloc)
+        self.work()
+        self._pcg_bufs(config.maxit)
+        if self.nd is not None:
+            self.nd._bufs()
         self._mark(ev, "done")
         self.phase_ms = self._finish(ev)
 
@@ -755,12 +763,25 @@ def _suggest_scaling(setup):
     dec = setup.dec
     if not dec.n_gamma or not dec.n_faces:
         return
-    k = setup.system.perm.k
-    lo, hi, starts = _face_cells(dec)
-    kmax = np.maximum.reduceat(k[lo].max(axis=1), starts)
-    kmin = np.minimum.reduceat(k[hi].min(axis=1), starts)
-    ratio = kmax / np.maximum(kmin, 1e-300)
-    if np.any((ratio > 1e3) | (ratio < 1e-3)):
+    # per face: max k over the low-side cells / min k over the high-side cells,
+    # reduced on the device (index tables cached on the decomposition)
+    dev = setup.dev
+    cache = getattr(dec, "_face_cells_dev", None)
+    if cache is None or cache[0] != dev:
+        lo, hi, starts = _face_cells(dec)
+        cnt = np.diff(np.append(starts, len(lo)))
+        seg = np.repeat(np.arange(len(starts)), cnt)
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.int64, device=dev)
+        cache = (dev, t(lo), t(hi), t(seg), len(starts))
+        dec._face_cells_dev = cache
+    _, lo, hi, seg, nfa = cache
+    k = setup.d_k.view(-1, setup.dec.grid.dim) if setup.d_k.dim() == 1 else setup.d_k
+    kl = k[lo].amax(dim=1)
+    kh = k[hi].amin(dim=1)
+    kmax = torch.full((nfa,), -math.inf, dtype=F64, device=dev).scatter_reduce(0, seg, kl, "amax")
+    kmin = torch.full((nfa,), math.inf, dtype=F64, device=dev).scatter_reduce(0, seg, kh, "amin")
+    ratio = kmax / torch.clamp(kmin, min=1e-300)
+    if bool(((ratio > 1e3) | (ratio < 1e-3)).any()):
         warnings.warn("coefficient jumps aligned with the partition detected; "
                       "consider --scaling stiffness")
 
@@ -829,12 +850,15 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     N, ng = setup.N, setup.n_gamma
     # fs = D f
     if f_device is None:
-        # staging through torch's caching pinned allocator (no cudaHostAlloc per call)
-        fh = torch.empty(G.n_cells, dtype=F64, pin_memory=True)
-        np.copyto(fh.numpy(), np.asarray(system.f, dtype=np.float64).reshape(-1))
-        W.f_host = fh   # keep the pinned buffer alive until the copy ran
         f_device = W.f_dev
-        f_device.copy_(fh, non_blocking=True)
+        if setup._solves == 0:
+            f_device.copy_(torch.as_tensor(np.asarray(system.f, dtype=np.float64).reshape(-1)))
+        else:
+            # staging through torch's caching pinned allocator (no cudaHostAlloc per call)
+            fh = torch.empty(G.n_cells, dtype=F64, pin_memory=True)
+            np.copyto(fh.numpy(), np.asarray(system.f, dtype=np.float64).reshape(-1))
+            W.f_host = fh   # keep the pinned buffer alive until the copy ran
+            f_device.copy_(fh, non_blocking=True)
     _scale_fs(setup, f_device, W.fs)
     # step 1: rq_i = sum fs over cells of i; x0 = Wq rq[1:]; g = average(Psi x0)
     nat.call("bddc_sub_sum", gp, _p(W.fs), _p(W.rq), 1.0, None, st)
@@ -863,9 +887,12 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
              _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     host = {}
-    if not return_device:
+    first = setup._solves == 0
+    setup._solves += 1
+    if not return_device and not first:
         # u0 and u* are final here: stream them to pinned host memory on a copy
-        # stream while the PCG runs
+        # stream while the PCG runs (from the second solve on: the first one would
+        # pay the pinned allocation, slower than a pageable copy of the same bytes)
         host["u0"], host["us"] = _d2h_async(setup, (W.u0, W.us))
     # div_defect = fs - Bs u*
     nat.call("bddc_cell_div", gp, _p(W.us), _p(W.fs), 1.0, -1.0, _p(setup.d_cell_sub),
@@ -891,7 +918,11 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         # subdomain net-flux targets (stiffness scaling only)
         nat.call("bddc_sub_sum", gp, _p(W.dd), _p(setup.w_phi), -1.0, _p(setup.d_Dsub), st)
         # sum |fs| = sum_c |f_c| D_sub(c) (D > 0); one 2-scalar read
-        tmax, fs_abs = torch.stack([setup.w_phi.abs().max(), W.fs.abs().sum()]).tolist()
+        # (into preallocated work vectors: temporaries on the solve stream would each
+        # be a fresh device allocation)
+        torch.abs(setup.w_phi, out=setup.w_z)
+        torch.abs(W.fs, out=W.tmpc)
+        tmax, fs_abs = torch.stack([setup.w_z.max(), W.tmpc.sum()]).tolist()
         if tmax > 1e-13 * max(fs_abs, 1.0):
             S3 = dec.S3
             nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
@@ -921,10 +952,13 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
     if return_device:
         return W, w_cg_it, kappa, history, converged
-    hu, hp = _d2h_async(setup, (W.u, W.pc))
-    setup.copy_stream.synchronize()
+    if first:
+        host = {"u": W.u.cpu(), "p": W.pc.cpu(), "u0": W.u0.cpu(), "us": W.us.cpu()}
+    else:
+        host["u"], host["p"] = _d2h_async(setup, (W.u, W.pc))
+        setup.copy_stream.synchronize()
     report = SolveReport(
-        u=hu.numpy(), p=hp.numpy(), it=w_cg_it, kappa=kappa,
+        u=host["u"].numpy(), p=host["p"].numpy(), it=w_cg_it, kappa=kappa,
         omega_tilde=omega, n_c=setup.n_c, residuals=history,
         u0=host["u0"].numpy(), u_star=host["us"].numpy(),
         conservation_defect=defect_norm, pressure_warning=p_warn,
@@ -1095,6 +1129,11 @@ def _pcg(setup, W, config, callback):
         top, body = setup._graph_kernels[(float(tol), int(maxit))]
         setup.graph_kernels_run += top + body * max(int(host[9]) - 1, 0)
     else:
+        pt = setup.pcg_timer
+        if pt is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         _pcg_first(setup, W, B)
         while True:
             host.copy_(scal, non_blocking=True)
@@ -1104,6 +1143,9 @@ def _pcg(setup, W, config, callback):
             if host[5] <= tol or host[8] != 0.0 or int(host[9]) >= maxit:
                 break
             _pcg_body(setup, W, B)
+        if pt is not None:
+            e1.record()
+            pt.append((e0, e1))
     it = int(host[9])
     if host[8] != 0.0:
         raise NonConvergenceError(
