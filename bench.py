@@ -166,20 +166,19 @@ def _load_meta(cfg_id):
 def _iteration_roofline(setup, dec, pcg_s, its, peak):
     """Whole PCG iteration against HBM: algorithmic bytes streamed per
     iteration = S_i and T_i (packed symmetric) + live Psi_i twice (restriction,
-    prolongation) + the ND coarse factors + Pc^-1 + the projection operator
+    prolongation) + the ND coarse factors (pressures included) + the projection operator
     (twice) + ~16 interface-length vectors; achieved = bytes x iterations over
     the device time of the PCG graph launches."""
     nG = dec.nG.astype(np.float64)
     sym = float(np.sum(8.0 * nG * (nG + 1) / 2))
     psi = float(np.sum(8.0 * np.asarray(setup.nC, dtype=np.float64) * nG))
     nd = float(setup.nd.bytes) if setup.nd is not None else 0.0
-    pc = 8.0 * (setup.N - 1) ** 2
     proj = 2.0 * 8.0 * setup.N ** 2 if getattr(setup, "d_Lp", None) is not None else 0.0
     vec = 16.0 * 8.0 * setup.n_gamma
-    per_it = 2 * sym + 2 * psi + nd + pc + proj + vec
+    per_it = 2 * sym + 2 * psi + nd + proj + vec
     achieved = per_it * its / pcg_s / 1e9 if pcg_s > 0 else None
     return {"bound": "hbm", "bytes_per_iteration": per_it,
-            "parts": {"S_T_packed": 2 * sym, "Psi": 2 * psi, "nd_factors": nd, "Pc_inv": pc,
+            "parts": {"S_T_packed": 2 * sym, "Psi": 2 * psi, "nd_factors": nd,
                       "projection": proj, "vectors": vec},
             "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None,

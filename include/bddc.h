@@ -158,7 +158,7 @@ int bddc_pad_identity(double* M, int n, int npad, void* stream);
 
 /* Nested-dissection multifrontal coarse solver (replaces the dense coarse
  * lu_factor / lu_solve of coarse.py:186-215; see coarse_nd.py). */
-int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, const int* cmap,
+int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, int K, const int* cmap,
                      const int* ckind, const int* sep_idx, double* F, const double* Fc, int Sc,
                      int nfc, const double* Kc, const int* sub_rows, const double* b0, int maxC,
                      void* stream);
@@ -173,18 +173,11 @@ int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* in
 int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
                 const double* ybuf, double* x, void* stream);
-int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
-                    const long long* data_off, double* Fc, void* stream);
-/* Root pressure block of the pinned coarse solve: x_p = -Pc^-1 (r_p - contributions). */
-int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const int* psrc, const double* cbuf,
-                     const double* Pcinv, const double* r, double* rp, double* x, void* stream);
-/* Pinned pressure Schur Pc = -U_root[1:,1:] (coarse.py:192-194). */
-int bddc_nd_extract_pc(const double* F, int nf, int S, int N, double* Pc, int npc, void* stream);
-/* Pressure coupling B0 (coarse.py:184-193): out = B0[1:] Y, r += alpha B0[1:]^T z. */
-int bddc_b0_apply(int N, int maxC, const int* sub_rows, const double* b0, const double* Y, int ldy,
-                  int nrhs, double* out, int ldo, void* stream);
-int bddc_b0t_apply(int nfc, int maxC, const int* cown, const double* b0, const double* z, int ldz,
-                   int nrhs, double alpha, double* r, int ldr, void* stream);
+int bddc_nd_compact(int m, int S, int Sf, int nf, int B, const double* F, const double* X,
+                    const int* info, const long long* data_off, double* Fc, void* stream);
+/* Quasi-definite pivot blocks [flux (Sf) | eliminated pressures (Sp)]: mode 0 negates
+ * the pressure block, mode 1 mirrors the off-diagonal block into the upper right. */
+int bddc_nd_qd(int mode, int m, int Sf, int Sp, int nf, double* F, void* stream);
 int bddc_fill(long long n, double v, double* a, void* stream);
 
 /* ------------------------------------------------------------------- PCG */

@@ -108,15 +108,12 @@ _SIGS = {
     "bddc_graph_destroy": [_P],
     "bddc_graph_handle": [_P],
     "bddc_pcg_cond": [_P, _P, _D, _I, _P],
-    "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
+    "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
                          _P, _P, _I, _P],
     "bddc_nd_fwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "bddc_nd_compact": [_I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
-    "bddc_nd_pressure": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
-    "bddc_nd_extract_pc": [_P, _I, _I, _I, _P, _I, _P],
+    "bddc_nd_compact": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_qd": [_I, _I, _I, _I, _I, _P, _P],
     "bddc_nd_bwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
-    "bddc_b0_apply": [_I, _I, _P, _P, _P, _I, _I, _P, _I, _P],
-    "bddc_b0t_apply": [_I, _I, _P, _P, _P, _I, _I, _D, _P, _I, _P],
     "bddc_fill": [_L, _D, _P, _P],
 
     "bddc_gather_gemv": [_I, _I, _P, _P, _P, _P, _P, _P, _P],

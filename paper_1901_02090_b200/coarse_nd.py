@@ -3,30 +3,30 @@
 The reference factors the coarse saddle problem densely (`coarse.py:186-215`:
 `lu_factor` of [[S_Pi, B0^T],[B0, 0]] with subdomain 0's pressure pinned).
 S_Pi couples coarse dofs only through shared subdomains, so for box
-partitions a plane of subdomain faces separates the subdomain grid.  We
-eliminate the flux coarse dofs by a multifrontal block-LDL^T over that
-nested-dissection tree while carrying the subdomain pressures along as
-never-eliminated front variables: the root's update matrix is then exactly
--B0 S_Pi^-1 B0^T, whose pinned part Pc (drop subdomain 0) is inverted
-densely.  Coarse solves (solver.py:117-118, 318-319) become
-
-    flux rhs r, pressure rhs 0 :  x = S_Pi^-1 (r - B0^T Pc^-1 B0 S_Pi^-1 r)
-    flux rhs 0, pressure rhs q :  w = S_Pi^-1 B0[1:]^T Pc^-1 q[1:]
-
+partitions a plane of subdomain faces separates the subdomain grid, and each
+subdomain pressure couples only to that subdomain's coarse flux dofs.  We
+factor the pinned saddle matrix itself by a multifrontal block LDL^T over the
+nested-dissection tree: a node's pivot block holds its separator's flux dofs
+and the pressures of the subdomains whose last face it eliminates
+([[A, B^T], [B, C]], A SPD and the pressure Schur complement negative
+definite, inverted in quasi-definite block form); subdomain 0's pressure is
+pinned and never appears.  The coarse solve (solver.py:117-118, 318-319) is
+then one forward and one backward sweep over the tree, pressures included,
 which is algebraically the pinned solve of the reference.
 
-Tree: every node is a box of subdomain strips; an internal node splits its
-box at the middle of its longest axis; its separator = the coarse dofs on
-the faces of that plane; its boundary = coarse dofs on the box's faces
-toward the rest of the domain, then the pressures of the box's subdomains.
-Leaves are single subdomains whose contribution is the local block
+Tree: every node is a box of subdomain strips; the bisection tree splits a
+box at the middle of its longest axis, and ND_MERGE consecutive bisection
+levels are merged into one node (separator = the union of their planes).
+A node's boundary = coarse dofs on the box's faces toward the rest of the
+domain, then the pressures of its subdomains still live above it.  Leaves are
+single subdomains whose contribution is the local block
 [[sigma sigma^T Kc_i, b0_i^T],[b0_i, 0]] (coarse.py:179-185).  Per internal
-node (front F over [sep | bnd]):
-    F11inv = F11^-1 (blocked symmetric sweep),  X = F21 F11inv,
-    U = F22 - X F12  (extend-added into the parent's front).
-Solve (flux part only): forward y_sep = F11inv (r_sep - descendant
-contributions), c = X r_sep (leaves -> root, left-looking gathers in a
-fixed order); backward x_sep = y_sep - X^T x_bnd (root -> leaves).
+node (front F over [pivot | bnd]):
+    F11inv = F11^-1,  X = F21 F11inv,  U = F22 - X F12  (extend-added into
+    the parent's front).
+Solve: forward y = F11inv (r_pivot - descendant contributions), c = X
+r_pivot (leaves -> root, left-looking gathers in a fixed order); backward
+x_pivot = y - X^T x_bnd (root -> leaves).
 """
 
 from __future__ import annotations
@@ -114,8 +114,40 @@ def nd_geometry(dec):
     if dec.n_subdomains > 1:
         rec((0, 0, 0), tuple(S3), 0)
     nodes = _contract(nodes, ND_MERGE)
+    _assign_pressures(nodes, dec)
     dec._nd_geometry = nodes
     return nodes
+
+
+def _assign_pressures(nodes, dec):
+    """Subdomain pressures are eliminated inside the tree, not carried to the root:
+    p_i couples only to i's coarse flux dofs, so once the last face of i has been
+    eliminated (at the highest node H_i whose separator holds a face of i) p_i is
+    eliminated too, in H_i's pivot block (quasi-definite: the flux block is SPD,
+    the pressure Schur complement negative definite).  Subdomain 0's pressure is
+    pinned (coarse.py:192-194) and appears nowhere.  Per internal node:
+    pres_elim = pressures eliminated there, pres = pressures of its box still
+    live above it (its boundary)."""
+    if not nodes:
+        return
+    internal = [k for k, n in enumerate(nodes) if not n["leaf"]]
+    face_node = np.full(dec.n_faces, -1, dtype=np.int64)
+    for k in internal:
+        face_node[nodes[k]["sep"]] = k
+    ft = dec.face_table
+    N = dec.n_subdomains
+    H = np.full(N, -1, dtype=np.int64)
+    for f in range(dec.n_faces):
+        k = int(face_node[f])
+        for sub in (int(ft[f, 0]), int(ft[f, 1])):
+            if H[sub] < 0 or nodes[k]["depth"] < nodes[int(H[sub])]["depth"]:
+                H[sub] = k
+    hdepth = np.array([nodes[int(h)]["depth"] if h >= 0 else -1 for h in H])
+    for k in internal:
+        box = nodes[k]["pres"]
+        box = box[box != 0]
+        nodes[k]["pres_elim"] = box[H[box] == k]
+        nodes[k]["pres"] = box[hdepth[box] < nodes[k]["depth"]]
 
 
 # Binary-tree levels merged per multifrontal node: a node eliminates the
@@ -183,6 +215,7 @@ def nd_geometry_flat(dec):
     F["sep_ptr"], F["sep"] = csr("sep")
     F["bnd_ptr"], F["bnd"] = csr("bnd")
     F["pres_ptr"], F["pres"] = csr("pres")
+    F["pel_ptr"], F["pel"] = csr("pres_elim")
     # children: internal index (>= 0) or -(1 + subdomain) for leaves; nch per node
     ns = max([len(geo[k]["ch"]) for k in internal] + [1])
     ch = np.zeros((len(internal), ns), dtype=np.int64)
@@ -235,15 +268,25 @@ class CoarseND:
         t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
         if not (N > 1 and nfc):
             self.cb_total = 1
-            self.pptr = t(np.zeros(max(N, 1), np.int32))
-            self.psrc = t(np.zeros(1, np.int32))
             return
         G = nd_geometry_flat(dec)
         nI = len(G["internal"])
-        # coarse dof lists per internal node: sep, boundary = boundary faces' dofs ++ pressures
-        sptr, sdofs = _expand(G["sep_ptr"], G["sep"], per_face, cstart)
+        # coarse dof lists per internal node: separator = its faces' dofs ++ the
+        # pressures eliminated there; boundary = boundary faces' dofs ++ live pressures
+        sptr_f, sdofs_f = _expand(G["sep_ptr"], G["sep"], per_face, cstart)
+        nsf = np.diff(sptr_f)
+        nsp = np.diff(G["pel_ptr"])
+        ns_all = nsf + nsp
+        sptr = np.concatenate([[0], np.cumsum(ns_all)])
+        node_s = np.repeat(np.arange(nI), ns_all)
+        within_s = np.arange(int(sptr[-1]), dtype=np.int64) - sptr[node_s]
+        isf_s = within_s < nsf[node_s]
+        sdofs = np.empty(int(sptr[-1]), dtype=np.int64)
+        sdofs[isf_s] = sdofs_f[sptr_f[node_s[isf_s]] + within_s[isf_s]]
+        nq_s = ~isf_s
+        sdofs[nq_s] = nfc + G["pel"][G["pel_ptr"][node_s[nq_s]] + within_s[nq_s] - nsf[node_s[nq_s]]]
         fptr, fdofs = _expand(G["bnd_ptr"], G["bnd"], per_face, cstart)
-        ns = np.diff(sptr)
+        ns = ns_all
         nbf = np.diff(fptr)
         npres = np.diff(G["pres_ptr"])
         nb = nbf + npres
@@ -281,21 +324,26 @@ class CoarseND:
             L = _Level()
             L.m = m = len(ids)
             s = ns[ids]
+            sf = nsf[ids]
             b = nb[ids]
-            L.S = S = _pad(int(s.max()), 32)
+            # pivot block [flux separator (padded to Sf) | eliminated pressures (to Sp)]
+            L.Sf = Sf = _pad(int(sf.max()), 32)
+            L.Sp = Sp = _pad(int(nsp[ids].max()), 32) if int(nsp[ids].max()) else 0
+            L.S = S = Sf + Sp
             L.B = _pad(int(b.max()), 2)
             L.nf = S + L.B
             sep_flat = sdofs[_ranges(sptr[ids], s)]
             bnd_flat = bdofs[_ranges(bptr[ids], b)]
             srow = np.repeat(np.arange(m), s)
             scol = _ranges(np.zeros(m, np.int64), s)
+            spos = np.where(scol < sf[srow], scol, Sf + scol - sf[srow])   # padded pivot position
             sep_idx = np.full((m, S), -1, dtype=np.int32)
-            sep_idx[srow, scol] = sep_flat
+            sep_idx[srow, spos] = sep_flat
             # parent fronts [sep | bnd] keyed by (parent, dof) -> position in the padded front
             brow = np.repeat(np.arange(m), b)
             bcol = _ranges(np.zeros(m, np.int64), b)
             fk = np.concatenate([srow * M + sep_flat, brow * M + bnd_flat])
-            fv = np.concatenate([scol, S + bcol])
+            fv = np.concatenate([spos, S + bcol])
             fo = np.argsort(fk, kind="stable")
             fk, fv = fk[fo], fv[fo]
             K = 1
@@ -307,7 +355,8 @@ class CoarseND:
                 valid = has[ids, slot]
                 leafc = (c < 0) & valid
                 subc = np.where(leafc, -c - 1, 0)
-                elen = np.where(leafc, nC[subc] + 1, nb[np.maximum(c, 0)])
+                # leaf export: its coarse dofs, then its pressure (none for the pinned 0)
+                elen = np.where(leafc, nC[subc] + (subc != 0), nb[np.maximum(c, 0)])
                 elen = np.where(valid, elen, 0)
                 erow = np.repeat(np.arange(m), elen)
                 ecol = _ranges(np.zeros(m, np.int64), elen)
@@ -336,6 +385,7 @@ class CoarseND:
             cmap = np.full((NS, m, K), -1, dtype=np.int32)
             for slot, (erow, ecol, v) in enumerate(maps):
                 cmap[slot, erow, ecol] = v
+            L._sf = sf
             L.sep_idx = t(sep_idx)
             L.cmap = t(cmap)
             L.ckind = t(ckind)
@@ -383,7 +433,7 @@ class CoarseND:
             L.ysize = int(sep_ptr[-1])
             L.csize = int(data_off[-1])
             lptr, lsrc = lists(L._sep_flat)
-            info = np.stack([s, b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off], axis=1).astype(np.int32)
+            info = np.stack([s, b, sep_ptr[:-1], bnd_ptr[:-1], L.cb_off, L._sf], axis=1).astype(np.int32)
             rf = rows_per_task(int((s + b).sum()))
             # backward rows are long (b): split a row over wpr warps when the
             # level has too few rows to fill the GPU
@@ -404,10 +454,7 @@ class CoarseND:
             L.n_ft, L.n_bt = len(ft), len(bt)
             L.smax = int(s.max())
             L.bmax = int(b.max())
-            del L._sep_flat, L._bnd_flat
-        # pressure gather lists (pressures 1..N-1; subdomain 0 is pinned)
-        pptr, psrc = lists(nfc + np.arange(1, N, dtype=np.int64))
-        self.pptr, self.psrc = t(pptr), t(psrc)
+            del L._sep_flat, L._bnd_flat, L._sf
 
     # --------------------------------------------------------------- numeric
 
@@ -420,17 +467,13 @@ class CoarseND:
             L.F = torch.empty(L.m * L.nf * L.nf, dtype=F64, device=self.dev)
             child = self.levels[li - 1] if li > 0 else None
             for slot in range(L.nslots):
-                nat.call("bddc_nd_assemble", L.m, L.S, L.B, L.nf, slot, L.K, _p(L.cmap),
+                nat.call("bddc_nd_assemble", L.m, L.S, L.Sf, L.B, L.nf, slot, L.K, _p(L.cmap),
                          _p(L.ckind), _p(L.sep_idx), _p(L.F),
                          _p(child.F) if child is not None else None,
                          child.S if child is not None else 0,
                          child.nf if child is not None else 1,
                          _p(Kc), _p(sub_rows_dev), _p(b0), self.maxC, st)
-            ws = torch.empty(lib.bddc_spd_inverse_workspace(L.S, L.m, 32) // 8 + 2, dtype=F64,
-                             device=self.dev)
-            nat.call("bddc_spd_inverse_batched", _p(L.F), L.S, L.nf, L.nf * L.nf, L.m, 32,
-                     _p(ws), _p(info), st)
-            del ws
+            self._pivot_inverse(L, info, st)
             L.X = torch.empty(L.m * L.B * L.S, dtype=F64, device=self.dev)
             F21 = L.F[L.S * L.nf:]
             nat.call("bddc_dgemm_batched", 0, 0, L.B, L.S, L.S, 1.0, _p(F21), L.nf,
@@ -446,22 +489,57 @@ class CoarseND:
         self.factored = True
         for L in self.levels:
             L.Fc = torch.empty(max(L.csize, 1), dtype=F64, device=self.dev)
-            nat.call("bddc_nd_compact", L.m, L.S, L.nf, L.B, _p(L.F), _p(L.X), _p(L.info),
+            nat.call("bddc_nd_compact", L.m, L.S, L.Sf, L.nf, L.B, _p(L.F), _p(L.X), _p(L.info),
                      _p(L.data_off), _p(L.Fc), st)
         # bytes streamed per solve: F11inv + X (forward) + X^T (backward)
         self.bytes = sum(L.csize * 8 for L in self.levels)
         return self.levels[-1]
 
+    def _pivot_inverse(self, L, info, st):
+        """F11^-1 in place for every front of a level.  Pivot blocks without
+        pressures are SPD; with eliminated pressures [[A, B^T], [B, C]] is
+        quasi-definite (A SPD, Sp = C - B A^-1 B^T negative definite):
+          A <- A^-1;  W = B A^-1;  C <- -(C - W B^T) -> inverse Ms = (-Sp)^-1;
+          B <- Ms W (= -Sp^-1 W);  A <- A^-1 - W^T B;  C <- -Ms;  mirror B^T."""
+        lib = nat.load()
+        m, nf, Sf, Sp = L.m, L.nf, L.Sf, L.Sp
+        sF = nf * nf
+        if Sp == 0:
+            ws = torch.empty(lib.bddc_spd_inverse_workspace(L.S, m, 32) // 8 + 2, dtype=F64,
+                             device=self.dev)
+            nat.call("bddc_spd_inverse_batched", _p(L.F), L.S, nf, sF, m, 32, _p(ws), _p(info), st)
+            return
+        ws = torch.empty(lib.bddc_spd_inverse_workspace(max(Sf, Sp), m, 32) // 8 + 2, dtype=F64,
+                         device=self.dev)
+        W = torch.empty(m * Sp * Sf, dtype=F64, device=self.dev)
+        A = L.F
+        Bb = L.F[Sf * nf:]            # pressure rows, flux columns
+        Cb = L.F[Sf * nf + Sf:]       # pressure block
+        nat.call("bddc_spd_inverse_batched", _p(A), Sf, nf, sF, m, 32, _p(ws), _p(info), st)
+        nat.call("bddc_dgemm_batched", 0, 0, Sp, Sf, Sf, 1.0, _p(Bb), nf, sF, _p(A), nf, sF,
+                 0.0, _p(W), Sf, Sp * Sf, m, 0, st)
+        nat.call("bddc_dgemm_batched", 0, 1, Sp, Sp, Sf, -1.0, _p(W), Sf, Sp * Sf, _p(Bb), nf, sF,
+                 1.0, _p(Cb), nf, sF, m, 0, st)
+        nat.call("bddc_nd_qd", 0, m, Sf, Sp, nf, _p(L.F), st)
+        nat.call("bddc_spd_inverse_batched", _p(Cb), Sp, nf, sF, m, 32, _p(ws), _p(info), st)
+        nat.call("bddc_dgemm_batched", 0, 0, Sp, Sf, Sp, 1.0, _p(Cb), nf, sF, _p(W), Sf, Sp * Sf,
+                 0.0, _p(Bb), nf, sF, m, 0, st)
+        nat.call("bddc_dgemm_batched", 1, 0, Sf, Sf, Sp, -1.0, _p(W), Sf, Sp * Sf, _p(Bb), nf, sF,
+                 1.0, _p(A), nf, sF, m, 0, st)
+        nat.call("bddc_nd_qd", 0, m, Sf, Sp, nf, _p(L.F), st)
+        nat.call("bddc_nd_qd", 1, m, Sf, Sp, nf, _p(L.F), st)
+
     def release_fronts(self):
-        """Drop the padded factorisation fronts once Pc has been read off the root."""
+        """Drop the padded factorisation fronts (the solves read the compact copies)."""
         for L in self.levels:
             L.F = None
             L.X = None
 
-    def solve(self, r, x, Pcinv, npc):
+    def solve(self, r, x):
         """Pinned coarse solve on the combined vector [flux | pressures] (coarse.py:208-215).
 
-        r, x: length nfc + N.  r is read-only; x[nfc] (subdomain 0) is pinned to 0.
+        r, x: length nfc + N.  r is read-only; x[nfc] (subdomain 0's pinned
+        pressure) is not written.
         """
         st = _stream()
         ys, cb = self._bufs()
@@ -469,8 +547,6 @@ class CoarseND:
             nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
                      _p(cb), st)
-        nat.call("bddc_nd_pressure", self.N, self.nfc, npc, _p(self.pptr), _p(self.psrc), _p(cb),
-                 _p(Pcinv), _p(r), _p(self._prhs), _p(x), st)
         for li in range(len(self.levels) - 1, -1, -1):
             L = self.levels[li]
             nat.call("bddc_nd_bwd", L.n_bt, L.bmax, L.wpr, _p(L.btasks), _p(L.info), _p(L.data_off),
@@ -481,6 +557,5 @@ class CoarseND:
             ys = [torch.empty(max(L.ysize, 1), dtype=F64, device=self.dev) for L in self.levels]
             cb = torch.empty(self.cb_total, dtype=F64, device=self.dev)
             self._yb = (ys, cb)
-            self._prhs = torch.empty(max(self.N, 1), dtype=F64, device=self.dev)
             self._rs = torch.empty(max([L.ysize for L in self.levels] + [1]), dtype=F64, device=self.dev)
         return self._yb

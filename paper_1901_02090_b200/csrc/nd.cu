@@ -6,7 +6,7 @@ namespace {
 
 // F = 0 with identity on the padded separator diagonal (slot == -1), or
 // extend-add of child `slot` of every node into its front.
-__global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K, const int* __restrict__ cmap,
+__global__ void nd_assemble_kernel(int m, int S, int Sf, int B, int nf, int slot, int K, const int* __restrict__ cmap,
                                    const int* __restrict__ ckind, const int* __restrict__ sep_idx,
                                    double* __restrict__ F, const double* __restrict__ Fc, int Sc, int nfc,
                                    const double* __restrict__ Kc, const int* __restrict__ sub_rows,
@@ -18,7 +18,9 @@ __global__ void nd_assemble_kernel(int m, int S, int B, int nf, int slot, int K,
          e += (long long)gridDim.x * blockDim.x) {
       int r = (int)(e / nf), c = (int)(e % nf);
       double v = 0.0;
-      if (r == c && r < S && sep_idx[(size_t)q * S + r] < 0) v = 1.0;
+      // padding of the pivot block: +1 on the flux part, -1 on the pressure part
+      // (keeps the flux block SPD and the pressure Schur complement negative definite)
+      if (r == c && r < S && sep_idx[(size_t)q * S + r] < 0) v = (r < Sf) ? 1.0 : -1.0;
       Fq[e] = v;
     }
     return;
@@ -95,7 +97,7 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
   extern __shared__ double rsm[];
   pdl_trigger();
   const int q = tasks[3 * blockIdx.x], row0 = tasks[3 * blockIdx.x + 1], row1 = tasks[3 * blockIdx.x + 2];
-  const int s = info[5 * q], sp = info[5 * q + 2], cbo = info[5 * q + 4];
+  const int s = info[6 * q], sp = info[6 * q + 2], cbo = info[6 * q + 4];
   const double* base = Fc + data_off[q];
   pdl_wait();
   if (lpe > 0) {
@@ -139,7 +141,7 @@ __global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restri
   __shared__ double part[8];
   pdl_trigger();
   const int q = tasks[3 * blockIdx.x], k0 = tasks[3 * blockIdx.x + 1], k1 = tasks[3 * blockIdx.x + 2];
-  const int s = info[5 * q], b = info[5 * q + 1], sp = info[5 * q + 2], bp = info[5 * q + 3];
+  const int s = info[6 * q], b = info[6 * q + 1], sp = info[6 * q + 2], bp = info[6 * q + 3];
   pdl_wait();
   for (int m = threadIdx.x; m < b; m += blockDim.x) xb[m] = x[bnd_flat[bp + m]];
   __syncthreads();
@@ -178,120 +180,52 @@ __global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restri
 }
 
 // Copy the padded fronts' F11inv and X blocks into the compact layout
-// (F11inv s x s, X b x s, X^T s x b).
-__global__ void nd_compact_kernel(int S, int nf, int B, const double* __restrict__ F, const double* __restrict__ X,
-                                  const int* __restrict__ info, const long long* __restrict__ data_off,
-                                  double* __restrict__ Fc) {
+// (F11inv s x s, X b x s, X^T s x b); live pivot entry k sits at padded position
+// k (flux, k < s_f) or Sf + k - s_f (eliminated pressure).
+__global__ void nd_compact_kernel(int S, int Sf, int nf, int B, const double* __restrict__ F,
+                                  const double* __restrict__ X, const int* __restrict__ info,
+                                  const long long* __restrict__ data_off, double* __restrict__ Fc) {
   const int q = blockIdx.y;
-  const int s = info[5 * q], b = info[5 * q + 1];
+  const int s = info[6 * q], b = info[6 * q + 1], sf = info[6 * q + 5];
   double* out = Fc + data_off[q];
   const long long ss = (long long)s * s, bs = (long long)b * s;
   const long long tot = ss + 2 * bs;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
     if (e < ss) {
       int rr = (int)(e / s), cc = (int)(e % s);
+      rr = rr < sf ? rr : Sf + rr - sf;
+      cc = cc < sf ? cc : Sf + cc - sf;
       out[e] = F[(size_t)q * nf * nf + (size_t)rr * nf + cc];
     } else if (e < ss + bs) {
       long long e2 = e - ss;
       int j = (int)(e2 / s), cc = (int)(e2 % s);
+      cc = cc < sf ? cc : Sf + cc - sf;
       out[e] = X[(size_t)q * B * S + (size_t)j * S + cc];
     } else {
       long long e2 = e - ss - bs;
       int k = (int)(e2 / b), j = (int)(e2 % b);
+      k = k < sf ? k : Sf + k - sf;
       out[e] = X[(size_t)q * B * S + (size_t)j * S + k];
     }
   }
 }
 
-// Root pressure block of the pinned coarse system: rp[i] = r_p[i] - contributions
-// (i >= 1), then x_p = -Pc^{-1} rp (the root update block is -Pc); x_p[0] = 0.
-__global__ void nd_pressure_gather_kernel(int N, int nfc, const int* __restrict__ pptr, const int* __restrict__ psrc,
-                                          const double* __restrict__ cbuf, const double* __restrict__ r,
-                                          double* __restrict__ rp) {
-  pdl_trigger();
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  pdl_wait();
-  if (i >= N - 1) return;
-  double acc = 0.0;
-  for (int p = pptr[i]; p < pptr[i + 1]; ++p) acc += cbuf[psrc[p]];
-  rp[i] = r[nfc + 1 + i] - acc;
-}
-
-__global__ void nd_pressure_gemv_kernel(int N, int nfc, int npc, const double* __restrict__ Pcinv,
-                                        const double* __restrict__ rp, double* __restrict__ x) {
-  pdl_trigger();
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  pdl_wait();
-  if (row == 0 && lane == 0) x[nfc] = 0.0;
-  if (row >= N - 1) return;
-  const double* mr = Pcinv + (size_t)row * npc;
-  double a[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) a[u] = 0.0;
-  const int n = N - 1;
-  int c = lane;
-  for (; c + 224 < n; c += 256) {
-    double m[8], v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      m[u] = __ldg(mr + c + 32 * u);
-      v[u] = rp[c + 32 * u];
+// Quasi-definite pivot block helpers (batched over the m fronts of a level):
+// mode 0: C <- -C on the pressure block F[Sf:S, Sf:S];
+// mode 1: F[0:Sf, Sf:S] <- F[Sf:S, 0:Sf]^T (mirror the off-diagonal block).
+__global__ void nd_qd_kernel(int mode, int Sf, int Sp, int nf, double* __restrict__ F) {
+  double* Fq = F + (size_t)blockIdx.y * nf * nf;
+  const long long tot = mode == 0 ? (long long)Sp * Sp : (long long)Sf * Sp;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    if (mode == 0) {
+      const int r = (int)(e / Sp), c = (int)(e % Sp);
+      double* p = Fq + (size_t)(Sf + r) * nf + Sf + c;
+      *p = -*p;
+    } else {
+      const int r = (int)(e / Sp), c = (int)(e % Sp);   // r < Sf, c < Sp
+      Fq[(size_t)r * nf + Sf + c] = Fq[(size_t)(Sf + c) * nf + r];
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
   }
-#pragma unroll
-  for (int u = 0; u < 8; ++u)
-    if (c + 32 * u < n) a[u] += __ldg(mr + c + 32 * u) * rp[c + 32 * u];
-  double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) x[nfc + 1 + row] = -acc;
-}
-
-// Pc[(i-1),(j-1)] = -U_root[i][j] (i, j >= 1): the pinned pressure Schur complement;
-// identity beyond N-1.
-__global__ void nd_extract_pc_kernel(const double* __restrict__ F, int nf, int S, int N, double* __restrict__ Pc,
-                                     int npc) {
-  long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)npc * npc) return;
-  int r = (int)(e / npc), c = (int)(e % npc);
-  double v;
-  if (r < N - 1 && c < N - 1) v = -F[(size_t)(S + 1 + r) * nf + S + 1 + c];
-  else v = (r == c) ? 1.0 : 0.0;
-  Pc[e] = v;
-}
-
-// out[(i-1) + j*ldo] = sum_r b0[i][r] Y[g_r + j*ldy]   (i >= 1); warp per (i, j)
-__global__ void b0_apply_kernel(int N, int maxC, const int* __restrict__ sub_rows, const double* __restrict__ b0,
-                                const double* __restrict__ Y, int ldy, int nrhs, double* __restrict__ out, int ldo) {
-  long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= (long long)(N - 1) * nrhs) return;
-  int i = 1 + (int)(w % (N - 1)), j = (int)(w / (N - 1));
-  double s = 0.0;
-  for (int r = lane; r < maxC; r += 32) {
-    int g = sub_rows[((size_t)i * maxC + r) * 4];
-    if (g >= 0) s += b0[(size_t)i * maxC + r] * Y[(size_t)g + (size_t)j * ldy];
-  }
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[(size_t)(i - 1) + (size_t)j * ldo] = s;
-}
-
-// r[g + j*ldr] += alpha * (b0[lo] z[i_lo-1] + b0[hi] z[i_hi-1])   (owners with i >= 1)
-__global__ void b0t_apply_kernel(int nfc, int maxC, const int* __restrict__ cown, const double* __restrict__ b0,
-                                 const double* __restrict__ z, int ldz, int nrhs, double alpha, double* __restrict__ r,
-                                 int ldr) {
-  long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (long long)nfc * nrhs) return;
-  int g = (int)(e % nfc), j = (int)(e / nfc);
-  double s = 0.0;
-  for (int w = 0; w < 2; ++w) {
-    int bi = cown[2 * g + w];
-    int i = bi / maxC;
-    if (i >= 1) s += b0[bi] * z[(size_t)(i - 1) + (size_t)j * ldz];
-  }
-  r[(size_t)g + (size_t)j * ldr] += alpha * s;
 }
 
 __global__ void fill_kernel(long long n, double v, double* __restrict__ a) {
@@ -301,20 +235,20 @@ __global__ void fill_kernel(long long n, double v, double* __restrict__ a) {
 
 }  // namespace
 
-extern "C" int bddc_nd_assemble(int m, int S, int B, int nf, int slot, int K, const int* cmap, const int* ckind,
+extern "C" int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, int K, const int* cmap, const int* ckind,
                                 const int* sep_idx, double* F, const double* Fc, int Sc, int nfc, const double* Kc,
                                 const int* sub_rows, const double* b0, int maxC, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (slot < 0 || slot == 0) {
     long long tot = (long long)nf * nf;
     dim3 g0((unsigned)imin((int)((tot + 255) / 256), 1024), m);
-    nd_assemble_kernel<<<g0, 256, 0, s>>>(m, S, B, nf, -1, K, cmap, ckind, sep_idx, F, Fc, Sc, nfc, Kc, sub_rows,
+    nd_assemble_kernel<<<g0, 256, 0, s>>>(m, S, Sf, B, nf, -1, K, cmap, ckind, sep_idx, F, Fc, Sc, nfc, Kc, sub_rows,
                                           b0, maxC);
     LAUNCH_OK();
   }
   long long tot = (long long)K * K;
   dim3 g((unsigned)imin((int)((tot + 255) / 256), 1024), m);
-  nd_assemble_kernel<<<g, 256, 0, s>>>(m, S, B, nf, slot, K, cmap, ckind, sep_idx, F, Fc, Sc, nfc, Kc, sub_rows, b0,
+  nd_assemble_kernel<<<g, 256, 0, s>>>(m, S, Sf, B, nf, slot, K, cmap, ckind, sep_idx, F, Fc, Sc, nfc, Kc, sub_rows, b0,
                                        maxC);
   LAUNCH_OK();
   return 0;
@@ -339,19 +273,6 @@ extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, co
   return 0;
 }
 
-extern "C" int bddc_nd_pressure(int N, int nfc, int npc, const int* pptr, const int* psrc, const double* cbuf,
-                                const double* Pcinv, const double* r, double* rp, double* x, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
-  if (N < 2) {
-    if (N == 1) CUDA_OK(cudaMemsetAsync(x + nfc, 0, sizeof(double), s));
-    return 0;
-  }
-  PDL_LAUNCH(nd_pressure_gather_kernel, dim3((N - 1 + 255) / 256), dim3(256), 0, s, N, nfc, pptr, psrc, cbuf, r, rp);
-  PDL_LAUNCH(nd_pressure_gemv_kernel, dim3((N - 1 + 7) / 8 + 1), dim3(256), 0, s, N, nfc, npc, Pcinv,
-             (const double*)rp, x);
-  return 0;
-}
-
 extern "C" int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
                            const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
                            const double* ybuf, double* x, void* stream) {
@@ -364,37 +285,18 @@ extern "C" int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, con
   return 0;
 }
 
-extern "C" int bddc_nd_compact(int m, int S, int nf, int B, const double* F, const double* X, const int* info,
-                               const long long* data_off, double* Fc, void* stream) {
+extern "C" int bddc_nd_compact(int m, int S, int Sf, int nf, int B, const double* F, const double* X,
+                               const int* info, const long long* data_off, double* Fc, void* stream) {
   dim3 g(64, m);
-  nd_compact_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(S, nf, B, F, X, info, data_off, Fc);
+  nd_compact_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(S, Sf, nf, B, F, X, info, data_off, Fc);
   LAUNCH_OK();
   return 0;
 }
 
-extern "C" int bddc_nd_extract_pc(const double* F, int nf, int S, int N, double* Pc, int npc, void* stream) {
-  long long tot = (long long)npc * npc;
-  nd_extract_pc_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(F, nf, S, N, Pc, npc);
-  LAUNCH_OK();
-  return 0;
-}
-
-extern "C" int bddc_b0_apply(int N, int maxC, const int* sub_rows, const double* b0, const double* Y, int ldy,
-                             int nrhs, double* out, int ldo, void* stream) {
-  if (N < 2) return 0;
-  long long tot = (long long)(N - 1) * nrhs * 32;
-  b0_apply_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(N, maxC, sub_rows, b0, Y, ldy,
-                                                                                    nrhs, out, ldo);
-  LAUNCH_OK();
-  return 0;
-}
-
-extern "C" int bddc_b0t_apply(int nfc, int maxC, const int* cown, const double* b0, const double* z, int ldz, int nrhs,
-                              double alpha, double* r, int ldr, void* stream) {
-  if (nfc <= 0) return 0;
-  long long tot = (long long)nfc * nrhs;
-  b0t_apply_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(nfc, maxC, cown, b0, z, ldz, nrhs,
-                                                                                     alpha, r, ldr);
+extern "C" int bddc_nd_qd(int mode, int m, int Sf, int Sp, int nf, double* F, void* stream) {
+  if (m <= 0 || Sp <= 0) return 0;
+  dim3 g(64, m);
+  nd_qd_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(mode, Sf, Sp, nf, F);
   LAUNCH_OK();
   return 0;
 }

@@ -326,13 +326,10 @@ class BddcSetup:
         nfc = self.n_flux_coarse
         self.nfc = nfc
         self.npad = _pad(max(nfc, 1), 64)
-        self.npc = _pad(max(N - 1, 1), 64)
         self.nd = None
-        self.d_Pcinv = None
         if nfc:
             self.nd = CoarseND(dec, per_face, cstart, self.sub_rows, self.nC, maxC, dev)
-            root = self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
-            self._build_pressure_schur(root)
+            self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
             self.nd.release_fronts()
         main.wait_stream(side)   # T_i done; its workspaces may go now
         del Ct, Y, E, gam, ws, Sinv, dims, cl_args, self.d_S, self.d_T
@@ -497,27 +494,9 @@ class BddcSetup:
         except Exception:
             pass
 
-    def _build_pressure_schur(self, root):
-        """Pc = B0[1:] S_Pi^-1 B0[1:]^T (subdomain 0 pinned, coarse.py:192-194), inverted.
-
-        Read off the root front's update matrix (= -B0 S_Pi^-1 B0^T over all pressures).
-        """
-        N, npc, st = self.N, self.npc, _stream()
-        dev = self.dev
-        Pc = torch.empty(npc * npc, dtype=F64, device=dev)
-        nat.call("bddc_nd_extract_pc", _p(root.F), root.nf, root.S, N, _p(Pc), npc, st)
-        info = torch.zeros(1, dtype=I32, device=dev)
-        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(npc, 1, 64) // 8 + 2,
-                         dtype=F64, device=dev)
-        nat.call("bddc_spd_inverse_batched", _p(Pc), npc, npc, 0, 1, 32, _p(ws), _p(info), st)
-        if int(info.item()):
-            raise ConfigurationError(
-                "coarse problem singular; initial constraints do not cover all faces")
-        self.d_Pcinv = Pc
-
     def _coarse_solve(self):
         """Pinned coarse solve w_xc = K0^-1 w_rc on [flux | pressures] (coarse.py:208-215)."""
-        self.nd.solve(self.w_rc, self.w_xc, self.d_Pcinv, self.npc)
+        self.nd.solve(self.w_rc, self.w_xc)
 
     # ----------------------------------------- interface operator (device)
 

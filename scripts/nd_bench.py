@@ -38,7 +38,7 @@ def gtime(fn, reps=50):
     return e0.elapsed_time(e1) / reps * 1000
 
 
-print(f"nd solve (graph) {gtime(lambda: nd.solve(r, x, st.d_Pcinv, st.npc)):.1f} us, factor MB {nd.bytes / 1e6:.1f}")
+print(f"nd solve (graph) {gtime(lambda: nd.solve(r, x)):.1f} us, factor MB {nd.bytes / 1e6:.1f}")
 ys, cb = nd._bufs()
 for li, L in enumerate(nd.levels):
     f = lambda: nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),

@@ -25,10 +25,13 @@ def _tables(counts, splits, seed):
 
 @pytest.mark.parametrize("counts,splits", [((12, 12, 12), (2, 3, 4)), ((9, 9, 6), (3, 3, 3)),
                                            ((16, 12), (4, 3))])
-def test_separators_partition_coarse_flux_dofs(counts, splits):
+def test_pivots_partition_coarse_dofs(counts, splits):
+    """Every flux coarse dof and every pressure but the pinned one is eliminated
+    exactly once (pressures at the node that eliminates their subdomain's last face)."""
     dec, per_face, fake, nd = _tables(counts, splits, 1)
     seps = np.concatenate([L.sep_flat.numpy()[:L.ysize] for L in nd.levels])
-    assert np.array_equal(np.sort(seps), np.arange(nd.nfc))
+    want = np.concatenate([np.arange(nd.nfc), nd.nfc + np.arange(1, dec.n_subdomains)])
+    assert np.array_equal(np.sort(seps), want)
 
 
 @pytest.mark.parametrize("counts,splits", [((12, 12, 12), (2, 3, 4)), ((9, 9, 6), (3, 3, 3))])
@@ -45,10 +48,10 @@ def test_child_maps_and_gather_lists(counts, splits):
                 assert np.all(v < L.nf)
         nb_total += int(L.b.sum())
     # every boundary entry of every node is one contribution to exactly one
-    # separator entry or pressure (pressure of subdomain 0 is pinned: not listed)
-    nlist = sum(int(L.lptr[-1]) for L in nd.levels) + int(nd.pptr[-1])
-    pinned = sum(int(np.sum(L.bnd_flat.numpy()[:int(L.b.sum())] == nd.nfc)) for L in nd.levels)
-    assert nlist + pinned == nb_total
+    # pivot entry of an ancestor (the pinned pressure appears nowhere)
+    nlist = sum(int(L.lptr[-1]) for L in nd.levels)
+    assert nlist == nb_total
+    assert not any(np.any(L.bnd_flat.numpy()[:int(L.b.sum())] == nd.nfc) for L in nd.levels)
 
 
 def test_tree_levels_parent_above_child():
