@@ -48,6 +48,14 @@ typedef struct bddc_geom {
   int maxP;                        /* padded cells per subdomain (multiple of 64) */
   int maxL;                        /* max strip width */
   int maxF;                        /* max dofs on one box face */
+  /* mode B (Dirichlet pressure on both ends of one axis; not in the reference):
+   * dir_axis = that axis or -1 (mode A).  The boundary faces of dir_axis are
+   * flux dofs numbered after the n_flux_int interior ones: low end, then high
+   * end, n_bt faces each, x-fastest over the transverse axes; n_flux counts
+   * them (n_flux = n_flux_int + 2 n_bt). */
+  int dir_axis;
+  int n_flux_int;
+  int n_bt;
 } bddc_geom;
 
 const char* bddc_last_error(void);

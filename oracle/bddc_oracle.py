@@ -883,6 +883,53 @@ def direct_solve(mesh, k, f):
     return u, p - p.mean()
 
 
+def dirichlet_faces(mesh, axis):
+    """Mode B: per-cell (low, high) `axis`-face dofs with the two boundary ends as
+    dofs n_flux + t (low end) and n_flux + nt + t (high end), t = x-fastest index
+    over the transverse axes.  Extension, not in the reference."""
+    lo, hi = mesh.cell_face_dofs(axis)
+    ca = mesh.coords[:, axis]
+    nt = mesh.n_cells // mesh.counts[axis]
+    lo = lo.copy(); hi = hi.copy()
+    lo[ca == 0] = mesh.n_flux + np.arange(nt)
+    hi[ca == mesh.counts[axis] - 1] = mesh.n_flux + nt + np.arange(nt)
+    return lo, hi, nt
+
+
+def direct_solve_dirichlet(mesh, k, f, axis, p_low, p_high):
+    """Monolithic sparse solve of [[A, B^T], [B, 0]] (u, p) = (g, f) with Dirichlet
+    pressure p_low / p_high on the two ends of `axis` (mode B).  A and B are
+    assembled from the element blocks c[[2,1],[1,2]] and B[cell, low] = +1,
+    B[cell, high] = -1 (grid.py:204-324) over all faces of the cells, boundary
+    faces of `axis` included; g = +p_low on low-end faces, -p_high on high-end
+    ones (the weak form -(p, div v) + <p_D, v.n>).  No pressure pin."""
+    lo_d, hi_d, nt = dirichlet_faces(mesh, axis)
+    nu = mesh.n_flux + 2 * nt
+    rows, cols, vals, brow, bcol, bval = [], [], [], [], [], []
+    cells = np.arange(mesh.n_cells)
+    for a in range(mesh.dim):
+        lo, hi = (lo_d, hi_d) if a == axis else mesh.cell_face_dofs(a)
+        c = mesh.sizes[a] ** 2 / (6.0 * mesh.vol) / k[:, a]
+        for d, o in ((lo, hi), (hi, lo)):
+            m = d >= 0
+            rows.append(d[m]); cols.append(d[m]); vals.append(2.0 * c[m])
+            mo = m & (o >= 0)
+            rows.append(d[mo]); cols.append(o[mo]); vals.append(c[mo])
+        for d, sgn in ((lo, 1.0), (hi, -1.0)):
+            m = d >= 0
+            brow.append(cells[m]); bcol.append(d[m]); bval.append(np.full(int(m.sum()), sgn))
+    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(nu, nu)).tocsr()
+    B = sp.coo_matrix((np.concatenate(bval), (np.concatenate(brow), np.concatenate(bcol))),
+                      shape=(mesh.n_cells, nu)).tocsr()
+    g = np.zeros(nu)
+    g[mesh.n_flux:mesh.n_flux + nt] = p_low
+    g[mesh.n_flux + nt:] = -p_high
+    K = sp.bmat([[A, B.T], [B, None]], format="csc")
+    sol = spla.spsolve(K, np.concatenate([g, f]))
+    return sol[:nu], sol[nu:]
+
+
 def run(counts, sizes, k, splits, cfg, wells=None):
     """Convenience: build + solve in mode A (wells at cells 0, n-1)."""
     mesh = Mesh(counts, sizes)

@@ -59,6 +59,7 @@ class Geom(C.Structure):
         ("n_gamma", C.c_int), ("n_faces", C.c_int),
         ("maxG", C.c_int), ("maxP", C.c_int), ("maxL", C.c_int),
         ("maxF", C.c_int),
+        ("dir_axis", C.c_int), ("n_flux_int", C.c_int), ("n_bt", C.c_int),
     ]
 
 

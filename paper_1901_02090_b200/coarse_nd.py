@@ -56,12 +56,22 @@ class _Level:
     pass
 
 
-def nd_geometry(dec):
+def _has_p(dec, has_p):
+    """Subdomains with a coarse pressure: all but the pinned subdomain 0 (mode A,
+    coarse.py:192-194), or the floating ones (mode B: no pin)."""
+    if has_p is None:
+        has_p = np.arange(dec.n_subdomains) != 0
+    return np.asarray(has_p, dtype=bool)
+
+
+def nd_geometry(dec, has_p=None):
     """Nested-dissection tree of the subdomain grid in face ids (cached on `dec`).
 
     Node: dict(leaf, depth, sub | sep (face ids), bnd (face ids), pres (subdomain ids), ch).
     """
-    cached = getattr(dec, "_nd_geometry", None)
+    has_p = _has_p(dec, has_p)
+    cache = dec.__dict__.setdefault("_nd_geometry", {})
+    cached = cache.get(has_p.tobytes())
     if cached is not None:
         return cached
     S3 = dec.S3
@@ -114,18 +124,19 @@ def nd_geometry(dec):
     if dec.n_subdomains > 1:
         rec((0, 0, 0), tuple(S3), 0)
     nodes = _contract(nodes, ND_MERGE)
-    _assign_pressures(nodes, dec)
-    dec._nd_geometry = nodes
+    _assign_pressures(nodes, dec, has_p)
+    cache[has_p.tobytes()] = nodes
     return nodes
 
 
-def _assign_pressures(nodes, dec):
+def _assign_pressures(nodes, dec, has_p):
     """Subdomain pressures are eliminated inside the tree, not carried to the root:
     p_i couples only to i's coarse flux dofs, so once the last face of i has been
     eliminated (at the highest node H_i whose separator holds a face of i) p_i is
     eliminated too, in H_i's pivot block (quasi-definite: the flux block is SPD,
-    the pressure Schur complement negative definite).  Subdomain 0's pressure is
-    pinned (coarse.py:192-194) and appears nowhere.  Per internal node:
+    the pressure Schur complement negative definite).  Subdomains without a
+    coarse pressure (`has_p` false: the pinned subdomain 0, coarse.py:192-194, or
+    in mode B every subdomain on a Dirichlet end) appear nowhere.  Per internal node:
     pres_elim = pressures eliminated there, pres = pressures of its box still
     live above it (its boundary)."""
     if not nodes:
@@ -145,7 +156,7 @@ def _assign_pressures(nodes, dec):
     hdepth = np.array([nodes[int(h)]["depth"] if h >= 0 else -1 for h in H])
     for k in internal:
         box = nodes[k]["pres"]
-        box = box[box != 0]
+        box = box[has_p[box]]
         nodes[k]["pres_elim"] = box[H[box] == k]
         nodes[k]["pres"] = box[hdepth[box] < nodes[k]["depth"]]
 
@@ -195,12 +206,14 @@ def _contract(nodes, c):
     return out
 
 
-def nd_geometry_flat(dec):
+def nd_geometry_flat(dec, has_p=None):
     """Flat arrays of the internal nodes of nd_geometry (cached on `dec`)."""
-    cached = getattr(dec, "_nd_geometry_flat", None)
+    has_p = _has_p(dec, has_p)
+    cache = dec.__dict__.setdefault("_nd_geometry_flat", {})
+    cached = cache.get(has_p.tobytes())
     if cached is not None:
         return cached
-    geo = nd_geometry(dec)
+    geo = nd_geometry(dec, has_p)
     internal = [k for k, n in enumerate(geo) if not n["leaf"]]
     gpos = {k: i for i, k in enumerate(internal)}
 
@@ -226,7 +239,7 @@ def nd_geometry_flat(dec):
             ch[i, s_] = gpos[c] if not geo[c]["leaf"] else -(1 + geo[c]["sub"])
     F["ch"] = ch
     F["nch"] = nch
-    dec._nd_geometry_flat = F
+    cache[has_p.tobytes()] = F
     return F
 
 
@@ -252,9 +265,12 @@ def _ranges(lo, cnt):
 class CoarseND:
     """Symbolic analysis (host, index tables only) + numeric factorisation (device)."""
 
-    def __init__(self, dec, per_face, cstart, sub_rows, nC, maxC, dev):
-        """Symbolic analysis, vectorised over all tree nodes (numpy, no per-node loops)."""
+    def __init__(self, dec, per_face, cstart, sub_rows, nC, maxC, dev, has_p=None):
+        """Symbolic analysis, vectorised over all tree nodes (numpy, no per-node loops).
+        has_p: subdomains carrying a coarse pressure (default: all but subdomain 0)."""
         self.dev = dev
+        has_p = _has_p(dec, has_p)
+        self.has_p = has_p
         N = dec.n_subdomains
         self.N = N
         nfaces = dec.n_faces
@@ -269,7 +285,7 @@ class CoarseND:
         if not (N > 1 and nfc):
             self.cb_total = 1
             return
-        G = nd_geometry_flat(dec)
+        G = nd_geometry_flat(dec, has_p)
         nI = len(G["internal"])
         # coarse dof lists per internal node: separator = its faces' dofs ++ the
         # pressures eliminated there; boundary = boundary faces' dofs ++ live pressures
@@ -356,7 +372,7 @@ class CoarseND:
                 leafc = (c < 0) & valid
                 subc = np.where(leafc, -c - 1, 0)
                 # leaf export: its coarse dofs, then its pressure (none for the pinned 0)
-                elen = np.where(leafc, nC[subc] + (subc != 0), nb[np.maximum(c, 0)])
+                elen = np.where(leafc, nC[subc] + has_p[subc], nb[np.maximum(c, 0)])
                 elen = np.where(valid, elen, 0)
                 erow = np.repeat(np.arange(m), elen)
                 ecol = _ranges(np.zeros(m, np.int64), elen)

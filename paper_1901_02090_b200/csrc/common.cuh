@@ -222,6 +222,29 @@ __device__ __forceinline__ void trans_axes(int a, int& t1, int& t2) {
   t2 = (a == 2) ? 1 : 2;
 }
 
+// Mode B: dof of the Dirichlet boundary face at end `side` (0 low, 1 high) of
+// axis G.dir_axis on the grid line through global cell coordinates gc.
+__device__ __forceinline__ int bnd_dof(const bddc_geom& G, int side, const int gc[3]) {
+  int t1, t2;
+  trans_axes(G.dir_axis, t1, t2);
+  return G.n_flux_int + side * G.n_bt + gc[t1] + G.n[t1] * gc[t2];
+}
+
+// Mode B: does the box's line along axis a end on a Dirichlet face (lo / hi)?
+__device__ __forceinline__ void line_open(const bddc_geom& G, const Box& b, int a, int& lo, int& hi) {
+  lo = (a == G.dir_axis && b.o[a] == 0);
+  hi = (a == G.dir_axis && b.o[a] + b.L[a] == G.n[a]);
+}
+
+// Floating subdomain: no Dirichlet face, so its interior pressure block is
+// singular (null space 1) and it carries a balance constraint / coarse pressure.
+__device__ __forceinline__ bool sub_floating(const bddc_geom& G, const Box& b) {
+  int lo, hi;
+  if (G.dir_axis < 0) return true;
+  line_open(G, b, G.dir_axis, lo, hi);
+  return !(lo || hi);
+}
+
 // Line geometry: line index q of axis a in a box -> local coords of the
 // transverse axes.  Line index ordering is x-fastest over the transverse
 // axes (matches the sorted global order of the dofs on one box face).

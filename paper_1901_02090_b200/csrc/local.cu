@@ -48,35 +48,42 @@ __device__ __forceinline__ int line_cell_global(const bddc_geom& G, const Box& b
   return cell_id(G, b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]);
 }
 
-// Global interior dof of interior face j (between line cells j and j+1).
-__device__ __forceinline__ int line_face_dof(const bddc_geom& G, const Box& b, int a, int line, int j) {
+// Interior dofs of a line of L cells: the faces at positions p = 1-lo .. L-1+hi
+// (position p separates cells p-1 and p; lo / hi = 1 when that end is a mode-B
+// Dirichlet face, which is then an interior dof too), m = L-1+lo+hi of them,
+// dof j <-> position p = j+1-lo.  Cell k has low face j = k-1+lo, high k+lo.
+
+// Global dof of line dof j.
+__device__ __forceinline__ int line_face_dof(const bddc_geom& G, const Box& b, int a, int line, int j, int lo) {
   int c[3];
   line_coords(b, a, line, c);
-  c[a] = j + 1;
-  return face_dof(G, a, b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]);
+  const int p = j + 1 - lo;
+  int gc[3] = {b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]};
+  if (p == 0) return bnd_dof(G, 0, gc);
+  if (p == b.L[a]) return bnd_dof(G, 1, gc);
+  gc[a] += p;
+  return face_dof(G, a, gc[0], gc[1], gc[2]);
 }
 
-// Thomas factorisation of the line tridiagonal T (order m = L-1):
-// diag d_j = 2c_j + 2c_{j+1}, off e_j = c_{j+1}.  Stores the modified
-// super-diagonal cp and pivots piv.
-__device__ __forceinline__ void line_factor(const double* c, int L, double* cp, double* piv) {
-  int m = L - 1;
+// Thomas factorisation of the line tridiagonal T (order m = L-1+lo+hi):
+// T[j][j] = 2c_{p-1} + 2c_p (cells that exist), T[j][j+1] = c_p, p = j+1-lo.
+// Stores the modified super-diagonal cp and pivots piv.
+__device__ __forceinline__ void line_factor(const double* c, int L, int lo, int hi, double* cp, double* piv) {
+  const int m = L - 1 + lo + hi;
   for (int j = 0; j < m; ++j) {
-    double d = 2.0 * c[j] + 2.0 * c[j + 1];
-    double sub = (j > 0) ? c[j] : 0.0;  // T[j][j-1] = c_j
-    double pv = d - ((j > 0) ? sub * cp[j - 1] : 0.0);
+    const int p = j + 1 - lo;
+    double d = (p >= 1 ? 2.0 * c[p - 1] : 0.0) + (p <= L - 1 ? 2.0 * c[p] : 0.0);
+    double pv = d - ((j > 0) ? c[p - 1] * cp[j - 1] : 0.0);  // T[j][j-1] = c_{p-1}
     piv[j] = pv;
-    cp[j] = (j + 1 < m) ? c[j + 1] / pv : 0.0;  // T[j][j+1] = c_{j+1}
+    cp[j] = (j + 1 < m) ? c[p] / pv : 0.0;
   }
 }
 
 // Solve T x = r in place with a factored line.
-__device__ __forceinline__ void line_solve(const double* c, int L, const double* cp, const double* piv, double* r) {
-  int m = L - 1;
-  for (int j = 0; j < m; ++j) {
-    double sub = (j > 0) ? c[j] : 0.0;
-    r[j] = (r[j] - ((j > 0) ? sub * r[j - 1] : 0.0)) / piv[j];
-  }
+__device__ __forceinline__ void line_solve(const double* c, int L, int lo, int hi, const double* cp,
+                                           const double* piv, double* r) {
+  const int m = L - 1 + lo + hi;
+  for (int j = 0; j < m; ++j) r[j] = (r[j] - ((j > 0) ? c[j - lo] * r[j - 1] : 0.0)) / piv[j];
   for (int j = m - 2; j >= 0; --j) r[j] -= cp[j] * r[j + 1];
 }
 
@@ -132,14 +139,16 @@ __global__ void rescale_kernel(bddc_geom G, const double* __restrict__ coef, dou
     for (int e = threadIdx.x; e < nf; e += blockDim.x) {
       int line = e / (L + 1), j = e % (L + 1);
       int fc = b.o[a] + j;  // global face coordinate along a
-      if (fc < 1 || fc > G.n[a] - 1) continue;
+      const bool dir = (a == G.dir_axis);  // mode B: the boundary faces are dofs too
+      if (!dir && (fc < 1 || fc > G.n[a] - 1)) continue;
       int c[3];
       line_coords(b, a, line, c);
       int gc[3] = {b.o[0] + c[0], b.o[1] + c[1], b.o[2] + c[2]};
       gc[a] = fc;  // the cell above the face
       int hi = cell_id(G, gc[0], gc[1], gc[2]);
       int lo = hi - stride_g;
-      acc += 2.0 * coef[(size_t)hi * 3 + a] + 2.0 * coef[(size_t)lo * 3 + a];
+      if (fc <= G.n[a] - 1) acc += 2.0 * coef[(size_t)hi * 3 + a];
+      if (fc >= 1) acc += 2.0 * coef[(size_t)lo * 3 + a];
       cnt += 1;
     }
   }
@@ -172,36 +181,42 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
     const int nl = n_lines(b, a);
     const int st = axis_stride(b, a);
     const bool has_lo = b.o[a] > 0, has_hi = b.o[a] + L < G.n[a];
+    int lo, hi;
+    line_open(G, b, a, lo, hi);
     for (int line = threadIdx.x; line < nl; line += blockDim.x) {
-      double c[MAXL], cp[MAXL], piv[MAXL], col[MAXL], colp[MAXL];
+      double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], col[MAXL + 1], colp[MAXL + 1];
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
       const int base = line_base(b, a, line);
-      const int m = L - 1;
-      if (m > 0) line_factor(c, L, cp, piv);
-      // P_line[k][k'] = Ainv[k-1][k'-1] - Ainv[k-1][k'] - Ainv[k][k'-1] + Ainv[k][k']
-      // Walk columns k' of P_line; keep Ainv columns k'-1 (colp) and k' (col).
-      double a00 = 0.0, aEE = 0.0, a0E = 0.0;
-      for (int j = 0; j < m; ++j) colp[j] = 0.0;
+      const int m = L - 1 + lo + hi;
+      if (m > 0) line_factor(c, L, lo, hi, cp, piv);
+      // P_line = B Ainv B^T with B[k][k-1+lo] = +1 (low face), B[k][k+lo] = -1:
+      // walk the cells kq, keeping the Ainv columns of kq's low face (colp) and
+      // high face (col); the high face of kq is the low face of kq+1.
+      for (int j = 0; j < m; ++j) colp[j] = (lo && j == 0) ? 1.0 : 0.0;
+      if (lo) line_solve(c, L, lo, hi, cp, piv, colp);
       for (int kq = 0; kq < L; ++kq) {
-        // col = Ainv[:, kq] (zero if kq == m)
-        for (int j = 0; j < m; ++j) col[j] = (j == kq) ? 1.0 : 0.0;
-        if (kq < m) line_solve(c, L, cp, piv, col);
-        else
-          for (int j = 0; j < m; ++j) col[j] = 0.0;
-        if (kq == 0 && m > 0) {
-          a00 = col[0];
-          a0E = col[m - 1];  // Ainv[m-1][0] = Ainv[0][m-1]
-        }
-        if (kq == m - 1 && m > 0) aEE = col[m - 1];
+        const int jh = kq + lo;
+        for (int j = 0; j < m; ++j) col[j] = (j == jh) ? 1.0 : 0.0;
+        if (jh < m) line_solve(c, L, lo, hi, cp, piv, col);
         for (int k = 0; k < L; ++k) {
+          const int kl = k - 1 + lo, kh = k + lo;
           double v = 0.0;
-          if (k >= 1) v += colp[k - 1] - col[k - 1];
-          if (k <= m - 1) v += -colp[k] + col[k];
-          // colp = Ainv[:, kq-1]: terms Ainv[k-1][kq-1] - Ainv[k][kq-1]; col: -Ainv[k-1][kq] + Ainv[k][kq]
-          // (signs arranged so that P_line = B Ainv B^T with B[k][k-1]=+1, B[k][k]=-1)
+          if (kl >= 0) v += colp[kl] - col[kl];
+          if (kh < m) v += -colp[kh] + col[kh];
           if (v != 0.0) Pi[(size_t)(base + k * st) * mp + base + kq * st] += v;
         }
         for (int j = 0; j < m; ++j) colp[j] = col[j];
+      }
+      // Ainv corner entries for the interface ends (Gamma ends are never Dirichlet ends)
+      double a00 = 0.0, aEE = 0.0, a0E = 0.0;
+      if (m > 0 && (has_lo || has_hi)) {
+        for (int j = 0; j < m; ++j) col[j] = (j == 0) ? 1.0 : 0.0;
+        line_solve(c, L, lo, hi, cp, piv, col);
+        a00 = col[0];
+        a0E = col[m - 1];
+        for (int j = 0; j < m; ++j) col[j] = (j == m - 1) ? 1.0 : 0.0;
+        line_solve(c, L, lo, hi, cp, piv, col);
+        aEE = col[m - 1];
       }
       // interface slots at the two ends of the line
       for (int side = 0; side < 2; ++side) {
@@ -217,11 +232,12 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
         if (m > 0) {
           int jend = side ? m - 1 : 0;
           for (int j = 0; j < m; ++j) col[j] = (j == jend) ? cend : 0.0;
-          line_solve(c, L, cp, piv, col);
+          line_solve(c, L, lo, hi, cp, piv, col);
           for (int k = 0; k < L; ++k) {
+            const int kl = k - 1 + lo, kh = k + lo;
             double bv = 0.0;
-            if (k >= 1) bv += col[k - 1];
-            if (k <= m - 1) bv -= col[k];
+            if (kl >= 0) bv += col[kl];
+            if (kh < m) bv -= col[kh];
             g[k] -= bv;
           }
         }
@@ -243,6 +259,9 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
   //   Ps = D^-1/2 P D^-1/2 + v v^T,  D = diag(P),  v = D^1/2 1 / |D^1/2 1|.
   // Scaling removes the coefficient-contrast part of cond(P) (1e7 -> 1e3 on
   // 6-decade fields), which keeps S_i accurate to ~1e-15.  scl = [dsq (maxP) | |D^1/2 1|].
+  // Mode B subdomains touching a Dirichlet end have a nonsingular P: no v v^T,
+  // and the stored norm is 0 (pinv_fix then inverts without projecting).
+  const bool flt = sub_floating(G, b);
   double* dsq = scl + (size_t)i * (mp + 1);
   double sd = 0.0;
   for (int r = threadIdx.x; r < np; r += blockDim.x) {
@@ -253,13 +272,13 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
   }
   sd = block_sum(sd, red);
   const double vn = sqrt(sd);
-  if (threadIdx.x == 0) dsq[mp] = vn;
+  if (threadIdx.x == 0) dsq[mp] = flt ? vn : 0.0;
   __syncthreads();
   for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
     int r = (int)(e / mp), cc = (int)(e % mp);
     if (r < np && cc < np) {
       const double vr = 1.0 / (dsq[r] * vn), vc = 1.0 / (dsq[cc] * vn);
-      Pi[e] = Pi[e] * dsq[r] * dsq[cc] + vr * vc;
+      Pi[e] = Pi[e] * dsq[r] * dsq[cc] + (flt ? vr * vc : 0.0);
     } else {
       Pi[e] = (r == cc) ? 1.0 : 0.0;
     }
@@ -277,6 +296,13 @@ __global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const doubl
   const double* dsq = scl + (size_t)i * (mp + 1);
   const double vn = dsq[mp];
   double* Pi = P + (size_t)i * mp * mp;
+  if (vn == 0.0) {  // mode B, not floating: Q = P^-1 = D^-1/2 Ps^-1 D^-1/2
+    for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
+      int r = (int)(e / mp), c = (int)(e % mp);
+      Pi[e] = (r < np && c < np) ? dsq[r] * Pi[e] * dsq[c] : 0.0;
+    }
+    return;
+  }
   double part = 0.0;
   for (int c = threadIdx.x; c < np; c += blockDim.x) {
     const double vc = 1.0 / (dsq[c] * vn);
@@ -402,14 +428,17 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
   double* xg = sm;            // mg
   double* rhs = xg + mg;      // mp
   double* pp = rhs + mp;      // mp
-  double* tI = pp + mp;       // 3 mp (interior faces, per axis blocks)
-  double* yw = tI + 3 * mp;   // (blockDim/32) x mp symv partials
-  int off[3];
+  double* tI = pp + mp;       // 3 mp + 2 maxF (interior faces, per axis blocks)
+  double* yw = tI + 3 * mp + 2 * G.maxF;   // (blockDim/32) x mp symv partials
+  int off[3], lo3[3] = {0, 0, 0}, hi3[3] = {0, 0, 0};
   {
     int o = 0;
     for (int a = 0; a < 3; ++a) {
       off[a] = o;
-      if (a < G.dim) o += (b.L[a] - 1) * n_lines(b, a);
+      if (a < G.dim) {
+        line_open(G, b, a, lo3[a], hi3[a]);
+        o += (b.L[a] - 1 + lo3[a] + hi3[a]) * n_lines(b, a);
+      }
     }
   }
   const double Di = Dsub[i];
@@ -452,27 +481,28 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
   for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
     const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
     const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
-    const int L = b.L[a], m = L - 1, st = axis_stride(b, a);
+    const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
     if (m <= 0) continue;
-    double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
+    double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
     for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
-    line_factor(c, L, cp, piv);
-    for (int j = 0; j < m; ++j) r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j)] : 0.0;
+    line_factor(c, L, lo, hi, cp, piv);
+    for (int j = 0; j < m; ++j)
+      r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo)] : 0.0;
     if (A.x_gamma) {
       int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
       int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
       if (qlo >= 0) r[0] -= c[0] * xg[qlo];
       if (qhi >= 0) r[m - 1] -= c[L - 1] * xg[qhi];
     }
-    line_solve(c, L, cp, piv, r);
+    line_solve(c, L, lo, hi, cp, piv, r);
     double* t = tI + off[a] + line * m;
     const int base = line_base(b, a, line);
     double* ra = radd + a * mp;
     for (int j = 0; j < m; ++j) t[j] = r[j];
     for (int k = 0; k < L; ++k) {
       double v = 0.0;
-      if (k >= 1) v += r[k - 1];
-      if (k <= m - 1) v -= r[k];
+      if (k - 1 + lo >= 0) v += r[k - 1 + lo];
+      if (k + lo < m) v -= r[k + lo];
       ra[base + k * st] = v;
     }
   }
@@ -490,21 +520,24 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
   for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
     const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
     const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
-    const int L = b.L[a], m = L - 1, st = axis_stride(b, a);
+    const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
     {
       if (m <= 0) continue;
-      double c[MAXL], cp[MAXL], piv[MAXL], r[MAXL];
+      double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
-      line_factor(c, L, cp, piv);
+      line_factor(c, L, lo, hi, cp, piv);
       const int base = line_base(b, a, line);
-      for (int j = 0; j < m; ++j) r[j] = pp[base + (j + 1) * st] - pp[base + j * st];
-      line_solve(c, L, cp, piv, r);
+      for (int j = 0; j < m; ++j) {
+        const int p = j + 1 - lo;  // (B_u^T p')_j = p'(cell above) - p'(cell below)
+        r[j] = (p <= L - 1 ? pp[base + p * st] : 0.0) - (p >= 1 ? pp[base + (p - 1) * st] : 0.0);
+      }
+      line_solve(c, L, lo, hi, cp, piv, r);
       double* t = tI + off[a] + line * m;
       for (int j = 0; j < m; ++j) {
         double u = t[j] - r[j];
         t[j] = u;
         if (A.u_out) {
-          size_t d = (size_t)line_face_dof(G, b, a, line, j);
+          size_t d = (size_t)line_face_dof(G, b, a, line, j, lo);
           if (A.u_mode) A.u_out[d] += u;
           else A.u_out[d] = u;
         }
@@ -524,7 +557,7 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
       double v = 0.0;
       if (code >= 0) {
         SlotLine s = decode_slot(b, code);
-        int m = s.L - 1;
+        int m = s.L - 1 + lo3[s.a] + hi3[s.a];
         int kend = s.side ? s.L - 1 : 0;
         if (m > 0) {
           double cend = coef[(size_t)line_cell_global(G, b, s.a, s.line, kend) * 3 + s.a];
@@ -595,7 +628,7 @@ extern "C" int bddc_local_solve(const bddc_geom* g, const double* coef, const in
                                 const int* fslot, const double* Q, const double* Dsub,
                                 const bddc_local_solve_args* a, void* stream) {
   if (g->maxP % 32) return bddc_set_error(BDDC_ERR_ARG, "local_solve: maxP must be a multiple of 32");
-  size_t shm = (size_t)(g->maxG + 5 * g->maxP + 8 * g->maxP) * sizeof(double);
+  size_t shm = (size_t)(g->maxG + 5 * g->maxP + 2 * g->maxF + 8 * g->maxP) * sizeof(double);
   if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "local_solve: subdomain too large for shared memory");
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));

@@ -8,6 +8,9 @@
 // (equivalent to the reference's pinned (Bs Bs^T) solve after unscaling and
 // re-centring) by an orthonormal DCT-II eigenbasis: three mode products with
 // dense cosine matrices on DMMA, a diagonal scale, and three more products.
+// Mode B (G.dir_axis >= 0): the boundary faces of that axis are dofs numbered
+// after the interior ones (bnd_dof), B B^T p = B(g - A u) has Dirichlet ends
+// along it (a DST-I basis there) and no null space.
 #include "common.cuh"
 
 extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
@@ -26,21 +29,51 @@ __device__ __forceinline__ void decode_dof(const bddc_geom& G, int d, int& a, in
   f[a] += 1;  // face coordinate along a in 1..n_a-1
 }
 
+// Mode B boundary dof d >= n_flux_int -> end (side) and the adjacent cell's coordinates.
+__device__ __forceinline__ void decode_bnd(const bddc_geom& G, int d, int& side, int gc[3]) {
+  int r = d - G.n_flux_int;
+  side = r >= G.n_bt;
+  r -= side * G.n_bt;
+  int t1, t2;
+  trans_axes(G.dir_axis, t1, t2);
+  gc[t1] = r % G.n[t1];
+  gc[t2] = r / G.n[t1];
+  gc[G.dir_axis] = side ? G.n[G.dir_axis] - 1 : 0;
+}
+
 // y = alpha * A u + beta * y
 __global__ void flux_A_kernel(bddc_geom G, const double* __restrict__ coef, const double* __restrict__ u, double alpha,
                               double beta, double* __restrict__ y) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
        e += (long long)gridDim.x * blockDim.x) {
     int d = (int)e, a, f[3];
-    decode_dof(G, d, a, f);
-    int hi = cell_id(G, f[0], f[1], f[2]);
-    int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-    int lo = hi - st;
-    double clo = coef[(size_t)lo * 3 + a], chi = coef[(size_t)hi * 3 + a];
-    double v = 2.0 * (clo + chi) * u[d];
-    // dof stride along a inside family a equals the cell stride st
-    if (f[a] > 1) v += clo * u[d - st];
-    if (f[a] < G.n[a] - 1) v += chi * u[d + st];
+    double v;
+    if (d >= G.n_flux_int) {  // mode B Dirichlet face: one cell, partner = that cell's other face
+      int side, gc[3];
+      decode_bnd(G, d, side, gc);
+      a = G.dir_axis;
+      const double c = coef[(size_t)cell_id(G, gc[0], gc[1], gc[2]) * 3 + a];
+      int other;
+      if (G.n[a] == 1) {
+        other = bnd_dof(G, 1 - side, gc);
+      } else {
+        gc[a] = side ? G.n[a] - 1 : 1;
+        other = face_dof(G, a, gc[0], gc[1], gc[2]);
+      }
+      v = 2.0 * c * u[d] + c * u[other];
+    } else {
+      decode_dof(G, d, a, f);
+      int hi = cell_id(G, f[0], f[1], f[2]);
+      int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+      int lo = hi - st;
+      double clo = coef[(size_t)lo * 3 + a], chi = coef[(size_t)hi * 3 + a];
+      v = 2.0 * (clo + chi) * u[d];
+      // dof stride along a inside family a equals the cell stride st
+      if (f[a] > 1) v += clo * u[d - st];
+      else if (a == G.dir_axis) v += clo * u[bnd_dof(G, 0, f)];
+      if (f[a] < G.n[a] - 1) v += chi * u[d + st];
+      else if (a == G.dir_axis) v += chi * u[bnd_dof(G, 1, f)];
+    }
     y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
 }
@@ -59,11 +92,15 @@ __global__ void cell_div_kernel(bddc_geom G, const double* __restrict__ u, const
       if (cc[a] > 0) {  // low face interior
         int f[3] = {x, y, z};
         b += u[face_dof(G, a, f[0], f[1], f[2])];
+      } else if (a == G.dir_axis) {
+        b += u[bnd_dof(G, 0, cc)];
       }
       if (cc[a] < G.n[a] - 1) {  // high face interior
         int f[3] = {x, y, z};
         f[a] += 1;
         b -= u[face_dof(G, a, f[0], f[1], f[2])];
+      } else if (a == G.dir_axis) {
+        b -= u[bnd_dof(G, 1, cc)];
       }
     }
     double D = Dsub ? Dsub[cell_sub[c]] : 1.0;
@@ -79,24 +116,38 @@ __global__ void grad_kernel(bddc_geom G, const double* __restrict__ p, double al
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
        e += (long long)gridDim.x * blockDim.x) {
     int d = (int)e, a, f[3];
-    decode_dof(G, d, a, f);
-    int hi = cell_id(G, f[0], f[1], f[2]);
-    int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-    double v = alpha * (p[hi] - p[hi - st]);
+    double v;
+    if (d >= G.n_flux_int) {  // Dirichlet face: +p of the cell above (low end), -p below (high end)
+      int side, gc[3];
+      decode_bnd(G, d, side, gc);
+      const double pc = p[cell_id(G, gc[0], gc[1], gc[2])];
+      v = alpha * (side ? -pc : pc);
+    } else {
+      decode_dof(G, d, a, f);
+      int hi = cell_id(G, f[0], f[1], f[2]);
+      int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+      v = alpha * (p[hi] - p[hi - st]);
+    }
     y[d] = v + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
 }
 
-// Orthonormal DCT-II matrix C[k][x] = s_k cos(pi k (x+1/2)/n) and eigenvalues 4 sin^2(pi k/(2n)).
-__global__ void dct_matrix_kernel(int n, double* __restrict__ C, double* __restrict__ lam) {
+// Orthonormal DCT-II matrix C[k][x] = s_k cos(pi k (x+1/2)/n) and eigenvalues 4 sin^2(pi k/(2n))
+// of the 1-D Neumann cell Laplacian; with `dir` the DST-I pair sqrt(2/(n+1)) sin(pi (k+1)(x+1)/(n+1)),
+// 4 sin^2(pi (k+1)/(2(n+1))) of tridiag(-1, 2, -1) (both ends on a Dirichlet face).
+__global__ void dct_matrix_kernel(int n, int dir, double* __restrict__ C, double* __restrict__ lam) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n * n) {
     int k = e / n, x = e % n;
-    double s = (k == 0) ? sqrt(1.0 / n) : sqrt(2.0 / n);
-    C[e] = s * cospi((double)k * (x + 0.5) / n);
+    if (dir) {
+      C[e] = sqrt(2.0 / (n + 1)) * sinpi((double)(k + 1) * (x + 1) / (n + 1));
+    } else {
+      double s = (k == 0) ? sqrt(1.0 / n) : sqrt(2.0 / n);
+      C[e] = s * cospi((double)k * (x + 0.5) / n);
+    }
   }
   if (e < n) {
-    double sn = sinpi((double)e / (2.0 * n));
+    double sn = dir ? sinpi((double)(e + 1) / (2.0 * (n + 1))) : sinpi((double)e / (2.0 * n));
     lam[e] = 4.0 * sn * sn;
   }
 }
@@ -107,7 +158,7 @@ __global__ void dct_scale_kernel(int nx, int ny, int nz, const double* __restric
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
     int x = (int)(e % nx), y = (int)((e / nx) % ny), z = (int)(e / ((long long)nx * ny));
     double l = lx[x] + ly[y] + lz[z];
-    v[e] = (x == 0 && y == 0 && z == 0) ? 0.0 : v[e] / l;
+    v[e] = (l == 0.0) ? 0.0 : v[e] / l;   // the Neumann null mode (k = 0 on every axis: l is exactly 0)
   }
 }
 
@@ -145,7 +196,7 @@ extern "C" int bddc_dct_init(const bddc_geom* g, double* dct, void* stream) {
   double* p = dct;
   for (int a = 0; a < 3; ++a) {
     int n = g->n[a];
-    dct_matrix_kernel<<<(n * n + 255) / 256, 256, 0, s>>>(n, p, p + n * n);
+    dct_matrix_kernel<<<(n * n + 255) / 256, 256, 0, s>>>(n, a == g->dir_axis, p, p + n * n);
     LAUNCH_OK();
     p += n * n + n;
   }

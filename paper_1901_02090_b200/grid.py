@@ -2,7 +2,10 @@
 
 Mirrors the reference's public types (`/root/reference/pkg/src/bddcflow/
 grid.py:21-357`): dof numbering is identical (interior faces only, x-faces
-then y-faces then z-faces, each family x-fastest).  No matrices are
+then y-faces then z-faces, each family x-fastest).  Mode B (`PressureDrop`,
+BASELINE's boundary condition, not expressible in the reference) appends the
+Dirichlet boundary faces of one axis after the interior ones: low-end faces,
+then high-end faces, each in x-fastest order over the transverse axes.  No matrices are
 assembled on the solve path: the device kernels apply the RT0 operators
 matrix-free (csrc/stencil.cu, csrc/local.cu).  `SaddleSystem.A/.B` exist
 only for API compatibility (users and tests may multiply with them) and are
@@ -81,12 +84,31 @@ class Grid:
             stride *= ext
         return np.where(ok, self.flux_offsets[a] + idx, -1)
 
-    def cell_faces(self, a):
-        """(low, high) interior dofs of every cell's a-faces, -1 on the boundary."""
+    def cell_faces(self, a, dirichlet_axis=None):
+        """(low, high) dofs of every cell's a-faces, -1 on a no-flow boundary.
+        With `dirichlet_axis == a` the boundary faces of that axis are dofs too
+        (numbered after the interior faces, see `boundary_face_dofs`)."""
         lo = self.interior_face_dof(a, self.cell_coords)
         hi_c = self.cell_coords.copy()
         hi_c[:, a] += 1
-        return lo, self.interior_face_dof(a, hi_c)
+        hi = self.interior_face_dof(a, hi_c)
+        if dirichlet_axis == a:
+            blo, bhi = self.boundary_face_dofs(a)
+            ca = self.cell_coords[:, a]
+            lo[ca == 0] = blo
+            hi[ca == self.counts[a] - 1] = bhi
+        return lo, hi
+
+    def n_boundary_faces(self, a):
+        """Faces on one end of axis a."""
+        return self.n_cells // self.counts[a]
+
+    def boundary_face_dofs(self, a):
+        """Dofs of the low-end and high-end a-faces (mode B numbering: after the
+        interior faces, low end then high end, x-fastest over the other axes)."""
+        nt = self.n_boundary_faces(a)
+        base = self.n_flux_dofs
+        return base + np.arange(nt), base + nt + np.arange(nt)
 
 
 def build_grid(dim, counts, sizes):
@@ -130,24 +152,56 @@ class Wells:
     strength: float = 1.0
 
 
-class SaddleSystem:
-    """Mixed system [[A, B^T],[B, 0]](u, p) = (0, f) (grid.py:230-267).
+@dataclass(frozen=True)
+class PressureDrop:
+    """Mode B boundary condition (BASELINE's): pressure `p_low` on the low end and
+    `p_high` on the high end of `axis`, no flow elsewhere.  The reference has no
+    Dirichlet pressure (its assemble_system, grid.py:327-341, only takes wells);
+    the boundary faces of `axis` become flux dofs with the momentum right-hand
+    side g = +p_low (low end) and -p_high (high end) in A u + B^T p = g."""
 
-    Holds the host inputs (permeability, source vector f).  `D` is the
-    per-cell pressure rescaling filled in by the setup (grid.py:344-357).
+    axis: int
+    p_low: float = 1.0
+    p_high: float = 0.0
+
+
+class SaddleSystem:
+    """Mixed system [[A, B^T],[B, 0]](u, p) = (g, f) (grid.py:230-267).
+
+    Holds the host inputs (permeability, source vector f, and in mode B the
+    pressure drop that defines g).  `D` is the per-cell pressure rescaling
+    filled in by the setup (grid.py:344-357).
     """
 
-    def __init__(self, grid, perm, f, wells=None, D=None, lumped=False):
+    def __init__(self, grid, perm, f, wells=None, D=None, lumped=False, dirichlet=None):
         self.grid = grid
         self.perm = perm
         self.f = np.asarray(f, dtype=np.float64)
         self.wells = wells
         self.D = D
         self.lumped = lumped
+        self.dirichlet = dirichlet
+
+    @property
+    def dirichlet_axis(self):
+        return None if self.dirichlet is None else self.dirichlet.axis
 
     @property
     def n_flux(self):
-        return self.grid.n_flux_dofs
+        n = self.grid.n_flux_dofs
+        if self.dirichlet is not None:
+            n += 2 * self.grid.n_boundary_faces(self.dirichlet.axis)
+        return n
+
+    @property
+    def g(self):
+        """Momentum right-hand side (zero in mode A)."""
+        g = np.zeros(self.n_flux)
+        if self.dirichlet is not None:
+            blo, bhi = self.grid.boundary_face_dofs(self.dirichlet.axis)
+            g[blo] = self.dirichlet.p_low
+            g[bhi] = -self.dirichlet.p_high
+        return g
 
     @property
     def n_pressure(self):
@@ -162,7 +216,7 @@ class SaddleSystem:
 
     def with_rescaling(self, D):
         return SaddleSystem(self.grid, self.perm, self.f, self.wells, D=D,
-                            lumped=self.lumped)
+                            lumped=self.lumped, dirichlet=self.dirichlet)
 
     # -- host matrices for API compatibility only (not used by solve) ------
 
@@ -172,7 +226,7 @@ class SaddleSystem:
         g, k = self.grid, self.perm.k
         rows, cols, vals = [], [], []
         for a in range(g.dim):
-            lo, hi = g.cell_faces(a)
+            lo, hi = g.cell_faces(a, self.dirichlet_axis)
             c = g.sizes[a] ** 2 / (6.0 * g.cell_volume) / k[:, a]
             for d, o in ((lo, hi), (hi, lo)):
                 m = d >= 0
@@ -183,7 +237,7 @@ class SaddleSystem:
                 rows += [d[mo]]
                 cols += [o[mo]]
                 vals += [c[mo]]
-        n = g.n_flux_dofs
+        n = self.n_flux
         return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
                                                      np.concatenate(cols))),
                              shape=(n, n)).tocsr()
@@ -195,7 +249,7 @@ class SaddleSystem:
         rows, cols, vals = [], [], []
         cells = np.arange(g.n_cells)
         for a in range(g.dim):
-            lo, hi = g.cell_faces(a)
+            lo, hi = g.cell_faces(a, self.dirichlet_axis)
             for d, s in ((lo, 1.0), (hi, -1.0)):
                 m = d >= 0
                 rows += [cells[m]]
@@ -203,16 +257,26 @@ class SaddleSystem:
                 vals += [np.full(int(m.sum()), s)]
         return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows),
                                                      np.concatenate(cols))),
-                             shape=(g.n_cells, g.n_flux_dofs)).tocsr()
+                             shape=(g.n_cells, self.n_flux)).tocsr()
 
 
 def assemble_system(grid, perm, wells, lumped=False):
-    """Validate inputs and form the well source vector (grid.py:327-341)."""
+    """Validate inputs and form the source vector (grid.py:327-341).
+
+    `wells` is a `Wells` (mode A, the reference's only boundary condition:
+    no flow everywhere, sources at two cells) or a `PressureDrop` (mode B:
+    Dirichlet pressure on both ends of one axis, zero source)."""
     if lumped:
         raise InvalidArgumentError(
             "lumped RT0 mass matrices are outside the accelerated path")
     if perm.k.shape != (grid.n_cells, grid.dim):
         raise InvalidArgumentError("permeability shape mismatch")
+    if isinstance(wells, PressureDrop):
+        if not 0 <= wells.axis < grid.dim:
+            raise InvalidArgumentError(f"pressure-drop axis {wells.axis} outside 0..{grid.dim - 1}")
+        if not (np.isfinite(wells.p_low) and np.isfinite(wells.p_high)):
+            raise InvalidArgumentError("boundary pressures must be finite")
+        return SaddleSystem(grid, perm, np.zeros(grid.n_cells), None, dirichlet=wells)
     for c in (wells.src_cell, wells.sink_cell):
         if not 0 <= c < grid.n_cells:
             raise InvalidArgumentError(f"well cell {c} outside grid")

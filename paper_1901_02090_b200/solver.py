@@ -83,7 +83,7 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _geom(dec):
+def _geom(dec, system=None):
     f = dec.geom_fields()
     g = nat.Geom()
     g.dim = f["dim"]
@@ -100,6 +100,12 @@ def _geom(dec):
     for key in ("n_cells", "n_flux", "N", "n_gamma", "n_faces", "maxG", "maxP",
                 "maxL", "maxF"):
         setattr(g, key, int(f[key]))
+    # mode B: the Dirichlet faces of one axis are flux dofs after the interior ones
+    ax = None if system is None else system.dirichlet_axis
+    g.dir_axis = -1 if ax is None else int(ax)
+    g.n_flux_int = g.n_flux
+    g.n_bt = 0 if ax is None else dec.grid.n_boundary_faces(ax)
+    g.n_flux = g.n_flux_int + 2 * g.n_bt
     return g
 
 
@@ -133,8 +139,23 @@ class BddcSetup:
         # the solve path only needs the ones above tau and the next one
         self.pair_spectra = bool(pair_spectra)
         self.pcg_timer = None   # list -> (start, end) CUDA events of every PCG graph launch
-        self.geom = _geom(dec)
+        self.geom = _geom(dec, system)
         G = self.geom
+        # mode B (PressureDrop): subdomains on a Dirichlet end have a nonsingular
+        # interior pressure block, no balance constraint and no coarse pressure;
+        # the others ("floating") keep both.  Mode A: all floating, subdomain 0's
+        # coarse pressure pinned (coarse.py:192-194).
+        self.mode_b = system.dirichlet is not None
+        if self.mode_b:
+            ax = system.dirichlet_axis
+            sidx = (np.arange(dec.n_subdomains) // int(np.prod(dec.S3[:ax]))) % dec.S3[ax]
+            self.floating = (sidx != 0) & (sidx != dec.S3[ax] - 1)
+            self.has_p = self.floating
+            if dec.n_subdomains > 4096:
+                raise InvalidArgumentError("mode B (PressureDrop) supports up to 4096 subdomains")
+        else:
+            self.floating = np.ones(dec.n_subdomains, dtype=bool)
+            self.has_p = np.arange(dec.n_subdomains) != 0
         gp = C.byref(G)
         st = _stream()
         self._timings = timings
@@ -164,8 +185,11 @@ class BddcSetup:
         # (N^2 doubles: used up to N = 4096, i.e. 134 MB per GEMV)
         S3 = dec.S3
         self.d_Lp = None
+        self.d_Lu = None
         self._lap_ws = torch.empty(2 * N, dtype=F64, device=dev)   # multi-CTA separable solve
-        if N <= 4096:
+        if self.mode_b:
+            self.d_Lp, self.d_Lu = self._dirichlet_laplacian_inverses()
+        elif N <= 4096:
             ws = torch.empty(2 * N * N, dtype=F64, device=dev)
             self.d_Lp = torch.empty(N * N, dtype=F64, device=dev)
             nat.call("bddc_lap_dense", S3[0], S3[1], S3[2], _p(self.d_eig_w), _p(self.d_dm_w),
@@ -328,7 +352,8 @@ class BddcSetup:
         self.npad = _pad(max(nfc, 1), 64)
         self.nd = None
         if nfc:
-            self.nd = CoarseND(dec, per_face, cstart, self.sub_rows, self.nC, maxC, dev)
+            self.nd = CoarseND(dec, per_face, cstart, self.sub_rows, self.nC, maxC, dev,
+                               has_p=self.has_p)
             self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
             self.nd.release_fronts()
         main.wait_stream(side)   # T_i done; its workspaces may go now
@@ -411,6 +436,35 @@ class BddcSetup:
         if isinstance(self._timings, dict):
             self._timings.update(out)
         return out
+
+    def _dirichlet_laplacian_inverses(self):
+        """Mode B balance operators: (Phi_F Phi_F^T)^-1 (projection, solver.py:166-179)
+        and the inverse face-graph Laplacian (balanced shift, solver.py:146-164) over
+        the floating subdomains F, as N x N matrices with zero rows and columns for
+        the others.  Both are principal submatrices of graph Laplacians whose graph
+        reaches a Dirichlet subdomain, hence SPD: one batched device inverse."""
+        dec, N, dev, st = self.dec, self.N, self.dev, _stream()
+        n = _pad(N, 64)
+        ft = torch.as_tensor(dec.face_table.astype(np.int64), device=dev)
+        i, j = ft[:, 0], ft[:, 1]
+        L = torch.zeros(2, n, n, dtype=F64, device=dev)
+        for b, w in ((0, ft[:, 3].to(F64)), (1, torch.ones(len(ft), dtype=F64, device=dev))):
+            L[b].index_put_((i, j), -w, accumulate=True)
+            L[b].index_put_((j, i), -w, accumulate=True)
+            L[b].index_put_((i, i), w, accumulate=True)
+            L[b].index_put_((j, j), w, accumulate=True)
+        mask = torch.zeros(n, dtype=F64, device=dev)
+        mask[:N] = torch.as_tensor(self.floating.astype(np.float64), device=dev)
+        L *= mask[:, None] * mask[None, :]
+        L[:, torch.arange(n, device=dev), torch.arange(n, device=dev)] += (1.0 - mask)
+        info = torch.zeros(1, dtype=I32, device=dev)
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(n, 2, 32) // 8 + 2,
+                         dtype=F64, device=dev)
+        nat.call("bddc_spd_inverse_batched", _p(L), n, n, n * n, 2, 32, _p(ws), _p(info), st)
+        if int(info.item()):
+            raise NumericalFailureError("mode B balance Laplacian not positive definite")
+        L *= mask[:, None] * mask[None, :]
+        return L[0, :N, :N].contiguous().view(-1), L[1, :N, :N].contiguous().view(-1)
 
     def _multiscale_rows(self, system, Sinv):
         """Face rows of the pair-local unit-transfer solves (adaptive.py:207-262),
@@ -791,6 +845,11 @@ class _Work:
         self.rq = z(setup.N)
         self.x0 = z(setup.npad)
         self.f_dev = z(G.n_cells)
+        self.gv = None
+        if setup.mode_b:
+            # momentum rhs g: +p_low on the low Dirichlet faces, -p_high on the high ones
+            self.gv = z(G.n_flux)
+            self.gv_vals = None
 
 
 def _dot(setup, x, y, n, op, hist=None):
@@ -808,6 +867,9 @@ def solve(system, dec, config, u_exact=None, setup=None, iterate_callback=None,
     """Three-step method + pressure recovery (solver.py:301-398)."""
     if setup is None:
         setup = BddcSetup(system, dec, config)
+    if setup.mode_b != (system.dirichlet is not None) or (
+            setup.mode_b and system.dirichlet.axis != setup.system.dirichlet.axis):
+        raise InvalidArgumentError("setup was built for a different boundary condition")
     if not setup._scaling_checked:
         _suggest_scaling(setup)
         setup._scaling_checked = True
@@ -839,10 +901,36 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
             W.f_host = fh   # keep the pinned buffer alive until the copy ran
             f_device.copy_(fh, non_blocking=True)
     _scale_fs(setup, f_device, W.fs)
+    gv = None
+    if setup.mode_b:
+        gv = W.gv
+        vals = (float(system.dirichlet.p_low), float(system.dirichlet.p_high))
+        if W.gv_vals != vals:
+            nb = G.n_bt
+            gv[G.n_flux_int:G.n_flux_int + nb].fill_(vals[0])
+            gv[G.n_flux_int + nb:G.n_flux_int + 2 * nb].fill_(-vals[1])
+            W.gv_vals = vals
     # step 1: rq_i = sum fs over cells of i; x0 = Wq rq[1:]; g = average(Psi x0)
     nat.call("bddc_sub_sum", gp, _p(W.fs), _p(W.rq), 1.0, None, st)
     if setup.nfc and N > 1:
-        nat.call("bddc_fill", setup.nfc, 0.0, _p(setup.w_rc), st)
+        if gv is not None:
+            # mode B: the coarse flux rhs is the BDDC coarse restriction of the
+            # interface residual of the boundary data, r = -sum_i R_i^T condense_i(g)
+            a = nat.LocalSolveArgs()
+            a.f_flux, a.f_scale = _p(gv).value, 1.0
+            a.rg_broken = _p(setup.w_yb).value
+            nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode),
+                     _p(setup.d_gpos), _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub),
+                     C.byref(a), st)
+            nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb), _p(W.r), st)
+            nat.call("bddc_gather_gemv_t", N, setup.maxG, setup.maxC, _p(setup.d_nG),
+                     _p(setup.d_nC), _p(setup.d_gpos), _p(setup.d_Psi), _p(W.r),
+                     _p(setup.d_delta), _p(setup.w_v), st)
+            nat.call("bddc_coarse_restrict", setup.nfc, _p(setup.d_cown), _p(setup.w_v),
+                     _p(setup.w_rc), st)
+            nat.call("bddc_axpby", setup.nfc, 0.0, _p(setup.w_rc), -1.0, _p(setup.w_rc), st)
+        else:
+            nat.call("bddc_fill", setup.nfc, 0.0, _p(setup.w_rc), st)
         nat.call("bddc_axpby", N, 1.0, _p(W.rq), 0.0, _p(setup.w_rc[setup.nfc:]), st)
         setup._coarse_solve()
         nat.call("bddc_axpby", setup.nfc, 1.0, _p(setup.w_xc), 0.0, _p(W.x0), st)
@@ -857,12 +945,16 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     a = nat.LocalSolveArgs()
     a.x_gamma, a.x_scale = _p(W.g).value, 1.0
     a.u_out, a.u_mode = _p(W.u0).value, 0
+    if gv is not None:
+        a.f_flux, a.f_scale = _p(gv).value, 1.0
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
              _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     a = nat.LocalSolveArgs()
     a.x_gamma, a.x_scale = _p(W.g).value, 1.0
     a.g_cell, a.g_scale = _p(W.fs).value, 1.0
     a.u_out, a.u_mode = _p(W.us).value, 0
+    if gv is not None:
+        a.f_flux, a.f_scale = _p(gv).value, 1.0
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
              _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     host = {}
@@ -877,15 +969,27 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     nat.call("bddc_cell_div", gp, _p(W.us), _p(W.fs), 1.0, -1.0, _p(setup.d_cell_sub),
              _p(setup.d_Dsub), _p(W.dd), st)
     nfs = _norm(setup, W.fs, G.n_cells)
-    defect_norm = _norm(setup, W.dd, G.n_cells) / max(nfs, 1e-300)
-    # step 3 rhs: r = -A u*; r_G -= sum condense
-    nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.us), -1.0, 0.0, _p(W.rf), st)
+    # relative to |fs| (solver.py:331-333); absolute when there is no source (mode B)
+    defect_norm = _norm(setup, W.dd, G.n_cells) / (nfs if nfs > 0 else 1.0)
+    # step 3 rhs: r = g - A u* (g = 0 in mode A, solver.py:342); r_G -= sum condense
+    if gv is not None:
+        nat.call("bddc_axpby", G.n_flux, 1.0, _p(gv), 0.0, _p(W.rf), st)
+        nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.us), -1.0, 1.0, _p(W.rf), st)
+    else:
+        nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.us), -1.0, 0.0, _p(W.rf), st)
     w_cg_it = 0
     kappa = 1.0
     history = np.array([1.0])
     converged = True
+    r_floor = 0.0
     if ng:
         nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.r), _p(W.rf), 2, st)
+        if gv is not None:
+            # mode B extension: an interface residual at rounding level relative to
+            # the uncondensed one means Steps 1-2 already solved the problem (e.g. a
+            # homogeneous field whose solution the coarse space contains); PCG
+            # on it would only chase rounding (the reference stops on r0 == 0 only)
+            r_floor = 1e-12 * _norm(setup, W.r, ng)
         a = nat.LocalSolveArgs()
         a.f_flux, a.f_scale = _p(W.rf).value, 1.0
         a.g_cell, a.g_scale = _p(W.dd).value, 1.0
@@ -904,8 +1008,11 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         tmax, fs_abs = torch.stack([setup.w_z.max(), W.tmpc.sum()]).tolist()
         if tmax > 1e-13 * max(fs_abs, 1.0):
             S3 = dec.S3
-            nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
-                     _p(setup.w_phi), _p(setup.w_z), st)
+            if setup.d_Lu is not None:   # mode B: floating subdomains only, zero elsewhere
+                nat.call("bddc_gemv", N, N, N, _p(setup.d_Lu), _p(setup.w_phi), _p(setup.w_z), st)
+            else:
+                nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
+                         _p(setup.w_phi), _p(setup.w_z), st)
             nat.call("bddc_face_shift", ng, dec.n_faces, _p(setup.d_gface), _p(setup.d_faces),
                      _p(setup.w_z), _p(W.wp), st)
             setup._schur(W.wp, W.Ap)
@@ -913,7 +1020,7 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         else:
             nat.call("bddc_fill", ng, 0.0, _p(W.wp), st)
         setup._project(W.r)
-        w_cg_it, kappa, history, converged = _pcg(setup, W, config, iterate_callback)
+        w_cg_it, kappa, history, converged = _pcg(setup, W, config, iterate_callback, r_floor)
         # u = u* + correction, interior recovery
         nat.call("bddc_axpby", ng, 1.0, _p(W.wp), 1.0, _p(W.x), st)
     nat.call("bddc_axpby", G.n_flux, 1.0, _p(W.us), 0.0, _p(W.u), st)
@@ -926,8 +1033,8 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         a.u_out, a.u_mode = _p(W.u).value, 1
         nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
                  _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
-    # pressure recovery: B B^T p = B(-A u), zero mean
-    p_warn = _recover_pressure(setup, W, config.tol)
+    # pressure recovery: B B^T p = B(g - A u), zero mean in mode A
+    p_warn = _recover_pressure(setup, W, config.tol, gv)
     omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
     if return_device:
         return W, w_cg_it, kappa, history, converged
@@ -976,17 +1083,22 @@ def _scale_fs(setup, f, fs):
              _p(setup.d_Dsub), _p(fs), _stream())
 
 
-def _recover_pressure(setup, W, tol):
+def _recover_pressure(setup, W, tol, gv=None):
+    """solver.py:254-274: (B B^T) p = B(g - A u) by the separable cosine (mode A,
+    pure Neumann: zero-mean p) or cosine/sine (mode B: Dirichlet ends) transform."""
     G = setup.geom
     gp = C.byref(G)
     st = _stream()
     nat.call("bddc_flux_A", gp, _p(setup.d_coef), _p(W.u), 1.0, 0.0, _p(W.rf), st)
-    # rhs = B(-A u)
+    if gv is not None:
+        nat.call("bddc_axpby", G.n_flux, -1.0, _p(gv), 1.0, _p(W.rf), st)
+    # rhs = B(g - A u)
     nat.call("bddc_cell_div", gp, _p(W.rf), None, 0.0, -1.0, None, None, _p(W.pc), st)
     nat.call("bddc_neumann_solve", gp, _p(setup.d_dct), _p(W.pc), _p(W.tmpc), st)
-    ones = _ones(setup, G.n_cells)
-    _dot(setup, W.pc, ones, G.n_cells, 100 + 11)
-    nat.call("bddc_sub_mean", G.n_cells, _p(setup.w_scal[11:]), _p(W.pc), st)
+    if gv is None:
+        ones = _ones(setup, G.n_cells)
+        _dot(setup, W.pc, ones, G.n_cells, 100 + 11)
+        nat.call("bddc_sub_mean", G.n_cells, _p(setup.w_scal[11:]), _p(W.pc), st)
     den = _norm(setup, W.rf, G.n_flux)
     nat.call("bddc_grad", gp, _p(W.pc), 1.0, 1.0, _p(W.rf), st)
     num = _norm(setup, W.rf, G.n_flux)
@@ -1071,7 +1183,7 @@ def _pcg_graph(setup, W, B, tol, maxit):
     return state
 
 
-def _pcg(setup, W, config, callback):
+def _pcg(setup, W, config, callback, r_floor=0.0):
     """PCG with Lanczos kappa (solver.py:186-233), fully device resident.
 
     Without a callback the whole loop is one CUDA-graph launch (conditional
@@ -1088,7 +1200,7 @@ def _pcg(setup, W, config, callback):
     host = setup._host_scal
     host.copy_(scal, non_blocking=True)
     torch.cuda.current_stream().synchronize()
-    if host[4] == 0.0:
+    if host[4] <= r_floor:   # host[4] = ||r0||
         return 0, 1.0, np.array([1.0]), True
     if callback is None and not setup.force_eager:
         # make sure every lazily-created buffer exists before capture
