@@ -11,12 +11,14 @@ ap.add_argument("--scaling", default=None)
 ap.add_argument("--tau", type=float, default=None)
 ap.add_argument("--tol", type=float, default=None)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--bc", default="A", choices=["A", "B"])
 a = ap.parse_args()
 c = dict(fields.CONFIGS[a.cfg])
 t = time.time(); k = fields.config_field(a.cfg); tk = time.time() - t
 g = B.build_grid(c["dim"], c["counts"], c["sizes"])
 t = time.time(); dec = B.regular_partition(g, c["splits"]); td = time.time() - t
-system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
+system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1) if a.bc == "A"
+                           else B.PressureDrop(1, 1.0, 0.0))
 tau = a.tau if a.tau is not None else c["tau"]
 cfg = B.SolveConfig(tau=tau, scaling=a.scaling or c["scaling"],
                     constraints="adaptive" if math.isfinite(tau) else c["constraints"],
@@ -36,6 +38,11 @@ for rep in range(a.reps):
         print(f"  solve[{rr}] {tsol:.3f}s it={r.it} kappa={r.kappa:.4f} it/s={r.it/tsol:.1f} cons={r.conservation_defect:.2e} pw={r.pressure_warning}", flush=True)
     del st
     torch.cuda.empty_cache()
+if a.bc == "B":
+    res = system.A @ r.u + system.B.T @ r.p - system.g
+    print(f"mode B residuals: momentum {np.linalg.norm(res) / np.linalg.norm(system.A @ r.u):.2e} "
+          f"mass {np.abs(system.B @ r.u).max() / np.abs(r.u).max():.2e} p in [{r.p.min():.4f}, {r.p.max():.4f}] "
+          f"outflow {r.u[-g.n_boundary_faces(1):].sum():.6e} inflow {r.u[g.n_flux_dofs:g.n_flux_dofs + g.n_boundary_faces(1)].sum():.6e}", flush=True)
 # per-call device-time breakdown of one setup + one solve
 from paper_1901_02090_b200 import _native as nat
 nat.profile_start()
