@@ -235,6 +235,10 @@ int bddc_p_update(long long n, const double* scal, const double* z, double* p, v
 int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const double* dm, double* ws, double* Lp,
                    void* stream);
 int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream);
+/* Tuning knob for bddc_gemv: warps per row (1, 2, 4, 8; 0 = automatic by shape). */
+void bddc_set_gemv_wpr(int wpr);
+/* Tuning knob: threads per CTA (256 or 512) of grid-stride bddc_gather_symv launches. */
+void bddc_set_symv_threads(int t);
 int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out,
                  void* stream);
 int bddc_axpby(long long n, double a, const double* x, double b, double* y, void* stream);

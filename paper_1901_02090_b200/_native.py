@@ -134,6 +134,8 @@ _SIGS = {
     "bddc_cg_update": [_L, _P, _P, _P, _P, _P, _P],
     "bddc_p_update": [_L, _P, _P, _P, _P],
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
+    "bddc_set_gemv_wpr": [_I],
+    "bddc_set_symv_threads": [_I],
     "bddc_lap_dense": [_I, _I, _I, _P, _P, _P, _P, _P],
     "bddc_lanczos": [_I, _P, _P, _P, _P, _P],
     "bddc_axpby": [_L, _D, _P, _D, _P, _P],

@@ -58,9 +58,34 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = shm;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = bddc_pdl_enabled() ? 1 : 0;
+  // the stream's priority as an explicit launch attribute, so that a kernel node
+  // captured into a graph (the PCG WHILE body) keeps it
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  at[1].id = cudaLaunchAttributePriority;
+  at[1].val.priority = prio;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Plain launch carrying the stream's priority as a launch attribute (see launch_pdl).
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_prio(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t shm, cudaStream_t s,
+                                      Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = shm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  int prio = 0;
+  cudaStreamGetPriority(s, &prio);
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = prio;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);

@@ -303,7 +303,7 @@ extern "C" int bddc_nd_qd(int mode, int m, int Sf, int Sp, int nf, double* F, vo
 
 extern "C" int bddc_fill(long long n, double v, double* a, void* stream) {
   if (n <= 0) return 0;
-  fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, v, a);
+  CUDA_OK(launch_prio(fill_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, n, v, a));
   LAUNCH_OK();
   return 0;
 }

@@ -66,7 +66,8 @@ __global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, doubl
 // Each warp streams whole tiles (coalesced rows), forms the column contribution in
 // registers and the row contribution with a 31-shuffle transpose-reduction; per-tile
 // partials are combined per output block in a fixed order (deterministic).
-__global__ void __launch_bounds__(256) gather_symv_kernel(int N, int maxG, const int* __restrict__ nG,
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, const int* __restrict__ nG,
                                                          const int* __restrict__ gpos,
                                                          const double* __restrict__ packed,
                                                          const double* __restrict__ x,
@@ -462,6 +463,49 @@ __global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ 
   if (lane == 0) y[row] = acc;
 }
 
+// y = M x with WPR warps per row (each a contiguous column chunk, partials summed
+// in fixed order through shared memory: deterministic).  More warps per row keep
+// more loads in flight when there are few rows (N x N projection operator).
+template <int WPR>
+__global__ void __launch_bounds__(256) gemv_split_kernel(int n, int ld, int ncol, const double* __restrict__ M,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ double part[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = blockIdx.x * (8 / WPR) + w / WPR, pi = w % WPR;
+  const int chunk = ((ncol + WPR * 32 - 1) / (WPR * 32)) * 32;
+  const int c0 = pi * chunk, c1 = min(ncol, c0 + chunk);
+  double acc = 0.0;
+  if (row < n) {
+    const double* mr = M + (size_t)row * ld;
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = 0.0;
+    int c = c0 + lane;
+    for (; c + 224 < c1; c += 256) {
+      double m[8], v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        m[u] = __ldg(mr + c + 32 * u);
+        v[u] = __ldg(x + c + 32 * u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (c + 32 * u < c1) a[u] += __ldg(mr + c + 32 * u) * __ldg(x + c + 32 * u);
+    acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  }
+  if (lane == 0) part[w] = acc;
+  __syncthreads();
+  if (pi == 0 && lane == 0 && row < n) {
+    double t = part[w];
+    for (int q = 1; q < WPR; ++q) t += part[w + q];
+    y[row] = t;
+  }
+}
+
 // Dense pseudo-inverse of the separable subdomain-grid Laplacian (setup):
 // W[e][f] = Qx[ex][fx] Qy[ey][fy] Qz[ez][fz] (spatial e, mode f), Ws = W Lambda^+.
 __global__ void lap_kron_kernel(int S0, int S1, int S2, const double* __restrict__ eig, double* __restrict__ W,
@@ -574,29 +618,39 @@ extern "C" int bddc_pack_sym(int N, int maxG, const double* full, double* packed
   return 0;
 }
 
+static int g_symv_threads = 256;
+extern "C" void bddc_set_symv_threads(int t) { g_symv_threads = (t == 512) ? 512 : 256; }
+
 extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
                                 const double* x, const double* win, double* yb, int grid, void* stream) {
   int nt = maxG / 32;
   size_t shm = ((size_t)maxG + (size_t)nt * (nt + 1) * 32) * sizeof(double);
   if (shm > 48 * 1024)
-    CUDA_OK(cudaFuncSetAttribute(gather_symv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    for (auto k : {gather_symv_kernel<256>, gather_symv_kernel<512>})
+      CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   if (grid <= 0 || grid > N) grid = N;
-  gather_symv_kernel<<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
+  // the grid-stride launch (T_i beside the coarse chain: one CTA per SM) may want
+  // more loads in flight per CTA than one CTA per subdomain
+  if (grid < N && g_symv_threads == 512)
+    gather_symv_kernel<512><<<grid, 512, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
+  else
+    gather_symv_kernel<256><<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
   LAUNCH_OK();
   return 0;
 }
 
 extern "C" int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,
                                   const double* PsiT, const double* x, const double* win, double* v, void* stream) {
-  gather_gemv_t_kernel<<<N, 256, maxG * sizeof(double), (cudaStream_t)stream>>>(maxG, maxC, nG, nC, gpos, PsiT, x,
-                                                                                  win, v);
+  CUDA_OK(launch_prio(gather_gemv_t_kernel, dim3(N), dim3(256), maxG * sizeof(double), (cudaStream_t)stream, maxG,
+                      maxC, nG, nC, gpos, PsiT, x, win, v));
   LAUNCH_OK();
   return 0;
 }
 
 extern "C" int bddc_coarse_restrict(int nfc, const int* cown, const double* v, double* rhs, void* stream) {
   if (nfc <= 0) return 0;
-  coarse_restrict_kernel<<<(nfc + 255) / 256, 256, 0, (cudaStream_t)stream>>>(nfc, cown, v, rhs);
+  CUDA_OK(launch_prio(coarse_restrict_kernel, dim3((nfc + 255) / 256), dim3(256), 0, (cudaStream_t)stream, nfc, cown,
+                      v, rhs));
   LAUNCH_OK();
   return 0;
 }
@@ -756,9 +810,21 @@ extern "C" int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const d
   return 0;
 }
 
+static int g_gemv_wpr = 0;   // 0: automatic
+extern "C" void bddc_set_gemv_wpr(int wpr) { g_gemv_wpr = wpr; }
+
 extern "C" int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream) {
   if (n <= 0) return 0;
-  gemv_kernel<<<(n + 7) / 8, 256, 0, (cudaStream_t)stream>>>(n, ld, ncol, M, x, y);
+  cudaStream_t s = (cudaStream_t)stream;
+  // enough warps for ~60 per SM on the row count (few long rows: split them)
+  int wpr = g_gemv_wpr;
+  if (wpr <= 0) wpr = (n >= 8192 || ncol < 1024) ? 1 : (n >= 4096 ? 2 : 4);
+  switch (wpr) {
+    case 1: gemv_kernel<<<(n + 7) / 8, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
+    case 2: gemv_split_kernel<2><<<(n + 3) / 4, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
+    case 4: gemv_split_kernel<4><<<(n + 1) / 2, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
+    default: gemv_split_kernel<8><<<n, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
+  }
   LAUNCH_OK();
   return 0;
 }

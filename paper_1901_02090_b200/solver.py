@@ -387,8 +387,11 @@ class BddcSetup:
         self._host_scal = torch.empty(16, dtype=F64, pin_memory=True)
         self.stream = torch.cuda.Stream(device=dev)
         self.n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-        # T_i GEMV grid beside the coarse chain: one CTA per SM (C3 whole solve: 29.5 ms
-        # at 1x SMs, 30.9 at 2x and 3x, 31.5 with one CTA per subdomain)
+        # T_i GEMV grid beside the coarse chain: one 256-thread CTA per SM (grid-stride
+        # over subdomains).  The latency-bound chain is the critical path; giving T more
+        # bandwidth starves it (C3 PCG-only it/s: 1424 at 1x SMs, 1363 at 2x, 1346 at 4x,
+        # 1357 with 512-thread CTAs; the chain's kernels carry the side stream's
+        # priority as a launch attribute so it survives graph capture)
         self.t_grid = self.n_sm
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
