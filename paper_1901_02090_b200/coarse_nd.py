@@ -89,9 +89,11 @@ def nd_geometry(dec, has_p=None):
                 for u in range(lo[t[0]], hi[t[0]])]
 
     def box_subs(lo, hi):
-        z, y, x = np.meshgrid(np.arange(lo[2], hi[2]), np.arange(lo[1], hi[1]),
-                              np.arange(lo[0], hi[0]), indexing="ij")
-        return np.sort((x + S3[0] * (y + S3[1] * z)).ravel())
+        # x-fastest over the box: already increasing
+        x = np.arange(lo[0], hi[0])
+        y = np.arange(lo[1], hi[1]) * S3[0]
+        z = np.arange(lo[2], hi[2]) * (S3[0] * S3[1])
+        return (z[:, None, None] + y[None, :, None] + x[None, None, :]).ravel()
 
     nodes = []
 

@@ -315,7 +315,7 @@ __global__ void lap_solve_kernel(int S0, int S1, int S2, const double* __restric
   for (int e = threadIdx.x; e < N; e += blockDim.x) {
     int a0 = e % S0, a1 = (e / S0) % S1, a2 = e / (S0 * S1);
     double l = lx[a0] + ly[a1] + lz[a2];
-    w[e] = (a0 == 0 && a1 == 0 && a2 == 0) ? 0.0 : w[e] / l;
+    w[e] = (l == 0.0) ? 0.0 : w[e] / l;   // Neumann null mode (exact 0); none with a Dirichlet axis
   }
   __syncthreads();
   for (int a = 0; a < 3; ++a) {
@@ -525,7 +525,7 @@ __global__ void lap_kron_kernel(int S0, int S1, int S2, const double* __restrict
     const double w = Qx[ex * S0 + fx] * Qy[ey * S1 + fy] * Qz[ez * S2 + fz];
     const double lam = lx[fx] + ly[fy] + lz[fz];
     W[t] = w;
-    Ws[t] = (f == 0) ? 0.0 : w / lam;
+    Ws[t] = (lam == 0.0) ? 0.0 : w / lam;
   }
 }
 
@@ -716,7 +716,7 @@ __global__ void lap_mode_kernel(int S0, int S1, int S2, int a, int backward, con
   if (lamdiv) {
     const int a0 = e % S0, a1 = (e / S0) % S1, a2 = e / (S0 * S1);
     const double l = lam[a0] + lam[S0 + a1] + lam[S0 + S1 + a2];
-    acc = (e == 0) ? 0.0 : acc / l;
+    acc = (l == 0.0) ? 0.0 : acc / l;   // Neumann null mode only (exact 0)
   }
   out[e] = dmo ? dmo[e] * acc : acc;
 }

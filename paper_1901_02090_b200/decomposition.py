@@ -143,7 +143,8 @@ class Decomposition:
         n3, S3 = self.n3, self.S3
         fam_off = list(g.flux_offsets) + [g.flux_offsets[-1]] * (4 - len(g.flux_offsets))
         self.fam_off = fam_off
-        subs, dofs, codes, face_key = [], [], [], []
+        subs, dofs, codes = [], [], []
+        lo_dofs = []
         face_rows = []
         for a in range(g.dim):
             t1 = 1 if a == 0 else 0
@@ -173,22 +174,28 @@ class Decomposition:
                 hi = sst[0] + S3[0] * (sst[1] + S3[1] * sst[2])
                 subs += [lo, hi]
                 dofs += [dof, dof]
+                lo_dofs.append(dof)
                 codes += [a | (1 << 2) | (line << 3), a | (0 << 2) | (line << 3)]
-                # faces: one per (lo, hi) pair
-                key = lo * (self.n_subdomains + 1) + hi
-                face_key.append(key)
-                uk, first, cnt = np.unique(key, return_index=True, return_counts=True)
-                for fi, m in zip(first, cnt):
-                    face_rows.append((int(lo[fi]), int(hi[fi]), a, int(m)))
+                # faces on this plane: one per transverse strip pair, m = w_t1 * w_t2
+                for u2 in range(S3[t2]):
+                    for u1 in range(S3[t1]):
+                        st_ = [0, 0, 0]
+                        st_[t1], st_[t2], st_[a] = u1, u2, s - 1
+                        i_lo = st_[0] + S3[0] * (st_[1] + S3[1] * st_[2])
+                        i_hi = i_lo + (1 if a == 0 else (S3[0] if a == 1 else S3[0] * S3[1]))
+                        face_rows.append((i_lo, i_hi, a, int(self.sw[t1][u1] * self.sw[t2][u2])))
         if subs:
             subs = np.concatenate(subs)
             dofs = np.concatenate(dofs)
             codes = np.concatenate(codes)
         else:
             subs = dofs = codes = np.zeros(0, dtype=np.int64)
-        self.gamma = np.unique(dofs)
+        # every interface dof has exactly one low-side copy
+        self.gamma = np.sort(np.concatenate(lo_dofs)) if lo_dofs else np.zeros(0, np.int64)
         n_gamma = len(self.gamma)
-        o = np.lexsort((dofs, subs))
+        # (subdomain, dof) pairs are unique: a plain argsort of the combined key is
+        # the lexicographic order (and deterministic)
+        o = np.argsort(subs.astype(np.int64) * (g.n_flux_dofs + 1) + dofs)
         subs, dofs, codes = subs[o], dofs[o], codes[o]
         N = self.n_subdomains
         counts = np.bincount(subs, minlength=N)
@@ -197,7 +204,9 @@ class Decomposition:
         self.nG = counts.astype(np.int32)
         maxG = _pad(int(counts.max()) if len(counts) else 1, 64)
         self.maxG = maxG
-        gpos = np.searchsorted(self.gamma, dofs)
+        inv = np.empty(g.n_flux_dofs, dtype=np.int64)
+        inv[self.gamma] = np.arange(n_gamma)
+        gpos = inv[dofs]
         self.gpos = np.full((N, maxG), -1, dtype=np.int32)
         self.gcode = np.full((N, maxG), -1, dtype=np.int32)
         self.gpos[subs, slot] = gpos
@@ -247,9 +256,15 @@ class Decomposition:
 
     # -------------------------------------------------- Laplacian eigendata
 
-    def laplacian_eigs(self, weighted):
-        """Eigen data of K_a = D_a^-1/2 Lpath_a D_a^-1/2 (weighted) or Lpath_a."""
+    def laplacian_eigs(self, weighted, dirichlet_axis=None):
+        """Eigen data of K_a = D_a^-1/2 Lpath_a D_a^-1/2 (weighted) or Lpath_a.
+
+        With `dirichlet_axis` d (mode B) the operator is the principal submatrix
+        over the floating subdomains (strips 1 .. S_d-2 of axis d): K_d loses its
+        first and last row/column (keeping their couplings on the diagonal), no
+        null mode, and `dm` lists the floating subdomains in increasing id."""
         Qs, lams = [], []
+        S3 = list(self.S3)
         for a in range(3):
             s = self.S3[a]
             L = np.zeros((s, s))
@@ -258,11 +273,16 @@ class Decomposition:
                 L[k + 1, k + 1] += 1
                 L[k, k + 1] -= 1
                 L[k + 1, k] -= 1
+            w = self.sw[a][:s].astype(np.float64)
+            if a == dirichlet_axis:
+                L, w = L[1:-1, 1:-1], w[1:-1]
+                S3[a] = s - 2
             if weighted:
-                dm = 1.0 / np.sqrt(self.sw[a].astype(np.float64))
+                dm = 1.0 / np.sqrt(w)
                 L = dm[:, None] * L * dm[None, :]
             lam, Q = np.linalg.eigh(L)
-            lam[0] = 0.0
+            if a != dirichlet_axis:
+                lam[0] = 0.0
             Qs.append(Q.ravel())
             lams.append(lam)
         eig = np.concatenate(Qs + lams)
@@ -270,7 +290,12 @@ class Decomposition:
         if weighted:
             ncell = (self.sw[0][self.sub_strip[:, 0]] * self.sw[1][self.sub_strip[:, 1]]
                      * self.sw[2][self.sub_strip[:, 2]]).astype(np.float64)
+            if dirichlet_axis is not None:
+                sd = self.sub_strip[:, dirichlet_axis]
+                ncell = ncell[(sd >= 1) & (sd <= self.S3[dirichlet_axis] - 2)]
             dm = 1.0 / np.sqrt(ncell)
+        if dirichlet_axis is not None:
+            return eig, dm, tuple(S3)
         return eig, dm
 
     # ------------------------------------------------ reference-compatible

@@ -73,6 +73,12 @@ class SolveReport:
     converged: bool = True
 
 
+# Largest subdomain count for which the balance operators (projection, shift) are
+# kept as dense N x N matrices applied by one multi-CTA GEMV (134 MB at 4096);
+# beyond it they are separable transforms over the subdomain grid.
+DENSE_BALANCE_MAX = 4096
+
+
 def _dev():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1901_02090_b200 needs a CUDA device (no CPU fallback)")
@@ -151,8 +157,6 @@ class BddcSetup:
             sidx = (np.arange(dec.n_subdomains) // int(np.prod(dec.S3[:ax]))) % dec.S3[ax]
             self.floating = (sidx != 0) & (sidx != dec.S3[ax] - 1)
             self.has_p = self.floating
-            if dec.n_subdomains > 4096:
-                raise InvalidArgumentError("mode B (PressureDrop) supports up to 4096 subdomains")
         else:
             self.floating = np.ones(dec.n_subdomains, dtype=bool)
             self.has_p = np.arange(dec.n_subdomains) != 0
@@ -187,9 +191,22 @@ class BddcSetup:
         self.d_Lp = None
         self.d_Lu = None
         self._lap_ws = torch.empty(2 * N, dtype=F64, device=dev)   # multi-CTA separable solve
-        if self.mode_b:
+        self.NF = 0
+        if self.mode_b and N <= DENSE_BALANCE_MAX:
             self.d_Lp, self.d_Lu = self._dirichlet_laplacian_inverses()
-        elif N <= 4096:
+        elif self.mode_b:
+            # large N: separable solves on the floating sub-box (strips 1..S_d-2 of the
+            # drop axis), gathered from / scattered to the full subdomain vector
+            ax = system.dirichlet_axis
+            ew, dw, self.S3F = dec.laplacian_eigs(True, ax)
+            eu, _, _ = dec.laplacian_eigs(False, ax)
+            self.NF = int(np.prod(self.S3F))
+            self.d_fidx = t(np.nonzero(self.floating)[0].astype(np.int32))
+            self.d_eig_wF, self.d_dm_wF, self.d_eig_uF = t(ew, F64), t(dw, F64), t(eu, F64)
+            zf = lambda n: torch.zeros(max(n, 1), dtype=F64, device=dev)
+            self._phiF, self._zF, self._lap_wsF = zf(self.NF), zf(self.NF), zf(2 * self.NF)
+            self.w_zp, self.w_zs = zf(N), zf(N)   # z on all subdomains, zero off the floating set
+        elif N <= DENSE_BALANCE_MAX:
             ws = torch.empty(2 * N * N, dtype=F64, device=dev)
             self.d_Lp = torch.empty(N * N, dtype=F64, device=dev)
             nat.call("bddc_lap_dense", S3[0], S3[1], S3[2], _p(self.d_eig_w), _p(self.d_dm_w),
@@ -580,6 +597,16 @@ class BddcSetup:
         if self.d_Lp is not None:
             nat.call("bddc_gemv", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi), _p(self.w_z),
                      st)
+        elif self.mode_b:
+            if self.NF:
+                S3 = self.S3F
+                nat.call("bddc_gamma_flux", self.NF, _p(self.d_fidx), _p(self._phiF), _p(self.w_phi), 2, st)
+                nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_wF),
+                         _p(self.d_dm_wF), _p(self._phiF), _p(self._zF), _p(self._lap_wsF), st)
+                nat.call("bddc_gamma_flux", self.NF, _p(self.d_fidx), _p(self._zF), _p(self.w_zp), 0, st)
+            nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
+                     _p(self.w_zp), _p(y), st)
+            return
         else:
             S3 = self.dec.S3
             nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_w),
@@ -1011,13 +1038,24 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         tmax, fs_abs = torch.stack([setup.w_z.max(), W.tmpc.sum()]).tolist()
         if tmax > 1e-13 * max(fs_abs, 1.0):
             S3 = dec.S3
+            zs = setup.w_z
             if setup.d_Lu is not None:   # mode B: floating subdomains only, zero elsewhere
                 nat.call("bddc_gemv", N, N, N, _p(setup.d_Lu), _p(setup.w_phi), _p(setup.w_z), st)
+            elif setup.mode_b:
+                zs = setup.w_zs
+                if setup.NF:
+                    S3F = setup.S3F
+                    nat.call("bddc_gamma_flux", setup.NF, _p(setup.d_fidx), _p(setup._phiF),
+                             _p(setup.w_phi), 2, st)
+                    nat.call("bddc_lap_solve_mc", S3F[0], S3F[1], S3F[2], _p(setup.d_eig_uF), None,
+                             _p(setup._phiF), _p(setup._zF), _p(setup._lap_wsF), st)
+                    nat.call("bddc_gamma_flux", setup.NF, _p(setup.d_fidx), _p(setup._zF),
+                             _p(setup.w_zs), 0, st)
             else:
                 nat.call("bddc_lap_solve", S3[0], S3[1], S3[2], _p(setup.d_eig_u), None,
                          _p(setup.w_phi), _p(setup.w_z), st)
             nat.call("bddc_face_shift", ng, dec.n_faces, _p(setup.d_gface), _p(setup.d_faces),
-                     _p(setup.w_z), _p(W.wp), st)
+                     _p(zs), _p(W.wp), st)
             setup._schur(W.wp, W.Ap)
             nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
         else:
