@@ -239,6 +239,9 @@ int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double*
 void bddc_set_gemv_wpr(int wpr);
 /* Tuning knob: threads per CTA (256 or 512) of grid-stride bddc_gather_symv launches. */
 void bddc_set_symv_threads(int t);
+/* Tuning knob: bddc_prolong streams PsiT straight from HBM (1, default) or
+ * through cp.async-staged shared-memory chunks (0). */
+void bddc_set_prolong_direct(int on);
 int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out,
                  void* stream);
 int bddc_axpby(long long n, double a, const double* x, double b, double* y, void* stream);

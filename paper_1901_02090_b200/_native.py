@@ -136,6 +136,7 @@ _SIGS = {
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
     "bddc_set_gemv_wpr": [_I],
     "bddc_set_symv_threads": [_I],
+    "bddc_set_prolong_direct": [_I],
     "bddc_lap_dense": [_I, _I, _I, _P, _P, _P, _P, _P],
     "bddc_lanczos": [_I, _P, _P, _P, _P, _P],
     "bddc_axpby": [_L, _D, _P, _D, _P, _P],

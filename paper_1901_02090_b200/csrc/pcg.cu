@@ -253,6 +253,67 @@ __global__ void __launch_bounds__(256) prolong_kernel(int maxG, int maxC, const 
   }
 }
 
+// Same product without shared-memory staging: thread per slot q (QPT slots per
+// thread), the live rows of PsiT_i streamed straight from HBM, 8 rows per batch so
+// 8*QPT independent coalesced loads per thread are in flight; only the coarse
+// coefficients live in shared memory (more CTAs per SM than the staged variant).
+template <int QPT>
+__global__ void __launch_bounds__(256) prolong_direct_kernel(int maxG, int maxC, const int* __restrict__ nG,
+                                                             const int* __restrict__ nC,
+                                                             const int* __restrict__ sub_rows,
+                                                             const double* __restrict__ PsiT,
+                                                             const double* __restrict__ xc,
+                                                             const double* __restrict__ yb,
+                                                             const double* __restrict__ wout,
+                                                             double* __restrict__ outb) {
+  extern __shared__ double cf[];
+  const int i = blockIdx.x;
+  const int n = nG[i], nc = nC[i];
+  for (int r = threadIdx.x; r < nc; r += blockDim.x) {
+    const int* sr = sub_rows + ((size_t)i * maxC + r) * 4;
+    cf[r] = (double)sr[3] * xc[sr[0]];
+  }
+  __syncthreads();
+  const double* Pi = PsiT + (size_t)i * maxC * maxG;
+  double acc[QPT];
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) acc[k] = 0.0;
+  int r = 0;
+  for (; r + 8 <= nc; r += 8) {
+    double m[8][QPT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int k = 0; k < QPT; ++k) {
+        const int q = threadIdx.x + k * 256;
+        m[u][k] = (q < n) ? __ldg(Pi + (size_t)(r + u) * maxG + q) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double w = cf[r + u];
+#pragma unroll
+      for (int k = 0; k < QPT; ++k) acc[k] += m[u][k] * w;
+    }
+  }
+  for (; r < nc; ++r) {
+    const double w = cf[r];
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+      const int q = threadIdx.x + k * 256;
+      if (q < n) acc[k] += __ldg(Pi + (size_t)r * maxG + q) * w;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    const int q = threadIdx.x + k * 256;
+    if (q < n) {
+      const size_t s = (size_t)i * maxG + q;
+      const double w = yb ? yb[s] + acc[k] : acc[k];
+      outb[s] = wout ? wout[s] * w : w;
+    }
+  }
+}
+
 // y[d] = y_b[lo slot] + y_b[hi slot]
 __global__ void scatter_kernel(int n_gamma, const int* __restrict__ gown, const double* __restrict__ yb,
                                double* __restrict__ y) {
@@ -655,10 +716,25 @@ extern "C" int bddc_coarse_restrict(int nfc, const int* cown, const double* v, d
   return 0;
 }
 
+static int g_prolong_direct = 1;
+extern "C" void bddc_set_prolong_direct(int on) { g_prolong_direct = on ? 1 : 0; }
+
 extern "C" int bddc_prolong(int N, int maxG, int maxC, const int* nG, const int* nC, const int* sub_rows,
                             const double* PsiT, const double* xc, const double* yb, const double* wout, double* outb,
                             void* stream) {
   if (maxG > PRO_QPT * 256) return bddc_set_error(BDDC_ERR_ARG, "prolong: maxG too large");
+  if (g_prolong_direct) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t cshm = (size_t)maxC * sizeof(double);
+    if (maxG <= 256)
+      prolong_direct_kernel<1><<<N, 256, cshm, st>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc, yb, wout, outb);
+    else if (maxG <= 512)
+      prolong_direct_kernel<2><<<N, 256, cshm, st>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc, yb, wout, outb);
+    else
+      prolong_direct_kernel<4><<<N, 256, cshm, st>>>(maxG, maxC, nG, nC, sub_rows, PsiT, xc, yb, wout, outb);
+    LAUNCH_OK();
+    return 0;
+  }
   const bool al = !(maxG & 1) && !(((uintptr_t)PsiT) & 15);
   const int ldt = al ? ((maxG + 1) & ~1) : maxG;
   size_t shm = ((size_t)((maxC + 1) & ~1) + 2 * (size_t)PRO_RB * ldt) * sizeof(double);

@@ -100,6 +100,13 @@ def with_tgrid(tg):
     return f
 
 
+def prolong_staged():
+    nat.load().bddc_set_prolong_direct(0)
+    prolong()
+    nat.load().bddc_set_prolong_direct(1)
+
+
+pieces["prolong staged"] = prolong_staged
 only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
 def body_tgrid(tg):
     def f():
