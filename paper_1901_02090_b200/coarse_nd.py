@@ -125,7 +125,7 @@ def nd_geometry(dec, has_p=None):
 
     if dec.n_subdomains > 1:
         rec((0, 0, 0), tuple(S3), 0)
-    nodes = _contract(nodes, ND_MERGE)
+    nodes = _contract(nodes, _merge_schedule(nodes, ND_MERGE))
     _assign_pressures(nodes, dec, has_p)
     cache[has_p.tobytes()] = nodes
     return nodes
@@ -170,6 +170,22 @@ def _assign_pressures(nodes, dec, has_p):
 # solve's latency (C3 coarse solve 284 us binary, 192 us with 2, 166 us with 3,
 # 201 us with 4: the 3394-dof root front of 4 is bandwidth-bound).
 ND_MERGE = 3
+
+
+def _merge_schedule(nodes, c):
+    """Per-depth merge counts: c binary levels per node from the root down, the
+    remainder of the separator depth folded into the bottom group instead of
+    leaving a last level of tiny nodes (C3, 13 separator levels: 3,3,3,4 -> 4
+    solve levels, coarse solve 133 -> 123 us)."""
+    if isinstance(c, (list, tuple)) or not nodes:
+        return c
+    depth = 1 + max((n["depth"] for n in nodes if not n["leaf"]), default=-1)
+    if depth <= c:
+        return [max(depth, 1)]
+    sched = [c] * (depth // c)
+    if depth % c:
+        sched[-1] += depth % c
+    return sched
 
 
 def _contract(nodes, c):
