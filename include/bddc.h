@@ -83,6 +83,8 @@ int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha
  * replaces SuperLU splu (substructure.py:66, coarse.py:159) and the dense
  * coarse lu_factor (coarse.py:196).  info counts non-positive pivots. */
 size_t bddc_spd_inverse_workspace(int n, int batch, int b);
+/* Tuning knob: leaves of order <= 32 in registers (1, default) or shared memory (0). */
+void bddc_set_leaf_regs(int on);
 int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                              int* info, void* stream);
 

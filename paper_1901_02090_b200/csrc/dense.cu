@@ -345,6 +345,92 @@ __global__ void __launch_bounds__(32) leaf_chol_inv_kernel(double* M, int nb, in
   }
 }
 
+// The same leaf for nb <= 32 entirely in registers: lane c owns column c (padding
+// columns c >= nb carry the identity), the row broadcasts go through warp
+// shuffles instead of shared-memory column walks (the shared-memory version is
+// bound by shared-memory bandwidth: 2 loads per FMA).  Cholesky and the
+// triangular inverse are 496 shuffle+FMA steps each, V V^T 528.
+template <int MODE>
+__global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info) {
+  __shared__ double tsm[32][33];
+  const unsigned FULL = 0xffffffffu;
+  const int c = threadIdx.x;
+  double* Mz = M + blockIdx.x * sM;
+  double x[32];
+  if (MODE & 1) {
+    double u[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      double v = (c >= nb && r == c) ? 1.0 : 0.0;
+      if (r < nb && c < nb && r <= c) v = Mz[(size_t)r * ld + c];
+      u[r] = v;
+    }
+    // right-looking upper Cholesky M = U^T U
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      double d = __shfl_sync(FULL, u[k], k);
+      if (!(d > 0.0)) {
+        bad = 1;
+        d = 1.0;
+      }
+      d = sqrt(d);
+      const double id = 1.0 / d;
+      u[k] = (c > k) ? u[k] * id : (c == k ? d : u[k]);
+#pragma unroll
+      for (int r = k + 1; r < 32; ++r) {
+        const double ukr = __shfl_sync(FULL, u[k], r);
+        if (c >= r) u[r] -= ukr * u[k];
+      }
+    }
+    if (c == 0 && bad) atomicAdd(info, 1);
+    // V = U^-1: column c solves U v = e_c by a backward sweep over the columns of U
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x[r] = (r == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 31; k >= 0; --k) {
+      const double ukk = __shfl_sync(FULL, u[k], k);
+      x[k] = x[k] / ukk;
+#pragma unroll
+      for (int i = 0; i < k; ++i) {
+        const double uik = __shfl_sync(FULL, u[i], k);
+        x[i] -= uik * x[k];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x[r] = (r < nb && c < nb && r <= c) ? Mz[(size_t)r * ld + c] : 0.0;
+  }
+  if (MODE & 2) {
+    // X = V V^T: lane c takes row c of V through shared memory, then
+    // X[i][c] = sum_k V[i][k] V[c][k] with V[i][k] (k >= i) shuffled from lane i
+#pragma unroll
+    for (int r = 0; r < 32; ++r) tsm[r][c] = x[r];
+    __syncwarp();
+    double rw[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) rw[k] = tsm[c][k];
+    double o[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+#pragma unroll
+      for (int i = 0; i <= k; ++i) o[i] += __shfl_sync(FULL, rw[k], i) * rw[k];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      if (r < nb && c < nb && r <= c) {
+        Mz[(size_t)r * ld + c] = o[r];
+        if (MODE == 3) Mz[(size_t)c * ld + r] = o[r];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < nb && c < nb) Mz[(size_t)r * ld + c] = (r <= c) ? x[r] : 0.0;
+  }
+}
+
 // Zero / copy an r x c block (row-major, leading dim ld, batch stride sM / sW).
 __global__ void block_copy_kernel(double* dst, int ld, long long sD, const double* src, int lds, long long sS,
                                   int rows, int cols) {
@@ -463,7 +549,16 @@ int trmm_launch(int right, int n1, int n2, double alpha, const double* U, double
   return 0;
 }
 
+static int g_leaf_regs = 1;
+
 int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
+  if (n <= 32 && g_leaf_regs) {
+    if (mode == 1) leaf32_chol_inv_kernel<1><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
+    else if (mode == 2) leaf32_chol_inv_kernel<2><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
+    else leaf32_chol_inv_kernel<3><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
+    LAUNCH_OK();
+    return 0;
+  }
   size_t shm = (size_t)n * (n + 1) * sizeof(double);
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -540,6 +635,8 @@ int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* 
 }
 
 }  // namespace
+
+extern "C" void bddc_set_leaf_regs(int on) { g_leaf_regs = on ? 1 : 0; }
 
 // In-place inverse of `batch` SPD matrices of order n (full symmetric storage,
 // leading dim ld, batch stride sM): M = U^T U, V = U^-1, M^-1 = V V^T, all

@@ -6,8 +6,10 @@ from paper_1901_02090_b200 import _native as nat
 lib = nat.load()
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 res = {}
-for (bt, n) in [(2244, 512), (2244, 448), (1, 2304), (1, 8960), (2244, 160)]:
-    for b in (32, 64):
+import itertools
+for (bt, n), regs in itertools.product([(2244, 512), (2244, 448), (2244, 160), (2244, 32), (1, 2304)], (1, 0)):
+    lib.bddc_set_leaf_regs(regs)
+    for b in (32,):
         if n % b:
             continue
         X = torch.randn(min(bt, 64), n, n, dtype=torch.float64, device="cuda")
@@ -26,6 +28,6 @@ for (bt, n) in [(2244, 512), (2244, 448), (1, 2304), (1, 8960), (2244, 160)]:
         e0.record(); run(); e1.record(); torch.cuda.synchronize()
         t = (e0.elapsed_time(e1) - e2.elapsed_time(e3)) / 1000
         err = float((M[0] @ A0[0] - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max())
-        res[f"{bt}x{n} b={b}"] = dict(ms=round(t * 1000, 3), tflops=round(bt * n ** 3 / t / 1e12, 2), err=err)
-        print(f"{bt}x{n} b={b}: {t*1000:.2f} ms  {bt*n**3/t/1e12:.2f} TF/s  |MA-I|={err:.1e}", flush=True)
+        res[f"{bt}x{n} b={b} regs={regs}"] = dict(ms=round(t * 1000, 3), tflops=round(bt * n ** 3 / t / 1e12, 2), err=err)
+        print(f"{bt}x{n} b={b} regs={regs}: {t*1000:.2f} ms  {bt*n**3/t/1e12:.2f} TF/s  |MA-I|={err:.1e}", flush=True)
 json.dump(res, open("gpurun_out/spd_bench.json", "w"), indent=1)
