@@ -394,6 +394,8 @@ class BddcSetup:
         self.w_z = z(N)
         self.w_dot = torch.zeros(nat.load().bddc_dot_workspace() // 8 + 1, dtype=F64, device=dev)
         self.w_scal = z(16)
+        self.w_norms = z(8)     # deferred per-solve norms (_N_* slots)
+        self._host_norms = torch.zeros(8, dtype=F64, pin_memory=True)
         self.d_dct = torch.empty(sum(n * n + n for n in dec.n3), dtype=F64, device=dev)
         nat.call("bddc_dct_init", gp, _p(self.d_dct), st)
         self._graphs = {}
@@ -892,6 +894,21 @@ def _norm(setup, x, n):
     return math.sqrt(float(setup.w_scal[10].item()))
 
 
+# deferred squared norms of one solve (read with the next unavoidable host sync)
+_N_FS, _N_DD, _N_R0, _N_PDEN, _N_PNUM = range(5)
+
+
+def _norm2_async(setup, x, n, slot):
+    nat.call("bddc_dot", _p(x), _p(x), int(n), _p(setup.w_dot), _p(setup.w_norms), 100 + slot,
+             None, _stream())
+
+
+def _norms_to_host(setup):
+    """Queue the copy of the deferred norms; valid after the stream's next sync."""
+    setup._host_norms.copy_(setup.w_norms, non_blocking=True)
+    return setup._host_norms
+
+
 def solve(system, dec, config, u_exact=None, setup=None, iterate_callback=None,
           f_device=None, return_device=False):
     """Three-step method + pressure recovery (solver.py:301-398)."""
@@ -998,9 +1015,10 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     # div_defect = fs - Bs u*
     nat.call("bddc_cell_div", gp, _p(W.us), _p(W.fs), 1.0, -1.0, _p(setup.d_cell_sub),
              _p(setup.d_Dsub), _p(W.dd), st)
-    nfs = _norm(setup, W.fs, G.n_cells)
-    # relative to |fs| (solver.py:331-333); absolute when there is no source (mode B)
-    defect_norm = _norm(setup, W.dd, G.n_cells) / (nfs if nfs > 0 else 1.0)
+    # |fs|, |div defect| (read with the next host sync)
+    _norm2_async(setup, W.fs, G.n_cells, _N_FS)
+    _norm2_async(setup, W.dd, G.n_cells, _N_DD)
+    defect_norm = None
     # step 3 rhs: r = g - A u* (g = 0 in mode A, solver.py:342); r_G -= sum condense
     if gv is not None:
         nat.call("bddc_axpby", G.n_flux, 1.0, _p(gv), 0.0, _p(W.rf), st)
@@ -1019,7 +1037,8 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
             # the uncondensed one means Steps 1-2 already solved the problem (e.g. a
             # homogeneous field whose solution the coarse space contains); PCG
             # on it would only chase rounding (the reference stops on r0 == 0 only)
-            r_floor = 1e-12 * _norm(setup, W.r, ng)
+            _norm2_async(setup, W.r, ng, _N_R0)
+            r_floor = None   # 1e-12 |r_uncondensed|, read in _pcg's first sync
         a = nat.LocalSolveArgs()
         a.f_flux, a.f_scale = _p(W.rf).value, 1.0
         a.g_cell, a.g_scale = _p(W.dd).value, 1.0
@@ -1035,7 +1054,10 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         # be a fresh device allocation)
         torch.abs(setup.w_phi, out=setup.w_z)
         torch.abs(W.fs, out=W.tmpc)
-        tmax, fs_abs = torch.stack([setup.w_z.max(), W.tmpc.sum()]).tolist()
+        tmax, fs_abs, nfs2, dd2 = torch.stack([setup.w_z.max(), W.tmpc.sum(),
+                                              setup.w_norms[_N_FS], setup.w_norms[_N_DD]]).tolist()
+        # relative to |fs| (solver.py:331-333); absolute when there is no source (mode B)
+        defect_norm = math.sqrt(dd2) / (math.sqrt(nfs2) if nfs2 > 0 else 1.0)
         if tmax > 1e-13 * max(fs_abs, 1.0):
             S3 = dec.S3
             zs = setup.w_z
@@ -1074,16 +1096,27 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         a.u_out, a.u_mode = _p(W.u).value, 1
         nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
                  _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
+    if not return_device and not first:
+        # u is final: stream it to the host while the pressure is recovered
+        (host["u"],) = _d2h_async(setup, (W.u,))
     # pressure recovery: B B^T p = B(g - A u), zero mean in mode A
-    p_warn = _recover_pressure(setup, W, config.tol, gv)
+    _recover_pressure(setup, W, gv)
     omega = setup.omega_tilde if setup.omega_tilde is not None else float("nan")
     if return_device:
         return W, w_cg_it, kappa, history, converged
+    hn = _norms_to_host(setup)
     if first:
         host = {"u": W.u.cpu(), "p": W.pc.cpu(), "u0": W.u0.cpu(), "us": W.us.cpu()}
     else:
-        host["u"], host["p"] = _d2h_async(setup, (W.u, W.pc))
+        (host["p"],) = _d2h_async(setup, (W.pc,))
         setup.copy_stream.synchronize()
+    torch.cuda.current_stream().synchronize()
+    hn = hn.tolist()
+    if defect_norm is None:
+        defect_norm = math.sqrt(hn[_N_DD]) / (math.sqrt(hn[_N_FS]) if hn[_N_FS] > 0 else 1.0)
+    den, num = math.sqrt(hn[_N_PDEN]), math.sqrt(hn[_N_PNUM])
+    # solver.py:271-273: warn if |A u + B^T p - g| > 10 tol |A u - g|
+    p_warn = bool(den > 0 and num > 10.0 * config.tol * den)
     report = SolveReport(
         u=host["u"].numpy(), p=host["p"].numpy(), it=w_cg_it, kappa=kappa,
         omega_tilde=omega, n_c=setup.n_c, residuals=history,
@@ -1124,7 +1157,7 @@ def _scale_fs(setup, f, fs):
              _p(setup.d_Dsub), _p(fs), _stream())
 
 
-def _recover_pressure(setup, W, tol, gv=None):
+def _recover_pressure(setup, W, gv=None):
     """solver.py:254-274: (B B^T) p = B(g - A u) by the separable cosine (mode A,
     pure Neumann: zero-mean p) or cosine/sine (mode B: Dirichlet ends) transform."""
     G = setup.geom
@@ -1140,10 +1173,9 @@ def _recover_pressure(setup, W, tol, gv=None):
         ones = _ones(setup, G.n_cells)
         _dot(setup, W.pc, ones, G.n_cells, 100 + 11)
         nat.call("bddc_sub_mean", G.n_cells, _p(setup.w_scal[11:]), _p(W.pc), st)
-    den = _norm(setup, W.rf, G.n_flux)
+    _norm2_async(setup, W.rf, G.n_flux, _N_PDEN)
     nat.call("bddc_grad", gp, _p(W.pc), 1.0, 1.0, _p(W.rf), st)
-    num = _norm(setup, W.rf, G.n_flux)
-    return bool(den > 0 and num > 10.0 * tol * den)
+    _norm2_async(setup, W.rf, G.n_flux, _N_PNUM)
 
 
 def _ones(setup, n):
@@ -1240,7 +1272,11 @@ def _pcg(setup, W, config, callback, r_floor=0.0):
     _dot(setup, W.r, W.r, ng, 4, B.res)
     host = setup._host_scal
     host.copy_(scal, non_blocking=True)
+    if r_floor is None:
+        hn = _norms_to_host(setup)
     torch.cuda.current_stream().synchronize()
+    if r_floor is None:
+        r_floor = 1e-12 * math.sqrt(float(hn[_N_R0]))
     if host[4] <= r_floor:   # host[4] = ||r0||
         return 0, 1.0, np.array([1.0]), True
     if callback is None and not setup.force_eager:
