@@ -174,11 +174,13 @@ int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, int K, const
                      void* stream);
 /* Solves on the compact per-node layout (info = {s, bf, sep_ptr, bnd_ptr, cb_off}). */
 /* tasks are triplets {node, row0, row1}; fwd gathers the level's separator
- * right-hand sides into rsbuf (ysize entries) first. */
+ * right-hand sides into rsbuf (ysize entries) first.  xdirect != NULL (a level
+ * whose nodes have no boundary, i.e. the root): the separator solution is final
+ * after the forward sweep and is written to x directly (no bwd for that level). */
 int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
                 const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
-                void* stream);
+                double* xdirect, void* stream);
 /* bwd: wpr (1, 2, 4, 8) warps share one separator row (tasks then hold 8/wpr rows per pass). */
 int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,

@@ -111,7 +111,7 @@ _SIGS = {
     "bddc_pcg_cond": [_P, _P, _D, _I, _P],
     "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
                          _P, _P, _I, _P],
-    "bddc_nd_fwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_fwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_nd_compact": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_nd_qd": [_I, _I, _I, _I, _I, _P, _P],
     "bddc_nd_bwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],

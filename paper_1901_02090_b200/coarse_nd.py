@@ -578,11 +578,15 @@ class CoarseND:
         st = _stream()
         ys, cb = self._bufs()
         for li, L in enumerate(self.levels):
+            # a level without boundary (the root) writes its solution directly
+            direct = L.bmax == 0
             nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
-                     _p(cb), st)
+                     _p(cb), _p(x) if direct else None, st)
         for li in range(len(self.levels) - 1, -1, -1):
             L = self.levels[li]
+            if L.bmax == 0:
+                continue
             nat.call("bddc_nd_bwd", L.n_bt, L.bmax, L.wpr, _p(L.btasks), _p(L.info), _p(L.data_off),
                      _p(L.sep_flat), _p(L.bnd_flat), _p(L.Fc), _p(ys[li]), _p(x), st)
 

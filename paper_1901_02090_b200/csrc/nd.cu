@@ -93,7 +93,7 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
                               const int* __restrict__ lptr, const int* __restrict__ lsrc,
                               const double* __restrict__ Fc, const double* __restrict__ r,
                               const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf,
-                              int lpe) {
+                              int lpe, double* __restrict__ xdirect) {
   extern __shared__ double rsm[];
   pdl_trigger();
   const int q = tasks[3 * blockIdx.x], row0 = tasks[3 * blockIdx.x + 1], row1 = tasks[3 * blockIdx.x + 2];
@@ -124,8 +124,13 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
     if (lane < nr) {
       const double v = lane == 0 ? acc[0] : lane == 1 ? acc[1] : lane == 2 ? acc[2] : acc[3];
       const int rr = row + lane;
-      if (rr < s) ybuf[sp + rr] = v;
-      else cbuf[cbo + rr - s] = v;
+      if (rr < s) {
+        // a node without boundary (the root) is final after the forward sweep
+        if (xdirect) xdirect[sep_flat[sp + rr]] = v;
+        else ybuf[sp + rr] = v;
+      } else {
+        cbuf[cbo + rr - s] = v;
+      }
     }
   }
 }
@@ -257,7 +262,7 @@ extern "C" int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, i
 extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
                            const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
                            const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
-                           void* stream) {
+                           double* xdirect, void* stream) {
   if (ntasks <= 0 || ysize <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   // small separators: every task gathers its own r_sep (lanes per entry so one
@@ -269,7 +274,7 @@ extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, co
   size_t shm = (size_t)(smax > 0 ? smax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   PDL_LAUNCH(nd_fwd_kernel, dim3(ntasks), dim3(256), shm, st, tasks, info, data_off, sep_flat, lptr, lsrc, Fc, r,
-             (const double*)rsbuf, ybuf, cbuf, lpe);
+             (const double*)rsbuf, ybuf, cbuf, lpe, xdirect);
   return 0;
 }
 
