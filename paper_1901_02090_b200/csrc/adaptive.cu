@@ -39,10 +39,11 @@ __device__ int sturm_below(const double* d, const double* e, int m, double x, do
   return cnt;
 }
 
-// One inverse-iteration solve (T - lam I) x = b for a symmetric tridiagonal with
-// partial pivoting (LAPACK dgttrf/dgtts2 pattern); b is overwritten by x.
-__device__ void tri_shift_solve(const double* d0, const double* e0, int m, double lam, double tiny, double* dd,
-                                double* du, double* du2, double* dl, unsigned char* piv, double* b) {
+// Inverse iteration on (T - lam I) for a symmetric tridiagonal with partial
+// pivoting (LAPACK dgttrf/dgtts2 pattern): tri_shift_factor once per shift,
+// tri_shift_apply per iteration (b overwritten by the solution).
+__device__ void tri_shift_factor(const double* d0, const double* e0, int m, double lam, double tiny, double* dd,
+                                 double* du, double* du2, double* dl, unsigned char* piv) {
   for (int i = 0; i < m; ++i) {
     dd[i] = d0[i] - lam;
     if (i < m - 1) {
@@ -73,6 +74,10 @@ __device__ void tri_shift_solve(const double* d0, const double* e0, int m, doubl
     }
   }
   if (dd[m - 1] == 0.0) dd[m - 1] = tiny;
+}
+
+__device__ void tri_shift_apply(int m, const double* dd, const double* du, const double* du2, const double* dl,
+                                const unsigned char* piv, double* b) {
   for (int i = 0; i < m - 1; ++i) {
     if (!piv[i]) {
       b[i + 1] -= dl[i] * b[i];
@@ -129,46 +134,41 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     Y[s * ld + t] = Ii[(size_t)as * mg + at] + Ij[(size_t)bs * mg + bt];
   }
   __syncthreads();
-  // ---- Cholesky M = R R^T (lower, in Y)
+  // ---- Cholesky M = R R^T (lower, in Y): every thread takes the pivot itself
+  // (two barriers per column), trailing update warp per row, lanes over columns
   for (int k = 0; k < m; ++k) {
-    if (threadIdx.x == 0) {
-      double d = Y[k * ld + k];
-      if (!(d > 0.0)) {
-        bad = 1;
-        d = 1.0;
-      }
-      Y[k * ld + k] = sqrt(d);
+    double d = Y[k * ld + k];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) bad = 1;
+      d = 1.0;
     }
-    __syncthreads();
-    double dk = Y[k * ld + k];
+    const double dk = sqrt(d);
     for (int r = k + 1 + threadIdx.x; r < m; r += blockDim.x) Y[r * ld + k] /= dk;
     __syncthreads();
-    const int w = m - k - 1;
-    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-      int r = k + 1 + e / w, c = k + 1 + e % w;
-      if (c <= r) Y[r * ld + c] -= Y[r * ld + k] * Y[c * ld + k];
+    if (threadIdx.x == 0) Y[k * ld + k] = dk;   // read again only after the next barrier
+    for (int r = k + 1 + warp; r < m; r += nw) {
+      const double yrk = Y[r * ld + k];
+      for (int c = k + 1 + lane; c <= r; c += 32) Y[r * ld + c] -= yrk * Y[c * ld + k];
     }
     __syncthreads();
   }
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int r = e / m, c = e % m;
-    if (c > r) Y[r * ld + c] = 0.0;
-  }
+  for (int r = warp; r < m; r += nw)
+    for (int c = r + 1 + lane; c < m; c += 32) Y[r * ld + c] = 0.0;
   __syncthreads();
-  // ---- T1 = A R (global scratch), then X = R^T T1, both one-shot
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int r = e / m, c = e % m;
-    double acc = 0.0;
-    for (int k = c; k < m; ++k) acc += X[r * ld + k] * Y[k * ld + c];
-    T1[(size_t)r * m + c] = acc;
-  }
+  // ---- T1 = A R (global scratch), then X = R^T T1, both one-shot (warp per row)
+  for (int r = warp; r < m; r += nw)
+    for (int c = lane; c < m; c += 32) {
+      double acc = 0.0;
+      for (int k = c; k < m; ++k) acc += X[r * ld + k] * Y[k * ld + c];
+      T1[(size_t)r * m + c] = acc;
+    }
   __syncthreads();
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int r = e / m, c = e % m;
-    double acc = 0.0;
-    for (int k = r; k < m; ++k) acc += Y[k * ld + r] * T1[(size_t)k * m + c];
-    X[r * ld + c] = acc;
-  }
+  for (int r = warp; r < m; r += nw)
+    for (int c = lane; c < m; c += 32) {
+      double acc = 0.0;
+      for (int k = r; k < m; ++k) acc += Y[k * ld + r] * T1[(size_t)k * m + c];
+      X[r * ld + c] = acc;
+    }
   __syncthreads();
   // ---- symmetrise and project out q = R^T 1 / |R^T 1|
   double* qv = vec;       // m
@@ -179,14 +179,12 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
     qv[r] = acc;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int r = e / m, c = e % m;
-    if (c > r) {
+  for (int r = warp; r < m; r += nw)
+    for (int c = r + 1 + lane; c < m; c += 32) {
       double v = 0.5 * (X[r * ld + c] + X[c * ld + r]);
       X[r * ld + c] = v;
       X[c * ld + r] = v;
     }
-  }
   double nq = 0.0;
   for (int r = threadIdx.x; r < m; r += blockDim.x) nq += qv[r] * qv[r];
   nq = sqrt(block_sum(nq, red));
@@ -201,22 +199,24 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   double sq = 0.0;
   for (int r = threadIdx.x; r < m; r += blockDim.x) sq += qv[r] * bq[r];
   sq = block_sum(sq, red);
-  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    int r = e / m, c = e % m;
-    X[r * ld + c] += -qv[r] * bq[c] - bq[r] * qv[c] + sq * qv[r] * qv[c];
+  for (int r = warp; r < m; r += nw) {
+    const double qr = qv[r], br = bq[r];
+    for (int c = lane; c < m; c += 32) X[r * ld + c] += -qr * bq[c] - br * qv[c] + sq * qr * qv[c];
   }
   __syncthreads();
-  // ---- Householder tridiagonalisation of X (Y rows hold the reflectors v_j)
+  // ---- Householder tridiagonalisation of X (Y rows hold the reflectors v_j).
+  // Three barriers per column: the column norm and v.p are reduced by every warp
+  // itself (same lane partition and shuffle tree in every warp: identical values),
+  // and q = p - K v is formed inside the rank-2 update.
   double* pv = vec;       // m
-  double* qq = vec + m;   // m
   for (int jj = 0; jj + 2 < m; ++jj) {
     const int n1 = m - jj - 1;   // length of the column below the diagonal
     double sx = 0.0;
-    for (int r = threadIdx.x; r < n1; r += blockDim.x) {
-      double v = X[(jj + 1 + r) * ld + jj];
-      sx += v * v;
+    for (int r = lane; r < n1; r += 32) {
+      const double t = X[(jj + 1 + r) * ld + jj];
+      sx += t * t;
     }
-    sx = block_sum(sx, red);
+    for (int o = 16; o > 0; o >>= 1) sx += __shfl_xor_sync(0xffffffffu, sx, o);
     const double x0 = X[(jj + 1) * ld + jj];
     const double nrm = sqrt(sx);
     const double alpha = (x0 >= 0.0) ? -nrm : nrm;
@@ -240,13 +240,12 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
       }
       __syncthreads();
       double K = 0.0;
-      for (int r = jj + 1 + threadIdx.x; r < m; r += blockDim.x) K += v[r] * pv[r];
-      K = block_sum(K, red);
-      for (int r = jj + 1 + threadIdx.x; r < m; r += blockDim.x) qq[r] = pv[r] - K * v[r];
-      __syncthreads();
-      for (int e = threadIdx.x; e < n1 * n1; e += blockDim.x) {
-        int r = jj + 1 + e / n1, c = jj + 1 + e % n1;
-        X[r * ld + c] -= 2.0 * (v[r] * qq[c] + qq[r] * v[c]);
+      for (int r = jj + 1 + lane; r < m; r += 32) K += v[r] * pv[r];
+      for (int o = 16; o > 0; o >>= 1) K += __shfl_xor_sync(0xffffffffu, K, o);
+      for (int r = jj + 1 + warp; r < m; r += nw) {
+        const double vr = v[r], qr = pv[r] - K * vr;
+        for (int c = jj + 1 + lane; c < m; c += 32)
+          X[r * ld + c] -= 2.0 * (vr * (pv[c] - K * v[c]) + qr * v[c]);
       }
       if (threadIdx.x == 0) {
         X[(jj + 1) * ld + jj] = alpha;
@@ -315,21 +314,27 @@ __global__ void pair_eig_kernel(bddc_geom G, const int* __restrict__ faces, cons
   __syncthreads();
   const int k = ksel;
   // ---- inverse iteration, one thread per selected eigenvalue; vectors -> X rows
+  // (one factorisation per shift; the factor arrays live in the rows of X behind
+  // the k vectors when they fit, in local memory otherwise)
   if (threadIdx.x < k) {
     const int l = threadIdx.x;
     const double lv = lam[m - 1 - l];
-    double dd[PAIR_MMAX], du[PAIR_MMAX], du2[PAIR_MMAX], dl[PAIR_MMAX], b[PAIR_MMAX];
+    double loc[4 * PAIR_MMAX];
+    double* fac = (5 * k <= m) ? X + (size_t)(k + 4 * l) * ld : loc;
+    const int fs = (5 * k <= m) ? ld : PAIR_MMAX;
+    double *dd = fac, *du = fac + fs, *du2 = fac + 2 * fs, *dl = fac + 3 * fs;
+    double* b = X + (size_t)l * ld;
     unsigned char pvt[PAIR_MMAX];
     for (int r = 0; r < m; ++r) b[r] = 1.0 + 0.5 * sin(1.7 * (r + 1) + 0.61 * (l + 1));
     const double tiny = fmax(2.2e-16 * tnorm, 1e-300);
+    tri_shift_factor(dg, eo, m, lv, tiny, dd, du, du2, dl, pvt);
     for (int it = 0; it < 3; ++it) {
-      tri_shift_solve(dg, eo, m, lv, tiny, dd, du, du2, dl, pvt, b);
+      tri_shift_apply(m, dd, du, du2, dl, pvt, b);
       double nb = 0.0;
       for (int r = 0; r < m; ++r) nb += b[r] * b[r];
       nb = 1.0 / sqrt(nb);
       for (int r = 0; r < m; ++r) b[r] *= nb;
     }
-    for (int r = 0; r < m; ++r) X[l * ld + r] = b[r];
   }
   __syncthreads();
   // full reorthogonalisation in descending-eigenvalue order (fixes near-degenerate clusters)
