@@ -243,6 +243,9 @@ int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double*
 void bddc_set_gemv_wpr(int wpr);
 /* Tuning knob: threads per CTA (256 or 512) of grid-stride bddc_gather_symv launches. */
 void bddc_set_symv_threads(int t);
+/* Tuning knob: threads per CTA (256 or 512) of bddc_pair_eigs launches whose
+ * faces need more than half an SM's shared memory (default 512). */
+void bddc_set_pair_threads(int t);
 /* Tuning knob: bddc_prolong streams PsiT straight from HBM (1, default) or
  * through cp.async-staged shared-memory chunks (0). */
 void bddc_set_prolong_direct(int on);

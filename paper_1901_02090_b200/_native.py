@@ -137,6 +137,7 @@ _SIGS = {
     "bddc_set_gemv_wpr": [_I],
     "bddc_set_leaf_regs": [_I],
     "bddc_set_symv_threads": [_I],
+    "bddc_set_pair_threads": [_I],
     "bddc_set_prolong_direct": [_I],
     "bddc_lap_dense": [_I, _I, _I, _P, _P, _P, _P, _P],
     "bddc_lanczos": [_I, _P, _P, _P, _P, _P],

@@ -611,6 +611,9 @@ extern "C" int bddc_multiscale_rows(const bddc_geom* g, const int* faces, const 
   return 0;
 }
 
+static int g_pair_threads_big = 512;
+extern "C" void bddc_set_pair_threads(int t) { g_pair_threads_big = (t == 512) ? 512 : 256; }
+
 extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* fslot, const double* S,
                               const double* Sinv, const double* delta, double tau, int maxsel, double* lam_out,
                               int lam_ld, int* nsel, int* nadd, double* rows, double* omega, double* scratch,
@@ -624,10 +627,12 @@ extern "C" int bddc_pair_eigs(const bddc_geom* g, const int* faces, const int* f
   const int m = flist ? imin(mmax, g->maxF) : g->maxF;
   const int ld = m + ((m & 1) ? 0 : 1);
   size_t shm = (size_t)(2 * m * ld + 4 * m + 3 * (m / 2 + 1)) * sizeof(double) + 2 * m * sizeof(int) + 16;
-  // one CTA per face; the per-thread inverse-iteration arrays live in local memory
+  // one CTA per face; faces whose two m x m blocks leave room for one CTA per SM
+  // only get 512 threads (latency hiding of the shared-memory sweeps)
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(pair_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  pair_eig_kernel<<<nblk, 256, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel, lam_out,
+  const int threads = (shm > 113 * 1024) ? g_pair_threads_big : 256;
+  pair_eig_kernel<<<nblk, threads, shm, (cudaStream_t)stream>>>(*g, faces, fslot, S, Sinv, delta, tau, maxsel, lam_out,
                                                             lam_ld, nsel, nadd, rows, omega, scratch, qbasis, err,
                                                             flist, full);
   LAUNCH_OK();
