@@ -299,7 +299,9 @@ class CoarseND:
         self.maxC = maxC
         self.factored = False
         self.levels = []
-        t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        def t(a, dt=I32):   # async upload (no wait for the queued device work)
+            h = torch.from_numpy(np.ascontiguousarray(a)).to(dt)
+            return h.pin_memory().to(dev, non_blocking=True)
         if not (N > 1 and nfc):
             self.cb_total = 1
             return
@@ -518,8 +520,7 @@ class CoarseND:
             nat.call("bddc_dgemm_batched", 0, 0, L.B, L.B, L.S, -1.0, _p(L.X), L.S,
                      L.B * L.S, _p(F12), L.nf, L.nf * L.nf, 1.0, _p(F22), L.nf,
                      L.nf * L.nf, L.m, 0, st)
-        if int(info.item()):
-            raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
+        self._factor_info = info   # checked by check() after the setup's final sync
         self.factored = True
         for L in self.levels:
             L.Fc = torch.empty(max(L.csize, 1), dtype=F64, device=self.dev)
@@ -562,6 +563,10 @@ class CoarseND:
                  1.0, _p(A), nf, sF, m, 0, st)
         nat.call("bddc_nd_qd", 0, m, Sf, Sp, nf, _p(L.F), st)
         nat.call("bddc_nd_qd", 1, m, Sf, Sp, nf, _p(L.F), st)
+
+    def check(self):
+        if int(self._factor_info.item()):
+            raise ConfigurationError("coarse problem singular (non-positive pivot in S_Pi)")
 
     def release_fronts(self):
         """Drop the padded factorisation fronts (the solves read the compact copies)."""

@@ -167,7 +167,8 @@ __global__ void copy_kernel(const double* __restrict__ a, double* __restrict__ b
 }  // namespace
 
 // Per-subdomain coarse pieces (part 1: Kc, Psi, b0 and the live-size table dims;
-// part 2: T, after part 1 ran; 3: both).  Workspaces: Ct, Y, E (N*maxG*maxC each),
+// part 2: T, independent of part 1 when given its own Ct, Y, inv_ws and dims;
+// 3: both).  Workspaces: Ct, Y, E (N*maxG*maxC each),
 // inv_ws (bddc_spd_inverse_workspace(max(maxC, maxG), N, 32|64)), gamma (N).
 extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const int* faces, const int* fslot,
                                  const int* gcode, const int* nG, const double* rows, const double* qbasis,
@@ -207,6 +208,12 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   LAUNCH_OK();
   }
   if (!(part & 2)) return 0;
+  if (!(part & 1)) {
+    // part 2 alone (concurrently with part 1 on another stream, with its own Ct, Y,
+    // workspace and dims): the live-size table first
+    coarse_dims_kernel<<<(N + 127) / 128, 128, 0, s>>>(N, maxC, nG, sub_rows, dims);
+    LAUNCH_OK();
+  }
   // ---- T = (P S P + g Q Q^T)^-1 - Q Q^T / g   (Q in Ct, S Q in Y, Q^T S Q in E[..maxC^2])
   qc_kernel<<<N, 128, 0, s>>>(*g, sub_rows, faces, fslot, qbasis, maxsel, maxC, Ct);
   LAUNCH_OK();

@@ -115,6 +115,14 @@ def _geom(dec, system=None):
     return g
 
 
+def _upload(a, dt, dev):
+    """Host table -> device without a stream sync: staged through pinned memory
+    (torch's caching host allocator keeps the block until the async copy ran).
+    torch.as_tensor(..., device=cuda) would wait for all queued device work."""
+    h = torch.from_numpy(np.ascontiguousarray(a)).to(dt)
+    return h.pin_memory().to(dev, non_blocking=True)
+
+
 def _pad(n, m):
     return max(m, ((n + m - 1) // m) * m)
 
@@ -169,7 +177,7 @@ class BddcSetup:
         self.side_stream = torch.cuda.Stream(device=dev, priority=-1)
         N, mg, mp = dec.n_subdomains, dec.maxG, dec.maxP
         self.N, self.maxG, self.maxP = N, mg, mp
-        t = lambda a, dt=I32: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+        t = lambda a, dt=I32: _upload(a, dt, dev)
         # topology tables
         self.d_gpos = t(dec.gpos)
         self.d_gcode = t(dec.gcode)
@@ -215,7 +223,7 @@ class BddcSetup:
         self.d_eig_u = t(eig_u, F64)
         # permeability -> cell coefficients, D, delta
         k = np.ascontiguousarray(system.perm.k, dtype=np.float64)
-        self.d_k = torch.as_tensor(k, device=dev)
+        self.d_k = _upload(k, F64, dev)
         self.d_coef = torch.empty(G.n_cells * 3, dtype=F64, device=dev)
         nat.call("bddc_cell_coeffs", gp, _p(self.d_k), _p(self.d_coef), st)
         self.d_Dsub = torch.empty(N, dtype=F64, device=dev)
@@ -338,8 +346,7 @@ class BddcSetup:
         self.d_Psi = torch.empty(N * mg * maxC, dtype=F64, device=dev)
         self.d_T = torch.empty(N * mg * mg, dtype=F64, device=dev)
         self.d_b0 = torch.empty(N * maxC, dtype=F64, device=dev)
-        wsz = max(nat.load().bddc_spd_inverse_workspace(maxC, N, 32),
-                  nat.load().bddc_spd_inverse_workspace(mg, N, 64))
+        wsz = nat.load().bddc_spd_inverse_workspace(maxC, N, 32)
         ws = torch.empty(wsz // 8 + 2, dtype=F64, device=dev)
         dims = torch.empty(N * 16, dtype=I32, device=dev)
         cl_args = [gp, _p(dev_rows), _p(self.d_faces), _p(self.d_fslot), _p(self.d_gcode),
@@ -347,19 +354,27 @@ class BddcSetup:
                    _p(self.d_S), _p(Sinv), _p(self.d_Dsub), maxC, _p(Ct), _p(Y), _p(E), _p(gam),
                    _p(self.d_Kc), _p(self.d_Psi), _p(self.d_T), _p(self.d_b0), _p(ws), _p(dims),
                    _p(info[2:])]
-        nat.call("bddc_coarse_local", *cl_args, 1, st)
-        # T_i (its batched inverse) on a side stream, concurrently with the global coarse
-        # factorisation below, whose small-batch inverses are latency-bound
+        # T_i (its batched inverse) on a side stream with its own workspaces, concurrently
+        # with Kc / Psi / b0 and then the global coarse factorisation (the critical
+        # path: host symbolic analysis, latency-bound small-batch inverses)
         npk = nat.load().bddc_sym_packed_elems(mg)
         self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
         self.d_Tp = torch.empty(N * npk, dtype=F64, device=dev)
+        Ct2 = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        Y2 = torch.empty(N * mg * maxC, dtype=F64, device=dev)
+        ws2 = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, 32) // 8 + 2,
+                          dtype=F64, device=dev)
+        dims2 = torch.empty(N * 16, dtype=I32, device=dev)
         main = torch.cuda.current_stream()
         side = torch.cuda.Stream(device=dev)   # normal priority: the ND branch is the critical path
         side.wait_stream(main)
+        cl2 = list(cl_args)
+        cl2[13], cl2[14], cl2[21], cl2[22], cl2[23] = _p(Ct2), _p(Y2), _p(ws2), _p(dims2), _p(info[4:])
         with torch.cuda.stream(side):
             ss = _stream()
-            nat.call("bddc_coarse_local", *cl_args[:-1], _p(info[4:]), 2, ss)
+            nat.call("bddc_coarse_local", *cl2, 2, ss)
             nat.call("bddc_pack_sym", N, mg, _p(self.d_T), _p(self.d_Tp), ss)
+        nat.call("bddc_coarse_local", *cl_args, 1, st)
         # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
         nat.call("bddc_pack_sym", N, mg, _p(self.d_S), _p(self.d_Sp), st)
         self._mark(ev, "coarse_local")
@@ -374,12 +389,14 @@ class BddcSetup:
             self.nd.factor(self.d_Kc, dev_rows, self.d_b0)
             self.nd.release_fronts()
         main.wait_stream(side)   # T_i done; its workspaces may go now
-        del Ct, Y, E, gam, ws, Sinv, dims, cl_args, self.d_S, self.d_T
+        del Ct, Y, E, gam, ws, Sinv, dims, cl_args, self.d_S, self.d_T, Ct2, Y2, ws2, dims2, cl2
         bad = info.cpu().numpy()
         if bad[0] or bad[1]:
             raise NumericalFailureError("local interior factorization failed", where=None)
         if bad[2] or bad[4]:
             raise NumericalFailureError("constrained coarse basis system singular")
+        if self.nd is not None:
+            self.nd.check()
         self._mark(ev, "coarse")
         # persistent PCG workspaces
         ng = dec.n_gamma
@@ -500,7 +517,7 @@ class BddcSetup:
         well = np.abs(tot) > 1e-14
         dist = np.where(well[dec.cell_sub], f / np.where(well, tot, 1.0)[dec.cell_sub],
                         1.0 / cnt[dec.cell_sub])
-        gdev = torch.as_tensor(dist, dtype=F64, device=dev)
+        gdev = _upload(dist, F64, dev)
         g = torch.empty_like(gdev)
         # D-scaled cell values (local_solve reads g / D)
         nat.call("bddc_scale_cells", C.byref(self.geom), _p(gdev), _p(self.d_cell_sub),

@@ -11,6 +11,5 @@ cfg = B.SolveConfig(tau=c["tau"], scaling=c["scaling"], constraints="adaptive", 
 st = B.BddcSetup(system, dec, cfg); torch.cuda.synchronize(); del st
 pr = cProfile.Profile(); pr.enable()
 st = B.BddcSetup(system, dec, cfg); torch.cuda.synchronize()
-r = B.solve(system, dec, cfg, setup=st)
 pr.disable()
-s = io.StringIO(); pstats.Stats(pr, stream=s).sort_stats("cumulative").print_stats(35); print(s.getvalue()[:6000])
+s = io.StringIO(); pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25); print(s.getvalue()[:5000])
