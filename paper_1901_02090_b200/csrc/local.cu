@@ -287,7 +287,7 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
 
 // Q = P^+ = Pi D^-1/2 (Ps^-1 - v v^T) D^-1/2 Pi,  Pi = I - 11^T/np (zero padding).
 __global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const double* __restrict__ scl) {
-  extern __shared__ double rm[];   // maxP column means
+  extern __shared__ double rm[];   // maxP column means, then dsq and 1/(dsq vn)
   __shared__ double red[32];
   const int i = blockIdx.x;
   const Box b = sub_box(G, i);
@@ -303,14 +303,28 @@ __global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const doubl
     }
     return;
   }
+  // per-row factors once (no division in the sweeps), column sums with four
+  // independent partial sums (loads in flight), coalesced over columns
+  double* sd = rm + mp;   // dsq
+  double* wv = sd + mp;   // 1 / (dsq vn)
+  for (int r = threadIdx.x; r < np; r += blockDim.x) {
+    sd[r] = dsq[r];
+    wv[r] = 1.0 / (dsq[r] * vn);
+  }
+  __syncthreads();
   double part = 0.0;
   for (int c = threadIdx.x; c < np; c += blockDim.x) {
-    const double vc = 1.0 / (dsq[c] * vn);
-    double acc = 0.0;
-    for (int r = 0; r < np; ++r) {
-      const double vr = 1.0 / (dsq[r] * vn);
-      acc += dsq[r] * (Pi[(size_t)r * mp + c] - vr * vc) * dsq[c];
+    const double vc = wv[c];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int r = 0;
+    for (; r + 4 <= np; r += 4) {
+      a0 += sd[r] * (Pi[(size_t)r * mp + c] - wv[r] * vc);
+      a1 += sd[r + 1] * (Pi[(size_t)(r + 1) * mp + c] - wv[r + 1] * vc);
+      a2 += sd[r + 2] * (Pi[(size_t)(r + 2) * mp + c] - wv[r + 2] * vc);
+      a3 += sd[r + 3] * (Pi[(size_t)(r + 3) * mp + c] - wv[r + 3] * vc);
     }
+    for (; r < np; ++r) a0 += sd[r] * (Pi[(size_t)r * mp + c] - wv[r] * vc);
+    const double acc = ((a0 + a1) + (a2 + a3)) * sd[c];
     rm[c] = acc / np;
     part += acc;
   }
@@ -319,10 +333,7 @@ __global__ void pinv_fix_kernel(bddc_geom G, double* __restrict__ P, const doubl
   for (size_t e = threadIdx.x; e < (size_t)mp * mp; e += blockDim.x) {
     int r = (int)(e / mp), c = (int)(e % mp);
     double v = 0.0;
-    if (r < np && c < np) {
-      const double vr = 1.0 / (dsq[r] * vn), vc = 1.0 / (dsq[c] * vn);
-      v = dsq[r] * (Pi[e] - vr * vc) * dsq[c] - rm[r] - rm[c] + tm;
-    }
+    if (r < np && c < np) v = sd[r] * (Pi[e] - wv[r] * wv[c]) * sd[c] - rm[r] - rm[c] + tm;
     Pi[e] = v;
   }
 }
@@ -602,7 +613,7 @@ extern "C" int bddc_local_build(const bddc_geom* g, const double* coef, const in
 }
 
 extern "C" int bddc_local_pinv_fix(const bddc_geom* g, double* P, const double* scl, void* stream) {
-  pinv_fix_kernel<<<g->N, 512, g->maxP * sizeof(double), (cudaStream_t)stream>>>(*g, P, scl);
+  pinv_fix_kernel<<<g->N, 512, 3 * g->maxP * sizeof(double), (cudaStream_t)stream>>>(*g, P, scl);
   LAUNCH_OK();
   return 0;
 }
