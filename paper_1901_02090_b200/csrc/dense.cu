@@ -186,6 +186,8 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
                                                     double beta, double* __restrict__ C, int ldc,
                                                     long long sC, int upper, const int* __restrict__ dims,
                                                     int dstride) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   const int bn = blockIdx.x, bm = blockIdx.y, bz = blockIdx.z;
   if ((upper & 1) && bm > bn) return;
   A += bz * sA;
@@ -234,6 +236,8 @@ template <bool aligned>
 __global__ void __launch_bounds__(128) trmm_left_upper_kernel(int n1, int n2, double alpha,
                                                               const double* __restrict__ U, double* B, int ld,
                                                               long long sM) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   const int n0 = blockIdx.x * BN, bz = blockIdx.y;
   const double* Uz = U + bz * sM;
   double* Bz = B + bz * sM;
@@ -252,6 +256,8 @@ template <bool aligned>
 __global__ void __launch_bounds__(128) trmm_right_upperT_kernel(int n1, int n2, double alpha,
                                                                 const double* __restrict__ U, double* B, int ld,
                                                                 long long sM) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   const int m0 = blockIdx.x * BM, bz = blockIdx.y;
   const double* Uz = U + bz * sM;
   double* Bz = B + bz * sM;
@@ -280,6 +286,8 @@ __global__ void __launch_bounds__(128) trmm_right_upperT_kernel(int n1, int n2, 
 //  mode 3: both (the whole matrix fits one leaf).
 __global__ void __launch_bounds__(32) leaf_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info,
                                                            int mode) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   extern __shared__ double sd[];
   const int ldp = nb + 1;
   const int lane = threadIdx.x;
@@ -352,6 +360,8 @@ __global__ void __launch_bounds__(32) leaf_chol_inv_kernel(double* M, int nb, in
 // triangular inverse are 496 shuffle+FMA steps each, V V^T 528.
 template <int MODE>
 __global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   __shared__ double tsm[32][33];
   const unsigned FULL = 0xffffffffu;
   const int c = threadIdx.x;
@@ -434,6 +444,8 @@ __global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, 
 // Zero / copy an r x c block (row-major, leading dim ld, batch stride sM / sW).
 __global__ void block_copy_kernel(double* dst, int ld, long long sD, const double* src, int lds, long long sS,
                                   int rows, int cols) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   const int z = blockIdx.y;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)rows * cols;
        e += (long long)gridDim.x * blockDim.x) {
@@ -444,6 +456,8 @@ __global__ void block_copy_kernel(double* dst, int ld, long long sD, const doubl
 
 // Lower triangle of an n x n block from its upper triangle (tile transposes).
 __global__ void lower_from_upper_kernel(double* M, int n, int ld, long long sM) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
   __shared__ double t[32][33];
   const int z = blockIdx.z;
   const int bi = blockIdx.y, bj = blockIdx.x;   // target tile (bi > bj) below the diagonal
@@ -489,12 +503,11 @@ extern "C" int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int
   cudaStream_t s = (cudaStream_t)stream;
   bool al = ((((uintptr_t)A) | ((uintptr_t)B)) % 16 == 0) && !((lda | ldb) & 1) && !((sA | sB) & 1);
 #define DG_LAUNCH(TA, TB)                                                                                   \
-  if (al)                                                                                                   \
-    dgemm_kernel<TA, TB, true><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper, \
-                                                    dims, dstride);                                         \
-  else                                                                                                      \
-    dgemm_kernel<TA, TB, false><<<grid, 128, 0, s>>>(M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, upper, \
-                                                     dims, dstride);
+  {                                                                                                         \
+    auto kfn = al ? dgemm_kernel<TA, TB, true> : dgemm_kernel<TA, TB, false>;                               \
+    CUDA_OK(launch_pdl(kfn, grid, dim3(128), 0, s, M, N, K, alpha, A, lda, sA, B, ldb, sB, beta, C, ldc, sC, \
+                       upper, dims, dstride));                                                              \
+  }
   if (!transA && !transB) {
     DG_LAUNCH(false, false)
   } else if (transA && !transB) {
@@ -521,7 +534,7 @@ int block_copy(double* dst, int ld, long long sD, const double* src, int lds, lo
   long long tot = (long long)rows * cols;
   int gx = (int)((tot + 255) / 256);
   if (gx > 64) gx = 64;
-  block_copy_kernel<<<dim3(gx, batch), 256, 0, s>>>(dst, ld, sD, src, lds, sS, rows, cols);
+  CUDA_OK(launch_pdl(block_copy_kernel, dim3(gx, batch), dim3(256), 0, s, dst, ld, sD, src, lds, sS, rows, cols));
   LAUNCH_OK();
   return 0;
 }
@@ -538,12 +551,12 @@ int trmm_launch(int right, int n1, int n2, double alpha, const double* U, double
   const bool al = !(((uintptr_t)U | (uintptr_t)B) & 15) && !(ld & 1) && !(sM & 1);
   if (!right) {
     dim3 g((n2 + BN - 1) / BN, batch);
-    if (al) trmm_left_upper_kernel<true><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
-    else trmm_left_upper_kernel<false><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+    auto kfn = al ? trmm_left_upper_kernel<true> : trmm_left_upper_kernel<false>;
+    CUDA_OK(launch_pdl(kfn, g, dim3(128), 0, s, n1, n2, alpha, U, B, ld, sM));
   } else {
     dim3 g((n1 + BM - 1) / BM, batch);
-    if (al) trmm_right_upperT_kernel<true><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
-    else trmm_right_upperT_kernel<false><<<g, 128, 0, s>>>(n1, n2, alpha, U, B, ld, sM);
+    auto kfn = al ? trmm_right_upperT_kernel<true> : trmm_right_upperT_kernel<false>;
+    CUDA_OK(launch_pdl(kfn, g, dim3(128), 0, s, n1, n2, alpha, U, B, ld, sM));
   }
   LAUNCH_OK();
   return 0;
@@ -553,16 +566,15 @@ static int g_leaf_regs = 1;
 
 int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
   if (n <= 32 && g_leaf_regs) {
-    if (mode == 1) leaf32_chol_inv_kernel<1><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
-    else if (mode == 2) leaf32_chol_inv_kernel<2><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
-    else leaf32_chol_inv_kernel<3><<<batch, 32, 0, s>>>(M, n, ld, sM, info);
+    auto kfn = mode == 1 ? leaf32_chol_inv_kernel<1> : (mode == 2 ? leaf32_chol_inv_kernel<2> : leaf32_chol_inv_kernel<3>);
+    CUDA_OK(launch_pdl(kfn, dim3(batch), dim3(32), 0, s, M, n, ld, sM, info));
     LAUNCH_OK();
     return 0;
   }
   size_t shm = (size_t)n * (n + 1) * sizeof(double);
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  leaf_chol_inv_kernel<<<batch, 32, shm, s>>>(M, n, ld, sM, info, mode);
+  CUDA_OK(launch_pdl(leaf_chol_inv_kernel, dim3(batch), dim3(32), shm, s, M, n, ld, sM, info, mode));
   LAUNCH_OK();
   return 0;
 }
@@ -657,7 +669,7 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
     if ((r = chol_inv_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
     if ((r = lauum_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
     dim3 ga((n + 31) / 32, (n + 31) / 32, batch);
-    lower_from_upper_kernel<<<ga, dim3(32, 8), 0, s>>>(Mat, n, ld, sM);
+    CUDA_OK(launch_pdl(lower_from_upper_kernel, ga, dim3(32, 8), 0, s, Mat, n, ld, sM));
     LAUNCH_OK();
   }
   return 0;

@@ -7,9 +7,13 @@ lib = nat.load()
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 res = {}
 import itertools
-for (bt, n), regs in itertools.product([(2244, 512), (2244, 448), (2244, 160), (2244, 32), (1, 2304)], (1, 0)):
+shapes = [(2244, 512), (2244, 448), (2244, 160), (2244, 32), (1, 2304)]
+if len(sys.argv) > 1:
+    shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1].split(",")]
+leaves = (32, 64) if len(sys.argv) > 1 else (32,)
+for (bt, n), regs in itertools.product(shapes, (1, 0) if len(sys.argv) <= 1 else (1,)):
     lib.bddc_set_leaf_regs(regs)
-    for b in (32,):
+    for b in leaves:
         if n % b:
             continue
         X = torch.randn(min(bt, 64), n, n, dtype=torch.float64, device="cuda")
@@ -30,4 +34,5 @@ for (bt, n), regs in itertools.product([(2244, 512), (2244, 448), (2244, 160), (
         err = float((M[0] @ A0[0] - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max())
         res[f"{bt}x{n} b={b} regs={regs}"] = dict(ms=round(t * 1000, 3), tflops=round(bt * n ** 3 / t / 1e12, 2), err=err)
         print(f"{bt}x{n} b={b} regs={regs}: {t*1000:.2f} ms  {bt*n**3/t/1e12:.2f} TF/s  |MA-I|={err:.1e}", flush=True)
-json.dump(res, open("gpurun_out/spd_bench.json", "w"), indent=1)
+if len(sys.argv) <= 1:
+    json.dump(res, open("gpurun_out/spd_bench.json", "w"), indent=1)
