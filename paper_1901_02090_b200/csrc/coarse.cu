@@ -240,7 +240,7 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
     return r;
   if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
     return r;
-  if ((r = bddc_spd_inverse_batched(T, mg, mg, sG, N, 32, inv_ws, info, stream))) return r;
+  if ((r = bddc_spd_inverse_batched(T, mg, mg, sG, N, 64, inv_ws, info, stream))) return r;
   // T -= (Q/sqrt g)(Q/sqrt g)^T
   dim3 gsc(64, N);
   scale_rows_kernel<<<gsc, 256, 0, s>>>(sGC, gamma, Ct);

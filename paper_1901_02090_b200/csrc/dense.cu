@@ -215,6 +215,16 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
   __shared__ __align__(16) double As[2][TILE_ELEMS];
   __shared__ __align__(16) double Bs[2][TILE_ELEMS];
   const int m0 = bm * BM, n0 = bn * BN;
+  if (beta != 0.0) {
+    // the epilogue reads C: start its HBM fetch now (two 128-byte lines of a row
+    // per thread), so the read-modify-write does not add a full memory latency
+    const int r = m0 + (threadIdx.x >> 1);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = n0 + (threadIdx.x & 1) * 32 + q * 16;
+      if (r < M && c < N) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(C + (size_t)r * ldc + c));
+    }
+  }
   double acc[4][4][2];
   acc_zero(acc);
   // triangular operands: only the K range that can be nonzero for this tile
@@ -441,6 +451,121 @@ __global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, 
   }
 }
 
+// The leaf for 32 < nb <= 64: two warps per matrix, thread c owns column c of
+// the block in registers (padding columns c >= nb carry the identity); one
+// replaces the seven launches of a 64 -> 32 + 32 recursion step.  Row
+// broadcasts go through shared memory (double-buffered, ONE barrier per step,
+// 16-byte broadcast loads: the leaf is bound by the one-warp-load-per-clock
+// shared-memory pipe and the FP64 FMA rate), every thread derives 1/U_kk itself
+// from the broadcast unscaled row and updates with a_kr * (U[k][c] / U_kk).
+//  MODE 1: upper Cholesky M = U^T U, V = U^-1 (column c solves U v = e_c
+//          against U in shared memory), V to the upper triangle, zeros below.
+//  MODE 2: X = V V^T from V (upper), upper triangle written.
+//  MODE 3: both, full symmetric result.
+constexpr int L64 = 66;   // shared row stride (doubles): 16-byte rows, 2-way worst case
+template <int MODE>
+__global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info) {
+  pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
+  pdl_wait();      // all memory of the predecessor grid visible
+  __shared__ __align__(16) double sU[64 * L64];
+  __shared__ __align__(16) double srow[2][64];
+  __shared__ double sinv[64];
+  const int c = threadIdx.x;
+  double* Mz = M + blockIdx.x * sM;
+  if (MODE & 1) {
+    double u[64];
+#pragma unroll
+    for (int r = 0; r < 64; ++r) {
+      double v = (c >= nb && r == c) ? 1.0 : 0.0;
+      if (r < nb && c < nb && r <= c) v = Mz[(size_t)r * ld + c];
+      u[r] = v;
+    }
+    int bad = 0;
+    // right-looking: row k (unscaled) is broadcast, every thread scales it itself
+    // (only 1/U_kk is ever needed: rsqrt); the broadcast reads are 16-byte
+#pragma unroll
+    for (int k = 0; k < 64; ++k) {
+      double* rb = srow[k & 1];
+      rb[c] = u[k];
+      __syncthreads();
+      double a = rb[k];
+      if (!(a > 0.0)) {
+        bad = 1;
+        a = 1.0;
+      }
+      const double id = rsqrt(a);
+      if (c == 0) sinv[k] = id;
+      const double ukc = (c > k) ? u[k] * id : (c == k ? a * id : 0.0);
+      u[k] = ukc;
+      const double w = ukc * id;   // U[k][r] U[k][c] = a_kr (U[k][c] / U_kk)
+      const double2* rb2 = reinterpret_cast<const double2*>(rb);
+#pragma unroll
+      for (int r2 = (k + 1) / 2; r2 < 32; ++r2) {
+        const double2 v = rb2[r2];
+        if (2 * r2 >= k + 1) u[2 * r2] -= v.x * w;
+        u[2 * r2 + 1] -= v.y * w;
+      }
+    }
+    if (c == 0 && bad) atomicAdd(info, 1);
+    // U to shared memory (upper; the strict lower part is never read)
+#pragma unroll
+    for (int r = 0; r < 64; ++r) sU[r * L64 + c] = u[r];
+    __syncthreads();
+    // column c of V = U^-1: x[i] = -(1/U_ii) sum_{j>i} U[i][j] x[j], x[c] = 1/U_cc,
+    // x[j] = 0 for j > c (so the same unrolled code runs in every thread)
+    double x[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) x[j] = 0.0;
+#pragma unroll
+    for (int i = 63; i >= 0; --i) {
+      const double2* ur = reinterpret_cast<const double2*>(sU + i * L64);
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int j2 = (i + 1) / 2; j2 < 32; ++j2) {
+        const double2 v = ur[j2];
+        if (2 * j2 >= i + 1) s0 += v.x * x[2 * j2];
+        s1 += v.y * x[2 * j2 + 1];
+      }
+      const double vi = sinv[i];
+      x[i] = (i == c) ? vi : (i < c ? -vi * (s0 + s1) : 0.0);
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int r = 0; r < 64; ++r)
+        if (r < nb && c < nb) Mz[(size_t)r * ld + c] = (r <= c) ? x[r] : 0.0;
+      return;
+    }
+    __syncthreads();   // every thread is done reading U
+#pragma unroll
+    for (int r = 0; r < 64; ++r) sU[r * L64 + c] = x[r];   // V, zeros below the diagonal
+  } else {
+#pragma unroll
+    for (int r = 0; r < 64; ++r)
+      sU[r * L64 + c] = (r < nb && c < nb && r <= c) ? Mz[(size_t)r * ld + c] : 0.0;
+  }
+  __syncthreads();
+  // X[i][c] = sum_{k >= max(i, c)} V[i][k] V[c][k]: thread c keeps row c of V
+  // (zero below k = c), rows i are broadcast from shared memory
+  double rw[64];
+#pragma unroll
+  for (int k = 0; k < 64; ++k) rw[k] = (k >= c) ? sU[c * L64 + k] : 0.0;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const double2* vr = reinterpret_cast<const double2*>(sU + i * L64);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k2 = i / 2; k2 < 32; ++k2) {
+      const double2 v = vr[k2];
+      if (2 * k2 >= i) s0 += v.x * rw[2 * k2];
+      s1 += v.y * rw[2 * k2 + 1];
+    }
+    if (i < nb && c < nb && i <= c) {
+      Mz[(size_t)i * ld + c] = s0 + s1;
+      if (MODE == 3) Mz[(size_t)c * ld + i] = s0 + s1;
+    }
+  }
+}
+
 // Zero / copy an r x c block (row-major, leading dim ld, batch stride sM / sW).
 __global__ void block_copy_kernel(double* dst, int ld, long long sD, const double* src, int lds, long long sS,
                                   int rows, int cols) {
@@ -454,24 +579,33 @@ __global__ void block_copy_kernel(double* dst, int ld, long long sD, const doubl
   }
 }
 
-// Lower triangle of an n x n block from its upper triangle (tile transposes).
-__global__ void lower_from_upper_kernel(double* M, int n, int ld, long long sM) {
+// Lower triangle of an n x n block from its upper triangle: one 64 x 64 tile
+// transpose per CTA, only the nt(nt+1)/2 tiles on or below the diagonal are
+// launched (blockIdx.x enumerates them), 16 loads in flight per thread.
+__global__ void __launch_bounds__(256) lower_from_upper_kernel(double* M, int n, int ld, long long sM) {
   pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
   pdl_wait();      // all memory of the predecessor grid visible
-  __shared__ double t[32][33];
-  const int z = blockIdx.z;
-  const int bi = blockIdx.y, bj = blockIdx.x;   // target tile (bi > bj) below the diagonal
-  if (bi < bj) return;
-  double* Mz = M + z * sM;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int rr = ty; rr < 32; rr += 8) {        // source tile (bj, bi) in the upper triangle
-    int r = bj * 32 + rr, c = bi * 32 + tx;
-    t[rr][tx] = (r < n && c < n) ? Mz[(size_t)r * ld + c] : 0.0;
+  __shared__ double t[64][65];
+  int bi = (int)((sqrtf(8.0f * blockIdx.x + 1.0f) - 1.0f) * 0.5f);   // target tile row
+  while ((bi + 1) * (bi + 2) / 2 <= (int)blockIdx.x) ++bi;
+  while (bi * (bi + 1) / 2 > (int)blockIdx.x) --bi;
+  const int bj = blockIdx.x - bi * (bi + 1) / 2;                     // bj <= bi
+  double* Mz = M + blockIdx.y * sM;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {             // source tile (bj, bi) in the upper triangle
+    const int r = bj * 64 + ty + 4 * q, c = bi * 64 + tx;
+    v[q] = (r < n && c < n) ? Mz[(size_t)r * ld + c] : 0.0;
   }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) t[ty + 4 * q][tx] = v[q];
   __syncthreads();
-  for (int cc = ty; cc < 32; cc += 8) {
-    int r = bi * 32 + tx, c = bj * 32 + cc;
-    if (r < n && c < n && r > c) Mz[(size_t)r * ld + c] = t[cc][tx];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {             // coalesced rows of the target tile
+    const int rr = ty + 4 * q;
+    const int r = bi * 64 + rr, c = bj * 64 + tx;
+    if (r < n && c < n && r > c) Mz[(size_t)r * ld + c] = t[tx][rr];
   }
 }
 
@@ -571,6 +705,12 @@ int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, in
     LAUNCH_OK();
     return 0;
   }
+  if (n <= 64 && g_leaf_regs) {
+    auto kfn = mode == 1 ? leaf64_chol_inv_kernel<1> : (mode == 2 ? leaf64_chol_inv_kernel<2> : leaf64_chol_inv_kernel<3>);
+    CUDA_OK(launch_pdl(kfn, dim3(batch), dim3(64), 0, s, M, n, ld, sM, info));
+    LAUNCH_OK();
+    return 0;
+  }
   size_t shm = (size_t)n * (n + 1) * sizeof(double);
   if (shm > 48 * 1024)
     CUDA_OK(cudaFuncSetAttribute(leaf_chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -597,7 +737,8 @@ int split_of(int n, int b) {
 //   V22 = rec(C);  V12 = -V11 U12 V22.
 // The Schur complement is formed as a Gram update of the Cholesky factor, so
 // rounding never sees an explicitly inverted pivot block (LAPACK potrf/trtri).
-int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, double* ws, int* info, cudaStream_t s) {
+int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, double* ws, int* info, cudaStream_t s,
+                 bool tile_aligned) {
   if (n <= b) return leaf_launch(M, n, ld, sM, batch, info, 1, s);
   const int n1 = split_of(n, b), n2 = n - n1;
   double* A = M;
@@ -607,10 +748,10 @@ int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, doubl
   double* ws_next = ws + (size_t)batch * n1 * n2;
   const long long sW = (long long)n1 * n2;
   int r;
-  if ((r = chol_inv_rec(A, n1, ld, sM, batch, b, ws_next, info, s))) return r;
+  if ((r = chol_inv_rec(A, n1, ld, sM, batch, b, ws_next, info, s, tile_aligned))) return r;
   if ((r = bddc_dgemm_batched(1, 0, n1, n2, n1, 1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 4, s))) return r;
   if ((r = bddc_dgemm_batched(1, 0, n2, n2, n1, -1.0, W, n2, sW, W, n2, sW, 1.0, C, ld, sM, batch, 1, s))) return r;
-  if ((r = chol_inv_rec(C, n2, ld, sM, batch, b, ws_next, info, s))) return r;
+  if ((r = chol_inv_rec(C, n2, ld, sM, batch, b, ws_next, info, s, tile_aligned && n1 % BM == 0))) return r;
   if (trmm_inplace_pays(n1, n2, batch)) {
     if ((r = bddc_dgemm_batched(0, 0, n1, n2, n2, 1.0, W, n2, sW, C, ld, sM, 0.0, B, ld, sM, batch, 8, s))) return r;
     if ((r = trmm_launch(0, n1, n2, -1.0, A, B, ld, sM, batch, s))) return r;   // B <- -V11 B
@@ -620,6 +761,11 @@ int chol_inv_rec(double* M, int n, int ld, long long sM, int batch, int b, doubl
     if ((r = bddc_dgemm_batched(0, 0, n1, n2, n1, -1.0, A, ld, sM, B, ld, sM, 0.0, W, n2, sW, batch, 2, s))) return r;
     if ((r = block_copy(B, ld, sM, W, n2, sW, n1, n2, batch, s))) return r;
   }
+  // The strict lower block is read only where it lies inside a diagonal GEMM
+  // tile (the triangular K-range skipping works on whole 64-tiles): when this
+  // block and all its ancestors start on a tile boundary and the split is one,
+  // it is never read and the final lower_from_upper overwrites it.
+  if (tile_aligned && n1 % BM == 0) return 0;
   return block_copy(M + (size_t)n1 * ld, ld, sM, nullptr, 0, 0, n2, n1, batch, s);
 }
 
@@ -666,10 +812,10 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
   if (n <= b) {
     if ((r = leaf_launch(Mat, n, ld, sM, batch, info, 3, s))) return r;
   } else {
-    if ((r = chol_inv_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
+    if ((r = chol_inv_rec(Mat, n, ld, sM, batch, b, rest, info, s, true))) return r;
     if ((r = lauum_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
-    dim3 ga((n + 31) / 32, (n + 31) / 32, batch);
-    CUDA_OK(launch_pdl(lower_from_upper_kernel, ga, dim3(32, 8), 0, s, Mat, n, ld, sM));
+    const int nt = (n + 63) / 64;
+    CUDA_OK(launch_pdl(lower_from_upper_kernel, dim3(nt * (nt + 1) / 2, batch), dim3(256), 0, s, Mat, n, ld, sM));
     LAUNCH_OK();
   }
   return 0;

@@ -29,6 +29,7 @@ from .errors import (ConfigurationError, InternalConsistencyError,
 _p = nat.ptr
 F64 = torch.float64
 I32 = torch.int32
+SPD_LEAF = 64   # leaf order of the batched SPD inverses (leaf64 kernel: one launch per 64-block)
 
 
 @dataclass
@@ -243,10 +244,10 @@ class BddcSetup:
                  _p(self.d_Q), _p(Gc), _p(SAd), _p(SApart), _p(SAoff),
                  _p(alpha), st)
         info = torch.zeros(5, dtype=I32, device=dev)
-        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, 32) // 8 + 2,
+        ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mp, N, SPD_LEAF) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(self.d_Q), mp, mp, mp * mp, N,
-                 32, _p(ws), _p(info), st)
+                 SPD_LEAF, _p(ws), _p(info), st)
         del ws
         nat.call("bddc_local_pinv_fix", gp, _p(self.d_Q), _p(alpha), st)
         Wt = torch.empty(N * mg * mp, dtype=F64, device=dev)
@@ -259,7 +260,7 @@ class BddcSetup:
         nat.call("bddc_pack_sym", N, mp, _p(self.d_Q), _p(self.d_Qp), st)
         del self.d_Q
         Sinv = self.d_S.clone()
-        leaf = 32
+        leaf = SPD_LEAF
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(mg, N, leaf) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(Sinv), mg, mg, mg * mg, N, leaf,

@@ -76,7 +76,9 @@ def test_dgemm_per_batch_dims(beta):
             assert torch.equal(Cm[z][part], C0[z][part])
 
 
-@pytest.mark.parametrize("n,b,batch", [(64, 32, 3), (192, 64, 5), (512, 64, 2)])
+@pytest.mark.parametrize("n,b,batch", [(64, 32, 3), (192, 64, 5), (512, 64, 2), (40, 64, 7), (64, 64, 3),
+                                       (100, 64, 4), (160, 64, 300), (448, 64, 80), (448, 32, 80),
+                                       (512, 32, 2)])
 def test_spd_inverse_vs_torch(n, b, batch):
     import torch
     nat = _lib()
