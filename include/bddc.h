@@ -79,11 +79,13 @@ int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha
                        long long sB, double beta, double* C, int ldc, long long sC, int batch,
                        int upper, void* stream);
 
-/* In-place SPD inverse by the blocked symmetric sweep (block b, n % b == 0);
- * replaces SuperLU splu (substructure.py:66, coarse.py:159) and the dense
- * coarse lu_factor (coarse.py:196).  info counts non-positive pivots. */
+/* In-place inverse of a batch of SPD matrices (Cholesky, triangular inverse,
+ * V V^T; recursive DMMA GEMMs above leaves of order <= b, b <= 64); replaces
+ * SuperLU splu (substructure.py:66, coarse.py:159) and the dense coarse
+ * lu_factor (coarse.py:196).  info counts non-positive pivots. */
 size_t bddc_spd_inverse_workspace(int n, int batch, int b);
-/* Tuning knob: leaves of order <= 32 in registers (1, default) or shared memory (0). */
+/* Tuning knob: bit 0 = register leaves (32 / 64, default on; off = shared-memory
+ * leaf), bit 1 = 64-leaf Cholesky and triangular inverse as two kernels (default on). */
 void bddc_set_leaf_regs(int on);
 int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                              int* info, void* stream);

@@ -462,9 +462,15 @@ __global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, 
 //          against U in shared memory), V to the upper triangle, zeros below.
 //  MODE 2: X = V V^T from V (upper), upper triangle written.
 //  MODE 3: both, full symmetric result.
+//  MODE 4 / 5: the two halves of MODE 1 as separate kernels (U through global
+//          memory): each unrolled body is half the code, which keeps the
+//          instruction cache from thrashing (ncu: "no instruction" was the top stall).
 constexpr int L64 = 66;   // shared row stride (doubles): 16-byte rows, 2-way worst case
 template <int MODE>
 __global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, int ld, long long sM, int* info) {
+  constexpr bool CHOL = MODE == 1 || MODE == 3 || MODE == 4;
+  constexpr bool TRTRI = MODE == 1 || MODE == 3 || MODE == 5;
+  constexpr bool LAUUM = MODE == 2 || MODE == 3;
   pdl_trigger();   // dependents may launch once every CTA started (tail overlap)
   pdl_wait();      // all memory of the predecessor grid visible
   __shared__ __align__(16) double sU[64 * L64];
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, 
   __shared__ double sinv[64];
   const int c = threadIdx.x;
   double* Mz = M + blockIdx.x * sM;
-  if (MODE & 1) {
+  if (CHOL) {
     double u[64];
 #pragma unroll
     for (int r = 0; r < 64; ++r) {
@@ -507,9 +513,26 @@ __global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, 
       }
     }
     if (c == 0 && bad) atomicAdd(info, 1);
+    if (MODE == 4) {   // U (upper) and 1/U_kk on the otherwise-zero diagonal-below slot
+#pragma unroll
+      for (int r = 0; r < 64; ++r)
+        if (r < nb && c < nb) Mz[(size_t)r * ld + c] = (r <= c) ? u[r] : 0.0;
+      __syncthreads();
+      if (c < nb && c + 1 < nb) Mz[(size_t)(c + 1) * ld + c] = sinv[c];
+      return;
+    }
     // U to shared memory (upper; the strict lower part is never read)
 #pragma unroll
     for (int r = 0; r < 64; ++r) sU[r * L64 + c] = u[r];
+  } else if (TRTRI) {
+    // MODE 5: U from MODE 4 (1/U_kk parked in the sub-diagonal slot k+1, k)
+#pragma unroll
+    for (int r = 0; r < 64; ++r)
+      sU[r * L64 + c] = (r < nb && c < nb && r <= c) ? Mz[(size_t)r * ld + c] : (r == c ? 1.0 : 0.0);
+    if (c < nb) sinv[c] = (c + 1 < nb) ? Mz[(size_t)(c + 1) * ld + c] : 1.0 / Mz[(size_t)c * ld + c];
+    else sinv[c] = 1.0;
+  }
+  if (TRTRI) {
     __syncthreads();
     // column c of V = U^-1: x[i] = -(1/U_ii) sum_{j>i} U[i][j] x[j], x[c] = 1/U_cc,
     // x[j] = 0 for j > c (so the same unrolled code runs in every thread)
@@ -529,7 +552,7 @@ __global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, 
       const double vi = sinv[i];
       x[i] = (i == c) ? vi : (i < c ? -vi * (s0 + s1) : 0.0);
     }
-    if (MODE == 1) {
+    if (!LAUUM) {
 #pragma unroll
       for (int r = 0; r < 64; ++r)
         if (r < nb && c < nb) Mz[(size_t)r * ld + c] = (r <= c) ? x[r] : 0.0;
@@ -697,6 +720,7 @@ int trmm_launch(int right, int n1, int n2, double alpha, const double* U, double
 }
 
 static int g_leaf_regs = 1;
+static int g_leaf_split = 1;
 
 int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, int mode, cudaStream_t s) {
   if (n <= 32 && g_leaf_regs) {
@@ -706,6 +730,12 @@ int leaf_launch(double* M, int n, int ld, long long sM, int batch, int* info, in
     return 0;
   }
   if (n <= 64 && g_leaf_regs) {
+    if (mode == 1 && g_leaf_split) {
+      CUDA_OK(launch_pdl(leaf64_chol_inv_kernel<4>, dim3(batch), dim3(64), 0, s, M, n, ld, sM, info));
+      CUDA_OK(launch_pdl(leaf64_chol_inv_kernel<5>, dim3(batch), dim3(64), 0, s, M, n, ld, sM, info));
+      LAUNCH_OK();
+      return 0;
+    }
     auto kfn = mode == 1 ? leaf64_chol_inv_kernel<1> : (mode == 2 ? leaf64_chol_inv_kernel<2> : leaf64_chol_inv_kernel<3>);
     CUDA_OK(launch_pdl(kfn, dim3(batch), dim3(64), 0, s, M, n, ld, sM, info));
     LAUNCH_OK();
@@ -794,7 +824,10 @@ int lauum_rec(double* M, int n, int ld, long long sM, int batch, int b, double* 
 
 }  // namespace
 
-extern "C" void bddc_set_leaf_regs(int on) { g_leaf_regs = on ? 1 : 0; }
+extern "C" void bddc_set_leaf_regs(int on) {
+  g_leaf_regs = on & 1;
+  g_leaf_split = (on >> 1) & 1;
+}
 
 // In-place inverse of `batch` SPD matrices of order n (full symmetric storage,
 // leading dim ld, batch stride sM): M = U^T U, V = U^-1, M^-1 = V V^T, all

@@ -1,4 +1,5 @@
-"""Batched SPD sweep-inverse throughput (flops = n^3 per matrix) for the setup shapes."""
+"""Batched SPD inverse throughput (flops = n^3 per matrix) for the setup shapes.
+regs: 3 = register leaves + split 64-leaf, 1 = register leaves, 0 = shared-memory leaves."""
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,8 +11,8 @@ import itertools
 shapes = [(2244, 512), (2244, 448), (2244, 160), (2244, 32), (1, 2304)]
 if len(sys.argv) > 1:
     shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1].split(",")]
-leaves = (32, 64) if len(sys.argv) > 1 else (32,)
-for (bt, n), regs in itertools.product(shapes, (1, 0) if len(sys.argv) <= 1 else (1,)):
+leaves = (32, 64) if len(sys.argv) > 1 else (64,)
+for (bt, n), regs in itertools.product(shapes, (3, 1, 0) if len(sys.argv) <= 1 else (3, 1)):
     lib.bddc_set_leaf_regs(regs)
     for b in leaves:
         if n % b:
