@@ -92,7 +92,8 @@ int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, 
 
 /* ------------------------------------------------------- local operators */
 
-/* c_a = h_a^2 / (6 V k_a) per cell (grid.py:204-227, 270-291). coef: n_cells x 3. */
+/* c_a = h_a^2 / (6 V k_a) per cell (grid.py:204-227, 270-291). coef: 3 x n_cells
+ * (one contiguous array per axis: coalesced rows in the stencil and line solves). */
 int bddc_cell_coeffs(const bddc_geom* g, const double* k, double* coef, void* stream);
 /* delta per interface slot (decomposition.py:212-239), N x maxG. */
 int bddc_weights(const bddc_geom* g, int stiffness, const double* coef, const int* gcode,

@@ -93,7 +93,7 @@ __global__ void cell_coeff_kernel(bddc_geom G, const double* __restrict__ k, dou
   for (int a = 0; a < 3; ++a) {
     double v = 0.0;
     if (a < G.dim) v = G.h[a] * G.h[a] / (6.0 * G.vol) / k[(size_t)c * G.dim + a];
-    coef[(size_t)c * 3 + a] = v;
+    coef[(size_t)(a) * G.n_cells + (c)] = v;
   }
 }
 
@@ -114,8 +114,8 @@ __global__ void weights_kernel(bddc_geom G, int stiffness, const double* __restr
         int own = line_cell_global(G, b, s.a, s.line, k_own);
         int stride_g = s.a == 0 ? 1 : (s.a == 1 ? G.n[0] : G.n[0] * G.n[1]);
         int oth = s.side ? own + stride_g : own - stride_g;
-        double d_own = 2.0 * coef[(size_t)own * 3 + s.a];
-        double d_oth = 2.0 * coef[(size_t)oth * 3 + s.a];
+        double d_own = 2.0 * coef[(size_t)(s.a) * G.n_cells + (own)];
+        double d_oth = 2.0 * coef[(size_t)(s.a) * G.n_cells + (oth)];
         w = d_own / (d_own + d_oth);
       }
     }
@@ -147,8 +147,8 @@ __global__ void rescale_kernel(bddc_geom G, const double* __restrict__ coef, dou
       gc[a] = fc;  // the cell above the face
       int hi = cell_id(G, gc[0], gc[1], gc[2]);
       int lo = hi - stride_g;
-      if (fc <= G.n[a] - 1) acc += 2.0 * coef[(size_t)hi * 3 + a];
-      if (fc >= 1) acc += 2.0 * coef[(size_t)lo * 3 + a];
+      if (fc <= G.n[a] - 1) acc += 2.0 * coef[(size_t)(a) * G.n_cells + (hi)];
+      if (fc >= 1) acc += 2.0 * coef[(size_t)(a) * G.n_cells + (lo)];
       cnt += 1;
     }
   }
@@ -185,7 +185,7 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
     line_open(G, b, a, lo, hi);
     for (int line = threadIdx.x; line < nl; line += blockDim.x) {
       double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], col[MAXL + 1], colp[MAXL + 1];
-      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
       const int base = line_base(b, a, line);
       const int m = L - 1 + lo + hi;
       if (m > 0) line_factor(c, L, lo, hi, cp, piv);
@@ -495,7 +495,7 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
     const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
     if (m <= 0) continue;
     double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
-    for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+    for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
     line_factor(c, L, lo, hi, cp, piv);
     for (int j = 0; j < m; ++j)
       r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo)] : 0.0;
@@ -535,7 +535,7 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
     {
       if (m <= 0) continue;
       double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
-      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)line_cell_global(G, b, a, line, k) * 3 + a];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
       line_factor(c, L, lo, hi, cp, piv);
       const int base = line_base(b, a, line);
       for (int j = 0; j < m; ++j) {
@@ -571,7 +571,7 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
         int m = s.L - 1 + lo3[s.a] + hi3[s.a];
         int kend = s.side ? s.L - 1 : 0;
         if (m > 0) {
-          double cend = coef[(size_t)line_cell_global(G, b, s.a, s.line, kend) * 3 + s.a];
+          double cend = coef[(size_t)(s.a) * G.n_cells + (line_cell_global(G, b, s.a, s.line, kend))];
           int jend = s.side ? m - 1 : 0;
           v += cend * tI[off[s.a] + s.line * m + jend];
         }

@@ -41,95 +41,142 @@ __device__ __forceinline__ void decode_bnd(const bddc_geom& G, int d, int& side,
   gc[G.dir_axis] = side ? G.n[G.dir_axis] - 1 : 0;
 }
 
-// y = alpha * A u + beta * y
-__global__ void flux_A_kernel(bddc_geom G, const double* __restrict__ coef, const double* __restrict__ u, double alpha,
-                              double beta, double* __restrict__ y) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
-       e += (long long)gridDim.x * blockDim.x) {
-    int d = (int)e, a, f[3];
-    double v;
-    if (d >= G.n_flux_int) {  // mode B Dirichlet face: one cell, partner = that cell's other face
-      int side, gc[3];
-      decode_bnd(G, d, side, gc);
-      a = G.dir_axis;
-      const double c = coef[(size_t)cell_id(G, gc[0], gc[1], gc[2]) * 3 + a];
-      int other;
-      if (G.n[a] == 1) {
-        other = bnd_dof(G, 1 - side, gc);
-      } else {
-        gc[a] = side ? G.n[a] - 1 : 1;
-        other = face_dof(G, a, gc[0], gc[1], gc[2]);
-      }
-      v = 2.0 * c * u[d] + c * u[other];
-    } else {
-      decode_dof(G, d, a, f);
-      int hi = cell_id(G, f[0], f[1], f[2]);
-      int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-      int lo = hi - st;
-      double clo = coef[(size_t)lo * 3 + a], chi = coef[(size_t)hi * 3 + a];
-      v = 2.0 * (clo + chi) * u[d];
-      // dof stride along a inside family a equals the cell stride st
-      if (f[a] > 1) v += clo * u[d - st];
-      else if (a == G.dir_axis) v += clo * u[bnd_dof(G, 0, f)];
-      if (f[a] < G.n[a] - 1) v += chi * u[d + st];
-      else if (a == G.dir_axis) v += chi * u[bnd_dof(G, 1, f)];
+// Row-structured launches, no integer division: thread (x, ty) of CTA
+// (bx, by, bz) handles element x (+ RX k) of grid row (f1, f2) = (RY bx + ty, by)
+// of family bz (flux operators; cells: bz = 0).  Consecutive threads touch
+// consecutive dofs, cells and (structure-of-arrays) coefficients.
+constexpr int RX = 64, RY = 4;
+
+// Row (f1, f2) of family a (interior faces, face coordinates): x-extent e0 and
+// the first dof d0; false outside the family.
+__device__ __forceinline__ bool fam_row(const bddc_geom& G, int a, int r1, int r2, int& e0, int f[3], int& d0) {
+  e0 = G.n[0] - (a == 0);
+  const int e1 = G.n[1] - (a == 1), e2 = (G.dim > 2) ? G.n[2] - (a == 2) : 1;
+  if (r1 >= e1 || r2 >= e2) return false;
+  f[0] = (a == 0);
+  f[1] = r1 + (a == 1);
+  f[2] = r2 + (a == 2);
+  d0 = G.fam_off[a] + e0 * (r1 + e1 * r2);
+  return true;
+}
+
+// y = alpha * A u + beta * y on the interior faces
+__global__ void __launch_bounds__(RX* RY) flux_A_kernel(bddc_geom G, const double* __restrict__ coef,
+                                                        const double* __restrict__ u, double alpha, double beta,
+                                                        double* __restrict__ y) {
+  const int a = blockIdx.z;
+  int e0, f[3], d0;
+  if (!fam_row(G, a, blockIdx.x * RY + threadIdx.y, blockIdx.y, e0, f, d0)) return;
+  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+  const double* ca = coef + (size_t)a * G.n_cells;
+  const int h0 = cell_id(G, f[0], f[1], f[2]);
+  const bool lo_in = f[a] > 1 || a == 0, hi_in = f[a] < G.n[a] - 1 || a == 0;   // along a (x: per element)
+  for (int x = threadIdx.x; x < e0; x += RX) {
+    const int d = d0 + x, hi = h0 + x, lo = hi - st;
+    const double clo = ca[lo], chi = ca[hi];
+    double v = 2.0 * (clo + chi) * u[d];
+    const bool l = a == 0 ? x > 0 : lo_in, h = a == 0 ? x < e0 - 1 : hi_in;
+    // dof stride along a inside family a equals the cell stride st
+    if (l) v += clo * u[d - st];
+    else if (a == G.dir_axis) {
+      int g[3] = {f[0] + x, f[1], f[2]};
+      v += clo * u[bnd_dof(G, 0, g)];
+    }
+    if (h) v += chi * u[d + st];
+    else if (a == G.dir_axis) {
+      int g[3] = {f[0] + x, f[1], f[2]};
+      v += chi * u[bnd_dof(G, 1, g)];
     }
     y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
 }
 
+// Mode B Dirichlet faces (dofs n_flux_int..n_flux-1): one cell each, partner =
+// that cell's other face along the drop axis
+__global__ void flux_A_bnd_kernel(bddc_geom G, const double* __restrict__ coef, const double* __restrict__ u,
+                                  double alpha, double beta, double* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * G.n_bt) return;
+  const int d = G.n_flux_int + r;
+  int side, gc[3];
+  decode_bnd(G, d, side, gc);
+  const int a = G.dir_axis;
+  const double c = coef[(size_t)a * G.n_cells + cell_id(G, gc[0], gc[1], gc[2])];
+  int other;
+  if (G.n[a] == 1) {
+    other = bnd_dof(G, 1 - side, gc);
+  } else {
+    gc[a] = side ? G.n[a] - 1 : 1;
+    other = face_dof(G, a, gc[0], gc[1], gc[2]);
+  }
+  const double v = 2.0 * c * u[d] + c * u[other];
+  y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
+}
+
 // out_c = s_f * fvec_c + s_b * Dcell_c * (B u)_c   (Dcell = D of the cell's subdomain, or 1)
-__global__ void cell_div_kernel(bddc_geom G, const double* __restrict__ u, const double* __restrict__ fvec, double s_f,
-                                double s_b, const int* __restrict__ cell_sub, const double* __restrict__ Dsub,
-                                double* __restrict__ out) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_cells;
-       e += (long long)gridDim.x * blockDim.x) {
-    int c = (int)e;
-    int x = c % G.n[0], y = (c / G.n[0]) % G.n[1], z = c / (G.n[0] * G.n[1]);
-    int cc[3] = {x, y, z};
+__global__ void __launch_bounds__(RX* RY) cell_div_kernel(bddc_geom G, const double* __restrict__ u,
+                                                          const double* __restrict__ fvec, double s_f, double s_b,
+                                                          const int* __restrict__ cell_sub,
+                                                          const double* __restrict__ Dsub, double* __restrict__ out) {
+  const int y = blockIdx.x * RY + threadIdx.y, z = blockIdx.y;
+  if (y >= G.n[1] || z >= G.n[2]) return;
+  const int c0 = G.n[0] * (y + G.n[1] * z);
+  // first dofs of this row's faces: x-faces (x-1, y, z) and the y / z faces (x, ., .)
+  const int ex = G.n[0] - 1;
+  const int dx = G.fam_off[0] + ex * (y + G.n[1] * z) - 1;
+  const int dyl = G.fam_off[1] + G.n[0] * (y - 1 + (G.n[1] - 1) * z), dyh = dyl + G.n[0];
+  const int dzl = G.fam_off[2] + G.n[0] * (y + G.n[1] * (z - 1)), dzh = dzl + G.n[0] * G.n[1];
+  for (int x = threadIdx.x; x < G.n[0]; x += RX) {
+    const int c3[3] = {x, y, z};
     double b = 0.0;
-    for (int a = 0; a < G.dim; ++a) {
-      if (cc[a] > 0) {  // low face interior
-        int f[3] = {x, y, z};
-        b += u[face_dof(G, a, f[0], f[1], f[2])];
-      } else if (a == G.dir_axis) {
-        b += u[bnd_dof(G, 0, cc)];
-      }
-      if (cc[a] < G.n[a] - 1) {  // high face interior
-        int f[3] = {x, y, z};
-        f[a] += 1;
-        b -= u[face_dof(G, a, f[0], f[1], f[2])];
-      } else if (a == G.dir_axis) {
-        b -= u[bnd_dof(G, 1, cc)];
-      }
+    if (x > 0) b += u[dx + x];
+    else if (G.dir_axis == 0) b += u[bnd_dof(G, 0, c3)];
+    if (x < G.n[0] - 1) b -= u[dx + x + 1];
+    else if (G.dir_axis == 0) b -= u[bnd_dof(G, 1, c3)];
+    if (G.dim > 1) {
+      if (y > 0) b += u[dyl + x];
+      else if (G.dir_axis == 1) b += u[bnd_dof(G, 0, c3)];
+      if (y < G.n[1] - 1) b -= u[dyh + x];
+      else if (G.dir_axis == 1) b -= u[bnd_dof(G, 1, c3)];
     }
-    double D = Dsub ? Dsub[cell_sub[c]] : 1.0;
+    if (G.dim > 2) {
+      if (z > 0) b += u[dzl + x];
+      else if (G.dir_axis == 2) b += u[bnd_dof(G, 0, c3)];
+      if (z < G.n[2] - 1) b -= u[dzh + x];
+      else if (G.dir_axis == 2) b -= u[bnd_dof(G, 1, c3)];
+    }
+    const int c = c0 + x;
+    const double D = Dsub ? Dsub[cell_sub[c]] : 1.0;
     double v = s_b * D * b;
     if (fvec) v += s_f * fvec[c];
     out[c] = v;
   }
 }
 
-// y_d = alpha (p_hi - p_lo) + beta y_d
-__global__ void grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha, double beta,
-                            double* __restrict__ y) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < G.n_flux;
-       e += (long long)gridDim.x * blockDim.x) {
-    int d = (int)e, a, f[3];
-    double v;
-    if (d >= G.n_flux_int) {  // Dirichlet face: +p of the cell above (low end), -p below (high end)
-      int side, gc[3];
-      decode_bnd(G, d, side, gc);
-      const double pc = p[cell_id(G, gc[0], gc[1], gc[2])];
-      v = alpha * (side ? -pc : pc);
-    } else {
-      decode_dof(G, d, a, f);
-      int hi = cell_id(G, f[0], f[1], f[2]);
-      int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-      v = alpha * (p[hi] - p[hi - st]);
-    }
-    y[d] = v + (beta == 0.0 ? 0.0 : beta * y[d]);
+// y_d = alpha (p_hi - p_lo) + beta y_d on the interior faces
+__global__ void __launch_bounds__(RX* RY) grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha,
+                                                      double beta, double* __restrict__ y) {
+  const int a = blockIdx.z;
+  int e0, f[3], d0;
+  if (!fam_row(G, a, blockIdx.x * RY + threadIdx.y, blockIdx.y, e0, f, d0)) return;
+  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+  const int h0 = cell_id(G, f[0], f[1], f[2]);
+  for (int x = threadIdx.x; x < e0; x += RX) {
+    const int hi = h0 + x, d = d0 + x;
+    y[d] = alpha * (p[hi] - p[hi - st]) + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
+}
+
+// Mode B Dirichlet faces: +p of the cell above (low end), -p below (high end)
+__global__ void grad_bnd_kernel(bddc_geom G, const double* __restrict__ p, double alpha, double beta,
+                                double* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * G.n_bt) return;
+  const int d = G.n_flux_int + r;
+  int side, gc[3];
+  decode_bnd(G, d, side, gc);
+  const double pc = p[cell_id(G, gc[0], gc[1], gc[2])];
+  y[d] = alpha * (side ? -pc : pc) + (beta == 0.0 ? 0.0 : beta * y[d]);
 }
 
 // Orthonormal DCT-II matrix C[k][x] = s_k cos(pi k (x+1/2)/n) and eigenvalues 4 sin^2(pi k/(2n))
@@ -170,23 +217,41 @@ __global__ void sub_mean_kernel(long long n, const double* __restrict__ sum, dou
 
 }  // namespace
 
+namespace {
+// (n1 / RY, n2) covers every family's (e1, e2)
+dim3 row_grid(const bddc_geom* g, int fams) {
+  return dim3((g->n[1] + RY - 1) / RY, g->n[2], fams);
+}
+}  // namespace
+
 extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double* u, double alpha, double beta,
                            double* y, void* stream) {
-  flux_A_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, coef, u, alpha, beta, y);
+  cudaStream_t s = (cudaStream_t)stream;
+  flux_A_kernel<<<row_grid(g, g->dim), dim3(RX, RY), 0, s>>>(*g, coef, u, alpha, beta, y);
   LAUNCH_OK();
+  if (g->dir_axis >= 0 && g->n_bt > 0) {
+    flux_A_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, coef, u, alpha, beta, y);
+    LAUNCH_OK();
+  }
   return 0;
 }
 
 extern "C" int bddc_cell_div(const bddc_geom* g, const double* u, const double* fvec, double s_f, double s_b,
                              const int* cell_sub, const double* Dsub, double* out, void* stream) {
-  cell_div_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b, cell_sub, Dsub, out);
+  cell_div_kernel<<<row_grid(g, 1), dim3(RX, RY), 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b, cell_sub,
+                                                                              Dsub, out);
   LAUNCH_OK();
   return 0;
 }
 
 extern "C" int bddc_grad(const bddc_geom* g, const double* p, double alpha, double beta, double* y, void* stream) {
-  grad_kernel<<<592, 256, 0, (cudaStream_t)stream>>>(*g, p, alpha, beta, y);
+  cudaStream_t s = (cudaStream_t)stream;
+  grad_kernel<<<row_grid(g, g->dim), dim3(RX, RY), 0, s>>>(*g, p, alpha, beta, y);
   LAUNCH_OK();
+  if (g->dir_axis >= 0 && g->n_bt > 0) {
+    grad_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, p, alpha, beta, y);
+    LAUNCH_OK();
+  }
   return 0;
 }
 
