@@ -273,11 +273,12 @@ def _factorisation_roofline(setup, dec, lib, nat, dev):
     peak = 2.0 * 8192 ** 3 / best / 1e12
     del a, b, c
     N = setup.N
-    shapes = [("Ps (interior pressure Schur, Q = P^+)", dec.maxP), ("S_i^-1", dec.maxG),
-              ("T_i (Delta-solve operator)", dec.maxG)]
+    # (name, order, flags of bddc_spd_inverse_batched_ex as the setup calls it)
+    shapes = [("Ps (interior pressure Schur, Q = P^+)", dec.maxP, 0), ("S_i^-1", dec.maxG, 0),
+              ("T_i (Delta-solve operator, upper triangle only)", dec.maxG, 1)]
     parts, flops, secs = {}, 0.0, 0.0
     g = torch.Generator(device=dev).manual_seed(11)
-    for name, n in shapes:
+    for name, n, flags in shapes:
         X = torch.randn(64, n, n, dtype=torch.float64, device=dev, generator=g)
         A0 = X @ X.transpose(1, 2) + n * torch.eye(n, dtype=torch.float64, device=dev)
         A0 = A0.repeat((N + 63) // 64, 1, 1)[:N].contiguous()
@@ -286,17 +287,18 @@ def _factorisation_roofline(setup, dec, lib, nat, dev):
                          dtype=torch.float64, device=dev)
         info = torch.zeros(1, dtype=torch.int32, device=dev)
         M = A0.clone()
-        nat.call("bddc_spd_inverse_batched", nat.ptr(M), n, n, n * n, N, SPD_LEAF,
-                 nat.ptr(ws), nat.ptr(info), st)
+        nat.call("bddc_spd_inverse_batched_ex", nat.ptr(M), n, n, n * n, N, SPD_LEAF,
+                 nat.ptr(ws), nat.ptr(info), flags, st)
         M.copy_(A0)
         torch.cuda.synchronize()
         e0.record()
-        nat.call("bddc_spd_inverse_batched", nat.ptr(M), n, n, n * n, N, SPD_LEAF,
-                 nat.ptr(ws), nat.ptr(info), st)
+        nat.call("bddc_spd_inverse_batched_ex", nat.ptr(M), n, n, n * n, N, SPD_LEAF,
+                 nat.ptr(ws), nat.ptr(info), flags, st)
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 1000.0
-        err = float((M[0] @ A0[0] - torch.eye(n, dtype=torch.float64, device=dev)).abs().max())
+        M0 = torch.triu(M[0]) + torch.triu(M[0], 1).T   # the upper triangle defines the result
+        err = float((M0 @ A0[0] - torch.eye(n, dtype=torch.float64, device=dev)).abs().max())
         f = float(N) * n ** 3
         parts[name] = {"batch": N, "n": n, "ms": 1000.0 * t, "tflops": f / t / 1e12,
                        "max_abs_MinvM_minus_I": err}

@@ -89,6 +89,9 @@ size_t bddc_spd_inverse_workspace(int n, int batch, int b);
 void bddc_set_leaf_regs(int on);
 int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                              int* info, void* stream);
+/* flags & 1: the caller reads the upper triangle only (no lower mirror pass). */
+int bddc_spd_inverse_batched_ex(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
+                                int* info, int flags, void* stream);
 
 /* ------------------------------------------------------- local operators */
 
@@ -201,8 +204,9 @@ int bddc_fill(long long n, double v, double* a, void* stream);
  * solver.py:114-124 Delta part of precondition). */
 int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos, const double* Mats,
                      const double* x, const double* win, double* yb, void* stream);
-/* Tile-packed symmetric storage (32x32 upper tiles) and the gathered symmetric GEMV
- * used for S_i and T_i in the PCG loop (same contract as bddc_gather_gemv). */
+/* Tile-packed symmetric storage (32x32 upper tiles; only the upper triangle of
+ * `full` is read) and the gathered symmetric GEMV used for S_i and T_i in the
+ * PCG loop (same contract as bddc_gather_gemv). */
 size_t bddc_sym_packed_elems(int maxG);
 int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream);
 int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,

@@ -87,6 +87,7 @@ _SIGS = {
                                 _P, _I, _L, _I, _I, _P, _I, _P],
     "bddc_spd_inverse_workspace": [_I, _I, _I],
     "bddc_spd_inverse_batched": [_P, _I, _I, _L, _I, _I, _P, _P, _P],
+    "bddc_spd_inverse_batched_ex": [_P, _I, _I, _L, _I, _I, _P, _P, _I, _P],
     "bddc_cell_coeffs": [_GP, _P, _P, _P],
     "bddc_weights": [_GP, _I, _P, _P, _P, _P],
     "bddc_rescale": [_GP, _P, _P, _P],

@@ -21,6 +21,8 @@ extern "C" int bddc_dgemm_batched_dims(int transA, int transB, int M, int N, int
                                        const double* A, int lda, long long sA, const double* B, int ldb,
                                        long long sB, double beta, double* C, int ldc, long long sC,
                                        int batch, int upper, const int* dims, int dstride, void* stream);
+extern "C" int bddc_spd_inverse_batched_ex(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
+                                           int* info, int flags, void* stream);
 extern "C" int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                                         int* info, void* stream);
 
@@ -230,22 +232,24 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
   long long tot = (long long)N * sG;
   copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(S, T, tot);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Y, maxC, sGC, 1.0, T, mg, sG, N, 1, dGGC, 16, stream)))
     return r;
-  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 1, dGGC, 16, stream)))
     return r;
   // Y <- Q (Q^T S Q + g I)   (reuse Y)
   if ((r = bddc_dgemm_batched_dims(0, 0, mg, maxC, maxC, 1.0, Ct, maxC, sGC, QtSQ, maxC, sCC, 0.0, Y, maxC, sGC, N, 0, dGCC,
                                    16, stream)))
     return r;
-  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, 1.0, Y, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 1, dGGC, 16, stream)))
     return r;
-  if ((r = bddc_spd_inverse_batched(T, mg, mg, sG, N, 64, inv_ws, info, stream))) return r;
+  // T is consumed through its upper tiles only (bddc_pack_sym): every product
+  // on it and its inverse skip the lower triangle
+  if ((r = bddc_spd_inverse_batched_ex(T, mg, mg, sG, N, 64, inv_ws, info, 1, stream))) return r;
   // T -= (Q/sqrt g)(Q/sqrt g)^T
   dim3 gsc(64, N);
   scale_rows_kernel<<<gsc, 256, 0, s>>>(sGC, gamma, Ct);
   LAUNCH_OK();
-  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 0, dGGC, 16, stream)))
+  if ((r = bddc_dgemm_batched_dims(0, 1, mg, mg, maxC, -1.0, Ct, maxC, sGC, Ct, maxC, sGC, 1.0, T, mg, sG, N, 1, dGGC, 16, stream)))
     return r;
   return 0;
 }

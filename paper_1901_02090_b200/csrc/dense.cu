@@ -835,8 +835,18 @@ extern "C" void bddc_set_leaf_regs(int on) {
 // rescaling: Cholesky-based inversion is insensitive to it, van der Sluis.)
 // `ws` must hold bddc_spd_inverse_workspace(n, batch, b) bytes; `info` (device
 // int) counts non-positive pivots.
+extern "C" int bddc_spd_inverse_batched_ex(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
+                                           int* info, int flags, void* stream);
+
 extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
                                         int* info, void* stream) {
+  return bddc_spd_inverse_batched_ex(Mat, n, ld, sM, batch, b, ws, info, 0, stream);
+}
+
+// flags & 1: only the upper triangle of the result is wanted (no lower mirror;
+// the strict lower triangle is left undefined).
+extern "C" int bddc_spd_inverse_batched_ex(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
+                                           int* info, int flags, void* stream) {
   if (n <= 0 || batch <= 0) return 0;
   if (b <= 0 || b > 64) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: leaf size must be in 1..64");
   cudaStream_t s = (cudaStream_t)stream;
@@ -847,6 +857,7 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
   } else {
     if ((r = chol_inv_rec(Mat, n, ld, sM, batch, b, rest, info, s, true))) return r;
     if ((r = lauum_rec(Mat, n, ld, sM, batch, b, rest, info, s))) return r;
+    if (flags & 1) return 0;
     const int nt = (n + 63) / 64;
     CUDA_OK(launch_pdl(lower_from_upper_kernel, dim3(nt * (nt + 1) / 2, batch), dim3(256), 0, s, Mat, n, ld, sM));
     LAUNCH_OK();

@@ -58,7 +58,9 @@ __global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, doubl
     while (bi + 1 < nt && tile_index(bi + 1, bi + 1, nt) <= t) ++bi;
     int bj = bi + (t - tile_index(bi, bi, nt));
     int r = bi * 32 + w / 32, c = bj * 32 + w % 32;
-    Pk[e] = F[(size_t)r * maxG + c];
+    // the upper triangle defines the matrix (diagonal tiles are stored full:
+    // their lower half is mirrored, so callers may leave the lower triangle undefined)
+    Pk[e] = (r <= c) ? F[(size_t)r * maxG + c] : F[(size_t)c * maxG + r];
   }
 }
 

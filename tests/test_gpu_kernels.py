@@ -96,6 +96,13 @@ def test_spd_inverse_vs_torch(n, b, batch):
     torch.cuda.synchronize()
     assert int(info.item()) == 0
     assert torch.allclose(M, ref, rtol=1e-11, atol=1e-14)
+    # upper-triangle-only variant: same upper triangle, bitwise
+    Mu = A.clone()
+    nat.call("bddc_spd_inverse_batched_ex", nat.ptr(Mu), n, n, n * n, batch, b, nat.ptr(ws),
+             nat.ptr(info), 1, st)
+    torch.cuda.synchronize()
+    iu = torch.triu_indices(n, n, device="cuda")
+    assert torch.equal(Mu[:, iu[0], iu[1]], M[:, iu[0], iu[1]])
 
 
 def test_rt0_operators_vs_scipy():
