@@ -134,8 +134,9 @@ def _mode_b(B, S, c, k, g, dec, cfg, args, rep, dev):
     del st
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tm = {}
     e0.record()
-    st = B.BddcSetup(system, dec, cfg)
+    st = B.BddcSetup(system, dec, cfg, timings=tm)
     e1.record()
     torch.cuda.synchronize()
     setup_s = rep.allmax(e0.elapsed_time(e1) / 1000.0)
@@ -173,7 +174,8 @@ def _mode_b(B, S, c, k, g, dec, cfg, args, rep, dev):
     out = {"bc": "BASELINE's: pressure 1 -> 0 along y, no-flow elsewhere, zero source "
                  "(mode B extension; no reference arm exists for it)",
            "value": value, "unit": "it/s", "time_to_solve_s": step_s / args.steps,
-           "setup_s": setup_s, "pcg_iterations": int(its[-1]), "kappa": float(kappa),
+           "setup_s": setup_s, "setup_phases_ms": tm, "pcg_iterations": int(its[-1]),
+           "kappa": float(kappa),
            "n_c": int(st.n_c),
            "e2e": {"value": rep.allsum(float(sum(e_its))) / e2e_s, "unit": "it/s",
                    "h2d_bytes_per_step": g.n_cells * 8,
