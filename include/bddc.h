@@ -82,7 +82,8 @@ int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha
 /* In-place inverse of a batch of SPD matrices (Cholesky, triangular inverse,
  * V V^T; recursive DMMA GEMMs above leaves of order <= b, b <= 64); replaces
  * SuperLU splu (substructure.py:66, coarse.py:159) and the dense coarse
- * lu_factor (coarse.py:196).  info counts non-positive pivots. */
+ * lu_factor (coarse.py:196).  info (zero on entry) receives 1 + the batch index
+ * of a matrix that met a non-positive pivot (0: all SPD). */
 size_t bddc_spd_inverse_workspace(int n, int batch, int b);
 /* Tuning knob: bit 0 = register leaves (32 / 64, default on; off = shared-memory
  * leaf), bit 1 = 64-leaf Cholesky and triangular inverse as two kernels (default on). */
@@ -303,6 +304,12 @@ int bddc_scale_cells(const bddc_geom* g, const double* f, const int* cell_sub, c
 size_t bddc_geom_size(void);
 /* Kernel launches issued so far (bench.py's gpu_launches). */
 unsigned long long bddc_launch_count(void);
+
+/* Page-lock a caller-owned host array in place / release it (solve()'s source
+ * upload, solver.py:301 f argument).  A failed registration is cleared from
+ * the runtime's error state before returning BDDC_ERR_CUDA. */
+int bddc_host_register(void* p, size_t bytes);
+int bddc_host_unregister(void* p);
 
 #ifdef __cplusplus
 }

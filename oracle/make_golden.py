@@ -41,10 +41,10 @@ def _random_k(counts, seed, orders=6.0):
     return 10.0 ** rng.uniform(-orders / 2, orders / 2, (n, len(counts)))
 
 
-def _c3_block(z0):
-    """30x30x15 cells cropped from the config-3 field (10x10x5 subdomains like C3)."""
+def _c3_block(z0, nz=15, ny=30, nx=30, y0=40, x0=10):
+    """Cells cropped from the config-3 field (default 30x30x15, C3's 10x10x5 subdomains)."""
     k = fields.config_field(3).reshape(85, 220, 60, 3)
-    return np.ascontiguousarray(k[z0:z0 + 15, 40:70, 10:40].reshape(-1, 3))
+    return np.ascontiguousarray(k[z0:z0 + nz, y0:y0 + ny, x0:x0 + nx].reshape(-1, 3))
 
 
 CASES = {
@@ -65,6 +65,13 @@ CASES = {
                     1e-8, lambda: _c3_block(28)),
     "g3d_uneven": ((12, 10, 8), (1.0, 2.0, 0.5), ((3, 5, 4), (2, 4, 4), (5, 3)), "multiplicity",
                    5.0, 1e-10, lambda: _random_k((12, 10, 8), 11)),
+    # C4-shaped subdomains (5x5x5 cells): 4x4x2 of them, across the z = 35 field seam
+    "g3d_c4block": ((20, 20, 10), (20.0, 10.0, 2.0), (4, 4, 2), "multiplicity", 10.0,
+                    1e-8, lambda: _c3_block(30, nz=10, ny=20, nx=20)),
+    # C3-shaped subdomains (10x10x5 cells), 4x4x4 = 64 of them (interior subdomains
+    # with all six faces shared), across the seam
+    "g3d_c3_64": ((40, 40, 20), (20.0, 10.0, 2.0), (4, 4, 4), "multiplicity", 10.0,
+                  1e-8, lambda: _c3_block(25, nz=20, ny=40, nx=40, y0=90, x0=10)),
     "g2d_ms": ((12, 12), (1.0, 1.0), (3, 3), "multiplicity", math.inf, 1e-10,
                lambda: _random_k((12, 12), 21)),
     "g3d_ms": ((8, 6, 6), (20.0, 10.0, 2.0), (2, 3, 2), "stiffness", math.inf, 1e-10,
@@ -84,7 +91,15 @@ CASES = {
     "c2_tau2": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
                 fields.CONFIGS[2]["splits"], "multiplicity", 2.0, 1e-8,
                 lambda: fields.config_field(2)),
+    "c2_tau100": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
+                  fields.CONFIGS[2]["splits"], "multiplicity", 100.0, 1e-8,
+                  lambda: fields.config_field(2)),
+    # tau = inf: face averages only, pairs still solved for omega~ (solver.py:85-88)
+    "c2_tauinf": (fields.CONFIGS[2]["counts"], fields.CONFIGS[2]["sizes"],
+                  fields.CONFIGS[2]["splits"], "multiplicity", math.inf, 1e-8,
+                  lambda: fields.config_field(2)),
 }
+ADAPTIVE_AT_INF = {"c2_tauinf"}
 
 
 def make(name):
@@ -106,7 +121,7 @@ def make(name):
         dec = R_dec.Decomposition(g, part)
     else:
         dec = R_dec.regular_partition(g, splits)
-    mode = "adaptive" if math.isfinite(tau) else "initial"
+    mode = "adaptive" if math.isfinite(tau) or name in ADAPTIVE_AT_INF else "initial"
     if name.endswith("_ms"):
         mode = "multiscale"   # MsMFEM baseline (adaptive.py:207-269)
     cfg = R_solver.SolveConfig(tau=tau, scaling=scaling, constraints=mode,

@@ -153,6 +153,8 @@ _SIGS = {
     "bddc_gamma_flux": [_I, _P, _P, _P, _I, _P],
     "bddc_face_shift": [_I, _I, _P, _P, _P, _P, _P],
     "bddc_scale_cells": [_GP, _P, _P, _P, _P, _P],
+    "bddc_host_register": [_P, C.c_size_t],
+    "bddc_host_unregister": [_P],
     "bddc_geom_size": [],
     "bddc_launch_count": [],
     "bddc_version": [],

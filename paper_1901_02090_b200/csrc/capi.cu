@@ -26,3 +26,25 @@ static int g_pdl = 1;
 extern "C" int bddc_pdl_enabled(void) { return g_pdl; }
 extern "C" void bddc_set_pdl(int on) { g_pdl = on ? 1 : 0; }
 extern "C" unsigned long long bddc_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+// Page-lock / release a caller-owned host array (the per-solve source upload
+// becomes one async DMA).  A failed registration (already registered by another
+// owner, unaligned or unsupported memory) is cleared from this runtime's sticky
+// error state here, so it can never surface at an unrelated later launch.
+extern "C" int bddc_host_register(void* p, size_t bytes) {
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+extern "C" int bddc_host_unregister(void* p) {
+  cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return 0;
+}

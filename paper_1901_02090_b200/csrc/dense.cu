@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(32) leaf_chol_inv_kernel(double* M, int nb, in
       __syncwarp();
     }
   }
-  if (lane == 0 && bad) atomicAdd(info, 1);
+  if (lane == 0 && bad) atomicCAS(info, 0, (int)blockIdx.x + 1);   // first failing matrix + 1
   if (mode & 2) {
     // X = V V^T: X[r][c] = sum_{k >= max(r,c)} V[r][k] V[c][k]
     for (int r = 0; r < nb; ++r)
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(32) leaf32_chol_inv_kernel(double* M, int nb, 
         if (c >= r) u[r] -= ukr * u[k];
       }
     }
-    if (c == 0 && bad) atomicAdd(info, 1);
+    if (c == 0 && bad) atomicCAS(info, 0, (int)blockIdx.x + 1);   // first failing matrix + 1
     // V = U^-1: column c solves U v = e_c by a backward sweep over the columns of U
 #pragma unroll
     for (int r = 0; r < 32; ++r) x[r] = (r == c) ? 1.0 : 0.0;
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(64) leaf64_chol_inv_kernel(double* M, int nb, 
         u[2 * r2 + 1] -= v.y * w;
       }
     }
-    if (c == 0 && bad) atomicAdd(info, 1);
+    if (c == 0 && bad) atomicCAS(info, 0, (int)blockIdx.x + 1);   // first failing matrix + 1
     if (MODE == 4) {   // U (upper) and 1/U_kk on the otherwise-zero diagonal-below slot
 #pragma unroll
       for (int r = 0; r < 64; ++r)

@@ -20,9 +20,10 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import views as _views
 from .coarse_nd import CoarseND
 from .decomposition import Decomposition
-from .errors import (ConfigurationError, InternalConsistencyError,
+from .errors import (ConfigurationError, ConstraintRankError, InternalConsistencyError,
                      InvalidArgumentError, NonConvergenceError,
                      NumericalFailureError)
 
@@ -312,9 +313,11 @@ class BddcSetup:
             self.pair_selected = d_nsel.cpu().numpy()
             self.pair_added = nadd
             self.pair_lambda = lam.view(nf, lam_ld)
-            if self.pair_spectra:
-                self.pair_reports = _pair_reports(dec, self.pair_lambda.cpu().numpy(),
-                                                  self.pair_selected)
+            # PairEigenReports for every adaptive setup (solver.py:76-88): the full
+            # spectrum with pair_spectra, else the eigenvalues the selection resolved
+            # (those above tau and the next one, which sets omega)
+            self.pair_reports = _pair_reports(dec, self.pair_lambda.cpu().numpy(),
+                                              self.pair_selected, complete=self.pair_spectra)
             self.face_omega = omega.cpu().numpy()
             self.omega_tilde = float(max(self.face_omega.max(), 1.0)) if nf else 1.0
         elif config.constraints == "adaptive":
@@ -331,6 +334,8 @@ class BddcSetup:
         self._mark(ev, "pairs")
         # coarse dof numbering: per face [initial, adaptive...]
         per_face = 1 + nadd
+        self._per_face = per_face
+        self._rows_dev, self._rows_maxsel = rows, maxsel   # harvested face rows (views.cset)
         cstart = np.concatenate([[0], np.cumsum(per_face)[:-1]]).astype(np.int64)
         self.n_flux_coarse = int(per_face.sum()) if nf else 0
         self._build_coarse_tables(cstart, per_face, maxsel)
@@ -392,10 +397,16 @@ class BddcSetup:
         main.wait_stream(side)   # T_i done; its workspaces may go now
         del Ct, Y, E, gam, ws, Sinv, dims, cl_args, self.d_S, self.d_T, Ct2, Y2, ws2, dims2, cl2
         bad = info.cpu().numpy()
+        # info slots hold 1 + the first failing subdomain (dense.cu leaf kernels)
         if bad[0] or bad[1]:
-            raise NumericalFailureError("local interior factorization failed", where=None)
+            i = int(bad[0] or bad[1]) - 1
+            raise NumericalFailureError(   # substructure.py:65-70
+                f"interior KKT factorization failed on subdomain {i}: "
+                "pressure Schur complement or S_i not positive definite", where=i)
         if bad[2] or bad[4]:
-            raise NumericalFailureError("constrained coarse basis system singular")
+            i = int(bad[2] or bad[4]) - 1
+            raise ConstraintRankError(   # coarse.py:159-163
+                f"constrained KKT singular on subdomain {i}; check constraint rank")
         if self.nd is not None:
             self.nd.check()
         self._mark(ev, "coarse")
@@ -572,8 +583,23 @@ class BddcSetup:
 
     def _pcg_bufs(self, maxit):
         if self._pcg_b is None or self._pcg_b.maxit < maxit:
+            # the captured PCG graphs hold the old history buffers' addresses: drop
+            # them before the buffers are freed (a cached graph would otherwise write
+            # alphas/betas/residuals into memory the allocator has handed out again)
+            self._drop_graphs()
             self._pcg_b = _PCGBufs(self, maxit)
         return self._pcg_b
+
+    def _drop_graphs(self):
+        graphs = getattr(self, "_graphs", None)
+        if not graphs:
+            return
+        torch.cuda.current_stream().synchronize()
+        lib = nat.load()
+        for g in graphs.values():
+            lib.bddc_graph_destroy(g)
+        graphs.clear()
+        self._graph_kernels.clear()
 
     def work(self):
         if self._work is None:
@@ -723,6 +749,53 @@ class BddcSetup:
                 t += 1
         return full[:n, :n]
 
+    # ------------------------------------- reference bookkeeping views (views.py)
+
+    def _view(self, name, make):
+        v = self.__dict__.get("_v_" + name)
+        if v is None:
+            v = make()
+            self.__dict__["_v_" + name] = v
+        return v
+
+    @property
+    def weights(self):
+        """WeightOperator (decomposition.py:199-209)."""
+        return self._view("weights", lambda: _views.WeightView(self))
+
+    @property
+    def broken(self):
+        """BrokenInterface (decomposition.py:242-279)."""
+        return self._view("broken", lambda: _views.BrokenInterface(self.weights))
+
+    @property
+    def subs(self):
+        """Per-subdomain operators (substructure.py:25-116)."""
+        return self._view("subs", lambda: [_views.SubdomainView(self, i)
+                                           for i in range(self.N)])
+
+    @property
+    def cset(self):
+        """ConstraintSet (coarse.py:36-118) in the reference's coarse numbering."""
+        return self._view("cset", lambda: _views.ConstraintSetView(self))
+
+    @property
+    def coarse(self):
+        """CoarseSpace.solve (coarse.py:208-215) on the device factorisation."""
+        return self._view("coarse", lambda: _views.CoarseView(self, self.cset))
+
+    def _face_row_values(self):
+        """Per face: (rows added beyond the initial one, m_f) i-side values on the
+        face's shared dofs (sorted), as the pair / multiscale kernels harvested them."""
+        dec = self.dec
+        nf = dec.n_faces
+        extra = self._per_face - 1
+        mx = int(extra.max()) if nf else 0
+        if mx == 0:
+            return [np.zeros((0, int(m))) for m in dec.face_table[:, 3]]
+        R = self._rows_dev.view(nf, self._rows_maxsel, -1)[:, :mx].cpu().numpy()
+        return [R[f, :int(extra[f]), :int(dec.face_table[f, 3])] for f in range(nf)]
+
     def net_flux_matrix(self):
         import scipy.sparse as sp
         dec = self.dec
@@ -747,6 +820,7 @@ class PairEigenReport:
     j: int
     eigenvalues: np.ndarray
     selected: int = 0
+    complete: bool = True   # False: only the leading selected + 1 eigenvalues resolved
 
     def omega(self, tau):
         lam = self.eigenvalues
@@ -754,15 +828,21 @@ class PairEigenReport:
         return float(max(below[0], 1.0)) if len(below) else 1.0
 
 
-def _pair_reports(dec, lam, selected):
+def _pair_reports(dec, lam, selected, complete=True):
+    """complete: the whole spectrum (reduced pencil resolved fully, then the zeros of
+    I - E); else the leading eigenvalues the selection resolved (selected + 1)."""
     ft = dec.face_table
     out = {}
     for f in range(dec.n_faces):
         i, j, m = int(ft[f, 0]), int(ft[f, 1]), int(ft[f, 3])
-        n_keep = int(dec.nG[i] + dec.nG[j]) - 1
-        ev = np.maximum(lam[f, :m], 0.0)
-        ev = np.concatenate([ev, np.zeros(max(n_keep - m, 0))])
-        out[(min(i, j), max(i, j))] = PairEigenReport(min(i, j), max(i, j), ev, int(selected[f]))
+        if complete:
+            n_keep = int(dec.nG[i] + dec.nG[j]) - 1
+            ev = np.maximum(lam[f, :m], 0.0)
+            ev = np.concatenate([ev, np.zeros(max(n_keep - m, 0))])
+        else:
+            ev = np.maximum(lam[f, :min(int(selected[f]) + 1, m)], 0.0)
+        out[(min(i, j), max(i, j))] = PairEigenReport(min(i, j), max(i, j), ev, int(selected[f]),
+                                                      complete)
     return out
 
 
@@ -1159,32 +1239,51 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
     return report
 
 
+# Process-wide page-lock table: (address, bytes) -> [owners, array, tensor].  Several
+# live setups may solve the same source array (a tau sweep keeping one setup per
+# tau); the array is registered once and released when its last owner lets go.
+_HOST_REG = {}
+
+
 def _pinned_source(setup, f):
-    """The caller's source array page-locked in place (cudaHostRegister, once per
-    array; the setup keeps a reference so the registration never outlives it), so
-    the per-solve upload is one async DMA without a host staging copy.  None when
-    f is not a contiguous float64 array or registration fails."""
+    """The caller's source array page-locked in place (bddc_host_register, once per
+    array and process; the setup holds a reference so the registration never
+    outlives the array), so the per-solve upload is one async DMA without a host
+    staging copy.  None when f is not a contiguous float64 array or registration
+    fails (the library clears the failed call's error state)."""
     if not (isinstance(f, np.ndarray) and f.dtype == np.float64 and f.flags.c_contiguous
             and f.size == setup.geom.n_cells):
         return None
     key = (f.__array_interface__["data"][0], f.nbytes)
     reg = getattr(setup, "_f_reg", None)
-    if reg is not None and reg[0] == key and reg[1] is f:
-        return reg[2]
+    if reg is not None and reg == key and _HOST_REG.get(key, (0, None))[1] is f:
+        return _HOST_REG[key][2]
     _unregister_source(setup)
-    cudart = torch.cuda.cudart()
-    if int(cudart.cudaHostRegister(key[0], key[1], 0)) != 0:
-        return None
-    setup._f_reg = (key, f, torch.from_numpy(f))
-    return setup._f_reg[2]
+    ent = _HOST_REG.get(key)
+    if ent is not None and ent[1] is not f:
+        return None   # another live array at this address: leave its registration alone
+    if ent is None:
+        if nat.load().bddc_host_register(C.c_void_p(key[0]), key[1]) != 0:
+            return None
+        ent = _HOST_REG[key] = [0, f, torch.from_numpy(f)]
+    ent[0] += 1
+    setup._f_reg = key
+    return ent[2]
 
 
 def _unregister_source(setup):
-    reg = getattr(setup, "_f_reg", None)
-    if reg is not None:
-        torch.cuda.current_stream().synchronize()
-        torch.cuda.cudart().cudaHostUnregister(reg[0][0])
-        setup._f_reg = None
+    key = getattr(setup, "_f_reg", None)
+    if key is None:
+        return
+    setup._f_reg = None
+    ent = _HOST_REG.get(key)
+    if ent is None:
+        return
+    ent[0] -= 1
+    if ent[0] <= 0:
+        del _HOST_REG[key]
+        torch.cuda.synchronize()   # no queued copy may still read the pages
+        nat.load().bddc_host_unregister(C.c_void_p(key[0]))
 
 
 def _d2h_async(setup, tensors):

@@ -1,0 +1,102 @@
+"""North-star parity at full size: BASELINE configs 3 and 4 against the oracle.
+
+Fixtures tests/golden/full_c{3,4}.npz come from `oracle/full_config.py` (the
+CPU restatement run once at 60x220x85 cells, mode A, with the harness
+substitutions pinned in tests/test_oracle_golden.py).  Long vectors are
+compared through their seeded CountSketch (oracle/sketch.py: linear, so the
+sketch of the difference is the difference of the sketches; relative
+spread ~1 % at K = 4096) and a seeded sample of entries, both estimating the
+relative L2 distance.  Gates (BASELINE north_star): identical coarse size,
+per-face constraint counts and selected counts, eigenvalues above tau and
+omega~ within 1e-8, PCG iterations within +-1, u and p within 1e-8.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from _golden import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+CFGS = [c for c in (3, 4) if os.path.exists(os.path.join(GOLDEN, f"full_c{c}.npz"))]
+
+
+def _load(c):
+    z = np.load(os.path.join(GOLDEN, f"full_c{c}.npz"), allow_pickle=False)
+    return {k: z[k] for k in z.files}
+
+
+def _dist(d, name, v):
+    """Relative L2 distance estimates of v from the oracle's vector `name`."""
+    from oracle.sketch import count_sketch
+    nrm = float(d[name + "_norm"])
+    sk = np.linalg.norm(count_sketch(v) - d[name + "_sketch"]) / nrm
+    s = d[name + "_sample"]
+    smp = np.linalg.norm(np.asarray(v)[d[name + "_idx"]] - s) / np.linalg.norm(s)
+    return sk, smp
+
+
+_RUNS = {}
+
+
+def _run(c):
+    if c in _RUNS:
+        return _RUNS[c]
+    import paper_1901_02090_b200 as B
+    from paper_1901_02090_b200 import fields
+    spec = fields.CONFIGS[c]
+    g = B.build_grid(3, spec["counts"], spec["sizes"])
+    system = B.assemble_system(g, B.Permeability(fields.config_field(c)), B.Wells(0, g.n_cells - 1))
+    dec = B.regular_partition(g, spec["splits"])
+    cfg = B.SolveConfig(tau=spec["tau"], scaling=spec["scaling"], constraints=spec["constraints"],
+                        tol=spec["tol"])
+    st = B.BddcSetup(system, dec, cfg)
+    rep = B.solve(system, dec, cfg, setup=st)
+    _RUNS[c] = (B, dec, st, rep)
+    return _RUNS[c]
+
+
+@pytest.mark.parametrize("c", CFGS)
+def test_full_config_constraints(c):
+    d = _load(c)
+    B, dec, st, rep = _run(c)
+    assert [tuple(p) for p in d["pairs"]] == dec.adjacent_pairs()
+    assert rep.n_c == int(d["n_c"])
+    np.testing.assert_array_equal(st.pair_selected, d["pair_selected"])
+    np.testing.assert_array_equal(st.pair_added + 1, d["face_rows"])
+    assert abs(st.omega_tilde - float(d["omega_tilde"])) <= 1e-8 * float(d["omega_tilde"])
+    np.testing.assert_allclose(st.face_omega, d["pair_omega"], rtol=1e-8)
+    lam = st.pair_lambda.cpu().numpy()
+    tau = float(d["tau"])
+    ref = d["pair_lam"]
+    for q in np.nonzero(d["pair_selected"])[0]:
+        k = int(d["pair_selected"][q])
+        assert np.all(ref[q, :k] > tau)
+        np.testing.assert_allclose(lam[q, :k], ref[q, :k], rtol=1e-8)
+
+
+@pytest.mark.parametrize("c", CFGS)
+def test_full_config_solution(c):
+    d = _load(c)
+    B, dec, st, rep = _run(c)
+    assert rep.converged and not rep.pressure_warning
+    assert abs(rep.it - int(d["it"])) <= 1
+    if rep.it == int(d["it"]):
+        assert abs(rep.kappa - float(d["kappa"])) <= 1e-4 * float(d["kappa"])
+    for name, v, bar in (("u", rep.u, 1e-8), ("p", rep.p, 1e-8),
+                         ("u0", rep.u0, 5e-8), ("u_star", rep.u_star, 5e-8)):
+        sk, smp = _dist(d, name, v)
+        assert sk <= bar and smp <= bar, (name, sk, smp)
+    assert abs(rep.conservation_defect - float(d["conservation_defect"])) <= 1e-10
+
+
+@pytest.mark.parametrize("c", CFGS)
+def test_full_config_operators(c):
+    d = _load(c)
+    B, dec, st, rep = _run(c)
+    x = np.random.default_rng(int(d["x_seed"])).standard_normal(int(d["n_gamma"]))
+    for name, v, bar in (("Sx", st.schur_matvec(x), 1e-10), ("Mx", st.precondition(x), 1e-9),
+                         ("Px", st.project_balanced(x), 1e-13)):
+        sk, smp = _dist(d, name, v)
+        assert sk <= bar and smp <= bar, (name, sk, smp)

@@ -2,10 +2,23 @@
 
 Gates (BASELINE north_star): same selected constraint count per face, PCG
 iterations within +-1, fluxes/pressures within 1e-8 rel L2, above-tau
-eigenvalues within 1e-8 rel.  Cases whose Lanczos kappa exceeds 100 (the
-rho-scaled C1 field, kappa ~ 841) have rounding-sensitive iteration counts
-(the reference and its own CPU oracle differ there too); for those the count
-bar is max(2, 5%) and the flux bar is 2e-8 (Parity).
+eigenvalues within 1e-8 rel.  Bars per case class (measured values in
+DESIGN.md, Parity; `scripts/parity_report.py` prints them):
+
+* kappa <= 100 (every adaptive case but c1_rho): it +-1, u and p <= 1e-8.
+* kappa > 100 (c1_rho kappa 841, g3d_ms 566, g2d_ms 121, g2d_small 1680):
+  rounding-sensitive iteration counts -- the reference and its own CPU
+  oracle differ there too -- so it +-max(2, 5%), u and p <= 2e-8.
+* tau = inf on the channelised C2 field (kappa 7.5e4, 775 iterations;
+  SURVEY 8c): it within +-1 %, u and p <= 1e-6.
+* intermediate iterates u0 (harmonic extension of the coarse trace) and u*
+  (trace solve): <= 5e-8 (the explicit-inverse coarse basis carries
+  cond(S_i) eps ~ 1e-9 relative; measured <= 1.5e-8 on the 6-decade C2
+  field, <= 3e-10 elsewhere); conservation defect of u* <= 1e-10 absolute
+  (the reference's own acceptance bar, test_acceptance.py:247).
+* operators: S x and M x within 1e-12 relative, or -- where the field's
+  contrast makes the assembled vector cancel -- within 1e-13 of the
+  norm-wise scale sum_i |S_i| |x_i| (resp. |M| |x|); P x within 1e-13.
 """
 import math
 
@@ -35,7 +48,6 @@ def _sensitive(d):
 @pytest.mark.parametrize("name", CASES)
 def test_solution_parity(name):
     d = load(name)
-    d["name"] = name
     B, system, dec, cfg = _setup(d)
     st = B.BddcSetup(system, dec, cfg)
     rep = B.solve(system, dec, cfg, setup=st)
@@ -43,17 +55,26 @@ def test_solution_parity(name):
     np.testing.assert_array_equal(st.pair_added + 1 if st.pair_added is not None
                                   else np.ones(dec.n_faces, int), d["face_rows"])
     it_ref = int(d["it"])
-    if _sensitive(d):
+    if not math.isfinite(d["tau"]) and d["mode"] == "adaptive":
+        assert abs(rep.it - it_ref) <= max(1, int(0.01 * it_ref))
+        bar = 1e-6
+    elif _sensitive(d):
         assert abs(rep.it - it_ref) <= max(2, int(0.05 * it_ref))
-        assert rel(rep.u, d["u"]) <= 2e-8
+        bar = 2e-8
     else:
         assert abs(rep.it - it_ref) <= 1
-        assert rel(rep.u, d["u"]) <= 1e-8
-        assert rel(rep.p, d["p"]) <= 1e-8
+        bar = 1e-8
         if rep.it == it_ref:
             assert abs(rep.kappa - float(d["kappa"])) <= 1e-4 * float(d["kappa"])
+    assert rel(rep.u, d["u"]) <= bar
+    assert rel(rep.p, d["p"]) <= bar
+    assert rel(rep.u0, d["u0"]) <= 5e-8
+    assert rel(rep.u_star, d["u_star"]) <= 5e-8
+    cd_ref = float(d["conservation_defect"])
+    assert abs(rep.conservation_defect - cd_ref) <= 1e-10 + 1e-8 * cd_ref
     assert rep.converged and not rep.pressure_warning
     assert abs(rep.p.mean()) <= 1e-12 * max(np.abs(rep.p).max(), 1.0)
+    assert len(rep.residuals) == rep.it + 1 and rep.residuals[0] == 1.0
 
 
 @pytest.mark.parametrize("name", [n for n in CASES if "pair_selected" in load(n)])
@@ -72,16 +93,31 @@ def test_adaptive_parity(name):
             np.testing.assert_allclose(lam[q, :int(m.sum())], ref[m], rtol=1e-8)
 
 
-@pytest.mark.parametrize("name", ["g2d_small", "g2d_adapt", "g3d_adapt", "g3d_thin", "c0"])
+def _op_close(mine, ref, scale, what):
+    err = np.linalg.norm(mine - ref)
+    assert err <= 1e-12 * np.linalg.norm(ref) or err <= 1e-13 * scale, (what, err, scale)
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n != "c2_tauinf"])
 def test_operator_parity(name):
     d = load(name)
     B, system, dec, cfg = _setup(d)
     st = B.BddcSetup(system, dec, cfg)
     assert rel(st.schur_dense(0), d["S_sub0"]) <= 1e-11
     assert rel(st.schur_dense(dec.n_subdomains - 1), d["S_sublast"]) <= 1e-11
-    assert rel(st.schur_matvec(d["x"]), d["Sx"]) <= 1e-10
-    assert rel(st.project_balanced(d["x"]), d["Px"]) <= 1e-13
-    assert rel(st.precondition(d["x"]), d["Mx"]) <= 1e-9
+    x = d["x"]
+    gd = dec.gamma_dofs
+    pos = [np.searchsorted(dec.gamma, g) for g in gd]
+    s_scale = math.sqrt(sum((np.linalg.norm(st.schur_dense(i), 2) * np.linalg.norm(x[pos[i]])) ** 2
+                            for i in range(dec.n_subdomains)))
+    _op_close(st.schur_matvec(x), d["Sx"], s_scale, "Sx")
+    assert rel(st.project_balanced(x), d["Px"]) <= 1e-13
+    # |M| from the action on x and on a few random vectors (power-iteration floor)
+    mx = st.precondition(x)
+    rng = np.random.default_rng(0)
+    m_norm = max(np.linalg.norm(st.precondition(v)) / np.linalg.norm(v)
+                 for v in [x] + [rng.standard_normal(len(x)) for _ in range(3)])
+    _op_close(mx, d["Mx"], m_norm * np.linalg.norm(x), "Mx")
 
 
 @pytest.mark.parametrize("name", [n for n in CASES if "pair_selected" in load(n)])

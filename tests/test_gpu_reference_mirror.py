@@ -106,3 +106,141 @@ def test_coarse_counts_2x7():
     st = B.BddcSetup(system, dec, B.SolveConfig(constraints="initial"))
     assert dec.n_faces == 1 * 7 + 2 * 6
     assert st.n_c == dec.n_faces + dec.n_subdomains
+
+
+# ------------------------------------------------ reference bookkeeping views
+
+def _golden_setup(name):
+    from _golden import load
+    import paper_1901_02090_b200 as B
+    d = load(name)
+    g = B.build_grid(len(d["counts"]), d["counts"], d["sizes"])
+    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1))
+    dec = B.regular_partition(g, d["splits"])
+    cfg = B.SolveConfig(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
+    return d, B, system, dec, B.BddcSetup(system, dec, cfg)
+
+
+@pytest.mark.parametrize("name", ["g2d_adapt", "g3d_thin", "c1_rho"])
+def test_broken_interface_E(name):
+    """test_decomposition.py:132-146 and test_acceptance.py:226-230: E is a projection
+    and average(expand(x)) = x; weights match the oracle's (decomposition.py:212-239)."""
+    from oracle import bddc_oracle as O
+    d, B, system, dec, st = _golden_setup(name)
+    br = st.broken
+    rng = np.random.default_rng(0)
+    w = rng.standard_normal(br.size)
+    ew = br.apply_E(w)
+    assert np.abs(br.apply_E(ew) - ew).max() <= 1e-12
+    x = rng.standard_normal(dec.n_gamma)
+    np.testing.assert_allclose(br.average(br.expand(x)), x, atol=1e-13)
+    mesh = O.Mesh(d["counts"], d["sizes"])
+    ref = O.weights(O.BoxPartition(mesh, d["splits"]), d["k"], d["scaling"])
+    for i in range(dec.n_subdomains):
+        np.testing.assert_allclose(st.weights.delta[i], ref[i], rtol=1e-14, atol=0)
+        assert len(br.local(w, i)) == int(dec.nG[i])
+
+
+@pytest.mark.parametrize("name", ["g2d_adapt", "g3d_adapt", "c2_tau10", "g3d_ms"])
+def test_constraint_set_view(name):
+    """test_adaptive.py:51-82, 105-110: rows per face match the reference's, rows are
+    antisymmetric across the face, every subdomain's rows have full rank, the coarse
+    size is the row count plus one pressure per subdomain."""
+    d, B, system, dec, st = _golden_setup(name)
+    cs = st.cset
+    assert cs.n_flux_coarse == st.n_flux_coarse
+    assert cs.n_coarse == int(d["n_c"])
+    counts = [len(cs.rows_for_face(i, j)) // 2 for (i, j) in dec.adjacent_pairs()]
+    np.testing.assert_array_equal(counts, d["face_rows"])
+    ids = sorted(r.coarse_dof for rows in cs.rows for r in rows if r.sign > 0)
+    assert ids == list(range(cs.n_flux_coarse))
+    for (i, j) in dec.adjacent_pairs():
+        rows = cs.rows_for_face(i, j)
+        byg = {}
+        for s, r in rows:
+            byg.setdefault(r.coarse_dof, []).append((s, r))
+        for g, pair in byg.items():
+            (si, ri), (sj, rj) = sorted(pair, key=lambda t: t[0])
+            shared = dec.faces[(i, j)][0].dofs
+            vi = ri.values[dec.gamma_index(si, shared)]
+            vj = rj.values[dec.gamma_index(sj, shared)]
+            np.testing.assert_allclose(vi, -vj, atol=0)
+            if ri.origin == "adaptive":   # adaptive.py:168-170: i-half scaled to max |c| = 1
+                assert np.abs(vi).max() == pytest.approx(1.0)
+            elif ri.origin == "initial":
+                np.testing.assert_array_equal(np.abs(vi), 1.0)
+    cs.check_rank()
+
+
+@pytest.mark.parametrize("name", ["g2d_adapt", "g3d_c3block", "c2_tau10", "c2_tau100"])
+def test_pair_reports_filled(name):
+    """solver.py:76-88: every adaptive setup carries PairEigenReports; their leading
+    eigenvalues match the reference's, selected counts and omega agree."""
+    d, B, system, dec, st = _golden_setup(name)
+    reps = st.pair_reports
+    pairs = [tuple(p) for p in d["pairs"]]
+    assert sorted(reps) == sorted(pairs)
+    tau = float(d["tau"])
+    for q, key in enumerate(pairs):
+        r = reps[key]
+        assert r.selected == int(d["pair_selected"][q])
+        ref = d["pair_lam"][q]
+        n = len(r.eigenvalues)
+        assert n == min(r.selected + 1, int(np.isfinite(ref).sum()))
+        scale = max(float(ref[0]), 1.0)
+        np.testing.assert_allclose(r.eigenvalues, ref[:n], rtol=1e-8, atol=1e-10 * scale)
+        assert r.omega(tau) == pytest.approx(st.face_omega[q], rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["g2d_adapt", "g3d_box"])
+def test_subs_and_coarse_views(name):
+    """substructure.py:90-99 (dense S_i) and coarse.py:208-215 (pinned coarse solve in
+    the reference's numbering) against the golden S and the oracle's coarse solve."""
+    from _golden import rel
+    from oracle import bddc_oracle as O
+    d, B, system, dec, st = _golden_setup(name)
+    assert rel(st.subs[0].schur_dense(), d["S_sub0"]) <= 1e-11
+    x = np.random.default_rng(3).standard_normal(int(dec.nG[0]))
+    assert rel(st.subs[0].schur_apply(x), d["S_sub0"] @ x) <= 1e-11
+    mesh = O.Mesh(d["counts"], d["sizes"])
+    cfg = O.Config(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
+    ost = O.Setup(mesh, d["k"], O.well_rhs(mesh, 0, mesh.n_cells - 1), d["splits"], cfg)
+    rng = np.random.default_rng(4)
+    rf = rng.standard_normal(st.cset.n_flux_coarse)
+    rq = rng.standard_normal(dec.n_subdomains)
+    rq -= rq.mean()
+    xf, xp = st.coarse.solve(rf, rq)
+    of, op = ost.coarse.solve(rf, rq)
+    assert rel(xf, of) <= 1e-10
+    assert rel(xp[1:], op[1:]) <= 1e-10
+
+
+def test_graph_cache_survives_history_realloc():
+    """a larger maxit reallocates the PCG history; cached graphs of the
+    smaller maxit must not write into the freed buffers (history and kappa of a
+    repeated solve stay identical)."""
+    B, g, system, dec = _problem(11)
+    cfg_s = B.SolveConfig(tol=1e-10, maxit=100)
+    st = B.BddcSetup(system, dec, cfg_s)
+    a = B.solve(system, dec, cfg_s, setup=st)
+    B.solve(system, dec, B.SolveConfig(tol=1e-10, maxit=10000), setup=st)
+    c = B.solve(system, dec, cfg_s, setup=st)
+    assert a.it == c.it and a.kappa == c.kappa
+    np.testing.assert_array_equal(a.residuals, c.residuals)
+    np.testing.assert_array_equal(a.u, c.u)
+
+
+def test_two_setups_same_source_twice():
+    """two live setups solving one source array twice each (the source is
+    page-locked once per process; a refused registration must not poison later
+    launches)."""
+    B, g, system, dec = _problem(12)
+    s1 = B.BddcSetup(system, dec, B.SolveConfig(tol=1e-10, constraints="adaptive", tau=10.0))
+    s2 = B.BddcSetup(system, dec, B.SolveConfig(tol=1e-10, constraints="adaptive", tau=3.0))
+    reps = [B.solve(system, dec, st.config, setup=st) for st in (s1, s2, s1, s2)]
+    np.testing.assert_array_equal(reps[0].u, reps[2].u)
+    np.testing.assert_array_equal(reps[1].u, reps[3].u)
+    assert all(r.converged for r in reps)
+    del s1
+    r = B.solve(system, dec, s2.config, setup=s2)
+    np.testing.assert_array_equal(r.u, reps[1].u)
