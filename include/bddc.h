@@ -301,6 +301,15 @@ int bddc_face_shift(int n, int n_faces, const int* gface, const int* faces, cons
 int bddc_scale_cells(const bddc_geom* g, const double* f, const int* cell_sub, const double* Dsub,
                      double* out, void* stream);
 
+/* Same product, persistent and bulk-streamed: `grid` CTAs (<= 0: one per SM)
+ * take subdomains from a ticket counter; each streams its live packed tiles
+ * with cp.async.bulk into an mbarrier-tracked shared-memory ring.  `sched`:
+ * two ints, zero before the first call, owned by one call site (the kernel
+ * re-arms them).  Replaces schur_apply / delta_solve loops (solver.py:103-128). */
+int bddc_gather_symv_bulk(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                          const double* x, const double* win, double* yb, int grid, int* sched,
+                          void* stream);
+
 size_t bddc_geom_size(void);
 /* Kernel launches issued so far (bench.py's gpu_launches). */
 unsigned long long bddc_launch_count(void);

@@ -53,6 +53,14 @@ def fingerprint(out, name, v):
     out[name + "_sample"] = v[idx]
 
 
+def compact_pair_lam(out, lams, sel):
+    """Per face the selected eigenvalues (> tau) and the next one (omega), flattened:
+    face q owns pair_lam_flat[pair_lam_ptr[q]:pair_lam_ptr[q + 1]]."""
+    parts = [np.asarray(l, dtype=np.float64)[:int(k) + 1] for l, k in zip(lams, sel)]
+    out["pair_lam_ptr"] = np.concatenate([[0], np.cumsum([len(p) for p in parts])]).astype(np.int64)
+    out["pair_lam_flat"] = np.concatenate(parts) if parts else np.zeros(0)
+
+
 def run(cfg_id, workers):
     spec = fields.CONFIGS[cfg_id]
     t0 = time.time()
@@ -92,12 +100,7 @@ def run(cfg_id, workers):
     out["face_rows"] = np.array([len(r) for r in st.cons.face_rows])
     sel = np.array([st.pairs[key].selected for key in pairs])
     out["pair_selected"] = sel
-    top = int(sel.max()) + 2 if len(sel) else 2
-    lam = np.full((len(pairs), top), np.nan)
-    for q, key in enumerate(pairs):
-        ev = st.pairs[key].lam[:top]
-        lam[q, :len(ev)] = ev
-    out["pair_lam"] = lam
+    compact_pair_lam(out, [st.pairs[key].lam for key in pairs], sel)
     out["pair_omega"] = np.array([st.pairs[key].omega(spec["tau"]) for key in pairs])
     path = os.path.join(REPO, "tests", "golden", f"full_c{cfg_id}.npz")
     np.savez_compressed(path, **out)

@@ -122,6 +122,7 @@ _SIGS = {
     "bddc_sym_packed_elems": [_I],
     "bddc_pack_sym": [_I, _I, _P, _P, _P],
     "bddc_gather_symv": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P],
+    "bddc_gather_symv_bulk": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P],
     "bddc_gather_gemv_t": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "bddc_coarse_restrict": [_I, _P, _P, _P, _P],
     "bddc_prolong": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],

@@ -142,6 +142,228 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// Persistent bulk-streamed symmetric GEMV (the interface operator S_i and the
+// preconditioner's T_i, solver.py:103-107 / coarse.py:237-245).
+//
+// One CTA per SM; subdomains are handed out by a global ticket counter.  Warp
+// roles (mbarrier-synchronised, no CTA-wide barrier after the prologue):
+//   gather   takes the ticket and stages win . x of the subdomain's interface
+//            slots into one of two x buffers (runs one subdomain ahead);
+//   issuer   streams the subdomain's live packed 32x32 tiles with
+//            cp.async.bulk (TMA engine, no register staging) into a ring of
+//            SB_NST slots;
+//   8 consumers: the CTA's G-th tile (counted across subdomains) goes to warp
+//            G % 8 through slot G % SB_NST, so every slot has one consumer warp
+//            and its mbarrier phases are consumed in order; the warp multiplies
+//            the tile by x on both sides (row and, off the diagonal, column
+//            contribution) into its own accumulator of that subdomain buffer;
+//   epilogue sums the eight accumulators in warp order, writes y and frees the
+//            buffer.
+// Consumers never wait at subdomain boundaries; 128 KB of tiles are in flight
+// per SM, so a grid of fewer CTAs than SMs still saturates HBM and leaves SMs to
+// a concurrent coarse chain.  Results do not depend on which CTA takes which
+// subdomain (bitwise reproducible).
+#define SB_NCW 8
+#define SB_NST 16
+#define SB_THREADS (32 * (SB_NCW + 3))
+#define SB_ISSUER SB_NCW
+#define SB_GATHER (SB_NCW + 1)
+#define SB_EPI (SB_NCW + 2)
+
+__device__ __forceinline__ void tile_symv(const double* T, const double* xr, const double* xc, int lane,
+                                          double& rsum, double& csum) {
+  // rsum (lane l) = sum_c T[l][c] xc[c];  csum (lane l) = sum_r T[r][l] xr[r]
+  const double xl = xc[lane];
+  double v[32];
+  double col = 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const double a = T[r * 32 + lane];
+    v[r] = a * xl;
+    col += a * xr[r];
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = lane & off;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      double send = up ? v[k] : v[k + off];
+      double recv = __shfl_xor_sync(0xffffffffu, send, off);
+      v[k] = (up ? v[k + off] : v[k]) + recv;
+    }
+  }
+  rsum = v[0];
+  csum = col;
+}
+
+// advance (bi, bj) by `steps` positions in the row-major order of the live upper
+// triangle (bi <= bj < ntl)
+__device__ __forceinline__ void tri_advance(int& bi, int& bj, int ntl, int steps) {
+  for (int s = 0; s < steps; ++s) {
+    if (++bj == ntl) {
+      ++bi;
+      bj = bi;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SB_THREADS, 1)
+symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restrict__ gpos,
+                 const double* __restrict__ packed, const double* __restrict__ x,
+                 const double* __restrict__ win, double* __restrict__ yb, int* __restrict__ sched) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const int nt = maxG / 32;
+  const size_t ntiles = (size_t)nt * (nt + 1) / 2;
+  double* ring = reinterpret_cast<double*>(smraw);    // SB_NST tiles
+  double* xs = ring + SB_NST * 1024;                   // 2 x maxG  (per subdomain buffer b)
+  double* yw = xs + 2 * maxG;                          // 2 x SB_NCW x maxG accumulators
+  uint64_t* full = reinterpret_cast<uint64_t*>(yw + 2 * SB_NCW * maxG);
+  uint64_t* empty = full + SB_NST;
+  uint64_t* xfull = empty + SB_NST;   // [2] x staged (gather -> issuer, consumers, epilogue)
+  uint64_t* xfree = xfull + 2;        // [2] buffer released (epilogue -> gather)
+  uint64_t* ydone = xfree + 2;        // [2] accumulators complete (consumers -> epilogue)
+  int* meta = reinterpret_cast<int*>(ydone + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < SB_NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(xfull + b, 32);
+      mbar_init(xfree + b, 32);
+      mbar_init(ydone + b, SB_NCW);
+    }
+    mbar_fence_init();
+  }
+  for (int e = threadIdx.x; e < 2 * SB_NCW * maxG; e += blockDim.x) yw[e] = 0.0;
+  __syncthreads();
+  if (warp == SB_GATHER) {
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(xfree + b, ((k >> 1) & 1) ^ 1);
+      int i = 0;
+      if (lane == 0) i = atomicAdd(sched, 1);
+      i = __shfl_sync(FULL, i, 0);
+      if (i >= N) {
+        if (lane == 0) meta[b] = -1;
+        __syncwarp();
+        mbar_arrive(xfull + b);
+        break;
+      }
+      const int n = nG[i];
+      const int ntl = (n + 31) / 32;
+      double* xb = xs + b * maxG;
+      int gp[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = lane + 32 * u;
+        gp[u] = (u < ntl && c < n) ? gpos[(size_t)i * maxG + c] : -1;
+      }
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = gp[u] >= 0 ? x[gp[u]] : 0.0;
+      if (win) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (gp[u] >= 0) v[u] *= win[(size_t)i * maxG + lane + 32 * u];
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (u < ntl) xb[lane + 32 * u] = v[u];
+      if (lane == 0) meta[b] = i;
+      __syncwarp();
+      mbar_arrive(xfull + b);
+    }
+    if (lane == 0) {
+      // the last CTA to finish re-arms the ticket counter for the next launch
+      __threadfence();
+      if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+        atomicExch(sched, 0);
+        atomicExch(sched + 1, 0);
+      }
+    }
+  } else if (warp == SB_ISSUER) {
+    if (lane == 0) {
+      unsigned G = 0;
+      for (int k = 0;; ++k) {
+        const int b = k & 1;
+        mbar_wait(xfull + b, (k >> 1) & 1);
+        const int i = meta[b];
+        if (i < 0) break;
+        const int ntl = (nG[i] + 31) / 32;
+        const double* Pk = packed + (size_t)i * ntiles * 1024;
+        for (int bi = 0; bi < ntl; ++bi) {
+          const double* row = Pk + (size_t)tile_index(bi, bi, nt) * 1024;
+          for (int bj = bi; bj < ntl; ++bj, ++G) {
+            const unsigned slot = G % SB_NST;
+            mbar_wait(empty + slot, ((G / SB_NST) & 1) ^ 1);
+            mbar_arrive_expect_tx(full + slot, 8192u);
+            bulk_g2s(ring + slot * 1024, row + (size_t)(bj - bi) * 1024, 8192u, full + slot);
+          }
+        }
+      }
+    }
+  } else if (warp == SB_EPI) {
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(xfull + b, (k >> 1) & 1);
+      const int i = meta[b];
+      if (i < 0) break;
+      const int n = nG[i];
+      const int ntl = (n + 31) / 32;
+      mbar_wait(ydone + b, (k >> 1) & 1);
+      double* yk = yw + (size_t)b * SB_NCW * maxG;
+      for (int e = lane; e < ntl * 32; e += 32) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < SB_NCW; ++w) {
+          acc += yk[w * maxG + e];
+          yk[w * maxG + e] = 0.0;
+        }
+        if (e < n) yb[(size_t)i * maxG + e] = acc;
+      }
+      __syncwarp();
+      mbar_arrive(xfree + b);
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    unsigned G = 0;   // CTA-wide index of the first tile of the current subdomain
+    for (int k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(xfull + b, (k >> 1) & 1);
+      const int i = meta[b];
+      if (i < 0) break;
+      const int ntl = (nG[i] + 31) / 32;
+      const int T = ntl * (ntl + 1) / 2;
+      const double* xb = xs + b * maxG;
+      int t = (int)((warp - G % SB_NCW + SB_NCW) % SB_NCW);
+      // accumulator by the subdomain-local tile class t % 8 (not by warp): the
+      // summation grouping is independent of the CTA's history (deterministic)
+      double* myy = yw + ((size_t)b * SB_NCW + t) * maxG;
+      int bi = 0, bj = 0;
+      tri_advance(bi, bj, ntl, t);
+      for (; t < T; t += SB_NCW) {
+        const unsigned g = G + t;
+        const unsigned slot = g % SB_NST;
+        mbar_wait(full + slot, (g / SB_NST) & 1);
+        double rs, cs;
+        tile_symv(ring + slot * 1024, xb + bi * 32, xb + bj * 32, lane, rs, cs);
+        myy[bi * 32 + lane] += rs;
+        if (bi != bj) myy[bj * 32 + lane] += cs;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + slot);
+        tri_advance(bi, bj, ntl, SB_NCW);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ydone + b);
+      G += T;
+    }
+  }
+}
+
 // v[i][r] = sum_q PsiT[i][r][q] * win[i][q] * x[gpos[i][q]]   (warp per coarse row r)
 __global__ void gather_gemv_t_kernel(int maxG, int maxC, const int* __restrict__ nG, const int* __restrict__ nC,
                                      const int* __restrict__ gpos, const double* __restrict__ PsiT,
@@ -698,6 +920,36 @@ extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos,
     gather_symv_kernel<512><<<grid, 512, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
   else
     gather_symv_kernel<256><<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
+  LAUNCH_OK();
+  return 0;
+}
+
+static size_t symv_bulk_smem(int maxG) {
+  return (size_t)SB_NST * 8192 + (size_t)(2 + 2 * SB_NCW) * maxG * sizeof(double) +
+         (2 * SB_NST + 6) * sizeof(uint64_t) + 2 * sizeof(int);
+}
+
+// Persistent bulk-streamed variant: `grid` CTAs (<= 0: one per SM), `sched` two
+// zero-initialised ints owned by this call site (re-armed by the kernel).
+extern "C" int bddc_gather_symv_bulk(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                                     const double* x, const double* win, double* yb, int grid, int* sched,
+                                     void* stream) {
+  if (maxG % 32 || maxG > 512) return bddc_set_error(BDDC_ERR_ARG, "gather_symv_bulk: maxG (multiple of 32, <= 512)");
+  const size_t shm = symv_bulk_smem(maxG);
+  static size_t configured = 0;
+  if (shm > configured) {
+    CUDA_OK(cudaFuncSetAttribute(symv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    configured = shm;
+  }
+  if (grid <= 0) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (grid > N) grid = N;
+  if (N == 0) return 0;
+  CUDA_OK(launch_prio(symv_bulk_kernel, dim3(grid), dim3(SB_THREADS), shm, (cudaStream_t)stream, N, maxG, nG,
+                      gpos, packed, x, win, yb, sched));
   LAUNCH_OK();
   return 0;
 }

@@ -441,6 +441,12 @@ class BddcSetup:
         # 1357 with 512-thread CTAs; the chain's kernels carry the side stream's
         # priority as a launch attribute so it survives graph capture)
         self.t_grid = self.n_sm
+        # persistent bulk-streamed S_i / T_i GEMVs (one CTA per SM, ~160 KB of tiles
+        # in flight each): S on every SM; T on t_grid_bulk SMs, the rest left to the
+        # concurrent coarse chain
+        self.symv_bulk = dec.maxG <= 512   # the bulk kernel stages up to 512 slots
+        self.t_grid_bulk = max(1, self.n_sm - 20)
+        self._sched = torch.zeros(8, dtype=I32, device=dev)   # ticket counters per call site
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._solves = 0   # public solves run on this setup
@@ -631,8 +637,7 @@ class BddcSetup:
         if kt is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e0.record()
-        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_Sp), _p(x), None, _p(self.w_yb), 0, st)
+        self._symv(self.d_Sp, x, None, self.w_yb, 0, 0, st)
         if kt is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
@@ -689,9 +694,10 @@ class BddcSetup:
                 join.record(side)
         # T_i GEMV with one CTA per SM (grid-stride over subdomains) so the
         # concurrent coarse chain finds free SM slots
-        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_Tp), _p(r), _p(self.d_delta), _p(self.w_yb),
-                 self.t_grid if self.nfc else 0, st)
+        if self.symv_bulk:
+            self._symv(self.d_Tp, r, self.d_delta, self.w_yb, self.t_grid_bulk if self.nfc else 0, 1, st)
+        else:
+            self._symv(self.d_Tp, r, self.d_delta, self.w_yb, self.t_grid if self.nfc else 0, 1, st)
         if self.nfc:
             main.wait_event(join)
         nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG), _p(self.d_nC),
@@ -699,19 +705,27 @@ class BddcSetup:
                  _p(self.d_delta), _p(self.w_yb2), st)
         nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
 
+    def _symv(self, mats, x, win, yb, grid, site, st):
+        """yb = blockdiag(M_i) (win . x) gathered per subdomain (bulk kernel unless
+        symv_bulk is off; `site` selects this call site's ticket counter)."""
+        if self.symv_bulk:
+            nat.call("bddc_gather_symv_bulk", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(mats), _p(x), _p(win), _p(yb), grid, _p(self._sched[2 * site:]), st)
+        else:
+            nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(mats), _p(x), _p(win), _p(yb), grid, st)
+
     def time_kernel(self, which="S", reps=20):
         """Mean device time (s) of one interface GEMV launch (bench roofline helper)."""
         mats = {"S": self.d_Sp, "T": self.d_Tp}[which]
         x = torch.ones(max(self.n_gamma, 1), dtype=F64, device=self.dev)
         st = _stream()
-        nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(mats), _p(x), None, _p(self.w_yb), 0, st)
+        self._symv(mats, x, None, self.w_yb, 0, 2, st)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(reps):
-            nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                     _p(mats), _p(x), None, _p(self.w_yb), 0, st)
+            self._symv(mats, x, None, self.w_yb, 0, 2, st)
         b.record()
         b.synchronize()
         return a.elapsed_time(b) / 1000.0 / reps

@@ -69,11 +69,12 @@ def test_full_config_constraints(c):
     np.testing.assert_allclose(st.face_omega, d["pair_omega"], rtol=1e-8)
     lam = st.pair_lambda.cpu().numpy()
     tau = float(d["tau"])
-    ref = d["pair_lam"]
+    ptr, flat = d["pair_lam_ptr"], d["pair_lam_flat"]
     for q in np.nonzero(d["pair_selected"])[0]:
         k = int(d["pair_selected"][q])
-        assert np.all(ref[q, :k] > tau)
-        np.testing.assert_allclose(lam[q, :k], ref[q, :k], rtol=1e-8)
+        ref = flat[ptr[q]:ptr[q] + k]
+        assert np.all(ref > tau)
+        np.testing.assert_allclose(lam[q, :k], ref, rtol=1e-8)
 
 
 @pytest.mark.parametrize("c", CFGS)
