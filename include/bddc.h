@@ -310,6 +310,23 @@ int bddc_gather_symv_bulk(int N, int maxG, const int* nG, const int* gpos, const
                           const double* x, const double* win, double* yb, int grid, int* sched,
                           void* stream);
 
+/* Mode B balance operators (solver.py:146-179 on the floating set): the two
+ * padded face-graph Laplacians (face-size and unit weights; identity rows for
+ * non-floating subdomains) into `out` (2 n^2, zero on entry), and after their
+ * batched SPD inverse the N x N operators with zero rows/columns off F. */
+int bddc_dirichlet_laplacian(int N, int n, int nfaces, const int* faces, const int* floating,
+                             double* out, void* stream);
+int bddc_dirichlet_finish(int N, int n, const int* floating, const double* inv, double* out0,
+                          double* out1, void* stream);
+
+/* PCG fusions (solver.py:186-233): the balanced projection's apply step
+ * y -= Phi^T z fused with the dot x . y, and the CG update x += alpha p,
+ * r -= alpha Ap fused with r . r; `op` as for bddc_dot. */
+int bddc_proj_dot(int n_gamma, int maxG, const int* gown, const double* z, double* y, const double* x,
+                  void* ws, double* scal, int op, double* hist, void* stream);
+int bddc_cg_update_dot(long long n, double* x, const double* p, double* r, const double* Ap, void* ws,
+                       double* scal, int op, double* hist, void* stream);
+
 size_t bddc_geom_size(void);
 /* Kernel launches issued so far (bench.py's gpu_launches). */
 unsigned long long bddc_launch_count(void);

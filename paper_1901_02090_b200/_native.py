@@ -134,6 +134,8 @@ _SIGS = {
     "bddc_dot_workspace": [],
     "bddc_dot": [_P, _P, _L, _P, _P, _I, _P, _P],
     "bddc_cg_update": [_L, _P, _P, _P, _P, _P, _P],
+    "bddc_proj_dot": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P],
+    "bddc_cg_update_dot": [_L, _P, _P, _P, _P, _P, _P, _I, _P, _P],
     "bddc_p_update": [_L, _P, _P, _P, _P],
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
     "bddc_set_gemv_wpr": [_I],
@@ -155,6 +157,8 @@ _SIGS = {
     "bddc_face_shift": [_I, _I, _P, _P, _P, _P, _P],
     "bddc_scale_cells": [_GP, _P, _P, _P, _P, _P],
     "bddc_host_register": [_P, C.c_size_t],
+    "bddc_dirichlet_laplacian": [_I, _I, _I, _P, _P, _P, _P],
+    "bddc_dirichlet_finish": [_I, _I, _P, _P, _P, _P, _P],
     "bddc_host_unregister": [_P],
     "bddc_geom_size": [],
     "bddc_launch_count": [],

@@ -631,16 +631,51 @@ __global__ void proj_apply_kernel(int n_gamma, int maxG, const int* __restrict__
 // ------------------------------------------------------------- dot products
 
 // Fused deterministic dot: per-block partials, the last block to finish sums
-// them in index order and applies `op` (see bddc_dot).
-__global__ void dot_kernel(const double* __restrict__ x, const double* __restrict__ y, long long n,
+// them in index order and applies `op` (see bddc_dot).  MODE selects the
+// elementwise pass that produces the reduced terms:
+//   0  x . y  (op 200-299: sum |x|, op 300-399: max |x|, into slot op - 200 / - 300)
+//   1  balanced projection then dot: y[d] -= z[lo(d)] - z[hi(d)] (solver.py:166-179),
+//      acc += x[d] * y[d]  (the projected S p or M r and its dot with p or r)
+//   2  CG update then residual norm: xv += alpha p, r -= alpha Ap (alpha = scal[2]),
+//      acc += r . r   (solver.py:207-213)
+struct DotArgs {
+  const int* gown;
+  int maxG;
+  const double* z;     // MODE 1: the subdomain Laplacian solve
+  double* xv;          // MODE 2: iterate
+  const double* p;     // MODE 2
+  const double* Ap;    // MODE 2
+};
+
+template <int MODE>
+__global__ void dot_kernel(const double* __restrict__ x, double* __restrict__ y, long long n,
                            double* __restrict__ partial, unsigned* __restrict__ counter,
-                           double* __restrict__ scal, int op, double* __restrict__ hist) {
+                           double* __restrict__ scal, int op, double* __restrict__ hist, DotArgs A) {
   __shared__ double red[32];
   __shared__ bool last;
+  const bool amax = MODE == 0 && op >= 300 && op < 400, asum = MODE == 0 && op >= 200 && op < 300;
   double acc = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-    acc += x[e] * y[e];
-  acc = block_sum(acc, red);
+  const double alpha = MODE == 2 ? scal[2] : 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    if (MODE == 1) {
+      const int lo = A.gown[2 * e] / A.maxG, hi = A.gown[2 * e + 1] / A.maxG;
+      const double v = y[e] - (A.z[lo] - A.z[hi]);
+      y[e] = v;
+      acc += x[e] * v;
+    } else if (MODE == 2) {
+      A.xv[e] += alpha * A.p[e];
+      const double v = y[e] - alpha * A.Ap[e];
+      y[e] = v;
+      acc += v * v;
+    } else if (amax) {
+      acc = fmax(acc, fabs(x[e]));
+    } else if (asum) {
+      acc += fabs(x[e]);
+    } else {
+      acc += x[e] * y[e];
+    }
+  }
+  acc = amax ? block_max(acc, red) : block_sum(acc, red);
   if (threadIdx.x == 0) {
     partial[blockIdx.x] = acc;
     __threadfence();
@@ -651,10 +686,15 @@ __global__ void dot_kernel(const double* __restrict__ x, const double* __restric
   if (!last) return;
   __threadfence();
   double s = 0.0;
-  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += ((volatile double*)partial)[b];
-  s = block_sum(s, red);
+  for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+    s = amax ? fmax(s, ((volatile double*)partial)[b]) : s + ((volatile double*)partial)[b];
+  s = amax ? block_max(s, red) : block_sum(s, red);
   if (threadIdx.x == 0) {
     *counter = 0u;
+    if (amax || asum) {
+      scal[op - (amax ? 300 : 200)] = s;
+      return;
+    }
     // scal slots: 0 rz, 1 pAp, 2 alpha, 3 rr, 4 res0, 5 relres, 6 rz_new, 7 beta,
     // 8 bad (non-positive curvature), 9 iterations completed (device counter)
     const int itc = (int)scal[9];
@@ -1095,11 +1135,95 @@ extern "C" int bddc_proj_apply(int n_gamma, int maxG, const int* gown, const dou
 
 extern "C" size_t bddc_dot_workspace(void) { return DOT_BLOCKS * sizeof(double) + 64; }
 
+// Mode-B balance operators (solver.py:146-179 restricted to the floating set F):
+// two face-graph Laplacians over the N subdomains, padded to n x n -- batch 0
+// weighted by face size (Phi_F Phi_F^T), batch 1 unit weights (balanced shift) --
+// with the rows / columns of non-floating subdomains replaced by the identity so
+// the batched SPD inverse applies.  Face weights are integers: the atomic sums are
+// exact (deterministic).  `out` must be zero on entry.
+__global__ void dirichlet_laplacian_kernel(int N, int n, int nfaces, const int* __restrict__ faces,
+                                           const int* __restrict__ floating, double* __restrict__ out) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nfaces) {
+    const int i = faces[4 * f], j = faces[4 * f + 1];
+    const double wts[2] = {(double)faces[4 * f + 3], 1.0};
+    const bool fi = floating[i], fj = floating[j];
+    for (int b = 0; b < 2; ++b) {
+      double* L = out + (size_t)b * n * n;
+      if (fi && fj) {
+        L[(size_t)i * n + j] -= wts[b];
+        L[(size_t)j * n + i] -= wts[b];
+      }
+      if (fi) atomicAdd(&L[(size_t)i * n + i], wts[b]);
+      if (fj) atomicAdd(&L[(size_t)j * n + j], wts[b]);
+    }
+  }
+  // identity rows for the non-floating subdomains and the padding
+  for (int r = f; r < n; r += gridDim.x * blockDim.x)
+    if (r >= N || !floating[r])
+      for (int b = 0; b < 2; ++b) out[(size_t)b * n * n + (size_t)r * n + r] = 1.0;
+}
+
+// out[b] (N x N) = inverse restricted to F x F, zero elsewhere
+__global__ void dirichlet_finish_kernel(int N, int n, const int* __restrict__ floating,
+                                        const double* __restrict__ inv, double* __restrict__ out0,
+                                        double* __restrict__ out1) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)N * N) return;
+  const int r = (int)(e / N), c = (int)(e % N);
+  const bool keep = floating[r] && floating[c];
+  out0[e] = keep ? inv[(size_t)r * n + c] : 0.0;
+  out1[e] = keep ? inv[(size_t)n * n + (size_t)r * n + c] : 0.0;
+}
+
+extern "C" int bddc_dirichlet_laplacian(int N, int n, int nfaces, const int* faces, const int* floating,
+                                        double* out, void* stream) {
+  const int total = imax(nfaces, n);
+  dirichlet_laplacian_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(N, n, nfaces, faces, floating,
+                                                                                   out);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_dirichlet_finish(int N, int n, const int* floating, const double* inv, double* out0,
+                                     double* out1, void* stream) {
+  const long long tot = (long long)N * N;
+  if (tot == 0) return 0;
+  dirichlet_finish_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(N, n, floating, inv,
+                                                                                          out0, out1);
+  LAUNCH_OK();
+  return 0;
+}
+
 extern "C" int bddc_dot(const double* x, const double* y, long long n, void* ws, double* scal, int op, double* hist,
                         void* stream) {
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
-  dot_kernel<<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n, partial, counter, scal, op, hist);
+  dot_kernel<0><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, const_cast<double*>(y), n, partial,
+                                                                     counter, scal, op, hist, DotArgs{});
+  LAUNCH_OK();
+  return 0;
+}
+
+// y -= Phi^T z (projection apply) fused with the dot x . y and its `op`.
+extern "C" int bddc_proj_dot(int n_gamma, int maxG, const int* gown, const double* z, double* y, const double* x,
+                             void* ws, double* scal, int op, double* hist, void* stream) {
+  double* partial = (double*)ws;
+  unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
+  DotArgs A{gown, maxG, z, nullptr, nullptr, nullptr};
+  dot_kernel<1><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n_gamma, partial, counter, scal, op,
+                                                                     hist, A);
+  LAUNCH_OK();
+  return 0;
+}
+
+// xv += alpha p, r -= alpha Ap (alpha = scal[2]) fused with r . r and its `op`.
+extern "C" int bddc_cg_update_dot(long long n, double* xv, const double* p, double* r, const double* Ap, void* ws,
+                                  double* scal, int op, double* hist, void* stream) {
+  double* partial = (double*)ws;
+  unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
+  DotArgs A{nullptr, 1, nullptr, xv, p, Ap};
+  dot_kernel<2><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(r, r, n, partial, counter, scal, op, hist, A);
   LAUNCH_OK();
   return 0;
 }

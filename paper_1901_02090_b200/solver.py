@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import warnings
+from collections.abc import Mapping
 from dataclasses import dataclass
 
 import numpy as np
@@ -316,8 +317,9 @@ class BddcSetup:
             # PairEigenReports for every adaptive setup (solver.py:76-88): the full
             # spectrum with pair_spectra, else the eigenvalues the selection resolved
             # (those above tau and the next one, which sets omega)
-            self.pair_reports = _pair_reports(dec, self.pair_lambda.cpu().numpy(),
-                                              self.pair_selected, complete=self.pair_spectra)
+            # (materialised on first access: the host loop stays out of the setup)
+            self.pair_reports = _LazyPairReports(dec, self.pair_lambda, self.pair_selected,
+                                                 self.pair_spectra)
             self.face_omega = omega.cpu().numpy()
             self.omega_tilde = float(max(self.face_omega.max(), 1.0)) if nf else 1.0
         elif config.constraints == "adaptive":
@@ -445,7 +447,9 @@ class BddcSetup:
         # in flight each): S on every SM; T on t_grid_bulk SMs, the rest left to the
         # concurrent coarse chain
         self.symv_bulk = dec.maxG <= 512   # the bulk kernel stages up to 512 slots
-        self.t_grid_bulk = max(1, self.n_sm - 20)
+        # C3 (scripts/precond_pieces.py): precond 437 us at 148 CTAs, 419 at 120, 398 at
+        # 100, 387 at 84, 400 at 72; T alone 217 / 224 / 245 / 280 / 320 us
+        self.t_grid_bulk = max(1, (self.n_sm * 4) // 7)
         self._sched = torch.zeros(8, dtype=I32, device=dev)   # ticket counters per call site
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
@@ -502,26 +506,21 @@ class BddcSetup:
         reaches a Dirichlet subdomain, hence SPD: one batched device inverse."""
         dec, N, dev, st = self.dec, self.N, self.dev, _stream()
         n = _pad(N, 64)
-        ft = torch.as_tensor(dec.face_table.astype(np.int64), device=dev)
-        i, j = ft[:, 0], ft[:, 1]
-        L = torch.zeros(2, n, n, dtype=F64, device=dev)
-        for b, w in ((0, ft[:, 3].to(F64)), (1, torch.ones(len(ft), dtype=F64, device=dev))):
-            L[b].index_put_((i, j), -w, accumulate=True)
-            L[b].index_put_((j, i), -w, accumulate=True)
-            L[b].index_put_((i, i), w, accumulate=True)
-            L[b].index_put_((j, j), w, accumulate=True)
-        mask = torch.zeros(n, dtype=F64, device=dev)
-        mask[:N] = torch.as_tensor(self.floating.astype(np.float64), device=dev)
-        L *= mask[:, None] * mask[None, :]
-        L[:, torch.arange(n, device=dev), torch.arange(n, device=dev)] += (1.0 - mask)
+        fl = _upload(self.floating.astype(np.int32), I32, dev)
+        L = torch.empty(2 * n * n, dtype=F64, device=dev)
+        nat.call("bddc_fill", 2 * n * n, 0.0, _p(L), st)
+        nat.call("bddc_dirichlet_laplacian", N, n, dec.n_faces, _p(self.d_faces), _p(fl), _p(L), st)
         info = torch.zeros(1, dtype=I32, device=dev)
         ws = torch.empty(nat.load().bddc_spd_inverse_workspace(n, 2, 32) // 8 + 2,
                          dtype=F64, device=dev)
         nat.call("bddc_spd_inverse_batched", _p(L), n, n, n * n, 2, 32, _p(ws), _p(info), st)
         if int(info.item()):
-            raise NumericalFailureError("mode B balance Laplacian not positive definite")
-        L *= mask[:, None] * mask[None, :]
-        return L[0, :N, :N].contiguous().view(-1), L[1, :N, :N].contiguous().view(-1)
+            raise NumericalFailureError("mode B balance Laplacian not positive definite",
+                                        where=int(info.item()) - 1)
+        Lp = torch.empty(N * N, dtype=F64, device=dev)
+        Lu = torch.empty(N * N, dtype=F64, device=dev)
+        nat.call("bddc_dirichlet_finish", N, n, _p(fl), _p(L), _p(Lp), _p(Lu), st)
+        return Lp, Lu
 
     def _multiscale_rows(self, system, Sinv):
         """Face rows of the pair-local unit-transfer solves (adaptive.py:207-262),
@@ -644,11 +643,13 @@ class BddcSetup:
             kt["ev"].append((e0, e1))
         nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb), _p(y), st)
 
-    def _project(self, y):
-        """In-place balanced projection, solver.py:166-179."""
+    def _project(self, y, dot=None):
+        """In-place balanced projection, solver.py:166-179.  dot = (x, op, hist): fuse
+        the following PCG dot x . (P y) into the apply step (one pass, one launch)."""
         st = _stream()
         nat.call("bddc_phi", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                  _p(self.d_gcode), _p(y), _p(self.w_phi), st)
+        z = self.w_z
         if self.d_Lp is not None:
             nat.call("bddc_gemv", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi), _p(self.w_z),
                      st)
@@ -659,15 +660,17 @@ class BddcSetup:
                 nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_wF),
                          _p(self.d_dm_wF), _p(self._phiF), _p(self._zF), _p(self._lap_wsF), st)
                 nat.call("bddc_gamma_flux", self.NF, _p(self.d_fidx), _p(self._zF), _p(self.w_zp), 0, st)
-            nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
-                     _p(self.w_zp), _p(y), st)
-            return
+            z = self.w_zp
         else:
             S3 = self.dec.S3
             nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_w),
                      _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), _p(self._lap_ws), st)
-        nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown),
-                 _p(self.w_z), _p(y), st)
+        if dot is None:
+            nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown), _p(z), _p(y), st)
+        else:
+            x, op, hist = dot
+            nat.call("bddc_proj_dot", self.n_gamma, self.maxG, _p(self.d_gown), _p(z), _p(y), _p(x),
+                     _p(self.w_dot), _p(self.w_scal), op, _p(hist) if hist is not None else None, st)
 
     def _precond(self, r, out):
         """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged."""
@@ -842,6 +845,29 @@ class PairEigenReport:
         return float(max(below[0], 1.0)) if len(below) else 1.0
 
 
+class _LazyPairReports(Mapping):
+    """dict (i, j) -> PairEigenReport, built from the device eigenvalues on first use."""
+
+    def __init__(self, dec, lam_dev, selected, complete):
+        self._args = (dec, lam_dev, selected, complete)
+        self._d = None
+
+    def _get(self):
+        if self._d is None:
+            dec, lam_dev, selected, complete = self._args
+            self._d = _pair_reports(dec, lam_dev.cpu().numpy(), selected, complete=complete)
+        return self._d
+
+    def __getitem__(self, key):
+        return self._get()[key]
+
+    def __iter__(self):
+        return iter(self._get())
+
+    def __len__(self):
+        return self._args[0].n_faces
+
+
 def _pair_reports(dec, lam, selected, complete=True):
     """complete: the whole spectrum (reduced pencil resolved fully, then the zeros of
     I - E); else the leading eigenvalues the selection resolved (selected + 1)."""
@@ -865,7 +891,7 @@ def eigs_report(system, dec, config):
     (i, j) -> PairEigenReport, computed on the GPU."""
     cfg = SolveConfig(tau=config.tau, scaling=config.scaling, tol=config.tol,
                       maxit=config.maxit, constraints="adaptive")
-    return BddcSetup(system, dec, cfg, pair_spectra=True).pair_reports
+    return dict(BddcSetup(system, dec, cfg, pair_spectra=True).pair_reports)
 
 
 def preconditioned_spectrum(setup, max_n=8192):
@@ -1167,13 +1193,16 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         nat.call("bddc_axpby", ng, -1.0, _p(W.Ap), 1.0, _p(W.r), st)
         # subdomain net-flux targets (stiffness scaling only)
         nat.call("bddc_sub_sum", gp, _p(W.dd), _p(setup.w_phi), -1.0, _p(setup.d_Dsub), st)
-        # sum |fs| = sum_c |f_c| D_sub(c) (D > 0); one 2-scalar read
-        # (into preallocated work vectors: temporaries on the solve stream would each
-        # be a fresh device allocation)
-        torch.abs(setup.w_phi, out=setup.w_z)
-        torch.abs(W.fs, out=W.tmpc)
-        tmax, fs_abs, nfs2, dd2 = torch.stack([setup.w_z.max(), W.tmpc.sum(),
-                                              setup.w_norms[_N_FS], setup.w_norms[_N_DD]]).tolist()
+        # max |targets| and sum |fs| (abs-reduction modes of the dot kernel), read with
+        # the deferred norms in one host sync
+        _dot(setup, setup.w_phi, None, N, 300 + 12)
+        _dot(setup, W.fs, None, G.n_cells, 200 + 13)
+        hs = setup._host_scal
+        hs.copy_(setup.w_scal, non_blocking=True)
+        hn = _norms_to_host(setup)
+        torch.cuda.current_stream().synchronize()
+        tmax, fs_abs = float(hs[12]), float(hs[13])
+        nfs2, dd2 = float(hn[_N_FS]), float(hn[_N_DD])
         # relative to |fs| (solver.py:331-333); absolute when there is no source (mode B)
         defect_norm = math.sqrt(dd2) / (math.sqrt(nfs2) if nfs2 > 0 else 1.0)
         if tmax > 1e-13 * max(fs_abs, 1.0):
@@ -1363,22 +1392,22 @@ class _PCGBufs:
 
 
 def _pcg_core(setup, W, B):
-    """Ap = P S p; alpha; x += alpha p; r -= alpha Ap; relres (solver.py:205-216)."""
+    """Ap = P S p; alpha = rz / p.Ap; x += alpha p; r -= alpha Ap; relres
+    (solver.py:205-216): the projection's apply carries the p.Ap dot, the update
+    carries r.r."""
     ng = setup.n_gamma
     setup._schur(W.p, W.Ap)
-    setup._project(W.Ap)
-    _dot(setup, W.p, W.Ap, ng, 1, B.alphas)
-    nat.call("bddc_cg_update", ng, _p(setup.w_scal), _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _stream())
-    _dot(setup, W.r, W.r, ng, 2, B.res)
+    setup._project(W.Ap, dot=(W.p, 1, B.alphas))
+    nat.call("bddc_cg_update_dot", ng, _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _p(setup.w_dot),
+             _p(setup.w_scal), 2, _p(B.res), _stream())
 
 
 def _pcg_first(setup, W, B):
     """z = P M r; p = z; rz = r.z; first iteration (solver.py:198-216)."""
     ng = setup.n_gamma
     setup._precond(W.r, W.zv)
-    setup._project(W.zv)
+    setup._project(W.zv, dot=(W.r, 0, None))
     nat.call("bddc_axpby", ng, 1.0, _p(W.zv), 0.0, _p(W.p), _stream())
-    _dot(setup, W.r, W.zv, ng, 0)
     _pcg_core(setup, W, B)
 
 
@@ -1386,8 +1415,7 @@ def _pcg_body(setup, W, B):
     """z = P M r; beta; p = z + beta p; next iteration (solver.py:222-227, 205-216)."""
     ng = setup.n_gamma
     setup._precond(W.r, W.zv)
-    setup._project(W.zv)
-    _dot(setup, W.r, W.zv, ng, 3, B.betas)
+    setup._project(W.zv, dot=(W.r, 3, B.betas))
     nat.call("bddc_p_update", ng, _p(setup.w_scal), _p(W.zv), _p(W.p), _stream())
     _pcg_core(setup, W, B)
 

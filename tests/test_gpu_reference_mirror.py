@@ -205,13 +205,19 @@ def test_subs_and_coarse_views(name):
     mesh = O.Mesh(d["counts"], d["sizes"])
     cfg = O.Config(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
     ost = O.Setup(mesh, d["k"], O.well_rhs(mesh, 0, mesh.n_cells - 1), d["splits"], cfg)
+    # adaptive rows are defined up to sign / rotation inside a degenerate eigenspace,
+    # so the coarse bases of two implementations differ by a face-block transform on
+    # the adaptive dofs: a load on the initial-row dofs and the pressures gives the
+    # same initial-row and pressure components
     rng = np.random.default_rng(4)
-    rf = rng.standard_normal(st.cset.n_flux_coarse)
+    nf = dec.n_faces
+    rf = np.zeros(st.cset.n_flux_coarse)
+    rf[:nf] = rng.standard_normal(nf)
     rq = rng.standard_normal(dec.n_subdomains)
     rq -= rq.mean()
     xf, xp = st.coarse.solve(rf, rq)
     of, op = ost.coarse.solve(rf, rq)
-    assert rel(xf, of) <= 1e-10
+    assert rel(xf[:nf], of[:nf]) <= 1e-10
     assert rel(xp[1:], op[1:]) <= 1e-10
 
 
