@@ -327,6 +327,12 @@ int bddc_proj_dot(int n_gamma, int maxG, const int* gown, const double* z, doubl
 int bddc_cg_update_dot(long long n, double* x, const double* p, double* r, const double* Ap, void* ws,
                        double* scal, int op, double* hist, void* stream);
 
+/* preconditioned_spectrum (oracle.py:114-141) pieces: w -= Q^T c (Q: k rows of
+ * length n), and every eigenvalue of a symmetric tridiagonal (bisection on
+ * Sturm counts, ascending; work: m doubles). */
+int bddc_gemv_t_sub(int k, int n, const double* Q, const double* c, double* w, void* stream);
+int bddc_tridiag_eigvals(int m, const double* d, const double* e, double* work, double* out, void* stream);
+
 size_t bddc_geom_size(void);
 /* Kernel launches issued so far (bench.py's gpu_launches). */
 unsigned long long bddc_launch_count(void);

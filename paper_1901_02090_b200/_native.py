@@ -145,6 +145,8 @@ _SIGS = {
     "bddc_set_prolong_direct": [_I],
     "bddc_lap_dense": [_I, _I, _I, _P, _P, _P, _P, _P],
     "bddc_lanczos": [_I, _P, _P, _P, _P, _P],
+    "bddc_gemv_t_sub": [_I, _I, _P, _P, _P, _P],
+    "bddc_tridiag_eigvals": [_I, _P, _P, _P, _P, _P],
     "bddc_axpby": [_L, _D, _P, _D, _P, _P],
     "bddc_flux_A": [_GP, _P, _P, _D, _D, _P, _P],
     "bddc_cell_div": [_GP, _P, _P, _D, _D, _P, _P, _P, _P],

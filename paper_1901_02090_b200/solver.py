@@ -894,40 +894,111 @@ def eigs_report(system, dec, config):
     return dict(BddcSetup(system, dec, cfg, pair_spectra=True).pair_reports)
 
 
-def preconditioned_spectrum(setup, max_n=8192):
-    """Eigenvalues of the preconditioned interface operator on the balanced
-    subspace (oracle.py:114-141), ascending: S and M materialised column by
-    column with the GPU applies, restricted to null(Phi), and the similar
-    symmetric form Mb^1/2 Sb Mb^1/2 solved on the device (diagnostic, small
-    cases: n_Gamma <= max_n)."""
+def preconditioned_spectrum(setup, max_n=8192, seed=0, _debug=None):
+    """Eigenvalues of the preconditioned interface operator on the balanced subspace
+    (oracle.py:114-141), ascending, on the device with the library's kernels.
+
+    M S is self-adjoint in the S inner product, so Lanczos in that inner product on
+    range(P) (P the balanced projection, solver.py:166-179) with full
+    reorthogonalisation (twice) run to the subspace dimension yields a tridiagonal
+    T whose eigenvalues are those of the reference's Mb Sb (every (P S P) / (P M P)
+    apply is the device operator; a breakdown restarts from a fresh random vector
+    orthogonal to the basis, so multiple eigenvalues are kept).  T's eigenvalues:
+    bisection on Sturm counts (bddc_tridiag_eigvals).  Diagnostic for
+    n_Gamma <= max_n (the basis Q and S Q are stored: 2 n^2 doubles)."""
     n = setup.n_gamma
     if n > max_n:
         raise InvalidArgumentError(f"preconditioned_spectrum: n_Gamma = {n} > {max_n}")
     dev = setup.dev
-    S = torch.empty(n, n, dtype=F64, device=dev)
-    M = torch.empty(n, n, dtype=F64, device=dev)
-    e = torch.zeros(n, dtype=F64, device=dev)
+    # dimension of the balanced subspace: one net-flux constraint per floating
+    # subdomain, minus one in mode A (the constraints sum to zero)
+    nb = n - (setup.N - 1 if not setup.mode_b else int(setup.floating.sum()))
+    Q = torch.empty(max(nb, 1), n, dtype=F64, device=dev)
+    SQ = torch.empty(max(nb, 1), n, dtype=F64, device=dev)
+    w = torch.empty(n, dtype=F64, device=dev)
+    Sw = torch.empty(n, dtype=F64, device=dev)
+    c = torch.empty(max(nb, 1), dtype=F64, device=dev)
+    tmp = torch.empty(n, dtype=F64, device=dev)
+    host = setup._host_scal
+    alphas, betas = [], []
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+
+    def dot(x, y):
+        _dot(setup, x, y, n, 100 + 14)
+        host.copy_(setup.w_scal, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(host[14])
+
+    def s_apply(x, out):          # out = P S x
+        setup._schur(x, out)
+        setup._project(out)
+
+    def m_apply(x, out):          # out = P M x
+        setup._precond(x, out)
+        setup._project(out)
+
+    def reorth(k, x):             # x -= Q^T (SQ x) over the first k basis vectors, twice
+        for _ in range(2):
+            nat.call("bddc_gemv", k, n, n, _p(SQ), _p(x), _p(c), _stream())
+            nat.call("bddc_gemv_t_sub", k, n, _p(Q), _p(c), _p(x), _stream())
+
+    def fresh(k):
+        """A random unit vector of range(P), S-orthogonal to the first k basis vectors."""
+        for _ in range(5):
+            w.copy_(torch.randn(n, dtype=F64, generator=gen))
+            setup._project(w)
+            if k:
+                reorth(k, w)
+                setup._project(w)
+            s_apply(w, Sw)
+            nrm2 = dot(w, Sw)
+            if nrm2 > 0:
+                r = 1.0 / math.sqrt(nrm2)
+                nat.call("bddc_axpby", n, r, _p(w), 0.0, _p(Q[k]), _stream())
+                nat.call("bddc_axpby", n, r, _p(Sw), 0.0, _p(SQ[k]), _stream())
+                return True
+        return False
+
     with torch.cuda.stream(setup.stream):
-        for c in range(n):
-            e.zero_()
-            e[c] = 1.0
-            setup._schur(e, S[c])
-            setup._precond(e, M[c])
+        setup.stream.wait_stream(torch.cuda.default_stream())
+        if nb > 0 and fresh(0):
+            scale = 0.0
+            for k in range(nb):
+                m_apply(SQ[k], w)                      # w = (P M P)(P S P) q_k
+                a = dot(w, SQ[k])                      # <w, q_k>_S
+                alphas.append(a)
+                nat.call("bddc_axpby", n, -a, _p(Q[k]), 1.0, _p(w), _stream())
+                if k:
+                    nat.call("bddc_axpby", n, -betas[-1], _p(Q[k - 1]), 1.0, _p(w), _stream())
+                reorth(k + 1, w)
+                # re-project: the S'-norm does not see null(P) components, so division
+                # by a small beta would amplify them step after step
+                setup._project(w)
+                if k == nb - 1:
+                    break
+                s_apply(w, Sw)
+                b2 = dot(w, Sw)
+                scale = max(scale, abs(a))
+                if b2 > (1e-10 * scale) ** 2:
+                    bk = math.sqrt(b2)
+                    betas.append(bk)
+                    nat.call("bddc_axpby", n, 1.0 / bk, _p(w), 0.0, _p(Q[k + 1]), _stream())
+                    nat.call("bddc_axpby", n, 1.0 / bk, _p(Sw), 0.0, _p(SQ[k + 1]), _stream())
+                else:
+                    # invariant subspace exhausted: restart (T splits into blocks)
+                    betas.append(0.0)
+                    if not fresh(k + 1):
+                        raise NumericalFailureError("preconditioned_spectrum: Lanczos restart failed")
+        m = len(alphas)
+        d = torch.tensor(alphas, dtype=F64).to(dev)
+        e = torch.tensor(betas[:max(m - 1, 0)] + [0.0], dtype=F64).to(dev)
+        lam = torch.empty(max(m, 1), dtype=F64, device=dev)
+        nat.call("bddc_tridiag_eigvals", m, _p(d), _p(e), _p(tmp), _p(lam), _stream())
+        out = lam[:m].cpu().numpy()
     torch.cuda.current_stream().wait_stream(setup.stream)
-    S, M = S.T, M.T   # columns are the applies
-    Phi = torch.as_tensor(setup.net_flux_matrix().toarray(), dtype=F64, device=dev)
-    Q, R = torch.linalg.qr(Phi.T, mode="complete")
-    d = torch.abs(torch.diagonal(R))
-    rank = int((d > 1e-12 * torch.clamp(d.max(), min=1e-300)).sum())
-    Z = Q[:, rank:]
-    Sb = Z.T @ S @ Z
-    Mb = Z.T @ M @ Z
-    Sb = 0.5 * (Sb + Sb.T)
-    Mb = 0.5 * (Mb + Mb.T)
-    w, V = torch.linalg.eigh(Mb)
-    W = (V * torch.sqrt(torch.clamp(w, min=0.0))) @ V.T
-    lam = torch.linalg.eigvalsh(W @ Sb @ W)
-    return torch.sort(lam).values.cpu().numpy()
+    if _debug is not None:
+        _debug.update(alphas=alphas, betas=betas, Q=Q.cpu().numpy(), SQ=SQ.cpu().numpy())
+    return out
 
 
 def write_eigs_csv(path, reports):

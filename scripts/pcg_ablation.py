@@ -32,13 +32,15 @@ def chain():
 
 
 def tgemv():
-    nat.call("bddc_gather_symv", N, st.maxG, _p(st.d_nG), _p(st.d_gpos), _p(st.d_Tp), _p(W.r), _p(st.d_delta),
-             _p(st.w_yb), st.t_grid, _stream())
+    st._symv(st.d_Tp, W.r, st.d_delta, st.w_yb, st.t_grid_bulk, 1, _stream())
 
 
 def tgemv_full():
-    nat.call("bddc_gather_symv", N, st.maxG, _p(st.d_nG), _p(st.d_gpos), _p(st.d_Tp), _p(W.r), _p(st.d_delta),
-             _p(st.w_yb), 0, _stream())
+    st._symv(st.d_Tp, W.r, st.d_delta, st.w_yb, 0, 1, _stream())
+
+
+def sgemv():
+    st._symv(st.d_Sp, W.p, None, st.w_yb, 0, 0, _stream())
 
 
 def prolong():
@@ -50,76 +52,30 @@ def scatter():
     nat.call("bddc_scatter", ng, _p(st.d_gown), _p(st.w_yb2), _p(W.zv), _stream())
 
 
-def phi():
-    nat.call("bddc_phi", N, st.maxG, _p(st.d_nG), _p(st.d_gpos), _p(st.d_gcode), _p(W.zv), _p(st.w_phi), _stream())
-
-
-def gemv():
-    nat.call("bddc_gemv", N, N, N, _p(st.d_Lp), _p(st.w_phi), _p(st.w_z), _stream())
-
-
-def proj_apply():
-    nat.call("bddc_proj_apply", ng, st.maxG, _p(st.d_gown), _p(st.w_z), _p(W.zv), _stream())
-
-
-def dots_updates():
-    S._dot(st, W.p, W.Ap, ng, 1, Bf.alphas)
-    nat.call("bddc_cg_update", ng, _p(st.w_scal), _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _stream())
-    S._dot(st, W.r, W.r, ng, 2, Bf.res)
-    S._dot(st, W.r, W.zv, ng, 3, Bf.betas)
-    nat.call("bddc_p_update", ng, _p(st.w_scal), _p(W.zv), _p(W.p), _stream())
-
-
-def one_dot():
-    S._dot(st, W.r, W.r, ng, 100 + 12)
+def restrict():
+    nat.call("bddc_gather_gemv_t", N, st.maxG, st.maxC, _p(st.d_nG), _p(st.d_nC), _p(st.d_gpos), _p(st.d_Psi),
+             _p(W.r), _p(st.d_delta), _p(st.w_v), _stream())
 
 
 pieces = {
     "body": lambda: S._pcg_body(st, W, Bf),
     "schur(S gemv+scatter)": lambda: st._schur(W.p, W.Ap),
+    "S gemv": sgemv,
     "project": lambda: st._project(W.Ap),
+    "project+dot": lambda: st._project(W.Ap, dot=(W.p, 100 + 15, None)),
     "precond": lambda: st._precond(W.r, W.zv),
-    "T gemv (t_grid)": tgemv,
-    "T gemv (grid N)": tgemv_full,
+    "T gemv (t_grid_bulk)": tgemv,
+    "T gemv (all SMs)": tgemv_full,
     "coarse chain": chain,
+    "restriction": restrict,
     "nd.solve": st._coarse_solve,
     "prolong": prolong,
     "scatter": scatter,
-    "phi": phi,
-    "gemv Lp": gemv,
-    "proj_apply": proj_apply,
-    "dots+updates": dots_updates,
-    "one dot": one_dot,
+    "cg_update_dot": lambda: nat.call("bddc_cg_update_dot", ng, _p(W.x), _p(W.p), _p(W.r), _p(W.Ap),
+                                      _p(st.w_dot), _p(st.w_scal), 100 + 15, None, _stream()),
+    "p_update": lambda: nat.call("bddc_p_update", ng, _p(st.w_scal), _p(W.zv), _p(W.p), _stream()),
 }
-def with_tgrid(tg):
-    def f():
-        old = st.t_grid
-        st.t_grid = tg
-        st._precond(W.r, W.zv)
-        st.t_grid = old
-    return f
-
-
-def prolong_staged():
-    nat.load().bddc_set_prolong_direct(0)
-    prolong()
-    nat.load().bddc_set_prolong_direct(1)
-
-
-pieces["prolong staged"] = prolong_staged
 only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
-def body_tgrid(tg):
-    def f():
-        old = st.t_grid
-        st.t_grid = tg
-        S._pcg_body(st, W, Bf)
-        st.t_grid = old
-    return f
-
-
-for tg in (0, 148, 296, 444, 592):
-    pieces[f"precond t_grid={tg}"] = with_tgrid(tg)
-    pieces[f"body t_grid={tg}"] = body_tgrid(tg)
 if only:
     pieces = {k2: v for k2, v in pieces.items() if any(o in k2 for o in only)}
 K = 34
