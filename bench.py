@@ -37,6 +37,8 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--tau", type=float, default=None,
+                    help="override the config's tau (config 2 sweep: inf, 100, 10, 2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mode-b", action="store_true",
                     help="skip the extra BASELINE-BC (pressure drop) measurement")
@@ -100,16 +102,22 @@ class Clocks:
                 "samples": len(self.rows)}
 
 
+_TAU = None   # --tau: BASELINE config 2's sweep {inf, 100, 10, 2}
+
+
 def _problem(cfg_id):
     import paper_1901_02090_b200 as B
     from paper_1901_02090_b200 import fields
-    c = fields.CONFIGS[cfg_id]
+    c = dict(fields.CONFIGS[cfg_id])
+    if _TAU is not None:
+        # tau = inf on an adaptive config: face averages only, the pair spectra still
+        # give omega~ (solver.py:85-88)
+        c["tau"] = _TAU
     k = fields.config_field(cfg_id)
     g = B.build_grid(c["dim"], c["counts"], c["sizes"])
     dec = B.regular_partition(g, c["splits"])
     system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
-    cfg = B.SolveConfig(tau=c["tau"], scaling=c["scaling"],
-                        constraints="adaptive" if math.isfinite(c["tau"]) else "initial",
+    cfg = B.SolveConfig(tau=c["tau"], scaling=c["scaling"], constraints=c["constraints"],
                         tol=c["tol"], maxit=5000)
     return c, k, g, dec, system, cfg
 
@@ -245,11 +253,55 @@ def reference_sample(cfg_id, c, k, steps, warmup):
     return vals, walls, detail, sample
 
 
+def reference_measured(c, k, steps, warmup):
+    """Small configs (C0-C2): the oracle port's complete solve with a prebuilt setup,
+    timed end to end on the host (nothing extrapolated); setup timed once."""
+    from oracle import bddc_oracle as O
+    mesh = O.Mesh(c["counts"], c["sizes"])
+    ocfg = O.Config(tau=c["tau"], scaling=c["scaling"], constraints=c["constraints"], tol=c["tol"],
+                    maxit=5000)
+    f = O.well_rhs(mesh, 0, mesh.n_cells - 1)
+    t0 = time.perf_counter()
+    st = O.Setup(mesh, k, f, c["splits"], ocfg)
+    setup_s = time.perf_counter() - t0
+    vals, walls, it = [], [], 0
+    for s_ in range(warmup + steps):
+        t0 = time.perf_counter()
+        rep = O.solve(st)
+        w = time.perf_counter() - t0
+        if s_ >= warmup:
+            vals.append(rep.it / w)
+            walls.append(w)
+        it = rep.it
+    sample = (f"measured: oracle port (SuperLU local KKTs, dense pair pencils, dense coarse LU, "
+              f"PCG + Lanczos, pressure recovery), complete solve with a prebuilt setup, "
+              f"{steps} timed solves; setup {setup_s:.2f} s; it={it}")
+    return vals, walls, {"setup_s": setup_s, "it": it, "n_c": st.n_c}, sample
+
+
 def run_reference(args):
+    global _TAU
+    _TAU = args.tau
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     c, k, g, dec, system, cfg = _problem(args.config)
+    if c["dim"] == 2:
+        vals, walls, detail, sample = reference_measured(c, k, args.steps, args.warmup)
+        v = float(np.median(vals))
+        line = {
+            "impl": "reference", "metric": "bddc_pcg_iterations_per_s", "value": v, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * float(np.mean(walls)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _workload(c, args.config),
+            "cpu_baseline": {"value": v, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "detail": detail,
+        }
+        print(json.dumps(line))
+        return
     vals, walls, detail, sample = reference_sample(args.config, c, k, args.steps, args.warmup)
     v = float(np.median(vals))
     cores = os.cpu_count()
@@ -452,7 +504,9 @@ class Replicas:
 
 
 def main():
+    global _TAU
     args = _args()
+    _TAU = args.tau
     if args.impl == "reference":
         run_reference(args)
         return
@@ -577,6 +631,12 @@ def main():
     torch.cuda.synchronize()
     e2e_s = allmax(a0.elapsed_time(a1) / 1000.0)
     e2e_val = allsum(float(sum(e2e_its))) / e2e_s
+    # every timed solve converged to rtol (a stalled run would inflate it/s), and the
+    # last one solves the saddle system: momentum A u + B^T p = 0, mass B u = f
+    if not (conv and rpt.converged):
+        raise RuntimeError("bench: PCG did not converge")
+    mom = float(np.linalg.norm(system.A @ rpt.u + system.B.T @ rpt.p) / np.linalg.norm(system.A @ rpt.u))
+    mass = float(np.linalg.norm(system.B @ rpt.u - system.f) / np.linalg.norm(system.f))
 
     line = {
         "metric": "bddc_pcg_iterations_per_s", "value": value, "unit": "it/s",
@@ -589,6 +649,7 @@ def main():
         "setup_runs_s": setup_runs, "setup_fresh_partition_s": setup_fresh_s, "partition_host_s": t_part,
         "setup_phases_ms": tm, "pcg_iterations": int(its[-1]), "kappa": float(kappa),
         "n_c": int(setup.n_c), "omega_tilde": setup.omega_tilde,
+        "converged": True, "momentum_residual_rel": mom, "mass_residual_rel": mass,
         "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "roofline": {"bound": "hbm", "kernel": "gather_symv_kernel (interface Schur S_i x_i, packed symmetric tiles)",
@@ -604,7 +665,11 @@ def main():
     }
     line["factorisation_roofline"] = _factorisation_roofline(setup, dec, lib, nat, dev)
     line["stencil_roofline"] = _stencil_roofline(setup, g, nat, peak, dev)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and c["dim"] == 2:
+        vals, walls, detail, sample = reference_measured(c, k, 1, 0)
+        line["cpu_baseline"] = {"value": vals[0], "unit": "it/s", "cores": os.cpu_count(),
+                                "kind": "port", "sample": sample}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         vals, walls, detail, sample = reference_sample(args.config, c, k, 1, 0)
         line["cpu_baseline"] = {"value": vals[0], "unit": "it/s", "cores": os.cpu_count(),
                                 "kind": "port", "extrapolated": True, "sample": sample,

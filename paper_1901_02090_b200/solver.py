@@ -451,6 +451,7 @@ class BddcSetup:
         # 100, 387 at 84, 400 at 72; T alone 217 / 224 / 245 / 280 / 320 us
         self.t_grid_bulk = max(1, (self.n_sm * 4) // 7)
         self._sched = torch.zeros(8, dtype=I32, device=dev)   # ticket counters per call site
+        self.restrict_first = False
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._solves = 0   # public solves run on this setup
@@ -679,16 +680,23 @@ class BddcSetup:
         if self.nfc:
             # the coarse chain (restriction, latency-bound ND solve) runs on a side
             # stream, concurrently with the bandwidth-bound T_i GEMV (a fork/join
-            # inside the captured PCG graph); they meet at the prolongation
+            # inside the captured PCG graph); they meet at the prolongation.
+            # restrict_first: the Psi^T restriction runs alone on every SM before the
+            # fork, so only the ND solve shares the machine with the T_i GEMV
+            if self.restrict_first:
+                nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                         _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
+                         _p(self.d_delta), _p(self.w_v), st)
             side = self.side_stream
             fork = torch.cuda.Event()
             fork.record(main)
             side.wait_event(fork)
             with torch.cuda.stream(side):
                 ss = _stream()
-                nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
-                         _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
-                         _p(self.d_delta), _p(self.w_v), ss)
+                if not self.restrict_first:
+                    nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
+                             _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
+                             _p(self.d_delta), _p(self.w_v), ss)
                 nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
                          _p(self.w_rc), ss)
                 nat.call("bddc_fill", self.N, 0.0, _p(self.w_rc[self.nfc:]), ss)
