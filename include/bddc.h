@@ -132,6 +132,13 @@ typedef struct bddc_local_solve_args {
   int u_mode;             /* 0: set, 1: add */
   double* rg_broken;      /* if non-NULL: A_IG^T u_I + B_G^T p per slot (N x maxG) */
   double* p_out;          /* if non-NULL: local pressures per cell */
+  /* optional second right-hand side sharing f_flux and x_gamma but with the cell
+   * load g_cell2 (Step 2's harmonic extension and trace solve, solver.py:326-335):
+   * both solves read the packed pressure Schur inverse once; its interior fluxes
+   * go to u_out2 (set) */
+  const double* g_cell2;
+  double g_scale2;
+  double* u_out2;
 } bddc_local_solve_args;
 int bddc_local_solve(const bddc_geom* g, const double* coef, const int* gcode, const int* gpos,
                      const int* fslot, const double* Q, const double* Dsub,

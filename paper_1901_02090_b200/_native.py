@@ -70,6 +70,7 @@ class LocalSolveArgs(C.Structure):
         ("x_gamma", C.c_void_p), ("x_scale", C.c_double),
         ("u_out", C.c_void_p), ("u_mode", C.c_int),
         ("rg_broken", C.c_void_p), ("p_out", C.c_void_p),
+        ("g_cell2", C.c_void_p), ("g_scale2", C.c_double), ("u_out2", C.c_void_p),
     ]
 
 

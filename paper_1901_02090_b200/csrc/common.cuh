@@ -191,6 +191,62 @@ __device__ __forceinline__ int tile_index(int bi, int bj, int nt) { return bi * 
 // contribution directly and the row contribution by a transpose-reduction, and
 // accumulates into its own slice of yw (nwarps x ntl*32 doubles of shared
 // memory); the slices are summed in warp order: deterministic.
+// Two right-hand sides through one read of the packed tiles: y = P x, y2 = P x2
+// (yw: 2 x warps x ntl*32 partials).
+__device__ __forceinline__ void cta_symv_packed2(const double* __restrict__ Pk, int nt, int ntl, const double* x,
+                                                 const double* x2, double* y, double* y2, double* yw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int len = ntl * 32;
+  for (int e = threadIdx.x; e < 2 * nw * len; e += blockDim.x) yw[e] = 0.0;
+  __syncthreads();
+  const int nlive = ntl * (ntl + 1) / 2;
+  for (int u = warp; u < nlive; u += nw) {
+    int bi = 0, rem = u;
+    while (rem >= ntl - bi) {
+      rem -= ntl - bi;
+      ++bi;
+    }
+    const int bj = bi + rem;
+    const double* T = Pk + (size_t)tile_index(bi, bj, nt) * 1024;
+    // the second pass re-reads the tile this warp just streamed (L1 / L2 hit): one
+    // DRAM read for both right-hand sides at the single-rhs register footprint
+#pragma unroll 1
+    for (int s = 0; s < 2; ++s) {
+      const double* xs = s ? x2 : x;
+      double* my = yw + ((size_t)s * nw + warp) * len;
+      const double xl = xs[bj * 32 + lane];
+      double v[32];
+      double col = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const double a = __ldg(T + r * 32 + lane);
+        v[r] = a * xl;
+        col += a * xs[bi * 32 + r];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = lane & off;
+#pragma unroll
+        for (int k = 0; k < off; ++k) {
+          const double send = up ? v[k] : v[k + off];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, off);
+          v[k] = (up ? v[k + off] : v[k]) + recv;
+        }
+      }
+      my[bi * 32 + lane] += v[0];
+      if (bi != bj) my[bj * 32 + lane] += col;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * len; e += blockDim.x) {
+    const int s = e >= len, ee = e - s * len;
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += yw[((size_t)s * nw + w) * len + ee];
+    (s ? y2 : y)[ee] = acc;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void cta_symv_packed(const double* __restrict__ Pk, int nt, int ntl, const double* x,
                                                 double* y, double* yw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;

@@ -427,7 +427,8 @@ __global__ void symmetrize_kernel(double* __restrict__ S, int n, long long strid
 // B_loc = D B_u (grid.py:250):  p' = Q (B_u A^{-1} f - g/D),
 // u_I = A^{-1}(f - B_u^T p'), p = p'/D  where f = f_flux - A_IG x and
 // g = g_cell - D B_uG x (substructure.py:72-116).
-__global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ gcode,
+template <bool TWO>
+__global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ gcode,
                                    const int* __restrict__ gpos, const int* __restrict__ fslot,
                                    const double* __restrict__ Q, const double* __restrict__ Dsub,
                                    bddc_local_solve_args A) {
@@ -440,7 +441,10 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
   double* rhs = xg + mg;      // mp
   double* pp = rhs + mp;      // mp
   double* tI = pp + mp;       // 3 mp + 2 maxF (interior faces, per axis blocks)
-  double* yw = tI + 3 * mp + 2 * G.maxF;   // (blockDim/32) x mp symv partials
+  double* yw = tI + 3 * mp + 2 * G.maxF;   // (blockDim/32) x mp symv partials (x2 with two rhs)
+  constexpr bool two = TWO;
+  double* rhs2 = yw + (two ? 16 : 8) * mp;   // second right-hand side (two only)
+  double* pp2 = rhs2 + mp;
   int off[3], lo3[3] = {0, 0, 0}, hi3[3] = {0, 0, 0};
   {
     int o = 0;
@@ -518,13 +522,30 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
     }
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < mp; c += blockDim.x) rhs[c] += (radd[c] + radd[mp + c]) + radd[2 * mp + c];
+  for (int c = threadIdx.x; c < mp; c += blockDim.x) {
+    const double v = (radd[c] + radd[mp + c]) + radd[2 * mp + c];
+    if (two) {
+      double g2 = 0.0;
+      if (c < np && A.g_cell2) {
+        int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
+        g2 = A.g_scale2 * A.g_cell2[cell_id(G, b.o[0] + lx, b.o[1] + ly, b.o[2] + lz)] / Di;
+      }
+      // the second system differs from the first only in its cell load
+      rhs2[c] = rhs[c] + v - g2;
+    }
+    rhs[c] += v;
+  }
   __syncthreads();
   // p' = Q rhs, Q tile-packed symmetric (half the bytes of full storage)
   {
     const int nt = mp / 32, ntl = (np + 31) / 32;
-    cta_symv_packed(Q + (size_t)i * (nt * (nt + 1) / 2) * 1024, nt, ntl, rhs, pp, yw);
-    for (int r = ntl * 32 + threadIdx.x; r < mp; r += blockDim.x) pp[r] = 0.0;
+    const double* Qi = Q + (size_t)i * (nt * (nt + 1) / 2) * 1024;
+    if (two) cta_symv_packed2(Qi, nt, ntl, rhs, rhs2, pp, pp2, yw);
+    else cta_symv_packed(Qi, nt, ntl, rhs, pp, yw);
+    for (int r = ntl * 32 + threadIdx.x; r < mp; r += blockDim.x) {
+      pp[r] = 0.0;
+      if (two) pp2[r] = 0.0;
+    }
     __syncthreads();
   }
   // u_I = t - A^{-1} B_u^T p' (lines of all axes at once: disjoint outputs)
@@ -538,12 +559,21 @@ __global__ void local_solve_kernel(bddc_geom G, const double* __restrict__ coef,
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
       line_factor(c, L, lo, hi, cp, piv);
       const int base = line_base(b, a, line);
+      double* t = tI + off[a] + line * m;
+      if (two) {   // second system first: t is still the shared A^{-1} f
+        for (int j = 0; j < m; ++j) {
+          const int p = j + 1 - lo;
+          r[j] = (p <= L - 1 ? pp2[base + p * st] : 0.0) - (p >= 1 ? pp2[base + (p - 1) * st] : 0.0);
+        }
+        line_solve(c, L, lo, hi, cp, piv, r);
+        for (int j = 0; j < m; ++j)
+          A.u_out2[(size_t)line_face_dof(G, b, a, line, j, lo)] = t[j] - r[j];
+      }
       for (int j = 0; j < m; ++j) {
         const int p = j + 1 - lo;  // (B_u^T p')_j = p'(cell above) - p'(cell below)
         r[j] = (p <= L - 1 ? pp[base + p * st] : 0.0) - (p >= 1 ? pp[base + (p - 1) * st] : 0.0);
       }
       line_solve(c, L, lo, hi, cp, piv, r);
-      double* t = tI + off[a] + line * m;
       for (int j = 0; j < m; ++j) {
         double u = t[j] - r[j];
         t[j] = u;
@@ -639,11 +669,15 @@ extern "C" int bddc_local_solve(const bddc_geom* g, const double* coef, const in
                                 const int* fslot, const double* Q, const double* Dsub,
                                 const bddc_local_solve_args* a, void* stream) {
   if (g->maxP % 32) return bddc_set_error(BDDC_ERR_ARG, "local_solve: maxP must be a multiple of 32");
-  size_t shm = (size_t)(g->maxG + 5 * g->maxP + 2 * g->maxF + 8 * g->maxP) * sizeof(double);
+  const bool two = a->u_out2 != nullptr;
+  size_t shm = (size_t)(g->maxG + 5 * g->maxP + 2 * g->maxF + (two ? 18 : 8) * g->maxP) * sizeof(double);
   if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "local_solve: subdomain too large for shared memory");
-  if (shm > 48 * 1024)
-    CUDA_OK(cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  local_solve_kernel<<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
+  if (shm > 48 * 1024) {
+    CUDA_OK(cudaFuncSetAttribute(local_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    CUDA_OK(cudaFuncSetAttribute(local_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  }
+  if (two) local_solve_kernel<true><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
+  else local_solve_kernel<false><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
   LAUNCH_OK();
   return 0;
 }

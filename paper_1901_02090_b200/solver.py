@@ -452,6 +452,11 @@ class BddcSetup:
         self.t_grid_bulk = max(1, (self.n_sm * 4) // 7)
         self._sched = torch.zeros(8, dtype=I32, device=dev)   # ticket counters per call site
         self.restrict_first = False
+        # Step 2's two local solves in one two-rhs pass over Q where the two-rhs kernel's
+        # shared memory still allows several CTAs per SM (C4: 36.98 -> 36.79 ms per
+        # solve); at C3 (maxP 512, ~96 KB per CTA) the two passes are faster
+        # (26.86 vs 27.21 ms, scripts/step2_check.py)
+        self.step2_fused = (dec.maxG + 23 * dec.maxP) * 8 <= 64 * 1024
         self._scaling_checked = False
         self.force_eager = False   # host-driven PCG loop (profiling); default is the graph
         self._solves = 0   # public solves run on this setup
@@ -1211,22 +1216,28 @@ def _solve_on_stream(system, setup, config, u_exact, iterate_callback, f_device,
         nat.call("bddc_scatter", ng, _p(setup.d_gown), _p(setup.w_yb2), _p(W.g), st)
         nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.g), _p(W.u0), 0, st)
         nat.call("bddc_gamma_flux", ng, _p(setup.d_gamma), _p(W.g), _p(W.us), 0, st)
-    # step 2: harmonic extension (u0) and trace solve (u*)
+    # step 2: harmonic extension (u0) and trace solve (u*) (solver.py:326-335): the
+    # same interface trace and flux load, different cell loads -- one pass over the
+    # packed pressure Schur inverses with two right-hand sides
     a = nat.LocalSolveArgs()
     a.x_gamma, a.x_scale = _p(W.g).value, 1.0
     a.u_out, a.u_mode = _p(W.u0).value, 0
     if gv is not None:
         a.f_flux, a.f_scale = _p(gv).value, 1.0
+    if setup.step2_fused:
+        a.g_cell2, a.g_scale2 = _p(W.fs).value, 1.0
+        a.u_out2 = _p(W.us).value
     nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
              _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
-    a = nat.LocalSolveArgs()
-    a.x_gamma, a.x_scale = _p(W.g).value, 1.0
-    a.g_cell, a.g_scale = _p(W.fs).value, 1.0
-    a.u_out, a.u_mode = _p(W.us).value, 0
-    if gv is not None:
-        a.f_flux, a.f_scale = _p(gv).value, 1.0
-    nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
-             _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
+    if not setup.step2_fused:
+        a = nat.LocalSolveArgs()
+        a.x_gamma, a.x_scale = _p(W.g).value, 1.0
+        a.g_cell, a.g_scale = _p(W.fs).value, 1.0
+        a.u_out, a.u_mode = _p(W.us).value, 0
+        if gv is not None:
+            a.f_flux, a.f_scale = _p(gv).value, 1.0
+        nat.call("bddc_local_solve", gp, _p(setup.d_coef), _p(setup.d_gcode), _p(setup.d_gpos),
+                 _p(setup.d_fslot), _p(setup.d_Qp), _p(setup.d_Dsub), C.byref(a), st)
     host = {}
     first = setup._solves == 0
     setup._solves += 1

@@ -49,12 +49,8 @@ def pcg_rate(reps=6):
     return its / s
 
 
-st.symv_bulk = False
-for tg in (st.n_sm, 2 * st.n_sm, 0):
-    st.t_grid = tg
-    print(f"ldg t_grid={tg}: PCG {pcg_rate():.0f} it/s", flush=True)
-st.t_grid = st.n_sm
-st.symv_bulk = True
-for tg in (148, 140, 132, 124, 116, 108, 100, 92, 84):
-    st.t_grid_bulk = tg
-    print(f"bulk t_grid={tg}: PCG {pcg_rate():.0f} it/s", flush=True)
+for rf in (False, True):
+    st.restrict_first = rf
+    for tg in (148, 136, 124, 112, 100, 92, 84, 76):
+        st.t_grid_bulk = tg
+        print(f"restrict_first={rf} t_grid={tg}: PCG {pcg_rate():.0f} it/s", flush=True)
