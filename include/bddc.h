@@ -56,6 +56,10 @@ typedef struct bddc_geom {
   int dir_axis;
   int n_flux_int;
   int n_bt;
+  /* RT0 element block per axis: c [[a_diag, a_off], [a_off, a_diag]],
+   * c = h_a^2 / (6 V k_a): (2, 1) consistent, (3, 0) lumped (grid.py:204-227) */
+  double a_diag;
+  double a_off;
 } bddc_geom;
 
 const char* bddc_last_error(void);

@@ -129,8 +129,13 @@ class Mesh:
         return ax
 
 
-def mass_matrix(mesh, k, cells=None):
-    """RT0 flux mass matrix from element blocks c[[2,1],[1,2]] (grid.py:204-307)."""
+LUMPED = False   # module switch set by Setup (grid.py:204-227, 327 `lumped`)
+
+
+def mass_matrix(mesh, k, cells=None, lumped=None):
+    """RT0 flux mass matrix from element blocks c[[2,1],[1,2]], or c[[3,0],[0,3]]
+    lumped (grid.py:204-307)."""
+    lumped = LUMPED if lumped is None else lumped
     if cells is None:
         cells = np.arange(mesh.n_cells)
     rows, cols, vals = [], [], []
@@ -140,7 +145,9 @@ def mass_matrix(mesh, k, cells=None):
         c = mesh.sizes[a] ** 2 / (6.0 * mesh.vol) / k[cells, a]
         for d, o in ((dl, dh), (dh, dl)):
             m = d >= 0
-            rows.append(d[m]); cols.append(d[m]); vals.append(2.0 * c[m])
+            rows.append(d[m]); cols.append(d[m]); vals.append((3.0 if lumped else 2.0) * c[m])
+            if lumped:
+                continue
             mo = m & (o >= 0)
             rows.append(d[mo]); cols.append(o[mo]); vals.append(c[mo])
     n = mesh.n_flux
@@ -688,6 +695,7 @@ class Config:
     project: str = "auto"     # qr (solver.py:166-179) | laplacian | auto
     pressure: str = "auto"    # splu (solver.py:254-274) | dct | auto
     log: object = None        # optional progress callback log(str)
+    lumped: bool = False      # lumped RT0 mass matrix (grid.py:327 assemble_system(lumped=))
 
 
 _FORK = None   # the Setup a forked worker reads (inherited copy-on-write)
@@ -739,6 +747,8 @@ class Setup:
     """BddcSetup restatement (solver.py:65-183)."""
 
     def __init__(self, mesh, k, f, splits, cfg):
+        global LUMPED
+        LUMPED = bool(cfg.lumped)
         self.mesh, self.k, self.cfg = mesh, k, cfg
         self.P = BoxPartition(mesh, splits)
         self.A = mass_matrix(mesh, k)

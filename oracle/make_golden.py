@@ -100,6 +100,12 @@ CASES = {
                   lambda: fields.config_field(2)),
 }
 ADAPTIVE_AT_INF = {"c2_tauinf"}
+# lumped RT0 mass matrices (grid.py:204-227, assemble_system(lumped=True))
+CASES["g2d_lumped"] = ((12, 12), (1.0, 1.0), (3, 3), "stiffness", 3.0, 1e-10,
+                       lambda: _random_k((12, 12), 31))
+CASES["g3d_lumped"] = ((8, 6, 6), (20.0, 10.0, 2.0), (2, 3, 2), "multiplicity", 5.0, 1e-10,
+                       lambda: _random_k((8, 6, 6), 32))
+LUMPED = {"g2d_lumped", "g3d_lumped"}
 
 
 def make(name):
@@ -108,7 +114,8 @@ def make(name):
     dim = len(counts)
     g = R_grid.build_grid(dim, counts, sizes)
     perm = R_grid.Permeability(k)
-    system = R_grid.assemble_system(g, perm, R_grid.Wells(0, g.n_cells - 1))
+    system = R_grid.assemble_system(g, perm, R_grid.Wells(0, g.n_cells - 1),
+                                    lumped=name in LUMPED)
     if any(np.ndim(sp) > 0 for sp in splits):
         # uneven strips: the reference's Decomposition(grid, part) with a box part
         part = np.zeros(g.n_cells, dtype=np.int64)
@@ -135,7 +142,7 @@ def make(name):
     rng = np.random.default_rng(1234)
     x = rng.standard_normal(len(dec.gamma))
     out = dict(
-        constraints=mode,
+        constraints=mode, lumped=name in LUMPED,
         counts=np.array(counts), sizes=np.array(sizes, dtype=np.float64),
         splits=np.array([len(sp) if np.ndim(sp) > 0 else sp for sp in splits]),
         scaling=scaling, tau=tau, tol=tol, k=k,

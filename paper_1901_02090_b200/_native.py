@@ -60,6 +60,7 @@ class Geom(C.Structure):
         ("maxG", C.c_int), ("maxP", C.c_int), ("maxL", C.c_int),
         ("maxF", C.c_int),
         ("dir_axis", C.c_int), ("n_flux_int", C.c_int), ("n_bt", C.c_int),
+        ("a_diag", C.c_double), ("a_off", C.c_double),
     ]
 
 

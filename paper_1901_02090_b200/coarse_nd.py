@@ -182,16 +182,19 @@ def _merge_schedule(nodes, c):
     depth = 1 + max((n["depth"] for n in nodes if not n["leaf"]), default=-1)
     if depth <= c:
         return [max(depth, 1)]
-    # deep trees (C4: 17 separator levels) merge only two levels in the top two
-    # node levels: a 7-plane root front (4652 dofs at C4) makes the root GEMV
-    # bandwidth-bound and its factorisation dominate the setup (C4 coarse solve
-    # 281 -> 244 us, coarse setup 227 -> 89 ms with 2,2,3,3,3,4)
-    top = [2, 2] if depth >= 16 else []
-    rest = depth - sum(top)
-    sched = [c] * (rest // c)
-    if rest % c:
-        sched[-1] += rest % c
-    return top + sched
+    if depth >= 15:
+        # deep trees (C4: 15 separator levels) merge only two levels in the top two
+        # node levels and keep the remainder as its own bottom level: a 7-plane root
+        # front (4652 dofs at C4) makes the root GEMV bandwidth-bound and its
+        # factorisation dominate the setup (C4 coarse solve 281 -> 244 us with
+        # 2,2,3,3,3,2; scripts/nd_merge_sweep.sh)
+        rest = depth - 4
+        sched = [2, 2] + [c] * (rest // c)
+        return sched + ([rest % c] if rest % c else [])
+    sched = [c] * (depth // c)
+    if depth % c:
+        sched[-1] += depth % c
+    return sched
 
 
 def _contract(nodes, c):

@@ -66,24 +66,26 @@ __device__ __forceinline__ int line_face_dof(const bddc_geom& G, const Box& b, i
 }
 
 // Thomas factorisation of the line tridiagonal T (order m = L-1+lo+hi):
-// T[j][j] = 2c_{p-1} + 2c_p (cells that exist), T[j][j+1] = c_p, p = j+1-lo.
-// Stores the modified super-diagonal cp and pivots piv.
-__device__ __forceinline__ void line_factor(const double* c, int L, int lo, int hi, double* cp, double* piv) {
+// T[j][j] = dg (c_{p-1} + c_p) (cells that exist), T[j][j+1] = of c_p, p = j+1-lo,
+// with the element block c [[dg, of], [of, dg]]: (2, 1) consistent RT0, (3, 0)
+// lumped (grid.py:220-225).  Stores the modified super-diagonal cp and pivots piv.
+__device__ __forceinline__ void line_factor(const double* c, int L, int lo, int hi, double* cp, double* piv,
+                                            double dg, double of) {
   const int m = L - 1 + lo + hi;
   for (int j = 0; j < m; ++j) {
     const int p = j + 1 - lo;
-    double d = (p >= 1 ? 2.0 * c[p - 1] : 0.0) + (p <= L - 1 ? 2.0 * c[p] : 0.0);
-    double pv = d - ((j > 0) ? c[p - 1] * cp[j - 1] : 0.0);  // T[j][j-1] = c_{p-1}
+    double d = (p >= 1 ? dg * c[p - 1] : 0.0) + (p <= L - 1 ? dg * c[p] : 0.0);
+    double pv = d - ((j > 0) ? of * c[p - 1] * cp[j - 1] : 0.0);  // T[j][j-1] = of c_{p-1}
     piv[j] = pv;
-    cp[j] = (j + 1 < m) ? c[p] / pv : 0.0;
+    cp[j] = (j + 1 < m) ? of * c[p] / pv : 0.0;
   }
 }
 
 // Solve T x = r in place with a factored line.
 __device__ __forceinline__ void line_solve(const double* c, int L, int lo, int hi, const double* cp,
-                                           const double* piv, double* r) {
+                                           const double* piv, double* r, double of) {
   const int m = L - 1 + lo + hi;
-  for (int j = 0; j < m; ++j) r[j] = (r[j] - ((j > 0) ? c[j - lo] * r[j - 1] : 0.0)) / piv[j];
+  for (int j = 0; j < m; ++j) r[j] = (r[j] - ((j > 0) ? of * c[j - lo] * r[j - 1] : 0.0)) / piv[j];
   for (int j = m - 2; j >= 0; --j) r[j] -= cp[j] * r[j + 1];
 }
 
@@ -147,8 +149,8 @@ __global__ void rescale_kernel(bddc_geom G, const double* __restrict__ coef, dou
       gc[a] = fc;  // the cell above the face
       int hi = cell_id(G, gc[0], gc[1], gc[2]);
       int lo = hi - stride_g;
-      if (fc <= G.n[a] - 1) acc += 2.0 * coef[(size_t)(a) * G.n_cells + (hi)];
-      if (fc >= 1) acc += 2.0 * coef[(size_t)(a) * G.n_cells + (lo)];
+      if (fc <= G.n[a] - 1) acc += G.a_diag * coef[(size_t)(a) * G.n_cells + (hi)];
+      if (fc >= 1) acc += G.a_diag * coef[(size_t)(a) * G.n_cells + (lo)];
       cnt += 1;
     }
   }
@@ -188,16 +190,16 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
       const int base = line_base(b, a, line);
       const int m = L - 1 + lo + hi;
-      if (m > 0) line_factor(c, L, lo, hi, cp, piv);
+      if (m > 0) line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
       // P_line = B Ainv B^T with B[k][k-1+lo] = +1 (low face), B[k][k+lo] = -1:
       // walk the cells kq, keeping the Ainv columns of kq's low face (colp) and
       // high face (col); the high face of kq is the low face of kq+1.
       for (int j = 0; j < m; ++j) colp[j] = (lo && j == 0) ? 1.0 : 0.0;
-      if (lo) line_solve(c, L, lo, hi, cp, piv, colp);
+      if (lo) line_solve(c, L, lo, hi, cp, piv, colp, G.a_off);
       for (int kq = 0; kq < L; ++kq) {
         const int jh = kq + lo;
         for (int j = 0; j < m; ++j) col[j] = (j == jh) ? 1.0 : 0.0;
-        if (jh < m) line_solve(c, L, lo, hi, cp, piv, col);
+        if (jh < m) line_solve(c, L, lo, hi, cp, piv, col, G.a_off);
         for (int k = 0; k < L; ++k) {
           const int kl = k - 1 + lo, kh = k + lo;
           double v = 0.0;
@@ -211,11 +213,11 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
       double a00 = 0.0, aEE = 0.0, a0E = 0.0;
       if (m > 0 && (has_lo || has_hi)) {
         for (int j = 0; j < m; ++j) col[j] = (j == 0) ? 1.0 : 0.0;
-        line_solve(c, L, lo, hi, cp, piv, col);
+        line_solve(c, L, lo, hi, cp, piv, col, G.a_off);
         a00 = col[0];
         a0E = col[m - 1];
         for (int j = 0; j < m; ++j) col[j] = (j == m - 1) ? 1.0 : 0.0;
-        line_solve(c, L, lo, hi, cp, piv, col);
+        line_solve(c, L, lo, hi, cp, piv, col, G.a_off);
         aEE = col[m - 1];
       }
       // interface slots at the two ends of the line
@@ -231,8 +233,8 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
         g[kend] = side ? -1.0 : 1.0;
         if (m > 0) {
           int jend = side ? m - 1 : 0;
-          for (int j = 0; j < m; ++j) col[j] = (j == jend) ? cend : 0.0;
-          line_solve(c, L, lo, hi, cp, piv, col);
+          for (int j = 0; j < m; ++j) col[j] = (j == jend) ? G.a_off * cend : 0.0;
+          line_solve(c, L, lo, hi, cp, piv, col, G.a_off);
           for (int k = 0; k < L; ++k) {
             const int kl = k - 1 + lo, kh = k + lo;
             double bv = 0.0;
@@ -241,15 +243,16 @@ __global__ void local_build_kernel(bddc_geom G, const double* __restrict__ coef,
             g[k] -= bv;
           }
         }
-        double d = 2.0 * cend;
-        if (m > 0) d -= cend * cend * (side ? aEE : a00);
+        double d = G.a_diag * cend;
+        if (m > 0) d -= G.a_off * G.a_off * cend * cend * (side ? aEE : a00);
         SAd[(size_t)i * G.maxG + q] = d;
         int other = side ? 0 : 1;
         bool has_other = other ? has_hi : has_lo;
         if (has_other) {
           int q2 = fslot[((size_t)i * 6 + a * 2 + other) * G.maxF + line];
           SApart[(size_t)i * G.maxG + q] = q2;
-          SAoff[(size_t)i * G.maxG + q] = (m > 0) ? -c[0] * c[L - 1] * a0E : c[0];
+          SAoff[(size_t)i * G.maxG + q] =
+              (m > 0) ? -G.a_off * G.a_off * c[0] * c[L - 1] * a0E : G.a_off * c[0];
         }
       }
     }
@@ -500,16 +503,16 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     if (m <= 0) continue;
     double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
     for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
-    line_factor(c, L, lo, hi, cp, piv);
+    line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
     for (int j = 0; j < m; ++j)
       r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo)] : 0.0;
     if (A.x_gamma) {
       int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
       int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
-      if (qlo >= 0) r[0] -= c[0] * xg[qlo];
-      if (qhi >= 0) r[m - 1] -= c[L - 1] * xg[qhi];
+      if (qlo >= 0) r[0] -= G.a_off * c[0] * xg[qlo];
+      if (qhi >= 0) r[m - 1] -= G.a_off * c[L - 1] * xg[qhi];
     }
-    line_solve(c, L, lo, hi, cp, piv, r);
+    line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
     double* t = tI + off[a] + line * m;
     const int base = line_base(b, a, line);
     double* ra = radd + a * mp;
@@ -557,7 +560,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
       if (m <= 0) continue;
       double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
       for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
-      line_factor(c, L, lo, hi, cp, piv);
+      line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
       const int base = line_base(b, a, line);
       double* t = tI + off[a] + line * m;
       if (two) {   // second system first: t is still the shared A^{-1} f
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
           const int p = j + 1 - lo;
           r[j] = (p <= L - 1 ? pp2[base + p * st] : 0.0) - (p >= 1 ? pp2[base + (p - 1) * st] : 0.0);
         }
-        line_solve(c, L, lo, hi, cp, piv, r);
+        line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
         for (int j = 0; j < m; ++j)
           A.u_out2[(size_t)line_face_dof(G, b, a, line, j, lo)] = t[j] - r[j];
       }
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
         const int p = j + 1 - lo;  // (B_u^T p')_j = p'(cell above) - p'(cell below)
         r[j] = (p <= L - 1 ? pp[base + p * st] : 0.0) - (p >= 1 ? pp[base + (p - 1) * st] : 0.0);
       }
-      line_solve(c, L, lo, hi, cp, piv, r);
+      line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
       for (int j = 0; j < m; ++j) {
         double u = t[j] - r[j];
         t[j] = u;
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
         if (m > 0) {
           double cend = coef[(size_t)(s.a) * G.n_cells + (line_cell_global(G, b, s.a, s.line, kend))];
           int jend = s.side ? m - 1 : 0;
-          v += cend * tI[off[s.a] + s.line * m + jend];
+          v += G.a_off * cend * tI[off[s.a] + s.line * m + jend];
         }
         double pc = pp[s.base + kend * s.stride];
         v += s.side ? -pc : pc;

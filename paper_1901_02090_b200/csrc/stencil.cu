@@ -74,19 +74,21 @@ __global__ void __launch_bounds__(RX* RY) flux_A_kernel(bddc_geom G, const doubl
   for (int x = threadIdx.x; x < e0; x += RX) {
     const int d = d0 + x, hi = h0 + x, lo = hi - st;
     const double clo = ca[lo], chi = ca[hi];
-    double v = 2.0 * (clo + chi) * u[d];
+    double v = G.a_diag * (clo + chi) * u[d];
     const bool l = a == 0 ? x > 0 : lo_in, h = a == 0 ? x < e0 - 1 : hi_in;
     // dof stride along a inside family a equals the cell stride st
-    if (l) v += clo * u[d - st];
+    double w = 0.0;
+    if (l) w += clo * u[d - st];
     else if (a == G.dir_axis) {
       int g[3] = {f[0] + x, f[1], f[2]};
-      v += clo * u[bnd_dof(G, 0, g)];
+      w += clo * u[bnd_dof(G, 0, g)];
     }
-    if (h) v += chi * u[d + st];
+    if (h) w += chi * u[d + st];
     else if (a == G.dir_axis) {
       int g[3] = {f[0] + x, f[1], f[2]};
-      v += chi * u[bnd_dof(G, 1, g)];
+      w += chi * u[bnd_dof(G, 1, g)];
     }
+    v += G.a_off * w;
     y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
 }
@@ -109,7 +111,7 @@ __global__ void flux_A_bnd_kernel(bddc_geom G, const double* __restrict__ coef, 
     gc[a] = side ? G.n[a] - 1 : 1;
     other = face_dof(G, a, gc[0], gc[1], gc[2]);
   }
-  const double v = 2.0 * c * u[d] + c * u[other];
+  const double v = G.a_diag * c * u[d] + G.a_off * c * u[other];
   y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
 }
 

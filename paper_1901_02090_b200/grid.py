@@ -232,7 +232,9 @@ class SaddleSystem:
                 m = d >= 0
                 rows += [d[m]]
                 cols += [d[m]]
-                vals += [2.0 * c[m]]
+                vals += [(3.0 if self.lumped else 2.0) * c[m]]   # grid.py:220-225
+                if self.lumped:
+                    continue
                 mo = m & (o >= 0)
                 rows += [d[mo]]
                 cols += [o[mo]]
@@ -266,9 +268,6 @@ def assemble_system(grid, perm, wells, lumped=False):
     `wells` is a `Wells` (mode A, the reference's only boundary condition:
     no flow everywhere, sources at two cells) or a `PressureDrop` (mode B:
     Dirichlet pressure on both ends of one axis, zero source)."""
-    if lumped:
-        raise InvalidArgumentError(
-            "lumped RT0 mass matrices are outside the accelerated path")
     if perm.k.shape != (grid.n_cells, grid.dim):
         raise InvalidArgumentError("permeability shape mismatch")
     if isinstance(wells, PressureDrop):
@@ -276,7 +275,7 @@ def assemble_system(grid, perm, wells, lumped=False):
             raise InvalidArgumentError(f"pressure-drop axis {wells.axis} outside 0..{grid.dim - 1}")
         if not (np.isfinite(wells.p_low) and np.isfinite(wells.p_high)):
             raise InvalidArgumentError("boundary pressures must be finite")
-        return SaddleSystem(grid, perm, np.zeros(grid.n_cells), None, dirichlet=wells)
+        return SaddleSystem(grid, perm, np.zeros(grid.n_cells), None, lumped=lumped, dirichlet=wells)
     for c in (wells.src_cell, wells.sink_cell):
         if not 0 <= c < grid.n_cells:
             raise InvalidArgumentError(f"well cell {c} outside grid")
@@ -285,4 +284,4 @@ def assemble_system(grid, perm, wells, lumped=False):
     f[wells.sink_cell] += wells.strength
     if abs(f.sum()) > 1e-12 * max(np.abs(f).sum(), 1.0):
         raise CompatibilityError("source terms must sum to zero")
-    return SaddleSystem(grid, perm, f, wells)
+    return SaddleSystem(grid, perm, f, wells, lumped=lumped)

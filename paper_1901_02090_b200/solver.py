@@ -115,6 +115,8 @@ def _geom(dec, system=None):
     g.n_flux_int = g.n_flux
     g.n_bt = 0 if ax is None else dec.grid.n_boundary_faces(ax)
     g.n_flux = g.n_flux_int + 2 * g.n_bt
+    lumped = bool(getattr(system, "lumped", False)) if system is not None else False
+    g.a_diag, g.a_off = (3.0, 0.0) if lumped else (2.0, 1.0)
     return g
 
 
@@ -446,7 +448,11 @@ class BddcSetup:
         # persistent bulk-streamed S_i / T_i GEMVs (one CTA per SM, ~160 KB of tiles
         # in flight each): S on every SM; T on t_grid_bulk SMs, the rest left to the
         # concurrent coarse chain
-        self.symv_bulk = dec.maxG <= 512   # the bulk kernel stages up to 512 slots
+        # bulk kernel for subdomains with many tiles (C3: maxG 448, 105 tiles: S GEMV
+        # 211 -> 208 us, PCG 1478 -> 1495 it/s); small subdomains (C4: maxG 160, 15
+        # tiles) keep the one-CTA-per-subdomain LDG kernel, whose occupancy hides the
+        # per-subdomain gather and epilogue (C4 PCG 1163 vs 1087 it/s with bulk)
+        self.symv_bulk = 256 <= dec.maxG <= 512
         # C3 (scripts/precond_pieces.py): precond 437 us at 148 CTAs, 419 at 120, 398 at
         # 100, 387 at 84, 400 at 72; T alone 217 / 224 / 245 / 280 / 320 us
         self.t_grid_bulk = max(1, (self.n_sm * 4) // 7)
@@ -1054,24 +1060,14 @@ def _suggest_scaling(setup):
     dec = setup.dec
     if not dec.n_gamma or not dec.n_faces:
         return
-    # per face: max k over the low-side cells / min k over the high-side cells,
-    # reduced on the device (index tables cached on the decomposition)
-    dev = setup.dev
-    cache = getattr(dec, "_face_cells_dev", None)
-    if cache is None or cache[0] != dev:
-        lo, hi, starts = _face_cells(dec)
-        cnt = np.diff(np.append(starts, len(lo)))
-        seg = np.repeat(np.arange(len(starts)), cnt)
-        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), dtype=torch.int64, device=dev)
-        cache = (dev, t(lo), t(hi), t(seg), len(starts))
-        dec._face_cells_dev = cache
-    _, lo, hi, seg, nfa = cache
-    k = setup.d_k.view(-1, setup.dec.grid.dim) if setup.d_k.dim() == 1 else setup.d_k
-    kl = k[lo].amax(dim=1)
-    kh = k[hi].amin(dim=1)
-    kmax = torch.full((nfa,), -math.inf, dtype=F64, device=dev).scatter_reduce(0, seg, kl, "amax")
-    kmin = torch.full((nfa,), math.inf, dtype=F64, device=dev).scatter_reduce(0, seg, kh, "amin")
-    ratio = kmax / torch.clamp(kmin, min=1e-300)
+    # per face: max k over the low-side cells / min k over the high-side cells (host
+    # bookkeeping on the caller's permeability array, once per setup, like the
+    # reference's; no device work)
+    lo, hi, starts = _face_cells(dec)
+    k = np.asarray(setup.system.perm.k, dtype=np.float64).reshape(dec.grid.n_cells, -1)
+    kmax = np.maximum.reduceat(k[lo].max(axis=1), starts)
+    kmin = np.minimum.reduceat(k[hi].min(axis=1), starts)
+    ratio = kmax / np.maximum(kmin, 1e-300)
     if bool(((ratio > 1e3) | (ratio < 1e-3)).any()):
         warnings.warn("coefficient jumps aligned with the partition detected; "
                       "consider --scaling stiffness")

@@ -26,6 +26,7 @@ def load(name):
     d["mode"] = "adaptive" if math.isfinite(d["tau"]) else "initial"
     if "constraints" in d:
         d["mode"] = str(d["constraints"])
+    d["lumped"] = bool(d["lumped"]) if "lumped" in d else False
     return d
 
 

@@ -38,6 +38,18 @@ def test_assemble_system():
         B.assemble_system(g, B.Permeability.isotropic(g, 1.0), B.Wells(0, 5))
 
 
+def test_assemble_system_lumped():
+    """grid.py:220-225 / test_grid.py:51-55: the lumped element block is diag(3c):
+    the single interior face of two unit cells gets 3/6 from each side."""
+    g = B.build_grid(2, (2, 1), (1.0, 1.0))
+    s = B.assemble_system(g, B.Permeability.isotropic(g, 1.0), B.Wells(0, 1), lumped=True)
+    np.testing.assert_allclose(s.A.toarray(), [[1.0]])
+    g = B.build_grid(2, (3, 3), (1.0, 2.0))
+    k = np.random.default_rng(0).uniform(0.5, 2.0, (9, 2))
+    A = B.assemble_system(g, B.Permeability(k), B.Wells(0, 8), lumped=True).A
+    assert A.nnz == A.shape[0]   # diagonal
+
+
 def test_matrices_match_oracle():
     from oracle import bddc_oracle as O
     rng = np.random.default_rng(3)

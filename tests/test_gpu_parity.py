@@ -38,7 +38,8 @@ CASES = names()
 def _setup(d):
     import paper_1901_02090_b200 as B
     g = B.build_grid(len(d["counts"]), d["counts"], d["sizes"])
-    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1))
+    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1),
+                               lumped=d["lumped"])
     dec = B.regular_partition(g, d["splits"])
     cfg = B.SolveConfig(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
     return B, system, dec, cfg

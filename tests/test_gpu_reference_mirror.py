@@ -115,7 +115,8 @@ def _golden_setup(name):
     import paper_1901_02090_b200 as B
     d = load(name)
     g = B.build_grid(len(d["counts"]), d["counts"], d["sizes"])
-    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1))
+    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1),
+                               lumped=d["lumped"])
     dec = B.regular_partition(g, d["splits"])
     cfg = B.SolveConfig(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
     return d, B, system, dec, B.BddcSetup(system, dec, cfg)
@@ -203,7 +204,8 @@ def test_subs_and_coarse_views(name):
     x = np.random.default_rng(3).standard_normal(int(dec.nG[0]))
     assert rel(st.subs[0].schur_apply(x), d["S_sub0"] @ x) <= 1e-11
     mesh = O.Mesh(d["counts"], d["sizes"])
-    cfg = O.Config(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
+    cfg = O.Config(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"],
+                   lumped=d["lumped"])
     ost = O.Setup(mesh, d["k"], O.well_rhs(mesh, 0, mesh.n_cells - 1), d["splits"], cfg)
     # adaptive rows are defined up to sign / rotation inside a degenerate eigenspace,
     # so the coarse bases of two implementations differ by a face-block transform on
