@@ -195,10 +195,14 @@ int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, int K, const
  * right-hand sides into rsbuf (ysize entries) first.  xdirect != NULL (a level
  * whose nodes have no boundary, i.e. the root): the separator solution is final
  * after the forward sweep and is written to x directly (no bwd for that level). */
+/* cown != NULL: the right-hand side is not read from r but formed on the fly from
+ * the per-subdomain restriction rows v (r[g] = v[cown[2g]] - v[cown[2g+1]] for the
+ * nfc flux dofs, 0 for the pressures: the preconditioner's coarse load,
+ * coarse.py:225-235), so no assembled rhs is written first. */
 int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
-                const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
-                double* xdirect, void* stream);
+                const double* Fc, const double* r, const double* v, const int* cown, int nfc,
+                double* rsbuf, double* ybuf, double* cbuf, double* xdirect, void* stream);
 /* bwd: wpr (1, 2, 4, 8) warps share one separator row (tasks then hold 8/wpr rows per pass). */
 int bddc_nd_bwd(int ntasks, int bfmax, int wpr, const int* tasks, const int* info,
                 const long long* data_off, const int* sep_flat, const int* bnd_flat, const double* Fc,
@@ -238,6 +242,9 @@ int bddc_scatter(int n_gamma, const int* gown, const double* yb, double* y, void
 /* Balanced projection (solver.py:166-179) as I - Phi^T (Phi Phi^T)^+ Phi. */
 int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const double* y,
              double* phi, void* stream);
+/* Same on the unassembled per-slot values yb (the scatter fused into the reads). */
+int bddc_phi_broken(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const int* gown,
+                    const double* yb, double* phi, void* stream);
 int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
                    double* z, void* stream);
 /* Same, multi-CTA: six mode-product launches (PDL), ws = 2 N doubles. */
@@ -337,6 +344,17 @@ int bddc_proj_dot(int n_gamma, int maxG, const int* gown, const double* z, doubl
                   void* ws, double* scal, int op, double* hist, void* stream);
 int bddc_cg_update_dot(long long n, double* x, const double* p, double* r, const double* Ap, void* ws,
                        double* scal, int op, double* hist, void* stream);
+/* The same inside the captured PCG loop: the reducing block also sets the WHILE
+ * node's condition `cond` (bddc_graph_handle) from relres, breakdown and maxit
+ * (solver.py:204-227's loop test), replacing the separate bddc_pcg_cond kernel. */
+int bddc_cg_update_dot_cond(long long n, double* x, const double* p, double* r, const double* Ap,
+                            void* ws, double* scal, int op, double* hist, unsigned long long cond,
+                            double tol, int maxit, void* stream);
+/* Scatter fused into the projection: y = (yb[own0] + yb[own1]) - Phi^T z and the
+ * dot x . y (yb: per-slot values, N x maxG, as written by the GEMV / prolongation). */
+int bddc_proj_dot_broken(int n_gamma, int maxG, const int* gown, const double* yb, const double* z,
+                         double* y, const double* x, void* ws, double* scal, int op, double* hist,
+                         void* stream);
 
 /* preconditioned_spectrum (oracle.py:114-141) pieces: w -= Q^T c (Q: k rows of
  * length n), and every eigenvalue of a symmetric tridiagonal (bisection on

@@ -114,7 +114,7 @@ _SIGS = {
     "bddc_pcg_cond": [_P, _P, _D, _I, _P],
     "bddc_nd_assemble": [_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _I, _I, _P,
                          _P, _P, _I, _P],
-    "bddc_nd_fwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_nd_fwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P],
     "bddc_nd_compact": [_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P],
     "bddc_nd_qd": [_I, _I, _I, _I, _I, _P, _P],
     "bddc_nd_bwd": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -138,6 +138,9 @@ _SIGS = {
     "bddc_cg_update": [_L, _P, _P, _P, _P, _P, _P],
     "bddc_proj_dot": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P],
     "bddc_cg_update_dot": [_L, _P, _P, _P, _P, _P, _P, _I, _P, _P],
+    "bddc_cg_update_dot_cond": [_L, _P, _P, _P, _P, _P, _P, _I, _P, C.c_ulonglong, _D, _I, _P],
+    "bddc_proj_dot_broken": [_I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P],
+    "bddc_phi_broken": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "bddc_p_update": [_L, _P, _P, _P, _P],
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
     "bddc_set_gemv_wpr": [_I],

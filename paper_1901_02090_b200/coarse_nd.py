@@ -585,20 +585,23 @@ class CoarseND:
             L.F = None
             L.X = None
 
-    def solve(self, r, x):
+    def solve(self, r, x, restricted=None):
         """Pinned coarse solve on the combined vector [flux | pressures] (coarse.py:208-215).
 
         r, x: length nfc + N.  r is read-only; x[nfc] (subdomain 0's pinned
-        pressure) is not written.
+        pressure) is not written.  restricted = (v, cown): r is not read; the
+        flux rhs is v[cown[:, 0]] - v[cown[:, 1]] and the pressure rhs zero
+        (the preconditioner's restriction, coarse.py:225-235).
         """
         st = _stream()
         ys, cb = self._bufs()
+        v, cown = restricted if restricted is not None else (None, None)
         for li, L in enumerate(self.levels):
             # a level without boundary (the root) writes its solution directly
             direct = L.bmax == 0
             nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
-                     _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(self._rs), _p(ys[li]),
-                     _p(cb), _p(x) if direct else None, st)
+                     _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(v), _p(cown), self.nfc,
+                     _p(self._rs), _p(ys[li]), _p(cb), _p(x) if direct else None, st)
         for li in range(len(self.levels) - 1, -1, -1):
             L = self.levels[li]
             if L.bmax == 0:

@@ -60,12 +60,22 @@ __global__ void nd_assemble_kernel(int m, int S, int Sf, int B, int nf, int slot
 // whole boundary (flux dofs and pressures, indices into the combined vector),
 // then X^T (s x b).
 
+// Coarse right-hand side entry g: r[g], or (cown != NULL, the preconditioner's
+// restriction) v[own+] - v[own-] for flux dofs and 0 for pressures (coarse.py:225-235
+// with a zero pressure load), so no assembled rhs vector is written.
+__device__ __forceinline__ double nd_rhs(const double* __restrict__ r, const double* __restrict__ v,
+                                         const int* __restrict__ cown, int nfc, int g) {
+  if (!cown) return r[g];
+  return g < nfc ? v[cown[2 * g]] - v[cown[2 * g + 1]] : 0.0;
+}
+
 // Forward gather (left-looking), 8 lanes per separator entry of the level:
 // rs[t] = r[g_t] - sum of the descendants' update entries (lane-strided over the
 // list, fixed shuffle tree: deterministic).
 __global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const int* __restrict__ lptr,
                                  const int* __restrict__ lsrc, const double* __restrict__ cbuf,
-                                 const double* __restrict__ r, double* __restrict__ rs) {
+                                 const double* __restrict__ r, const double* __restrict__ v,
+                                 const int* __restrict__ cown, int nfc, double* __restrict__ rs) {
   pdl_trigger();
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = gt >> 3, sub = gt & 7;
@@ -81,7 +91,7 @@ __global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const 
   acc += __shfl_xor_sync(0xffffffffu, acc, 4);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-  if (t < n && sub == 0) rs[t] = r[g] - acc;
+  if (t < n && sub == 0) rs[t] = nd_rhs(r, v, cown, nfc, g) - acc;
 }
 
 // Forward GEMV, task = rows [row0, row1) of one node, 4 rows per warp pass:
@@ -92,6 +102,7 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
                               const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
                               const int* __restrict__ lptr, const int* __restrict__ lsrc,
                               const double* __restrict__ Fc, const double* __restrict__ r,
+                              const double* __restrict__ v, const int* __restrict__ cown, int nfc,
                               const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf,
                               int lpe, double* __restrict__ xdirect) {
   extern __shared__ double rsm[];
@@ -110,13 +121,49 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
         for (int p = lptr[sp + t] + sub; p < p1; p += lpe) acc += cbuf[lsrc[p]];
       }
       for (int o = lpe >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (t < s && sub == 0) rsm[t] = r[sep_flat[sp + t]] - acc;
+      if (t < s && sub == 0) rsm[t] = nd_rhs(r, v, cown, nfc, sep_flat[sp + t]) - acc;
     }
   } else {
     for (int k = threadIdx.x; k < s; k += blockDim.x) rsm[k] = rs[sp + k];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nq = (row1 - row0 + 3) / 4;
+  int cs = 1;
+  while (cs < 8 && 2 * cs * nq <= nw) cs *= 2;
+  if (cs > 1) {
+    // short task (long rows, few of them): cs warps split each row quad's columns,
+    // partials combined in warp order (deterministic)
+    __shared__ double part[8][4];
+    const int qd = warp / cs, pc = warp % cs;
+    const int chunk = ((s + cs - 1) / cs + 31) & ~31;
+    const int c0 = imin(pc * chunk, s), c1 = imin(c0 + chunk, s);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (qd < nq) {
+      const int row = row0 + 4 * qd;
+      warp_rows4_dot(base + (size_t)row * s + c0, s, imin(4, row1 - row), rsm + c0, c1 - c0, lane, acc);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) part[warp][k] = acc[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 * nq) {
+      const int qd2 = threadIdx.x >> 2, k = threadIdx.x & 3;
+      const int rr = row0 + 4 * qd2 + k;
+      if (rr < row1) {
+        double v = 0.0;
+        for (int u = 0; u < cs; ++u) v += part[qd2 * cs + u][k];
+        if (rr < s) {
+          if (xdirect) xdirect[sep_flat[sp + rr]] = v;
+          else ybuf[sp + rr] = v;
+        } else {
+          cbuf[cbo + rr - s] = v;
+        }
+      }
+    }
+    return;
+  }
   for (int row = row0 + 4 * warp; row < row1; row += 4 * nw) {
     const int nr = imin(4, row1 - row);
     double acc[4];
@@ -261,8 +308,8 @@ extern "C" int bddc_nd_assemble(int m, int S, int Sf, int B, int nf, int slot, i
 
 extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, const int* info,
                            const long long* data_off, const int* sep_flat, const int* lptr, const int* lsrc,
-                           const double* Fc, const double* r, double* rsbuf, double* ybuf, double* cbuf,
-                           double* xdirect, void* stream) {
+                           const double* Fc, const double* r, const double* v, const int* cown, int nfc,
+                           double* rsbuf, double* ybuf, double* cbuf, double* xdirect, void* stream) {
   if (ntasks <= 0 || ysize <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   // small separators: every task gathers its own r_sep (lanes per entry so one
@@ -270,11 +317,11 @@ extern "C" int bddc_nd_fwd(int ysize, int ntasks, int smax, const int* tasks, co
   const int lpe = (smax <= 32 && ntasks <= 2 * ysize / (smax > 0 ? smax : 1)) ? 8 : 0;
   if (lpe == 0)
     PDL_LAUNCH(nd_gather_kernel, dim3((unsigned)(((long long)ysize * 8 + 255) / 256)), dim3(256), 0, st, ysize,
-               sep_flat, lptr, lsrc, (const double*)cbuf, r, rsbuf);
+               sep_flat, lptr, lsrc, (const double*)cbuf, r, v, cown, nfc, rsbuf);
   size_t shm = (size_t)(smax > 0 ? smax : 1) * sizeof(double);
   if (shm > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(nd_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   PDL_LAUNCH(nd_fwd_kernel, dim3(ntasks), dim3(256), shm, st, tasks, info, data_off, sep_flat, lptr, lsrc, Fc, r,
-             (const double*)rsbuf, ybuf, cbuf, lpe, xdirect);
+             v, cown, nfc, (const double*)rsbuf, ybuf, cbuf, lpe, xdirect);
   return 0;
 }
 

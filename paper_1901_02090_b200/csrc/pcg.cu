@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
 #define SB_ISSUER SB_NCW
 #define SB_GATHER (SB_NCW + 1)
 #define SB_EPI (SB_NCW + 2)
+#define SB_TMAX 136   // live tiles of a 512-slot subdomain (16 * 17 / 2)
 
 __device__ __forceinline__ void tile_symv(const double* T, const double* xr, const double* xc, int lane,
                                           double& rsum, double& csum) {
@@ -195,6 +196,21 @@ __device__ __forceinline__ void tile_symv(const double* T, const double* xr, con
   }
   rsum = v[0];
   csum = col;
+}
+
+// lane l returns sum over lanes of v[l] (31-shuffle transposed reduction; v is consumed)
+__device__ __forceinline__ double lane_transpose_sum(double (&v)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = lane & off;
+#pragma unroll
+    for (int k = 0; k < off; ++k) {
+      double send = up ? v[k] : v[k + off];
+      double recv = __shfl_xor_sync(0xffffffffu, send, off);
+      v[k] = (up ? v[k + off] : v[k]) + recv;
+    }
+  }
+  return v[0];
 }
 
 // advance (bi, bj) by `steps` positions in the row-major order of the live upper
@@ -224,6 +240,7 @@ symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restr
   uint64_t* xfree = xfull + 2;        // [2] buffer released (epilogue -> gather)
   uint64_t* ydone = xfree + 2;        // [2] accumulators complete (consumers -> epilogue)
   int* meta = reinterpret_cast<int*>(ydone + 2);
+  int* toff = meta + 2;               // [2][SB_TMAX] packed tile index per issue slot
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   if (threadIdx.x == 0) {
@@ -273,6 +290,22 @@ symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restr
 #pragma unroll
       for (int u = 0; u < 16; ++u)
         if (u < ntl) xb[lane + 32 * u] = v[u];
+      // issue order j -> class c = j % 8 (its consumer warp), k = j / 8: the k-th
+      // tile of class c's contiguous chunk of the row-major live tiles
+      {
+        const int T = ntl * (ntl + 1) / 2;
+        const int q = T / SB_NCW, rm = T % SB_NCW;
+        for (int j = lane; j < T; j += 32) {
+          const int c = j % SB_NCW;
+          int u = c * q + imin(c, rm) + j / SB_NCW;
+          int bi = 0;
+          while (u >= ntl - bi) {
+            u -= ntl - bi;
+            ++bi;
+          }
+          toff[b * SB_TMAX + j] = tile_index(bi, bi + u, nt);
+        }
+      }
       if (lane == 0) meta[b] = i;
       __syncwarp();
       mbar_arrive(xfull + b);
@@ -294,15 +327,14 @@ symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restr
         const int i = meta[b];
         if (i < 0) break;
         const int ntl = (nG[i] + 31) / 32;
+        const int T = ntl * (ntl + 1) / 2;
         const double* Pk = packed + (size_t)i * ntiles * 1024;
-        for (int bi = 0; bi < ntl; ++bi) {
-          const double* row = Pk + (size_t)tile_index(bi, bi, nt) * 1024;
-          for (int bj = bi; bj < ntl; ++bj, ++G) {
-            const unsigned slot = G % SB_NST;
-            mbar_wait(empty + slot, ((G / SB_NST) & 1) ^ 1);
-            mbar_arrive_expect_tx(full + slot, 8192u);
-            bulk_g2s(ring + slot * 1024, row + (size_t)(bj - bi) * 1024, 8192u, full + slot);
-          }
+        const int* to = toff + b * SB_TMAX;
+        for (int j = 0; j < T; ++j, ++G) {
+          const unsigned slot = G % SB_NST;
+          mbar_wait(empty + slot, ((G / SB_NST) & 1) ^ 1);
+          mbar_arrive_expect_tx(full + slot, 8192u);
+          bulk_g2s(ring + slot * 1024, Pk + (size_t)to[j] * 1024, 8192u, full + slot);
         }
       }
     }
@@ -339,24 +371,62 @@ symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restr
       const int ntl = (nG[i] + 31) / 32;
       const int T = ntl * (ntl + 1) / 2;
       const double* xb = xs + b * maxG;
-      int t = (int)((warp - G % SB_NCW + SB_NCW) % SB_NCW);
-      // accumulator by the subdomain-local tile class t % 8 (not by warp): the
-      // summation grouping is independent of the CTA's history (deterministic)
-      double* myy = yw + ((size_t)b * SB_NCW + t) * maxG;
+      const int c = (int)((warp - G % SB_NCW + SB_NCW) % SB_NCW);
+      // class c (subdomain-local, not the warp) owns a contiguous chunk of the
+      // row-major live tiles and its own accumulator: the summation grouping is
+      // independent of the CTA's history (deterministic)
+      double* myy = yw + ((size_t)b * SB_NCW + c) * maxG;
+      const int q = T / SB_NCW, rm = T % SB_NCW;
+      const int len = q + (c < rm ? 1 : 0);
       int bi = 0, bj = 0;
-      tri_advance(bi, bj, ntl, t);
-      for (; t < T; t += SB_NCW) {
-        const unsigned g = G + t;
+      {
+        int u = c * q + imin(c, rm);
+        while (u >= ntl - bi) {
+          u -= ntl - bi;
+          ++bi;
+        }
+        bj = bi + u;
+      }
+      // row contributions stay lane-partial (v[r] over this lane's column) while
+      // the chunk walks one tile row; one transposed reduction per row run
+      double v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = 0.0;
+      int cur = bi;
+      for (int k = 0; k < len; ++k) {
+        if (bi != cur) {
+          myy[cur * 32 + lane] += lane_transpose_sum(v, lane);
+#pragma unroll
+          for (int r = 0; r < 32; ++r) v[r] = 0.0;
+          cur = bi;
+        }
+        const unsigned g = G + (unsigned)(k * SB_NCW + c);
         const unsigned slot = g % SB_NST;
         mbar_wait(full + slot, (g / SB_NST) & 1);
-        double rs, cs;
-        tile_symv(ring + slot * 1024, xb + bi * 32, xb + bj * 32, lane, rs, cs);
-        myy[bi * 32 + lane] += rs;
-        if (bi != bj) myy[bj * 32 + lane] += cs;
+        const double* Tt = ring + slot * 1024;
+        const double* xr = xb + bi * 32;
+        const double xl = xb[bj * 32 + lane];
+        double cs0 = 0.0, cs1 = 0.0, cs2 = 0.0, cs3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; r += 4) {
+          const double a0 = Tt[r * 32 + lane], a1 = Tt[(r + 1) * 32 + lane];
+          const double a2 = Tt[(r + 2) * 32 + lane], a3 = Tt[(r + 3) * 32 + lane];
+          v[r] = fma(a0, xl, v[r]);
+          v[r + 1] = fma(a1, xl, v[r + 1]);
+          v[r + 2] = fma(a2, xl, v[r + 2]);
+          v[r + 3] = fma(a3, xl, v[r + 3]);
+          cs0 = fma(a0, xr[r], cs0);
+          cs1 = fma(a1, xr[r + 1], cs1);
+          cs2 = fma(a2, xr[r + 2], cs2);
+          cs3 = fma(a3, xr[r + 3], cs3);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + slot);
-        tri_advance(bi, bj, ntl, SB_NCW);
+        // off the diagonal the tile also acts transposed (diagonal tiles are stored full)
+        if (bi != bj) myy[bj * 32 + lane] += (cs0 + cs1) + (cs2 + cs3);
+        tri_advance(bi, bj, ntl, 1);
       }
+      if (len > 0) myy[cur * 32 + lane] += lane_transpose_sum(v, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(ydone + b);
       G += T;
@@ -547,14 +617,19 @@ __global__ void scatter_kernel(int n_gamma, const int* __restrict__ gown, const 
 }
 
 // phi[i] = sum_q sign_q y[gpos[i][q]], sign = +1 on the high side of the box
+// phi_i = sum over the interface slots of i of sign * y; gown != NULL: y is not
+// assembled yet and is read from the per-slot values yb (y[g] = yb[own0] + yb[own1],
+// the scatter fused away).
 __global__ void phi_kernel(int maxG, const int* __restrict__ nG, const int* __restrict__ gpos,
-                           const int* __restrict__ gcode, const double* __restrict__ y, double* __restrict__ phi) {
+                           const int* __restrict__ gcode, const double* __restrict__ y, double* __restrict__ phi,
+                           const int* __restrict__ gown, const double* __restrict__ yb) {
   __shared__ double red[32];
   const int i = blockIdx.x;
   double acc = 0.0;
   for (int q = threadIdx.x; q < nG[i]; q += blockDim.x) {
     size_t s = (size_t)i * maxG + q;
-    double v = y[gpos[s]];
+    const int g = gpos[s];
+    double v = gown ? yb[gown[2 * g]] + yb[gown[2 * g + 1]] : y[g];
     acc += ((gcode[s] >> 2) & 1) ? v : -v;
   }
   acc = block_sum(acc, red);
@@ -641,10 +716,16 @@ __global__ void proj_apply_kernel(int n_gamma, int maxG, const int* __restrict__
 struct DotArgs {
   const int* gown;
   int maxG;
-  const double* z;     // MODE 1: the subdomain Laplacian solve
+  const double* z;     // MODE 1, 3: the subdomain Laplacian solve
   double* xv;          // MODE 2: iterate
   const double* p;     // MODE 2
   const double* Ap;    // MODE 2
+  const double* yb;    // MODE 3: per-slot values, assembled on the fly
+  // op 2 with cond != 0: the PCG WHILE node's condition is set by the reducing
+  // block (relres > tol, no breakdown, it < maxit), no separate condition kernel
+  unsigned long long cond;
+  double tol;
+  int maxit;
 };
 
 template <int MODE>
@@ -657,9 +738,10 @@ __global__ void dot_kernel(const double* __restrict__ x, double* __restrict__ y,
   double acc = 0.0;
   const double alpha = MODE == 2 ? scal[2] : 0.0;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    if (MODE == 1) {
-      const int lo = A.gown[2 * e] / A.maxG, hi = A.gown[2 * e + 1] / A.maxG;
-      const double v = y[e] - (A.z[lo] - A.z[hi]);
+    if (MODE == 1 || MODE == 3) {
+      const int s0 = A.gown[2 * e], s1 = A.gown[2 * e + 1];
+      const int lo = s0 / A.maxG, hi = s1 / A.maxG;
+      const double v = (MODE == 3 ? A.yb[s0] + A.yb[s1] : y[e]) - (A.z[lo] - A.z[hi]);
       y[e] = v;
       acc += x[e] * v;
     } else if (MODE == 2) {
@@ -716,6 +798,10 @@ __global__ void dot_kernel(const double* __restrict__ x, double* __restrict__ y,
         scal[5] = rel;
         scal[9] = (double)(itc + 1);
         if (hist) hist[itc + 1] = rel;
+        if (A.cond) {
+          const bool go = !(rel <= A.tol) && scal[8] == 0.0 && itc + 1 < A.maxit;
+          cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond, go ? 1u : 0u);
+        }
         break;
       }
       case 3: {  // rz_new -> beta, betas[it-1]
@@ -1009,7 +1095,7 @@ extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos,
 
 static size_t symv_bulk_smem(int maxG) {
   return (size_t)SB_NST * 8192 + (size_t)(2 + 2 * SB_NCW) * maxG * sizeof(double) +
-         (2 * SB_NST + 6) * sizeof(uint64_t) + 2 * sizeof(int);
+         (2 * SB_NST + 6) * sizeof(uint64_t) + (2 + 2 * SB_TMAX) * sizeof(int);
 }
 
 // Persistent bulk-streamed variant: `grid` CTAs (<= 0: one per SM), `sched` two
@@ -1099,7 +1185,14 @@ extern "C" int bddc_scatter(int n_gamma, const int* gown, const double* yb, doub
 
 extern "C" int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const double* y, double* phi,
                         void* stream) {
-  phi_kernel<<<N, 256, 0, (cudaStream_t)stream>>>(maxG, nG, gpos, gcode, y, phi);
+  phi_kernel<<<N, 256, 0, (cudaStream_t)stream>>>(maxG, nG, gpos, gcode, y, phi, nullptr, nullptr);
+  LAUNCH_OK();
+  return 0;
+}
+
+extern "C" int bddc_phi_broken(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const int* gown,
+                               const double* yb, double* phi, void* stream) {
+  phi_kernel<<<N, 256, 0, (cudaStream_t)stream>>>(maxG, nG, gpos, gcode, nullptr, phi, gown, yb);
   LAUNCH_OK();
   return 0;
 }
@@ -1253,8 +1346,21 @@ extern "C" int bddc_proj_dot(int n_gamma, int maxG, const int* gown, const doubl
                              void* ws, double* scal, int op, double* hist, void* stream) {
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
-  DotArgs A{gown, maxG, z, nullptr, nullptr, nullptr};
+  DotArgs A{gown, maxG, z, nullptr, nullptr, nullptr, nullptr, 0ull, 0.0, 0};
   dot_kernel<1><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n_gamma, partial, counter, scal, op,
+                                                                     hist, A);
+  LAUNCH_OK();
+  return 0;
+}
+
+// y = (yb[own0] + yb[own1]) - Phi^T z: scatter, projection apply and the dot x . y in one pass.
+extern "C" int bddc_proj_dot_broken(int n_gamma, int maxG, const int* gown, const double* yb, const double* z,
+                                    double* y, const double* x, void* ws, double* scal, int op, double* hist,
+                                    void* stream) {
+  double* partial = (double*)ws;
+  unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
+  DotArgs A{gown, maxG, z, nullptr, nullptr, nullptr, yb, 0ull, 0.0, 0};
+  dot_kernel<3><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n_gamma, partial, counter, scal, op,
                                                                      hist, A);
   LAUNCH_OK();
   return 0;
@@ -1265,7 +1371,20 @@ extern "C" int bddc_cg_update_dot(long long n, double* xv, const double* p, doub
                                   double* scal, int op, double* hist, void* stream) {
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
-  DotArgs A{nullptr, 1, nullptr, xv, p, Ap};
+  DotArgs A{nullptr, 1, nullptr, xv, p, Ap, nullptr, 0ull, 0.0, 0};
+  dot_kernel<2><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(r, r, n, partial, counter, scal, op, hist, A);
+  LAUNCH_OK();
+  return 0;
+}
+
+// Same, and (op 2) the reducing block sets the PCG WHILE node's condition `cond`
+// (a cudaGraphConditionalHandle from bddc_graph_handle).
+extern "C" int bddc_cg_update_dot_cond(long long n, double* xv, const double* p, double* r, const double* Ap,
+                                       void* ws, double* scal, int op, double* hist, unsigned long long cond,
+                                       double tol, int maxit, void* stream) {
+  double* partial = (double*)ws;
+  unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
+  DotArgs A{nullptr, 1, nullptr, xv, p, Ap, nullptr, cond, tol, maxit};
   dot_kernel<2><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(r, r, n, partial, counter, scal, op, hist, A);
   LAUNCH_OK();
   return 0;

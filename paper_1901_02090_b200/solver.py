@@ -453,9 +453,9 @@ class BddcSetup:
         # tiles) keep the one-CTA-per-subdomain LDG kernel, whose occupancy hides the
         # per-subdomain gather and epilogue (C4 PCG 1163 vs 1087 it/s with bulk)
         self.symv_bulk = 256 <= dec.maxG <= 512
-        # C3 (scripts/precond_pieces.py): precond 437 us at 148 CTAs, 419 at 120, 398 at
-        # 100, 387 at 84, 400 at 72; T alone 217 / 224 / 245 / 280 / 320 us
-        self.t_grid_bulk = max(1, (self.n_sm * 4) // 7)
+        # C3 (scripts/precond_tune.py, chunked tile classes): precond 399 us at 148
+        # CTAs, 376 at 120, 354 at 100, 366 at 84; T alone 218 / 223 / 235 / 263 us
+        self.t_grid_bulk = max(1, (self.n_sm * 2) // 3)
         self._sched = torch.zeros(8, dtype=I32, device=dev)   # ticket counters per call site
         self.restrict_first = False
         # Step 2's two local solves in one two-rhs pass over Q where the two-rhs kernel's
@@ -641,8 +641,9 @@ class BddcSetup:
 
     # ----------------------------------------- interface operator (device)
 
-    def _schur(self, x, y):
-        """y = S x (continuous interface vectors), solver.py:103-107."""
+    def _schur(self, x, y, assemble=True):
+        """y = S x (continuous interface vectors), solver.py:103-107.  assemble=False:
+        the per-slot products stay in w_yb (the caller's projection assembles them)."""
         st = _stream()
         kt = self._ktimer
         if kt is not None:
@@ -653,14 +654,21 @@ class BddcSetup:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
             kt["ev"].append((e0, e1))
-        nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb), _p(y), st)
+        if assemble:
+            nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb), _p(y), st)
 
-    def _project(self, y, dot=None):
+    def _project(self, y, dot=None, yb=None):
         """In-place balanced projection, solver.py:166-179.  dot = (x, op, hist): fuse
-        the following PCG dot x . (P y) into the apply step (one pass, one launch)."""
+        the following PCG dot x . (P y) into the apply step (one pass, one launch).
+        yb: y is not assembled yet; its per-slot values yb are summed on the fly by
+        the phi and apply kernels (the scatter fused away; requires dot)."""
         st = _stream()
-        nat.call("bddc_phi", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
-                 _p(self.d_gcode), _p(y), _p(self.w_phi), st)
+        if yb is not None:
+            nat.call("bddc_phi_broken", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(self.d_gcode), _p(self.d_gown), _p(yb), _p(self.w_phi), st)
+        else:
+            nat.call("bddc_phi", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(self.d_gcode), _p(y), _p(self.w_phi), st)
         z = self.w_z
         if self.d_Lp is not None:
             nat.call("bddc_gemv", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi), _p(self.w_z),
@@ -677,15 +685,21 @@ class BddcSetup:
             S3 = self.dec.S3
             nat.call("bddc_lap_solve_mc", S3[0], S3[1], S3[2], _p(self.d_eig_w),
                      _p(self.d_dm_w), _p(self.w_phi), _p(self.w_z), _p(self._lap_ws), st)
-        if dot is None:
+        if yb is not None:
+            x, op, hist = dot
+            nat.call("bddc_proj_dot_broken", self.n_gamma, self.maxG, _p(self.d_gown), _p(yb), _p(z),
+                     _p(y), _p(x), _p(self.w_dot), _p(self.w_scal), op,
+                     _p(hist) if hist is not None else None, st)
+        elif dot is None:
             nat.call("bddc_proj_apply", self.n_gamma, self.maxG, _p(self.d_gown), _p(z), _p(y), st)
         else:
             x, op, hist = dot
             nat.call("bddc_proj_dot", self.n_gamma, self.maxG, _p(self.d_gown), _p(z), _p(y), _p(x),
                      _p(self.w_dot), _p(self.w_scal), op, _p(hist) if hist is not None else None, st)
 
-    def _precond(self, r, out):
-        """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged."""
+    def _precond(self, r, out, assemble=True):
+        """BDDC Algorithm 2 (solver.py:109-128): coarse + Delta, averaged.  assemble=False:
+        the averaged per-slot result stays in w_yb2 (the projection assembles it)."""
         st = _stream()
         main = torch.cuda.current_stream()
         if self.nfc:
@@ -708,10 +722,9 @@ class BddcSetup:
                     nat.call("bddc_gather_gemv_t", self.N, self.maxG, self.maxC, _p(self.d_nG),
                              _p(self.d_nC), _p(self.d_gpos), _p(self.d_Psi), _p(r),
                              _p(self.d_delta), _p(self.w_v), ss)
-                nat.call("bddc_coarse_restrict", self.nfc, _p(self.d_cown), _p(self.w_v),
-                         _p(self.w_rc), ss)
-                nat.call("bddc_fill", self.N, 0.0, _p(self.w_rc[self.nfc:]), ss)
-                self._coarse_solve()
+                # the ND forward sweep forms the coarse load v[own+] - v[own-] (zero
+                # pressure load) itself: no assembled rhs
+                self.nd.solve(None, self.w_xc, restricted=(self.w_v, self.d_cown))
                 join = torch.cuda.Event()
                 join.record(side)
         # T_i GEMV with one CTA per SM (grid-stride over subdomains) so the
@@ -725,7 +738,8 @@ class BddcSetup:
         nat.call("bddc_prolong", self.N, self.maxG, self.maxC, _p(self.d_nG), _p(self.d_nC),
                  _p(self.d_sub_rows), _p(self.d_Psi), _p(self.w_xc), _p(self.w_yb),
                  _p(self.d_delta), _p(self.w_yb2), st)
-        nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
+        if assemble:
+            nat.call("bddc_scatter", self.n_gamma, _p(self.d_gown), _p(self.w_yb2), _p(out), st)
 
     def _symv(self, mats, x, win, yb, grid, site, st):
         """yb = blockdiag(M_i) (win . x) gathered per subdomain (bulk kernel unless
@@ -1477,33 +1491,38 @@ class _PCGBufs:
         self.res = z(maxit + 2)
 
 
-def _pcg_core(setup, W, B):
+def _pcg_core(setup, W, B, cond=None):
     """Ap = P S p; alpha = rz / p.Ap; x += alpha p; r -= alpha Ap; relres
-    (solver.py:205-216): the projection's apply carries the p.Ap dot, the update
-    carries r.r."""
+    (solver.py:205-216): the projection assembles S p from the per-slot products and
+    carries the p.Ap dot, the update carries r.r.  cond = (handle, tol, maxit) inside
+    the captured loop: the update's reducing block also sets the WHILE condition."""
     ng = setup.n_gamma
-    setup._schur(W.p, W.Ap)
-    setup._project(W.Ap, dot=(W.p, 1, B.alphas))
-    nat.call("bddc_cg_update_dot", ng, _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _p(setup.w_dot),
-             _p(setup.w_scal), 2, _p(B.res), _stream())
+    setup._schur(W.p, W.Ap, assemble=False)
+    setup._project(W.Ap, dot=(W.p, 1, B.alphas), yb=setup.w_yb)
+    if cond is None:
+        nat.call("bddc_cg_update_dot", ng, _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _p(setup.w_dot),
+                 _p(setup.w_scal), 2, _p(B.res), _stream())
+    else:
+        nat.call("bddc_cg_update_dot_cond", ng, _p(W.x), _p(W.p), _p(W.r), _p(W.Ap), _p(setup.w_dot),
+                 _p(setup.w_scal), 2, _p(B.res), cond[0], float(cond[1]), int(cond[2]), _stream())
 
 
-def _pcg_first(setup, W, B):
+def _pcg_first(setup, W, B, cond=None):
     """z = P M r; p = z; rz = r.z; first iteration (solver.py:198-216)."""
     ng = setup.n_gamma
-    setup._precond(W.r, W.zv)
-    setup._project(W.zv, dot=(W.r, 0, None))
+    setup._precond(W.r, W.zv, assemble=False)
+    setup._project(W.zv, dot=(W.r, 0, None), yb=setup.w_yb2)
     nat.call("bddc_axpby", ng, 1.0, _p(W.zv), 0.0, _p(W.p), _stream())
-    _pcg_core(setup, W, B)
+    _pcg_core(setup, W, B, cond)
 
 
-def _pcg_body(setup, W, B):
+def _pcg_body(setup, W, B, cond=None):
     """z = P M r; beta; p = z + beta p; next iteration (solver.py:222-227, 205-216)."""
     ng = setup.n_gamma
-    setup._precond(W.r, W.zv)
-    setup._project(W.zv, dot=(W.r, 3, B.betas))
+    setup._precond(W.r, W.zv, assemble=False)
+    setup._project(W.zv, dot=(W.r, 3, B.betas), yb=setup.w_yb2)
     nat.call("bddc_p_update", ng, _p(setup.w_scal), _p(W.zv), _p(W.p), _stream())
-    _pcg_core(setup, W, B)
+    _pcg_core(setup, W, B, cond)
 
 
 def _pcg_graph(setup, W, B, tol, maxit):
@@ -1518,12 +1537,11 @@ def _pcg_graph(setup, W, B, tol, maxit):
     nat.call("bddc_graph_begin", C.byref(state), st)
     try:
         c0 = lib.bddc_launch_count()
-        _pcg_first(setup, W, B)
-        nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        cond = (lib.bddc_graph_handle(state), tol, maxit)
+        _pcg_first(setup, W, B, cond)
         c1 = lib.bddc_launch_count()
         nat.call("bddc_graph_while", state, st)
-        _pcg_body(setup, W, B)
-        nat.call("bddc_pcg_cond", state, _p(setup.w_scal), float(tol), int(maxit), st)
+        _pcg_body(setup, W, B, cond)
         c2 = lib.bddc_launch_count()
         nat.call("bddc_graph_end", state, st)
     except Exception:

@@ -42,7 +42,7 @@ print(f"nd solve (graph) {gtime(lambda: nd.solve(r, x)):.1f} us, factor MB {nd.b
 ys, cb = nd._bufs()
 for li, L in enumerate(nd.levels):
     f = lambda: nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
-                         _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(nd._rs), _p(ys[li]), _p(cb), None, _stream())
+                         _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), None, None, 0, _p(nd._rs), _p(ys[li]), _p(cb), None, _stream())
     b = lambda: nat.call("bddc_nd_bwd", L.n_bt, L.bmax, L.wpr, _p(L.btasks), _p(L.info), _p(L.data_off),
                          _p(L.sep_flat), _p(L.bnd_flat), _p(L.Fc), _p(ys[li]), _p(x), _stream())
     tf = gtime(lambda: [f() for _ in range(10)]) / 10

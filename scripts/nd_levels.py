@@ -38,7 +38,7 @@ print(sys.argv[2:], "levels", len(nd.levels), "whole solve", round(timeit(lambda
 tot_bytes = 0
 for li, L in enumerate(nd.levels):
     fwd = lambda L=L, li=li: nat.call("bddc_nd_fwd", L.ysize, L.n_ft, L.smax, _p(L.ftasks), _p(L.info), _p(L.data_off),
-                                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), _p(nd._rs), _p(ys[li]),
+                                      _p(L.sep_flat), _p(L.lptr), _p(L.lsrc), _p(L.Fc), _p(r), None, None, 0, _p(nd._rs), _p(ys[li]),
                                       _p(cb), None, _stream())
     bwd = lambda L=L, li=li: nat.call("bddc_nd_bwd", L.n_bt, L.bmax, L.wpr, _p(L.btasks), _p(L.info), _p(L.data_off),
                                       _p(L.sep_flat), _p(L.bnd_flat), _p(L.Fc), _p(ys[li]), _p(x), _stream())

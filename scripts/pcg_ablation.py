@@ -26,9 +26,7 @@ def chain():
     ss = _stream()
     nat.call("bddc_gather_gemv_t", N, st.maxG, st.maxC, _p(st.d_nG), _p(st.d_nC), _p(st.d_gpos), _p(st.d_Psi),
              _p(W.r), _p(st.d_delta), _p(st.w_v), ss)
-    nat.call("bddc_coarse_restrict", st.nfc, _p(st.d_cown), _p(st.w_v), _p(st.w_rc), ss)
-    nat.call("bddc_fill", N, 0.0, _p(st.w_rc[st.nfc:]), ss)
-    st._coarse_solve()
+    st.nd.solve(None, st.w_xc, restricted=(st.w_v, st.d_cown))
 
 
 def tgemv():
@@ -63,6 +61,7 @@ pieces = {
     "S gemv": sgemv,
     "project": lambda: st._project(W.Ap),
     "project+dot": lambda: st._project(W.Ap, dot=(W.p, 100 + 15, None)),
+    "project+dot (from slots)": lambda: st._project(W.Ap, dot=(W.p, 100 + 15, None), yb=st.w_yb),
     "precond": lambda: st._precond(W.r, W.zv),
     "T gemv (t_grid_bulk)": tgemv,
     "T gemv (all SMs)": tgemv_full,
