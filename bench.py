@@ -353,7 +353,39 @@ def _iteration_roofline(setup, dec, pcg_s, its, peak):
             "timing": "PCG graph launches only (CUDA events), iterations of the timed steps"}
 
 
-def _factorisation_roofline(setup, dec, lib, nat, dev):
+def _spd_in_situ(rebuild, lib, peak):
+    """Every batched SPD inverse of one real setup (Ps, S_i, Kc, T_i, the ND pivot
+    blocks), timed in place by events on its own stream (bddc_spd_log_*): the
+    concurrent T_i branch shares the machine with the Kc / ND work, as in the setup."""
+    import numpy as np
+    import torch
+    lib.bddc_spd_log_enable(1)
+    try:
+        st = rebuild()
+        torch.cuda.synchronize()
+        buf = np.zeros(4 * 256)
+        n = lib.bddc_spd_log_read(buf.ctypes.data_as(__import__("ctypes").c_void_p), 256)
+    finally:
+        lib.bddc_spd_log_enable(0)
+    del st
+    calls = buf[:4 * max(n, 0)].reshape(-1, 4)
+    groups = {}
+    for nn, bt, fl, ms in calls:
+        k = f"{int(bt)}x{int(nn)}" + (" upper" if int(fl) & 1 else "")
+        gcount, gfl, gms = groups.get(k, (0, 0.0, 0.0))
+        groups[k] = (gcount + 1, gfl + bt * nn ** 3, gms + ms)
+    fl = float(sum(bt * nn ** 3 for nn, bt, _, _ in calls))
+    sec = float(calls[:, 3].sum()) / 1000.0 if len(calls) else 0.0
+    ach = fl / sec / 1e12 if sec else None
+    return {"calls": int(len(calls)), "flops": fl, "seconds": sec, "achieved": ach,
+            "frac": (ach / peak) if ach else None,
+            "by_shape": {k: {"calls": v[0], "ms": v[2], "tflops": v[1] / (v[2] / 1000.0) / 1e12}
+                         for k, v in groups.items()},
+            "timing": "events around each bddc_spd_inverse_batched_ex call of one setup, on the "
+                      "calling stream (T_i's branch runs concurrently with Kc / the ND pivots)"}
+
+
+def _factorisation_roofline(setup, dec, lib, nat, dev, rebuild=None):
     """Batched factorisations against the FP64 tensor pipe: the setup's
     three batched SPD inverses (Ps of the interior pressure Schur complements, S_i,
     T_i; Cholesky + triangular inverse + V V^T = n^3 flops per matrix) re-run on
@@ -417,7 +449,8 @@ def _factorisation_roofline(setup, dec, lib, nat, dev):
             "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
             "peak_kind": "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul fp64)",
             "flops": "n^3 per matrix (potrf n^3/3 + trtri n^3/3 + lauum n^3/3)",
-            "parts": parts, "traffic": None}
+            "parts": parts, "traffic": None,
+            "in_situ": _spd_in_situ(rebuild, lib, peak) if rebuild is not None else None}
 
 
 def _stencil_roofline(setup, g, nat, peak, dev, reps=10):
@@ -663,7 +696,8 @@ def main():
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
     }
-    line["factorisation_roofline"] = _factorisation_roofline(setup, dec, lib, nat, dev)
+    line["factorisation_roofline"] = _factorisation_roofline(setup, dec, lib, nat, dev,
+                                                             rebuild=lambda: B.BddcSetup(system, dec, cfg))
     line["stencil_roofline"] = _stencil_roofline(setup, g, nat, peak, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and c["dim"] == 2:
         vals, walls, detail, sample = reference_measured(c, k, 1, 0)

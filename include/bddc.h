@@ -94,6 +94,11 @@ size_t bddc_spd_inverse_workspace(int n, int batch, int b);
 void bddc_set_leaf_regs(int on);
 int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                              int* info, void* stream);
+/* In-situ timing log of the batched SPD inverses (bench's factorisation roofline
+ * from the setup's own calls): enable (clears the log), then read entries
+ * {n, batch, flags, ms} (events recorded on each call's stream). */
+void bddc_spd_log_enable(int on);
+int bddc_spd_log_read(double* out, int max_entries);
 /* flags & 1: the caller reads the upper triangle only (no lower mirror pass). */
 int bddc_spd_inverse_batched_ex(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                                 int* info, int flags, void* stream);

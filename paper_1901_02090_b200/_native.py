@@ -14,7 +14,7 @@ import subprocess
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbddc.so")
+LIB_PATH = os.environ.get("BDDC_LIB") or os.path.join(HERE, "libbddc.so")
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["capi.cu", "dense.cu", "local.cu", "adaptive.cu", "coarse.cu",
            "nd.cu", "pcg.cu", "stencil.cu", "graph.cu"]
@@ -88,6 +88,8 @@ _SIGS = {
     "bddc_dgemm_batched_dims": [_I, _I, _I, _I, _I, _D, _P, _I, _L, _P, _I, _L, _D,
                                 _P, _I, _L, _I, _I, _P, _I, _P],
     "bddc_spd_inverse_workspace": [_I, _I, _I],
+    "bddc_spd_log_enable": [_I],
+    "bddc_spd_log_read": [_P, _I],
     "bddc_spd_inverse_batched": [_P, _I, _I, _L, _I, _I, _P, _P, _P],
     "bddc_spd_inverse_batched_ex": [_P, _I, _I, _L, _I, _I, _P, _P, _I, _P],
     "bddc_cell_coeffs": [_GP, _P, _P, _P],
@@ -180,6 +182,7 @@ _RESTYPES = {
     "bddc_geom_size": C.c_size_t,
     "bddc_launch_count": C.c_ulonglong,
     "bddc_graph_handle": C.c_ulonglong,
+    "bddc_spd_log_enable": None,
     "bddc_last_error": C.c_char_p,
 }
 

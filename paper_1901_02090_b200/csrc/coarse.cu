@@ -27,6 +27,9 @@ extern "C" int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, 
                                         int* info, void* stream);
 
 #define PAIR_MMAX 112
+#ifndef KC_LEAF
+#define KC_LEAF 64   // leaf order of the Kc inverses (maxC = 160: 128 + 32 instead of five 32-leaves)
+#endif
 
 namespace {
 
@@ -202,7 +205,7 @@ extern "C" int bddc_coarse_local(const bddc_geom* g, const int* sub_rows, const 
     return r;
   pad_identity_kernel<<<N, 256, 0, s>>>(maxC, sub_rows, Kc);
   LAUNCH_OK();
-  if ((r = bddc_spd_inverse_batched(Kc, maxC, maxC, sCC, N, 32, inv_ws, info, stream))) return r;
+  if ((r = bddc_spd_inverse_batched(Kc, maxC, maxC, sCC, N, KC_LEAF, inv_ws, info, stream))) return r;
   if ((r = bddc_dgemm_batched_dims(0, 1, maxC, mg, maxC, 1.0, Kc, maxC, sCC, Y, maxC, sGC, 0.0, Psi, mg, sGC, N, 0, dCGC,
                                    16, stream)))
     return r;

@@ -106,7 +106,7 @@ template <bool transA, bool transB, bool aligned>
 __device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const double* __restrict__ A, int lda,
                                          const double* __restrict__ B, int ldb, int Ml, int Nl, int K, int m0,
                                          int n0, int kbeg, int kend, double (*As)[TILE_ELEMS],
-                                         double (*Bs)[TILE_ELEMS]) {
+                                         double (*Bs)[TILE_ELEMS], bool idle = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int g = lane >> 2, t = lane & 3;
@@ -131,6 +131,9 @@ __device__ __forceinline__ void tile_mma(double (&acc)[4][4][2], const double* _
     __syncthreads();
     const double* as = As[kt & 1];
     const double* bs = Bs[kt & 1];
+    // idle: this warp's 32x32 output lies strictly below the diagonal of an
+    // upper-only diagonal tile (it still stages and synchronises with the CTA)
+    if (!idle)
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[4], bf[4];
@@ -233,8 +236,11 @@ __global__ void __launch_bounds__(128) dgemm_kernel(int M, int N, int K, double 
   if (upper & 4) kend = min(kend, m0 + BM);      // op(A) lower: k <= m
   if (upper & 8) kend = min(kend, n0 + BN);      // op(B) upper: k <= n
   if (upper & 16) kbeg = max(kbeg, n0);          // op(B) lower: k >= n
-  tile_mma<transA, transB, aligned>(acc, A, lda, B, ldb, Ml, Nl, K, m0, n0, kbeg, kend, As, Bs);
-  tile_store(acc, C, ldc, M, N, m0, n0, alpha, beta);
+  // upper-only output: in a diagonal tile the warp at (32, 0) holds only strictly
+  // lower entries, which no caller of an upper-only product reads: no DMMA, no store
+  const bool idle = (upper & 1) && bm == bn && (threadIdx.x >> 5) == 2;
+  tile_mma<transA, transB, aligned>(acc, A, lda, B, ldb, Ml, Nl, K, m0, n0, kbeg, kend, As, Bs, idle);
+  if (!idle) tile_store(acc, C, ldc, M, N, m0, n0, alpha, beta);
 }
 
 // In-place triangular products (TRMM) of the SPD inverse, no scratch copy:
@@ -843,13 +849,71 @@ extern "C" int bddc_spd_inverse_batched(double* Mat, int n, int ld, long long sM
   return bddc_spd_inverse_batched_ex(Mat, n, ld, sM, batch, b, ws, info, 0, stream);
 }
 
+// In-situ timing log of every batched SPD inverse (bench: the setup's own
+// factorisation roofline).  Off by default; when on, each call records a pair of
+// events on its own stream (no synchronisation) and bddc_spd_log_read resolves them.
+namespace {
+struct SpdLogEntry {
+  int n, batch, flags;
+  cudaEvent_t e0, e1;
+};
+constexpr int SPD_LOG_MAX = 256;
+SpdLogEntry g_spd_log[SPD_LOG_MAX];
+int g_spd_log_n = 0;
+bool g_spd_log_on = false;
+}  // namespace
+
+extern "C" void bddc_spd_log_enable(int on) {
+  for (int k = 0; k < g_spd_log_n; ++k) {
+    cudaEventDestroy(g_spd_log[k].e0);
+    cudaEventDestroy(g_spd_log[k].e1);
+  }
+  g_spd_log_n = 0;
+  g_spd_log_on = on != 0;
+}
+
+// out[4k..4k+3] = {n, batch, flags, milliseconds}; returns the number of entries
+// (synchronises on each entry's end event).
+extern "C" int bddc_spd_log_read(double* out, int max_entries) {
+  int k = 0;
+  for (; k < g_spd_log_n && k < max_entries; ++k) {
+    float ms = 0.f;
+    CUDA_OK(cudaEventSynchronize(g_spd_log[k].e1));
+    CUDA_OK(cudaEventElapsedTime(&ms, g_spd_log[k].e0, g_spd_log[k].e1));
+    out[4 * k] = g_spd_log[k].n;
+    out[4 * k + 1] = g_spd_log[k].batch;
+    out[4 * k + 2] = g_spd_log[k].flags;
+    out[4 * k + 3] = ms;
+  }
+  return k;
+}
+
+static int spd_inverse_impl(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws, int* info,
+                            int flags, cudaStream_t s);
+
 // flags & 1: only the upper triangle of the result is wanted (no lower mirror;
 // the strict lower triangle is left undefined).
 extern "C" int bddc_spd_inverse_batched_ex(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws,
                                            int* info, int flags, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!g_spd_log_on || g_spd_log_n >= SPD_LOG_MAX || n <= 0 || batch <= 0)
+    return spd_inverse_impl(Mat, n, ld, sM, batch, b, ws, info, flags, s);
+  SpdLogEntry& e = g_spd_log[g_spd_log_n++];
+  e.n = n;
+  e.batch = batch;
+  e.flags = flags;
+  CUDA_OK(cudaEventCreate(&e.e0));
+  CUDA_OK(cudaEventCreate(&e.e1));
+  CUDA_OK(cudaEventRecord(e.e0, s));
+  const int r = spd_inverse_impl(Mat, n, ld, sM, batch, b, ws, info, flags, s);
+  CUDA_OK(cudaEventRecord(e.e1, s));
+  return r;
+}
+
+static int spd_inverse_impl(double* Mat, int n, int ld, long long sM, int batch, int b, void* ws, int* info,
+                            int flags, cudaStream_t s) {
   if (n <= 0 || batch <= 0) return 0;
   if (b <= 0 || b > 64) return bddc_set_error(BDDC_ERR_ARG, "spd_inverse: leaf size must be in 1..64");
-  cudaStream_t s = (cudaStream_t)stream;
   double* rest = (double*)ws;
   int r;
   if (n <= b) {
