@@ -41,11 +41,8 @@ __device__ __forceinline__ void decode_bnd(const bddc_geom& G, int d, int& side,
   gc[G.dir_axis] = side ? G.n[G.dir_axis] - 1 : 0;
 }
 
-// Row-structured launches, no integer division: thread (x, ty) of CTA
-// (bx, by, bz) handles element x (+ RX k) of grid row (f1, f2) = (RY bx + ty, by)
-// of family bz (flux operators; cells: bz = 0).  Consecutive threads touch
-// consecutive dofs, cells and (structure-of-arrays) coefficients.
-constexpr int RX = 64, RY = 4;
+// Row-structured operators: consecutive lanes touch consecutive dofs, cells and
+// (structure-of-arrays) coefficients of one grid row.
 
 // Row (f1, f2) of family a (interior faces, face coordinates): x-extent e0 and
 // the first dof d0; false outside the family.
@@ -60,36 +57,105 @@ __device__ __forceinline__ bool fam_row(const bddc_geom& G, int a, int r1, int r
   return true;
 }
 
-// y = alpha * A u + beta * y on the interior faces
-__global__ void __launch_bounds__(RX* RY) flux_A_kernel(bddc_geom G, const double* __restrict__ coef,
-                                                        const double* __restrict__ u, double alpha, double beta,
-                                                        double* __restrict__ y) {
-  const int a = blockIdx.z;
-  int e0, f[3], d0;
-  if (!fam_row(G, a, blockIdx.x * RY + threadIdx.y, blockIdx.y, e0, f, d0)) return;
-  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-  const double* ca = coef + (size_t)a * G.n_cells;
-  const int h0 = cell_id(G, f[0], f[1], f[2]);
-  const bool lo_in = f[a] > 1 || a == 0, hi_in = f[a] < G.n[a] - 1 || a == 0;   // along a (x: per element)
-  for (int x = threadIdx.x; x < e0; x += RX) {
-    const int d = d0 + x, hi = h0 + x, lo = hi - st;
-    const double clo = ca[lo], chi = ca[hi];
-    double v = G.a_diag * (clo + chi) * u[d];
-    const bool l = a == 0 ? x > 0 : lo_in, h = a == 0 ? x < e0 - 1 : hi_in;
-    // dof stride along a inside family a equals the cell stride st
-    double w = 0.0;
-    if (l) w += clo * u[d - st];
-    else if (a == G.dir_axis) {
-      int g[3] = {f[0] + x, f[1], f[2]};
-      w += clo * u[bnd_dof(G, 0, g)];
+// Flat row index R over the families' rows (family a: (n1 - [a==1]) x (n2 - [a==2])
+// rows, row-major in (r1, r2)); the launches are persistent-style grid-stride
+// loops over rows (a few CTAs per SM, ~10 rows per thread row) instead of one
+// short-lived CTA per four rows.
+__device__ __forceinline__ void flat_row(const bddc_geom& G, int R, int& a, int& r1, int& r2) {
+  for (a = 0; a < G.dim - 1; ++a) {
+    const int e1 = G.n[1] - (a == 1), e2 = (G.dim > 2) ? G.n[2] - (a == 2) : 1;
+    if (R < e1 * e2) break;
+    R -= e1 * e2;
+  }
+  const int e1 = G.n[1] - (a == 1);
+  r1 = R % e1;
+  r2 = R / e1;
+}
+
+// Warp-per-row launches: a warp takes one grid row at a time (row parameters are
+// warp-uniform: computed once per ~60 elements), its lanes cover x in steps of 32
+// with SX elements per lane whose loads are all issued before any is used; warps
+// stride over the rows of a grid that fills every SM (a few CTAs per SM).
+constexpr int ST = 256, SX = 2, RW = 2;   // threads, x per lane, rows per warp pass
+
+struct FluxRow {
+  int a, e0, d0, st, h0, fx, fy, fz;
+  bool lo_in, hi_in;
+};
+
+// row R of the flattened interior-face families
+__device__ __forceinline__ FluxRow flux_row(const bddc_geom& G, int R) {
+  FluxRow w;
+  int r1, r2, a;
+  flat_row(G, R, a, r1, r2);
+  w.a = a;
+  w.e0 = G.n[0] - (a == 0);
+  const int e1 = G.n[1] - (a == 1);
+  w.fx = (a == 0);
+  w.fy = r1 + (a == 1);
+  w.fz = r2 + (a == 2);
+  w.d0 = G.fam_off[a] + w.e0 * (r1 + e1 * r2);
+  w.st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+  w.h0 = cell_id(G, w.fx, w.fy, w.fz);
+  const int fa = a == 1 ? w.fy : w.fz, na = a == 1 ? G.n[1] : G.n[2];
+  w.lo_in = a == 0 || fa > 1;
+  w.hi_in = a == 0 || fa < na - 1;
+  return w;
+}
+
+// y = alpha * A u + beta * y on the interior faces (dof stride along a inside
+// family a equals the cell stride st; partners outside the family are predicated
+// off or, in mode B, the Dirichlet face)
+__global__ void __launch_bounds__(ST) flux_A_kernel(bddc_geom G, const double* __restrict__ coef,
+                                                    const double* __restrict__ u, double alpha, double beta,
+                                                    double* __restrict__ y, int nrows) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * ST) >> 5;
+  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
+    FluxRow r[RW];
+    int emax = 0;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      r[j] = flux_row(G, imin(R0 + j, nrows - 1));
+      if (R0 + j >= nrows) r[j].e0 = 0;
+      emax = imax(emax, r[j].e0);
     }
-    if (h) w += chi * u[d + st];
-    else if (a == G.dir_axis) {
-      int g[3] = {f[0] + x, f[1], f[2]};
-      w += chi * u[bnd_dof(G, 1, g)];
+    for (int x0 = 0; x0 < emax; x0 += 32 * SX) {
+      double clo[RW][SX], chi[RW][SX], u0[RW][SX], ul[RW][SX], uh[RW][SX];
+      int dd[RW][SX];
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          const FluxRow& w = r[j];
+          const int x = x0 + lane + 32 * k;
+          const bool act = x < w.e0;
+          const int d = w.d0 + x, hi = w.h0 + x;
+          dd[j][k] = act ? d : -1;
+          const bool l = w.a == 0 ? x > 0 : w.lo_in, h = w.a == 0 ? x < w.e0 - 1 : w.hi_in;
+          int dl = l ? d - w.st : -1, dh = h ? d + w.st : -1;
+          if (w.a == G.dir_axis && act && (!l || !h)) {
+            const int g[3] = {w.fx + x, w.fy, w.fz};
+            if (!l) dl = bnd_dof(G, 0, g);
+            if (!h) dh = bnd_dof(G, 1, g);
+          }
+          const double* ca = coef + (size_t)w.a * G.n_cells;
+          clo[j][k] = act ? __ldg(ca + hi - w.st) : 0.0;
+          chi[j][k] = act ? __ldg(ca + hi) : 0.0;
+          u0[j][k] = act ? __ldg(u + d) : 0.0;
+          ul[j][k] = (act && dl >= 0) ? __ldg(u + dl) : 0.0;
+          uh[j][k] = (act && dh >= 0) ? __ldg(u + dh) : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          if (dd[j][k] < 0) continue;
+          const double v = G.a_diag * (clo[j][k] + chi[j][k]) * u0[j][k] +
+                           G.a_off * (clo[j][k] * ul[j][k] + chi[j][k] * uh[j][k]);
+          y[dd[j][k]] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[dd[j][k]]);
+        }
     }
-    v += G.a_off * w;
-    y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
   }
 }
 
@@ -115,57 +181,105 @@ __global__ void flux_A_bnd_kernel(bddc_geom G, const double* __restrict__ coef, 
   y[d] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[d]);
 }
 
-// out_c = s_f * fvec_c + s_b * Dcell_c * (B u)_c   (Dcell = D of the cell's subdomain, or 1)
-__global__ void __launch_bounds__(RX* RY) cell_div_kernel(bddc_geom G, const double* __restrict__ u,
-                                                          const double* __restrict__ fvec, double s_f, double s_b,
-                                                          const int* __restrict__ cell_sub,
-                                                          const double* __restrict__ Dsub, double* __restrict__ out) {
-  const int y = blockIdx.x * RY + threadIdx.y, z = blockIdx.y;
-  if (y >= G.n[1] || z >= G.n[2]) return;
-  const int c0 = G.n[0] * (y + G.n[1] * z);
-  // first dofs of this row's faces: x-faces (x-1, y, z) and the y / z faces (x, ., .)
+// out_c = s_f * fvec_c + s_b * Dcell_c * (B u)_c   (Dcell = D of the cell's subdomain, or 1);
+// warp per cell row, the 2 dim face loads of each cell predicated and issued first
+__global__ void __launch_bounds__(ST) cell_div_kernel(bddc_geom G, const double* __restrict__ u,
+                                                      const double* __restrict__ fvec, double s_f, double s_b,
+                                                      const int* __restrict__ cell_sub,
+                                                      const double* __restrict__ Dsub, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * ST) >> 5;
+  const int nrows = G.n[1] * G.n[2];
   const int ex = G.n[0] - 1;
-  const int dx = G.fam_off[0] + ex * (y + G.n[1] * z) - 1;
-  const int dyl = G.fam_off[1] + G.n[0] * (y - 1 + (G.n[1] - 1) * z), dyh = dyl + G.n[0];
-  const int dzl = G.fam_off[2] + G.n[0] * (y + G.n[1] * (z - 1)), dzh = dzl + G.n[0] * G.n[1];
-  for (int x = threadIdx.x; x < G.n[0]; x += RX) {
-    const int c3[3] = {x, y, z};
-    double b = 0.0;
-    if (x > 0) b += u[dx + x];
-    else if (G.dir_axis == 0) b += u[bnd_dof(G, 0, c3)];
-    if (x < G.n[0] - 1) b -= u[dx + x + 1];
-    else if (G.dir_axis == 0) b -= u[bnd_dof(G, 1, c3)];
-    if (G.dim > 1) {
-      if (y > 0) b += u[dyl + x];
-      else if (G.dir_axis == 1) b += u[bnd_dof(G, 0, c3)];
-      if (y < G.n[1] - 1) b -= u[dyh + x];
-      else if (G.dir_axis == 1) b -= u[bnd_dof(G, 1, c3)];
+  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
+    for (int x0 = 0; x0 < G.n[0]; x0 += 32 * SX) {
+      double b[RW][SX], fv[RW][SX], D[RW][SX];
+      int cc[RW][SX];
+#pragma unroll
+      for (int j = 0; j < RW; ++j) {
+        const int R = imin(R0 + j, nrows - 1);
+        const int yy = R % G.n[1], z = R / G.n[1];
+        const int c0 = G.n[0] * (yy + G.n[1] * z);
+        const int dx0 = G.fam_off[0] + ex * (yy + G.n[1] * z) - 1;
+        const int dyl0 = G.fam_off[1] + G.n[0] * (yy - 1 + (G.n[1] - 1) * z);
+        const int dzl0 = G.fam_off[2] + G.n[0] * (yy + G.n[1] * (z - 1));
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          const int x = x0 + lane + 32 * k;
+          const bool act = x < G.n[0] && R0 + j < nrows;
+          const int c3[3] = {x, yy, z};
+          cc[j][k] = act ? c0 + x : -1;
+          int dlo[3] = {-1, -1, -1}, dhi[3] = {-1, -1, -1};
+          dlo[0] = x > 0 ? dx0 + x : (G.dir_axis == 0 ? bnd_dof(G, 0, c3) : -1);
+          dhi[0] = x < G.n[0] - 1 ? dx0 + x + 1 : (G.dir_axis == 0 ? bnd_dof(G, 1, c3) : -1);
+          if (G.dim > 1) {
+            dlo[1] = yy > 0 ? dyl0 + x : (G.dir_axis == 1 ? bnd_dof(G, 0, c3) : -1);
+            dhi[1] = yy < G.n[1] - 1 ? dyl0 + G.n[0] + x : (G.dir_axis == 1 ? bnd_dof(G, 1, c3) : -1);
+          }
+          if (G.dim > 2) {
+            dlo[2] = z > 0 ? dzl0 + x : (G.dir_axis == 2 ? bnd_dof(G, 0, c3) : -1);
+            dhi[2] = z < G.n[2] - 1 ? dzl0 + G.n[0] * G.n[1] + x : (G.dir_axis == 2 ? bnd_dof(G, 1, c3) : -1);
+          }
+          double sacc = 0.0;
+#pragma unroll
+          for (int a2 = 0; a2 < 3; ++a2) {
+            const double vl = (act && dlo[a2] >= 0) ? __ldg(u + dlo[a2]) : 0.0;
+            const double vh = (act && dhi[a2] >= 0) ? __ldg(u + dhi[a2]) : 0.0;
+            sacc += vl - vh;
+          }
+          b[j][k] = sacc;
+          fv[j][k] = (act && fvec) ? __ldg(fvec + c0 + x) : 0.0;
+          D[j][k] = (act && Dsub) ? __ldg(Dsub + __ldg(cell_sub + c0 + x)) : 1.0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          if (cc[j][k] < 0) continue;
+          double v = s_b * D[j][k] * b[j][k];
+          if (fvec) v += s_f * fv[j][k];
+          out[cc[j][k]] = v;
+        }
     }
-    if (G.dim > 2) {
-      if (z > 0) b += u[dzl + x];
-      else if (G.dir_axis == 2) b += u[bnd_dof(G, 0, c3)];
-      if (z < G.n[2] - 1) b -= u[dzh + x];
-      else if (G.dir_axis == 2) b -= u[bnd_dof(G, 1, c3)];
-    }
-    const int c = c0 + x;
-    const double D = Dsub ? Dsub[cell_sub[c]] : 1.0;
-    double v = s_b * D * b;
-    if (fvec) v += s_f * fvec[c];
-    out[c] = v;
   }
 }
 
-// y_d = alpha (p_hi - p_lo) + beta y_d on the interior faces
-__global__ void __launch_bounds__(RX* RY) grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha,
-                                                      double beta, double* __restrict__ y) {
-  const int a = blockIdx.z;
-  int e0, f[3], d0;
-  if (!fam_row(G, a, blockIdx.x * RY + threadIdx.y, blockIdx.y, e0, f, d0)) return;
-  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-  const int h0 = cell_id(G, f[0], f[1], f[2]);
-  for (int x = threadIdx.x; x < e0; x += RX) {
-    const int hi = h0 + x, d = d0 + x;
-    y[d] = alpha * (p[hi] - p[hi - st]) + (beta == 0.0 ? 0.0 : beta * y[d]);
+// y_d = alpha (p_hi - p_lo) + beta y_d on the interior faces (warp per row)
+__global__ void __launch_bounds__(ST) grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha,
+                                                  double beta, double* __restrict__ y, int nrows) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * ST) >> 5;
+  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
+    FluxRow r[RW];
+    int emax = 0;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      r[j] = flux_row(G, imin(R0 + j, nrows - 1));
+      if (R0 + j >= nrows) r[j].e0 = 0;
+      emax = imax(emax, r[j].e0);
+    }
+    for (int x0 = 0; x0 < emax; x0 += 32 * SX) {
+      double ph[RW][SX], pl[RW][SX];
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          const int x = x0 + lane + 32 * k;
+          const bool act = x < r[j].e0;
+          ph[j][k] = act ? __ldg(p + r[j].h0 + x) : 0.0;
+          pl[j][k] = act ? __ldg(p + r[j].h0 + x - r[j].st) : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < RW; ++j)
+#pragma unroll
+        for (int k = 0; k < SX; ++k) {
+          const int x = x0 + lane + 32 * k;
+          if (x >= r[j].e0) continue;
+          const int d = r[j].d0 + x;
+          y[d] = alpha * (ph[j][k] - pl[j][k]) + (beta == 0.0 ? 0.0 : beta * y[d]);
+        }
+    }
   }
 }
 
@@ -220,16 +334,30 @@ __global__ void sub_mean_kernel(long long n, const double* __restrict__ sum, dou
 }  // namespace
 
 namespace {
-// (n1 / RY, n2) covers every family's (e1, e2)
-dim3 row_grid(const bddc_geom* g, int fams) {
-  return dim3((g->n[1] + RY - 1) / RY, g->n[2], fams);
+// rows of the interior-face families (flux operators) or of the cells
+int flux_rows(const bddc_geom* g) {
+  int t = 0;
+  for (int a = 0; a < g->dim; ++a) t += (g->n[1] - (a == 1)) * ((g->dim > 2) ? g->n[2] - (a == 2) : 1);
+  return t;
+}
+// grid-stride launch: exactly the CTAs that are co-resident (one wave), never more
+// than the rows need
+template <typename K>
+dim3 row_grid(K kernel, int nrows) {
+  int dev = 0, nsm = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, ST, 0);
+  const int need = (nrows + RW * ST / 32 - 1) / (RW * ST / 32);
+  return dim3((unsigned)imax(1, imin(need, nsm * imax(occ, 1))));
 }
 }  // namespace
 
 extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double* u, double alpha, double beta,
                            double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  flux_A_kernel<<<row_grid(g, g->dim), dim3(RX, RY), 0, s>>>(*g, coef, u, alpha, beta, y);
+  const int nr = flux_rows(g);
+  flux_A_kernel<<<row_grid(flux_A_kernel, nr), ST, 0, s>>>(*g, coef, u, alpha, beta, y, nr);
   LAUNCH_OK();
   if (g->dir_axis >= 0 && g->n_bt > 0) {
     flux_A_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, coef, u, alpha, beta, y);
@@ -240,7 +368,8 @@ extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double*
 
 extern "C" int bddc_cell_div(const bddc_geom* g, const double* u, const double* fvec, double s_f, double s_b,
                              const int* cell_sub, const double* Dsub, double* out, void* stream) {
-  cell_div_kernel<<<row_grid(g, 1), dim3(RX, RY), 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b, cell_sub,
+  cell_div_kernel<<<row_grid(cell_div_kernel, g->n[1] * g->n[2]), ST, 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b,
+                                                                                           cell_sub,
                                                                               Dsub, out);
   LAUNCH_OK();
   return 0;
@@ -248,7 +377,8 @@ extern "C" int bddc_cell_div(const bddc_geom* g, const double* u, const double* 
 
 extern "C" int bddc_grad(const bddc_geom* g, const double* p, double alpha, double beta, double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  grad_kernel<<<row_grid(g, g->dim), dim3(RX, RY), 0, s>>>(*g, p, alpha, beta, y);
+  const int nr = flux_rows(g);
+  grad_kernel<<<row_grid(grad_kernel, nr), ST, 0, s>>>(*g, p, alpha, beta, y, nr);
   LAUNCH_OK();
   if (g->dir_axis >= 0 && g->n_bt > 0) {
     grad_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, p, alpha, beta, y);
