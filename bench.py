@@ -646,8 +646,11 @@ def main():
     alg_bytes = float(np.sum(8.0 * nG * (nG + 1) / 2 + 8.0 * nG * 2 + 4.0 * nG))
     peak, peak_kind = _peaks()
     achieved = alg_bytes / kmean / 1e9 if kdur else None
+    # ncu DRAM bytes of the same kernel on the same config (profiles/, from the
+    # --set full capture of scripts/prof_round2.sh)
+    kname = "symv_bulk_kernel" if setup.symv_bulk else "gather_symv_kernel"
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_gather_symv.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{kname}_c{args.config}.json")
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")
@@ -693,7 +696,7 @@ def main():
         "converged": True, "momentum_residual_rel": mom, "mass_residual_rel": mass,
         "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "roofline": {"bound": "hbm", "kernel": "gather_symv_kernel (interface Schur S_i x_i, packed symmetric tiles)",
+        "roofline": {"bound": "hbm", "kernel": f"{kname} (interface Schur S_i x_i, packed symmetric tiles)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
