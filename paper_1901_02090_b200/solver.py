@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import warnings
 from collections.abc import Mapping
 from dataclasses import dataclass
@@ -452,7 +453,7 @@ class BddcSetup:
         # 211 -> 208 us, PCG 1478 -> 1495 it/s); small subdomains (C4: maxG 160, 15
         # tiles) keep the one-CTA-per-subdomain LDG kernel, whose occupancy hides the
         # per-subdomain gather and epilogue (C4 PCG 1163 vs 1087 it/s with bulk)
-        self.symv_bulk = 256 <= dec.maxG <= 512
+        self.symv_bulk = {"1": True, "0": False}.get(os.environ.get("BDDC_SYMV_BULK", ""), 256 <= dec.maxG <= 512)
         # C3 (scripts/precond_tune.py, chunked tile classes): precond 399 us at 148
         # CTAs, 376 at 120, 354 at 100, 366 at 84; T alone 218 / 223 / 235 / 263 us
         self.t_grid_bulk = max(1, (self.n_sm * 2) // 3)
