@@ -95,7 +95,8 @@ void bddc_set_leaf_regs(int on);
 int bddc_spd_inverse_batched(double* M, int n, int ld, long long sM, int batch, int b, void* ws,
                              int* info, void* stream);
 /* In-situ timing log of the batched SPD inverses (bench's factorisation roofline
- * from the setup's own calls): enable (clears the log), then read entries
+ * from the setup's own calls, i.e. the factorisations replacing substructure.py:66
+ * and coarse.py:159, 196): enable (clears the log), then read entries
  * {n, batch, flags, ms} (events recorded on each call's stream). */
 void bddc_spd_log_enable(int on);
 int bddc_spd_log_read(double* out, int max_entries);
@@ -247,7 +248,8 @@ int bddc_scatter(int n_gamma, const int* gown, const double* yb, double* y, void
 /* Balanced projection (solver.py:166-179) as I - Phi^T (Phi Phi^T)^+ Phi. */
 int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const double* y,
              double* phi, void* stream);
-/* Same on the unassembled per-slot values yb (the scatter fused into the reads). */
+/* Same on the unassembled per-slot values yb (the scatter_add of solver.py:100-101
+ * fused into the reads; net_flux_matrix solver.py:132-144). */
 int bddc_phi_broken(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const int* gown,
                     const double* yb, double* phi, void* stream);
 int bddc_lap_solve(int S0, int S1, int S2, const double* eig, const double* dm, const double* phi,
@@ -355,8 +357,9 @@ int bddc_cg_update_dot(long long n, double* x, const double* p, double* r, const
 int bddc_cg_update_dot_cond(long long n, double* x, const double* p, double* r, const double* Ap,
                             void* ws, double* scal, int op, double* hist, unsigned long long cond,
                             double tol, int maxit, void* stream);
-/* Scatter fused into the projection: y = (yb[own0] + yb[own1]) - Phi^T z and the
- * dot x . y (yb: per-slot values, N x maxG, as written by the GEMV / prolongation). */
+/* Scatter fused into the projection (solver.py:100-101 + 166-179):
+ * y = (yb[own0] + yb[own1]) - Phi^T z and the PCG dot x . y (solver.py:205-222)
+ * (yb: per-slot values, N x maxG, as written by the GEMV / prolongation). */
 int bddc_proj_dot_broken(int n_gamma, int maxG, const int* gown, const double* yb, const double* z,
                          double* y, const double* x, void* ws, double* scal, int op, double* hist,
                          void* stream);
