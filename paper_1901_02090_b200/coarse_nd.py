@@ -184,13 +184,15 @@ def _merge_schedule(nodes, c):
         return [max(depth, 1)]
     if depth >= 15:
         # deep trees (C4: 15 separator levels) merge only two levels in the top two
-        # node levels and keep the remainder as its own bottom level: a 7-plane root
-        # front (4652 dofs at C4) makes the root GEMV bandwidth-bound and its
-        # factorisation dominate the setup (C4 coarse solve 281 -> 244 us with
-        # 2,2,3,3,3,2; scripts/nd_merge_sweep.sh)
+        # node levels (a 7-plane root front, 4652 dofs at C4, makes the root GEMV
+        # bandwidth-bound and its factorisation dominate the setup) and fold the
+        # remainder into the bottom group (C4 coarse solve 228 us with 2,2,3,3,3,2,
+        # 196 us with 2,2,3,3,5, setup coarse 70 -> 63 ms; scripts/nd_merge_sweep.sh)
         rest = depth - 4
         sched = [2, 2] + [c] * (rest // c)
-        return sched + ([rest % c] if rest % c else [])
+        if rest % c:
+            sched[-1] += rest % c
+        return sched
     sched = [c] * (depth // c)
     if depth % c:
         sched[-1] += depth % c
