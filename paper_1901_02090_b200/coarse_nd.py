@@ -32,6 +32,7 @@ x_pivot = y - X^T x_bnd (root -> leaves).
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -170,6 +171,8 @@ def _assign_pressures(nodes, dec, has_p):
 # solve's latency (C3 coarse solve 284 us binary, 192 us with 2, 166 us with 3,
 # 201 us with 4: the 3394-dof root front of 4 is bandwidth-bound).
 ND_MERGE = 3
+if os.environ.get("BDDC_ND_MERGE"):   # explicit per-level schedule, e.g. "3,4,6" (tuning)
+    ND_MERGE = [int(v) for v in os.environ["BDDC_ND_MERGE"].split(",")]
 
 
 def _merge_schedule(nodes, c):

@@ -199,3 +199,36 @@ def test_lap_solvers_agree(S3):
         nat.call("bddc_gemv", N, N, N, nat.ptr(Lp), nat.ptr(phi), nat.ptr(z3), st)
         torch.cuda.synchronize()
         assert torch.allclose(z1, z3, rtol=1e-11, atol=1e-11 * float(z1.abs().max()))
+
+
+def test_fused_scatter_projection_matches_unfused():
+    """bddc_phi_broken / bddc_proj_dot_broken (the scatter fused into the balanced
+    projection, solver.py:100-101 + 166-179) against scatter -> phi -> proj_dot:
+    bitwise equal projected vector and dot."""
+    import torch
+    import paper_1901_02090_b200 as B
+    from _golden import load
+    nat = _lib()
+    d = load("g3d_c3block")
+    g = B.build_grid(3, d["counts"], d["sizes"])
+    system = B.assemble_system(g, B.Permeability(d["k"]), B.Wells(0, g.n_cells - 1))
+    dec = B.regular_partition(g, d["splits"])
+    cfg = B.SolveConfig(tau=d["tau"], scaling=d["scaling"], constraints=d["mode"], tol=d["tol"])
+    st = B.BddcSetup(system, dec, cfg)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    yb = torch.randn(st.w_yb.numel(), dtype=torch.float64, device="cuda", generator=gen)
+    x = torch.randn(st.n_gamma, dtype=torch.float64, device="cuda", generator=gen)
+    res = []
+    for fused in (False, True):
+        st.w_yb.copy_(yb)
+        y = torch.empty(st.n_gamma, dtype=torch.float64, device="cuda")
+        if not fused:
+            nat.call("bddc_scatter", st.n_gamma, nat.ptr(st.d_gown), nat.ptr(st.w_yb), nat.ptr(y),
+                     C.c_void_p(torch.cuda.current_stream().cuda_stream))
+            st._project(y, dot=(x, 100 + 12, None))
+        else:
+            st._project(y, dot=(x, 100 + 12, None), yb=st.w_yb)
+        torch.cuda.synchronize()
+        res.append((y.clone(), float(st.w_scal[12])))
+    assert torch.equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
