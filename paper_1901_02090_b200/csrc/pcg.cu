@@ -148,18 +148,23 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
 //
 // One CTA per SM; subdomains are handed out by a global ticket counter.  Warp
 // roles (mbarrier-synchronised, no CTA-wide barrier after the prologue):
-//   gather   takes the ticket and stages win . x of the subdomain's interface
-//            slots into one of two x buffers (runs one subdomain ahead);
+//   gather   takes the ticket, stages win . x of the subdomain's interface
+//            slots into one of two x buffers (runs one subdomain ahead) and the
+//            subdomain's tile issue order;
 //   issuer   streams the subdomain's live packed 32x32 tiles with
 //            cp.async.bulk (TMA engine, no register staging) into a ring of
-//            SB_NST slots;
-//   8 consumers: the CTA's G-th tile (counted across subdomains) goes to warp
-//            G % 8 through slot G % SB_NST, so every slot has one consumer warp
-//            and its mbarrier phases are consumed in order; the warp multiplies
-//            the tile by x on both sides (row and, off the diagonal, column
-//            contribution) into its own accumulator of that subdomain buffer;
-//   epilogue sums the eight accumulators in warp order, writes y and frees the
-//            buffer.
+//            SB_NST slots, issue slot j = 8k + c carrying the k-th tile of
+//            chunk c (the live tiles in row-major order cut into 8 contiguous
+//            chunks);
+//   8 consumers: issue slot G (counted across subdomains) goes to warp G % 8
+//            through ring slot G % SB_NST, so every ring slot has one consumer
+//            warp and its mbarrier phases are consumed in order; a warp walks its
+//            chunk keeping the row contributions lane-partial in registers while
+//            the chunk stays in one tile row (one transposed reduction per row
+//            run), and adds the column contributions of off-diagonal tiles to the
+//            chunk's accumulator;
+//   epilogue sums the eight chunk accumulators in chunk order, writes y and
+//            frees the buffer.
 // Consumers never wait at subdomain boundaries; 128 KB of tiles are in flight
 // per SM, so a grid of fewer CTAs than SMs still saturates HBM and leaves SMs to
 // a concurrent coarse chain.  Results do not depend on which CTA takes which
@@ -171,32 +176,6 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
 #define SB_GATHER (SB_NCW + 1)
 #define SB_EPI (SB_NCW + 2)
 #define SB_TMAX 136   // live tiles of a 512-slot subdomain (16 * 17 / 2)
-
-__device__ __forceinline__ void tile_symv(const double* T, const double* xr, const double* xc, int lane,
-                                          double& rsum, double& csum) {
-  // rsum (lane l) = sum_c T[l][c] xc[c];  csum (lane l) = sum_r T[r][l] xr[r]
-  const double xl = xc[lane];
-  double v[32];
-  double col = 0.0;
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const double a = T[r * 32 + lane];
-    v[r] = a * xl;
-    col += a * xr[r];
-  }
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const bool up = lane & off;
-#pragma unroll
-    for (int k = 0; k < off; ++k) {
-      double send = up ? v[k] : v[k + off];
-      double recv = __shfl_xor_sync(0xffffffffu, send, off);
-      v[k] = (up ? v[k + off] : v[k]) + recv;
-    }
-  }
-  rsum = v[0];
-  csum = col;
-}
 
 // lane l returns sum over lanes of v[l] (31-shuffle transposed reduction; v is consumed)
 __device__ __forceinline__ double lane_transpose_sum(double (&v)[32], int lane) {
