@@ -648,7 +648,8 @@ def main():
     achieved = alg_bytes / kmean / 1e9 if kdur else None
     # ncu DRAM bytes of the same kernel on the same config (profiles/, from the
     # --set full capture of scripts/prof_round2.sh)
-    kname = "symv_bulk_kernel" if setup.symv_bulk else "gather_symv_kernel"
+    kname = ("symv_bulk_kernel" if setup.symv_bulk else
+             "gather_symv16_kernel" if getattr(setup, "tile16", False) else "gather_symv_kernel")
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{kname}_c{args.config}.json")
     if os.path.exists(tp):

@@ -233,6 +233,12 @@ size_t bddc_sym_packed_elems(int maxG);
 int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream);
 int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
                      const double* x, const double* win, double* yb, int grid, void* stream);
+/* 16 x 16-tile variant for small subdomains (maxG <= 256, a multiple of 16): the
+ * packed bytes follow the live triangle more closely than 32-tiles. */
+size_t bddc_sym_packed16_elems(int maxG);
+int bddc_pack_sym16(int N, int maxG, const double* full, double* packed, void* stream);
+int bddc_gather_symv16(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                       const double* x, const double* win, double* yb, int grid, void* stream);
 /* v_i = Psi_i^T (win .* gather(x)) (coarse.py:225-235 weighted_restriction); PsiT is
  * stored maxC x maxG per subdomain. */
 int bddc_gather_gemv_t(int N, int maxG, int maxC, const int* nG, const int* nC, const int* gpos,

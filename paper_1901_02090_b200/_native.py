@@ -125,6 +125,9 @@ _SIGS = {
     "bddc_gather_gemv": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "bddc_sym_packed_elems": [_I],
     "bddc_pack_sym": [_I, _I, _P, _P, _P],
+    "bddc_sym_packed16_elems": [_I],
+    "bddc_pack_sym16": [_I, _I, _P, _P, _P],
+    "bddc_gather_symv16": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P],
     "bddc_gather_symv": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P],
     "bddc_gather_symv_bulk": [_I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P],
     "bddc_gather_gemv_t": [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
@@ -179,6 +182,7 @@ _RESTYPES = {
     "bddc_pair_scratch_bytes": C.c_size_t,
     "bddc_dot_workspace": C.c_size_t,
     "bddc_sym_packed_elems": C.c_size_t,
+    "bddc_sym_packed16_elems": C.c_size_t,
     "bddc_geom_size": C.c_size_t,
     "bddc_launch_count": C.c_ulonglong,
     "bddc_graph_handle": C.c_ulonglong,

@@ -142,6 +142,107 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
   }
 }
 
+// Small subdomains (maxG <= 256, C4: <= 150 live slots): 16 x 16 tiles, so the
+// packed bytes follow the live triangle closely (C4: 92 KB vs 123 KB with 32-tiles
+// for the 81 KB algorithmic n(n+1)/2).  Each warp takes two tiles at a time, one
+// per half-warp (lane = tile column): 16 coalesced 128-byte row loads per half,
+// the row contribution by a 15-shuffle transposed reduction inside the half, the
+// column contribution in registers; partials combined per output in fixed order.
+__device__ __forceinline__ int tile_index16(int bi, int bj, int nt) { return bi * nt - (bi * (bi - 1)) / 2 + (bj - bi); }
+
+__global__ void pack_sym16_kernel(int maxG, const double* __restrict__ full, double* __restrict__ packed) {
+  const int i = blockIdx.y;
+  const int nt = maxG / 16;
+  const int ntiles = nt * (nt + 1) / 2;
+  const double* F = full + (size_t)i * maxG * maxG;
+  double* Pk = packed + (size_t)i * ntiles * 256;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)ntiles * 256;
+       e += (long long)gridDim.x * blockDim.x) {
+    int t = (int)(e / 256), w = (int)(e % 256);
+    int bi = 0;
+    while (bi + 1 < nt && tile_index16(bi + 1, bi + 1, nt) <= t) ++bi;
+    int bj = bi + (t - tile_index16(bi, bi, nt));
+    int r = bi * 16 + w / 16, c = bj * 16 + w % 16;
+    Pk[e] = (r <= c) ? F[(size_t)r * maxG + c] : F[(size_t)c * maxG + r];
+  }
+}
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) gather_symv16_kernel(int N, int maxG, const int* __restrict__ nG,
+                                                           const int* __restrict__ gpos,
+                                                           const double* __restrict__ packed,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ win, double* __restrict__ yb) {
+  extern __shared__ double sm[];
+  for (int i = blockIdx.x; i < N; i += gridDim.x) {
+    const int n = nG[i];
+    const int nt = maxG / 16;
+    const int ntl = (n + 15) / 16;
+    const int ntiles = nt * (nt + 1) / 2;
+    double* xs = sm;                         // maxG
+    double* rowp = xs + maxG;                // ntiles x 16
+    double* colp = rowp + (size_t)ntiles * 16;
+    __syncthreads();
+    for (int c = threadIdx.x; c < ntl * 16; c += blockDim.x) {
+      double v = 0.0;
+      if (c < n) {
+        v = x[gpos[(size_t)i * maxG + c]];
+        if (win) v *= win[(size_t)i * maxG + c];
+      }
+      xs[c] = v;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int h = lane >> 4, l = lane & 15;
+    const double* Pk = packed + (size_t)i * ntiles * 256;
+    const int nlive = ntl * (ntl + 1) / 2;
+    for (int u0 = 2 * warp; u0 < nlive; u0 += 2 * nw) {
+      const int u = u0 + h;
+      const bool act = u < nlive;
+      int bi = 0, rem = act ? u : 0;
+      while (rem >= ntl - bi) {
+        rem -= ntl - bi;
+        ++bi;
+      }
+      const int bj = bi + rem;
+      const double* T = Pk + (size_t)tile_index16(bi, bj, nt) * 256;
+      const double xl = xs[bj * 16 + l];
+      double v[16];
+      double col = 0.0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const double a = act ? __ldg(T + r * 16 + l) : 0.0;
+        v[r] = a * xl;
+        col += a * xs[bi * 16 + r];
+      }
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) {
+        const bool up = l & off;
+#pragma unroll
+        for (int k = 0; k < off; ++k) {
+          const double send = up ? v[k] : v[k + off];
+          const double recv = __shfl_xor_sync(0xffffffffu, send, off);
+          v[k] = (up ? v[k + off] : v[k]) + recv;
+        }
+      }
+      if (act) {
+        const int t = tile_index16(bi, bj, nt);
+        rowp[(size_t)t * 16 + l] = v[0];
+        colp[(size_t)t * 16 + l] = (bi != bj) ? col : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < ntl * 16; e += blockDim.x) {
+      const int b = e / 16, ll = e % 16;
+      if (e >= n) continue;
+      double acc = 0.0;
+      for (int bj = b; bj < ntl; ++bj) acc += rowp[(size_t)tile_index16(b, bj, nt) * 16 + ll];
+      for (int bi = 0; bi < b; ++bi) acc += colp[(size_t)tile_index16(bi, b, nt) * 16 + ll];
+      yb[(size_t)i * maxG + e] = acc;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Persistent bulk-streamed symmetric GEMV (the interface operator S_i and the
 // preconditioner's T_i, solver.py:103-107 / coarse.py:237-245).
@@ -1041,6 +1142,30 @@ extern "C" int bddc_gather_gemv(int N, int maxG, const int* nG, const int* gpos,
 extern "C" size_t bddc_sym_packed_elems(int maxG) {
   int nt = maxG / 32;
   return (size_t)nt * (nt + 1) / 2 * 1024;
+}
+
+extern "C" size_t bddc_sym_packed16_elems(int maxG) {
+  int nt = maxG / 16;
+  return (size_t)nt * (nt + 1) / 2 * 256;
+}
+extern "C" int bddc_pack_sym16(int N, int maxG, const double* full, double* packed, void* stream) {
+  if (maxG % 16) return bddc_set_error(BDDC_ERR_ARG, "pack_sym16: maxG must be a multiple of 16");
+  dim3 g(64, N);
+  pack_sym16_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(maxG, full, packed);
+  LAUNCH_OK();
+  return 0;
+}
+extern "C" int bddc_gather_symv16(int N, int maxG, const int* nG, const int* gpos, const double* packed,
+                                  const double* x, const double* win, double* yb, int grid, void* stream) {
+  if (maxG % 16) return bddc_set_error(BDDC_ERR_ARG, "gather_symv16: maxG must be a multiple of 16");
+  const int nt = maxG / 16;
+  const size_t shm = ((size_t)maxG + (size_t)nt * (nt + 1) * 16) * sizeof(double);
+  if (shm > 48 * 1024)
+    CUDA_OK(cudaFuncSetAttribute(gather_symv16_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  if (grid <= 0 || grid > N) grid = N;
+  gather_symv16_kernel<256><<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
+  LAUNCH_OK();
+  return 0;
 }
 
 extern "C" int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream) {

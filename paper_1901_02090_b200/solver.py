@@ -368,8 +368,14 @@ class BddcSetup:
         # T_i (its batched inverse) on a side stream with its own workspaces, concurrently
         # with Kc / Psi / b0 and then the global coarse factorisation (the critical
         # path: host symbolic analysis, latency-bound small-batch inverses)
+        # small subdomains (LDG GEMV, maxG < 256) pack S_i in 16 x 16 tiles (the packed
+        # bytes follow the live triangle: C4 S GEMV 186 -> 165 us); T_i keeps 32-tiles,
+        # whose fewer, larger tiles suit the one-CTA-per-SM launch beside the coarse chain
+        self.tile16 = (mg < 256 and mg % 16 == 0 and os.environ.get("BDDC_TILE16", "1") != "0"
+                       and os.environ.get("BDDC_SYMV_BULK", "") != "1")
         npk = nat.load().bddc_sym_packed_elems(mg)
-        self.d_Sp = torch.empty(N * npk, dtype=F64, device=dev)
+        npk16 = nat.load().bddc_sym_packed16_elems(mg) if self.tile16 else npk
+        self.d_Sp = torch.empty(N * npk16, dtype=F64, device=dev)
         self.d_Tp = torch.empty(N * npk, dtype=F64, device=dev)
         Ct2 = torch.empty(N * mg * maxC, dtype=F64, device=dev)
         Y2 = torch.empty(N * mg * maxC, dtype=F64, device=dev)
@@ -387,7 +393,8 @@ class BddcSetup:
             nat.call("bddc_pack_sym", N, mg, _p(self.d_T), _p(self.d_Tp), ss)
         nat.call("bddc_coarse_local", *cl_args, 1, st)
         # tile-packed symmetric S_i, T_i for the PCG loop (half the bytes of full storage)
-        nat.call("bddc_pack_sym", N, mg, _p(self.d_S), _p(self.d_Sp), st)
+        nat.call("bddc_pack_sym16" if self.tile16 else "bddc_pack_sym", N, mg, _p(self.d_S),
+                 _p(self.d_Sp), st)
         self._mark(ev, "coarse_local")
         # global coarse: multifrontal S_Pi (nested dissection) + pinned pressure Schur Pc
         nfc = self.n_flux_coarse
@@ -748,6 +755,9 @@ class BddcSetup:
         if self.symv_bulk:
             nat.call("bddc_gather_symv_bulk", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                      _p(mats), _p(x), _p(win), _p(yb), grid, _p(self._sched[2 * site:]), st)
+        elif self.tile16 and mats is self.d_Sp:
+            nat.call("bddc_gather_symv16", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
+                     _p(mats), _p(x), _p(win), _p(yb), grid, st)
         else:
             nat.call("bddc_gather_symv", self.N, self.maxG, _p(self.d_nG), _p(self.d_gpos),
                      _p(mats), _p(x), _p(win), _p(yb), grid, st)
@@ -788,15 +798,16 @@ class BddcSetup:
     def schur_dense(self, i):
         """Dense S_i (n_Gamma_i x n_Gamma_i), substructure.py:90-99 (unpacked from tiles)."""
         n = int(self.dec.nG[i])
-        nt = self.maxG // 32
-        npk = nt * (nt + 1) // 2 * 1024
-        tiles = self.d_Sp[i * npk:(i + 1) * npk].view(-1, 32, 32).cpu().numpy()
+        ts = 16 if self.tile16 else 32
+        nt = self.maxG // ts
+        npk = nt * (nt + 1) // 2 * ts * ts
+        tiles = self.d_Sp[i * npk:(i + 1) * npk].view(-1, ts, ts).cpu().numpy()
         full = np.zeros((self.maxG, self.maxG))
         t = 0
         for bi in range(nt):
             for bj in range(bi, nt):
-                full[bi * 32:(bi + 1) * 32, bj * 32:(bj + 1) * 32] = tiles[t]
-                full[bj * 32:(bj + 1) * 32, bi * 32:(bi + 1) * 32] = tiles[t].T
+                full[bi * ts:(bi + 1) * ts, bj * ts:(bj + 1) * ts] = tiles[t]
+                full[bj * ts:(bj + 1) * ts, bi * ts:(bi + 1) * ts] = tiles[t].T
                 t += 1
         return full[:n, :n]
 
