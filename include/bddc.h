@@ -233,6 +233,8 @@ size_t bddc_sym_packed_elems(int maxG);
 int bddc_pack_sym(int N, int maxG, const double* full, double* packed, void* stream);
 int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
                      const double* x, const double* win, double* yb, int grid, void* stream);
+/* Tuning knob: subdomains taken at a time per CTA by the grid-stride launch (1, 2, 4). */
+void bddc_set_symv_groups(int g);
 /* 16 x 16-tile variant for small subdomains (maxG <= 256, a multiple of 16): the
  * packed bytes follow the live triangle more closely than 32-tiles. */
 size_t bddc_sym_packed16_elems(int maxG);

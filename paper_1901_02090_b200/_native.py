@@ -151,6 +151,7 @@ _SIGS = {
     "bddc_set_gemv_wpr": [_I],
     "bddc_set_leaf_regs": [_I],
     "bddc_set_symv_threads": [_I],
+    "bddc_set_symv_groups": [_I],
     "bddc_set_pair_threads": [_I],
     "bddc_set_prolong_direct": [_I],
     "bddc_lap_dense": [_I, _I, _I, _P, _P, _P, _P, _P],
@@ -186,6 +187,7 @@ _RESTYPES = {
     "bddc_geom_size": C.c_size_t,
     "bddc_launch_count": C.c_ulonglong,
     "bddc_graph_handle": C.c_ulonglong,
+    "bddc_set_symv_groups": None,
     "bddc_spd_log_enable": None,
     "bddc_last_error": C.c_char_p,
 }

@@ -68,77 +68,81 @@ __global__ void pack_sym_kernel(int maxG, const double* __restrict__ full, doubl
 // Each warp streams whole tiles (coalesced rows), forms the column contribution in
 // registers and the row contribution with a 31-shuffle transpose-reduction; per-tile
 // partials are combined per output block in a fixed order (deterministic).
-template <int MAXT>
+template <int MAXT, int G>
 __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, const int* __restrict__ nG,
                                                          const int* __restrict__ gpos,
                                                          const double* __restrict__ packed,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ win, double* __restrict__ yb) {
   extern __shared__ double sm[];
-  // grid-stride over subdomains: a grid smaller than N leaves SM room for the
-  // concurrently running coarse chain
-  for (int i = blockIdx.x; i < N; i += gridDim.x) {
-  const int n = nG[i];
   const int nt = maxG / 32;
-  const int ntl = (n + 31) / 32;
   const int ntiles = nt * (nt + 1) / 2;
-  double* xs = sm;                       // maxG
-  double* rowp = xs + maxG;              // ntiles x 32
-  double* colp = rowp + (size_t)ntiles * 32;  // ntiles x 32
-  __syncthreads();
-  for (int c = threadIdx.x; c < ntl * 32; c += blockDim.x) {
-    double v = 0.0;
-    if (c < n) {
-      v = x[gpos[(size_t)i * maxG + c]];
-      if (win) v *= win[(size_t)i * maxG + c];
-    }
-    xs[c] = v;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* Pk = packed + (size_t)i * ntiles * 1024;
-  const int nlive = ntl * (ntl + 1) / 2;
-  for (int u = warp; u < nlive; u += nw) {
-    // enumerate live tiles (bi <= bj < ntl) in row-major order
-    int bi = 0, rem = u;
-    while (rem >= ntl - bi) {
-      rem -= ntl - bi;
-      ++bi;
-    }
-    const int bj = bi + rem;
-    const double* T = Pk + (size_t)tile_index(bi, bj, nt) * 1024;
-    const double xl = xs[bj * 32 + lane];
-    double v[32];
-    double col = 0.0;
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      double a = T[r * 32 + lane];
-      v[r] = a * xl;
-      col += a * xs[bi * 32 + r];
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      const bool up = lane & off;
-#pragma unroll
-      for (int k = 0; k < off; ++k) {
-        double send = up ? v[k] : v[k + off];
-        double recv = __shfl_xor_sync(0xffffffffu, send, off);
-        v[k] = (up ? v[k + off] : v[k]) + recv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // G groups of warps take G subdomains at a time (the grid-stride launch beside the
+  // coarse chain, one CTA per SM: more subdomains, and loads, in flight per CTA)
+  const int gw = (blockDim.x >> 5) / G, grp = warp / gw, wl = warp % gw;
+  const int gt = threadIdx.x - grp * gw * 32, gthreads = gw * 32;
+  double* xs = sm + (size_t)grp * (maxG + (size_t)ntiles * 64);   // maxG
+  double* rowp = xs + maxG;                                        // ntiles x 32
+  double* colp = rowp + (size_t)ntiles * 32;                       // ntiles x 32
+  for (int i0 = blockIdx.x * G; i0 < N; i0 += gridDim.x * G) {
+    const int i = i0 + grp;
+    const bool act = i < N;
+    const int n = act ? nG[i] : 0;
+    const int ntl = (n + 31) / 32;
+    __syncthreads();
+    for (int c = gt; c < ntl * 32; c += gthreads) {
+      double v = 0.0;
+      if (c < n) {
+        v = x[gpos[(size_t)i * maxG + c]];
+        if (win) v *= win[(size_t)i * maxG + c];
       }
+      xs[c] = v;
     }
-    const int t = tile_index(bi, bj, nt);
-    rowp[(size_t)t * 32 + lane] = v[0];
-    colp[(size_t)t * 32 + lane] = (bi != bj) ? col : 0.0;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < ntl * 32; e += blockDim.x) {
-    const int b = e / 32, l = e % 32;
-    if (e >= n) continue;
-    double acc = 0.0;
-    for (int bj = b; bj < ntl; ++bj) acc += rowp[(size_t)tile_index(b, bj, nt) * 32 + l];
-    for (int bi = 0; bi < b; ++bi) acc += colp[(size_t)tile_index(bi, b, nt) * 32 + l];
-    yb[(size_t)i * maxG + e] = acc;
-  }
+    __syncthreads();
+    const double* Pk = packed + (size_t)(act ? i : 0) * ntiles * 1024;
+    const int nlive = ntl * (ntl + 1) / 2;
+    for (int u = wl; u < nlive; u += gw) {
+      // enumerate live tiles (bi <= bj < ntl) in row-major order
+      int bi = 0, rem = u;
+      while (rem >= ntl - bi) {
+        rem -= ntl - bi;
+        ++bi;
+      }
+      const int bj = bi + rem;
+      const double* T = Pk + (size_t)tile_index(bi, bj, nt) * 1024;
+      const double xl = xs[bj * 32 + lane];
+      double v[32];
+      double col = 0.0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        double a = T[r * 32 + lane];
+        v[r] = a * xl;
+        col += a * xs[bi * 32 + r];
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        const bool up = lane & off;
+#pragma unroll
+        for (int k = 0; k < off; ++k) {
+          double send = up ? v[k] : v[k + off];
+          double recv = __shfl_xor_sync(0xffffffffu, send, off);
+          v[k] = (up ? v[k + off] : v[k]) + recv;
+        }
+      }
+      const int t = tile_index(bi, bj, nt);
+      rowp[(size_t)t * 32 + lane] = v[0];
+      colp[(size_t)t * 32 + lane] = (bi != bj) ? col : 0.0;
+    }
+    __syncthreads();
+    for (int e = gt; e < ntl * 32; e += gthreads) {
+      const int b = e / 32, l = e % 32;
+      if (e >= n) continue;
+      double acc = 0.0;
+      for (int bj = b; bj < ntl; ++bj) acc += rowp[(size_t)tile_index(b, bj, nt) * 32 + l];
+      for (int bi = 0; bi < b; ++bi) acc += colp[(size_t)tile_index(bi, b, nt) * 32 + l];
+      yb[(size_t)i * maxG + e] = acc;
+    }
   }
 }
 
@@ -1179,20 +1183,35 @@ extern "C" int bddc_pack_sym(int N, int maxG, const double* full, double* packed
 static int g_symv_threads = 256;
 extern "C" void bddc_set_symv_threads(int t) { g_symv_threads = (t == 512) ? 512 : 256; }
 
+static int g_symv_groups = 4;   // C4 precond beside the chain: 462 us (1), 430 (2), 426 (4)
+extern "C" void bddc_set_symv_groups(int g) { g_symv_groups = (g == 1 || g == 2) ? g : 4; }
+
 extern "C" int bddc_gather_symv(int N, int maxG, const int* nG, const int* gpos, const double* packed,
                                 const double* x, const double* win, double* yb, int grid, void* stream) {
   int nt = maxG / 32;
-  size_t shm = ((size_t)maxG + (size_t)nt * (nt + 1) * 32) * sizeof(double);
-  if (shm > 48 * 1024)
-    for (auto k : {gather_symv_kernel<256>, gather_symv_kernel<512>})
-      CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  const size_t per = ((size_t)maxG + (size_t)nt * (nt + 1) * 32) * sizeof(double);
   if (grid <= 0 || grid > N) grid = N;
-  // the grid-stride launch (T_i beside the coarse chain: one CTA per SM) may want
-  // more loads in flight per CTA than one CTA per subdomain
-  if (grid < N && g_symv_threads == 512)
-    gather_symv_kernel<512><<<grid, 512, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
-  else
-    gather_symv_kernel<256><<<grid, 256, shm, (cudaStream_t)stream>>>(N, maxG, nG, gpos, packed, x, win, yb);
+  // the grid-stride launch (T_i beside the coarse chain: one CTA per SM) takes
+  // g_symv_groups subdomains at a time per CTA (more loads in flight per CTA)
+  const int G = (grid < N) ? g_symv_groups : 1;
+  const size_t shm = per * G;
+  cudaStream_t s = (cudaStream_t)stream;
+#define SYMV_CASE(T, GG)                                                                              \
+  do {                                                                                                \
+    if (shm > 48 * 1024)                                                                              \
+      CUDA_OK(cudaFuncSetAttribute(gather_symv_kernel<T, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
+    gather_symv_kernel<T, GG><<<grid, T, shm, s>>>(N, maxG, nG, gpos, packed, x, win, yb);            \
+  } while (0)
+  if (grid < N && g_symv_threads == 512) {
+    if (G == 4) SYMV_CASE(512, 4);
+    else if (G == 2) SYMV_CASE(512, 2);
+    else SYMV_CASE(512, 1);
+  } else {
+    if (G == 4) SYMV_CASE(256, 4);
+    else if (G == 2) SYMV_CASE(256, 2);
+    else SYMV_CASE(256, 1);
+  }
+#undef SYMV_CASE
   LAUNCH_OK();
   return 0;
 }

@@ -8,6 +8,9 @@ import paper_1901_02090_b200 as B
 from paper_1901_02090_b200 import fields
 
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+if os.environ.get("SYMV_GROUPS"):   # subdomains per CTA of the grid-stride LDG GEMV
+    from paper_1901_02090_b200 import _native as _nat
+    _nat.load().bddc_set_symv_groups(int(os.environ["SYMV_GROUPS"]))
 c = fields.CONFIGS[cid]
 g = B.build_grid(3, c["counts"], c["sizes"])
 dec = B.regular_partition(g, c["splits"])
