@@ -11,6 +11,8 @@
 // Mode B (G.dir_axis >= 0): the boundary faces of that axis are dofs numbered
 // after the interior ones (bnd_dof), B B^T p = B(g - A u) has Dirichlet ends
 // along it (a DST-I basis there) and no null space.
+#include <cstdlib>
+
 #include "common.cuh"
 
 extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, double alpha, const double* A,
@@ -18,16 +20,6 @@ extern "C" int bddc_dgemm_batched(int transA, int transB, int M, int N, int K, d
                                   double* C, int ldc, long long sC, int batch, int upper, void* stream);
 
 namespace {
-
-__device__ __forceinline__ void decode_dof(const bddc_geom& G, int d, int& a, int f[3]) {
-  a = (d >= G.fam_off[1]) + (d >= G.fam_off[2]);
-  int r = d - G.fam_off[a];
-  int e0 = G.n[0] - (a == 0), e1 = G.n[1] - (a == 1);
-  f[0] = r % e0;
-  f[1] = (r / e0) % e1;
-  f[2] = r / (e0 * e1);
-  f[a] += 1;  // face coordinate along a in 1..n_a-1
-}
 
 // Mode B boundary dof d >= n_flux_int -> end (side) and the adjacent cell's coordinates.
 __device__ __forceinline__ void decode_bnd(const bddc_geom& G, int d, int& side, int gc[3]) {
@@ -41,121 +33,121 @@ __device__ __forceinline__ void decode_bnd(const bddc_geom& G, int d, int& side,
   gc[G.dir_axis] = side ? G.n[G.dir_axis] - 1 : 0;
 }
 
-// Row-structured operators: consecutive lanes touch consecutive dofs, cells and
-// (structure-of-arrays) coefficients of one grid row.
+// Flat operators: each family's dofs (and the cells) are one contiguous range;
+// a CTA takes a block-uniform family and ST x SV consecutive entries of it, a
+// thread SV entries ST apart (every warp access is 32 consecutive doubles), all
+// loads of its SV entries issued before any is used.  Coordinates come from
+// multiply-high divisions by the grid extents (FDiv, set up on the host).
+constexpr int ST = 256;
 
-// Row (f1, f2) of family a (interior faces, face coordinates): x-extent e0 and
-// the first dof d0; false outside the family.
-__device__ __forceinline__ bool fam_row(const bddc_geom& G, int a, int r1, int r2, int& e0, int f[3], int& d0) {
-  e0 = G.n[0] - (a == 0);
-  const int e1 = G.n[1] - (a == 1), e2 = (G.dim > 2) ? G.n[2] - (a == 2) : 1;
-  if (r1 >= e1 || r2 >= e2) return false;
-  f[0] = (a == 0);
-  f[1] = r1 + (a == 1);
-  f[2] = r2 + (a == 2);
-  d0 = G.fam_off[a] + e0 * (r1 + e1 * r2);
-  return true;
-}
-
-// Flat row index R over the families' rows (family a: (n1 - [a==1]) x (n2 - [a==2])
-// rows, row-major in (r1, r2)); the launches are persistent-style grid-stride
-// loops over rows (a few CTAs per SM, ~10 rows per thread row) instead of one
-// short-lived CTA per four rows.
-__device__ __forceinline__ void flat_row(const bddc_geom& G, int R, int& a, int& r1, int& r2) {
-  for (a = 0; a < G.dim - 1; ++a) {
-    const int e1 = G.n[1] - (a == 1), e2 = (G.dim > 2) ? G.n[2] - (a == 2) : 1;
-    if (R < e1 * e2) break;
-    R -= e1 * e2;
-  }
-  const int e1 = G.n[1] - (a == 1);
-  r1 = R % e1;
-  r2 = R / e1;
-}
-
-// Warp-per-row launches: a warp takes one grid row at a time (row parameters are
-// warp-uniform: computed once per ~60 elements), its lanes cover x in steps of 32
-// with SX elements per lane whose loads are all issued before any is used; warps
-// stride over the rows of a grid that fills every SM (a few CTAs per SM).
-constexpr int ST = 256, SX = 2, RW = 2;   // threads, x per lane, rows per warp pass
-
-struct FluxRow {
-  int a, e0, d0, st, h0, fx, fy, fz;
-  bool lo_in, hi_in;
+struct FDiv {
+  unsigned d, m, s;   // n / d = (umulhi(n, m) + n) >> s  for n < 2^31
 };
 
-// row R of the flattened interior-face families
-__device__ __forceinline__ FluxRow flux_row(const bddc_geom& G, int R) {
-  FluxRow w;
-  int r1, r2, a;
-  flat_row(G, R, a, r1, r2);
-  w.a = a;
-  w.e0 = G.n[0] - (a == 0);
-  const int e1 = G.n[1] - (a == 1);
-  w.fx = (a == 0);
-  w.fy = r1 + (a == 1);
-  w.fz = r2 + (a == 2);
-  w.d0 = G.fam_off[a] + w.e0 * (r1 + e1 * r2);
-  w.st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
-  w.h0 = cell_id(G, w.fx, w.fy, w.fz);
-  const int fa = a == 1 ? w.fy : w.fz, na = a == 1 ? G.n[1] : G.n[2];
-  w.lo_in = a == 0 || fa > 1;
-  w.hi_in = a == 0 || fa < na - 1;
-  return w;
+FDiv fdiv(unsigned d) {
+  unsigned s = 0;
+  while ((1ull << s) < d) ++s;
+  const unsigned long long m = (((1ull << 32) * ((1ull << s) - d)) / d) + 1;
+  return FDiv{d, (unsigned)m, s};
 }
 
-// y = alpha * A u + beta * y on the interior faces (dof stride along a inside
-// family a equals the cell stride st; partners outside the family are predicated
-// off or, in mode B, the Dirichlet face)
-__global__ void __launch_bounds__(ST) flux_A_kernel(bddc_geom G, const double* __restrict__ coef,
+__device__ __forceinline__ int fdivu(const FDiv& f, int n) {
+  const unsigned t = __umulhi((unsigned)n, f.m);
+  return (int)((t + (unsigned)n) >> f.s);
+}
+
+struct FlatArgs {
+  int nb[3];    // CTAs per family
+  FDiv dx0;     // nx - 1
+  FDiv dx;      // nx
+  FDiv dy0;     // ny - 1
+  FDiv dy;      // ny
+  FDiv dxy;     // nx * ny
+};
+
+// Interior face dof d of family a (r = d - fam_off[a]): its high cell and whether
+// the partner faces d -+ st along a are interior faces (else: wall, or in mode B
+// on the drop axis the Dirichlet face).
+struct FaceAt {
+  int hi;
+  bool l, h;
+};
+
+__device__ __forceinline__ FaceAt face_at(const bddc_geom& G, const FlatArgs& F, int a, int r) {
+  FaceAt f;
+  if (a == 0) {
+    const int q = fdivu(F.dx0, r), x = r - q * (G.n[0] - 1);
+    f.hi = r + q + 1;
+    f.l = x > 0;
+    f.h = x < G.n[0] - 2;
+  } else if (a == 1) {
+    const int q = fdivu(F.dx, r), z = fdivu(F.dy0, q), y1 = q - z * (G.n[1] - 1);
+    f.hi = r + G.n[0] * (1 + z);
+    f.l = y1 > 0;
+    f.h = y1 < G.n[1] - 2;
+  } else {
+    const int z1 = fdivu(F.dxy, r);
+    f.hi = r + G.n[0] * G.n[1];
+    f.l = z1 > 0;
+    f.h = z1 < G.n[2] - 2;
+  }
+  return f;
+}
+
+// mode B: the Dirichlet face at end `side` of the line through cell `c` (along dir_axis)
+__device__ __forceinline__ int bnd_of_cell(const bddc_geom& G, int side, int c) {
+  const int x = c % G.n[0], y = (c / G.n[0]) % G.n[1], z = c / (G.n[0] * G.n[1]);
+  // transverse coordinates of the drop axis (bnd_dof without a dynamically indexed array)
+  const int g1 = G.dir_axis == 0 ? y : x, g2 = G.dir_axis == 2 ? y : z;
+  const int n1 = G.dir_axis == 0 ? G.n[1] : G.n[0];
+  return G.n_flux_int + side * G.n_bt + g1 + n1 * g2;
+}
+
+__device__ __forceinline__ int block_family(const FlatArgs& F, int& blk) {
+  int a = 0;
+  blk = blockIdx.x;
+  if (blk >= F.nb[0]) { a = 1; blk -= F.nb[0]; }
+  if (a == 1 && blk >= F.nb[1]) { a = 2; blk -= F.nb[1]; }
+  return a;
+}
+
+// y = alpha * A u + beta * y on the interior faces (grid.py:270-307):
+//   (A u)_d = a_diag (c_lo + c_hi) u_d + a_off (c_lo u_{d-st} + c_hi u_{d+st})
+template <int SV>
+__global__ void __launch_bounds__(ST) flux_A_kernel(bddc_geom G, FlatArgs F, const double* __restrict__ coef,
                                                     const double* __restrict__ u, double alpha, double beta,
-                                                    double* __restrict__ y, int nrows) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * ST) >> 5;
-  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
-    FluxRow r[RW];
-    int emax = 0;
+                                                    double* __restrict__ y) {
+  int blk;
+  const int a = block_family(F, blk);
+  const int off = G.fam_off[a], nfam = G.fam_off[a + 1] - off;
+  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+  const double* __restrict__ ca = coef + (size_t)a * G.n_cells;
+  const int r0 = blk * ST * SV + threadIdx.x;
+  double clo[SV], chi[SV], u0[SV], ul[SV], uh[SV], yo[SV];
 #pragma unroll
-    for (int j = 0; j < RW; ++j) {
-      r[j] = flux_row(G, imin(R0 + j, nrows - 1));
-      if (R0 + j >= nrows) r[j].e0 = 0;
-      emax = imax(emax, r[j].e0);
+  for (int k = 0; k < SV; ++k) {
+    const int r = r0 + k * ST;
+    const bool act = r < nfam;
+    const FaceAt f = face_at(G, F, a, act ? r : 0);
+    const int d = off + r;
+    int dl = f.l ? d - st : -1, dh = f.h ? d + st : -1;
+    if (a == G.dir_axis && act && (!f.l || !f.h)) {
+      if (!f.l) dl = bnd_of_cell(G, 0, f.hi);
+      if (!f.h) dh = bnd_of_cell(G, 1, f.hi);
     }
-    for (int x0 = 0; x0 < emax; x0 += 32 * SX) {
-      double clo[RW][SX], chi[RW][SX], u0[RW][SX], ul[RW][SX], uh[RW][SX];
-      int dd[RW][SX];
+    clo[k] = act ? __ldg(ca + f.hi - st) : 0.0;
+    chi[k] = act ? __ldg(ca + f.hi) : 0.0;
+    u0[k] = act ? __ldg(u + d) : 0.0;
+    ul[k] = (act && dl >= 0) ? __ldg(u + dl) : 0.0;
+    uh[k] = (act && dh >= 0) ? __ldg(u + dh) : 0.0;
+    yo[k] = (act && beta != 0.0) ? y[d] : 0.0;
+  }
 #pragma unroll
-      for (int j = 0; j < RW; ++j)
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          const FluxRow& w = r[j];
-          const int x = x0 + lane + 32 * k;
-          const bool act = x < w.e0;
-          const int d = w.d0 + x, hi = w.h0 + x;
-          dd[j][k] = act ? d : -1;
-          const bool l = w.a == 0 ? x > 0 : w.lo_in, h = w.a == 0 ? x < w.e0 - 1 : w.hi_in;
-          int dl = l ? d - w.st : -1, dh = h ? d + w.st : -1;
-          if (w.a == G.dir_axis && act && (!l || !h)) {
-            const int g[3] = {w.fx + x, w.fy, w.fz};
-            if (!l) dl = bnd_dof(G, 0, g);
-            if (!h) dh = bnd_dof(G, 1, g);
-          }
-          const double* ca = coef + (size_t)w.a * G.n_cells;
-          clo[j][k] = act ? __ldg(ca + hi - w.st) : 0.0;
-          chi[j][k] = act ? __ldg(ca + hi) : 0.0;
-          u0[j][k] = act ? __ldg(u + d) : 0.0;
-          ul[j][k] = (act && dl >= 0) ? __ldg(u + dl) : 0.0;
-          uh[j][k] = (act && dh >= 0) ? __ldg(u + dh) : 0.0;
-        }
-#pragma unroll
-      for (int j = 0; j < RW; ++j)
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          if (dd[j][k] < 0) continue;
-          const double v = G.a_diag * (clo[j][k] + chi[j][k]) * u0[j][k] +
-                           G.a_off * (clo[j][k] * ul[j][k] + chi[j][k] * uh[j][k]);
-          y[dd[j][k]] = alpha * v + (beta == 0.0 ? 0.0 : beta * y[dd[j][k]]);
-        }
-    }
+  for (int k = 0; k < SV; ++k) {
+    const int r = r0 + k * ST;
+    if (r >= nfam) break;
+    const double v = G.a_diag * (clo[k] + chi[k]) * u0[k] + G.a_off * (clo[k] * ul[k] + chi[k] * uh[k]);
+    y[off + r] = alpha * v + beta * yo[k];
   }
 }
 
@@ -182,104 +174,78 @@ __global__ void flux_A_bnd_kernel(bddc_geom G, const double* __restrict__ coef, 
 }
 
 // out_c = s_f * fvec_c + s_b * Dcell_c * (B u)_c   (Dcell = D of the cell's subdomain, or 1);
-// warp per cell row, the 2 dim face loads of each cell predicated and issued first
-__global__ void __launch_bounds__(ST) cell_div_kernel(bddc_geom G, const double* __restrict__ u,
+// (B u)_c = sum_a u(low a-face) - u(high a-face), wall faces 0 (grid.py:310-324)
+template <int SV>
+__global__ void __launch_bounds__(ST) cell_div_kernel(bddc_geom G, FlatArgs F, const double* __restrict__ u,
                                                       const double* __restrict__ fvec, double s_f, double s_b,
                                                       const int* __restrict__ cell_sub,
                                                       const double* __restrict__ Dsub, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * ST) >> 5;
-  const int nrows = G.n[1] * G.n[2];
-  const int ex = G.n[0] - 1;
-  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
-    for (int x0 = 0; x0 < G.n[0]; x0 += 32 * SX) {
-      double b[RW][SX], fv[RW][SX], D[RW][SX];
-      int cc[RW][SX];
+  const int nx = G.n[0], ny = G.n[1], nxy = nx * ny;
+  const int c0 = blockIdx.x * ST * SV + threadIdx.x;
+  double b[SV], fv[SV], D[SV];
 #pragma unroll
-      for (int j = 0; j < RW; ++j) {
-        const int R = imin(R0 + j, nrows - 1);
-        const int yy = R % G.n[1], z = R / G.n[1];
-        const int c0 = G.n[0] * (yy + G.n[1] * z);
-        const int dx0 = G.fam_off[0] + ex * (yy + G.n[1] * z) - 1;
-        const int dyl0 = G.fam_off[1] + G.n[0] * (yy - 1 + (G.n[1] - 1) * z);
-        const int dzl0 = G.fam_off[2] + G.n[0] * (yy + G.n[1] * (z - 1));
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          const int x = x0 + lane + 32 * k;
-          const bool act = x < G.n[0] && R0 + j < nrows;
-          const int c3[3] = {x, yy, z};
-          cc[j][k] = act ? c0 + x : -1;
-          int dlo[3] = {-1, -1, -1}, dhi[3] = {-1, -1, -1};
-          dlo[0] = x > 0 ? dx0 + x : (G.dir_axis == 0 ? bnd_dof(G, 0, c3) : -1);
-          dhi[0] = x < G.n[0] - 1 ? dx0 + x + 1 : (G.dir_axis == 0 ? bnd_dof(G, 1, c3) : -1);
-          if (G.dim > 1) {
-            dlo[1] = yy > 0 ? dyl0 + x : (G.dir_axis == 1 ? bnd_dof(G, 0, c3) : -1);
-            dhi[1] = yy < G.n[1] - 1 ? dyl0 + G.n[0] + x : (G.dir_axis == 1 ? bnd_dof(G, 1, c3) : -1);
-          }
-          if (G.dim > 2) {
-            dlo[2] = z > 0 ? dzl0 + x : (G.dir_axis == 2 ? bnd_dof(G, 0, c3) : -1);
-            dhi[2] = z < G.n[2] - 1 ? dzl0 + G.n[0] * G.n[1] + x : (G.dir_axis == 2 ? bnd_dof(G, 1, c3) : -1);
-          }
-          double sacc = 0.0;
-#pragma unroll
-          for (int a2 = 0; a2 < 3; ++a2) {
-            const double vl = (act && dlo[a2] >= 0) ? __ldg(u + dlo[a2]) : 0.0;
-            const double vh = (act && dhi[a2] >= 0) ? __ldg(u + dhi[a2]) : 0.0;
-            sacc += vl - vh;
-          }
-          b[j][k] = sacc;
-          fv[j][k] = (act && fvec) ? __ldg(fvec + c0 + x) : 0.0;
-          D[j][k] = (act && Dsub) ? __ldg(Dsub + __ldg(cell_sub + c0 + x)) : 1.0;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < RW; ++j)
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          if (cc[j][k] < 0) continue;
-          double v = s_b * D[j][k] * b[j][k];
-          if (fvec) v += s_f * fv[j][k];
-          out[cc[j][k]] = v;
-        }
+  for (int k = 0; k < SV; ++k) {
+    const int c = c0 + k * ST;
+    const bool act = c < G.n_cells;
+    const int q = fdivu(F.dx, c), x = c - q * nx;
+    const int z = fdivu(F.dy, q), yy = q - z * ny;
+    int l0 = x > 0 ? G.fam_off[0] + c - q - 1 : -1;
+    int h0 = x < nx - 1 ? G.fam_off[0] + c - q : -1;
+    int l1 = (G.dim > 1 && yy > 0) ? G.fam_off[1] + c - nx * (1 + z) : -1;
+    int h1 = (G.dim > 1 && yy < ny - 1) ? G.fam_off[1] + c - nx * z : -1;
+    int l2 = (G.dim > 2 && z > 0) ? G.fam_off[2] + c - nxy : -1;
+    int h2 = (G.dim > 2 && z < G.n[2] - 1) ? G.fam_off[2] + c : -1;
+    if (G.dir_axis >= 0 && act) {   // mode B: the drop axis ends on Dirichlet faces
+      const int ad = G.dir_axis;
+      if (ad == 0 && l0 < 0) l0 = bnd_of_cell(G, 0, c);
+      if (ad == 0 && h0 < 0) h0 = bnd_of_cell(G, 1, c);
+      if (ad == 1 && l1 < 0) l1 = bnd_of_cell(G, 0, c);
+      if (ad == 1 && h1 < 0) h1 = bnd_of_cell(G, 1, c);
+      if (ad == 2 && l2 < 0) l2 = bnd_of_cell(G, 0, c);
+      if (ad == 2 && h2 < 0) h2 = bnd_of_cell(G, 1, c);
     }
+    const double v0 = (act && l0 >= 0) ? __ldg(u + l0) : 0.0, w0 = (act && h0 >= 0) ? __ldg(u + h0) : 0.0;
+    const double v1 = (act && l1 >= 0) ? __ldg(u + l1) : 0.0, w1 = (act && h1 >= 0) ? __ldg(u + h1) : 0.0;
+    const double v2 = (act && l2 >= 0) ? __ldg(u + l2) : 0.0, w2 = (act && h2 >= 0) ? __ldg(u + h2) : 0.0;
+    const double sacc = ((v0 - w0) + (v1 - w1)) + (v2 - w2);
+    b[k] = sacc;
+    fv[k] = (act && fvec) ? __ldg(fvec + c) : 0.0;
+    D[k] = (act && Dsub) ? __ldg(Dsub + __ldg(cell_sub + c)) : 1.0;
+  }
+#pragma unroll
+  for (int k = 0; k < SV; ++k) {
+    const int c = c0 + k * ST;
+    if (c >= G.n_cells) break;
+    double v = s_b * D[k] * b[k];
+    if (fvec) v += s_f * fv[k];
+    out[c] = v;
   }
 }
 
-// y_d = alpha (p_hi - p_lo) + beta y_d on the interior faces (warp per row)
-__global__ void __launch_bounds__(ST) grad_kernel(bddc_geom G, const double* __restrict__ p, double alpha,
-                                                  double beta, double* __restrict__ y, int nrows) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * ST) >> 5;
-  for (int R0 = ((blockIdx.x * ST + threadIdx.x) >> 5) * RW; R0 < nrows; R0 += nw * RW) {
-    FluxRow r[RW];
-    int emax = 0;
+// y_d = alpha (p_hi - p_lo) + beta y_d on the interior faces
+template <int SV>
+__global__ void __launch_bounds__(ST) grad_kernel(bddc_geom G, FlatArgs F, const double* __restrict__ p,
+                                                  double alpha, double beta, double* __restrict__ y) {
+  int blk;
+  const int a = block_family(F, blk);
+  const int off = G.fam_off[a], nfam = G.fam_off[a + 1] - off;
+  const int st = a == 0 ? 1 : (a == 1 ? G.n[0] : G.n[0] * G.n[1]);
+  const int r0 = blk * ST * SV + threadIdx.x;
+  double ph[SV], pl[SV], yo[SV];
 #pragma unroll
-    for (int j = 0; j < RW; ++j) {
-      r[j] = flux_row(G, imin(R0 + j, nrows - 1));
-      if (R0 + j >= nrows) r[j].e0 = 0;
-      emax = imax(emax, r[j].e0);
-    }
-    for (int x0 = 0; x0 < emax; x0 += 32 * SX) {
-      double ph[RW][SX], pl[RW][SX];
+  for (int k = 0; k < SV; ++k) {
+    const int r = r0 + k * ST;
+    const bool act = r < nfam;
+    const FaceAt f = face_at(G, F, a, act ? r : 0);
+    ph[k] = act ? __ldg(p + f.hi) : 0.0;
+    pl[k] = act ? __ldg(p + f.hi - st) : 0.0;
+    yo[k] = (act && beta != 0.0) ? y[off + r] : 0.0;
+  }
 #pragma unroll
-      for (int j = 0; j < RW; ++j)
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          const int x = x0 + lane + 32 * k;
-          const bool act = x < r[j].e0;
-          ph[j][k] = act ? __ldg(p + r[j].h0 + x) : 0.0;
-          pl[j][k] = act ? __ldg(p + r[j].h0 + x - r[j].st) : 0.0;
-        }
-#pragma unroll
-      for (int j = 0; j < RW; ++j)
-#pragma unroll
-        for (int k = 0; k < SX; ++k) {
-          const int x = x0 + lane + 32 * k;
-          if (x >= r[j].e0) continue;
-          const int d = r[j].d0 + x;
-          y[d] = alpha * (ph[j][k] - pl[j][k]) + (beta == 0.0 ? 0.0 : beta * y[d]);
-        }
-    }
+  for (int k = 0; k < SV; ++k) {
+    const int r = r0 + k * ST;
+    if (r >= nfam) break;
+    y[off + r] = alpha * (ph[k] - pl[k]) + beta * yo[k];
   }
 }
 
@@ -334,31 +300,51 @@ __global__ void sub_mean_kernel(long long n, const double* __restrict__ sum, dou
 }  // namespace
 
 namespace {
-// rows of the interior-face families (flux operators) or of the cells
-int flux_rows(const bddc_geom* g) {
-  int t = 0;
-  for (int a = 0; a < g->dim; ++a) t += (g->n[1] - (a == 1)) * ((g->dim > 2) ? g->n[2] - (a == 2) : 1);
-  return t;
+// entries per thread: BDDC_STENCIL_SV overrides (tuning sweeps), else `def`
+// (C3 sweep over 1/2/4/8: A u 3.9/4.4/4.6/3.6 TB/s, B u 3.4/3.4/2.9/2.0, B^T p 2.8/3.4/3.4/3.4)
+int stencil_sv(int def) {
+  static int ov = -1;
+  if (ov < 0) {
+    const char* e = getenv("BDDC_STENCIL_SV");
+    ov = e ? atoi(e) : 0;
+  }
+  return (ov == 1 || ov == 2 || ov == 4 || ov == 8) ? ov : def;
 }
-// grid-stride launch: exactly the CTAs that are co-resident (one wave), never more
-// than the rows need
-template <typename K>
-dim3 row_grid(K kernel, int nrows) {
-  int dev = 0, nsm = 148, occ = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, ST, 0);
-  const int need = (nrows + RW * ST / 32 - 1) / (RW * ST / 32);
-  return dim3((unsigned)imax(1, imin(need, nsm * imax(occ, 1))));
+
+// one CTA per ST x sv consecutive entries of a family (block-uniform family)
+FlatArgs flat_args(const bddc_geom* g, int sv) {
+  FlatArgs F;
+  for (int a = 0; a < 3; ++a) {
+    const int nfam = a < g->dim ? g->fam_off[a + 1] - g->fam_off[a] : 0;
+    F.nb[a] = (nfam + ST * sv - 1) / (ST * sv);
+  }
+  F.dx0 = fdiv((unsigned)imax(1, g->n[0] - 1));
+  F.dx = fdiv((unsigned)g->n[0]);
+  F.dy0 = fdiv((unsigned)imax(1, g->n[1] - 1));
+  F.dy = fdiv((unsigned)g->n[1]);
+  F.dxy = fdiv((unsigned)(g->n[0] * g->n[1]));
+  return F;
 }
+int flat_blocks(const FlatArgs& F) { return F.nb[0] + F.nb[1] + F.nb[2]; }
+
+#define STENCIL_DISPATCH(sv, KER, GRID, STREAM, ...)                               \
+  switch (sv) {                                                                    \
+    case 1: KER<1><<<GRID, ST, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 2: KER<2><<<GRID, ST, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 8: KER<8><<<GRID, ST, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    default: KER<4><<<GRID, ST, 0, STREAM>>>(__VA_ARGS__); break;                  \
+  }
 }  // namespace
 
 extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double* u, double alpha, double beta,
                            double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int nr = flux_rows(g);
-  flux_A_kernel<<<row_grid(flux_A_kernel, nr), ST, 0, s>>>(*g, coef, u, alpha, beta, y, nr);
-  LAUNCH_OK();
+  const int sv = stencil_sv(4);
+  const FlatArgs F = flat_args(g, sv);
+  if (flat_blocks(F) > 0) {
+    STENCIL_DISPATCH(sv, flux_A_kernel, flat_blocks(F), s, *g, F, coef, u, alpha, beta, y);
+    LAUNCH_OK();
+  }
   if (g->dir_axis >= 0 && g->n_bt > 0) {
     flux_A_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, coef, u, alpha, beta, y);
     LAUNCH_OK();
@@ -368,18 +354,22 @@ extern "C" int bddc_flux_A(const bddc_geom* g, const double* coef, const double*
 
 extern "C" int bddc_cell_div(const bddc_geom* g, const double* u, const double* fvec, double s_f, double s_b,
                              const int* cell_sub, const double* Dsub, double* out, void* stream) {
-  cell_div_kernel<<<row_grid(cell_div_kernel, g->n[1] * g->n[2]), ST, 0, (cudaStream_t)stream>>>(*g, u, fvec, s_f, s_b,
-                                                                                           cell_sub,
-                                                                              Dsub, out);
+  const int sv = stencil_sv(2);   // C3: 2.87 TB/s at 4 entries per thread, 3.43 at 2
+  const FlatArgs F = flat_args(g, sv);
+  const int nb = (g->n_cells + ST * sv - 1) / (ST * sv);
+  STENCIL_DISPATCH(sv, cell_div_kernel, nb, (cudaStream_t)stream, *g, F, u, fvec, s_f, s_b, cell_sub, Dsub, out);
   LAUNCH_OK();
   return 0;
 }
 
 extern "C" int bddc_grad(const bddc_geom* g, const double* p, double alpha, double beta, double* y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int nr = flux_rows(g);
-  grad_kernel<<<row_grid(grad_kernel, nr), ST, 0, s>>>(*g, p, alpha, beta, y, nr);
-  LAUNCH_OK();
+  const int sv = stencil_sv(4);
+  const FlatArgs F = flat_args(g, sv);
+  if (flat_blocks(F) > 0) {
+    STENCIL_DISPATCH(sv, grad_kernel, flat_blocks(F), s, *g, F, p, alpha, beta, y);
+    LAUNCH_OK();
+  }
   if (g->dir_axis >= 0 && g->n_bt > 0) {
     grad_bnd_kernel<<<(2 * g->n_bt + 255) / 256, 256, 0, s>>>(*g, p, alpha, beta, y);
     LAUNCH_OK();
