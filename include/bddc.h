@@ -106,6 +106,19 @@ int bddc_spd_inverse_batched_ex(double* M, int n, int ld, long long sM, int batc
 
 /* ------------------------------------------------------- local operators */
 
+/* Interface topology of a box partition built on the device in closed form
+ * (decomposition.py:32-125: gamma_dofs, faces, signs; solver.py:92-93 _local_pos).
+ * face_base[i] = number of faces (i', j') with i' < i (host prefix sum over N).
+ * Out: nG (N), gpos / gcode (N x maxG, -1 padded; code = axis | side << 2 |
+ * line << 3, side 1 = the +axis normal points out), fslot (N x 6 x maxF), gown
+ * (n_gamma x 2 broken slots: [side-1 copy, side-0 copy]), gamma (global dof ids,
+ * increasing), gface (face index per interface dof), cell_sub (n_cells). */
+int bddc_topology_box(const bddc_geom* g, const int* face_base, int* nG, int* gpos, int* gcode,
+                      int* fslot, int* gown, int* gamma, int* gface, int* cell_sub, void* stream);
+/* solver.py:286-298: *flag = 1 when some face has max k (low-side cells) / min k
+ * (high-side cells) outside [1e-3, 1e3].  faces: n_faces x 4 (i, j, axis, m). */
+int bddc_face_jumps(const bddc_geom* g, const int* faces, const double* k, int* flag, void* stream);
+
 /* c_a = h_a^2 / (6 V k_a) per cell (grid.py:204-227, 270-291). coef: 3 x n_cells
  * (one contiguous array per axis: coalesced rows in the stencil and line solves). */
 int bddc_cell_coeffs(const bddc_geom* g, const double* k, double* coef, void* stream);

@@ -16,7 +16,7 @@ from . import errors
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BDDC_LIB") or os.path.join(HERE, "libbddc.so")
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["capi.cu", "dense.cu", "local.cu", "adaptive.cu", "coarse.cu",
+SOURCES = ["capi.cu", "dense.cu", "topology.cu", "local.cu", "adaptive.cu", "coarse.cu",
            "nd.cu", "pcg.cu", "stencil.cu", "graph.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
@@ -92,6 +92,8 @@ _SIGS = {
     "bddc_spd_log_read": [_P, _I],
     "bddc_spd_inverse_batched": [_P, _I, _I, _L, _I, _I, _P, _P, _P],
     "bddc_spd_inverse_batched_ex": [_P, _I, _I, _L, _I, _I, _P, _P, _I, _P],
+    "bddc_topology_box": [_GP, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "bddc_face_jumps": [_GP, _P, _P, _P, _P],
     "bddc_cell_coeffs": [_GP, _P, _P, _P],
     "bddc_weights": [_GP, _I, _P, _P, _P, _P],
     "bddc_rescale": [_GP, _P, _P, _P],

@@ -129,20 +129,76 @@ class Decomposition:
                                for a in range(3)], axis=1)
         self.box_L = np.stack([self.sw[a][self.sub_strip[:, a]]
                                for a in range(3)], axis=1)
+        self._closed_forms()
+
+    # ------------------------------------------------------------ topology
+
+    def _closed_forms(self):
+        """Sizes and the per-subdomain / per-face tables (O(N) host work).  The
+        per-slot and per-dof tables are built on the device by the solver
+        (csrc/topology.cu); their host copies below are made on first access."""
+        g = self.grid
+        n3, S3, dim = self.n3, self.S3, g.dim
+        N = self.n_subdomains
+        self.fam_off = list(g.flux_offsets) + [g.flux_offsets[-1]] * (4 - len(g.flux_offsets))
+        ss, L = self.sub_strip, self.box_L
+        stride = (1, S3[0], S3[0] * S3[1])
+        nG = np.zeros(N, dtype=np.int64)
+        n_hi = np.zeros(N, dtype=np.int64)
+        rows = []
+        n_gamma, maxF = 0, 1
+        for a in range(dim):
+            t1 = 1 if a == 0 else 0
+            t2 = 1 if a == 2 else 2
+            lines = L[:, t1] * L[:, t2]
+            lo = ss[:, a] > 0
+            hi = ss[:, a] < S3[a] - 1
+            nG += (lo.astype(np.int64) + hi) * lines
+            n_hi += hi
+            i_lo = np.nonzero(hi)[0]
+            rows.append(np.stack([i_lo, i_lo + stride[a], np.full(len(i_lo), a),
+                                  lines[i_lo]], axis=1))
+            n_gamma += (S3[a] - 1) * n3[t1] * n3[t2]
+            maxF = max(maxF, int(self.sw[t1].max() * self.sw[t2].max()))
+        self.nG = nG.astype(np.int32)
+        self.maxG = _pad(int(nG.max()) if N else 1, 64)
+        self.maxF = maxF
+        self._n_gamma = int(n_gamma)
+        # faces sorted by (i, j): for one i the x, y, z neighbours have increasing ids
+        ft = np.concatenate(rows) if rows else np.zeros((0, 4), dtype=np.int64)
+        ft = ft[np.lexsort((ft[:, 1], ft[:, 0]))]
+        self.face_table = ft.astype(np.int32).reshape(-1, 4)
+        self.n_faces = len(ft)
+        self.face_base = (np.cumsum(n_hi) - n_hi).astype(np.int32)
+        P = np.prod([int(w.max()) for w in self.sw])
+        self.maxP = _pad(int(P), 64)
+        self.maxL = int(max(int(w.max()) for w in self.sw))
+
+    _LAZY = ("gamma", "gpos", "gcode", "fslot", "gown", "gface", "dof_sub_low",
+             "dof_sub_high", "_slot_sub", "_slot_q", "_slot_dof", "_fidx")
+
+    def __getattr__(self, name):
+        # host copies of the big tables (reference-compatible views, tests): built
+        # once, on demand, by the vectorised NumPy restatement below
+        if name in Decomposition._LAZY:
+            self._build_interface()
+            return self.__dict__[name]
+        raise AttributeError(name)
+
+    @cached_property
+    def part(self):
+        """Cell -> subdomain map (decomposition.py:33)."""
+        n3, S3, strip_of = self.n3, self.S3, self.strip_of
         cz, cy, cx = np.meshgrid(np.arange(n3[2]), np.arange(n3[1]),
                                  np.arange(n3[0]), indexing="ij")
         cx, cy, cz = cx.ravel(), cy.ravel(), cz.ravel()
-        self.part = (strip_of[0][cx] + S3[0] * (strip_of[1][cy]
-                     + S3[1] * strip_of[2][cz])).astype(np.int64)
-        self._build_interface()
-
-    # ------------------------------------------------------------ topology
+        return (strip_of[0][cx] + S3[0] * (strip_of[1][cy]
+                + S3[1] * strip_of[2][cz])).astype(np.int64)
 
     def _build_interface(self):
         g = self.grid
         n3, S3 = self.n3, self.S3
-        fam_off = list(g.flux_offsets) + [g.flux_offsets[-1]] * (4 - len(g.flux_offsets))
-        self.fam_off = fam_off
+        fam_off = self.fam_off
         subs, dofs, codes = [], [], []
         lo_dofs = []
         face_rows = []
@@ -201,9 +257,8 @@ class Decomposition:
         counts = np.bincount(subs, minlength=N)
         starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
         slot = np.arange(len(subs)) - starts[subs]
-        self.nG = counts.astype(np.int32)
-        maxG = _pad(int(counts.max()) if len(counts) else 1, 64)
-        self.maxG = maxG
+        assert np.array_equal(counts, self.nG) and n_gamma == self._n_gamma
+        maxG = self.maxG
         inv = np.empty(g.n_flux_dofs, dtype=np.int64)
         inv[self.gamma] = np.arange(n_gamma)
         gpos = inv[dofs]
@@ -213,12 +268,7 @@ class Decomposition:
         self.gcode[subs, slot] = codes
         self._slot_sub, self._slot_q, self._slot_dof = subs, slot, dofs
         # fslot
-        maxF = 1
-        for a in range(g.dim):
-            t1 = 1 if a == 0 else 0
-            t2 = 1 if a == 2 else 2
-            maxF = max(maxF, int(self.sw[t1].max() * self.sw[t2].max()))
-        self.maxF = maxF
+        maxF = self.maxF
         self.fslot = np.full((N, 6, maxF), -1, dtype=np.int32)
         a_ = codes & 3
         side_ = (codes >> 2) & 1
@@ -232,8 +282,7 @@ class Decomposition:
         self.gown = own
         # faces sorted by (i, j)
         fr = sorted(face_rows)
-        self.face_table = np.array(fr, dtype=np.int32).reshape(-1, 4)
-        self.n_faces = len(fr)
+        assert np.array_equal(np.array(fr, dtype=np.int32).reshape(-1, 4), self.face_table)
         fidx = {(r[0], r[1]): k for k, r in enumerate(fr)}
         lo_sub = subs[side_ == 1]
         # the face of each gamma dof (via its low copy)
@@ -250,9 +299,6 @@ class Decomposition:
         self.dof_sub_low = lo_s
         self.dof_sub_high = hi_sub
         self._fidx = fidx
-        P = np.prod([int(w.max()) for w in self.sw])
-        self.maxP = _pad(int(P), 64)
-        self.maxL = int(max(int(w.max()) for w in self.sw))
 
     # -------------------------------------------------- Laplacian eigendata
 
@@ -302,7 +348,7 @@ class Decomposition:
 
     @property
     def n_gamma(self):
-        return len(self.gamma)
+        return self._n_gamma
 
     @cached_property
     def cells(self):

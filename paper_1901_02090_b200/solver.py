@@ -184,16 +184,23 @@ class BddcSetup:
         N, mg, mp = dec.n_subdomains, dec.maxG, dec.maxP
         self.N, self.maxG, self.maxP = N, mg, mp
         t = lambda a, dt=I32: _upload(a, dt, dev)
-        # topology tables
-        self.d_gpos = t(dec.gpos)
-        self.d_gcode = t(dec.gcode)
-        self.d_nG = t(dec.nG)
-        self.d_fslot = t(dec.fslot)
-        self.d_gown = t(dec.gown)
-        self.d_gamma = t(dec.gamma)
+        # topology tables: per-slot / per-dof / per-cell ones in closed form on the
+        # device (csrc/topology.cu); the host keeps only O(N) and per-face tables
+        e = lambda *shape: torch.empty(shape, dtype=I32, device=dev)
+        ngam = max(dec.n_gamma, 1)
+        self.d_gpos = e(N, mg)
+        self.d_gcode = e(N, mg)
+        self.d_nG = e(N)
+        self.d_fslot = e(N, 6, dec.maxF)
+        self.d_gown = e(ngam, 2)
+        self.d_gamma = e(ngam)
+        self.d_gface = e(ngam)
+        self.d_cell_sub = e(G.n_cells)
         self.d_faces = t(dec.face_table if dec.n_faces else np.zeros((1, 4)))
-        self.d_gface = t(dec.gface)
-        self.d_cell_sub = t(dec.cell_sub)
+        self.d_face_base = t(dec.face_base)
+        nat.call("bddc_topology_box", gp, _p(self.d_face_base), _p(self.d_nG), _p(self.d_gpos),
+                 _p(self.d_gcode), _p(self.d_fslot), _p(self.d_gown), _p(self.d_gamma),
+                 _p(self.d_gface), _p(self.d_cell_sub), st)
         eig_w, dm_w = dec.laplacian_eigs(True)
         eig_u, _ = dec.laplacian_eigs(False)
         self.d_eig_w = t(eig_w, F64)
@@ -1056,45 +1063,19 @@ def write_eigs_csv(path, reports):
         f.write("\n".join(lines) + "\n")
 
 
-def _face_cells(dec):
-    """Per interface dof: low / high neighbour cell, grouped by face (cached on dec)."""
-    cached = getattr(dec, "_face_cells_cache", None)
-    if cached is not None:
-        return cached
-    g = dec.grid
-    cells = np.arange(g.n_cells)
-    fc_lo = np.empty(g.n_flux_dofs, dtype=np.int64)
-    fc_hi = np.empty(g.n_flux_dofs, dtype=np.int64)
-    for a in range(g.dim):
-        lo, hi = g.cell_faces(a)
-        m = hi >= 0
-        fc_lo[hi[m]] = cells[m]
-        m = lo >= 0
-        fc_hi[lo[m]] = cells[m]
-    o = np.argsort(dec.gface, kind="stable")
-    d = dec.gamma[o]
-    starts = np.searchsorted(dec.gface[o], np.arange(dec.n_faces))
-    out = (fc_lo[d], fc_hi[d], starts)
-    dec._face_cells_cache = out
-    return out
-
-
 def _suggest_scaling(setup):
-    """solver.py:286-298 (warning only): aligned coefficient jumps."""
+    """solver.py:286-298 (warning only): aligned coefficient jumps, per face max k
+    over the low-side cells against min k over the high-side cells (one CTA per
+    face on the setup's permeability copy; the host reads one flag)."""
     if setup.config.scaling != "multiplicity":
         return
     dec = setup.dec
     if not dec.n_gamma or not dec.n_faces:
         return
-    # per face: max k over the low-side cells / min k over the high-side cells (host
-    # bookkeeping on the caller's permeability array, once per setup, like the
-    # reference's; no device work)
-    lo, hi, starts = _face_cells(dec)
-    k = np.asarray(setup.system.perm.k, dtype=np.float64).reshape(dec.grid.n_cells, -1)
-    kmax = np.maximum.reduceat(k[lo].max(axis=1), starts)
-    kmin = np.minimum.reduceat(k[hi].min(axis=1), starts)
-    ratio = kmax / np.maximum(kmin, 1e-300)
-    if bool(((ratio > 1e3) | (ratio < 1e-3)).any()):
+    flag = torch.empty(1, dtype=I32, device=setup.dev)
+    nat.call("bddc_face_jumps", C.byref(setup.geom), _p(setup.d_faces), _p(setup.d_k), _p(flag),
+             _stream())
+    if int(flag.item()):
         warnings.warn("coefficient jumps aligned with the partition detected; "
                       "consider --scaling stiffness")
 

@@ -232,3 +232,52 @@ def test_fused_scatter_projection_matches_unfused():
         res.append((y.clone(), float(st.w_scal[12])))
     assert torch.equal(res[0][0], res[1][0])
     assert res[0][1] == res[1][1]
+
+
+@pytest.mark.parametrize("dim,counts,splits", [
+    (2, (12, 12), (3, 3)), (2, (10, 7), (1, 3)), (2, (10, 7), (3, 1)), (2, (5, 5), (1, 1)),
+    (3, (12, 10, 8), (3, 2, 2)), (3, (12, 10, 8), (1, 2, 2)), (3, (12, 10, 8), (3, 1, 2)),
+    (3, (12, 10, 8), (3, 2, 1)), (3, (12, 10, 8), (1, 1, 4)),
+    (3, (12, 12, 9), ([3, 5, 4], [2, 4, 6], [5, 4])), (3, (30, 44, 15), (6, 11, 3))])
+def test_device_topology_bitwise(dim, counts, splits):
+    """csrc/topology.cu (closed-form index kernels) against the host NumPy
+    restatement of decomposition.py:32-125: every table identical, and the setup
+    never materialises the host copies."""
+    import torch
+    import paper_1901_02090_b200 as B
+    g = B.build_grid(dim, counts, (1.0,) * dim)
+    rng = np.random.default_rng(7)
+    k = 10.0 ** rng.uniform(-1, 1, (g.n_cells, dim))
+    system = B.assemble_system(g, B.Permeability(k), B.Wells(0, g.n_cells - 1))
+    dec = B.Decomposition(g, splits)
+    st = B.BddcSetup(system, dec, B.SolveConfig(tau=float("inf"), constraints="initial"))
+    torch.cuda.synchronize()
+    lazy = set(B.Decomposition._LAZY) | {"part"}
+    assert not (lazy & set(dec.__dict__)), lazy & set(dec.__dict__)
+    ng = dec.n_gamma
+    pairs = [("nG", st.d_nG), ("gpos", st.d_gpos), ("gcode", st.d_gcode), ("fslot", st.d_fslot),
+             ("cell_sub", st.d_cell_sub)]
+    if ng:
+        pairs += [("gown", st.d_gown[:ng]), ("gamma", st.d_gamma[:ng]), ("gface", st.d_gface[:ng])]
+    for name, dev in pairs:
+        host = np.asarray(getattr(dec, name))
+        assert np.array_equal(dev.cpu().numpy().astype(np.int64), host.astype(np.int64)), name
+
+
+def test_face_jump_warning_matches_reference_rule():
+    """solver.py:286-298: warn (multiplicity scaling) iff some face sees a k ratio
+    beyond 1e3 between its two sides."""
+    import warnings
+    import paper_1901_02090_b200 as B
+    g = B.build_grid(2, (12, 12), (1.0, 1.0))
+    dec = B.regular_partition(g, (3, 3))
+    cfg = B.SolveConfig(tau=float("inf"), constraints="initial", scaling="multiplicity")
+    for jump, expect in ((1e4, True), (5e2, False)):
+        k = np.ones((144, 2))
+        k[np.arange(144) % 12 < 4] = jump          # aligned with the x = 4 strip boundary
+        system = B.assemble_system(g, B.Permeability(k), B.Wells(0, 143))
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            B.solve(system, dec, cfg)
+        hit = any("coefficient jumps aligned" in str(x.message) for x in w)
+        assert hit == expect, (jump, hit)
