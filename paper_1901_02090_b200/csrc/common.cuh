@@ -247,6 +247,14 @@ __device__ __forceinline__ void cta_symv_packed2(const double* __restrict__ Pk, 
   __syncthreads();
 }
 
+// Streaming read that bypasses L1 allocation: a once-read matrix stream must not evict
+// the CTA's (and its co-resident CTA's) L1-cached local-memory lines.
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ void cta_symv_packed(const double* __restrict__ Pk, int nt, int ntl, const double* x,
                                                 double* y, double* yw) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -268,7 +276,7 @@ __device__ __forceinline__ void cta_symv_packed(const double* __restrict__ Pk, i
     double col = 0.0;
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const double a = __ldg(T + r * 32 + lane);
+      const double a = ldg_stream(T + r * 32 + lane);
       v[r] = a * xl;
       col += a * x[bi * 32 + r];
     }

@@ -68,7 +68,8 @@ __device__ __forceinline__ int line_face_dof(const bddc_geom& G, const Box& b, i
 // Thomas factorisation of the line tridiagonal T (order m = L-1+lo+hi):
 // T[j][j] = dg (c_{p-1} + c_p) (cells that exist), T[j][j+1] = of c_p, p = j+1-lo,
 // with the element block c [[dg, of], [of, dg]]: (2, 1) consistent RT0, (3, 0)
-// lumped (grid.py:220-225).  Stores the modified super-diagonal cp and pivots piv.
+// lumped (grid.py:220-225).  Stores the modified super-diagonal cp and the reciprocal
+// pivots piv (one division per dof here, none in the solves).
 __device__ __forceinline__ void line_factor(const double* c, int L, int lo, int hi, double* cp, double* piv,
                                             double dg, double of) {
   const int m = L - 1 + lo + hi;
@@ -76,8 +77,9 @@ __device__ __forceinline__ void line_factor(const double* c, int L, int lo, int 
     const int p = j + 1 - lo;
     double d = (p >= 1 ? dg * c[p - 1] : 0.0) + (p <= L - 1 ? dg * c[p] : 0.0);
     double pv = d - ((j > 0) ? of * c[p - 1] * cp[j - 1] : 0.0);  // T[j][j-1] = of c_{p-1}
-    piv[j] = pv;
-    cp[j] = (j + 1 < m) ? of * c[p] / pv : 0.0;
+    const double rp = 1.0 / pv;
+    piv[j] = rp;
+    cp[j] = (j + 1 < m) ? of * c[p] * rp : 0.0;
   }
 }
 
@@ -85,7 +87,19 @@ __device__ __forceinline__ void line_factor(const double* c, int L, int lo, int 
 __device__ __forceinline__ void line_solve(const double* c, int L, int lo, int hi, const double* cp,
                                            const double* piv, double* r, double of) {
   const int m = L - 1 + lo + hi;
-  for (int j = 0; j < m; ++j) r[j] = (r[j] - ((j > 0) ? of * c[j - lo] * r[j - 1] : 0.0)) / piv[j];
+  for (int j = 0; j < m; ++j) r[j] = (r[j] - ((j > 0) ? of * c[j - lo] * r[j - 1] : 0.0)) * piv[j];
+  for (int j = m - 2; j >= 0; --j) r[j] -= cp[j] * r[j + 1];
+}
+
+// The same solve from the factor alone (T symmetric: T[j][j-1] = cp[j-1] / piv[j-1]):
+// z_j = r_j - cp[j-1] z_{j-1}, y_j = z_j piv_j, x_j = y_j - cp_j x_{j+1}.  cp / piv may
+// live in shared memory (factor kept from an earlier phase), element stride 1.
+__device__ __forceinline__ void line_solve_sym(int m, const double* cp, const double* piv, double* r) {
+  double z = 0.0;
+  for (int j = 0; j < m; ++j) {
+    z = r[j] - ((j > 0) ? cp[j - 1] * z : 0.0);
+    r[j] = z * piv[j];
+  }
   for (int j = m - 2; j >= 0; --j) r[j] -= cp[j] * r[j + 1];
 }
 
@@ -430,11 +444,31 @@ __global__ void symmetrize_kernel(double* __restrict__ S, int n, long long strid
 // B_loc = D B_u (grid.py:250):  p' = Q (B_u A^{-1} f - g/D),
 // u_I = A^{-1}(f - B_u^T p'), p = p'/D  where f = f_flux - A_IG x and
 // g = g_cell - D B_uG x (substructure.py:72-116).
+#ifndef LS_CTAS
+#define LS_CTAS 2
+#endif
+#ifndef LS_PREFETCH_KB
+#define LS_PREFETCH_KB 0
+#endif
+#ifdef LS_TIMING
+__device__ unsigned long long g_ls_t[8];
+#define LS_T(k)                                                                  \
+  do {                                                                           \
+    __syncthreads();                                                             \
+    if (threadIdx.x == 0) {                                                      \
+      long long t_ = clock64();                                                  \
+      atomicAdd(&g_ls_t[k], (unsigned long long)(t_ - t0_));                     \
+      t0_ = t_;                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define LS_T(k)
+#endif
 template <bool TWO>
-__global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ gcode,
+__global__ void __launch_bounds__(256, LS_CTAS) local_solve_kernel(bddc_geom G, const double* __restrict__ coef, const int* __restrict__ gcode,
                                    const int* __restrict__ gpos, const int* __restrict__ fslot,
                                    const double* __restrict__ Q, const double* __restrict__ Dsub,
-                                   bddc_local_solve_args A) {
+                                   bddc_local_solve_args A, int stash) {
   extern __shared__ double sm[];
   const int i = blockIdx.x;
   const Box b = sub_box(G, i);
@@ -448,6 +482,9 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
   constexpr bool two = TWO;
   double* rhs2 = yw + (two ? 16 : 8) * mp;   // second right-hand side (two only)
   double* pp2 = rhs2 + mp;
+  // line factors kept from the first line phase for the second (when they fit)
+  double* sCp = (two ? pp2 + mp : rhs2);
+  double* sRp = sCp + 3 * mp + 2 * G.maxF;
   int off[3], lo3[3] = {0, 0, 0}, hi3[3] = {0, 0, 0};
   {
     int o = 0;
@@ -460,6 +497,20 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     }
   }
   const double Di = Dsub[i];
+#ifdef LS_TIMING
+  long long t0_ = clock64();
+#endif
+#if LS_PREFETCH_KB > 0
+  {
+    // pull the head of this subdomain's packed Q towards L2 while the line phase runs
+    const int nt_ = mp / 32;
+    const char* Qb = (const char*)(Q + (size_t)i * (nt_ * (nt_ + 1) / 2) * 1024);
+    const size_t bytes = (size_t)(nt_ * (nt_ + 1) / 2) * 8192;
+    const size_t lim = bytes < (size_t)LS_PREFETCH_KB * 1024 ? bytes : (size_t)LS_PREFETCH_KB * 1024;
+    for (size_t o = (size_t)threadIdx.x * 128; o < lim; o += (size_t)blockDim.x * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(Qb + o));
+  }
+#endif
   for (int q = threadIdx.x; q < mg; q += blockDim.x) {
     int gp = gpos[(size_t)i * mg + q];
     xg[q] = (A.x_gamma && gp >= 0) ? A.x_scale * A.x_gamma[gp] : 0.0;
@@ -491,37 +542,103 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
   // t = A^{-1}(f - A_IG x) per line, the lines of all axes at once (thread per
   // line); rhs += B_u t through per-axis buffers (lines of one axis are
   // cell-disjoint, different axes are not), summed after the barrier
+  LS_T(0);
   int nla[3] = {0, 0, 0};
   for (int a = 0; a < G.dim; ++a) nla[a] = n_lines(b, a);
   double* radd = yw;   // 3 x mp, free until the symv
   for (int c = threadIdx.x; c < 3 * mp; c += blockDim.x) radd[c] = 0.0;
   __syncthreads();
-  for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
-    const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
-    const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
-    const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
-    if (m <= 0) continue;
-    double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
-    for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
-    line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
-    for (int j = 0; j < m; ++j)
-      r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo)] : 0.0;
-    if (A.x_gamma) {
-      int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
-      int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
-      if (qlo >= 0) r[0] -= G.a_off * c[0] * xg[qlo];
-      if (qhi >= 0) r[m - 1] -= G.a_off * c[L - 1] * xg[qhi];
+  if (stash) {
+    // every operand of the line phase staged in shared memory by the whole CTA
+    // (coalesced, all loads in flight at once): the per-axis coefficients of the
+    // box and the flux load; the factor / forward / backward sweeps then run out of
+    // shared memory and registers (no per-thread local arrays)
+    double* cs = yw + 3 * mp;   // 3 x mp, free until the symv
+    for (int a = 0; a < G.dim; ++a)
+      for (int c = threadIdx.x; c < np; c += blockDim.x) {
+        const int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
+        cs[a * mp + c] = coef[(size_t)a * G.n_cells + cell_id(G, b.o[0] + lx, b.o[1] + ly, b.o[2] + lz)];
+      }
+    for (int a = 0; a < G.dim; ++a) {
+      const int m = b.L[a] - 1 + lo3[a] + hi3[a];
+      if (m <= 0) continue;
+      const int tot = nla[a] * m;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int line = e / m, j = e - line * m;
+        tI[off[a] + e] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo3[a])] : 0.0;
+      }
     }
-    line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
-    double* t = tI + off[a] + line * m;
-    const int base = line_base(b, a, line);
-    double* ra = radd + a * mp;
-    for (int j = 0; j < m; ++j) t[j] = r[j];
-    for (int k = 0; k < L; ++k) {
-      double v = 0.0;
-      if (k - 1 + lo >= 0) v += r[k - 1 + lo];
-      if (k + lo < m) v -= r[k + lo];
-      ra[base + k * st] = v;
+    __syncthreads();
+    const double dg = G.a_diag, of = G.a_off;
+    for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
+      const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
+      const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
+      const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
+      if (m <= 0) continue;
+      const int base = line_base(b, a, line);
+      const double* cl = cs + a * mp + base;   // c[k] = cl[k st]
+      double* t = tI + off[a] + line * m;
+      double* scp = sCp + off[a] + line * m;
+      double* srp = sRp + off[a] + line * m;
+      if (A.x_gamma) {
+        const int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
+        const int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
+        if (qlo >= 0) t[0] -= of * cl[0] * xg[qlo];
+        if (qhi >= 0) t[m - 1] -= of * cl[(L - 1) * st] * xg[qhi];
+      }
+      double cpp = 0.0, rprev = 0.0;
+      for (int j = 0; j < m; ++j) {   // Thomas factor and forward sweep (see line_factor)
+        const int p = j + 1 - lo;
+        const double c_lo = p >= 1 ? cl[(p - 1) * st] : 0.0;
+        const double c_hi = p <= L - 1 ? cl[p * st] : 0.0;
+        const double pv = (dg * c_lo + dg * c_hi) - of * c_lo * cpp;
+        const double rp = 1.0 / pv;
+        cpp = (j + 1 < m) ? of * c_hi * rp : 0.0;
+        rprev = (t[j] - of * c_lo * rprev) * rp;
+        scp[j] = cpp;
+        srp[j] = rp;
+        t[j] = rprev;
+      }
+      for (int j = m - 2; j >= 0; --j) {
+        rprev = t[j] - scp[j] * rprev;
+        t[j] = rprev;
+      }
+      double* ra = radd + a * mp;
+      for (int k = 0; k < L; ++k) {
+        double v = 0.0;
+        if (k - 1 + lo >= 0) v += t[k - 1 + lo];
+        if (k + lo < m) v -= t[k + lo];
+        ra[base + k * st] = v;
+      }
+    }
+  } else {
+    for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
+      const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
+      const int line = gl - (a > 0 ? nla[0] : 0) - (a > 1 ? nla[1] : 0);
+      const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
+      if (m <= 0) continue;
+      double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
+      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
+      line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
+      for (int j = 0; j < m; ++j)
+        r[j] = A.f_flux ? A.f_scale * A.f_flux[line_face_dof(G, b, a, line, j, lo)] : 0.0;
+      if (A.x_gamma) {
+        int qlo = fslot[((size_t)i * 6 + a * 2 + 0) * G.maxF + line];
+        int qhi = fslot[((size_t)i * 6 + a * 2 + 1) * G.maxF + line];
+        if (qlo >= 0) r[0] -= G.a_off * c[0] * xg[qlo];
+        if (qhi >= 0) r[m - 1] -= G.a_off * c[L - 1] * xg[qhi];
+      }
+      line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
+      double* t = tI + off[a] + line * m;
+      const int base = line_base(b, a, line);
+      double* ra = radd + a * mp;
+      for (int j = 0; j < m; ++j) t[j] = r[j];
+      for (int k = 0; k < L; ++k) {
+        double v = 0.0;
+        if (k - 1 + lo >= 0) v += r[k - 1 + lo];
+        if (k + lo < m) v -= r[k + lo];
+        ra[base + k * st] = v;
+      }
     }
   }
   __syncthreads();
@@ -539,6 +656,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     rhs[c] += v;
   }
   __syncthreads();
+  LS_T(1);
   // p' = Q rhs, Q tile-packed symmetric (half the bytes of full storage)
   {
     const int nt = mp / 32, ntl = (np + 31) / 32;
@@ -551,6 +669,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     }
     __syncthreads();
   }
+  LS_T(2);
   // u_I = t - A^{-1} B_u^T p' (lines of all axes at once: disjoint outputs)
   for (int gl = threadIdx.x; gl < nla[0] + nla[1] + nla[2]; gl += blockDim.x) {
     const int a = gl < nla[0] ? 0 : (gl < nla[0] + nla[1] ? 1 : 2);
@@ -558,9 +677,16 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     const int L = b.L[a], lo = lo3[a], hi = hi3[a], m = L - 1 + lo + hi, st = axis_stride(b, a);
     {
       if (m <= 0) continue;
-      double c[MAXL], cp[MAXL + 1], piv[MAXL + 1], r[MAXL + 1];
-      for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
-      line_factor(c, L, lo, hi, cp, piv, G.a_diag, G.a_off);
+      double cpl[MAXL + 1], pivl[MAXL + 1], r[MAXL + 1];
+      const double* cp = sCp + off[a] + line * m;
+      const double* piv = sRp + off[a] + line * m;
+      if (!stash) {
+        double c[MAXL];
+        for (int k = 0; k < L; ++k) c[k] = coef[(size_t)(a) * G.n_cells + (line_cell_global(G, b, a, line, k))];
+        line_factor(c, L, lo, hi, cpl, pivl, G.a_diag, G.a_off);
+        cp = cpl;
+        piv = pivl;
+      }
       const int base = line_base(b, a, line);
       double* t = tI + off[a] + line * m;
       if (two) {   // second system first: t is still the shared A^{-1} f
@@ -568,7 +694,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
           const int p = j + 1 - lo;
           r[j] = (p <= L - 1 ? pp2[base + p * st] : 0.0) - (p >= 1 ? pp2[base + (p - 1) * st] : 0.0);
         }
-        line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
+        line_solve_sym(m, cp, piv, r);
         for (int j = 0; j < m; ++j)
           A.u_out2[(size_t)line_face_dof(G, b, a, line, j, lo)] = t[j] - r[j];
       }
@@ -576,7 +702,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
         const int p = j + 1 - lo;  // (B_u^T p')_j = p'(cell above) - p'(cell below)
         r[j] = (p <= L - 1 ? pp[base + p * st] : 0.0) - (p >= 1 ? pp[base + (p - 1) * st] : 0.0);
       }
-      line_solve(c, L, lo, hi, cp, piv, r, G.a_off);
+      line_solve_sym(m, cp, piv, r);
       for (int j = 0; j < m; ++j) {
         double u = t[j] - r[j];
         t[j] = u;
@@ -589,6 +715,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
     }
   }
   __syncthreads();
+  LS_T(3);
   if (A.p_out) {
     for (int c = threadIdx.x; c < np; c += blockDim.x) {
       int lx = c % b.L[0], ly = (c / b.L[0]) % b.L[1], lz = c / (b.L[0] * b.L[1]);
@@ -614,6 +741,7 @@ __global__ void __launch_bounds__(256, 2) local_solve_kernel(bddc_geom G, const 
       A.rg_broken[(size_t)i * mg + q] = v;
     }
   }
+  LS_T(4);
 }
 
 }  // namespace
@@ -623,6 +751,17 @@ extern "C" int bddc_cell_coeffs(const bddc_geom* g, const double* k, double* coe
   LAUNCH_OK();
   return 0;
 }
+
+#ifdef LS_TIMING
+extern "C" int bddc_ls_timing_read(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_ls_t, sizeof(g_ls_t));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_ls_t, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 extern "C" int bddc_weights(const bddc_geom* g, int stiffness, const double* coef, const int* gcode, double* delta,
                             void* stream) {
@@ -674,13 +813,18 @@ extern "C" int bddc_local_solve(const bddc_geom* g, const double* coef, const in
   if (g->maxP % 32) return bddc_set_error(BDDC_ERR_ARG, "local_solve: maxP must be a multiple of 32");
   const bool two = a->u_out2 != nullptr;
   size_t shm = (size_t)(g->maxG + 5 * g->maxP + 2 * g->maxF + (two ? 18 : 8) * g->maxP) * sizeof(double);
+  // the line factors of the first phase stay in shared memory for the second while
+  // two CTAs still fit on an SM; larger subdomains refactor their lines
+  const size_t shm_stash = shm + 2 * (size_t)(3 * g->maxP + 2 * g->maxF) * sizeof(double);
+  const int stash = shm_stash <= 113 * 1024;
+  if (stash) shm = shm_stash;
   if (shm > 227 * 1024) return bddc_set_error(BDDC_ERR_ARG, "local_solve: subdomain too large for shared memory");
   if (shm > 48 * 1024) {
     CUDA_OK(cudaFuncSetAttribute(local_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     CUDA_OK(cudaFuncSetAttribute(local_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
   }
-  if (two) local_solve_kernel<true><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
-  else local_solve_kernel<false><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a);
+  if (two) local_solve_kernel<true><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a, stash);
+  else local_solve_kernel<false><<<g->N, 256, shm, (cudaStream_t)stream>>>(*g, coef, gcode, gpos, fslot, Q, Dsub, *a, stash);
   LAUNCH_OK();
   return 0;
 }
