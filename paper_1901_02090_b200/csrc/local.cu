@@ -447,9 +447,6 @@ __global__ void symmetrize_kernel(double* __restrict__ S, int n, long long strid
 #ifndef LS_CTAS
 #define LS_CTAS 2
 #endif
-#ifndef LS_PREFETCH_KB
-#define LS_PREFETCH_KB 0
-#endif
 #ifdef LS_TIMING
 __device__ unsigned long long g_ls_t[8];
 #define LS_T(k)                                                                  \
@@ -499,17 +496,6 @@ __global__ void __launch_bounds__(256, LS_CTAS) local_solve_kernel(bddc_geom G, 
   const double Di = Dsub[i];
 #ifdef LS_TIMING
   long long t0_ = clock64();
-#endif
-#if LS_PREFETCH_KB > 0
-  {
-    // pull the head of this subdomain's packed Q towards L2 while the line phase runs
-    const int nt_ = mp / 32;
-    const char* Qb = (const char*)(Q + (size_t)i * (nt_ * (nt_ + 1) / 2) * 1024);
-    const size_t bytes = (size_t)(nt_ * (nt_ + 1) / 2) * 8192;
-    const size_t lim = bytes < (size_t)LS_PREFETCH_KB * 1024 ? bytes : (size_t)LS_PREFETCH_KB * 1024;
-    for (size_t o = (size_t)threadIdx.x * 128; o < lim; o += (size_t)blockDim.x * 128)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(Qb + o));
-  }
 #endif
   for (int q = threadIdx.x; q < mg; q += blockDim.x) {
     int gp = gpos[(size_t)i * mg + q];

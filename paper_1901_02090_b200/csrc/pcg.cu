@@ -1059,7 +1059,11 @@ __global__ void lanczos_kernel(int m, const double* __restrict__ al, const doubl
     }
   }
   __syncthreads();
-  if (threadIdx.x < 2) {
+  {
+    // warp 0: smallest eigenvalue (Sturm count >= 1), warp 1: largest (count >= m).
+    // Multisection: the 32 lanes count at 32 interior points of the bracket at once,
+    // so every pass shrinks it 33-fold (12 passes instead of ~60 dependent bisections).
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double lo = 1e308, hi = -1e308;
     for (int k = 0; k < m; ++k) {
       double r = 0.0;
@@ -1068,16 +1072,21 @@ __global__ void lanczos_kernel(int m, const double* __restrict__ al, const doubl
       lo = fmin(lo, d[k] - r);
       hi = fmax(hi, d[k] + r);
     }
-    // threadIdx 0: smallest (count >= 1), 1: largest (count >= m)
-    int target = threadIdx.x == 0 ? 1 : m;
+    const int target = warp == 0 ? 1 : m;
     double a = lo, b = hi;
-    for (int itb = 0; itb < 200; ++itb) {
-      double mid = 0.5 * (a + b);
-      if (mid == a || mid == b) break;
-      if (sturm_count(d, e2, m, mid) >= target) b = mid;
-      else a = mid;
+    for (int pass = 0; pass < 40; ++pass) {
+      const double h = (b - a) / 33.0;
+      if (!(h > 0.0) || a + h == a || b - h == b) break;
+      const double x = a + (lane + 1) * h;
+      const bool ge = sturm_count(d, e2, m, x) >= target;
+      const unsigned mask = __ballot_sync(0xffffffffu, ge);
+      const int first = mask ? __ffs(mask) - 1 : 32;   // counts are monotone in x
+      const double nb = first < 32 ? a + (first + 1) * h : b;
+      const double na = first > 0 ? a + first * h : a;
+      a = na;
+      b = nb;
     }
-    out[threadIdx.x] = 0.5 * (a + b);
+    if (lane == 0) out[warp] = 0.5 * (a + b);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1590,7 +1599,7 @@ extern "C" int bddc_tridiag_eigvals(int m, const double* d, const double* e, dou
 
 extern "C" int bddc_lanczos(int m, const double* al, const double* be, double* work, double* out, void* stream) {
   if (m <= 0) return 0;
-  lanczos_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(m, al, be, work, out);
+  lanczos_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(m, al, be, work, out);
   LAUNCH_OK();
   return 0;
 }

@@ -314,6 +314,10 @@ class BddcSetup:
                              _p(omega), _p(scratch), _p(qbasis), _p(err), _p(fl), len(fl), mm,
                              int(self.pair_spectra), st)
             del scratch
+            # the nested-dissection tree of the subdomain grid depends on the partition
+            # only: build it (once per Decomposition) while the device works through the
+            # local and pair phases, before the first host sync of the setup
+            _nd_prefetch(dec, self.has_p)
             e = int(err.item())
             if e & 1:
                 raise NumericalFailureError("pair eigensolver: M not positive definite")
@@ -1061,6 +1065,12 @@ def write_eigs_csv(path, reports):
             lines.append(f"{i},{j},{rank},{float(lam)!r}")
     with open(path, "w") as f:
         f.write("\n".join(lines) + "\n")
+
+
+def _nd_prefetch(dec, has_p):
+    from .coarse_nd import nd_geometry_flat
+    if dec.n_faces:
+        nd_geometry_flat(dec, has_p)
 
 
 def _suggest_scaling(setup):
