@@ -225,6 +225,10 @@ def load(path=None):
         fn.restype = _RESTYPES.get(name, C.c_int)
     if lib.bddc_geom_size() != C.sizeof(Geom):
         raise ImportError("bddc_geom layout mismatch between header and binding")
+    # tuning override (A/B measurements): BDDC_PDL_PCG=<mask> selects which small PCG
+    # kernels use programmatic dependent launch (0: none)
+    if os.environ.get("BDDC_PDL_PCG", "").isdigit():   # bit mask, see capi.cu
+        lib.bddc_set_pdl_pcg(int(os.environ["BDDC_PDL_PCG"]))
     if path is None:
         _lib = lib
     return lib

@@ -25,6 +25,9 @@ extern "C" void bddc_count_launch(void) { __atomic_add_fetch(&g_launches, 1ull, 
 static int g_pdl = 1;
 extern "C" int bddc_pdl_enabled(void) { return g_pdl; }
 extern "C" void bddc_set_pdl(int on) { g_pdl = on ? 1 : 0; }
+static int g_pdl_pcg = 31;   // bit mask: 1 phi, 2 gemv, 4 projection+dot, 8 CG update, 16 p update
+extern "C" int bddc_pdl_pcg_enabled(void) { return g_pdl_pcg; }
+extern "C" void bddc_set_pdl_pcg(int mask) { g_pdl_pcg = mask; }
 extern "C" unsigned long long bddc_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 // Page-lock / release a caller-owned host array (the per-solve source upload

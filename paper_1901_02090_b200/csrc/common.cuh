@@ -78,9 +78,11 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 
 extern "C" int bddc_pdl_enabled(void);
 
+extern "C" int bddc_pdl_pcg_enabled(void);
+
 template <typename... KArgs, typename... Args>
-static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t shm, cudaStream_t s,
-                                     Args... args) {
+static inline cudaError_t launch_pdl_if(int allowed, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t shm,
+                                        cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -88,7 +90,7 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = bddc_pdl_enabled() ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = allowed ? 1 : 0;
   // the stream's priority as an explicit launch attribute, so that a kernel node
   // captured into a graph (the PCG WHILE body) keeps it
   int prio = 0;
@@ -98,6 +100,12 @@ static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 b
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t shm, cudaStream_t s,
+                                     Args... args) {
+  return launch_pdl_if(bddc_pdl_enabled(), kernel, grid, block, shm, s, args...);
 }
 
 // Plain launch carrying the stream's priority as a launch attribute (see launch_pdl).
@@ -123,6 +131,16 @@ static inline cudaError_t launch_prio(void (*kernel)(KArgs...), dim3 grid, dim3 
   do {                                                                    \
     bddc_count_launch();                                                  \
     cudaError_t _e = launch_pdl(kernel, grid, block, shm, stream, __VA_ARGS__); \
+    if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
+  } while (0)
+
+// The small dependent kernels of the PCG iteration (projection, dots, updates): PDL
+// launches whose kernels trigger and wait at their top, so each becomes resident
+// during its predecessor instead of paying a launch latency after it.
+#define PCG_LAUNCH(bit, kernel, grid, block, shm, stream, ...)             \
+  do {                                                                    \
+    bddc_count_launch();                                                  \
+    cudaError_t _e = launch_pdl_if((bddc_pdl_pcg_enabled() >> (bit)) & 1, kernel, grid, block, shm, stream, __VA_ARGS__); \
     if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
   } while (0)
 

@@ -313,6 +313,7 @@ symv_bulk_kernel(int N, int maxG, const int* __restrict__ nG, const int* __restr
                  const double* __restrict__ packed, const double* __restrict__ x,
                  const double* __restrict__ win, double* __restrict__ yb, int* __restrict__ sched) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  pdl_trigger();   // the dependent small kernel waits resident instead of paying a launch
   const int nt = maxG / 32;
   const size_t ntiles = (size_t)nt * (nt + 1) / 2;
   double* ring = reinterpret_cast<double*>(smraw);    // SB_NST tiles
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(256) prolong_direct_kernel(int maxG, int maxC,
                                                              const double* __restrict__ wout,
                                                              double* __restrict__ outb) {
   extern __shared__ double cf[];
+  pdl_trigger();
   const int i = blockIdx.x;
   const int n = nG[i], nc = nC[i];
   for (int r = threadIdx.x; r < nc; r += blockDim.x) {
@@ -704,10 +706,14 @@ __global__ void scatter_kernel(int n_gamma, const int* __restrict__ gown, const 
 // phi_i = sum over the interface slots of i of sign * y; gown != NULL: y is not
 // assembled yet and is read from the per-slot values yb (y[g] = yb[own0] + yb[own1],
 // the scatter fused away).
+// (Vectors written by the stream predecessor carry no __restrict__ in the kernels that
+// wait on it inside their own lifetime: their loads must not take the non-coherent path.)
 __global__ void phi_kernel(int maxG, const int* __restrict__ nG, const int* __restrict__ gpos,
-                           const int* __restrict__ gcode, const double* __restrict__ y, double* __restrict__ phi,
-                           const int* __restrict__ gown, const double* __restrict__ yb) {
+                           const int* __restrict__ gcode, const double* y, double* __restrict__ phi,
+                           const int* __restrict__ gown, const double* yb) {
   __shared__ double red[32];
+  pdl_trigger();   // PCG chain: the next small kernel may become resident now
+  pdl_wait();      // predecessor complete, its writes visible
   const int i = blockIdx.x;
   double acc = 0.0;
   for (int q = threadIdx.x; q < nG[i]; q += blockDim.x) {
@@ -813,11 +819,13 @@ struct DotArgs {
 };
 
 template <int MODE>
-__global__ void dot_kernel(const double* __restrict__ x, double* __restrict__ y, long long n,
+__global__ void dot_kernel(const double* x, double* y, long long n,
                            double* __restrict__ partial, unsigned* __restrict__ counter,
                            double* __restrict__ scal, int op, double* __restrict__ hist, DotArgs A) {
   __shared__ double red[32];
   __shared__ bool last;
+  pdl_trigger();   // PCG chain: the next small kernel may become resident now
+  pdl_wait();      // predecessor complete, its writes visible
   const bool amax = MODE == 0 && op >= 300 && op < 400, asum = MODE == 0 && op >= 200 && op < 300;
   double acc = 0.0;
   const double alpha = MODE == 2 ? scal[2] : 0.0;
@@ -921,8 +929,9 @@ __global__ void cg_update_kernel(long long n, const double* __restrict__ scal, d
 }
 
 // p = z + beta p
-__global__ void p_update_kernel(long long n, const double* __restrict__ scal, const double* __restrict__ z,
-                                double* __restrict__ p) {
+__global__ void p_update_kernel(long long n, const double* scal, const double* z, double* p) {
+  pdl_trigger();   // PCG chain: the next small kernel may become resident now
+  pdl_wait();      // predecessor complete, its writes visible
   const double b = scal[7];
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     p[e] = z[e] + b * p[e];
@@ -930,8 +939,10 @@ __global__ void p_update_kernel(long long n, const double* __restrict__ scal, co
 
 // Dense (row-major, symmetric) GEMV y = M x over n rows, warp per row.
 // y = M x, warp per row, 8 loads per lane in flight (fixed order: deterministic).
-__global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ M, const double* __restrict__ x,
+__global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ M, const double* x,
                             double* __restrict__ y) {
+  pdl_trigger();   // PCG chain: the next small kernel may become resident now
+  pdl_wait();      // predecessor complete, its writes visible
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n) return;
@@ -945,14 +956,14 @@ __global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ 
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       m[u] = __ldg(mr + c + 32 * u);
-      v[u] = __ldg(x + c + 32 * u);
+      v[u] = x[c + 32 * u];
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
-    if (c + 32 * u < ncol) a[u] += __ldg(mr + c + 32 * u) * __ldg(x + c + 32 * u);
+    if (c + 32 * u < ncol) a[u] += __ldg(mr + c + 32 * u) * x[c + 32 * u];
   double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) y[row] = acc;
@@ -963,8 +974,10 @@ __global__ void gemv_kernel(int n, int ld, int ncol, const double* __restrict__ 
 // more loads in flight when there are few rows (N x N projection operator).
 template <int WPR>
 __global__ void __launch_bounds__(256) gemv_split_kernel(int n, int ld, int ncol, const double* __restrict__ M,
-                                                         const double* __restrict__ x, double* __restrict__ y) {
+                                                         const double* x, double* __restrict__ y) {
   __shared__ double part[8];
+  pdl_trigger();   // PCG chain: the next small kernel may become resident now
+  pdl_wait();      // predecessor complete, its writes visible
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int row = blockIdx.x * (8 / WPR) + w / WPR, pi = w % WPR;
   const int chunk = ((ncol + WPR * 32 - 1) / (WPR * 32)) * 32;
@@ -981,14 +994,14 @@ __global__ void __launch_bounds__(256) gemv_split_kernel(int n, int ld, int ncol
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         m[u] = __ldg(mr + c + 32 * u);
-        v[u] = __ldg(x + c + 32 * u);
+        v[u] = x[c + 32 * u];
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) a[u] += m[u] * v[u];
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (c + 32 * u < c1) a[u] += __ldg(mr + c + 32 * u) * __ldg(x + c + 32 * u);
+      if (c + 32 * u < c1) a[u] += __ldg(mr + c + 32 * u) * x[c + 32 * u];
     acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   }
@@ -1324,8 +1337,8 @@ extern "C" int bddc_phi(int N, int maxG, const int* nG, const int* gpos, const i
 
 extern "C" int bddc_phi_broken(int N, int maxG, const int* nG, const int* gpos, const int* gcode, const int* gown,
                                const double* yb, double* phi, void* stream) {
-  phi_kernel<<<N, 256, 0, (cudaStream_t)stream>>>(maxG, nG, gpos, gcode, nullptr, phi, gown, yb);
-  LAUNCH_OK();
+  PCG_LAUNCH(0, phi_kernel, dim3(N), dim3(256), 0, (cudaStream_t)stream, maxG, nG, gpos, gcode, (const double*)nullptr,
+             phi, gown, yb);
   return 0;
 }
 
@@ -1492,9 +1505,8 @@ extern "C" int bddc_proj_dot_broken(int n_gamma, int maxG, const int* gown, cons
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
   DotArgs A{gown, maxG, z, nullptr, nullptr, nullptr, yb, 0ull, 0.0, 0};
-  dot_kernel<3><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(x, y, n_gamma, partial, counter, scal, op,
-                                                                     hist, A);
-  LAUNCH_OK();
+  PCG_LAUNCH(2, dot_kernel<3>, dim3(DOT_BLOCKS), dim3(DOT_THREADS), 0, (cudaStream_t)stream, x, y, (long long)n_gamma,
+             partial, counter, scal, op, hist, A);
   return 0;
 }
 
@@ -1517,8 +1529,8 @@ extern "C" int bddc_cg_update_dot_cond(long long n, double* xv, const double* p,
   double* partial = (double*)ws;
   unsigned* counter = (unsigned*)(partial + DOT_BLOCKS);
   DotArgs A{nullptr, 1, nullptr, xv, p, Ap, nullptr, cond, tol, maxit};
-  dot_kernel<2><<<DOT_BLOCKS, DOT_THREADS, 0, (cudaStream_t)stream>>>(r, r, n, partial, counter, scal, op, hist, A);
-  LAUNCH_OK();
+  PCG_LAUNCH(3, dot_kernel<2>, dim3(DOT_BLOCKS), dim3(DOT_THREADS), 0, (cudaStream_t)stream, (const double*)r, r, n,
+             partial, counter, scal, op, hist, A);
   return 0;
 }
 
@@ -1530,8 +1542,7 @@ extern "C" int bddc_cg_update(long long n, const double* scal, double* x, const 
 }
 
 extern "C" int bddc_p_update(long long n, const double* scal, const double* z, double* p, void* stream) {
-  p_update_kernel<<<DOT_BLOCKS, 256, 0, (cudaStream_t)stream>>>(n, scal, z, p);
-  LAUNCH_OK();
+  PCG_LAUNCH(4, p_update_kernel, dim3(DOT_BLOCKS), dim3(256), 0, (cudaStream_t)stream, n, scal, z, p);
   return 0;
 }
 
@@ -1568,12 +1579,11 @@ extern "C" int bddc_gemv(int n, int ld, int ncol, const double* M, const double*
   int wpr = g_gemv_wpr;
   if (wpr <= 0) wpr = (n >= 8192 || ncol < 1024) ? 1 : (n >= 4096 ? 2 : 4);
   switch (wpr) {
-    case 1: gemv_kernel<<<(n + 7) / 8, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
-    case 2: gemv_split_kernel<2><<<(n + 3) / 4, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
-    case 4: gemv_split_kernel<4><<<(n + 1) / 2, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
-    default: gemv_split_kernel<8><<<n, 256, 0, s>>>(n, ld, ncol, M, x, y); break;
+    case 1: PCG_LAUNCH(1, gemv_kernel, dim3((n + 7) / 8), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    case 2: PCG_LAUNCH(1, gemv_split_kernel<2>, dim3((n + 3) / 4), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    case 4: PCG_LAUNCH(1, gemv_split_kernel<4>, dim3((n + 1) / 2), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    default: PCG_LAUNCH(1, gemv_split_kernel<8>, dim3(n), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
   }
-  LAUNCH_OK();
   return 0;
 }
 
