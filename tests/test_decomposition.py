@@ -71,3 +71,38 @@ def test_box_partition_uneven_strips_and_part_roundtrip(tmp_path):
     np.testing.assert_array_equal(d1.gcode, d3.gcode)
     with pytest.raises(ConfigurationError):
         B.Decomposition(g, np.random.default_rng(0).integers(0, 4, g.n_cells))
+
+
+@pytest.mark.parametrize("dim,counts,splits", [
+    (2, (12, 12), (3, 3)), (2, (10, 7), (1, 3)), (2, (5, 5), (1, 1)),
+    (3, (12, 10, 8), (3, 2, 2)), (3, (12, 10, 8), (1, 1, 4)),
+    (3, (12, 12, 9), ([3, 5, 4], [2, 4, 6], [5, 4]))])
+def test_closed_form_tables_and_lazy_host_copies(dim, counts, splits):
+    """Constructing a Decomposition does O(N) host work only (sizes, nG, face table,
+    face prefix counts in closed form); the per-slot / per-dof tables appear on first
+    access and agree with the closed forms (asserted inside the lazy build) and with
+    the reference's definitions (decomposition.py:60-125)."""
+    import paper_1901_02090_b200 as B
+    g = B.build_grid(dim, counts, (1.0,) * dim)
+    d = B.Decomposition(g, splits)
+    lazy = set(B.Decomposition._LAZY) | {"part"}
+    assert not (lazy & set(d.__dict__))
+    N = d.n_subdomains
+    # face prefix counts: faces are sorted by (i, j)
+    assert np.array_equal(d.face_base, np.searchsorted(d.face_table[:, 0], np.arange(N)))
+    gam = d.gamma                      # triggers the lazy build (with its own asserts)
+    assert len(gam) == d.n_gamma == len(np.unique(gam))
+    part = d.part
+    # Gamma = interior faces whose two cells lie in different subdomains
+    expect = []
+    for a in range(dim):
+        lo, hi = g.cell_faces(a)
+        m = hi >= 0
+        cells = np.nonzero(m)[0]
+        stride = int(np.prod(g.counts[:a]))
+        cut = part[cells] != part[cells + stride]
+        expect.append(hi[m][cut])
+    assert np.array_equal(np.sort(np.concatenate(expect)), gam)
+    assert np.array_equal(d.nG, [len(x) for x in d.gamma_dofs])
+    for f, (i, j, a, m) in enumerate(d.face_table):
+        assert int((d.gface == f).sum()) == m
