@@ -60,10 +60,13 @@ __global__ void nd_assemble_kernel(int m, int S, int Sf, int B, int nf, int slot
 // whole boundary (flux dofs and pressures, indices into the combined vector),
 // then X^T (s x b).
 
+// (Vectors written by the PDL predecessor -- r, v, rs, cbuf, ybuf -- carry no __restrict__:
+// their loads follow pdl_wait() inside the kernel's own lifetime and must be ordinary
+// global loads, never the non-coherent path.)
 // Coarse right-hand side entry g: r[g], or (cown != NULL, the preconditioner's
 // restriction) v[own+] - v[own-] for flux dofs and 0 for pressures (coarse.py:225-235
 // with a zero pressure load), so no assembled rhs vector is written.
-__device__ __forceinline__ double nd_rhs(const double* __restrict__ r, const double* __restrict__ v,
+__device__ __forceinline__ double nd_rhs(const double* r, const double* v,
                                          const int* __restrict__ cown, int nfc, int g) {
   if (!cown) return r[g];
   return g < nfc ? v[cown[2 * g]] - v[cown[2 * g + 1]] : 0.0;
@@ -73,8 +76,7 @@ __device__ __forceinline__ double nd_rhs(const double* __restrict__ r, const dou
 // rs[t] = r[g_t] - sum of the descendants' update entries (lane-strided over the
 // list, fixed shuffle tree: deterministic).
 __global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const int* __restrict__ lptr,
-                                 const int* __restrict__ lsrc, const double* __restrict__ cbuf,
-                                 const double* __restrict__ r, const double* __restrict__ v,
+                                 const int* __restrict__ lsrc, const double* cbuf, const double* r, const double* v,
                                  const int* __restrict__ cown, int nfc, double* __restrict__ rs) {
   pdl_trigger();
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
@@ -101,9 +103,9 @@ __global__ void nd_gather_kernel(int n, const int* __restrict__ sep_flat, const 
 __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
                               const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
                               const int* __restrict__ lptr, const int* __restrict__ lsrc,
-                              const double* __restrict__ Fc, const double* __restrict__ r,
-                              const double* __restrict__ v, const int* __restrict__ cown, int nfc,
-                              const double* __restrict__ rs, double* __restrict__ ybuf, double* __restrict__ cbuf,
+                              const double* __restrict__ Fc, const double* r,
+                              const double* v, const int* __restrict__ cown, int nfc,
+                              const double* rs, double* __restrict__ ybuf, double* __restrict__ cbuf,
                               int lpe, double* __restrict__ xdirect) {
   extern __shared__ double rsm[];
   pdl_trigger();
@@ -188,7 +190,7 @@ __global__ void nd_fwd_kernel(const int* __restrict__ tasks, const int* __restri
 __global__ void nd_bwd_kernel(const int* __restrict__ tasks, const int* __restrict__ info,
                               const long long* __restrict__ data_off, const int* __restrict__ sep_flat,
                               const int* __restrict__ bnd_flat, const double* __restrict__ Fc,
-                              const double* __restrict__ ybuf, double* __restrict__ x, int wpr) {
+                              const double* ybuf, double* __restrict__ x, int wpr) {
   extern __shared__ double xb[];  // bmax
   __shared__ double part[8];
   pdl_trigger();

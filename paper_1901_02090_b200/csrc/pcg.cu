@@ -1347,7 +1347,7 @@ extern "C" int bddc_phi_broken(int N, int maxG, const int* nG, const int* gpos, 
 // uses Q_a^T (Q[k][c]), backward Q_a (Q[c][k]).
 __global__ void lap_mode_kernel(int S0, int S1, int S2, int a, int backward, const double* __restrict__ eig,
                                 const double* __restrict__ dmi, const double* __restrict__ dmo, int lamdiv,
-                                const double* __restrict__ in, double* __restrict__ out) {
+                                const double* in, double* __restrict__ out) {   // in: predecessor-written
   pdl_trigger();
   const int N = S0 * S1 * S2;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
