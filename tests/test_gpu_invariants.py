@@ -111,6 +111,34 @@ def test_bitwise_determinism():
     np.testing.assert_array_equal(r1.u, r3.u)
 
 
+@pytest.mark.parametrize("counts,splits,seed", [((16, 16), (4, 4), 10), ((12, 12, 8), (3, 3, 2), 4)])
+def test_pdl_launches_do_not_change_results(counts, splits, seed):
+    """The small PCG kernels as programmatic dependent launches (they become resident
+    while their predecessor runs and wait at their top) against plain stream-ordered
+    launches of the same kernels: bitwise the same solve.  A load that took the
+    non-coherent path, or work placed ahead of the dependency wait, would show here."""
+    from paper_1901_02090_b200 import _native as nat
+    B, g, k, system, dec, cfg = _problem(counts, splits, seed, tau=5.0, tol=1e-9)
+    lib = nat.load()
+    out = {}
+    try:
+        for mask in (31, 0):
+            lib.bddc_set_pdl_pcg(mask)
+            lib.bddc_set_pdl(1 if mask else 0)
+            st = B.BddcSetup(system, dec, cfg)      # fresh setup: fresh captured graphs
+            reps = [B.solve(system, dec, cfg, setup=st) for _ in range(3)]
+            for r in reps[1:]:
+                np.testing.assert_array_equal(reps[0].u, r.u)
+            out[mask] = reps[0]
+    finally:
+        lib.bddc_set_pdl_pcg(31)
+        lib.bddc_set_pdl(1)
+    assert out[31].it == out[0].it
+    np.testing.assert_array_equal(out[31].u, out[0].u)
+    np.testing.assert_array_equal(out[31].p, out[0].p)
+    np.testing.assert_array_equal(out[31].residuals, out[0].residuals)
+
+
 def test_nonconvergence_partial_report():
     """test_solver.py:139-144."""
     B, g, k, system, dec, cfg = _problem((8, 8), (2, 2), 8, tol=1e-12)
