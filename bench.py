@@ -453,6 +453,46 @@ def _factorisation_roofline(setup, dec, lib, nat, dev, rebuild=None):
             "in_situ": _spd_in_situ(rebuild, lib, peak) if rebuild is not None else None}
 
 
+def _local_solve_roofline(setup, nat, peak, reps=20):
+    """Interior (harmonic-extension) solves of all subdomains, substructure.py:72-116:
+    one CTA per subdomain streams its tile-packed symmetric Q = P^+ once (algorithmic
+    bytes: 8 * maxP(maxP+32)/2 per subdomain, the 32x32-tile packed upper triangle)
+    between two line phases; 4 launches per solve.  CUDA events around `reps`
+    back-to-back launches (2.5 GB of Q at C3: every launch streams from HBM)."""
+    import ctypes as C
+    import torch
+    if not setup.n_gamma:
+        return None
+    W = setup.work()
+    gp = C.byref(setup.geom)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    p = nat.ptr
+    x = torch.ones(setup.n_gamma, dtype=torch.float64, device=setup.dev)
+    a = nat.LocalSolveArgs()
+    a.x_gamma, a.x_scale = p(x).value, 1.0
+    a.u_out, a.u_mode = p(W.u0).value, 0
+
+    def run():
+        nat.call("bddc_local_solve", gp, p(setup.d_coef), p(setup.d_gcode), p(setup.d_gpos),
+                 p(setup.d_fslot), p(setup.d_Qp), p(setup.d_Dsub), C.byref(a), st)
+    for _ in range(3):
+        run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    e1.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / reps
+    nt = setup.maxP // 32
+    alg = float(setup.N) * (nt * (nt + 1) // 2) * 8192
+    ach = alg / sec / 1e9
+    return {"bound": "hbm", "kernel": "local_solve_kernel (packed Q symv between two line phases)",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "alg_bytes_per_launch": alg, "mean_launch_s": sec, "launches_per_solve": 4,
+            "timing": f"CUDA events around {reps} back-to-back launches"}
+
+
 def _stencil_roofline(setup, g, nat, peak, dev, reps=24, nsets=4):
     """Matrix-free RT0 operators (stencil row): A u, B u, B^T p on the
     whole grid, `reps` launches back to back cycling over `nsets` independent operand
@@ -711,6 +751,7 @@ def main():
     line["factorisation_roofline"] = _factorisation_roofline(setup, dec, lib, nat, dev,
                                                              rebuild=lambda: B.BddcSetup(system, dec, cfg))
     line["stencil_roofline"] = _stencil_roofline(setup, g, nat, peak, dev)
+    line["local_solve_roofline"] = _local_solve_roofline(setup, nat, peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and c["dim"] == 2:
         vals, walls, detail, sample = reference_measured(c, k, 1, 0)
         line["cpu_baseline"] = {"value": vals[0], "unit": "it/s", "cores": os.cpu_count(),
