@@ -144,6 +144,17 @@ static inline cudaError_t launch_prio(void (*kernel)(KArgs...), dim3 grid, dim3 
     if (_e != cudaSuccess) return bddc_set_error(BDDC_ERR_CUDA, cudaGetErrorString(_e)); \
   } while (0)
 
+// Streaming read that bypasses L1 allocation.  Every once-read matrix stream of the solve
+// (packed Q, S_i / T_i tiles of the LDG kernels, Psi, the ND factors) uses it: the stream
+// would otherwise evict what the SM does re-read from L1 -- per-thread local-memory
+// arrays, gathered vectors, index tables (local solves 627 -> 550 us, ND solve 103 -> 93 us,
+// C4 S_i GEMV 165 -> 151 us).
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // Warp GEMV helpers over row-major rows (read-only matrix via the non-coherent
 // path, vector in shared memory).  Fixed summation order: deterministic.
 
@@ -156,13 +167,13 @@ __device__ __forceinline__ double warp_row_dot(const double* __restrict__ row, c
   for (; c + 224 < len; c += 256) {
     double x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = __ldg(row + c + 32 * u);
+    for (int u = 0; u < 8; ++u) x[u] = ldg_stream(row + c + 32 * u);
 #pragma unroll
     for (int u = 0; u < 8; ++u) a[u] += x[u] * v[c + 32 * u];
   }
 #pragma unroll
   for (int u = 0; u < 8; ++u)
-    if (c + 32 * u < len) a[u] += __ldg(row + c + 32 * u) * v[c + 32 * u];
+    if (c + 32 * u < len) a[u] += ldg_stream(row + c + 32 * u) * v[c + 32 * u];
   double acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -181,7 +192,7 @@ __device__ __forceinline__ void warp_rows4_dot(const double* __restrict__ base, 
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int c = c0 + lane + 32 * u;
-        x[k][u] = (k < nr && c < len) ? __ldg(base + (size_t)k * ld + c) : 0.0;
+        x[k][u] = (k < nr && c < len) ? ldg_stream(base + (size_t)k * ld + c) : 0.0;
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -263,14 +274,6 @@ __device__ __forceinline__ void cta_symv_packed2(const double* __restrict__ Pk, 
     (s ? y2 : y)[ee] = acc;
   }
   __syncthreads();
-}
-
-// Streaming read that bypasses L1 allocation: a once-read matrix stream must not evict
-// the CTA's (and its co-resident CTA's) L1-cached local-memory lines.
-__device__ __forceinline__ double ldg_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
 }
 
 __device__ __forceinline__ void cta_symv_packed(const double* __restrict__ Pk, int nt, int ntl, const double* x,

@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(MAXT) gather_symv_kernel(int N, int maxG, cons
       double col = 0.0;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        double a = T[r * 32 + lane];
+        const double a = ldg_stream(T + r * 32 + lane);   // once-read stream: no L1 allocation
         v[r] = a * xl;
         col += a * xs[bi * 32 + r];
       }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(MAXT) gather_symv16_kernel(int N, int maxG, co
       double col = 0.0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
-        const double a = act ? __ldg(T + r * 16 + l) : 0.0;
+        const double a = act ? ldg_stream(T + r * 16 + l) : 0.0;
         v[r] = a * xl;
         col += a * xs[bi * 16 + r];
       }
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(256) prolong_direct_kernel(int maxG, int maxC,
 #pragma unroll
       for (int k = 0; k < QPT; ++k) {
         const int q = threadIdx.x + k * 256;
-        m[u][k] = (q < n) ? __ldg(Pi + (size_t)(r + u) * maxG + q) : 0.0;
+        m[u][k] = (q < n) ? ldg_stream(Pi + (size_t)(r + u) * maxG + q) : 0.0;
       }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(256) prolong_direct_kernel(int maxG, int maxC,
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
       const int q = threadIdx.x + k * 256;
-      if (q < n) acc[k] += __ldg(Pi + (size_t)r * maxG + q) * w;
+      if (q < n) acc[k] += ldg_stream(Pi + (size_t)r * maxG + q) * w;
     }
   }
 #pragma unroll
