@@ -293,6 +293,10 @@ int bddc_p_update(long long n, const double* scal, const double* z, double* p, v
 int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const double* dm, double* ws, double* Lp,
                    void* stream);
 int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream);
+/* The same product for a static M (written by no kernel queued before the call, e.g. the
+ * balance operator of solver.py:166-179 built at setup), launched as a programmatic
+ * dependent launch inside the PCG chain. */
+int bddc_gemv_static(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream);
 /* Tuning knob for bddc_gemv: warps per row (1, 2, 4, 8; 0 = automatic by shape). */
 void bddc_set_gemv_wpr(int wpr);
 /* Tuning knob: threads per CTA (256 or 512) of grid-stride bddc_gather_symv launches. */

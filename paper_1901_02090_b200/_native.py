@@ -150,6 +150,7 @@ _SIGS = {
     "bddc_phi_broken": [_I, _I, _P, _P, _P, _P, _P, _P, _P],
     "bddc_p_update": [_L, _P, _P, _P, _P],
     "bddc_gemv": [_I, _I, _I, _P, _P, _P, _P],
+    "bddc_gemv_static": [_I, _I, _I, _P, _P, _P, _P],
     "bddc_set_gemv_wpr": [_I],
     "bddc_set_leaf_regs": [_I],
     "bddc_set_symv_threads": [_I],

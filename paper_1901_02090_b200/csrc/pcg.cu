@@ -1572,19 +1572,31 @@ extern "C" int bddc_lap_dense(int S0, int S1, int S2, const double* eig, const d
 static int g_gemv_wpr = 0;   // 0: automatic
 extern "C" void bddc_set_gemv_wpr(int wpr) { g_gemv_wpr = wpr; }
 
-extern "C" int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream) {
+// `pdl`: launch as a programmatic dependent launch (PCG mask bit 1).  Only for a matrix no
+// kernel queued before the call writes: the rows go through the non-coherent path, which
+// requires them read-only for the kernel's whole (early-started) lifetime.
+static int gemv_launch(int n, int ld, int ncol, const double* M, const double* x, double* y, int pdl, void* stream) {
   if (n <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   // enough warps for ~60 per SM on the row count (few long rows: split them)
   int wpr = g_gemv_wpr;
   if (wpr <= 0) wpr = (n >= 8192 || ncol < 1024) ? 1 : (n >= 4096 ? 2 : 4);
+  const int bit = pdl ? 1 : 31;   // bit 31 of the mask is never set: plain launch
   switch (wpr) {
-    case 1: PCG_LAUNCH(1, gemv_kernel, dim3((n + 7) / 8), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
-    case 2: PCG_LAUNCH(1, gemv_split_kernel<2>, dim3((n + 3) / 4), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
-    case 4: PCG_LAUNCH(1, gemv_split_kernel<4>, dim3((n + 1) / 2), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
-    default: PCG_LAUNCH(1, gemv_split_kernel<8>, dim3(n), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    case 1: PCG_LAUNCH(bit, gemv_kernel, dim3((n + 7) / 8), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    case 2: PCG_LAUNCH(bit, gemv_split_kernel<2>, dim3((n + 3) / 4), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    case 4: PCG_LAUNCH(bit, gemv_split_kernel<4>, dim3((n + 1) / 2), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
+    default: PCG_LAUNCH(bit, gemv_split_kernel<8>, dim3(n), dim3(256), 0, s, n, ld, ncol, M, x, y); break;
   }
   return 0;
+}
+
+extern "C" int bddc_gemv(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream) {
+  return gemv_launch(n, ld, ncol, M, x, y, 0, stream);
+}
+
+extern "C" int bddc_gemv_static(int n, int ld, int ncol, const double* M, const double* x, double* y, void* stream) {
+  return gemv_launch(n, ld, ncol, M, x, y, 1, stream);
 }
 
 // w -= Q^T c for Q with k rows of length n (row-major), c of length k.

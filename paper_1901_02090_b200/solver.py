@@ -690,8 +690,8 @@ class BddcSetup:
                      _p(self.d_gcode), _p(y), _p(self.w_phi), st)
         z = self.w_z
         if self.d_Lp is not None:
-            nat.call("bddc_gemv", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi), _p(self.w_z),
-                     st)
+            nat.call("bddc_gemv_static", self.N, self.N, self.N, _p(self.d_Lp), _p(self.w_phi),
+                     _p(self.w_z), st)
         elif self.mode_b:
             if self.NF:
                 S3 = self.S3F
