@@ -48,8 +48,10 @@ def timeit(fn):
 
 
 grids = [0, 444, 296, 148, 120, 100, 84]
+if os.environ.get("T_GRIDS"):   # e.g. T_GRIDS=88,92,96,100,104,108 for a fine scan
+    grids = [int(v) for v in os.environ["T_GRIDS"].split(",")]
 print(f"config {cid}: symv_bulk {st.symv_bulk}", flush=True)
-for rf in (False, True):
+for rf in ((False,) if os.environ.get("T_GRIDS") else (False, True)):
     st.restrict_first = rf
     for tg in grids:
         st.t_grid_bulk = tg
